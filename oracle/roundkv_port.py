@@ -1,0 +1,447 @@
+"""CPU oracle for the TokenDance collector + diff-codec hot path.
+
+TEST INFRASTRUCTURE ONLY.  This module is a plain-numpy restatement of the
+reference package ``roundkv`` 0.1.0 (``/root/reference/pkg/src/roundkv``) for
+the functions on the hot path.  Only ``tests/``, ``__graft_entry__.smoke()``
+and ``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import it,
+and only as the checker or the timed CPU baseline -- never as the product.
+The product path (``paper_2604_03143_b200``) never imports this module.
+
+Parity pinning: every function here is checked bit-for-bit against golden
+vectors produced by the reference itself (``tests/golden/make_golden.py``
+imports ``roundkv`` from ``/root/reference`` in the build container and
+records its outputs under ``tests/golden/*.npz``); see
+``tests/test_oracle_golden.py``.
+
+Arithmetic conventions restated from the reference:
+  * rotary pairs are interleaved ``(2j, 2j+1)``; ``inv_freq = base^(-2j/D)``
+    in float64; angle ``= delta * inv_freq`` in float64; the rotation is
+    evaluated in float64 and rounded once to float32
+    (``toymodel.py:60-83``);
+  * a span whose deltas are all zero is an exact copy (``toymodel.py:86-96``,
+    ``pic.py:228``);
+  * diff block equality is float ``==`` (``np.array_equal``), so ``+0 == -0``
+    and ``NaN != NaN`` (``diffstore.py:151-153``).
+"""
+from __future__ import annotations
+
+import math
+import struct
+from dataclasses import dataclass
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+__all__ = [
+    "inv_freq", "rope_apply", "rope_recover", "block_count", "block_range",
+    "valid_len", "allocate_slots", "CollectJob", "collect_into_contexts",
+    "collect_into_pool", "DiffLayer", "HintViolation", "encode_diff",
+    "decode_dense", "wire_size", "serialize", "deserialize", "WireError",
+    "fused_restore", "dense_restore", "mirror_hints", "select_master",
+]
+
+
+# ---------------------------------------------------------------------------
+# rotary arithmetic -- toymodel.py:60-96
+
+
+def inv_freq(head_dim: int, base: float = 10000.0) -> np.ndarray:
+    """``base ** (-(0,2,4,..)/D)`` in float64 (toymodel.py:74)."""
+    exps = -np.arange(0, head_dim, 2, dtype=np.float64) / head_dim
+    return float(base) ** exps
+
+
+def rope_apply(k: np.ndarray, positions: np.ndarray, base: float = 10000.0) -> np.ndarray:
+    """Rotate interleaved pairs of ``k`` (T, H, D) by ``positions`` (T,).
+
+    Restates toymodel.py:60-83: float64 angles, float64 rotation, one final
+    round-to-nearest cast to float32.
+    """
+    if k.ndim != 3:
+        raise ValueError("expected (tokens, heads, head_dim)")
+    t, _, d = k.shape
+    if d % 2:
+        raise ValueError("head_dim must be even")
+    pos = np.asarray(positions, dtype=np.float64)
+    if pos.shape != (t,):
+        raise ValueError("one position per token required")
+    theta = pos.reshape(t, 1) * inv_freq(d, base).reshape(1, d // 2)
+    c = np.cos(theta).reshape(t, 1, d // 2)
+    s = np.sin(theta).reshape(t, 1, d // 2)
+    pairs = k.astype(np.float64).reshape(k.shape[0], k.shape[1], d // 2, 2)
+    even, odd = pairs[..., 0], pairs[..., 1]
+    out = np.stack((even * c - odd * s, even * s + odd * c), axis=-1)
+    return out.reshape(k.shape).astype(np.float32)
+
+
+def rope_recover(old_positions: np.ndarray, new_positions: np.ndarray,
+                 k: np.ndarray, base: float = 10000.0) -> np.ndarray:
+    """Re-encode K rows from old to new positions (toymodel.py:86-96)."""
+    old = np.asarray(old_positions, dtype=np.int64)
+    new = np.asarray(new_positions, dtype=np.int64)
+    if k.shape[0] != old.size:
+        raise ValueError("span length must match token count")
+    delta = new - old
+    if not delta.any():
+        return k.copy()
+    return rope_apply(k, delta, base)
+
+
+# ---------------------------------------------------------------------------
+# block geometry -- core.py:240-263
+
+
+def block_count(num_tokens: int, block_size: int) -> int:
+    return (num_tokens + block_size - 1) // block_size
+
+
+def block_range(b: int, num_tokens: int, block_size: int) -> Tuple[int, int]:
+    lo = b * block_size
+    if lo >= num_tokens:
+        raise ValueError("block index out of range")
+    return lo, min(lo + block_size, num_tokens)
+
+
+def valid_len(num_tokens: int, block_size: int) -> int:
+    rem = num_tokens % block_size
+    return rem if rem else min(block_size, num_tokens)
+
+
+# ---------------------------------------------------------------------------
+# slot allocation policy -- paged_pool.py:106-135
+
+
+def allocate_slots(free: np.ndarray, num_tokens: int, block_size: int) -> np.ndarray:
+    """Pick ``num_tokens`` slots from the boolean ``free`` mask (mutated).
+
+    Policy restated from paged_pool.py:117-133: scan blocks in ascending
+    order and take each block whose every slot is free (a prefix of it when
+    less is needed); then top up with the lowest remaining free slots.
+    """
+    cap = free.size
+    if num_tokens > int(free.sum()):
+        raise RuntimeError(f"requested {num_tokens} slots, {int(free.sum())} free")
+    picked: List[int] = []
+    need = num_tokens
+    for b in range(block_count(cap, block_size)):
+        if need <= 0:
+            break
+        lo, hi = b * block_size, min(b * block_size + block_size, cap)
+        if free[lo:hi].all():
+            n = min(need, hi - lo)
+            picked.extend(range(lo, lo + n))
+            need -= n
+    if need > 0:
+        taken = np.zeros(cap, dtype=bool)
+        taken[picked] = True
+        rest = np.flatnonzero(free & ~taken)[:need]
+        picked.extend(rest.tolist())
+    out = np.asarray(picked, dtype=np.int64)
+    free[out] = False
+    return out
+
+
+# ---------------------------------------------------------------------------
+# the KV Collector -- pic.py:192-235 (+ paged_pool.py:150-156 for the pool)
+
+
+@dataclass
+class CollectJob:
+    """One (agent, shared segment) hit.
+
+    ``master_k``/``master_v``: (L, n, H, D) float32 cached rows at their
+    source positions; ``target_idx``: (n,) prompt rows; ``delta``: (n,) int64
+    ``target_idx - source_positions`` (pic.py:60-61).
+    """
+
+    agent: int
+    master_k: np.ndarray
+    master_v: np.ndarray
+    target_idx: np.ndarray
+    delta: np.ndarray
+
+
+def _rotate_jobs_layer(jobs: Sequence[CollectJob], layer: int, base: float,
+                       any_delta: bool) -> np.ndarray:
+    stacked = np.concatenate([j.master_k[layer] for j in jobs])
+    if not any_delta:
+        return stacked
+    deltas = np.concatenate([j.delta for j in jobs])
+    return rope_apply(stacked, deltas, base)
+
+
+def collect_into_contexts(jobs: Sequence[CollectJob],
+                          contexts: Sequence[Tuple[np.ndarray, np.ndarray]],
+                          base: float) -> int:
+    """Batched align (pic.py:208-235) plus the skeleton V copy
+    (pic.py:203-204): writes rotated K and copied V rows into each agent's
+    dense (L, T, H, D) context.  Returns the number of rotation calls (one
+    per layer, the ledger law of pic.py:229-230)."""
+    if not jobs:
+        return 0
+    any_delta = any(bool(np.any(j.delta)) for j in jobs)
+    layers = jobs[0].master_k.shape[0]
+    for j in jobs:
+        contexts[j.agent][1][:, j.target_idx] = j.master_v
+    for layer in range(layers):
+        rotated = _rotate_jobs_layer(jobs, layer, base, any_delta)
+        row = 0
+        for j in jobs:
+            n = j.target_idx.size
+            contexts[j.agent][0][layer][j.target_idx] = rotated[row:row + n]
+            row += n
+    return layers
+
+
+def collect_into_pool(jobs: Sequence[CollectJob], slot_maps: Sequence[np.ndarray],
+                      pool_k: np.ndarray, pool_v: np.ndarray, base: float) -> int:
+    """The collector with the pool as its destination: the rows the
+    reference first rotates into a dense context (pic.py:234) and later
+    copies with PagedPool.write_rows (trace.py:148-152, paged_pool.py:150-156)
+    land at ``pool[l, slot_map[agent][target_idx]]``."""
+    if not jobs:
+        return 0
+    any_delta = any(bool(np.any(j.delta)) for j in jobs)
+    layers = jobs[0].master_k.shape[0]
+    for layer in range(layers):
+        rotated = _rotate_jobs_layer(jobs, layer, base, any_delta)
+        row = 0
+        for j in jobs:
+            n = j.target_idx.size
+            slots = slot_maps[j.agent][j.target_idx]
+            pool_k[layer, slots] = rotated[row:row + n]
+            pool_v[layer, slots] = j.master_v[layer]
+            row += n
+    return layers
+
+
+# ---------------------------------------------------------------------------
+# block-sparse diff codec -- diffstore.py:110-306
+
+
+class HintViolation(RuntimeError):
+    """Mirror differs from master outside the hinted blocks (diffstore.py:156-164)."""
+
+
+@dataclass
+class DiffLayer:
+    indices: np.ndarray          # int64, strictly ascending
+    k_blocks: np.ndarray         # (count, bs, H, D) float32, zero padded
+    v_blocks: np.ndarray
+    v_indices: Optional[np.ndarray] = None   # escape form (separate V list)
+
+
+def _padded(rows: np.ndarray, bs: int) -> np.ndarray:
+    out = np.zeros((bs,) + rows.shape[1:], dtype=np.float32)
+    out[: rows.shape[0]] = rows
+    return out
+
+
+def encode_diff(master_k: np.ndarray, master_v: np.ndarray,
+                mirror_k: np.ndarray, mirror_v: np.ndarray,
+                hints: np.ndarray, block_size: int) -> List[DiffLayer]:
+    """Restates encode_diff (diffstore.py:119-182): every (layer, block) is
+    compared with float equality; changed blocks must be hinted (the first
+    violation in layer-major, block-ascending order raises with the block's
+    max-abs difference); changed blocks are stored whole, zero-padded."""
+    if master_k.shape != mirror_k.shape:
+        raise ValueError("master and mirror must have identical plane shapes")
+    layers, total, heads, dim = master_k.shape
+    nb = block_count(total, block_size)
+    hints = np.asarray(hints, dtype=np.int64)
+    if hints.size and (hints.min() < 0 or hints.max() >= total):
+        raise ValueError("hint positions out of range")
+    hinted = np.zeros(nb, dtype=bool)
+    hinted[hints // block_size] = True
+    out: List[DiffLayer] = []
+    for layer in range(layers):
+        changed: List[int] = []
+        for b in range(nb):
+            lo, hi = block_range(b, total, block_size)
+            a_k, b_k = mirror_k[layer, lo:hi], master_k[layer, lo:hi]
+            a_v, b_v = mirror_v[layer, lo:hi], master_v[layer, lo:hi]
+            if np.array_equal(a_k, b_k) and np.array_equal(a_v, b_v):
+                continue
+            if not hinted[b]:
+                worst = max(float(np.abs(a_k - b_k).max()), float(np.abs(a_v - b_v).max()))
+                raise HintViolation(
+                    f"layer {layer} block {b} differs outside the hinted"
+                    f" positions (max abs {worst:.3e})")
+            changed.append(b)
+        if changed:
+            kb = np.stack([_padded(mirror_k[layer, lo:hi], block_size)
+                           for lo, hi in (block_range(b, total, block_size) for b in changed)])
+            vb = np.stack([_padded(mirror_v[layer, lo:hi], block_size)
+                           for lo, hi in (block_range(b, total, block_size) for b in changed)])
+        else:
+            kb = np.zeros((0, block_size, heads, dim), np.float32)
+            vb = np.zeros((0, block_size, heads, dim), np.float32)
+        out.append(DiffLayer(np.asarray(changed, dtype=np.int64), kb, vb))
+    return out
+
+
+def _overlay(plane: np.ndarray, idx: np.ndarray, blocks: np.ndarray, bs: int) -> None:
+    total = plane.shape[0]
+    for j, b in enumerate(idx.tolist()):
+        lo, hi = block_range(int(b), total, bs)
+        plane[lo:hi] = blocks[j, : hi - lo]
+
+
+def decode_dense(master_k: np.ndarray, master_v: np.ndarray,
+                 layers: Sequence[DiffLayer], block_size: int) -> Tuple[np.ndarray, np.ndarray]:
+    """Master copy with the changed blocks overlaid (diffstore.py:185-203)."""
+    k, v = master_k.copy(), master_v.copy()
+    for layer, ld in enumerate(layers):
+        _overlay(k[layer], ld.indices, ld.k_blocks, block_size)
+        vidx = ld.indices if ld.v_indices is None else ld.v_indices
+        _overlay(v[layer], vidx, ld.v_blocks, block_size)
+    return k, v
+
+
+# wire format (diffstore.py:10-23, 210-306; README "Diff wire format")
+
+_HDR = struct.Struct("<4sHHIIII")
+
+
+class WireError(ValueError):
+    """Malformed serialized diff (diffstore.py:41-42)."""
+
+
+def wire_size(counts: Sequence[int], block_size: int, heads: int, dim: int) -> int:
+    """Bytes of the flag-1 serialization: 24 B header, per layer 5 B plus
+    4 B per index plus K and V payload, 4 B trailer."""
+    blk = block_size * heads * dim * 4
+    return _HDR.size + sum(5 + 4 * c + 2 * c * blk for c in counts) + 4
+
+
+def serialize(layers: Sequence[DiffLayer], block_size: int, heads: int,
+              dim: int, total: int) -> bytes:
+    buf = bytearray(_HDR.pack(b"TDDF", 1, len(layers), block_size, heads, dim, total))
+    for ld in layers:
+        shared = ld.v_indices is None
+        buf += struct.pack("<IB", ld.indices.size, 1 if shared else 0)
+        buf += ld.indices.astype("<u4").tobytes()
+        buf += np.ascontiguousarray(ld.k_blocks, dtype="<f4").tobytes()
+        if not shared:
+            buf += struct.pack("<I", ld.v_indices.size)
+            buf += ld.v_indices.astype("<u4").tobytes()
+        buf += np.ascontiguousarray(ld.v_blocks, dtype="<f4").tobytes()
+    buf += struct.pack("<I", valid_len(total, block_size))
+    return bytes(buf)
+
+
+def deserialize(buf: bytes):
+    """Strict parser: returns (geometry tuple, layers) or raises WireError."""
+    pos = 0
+
+    def take(n: int, what: str) -> bytes:
+        nonlocal pos
+        if pos + n > len(buf):
+            raise WireError(f"truncated diff: expected {what}")
+        chunk = buf[pos:pos + n]
+        pos += n
+        return chunk
+
+    magic, ver, nl, bs, h, d, total = _HDR.unpack(take(_HDR.size, "header"))
+    if magic != b"TDDF":
+        raise WireError("bad magic")
+    if ver != 1:
+        raise WireError(f"unsupported version {ver}")
+    if min(nl, bs, h, d, total) <= 0:
+        raise WireError("non-positive geometry field")
+
+    def ids(count: int, what: str) -> np.ndarray:
+        a = np.frombuffer(take(4 * count, what), dtype="<u4").astype(np.int64)
+        if a.size > 1 and not (np.diff(a) > 0).all():
+            raise WireError(f"{what} must be strictly increasing")
+        return a
+
+    def blocks(count: int, what: str) -> np.ndarray:
+        raw = take(count * bs * h * d * 4, what)
+        return np.frombuffer(raw, dtype="<f4").astype(np.float32).reshape(count, bs, h, d)
+
+    layers = []
+    for layer in range(nl):
+        (count,) = struct.unpack("<I", take(4, f"layer {layer} count"))
+        flag = take(1, f"layer {layer} index flag")[0]
+        if flag not in (0, 1):
+            raise WireError(f"layer {layer}: unknown index flag {flag}")
+        idx = ids(count, f"layer {layer} indices")
+        kb = blocks(count, f"layer {layer} K payload")
+        if flag == 1:
+            layers.append(DiffLayer(idx, kb, blocks(count, f"layer {layer} V payload")))
+        else:
+            (vc,) = struct.unpack("<I", take(4, f"layer {layer} V count"))
+            vidx = ids(vc, f"layer {layer} V indices")
+            layers.append(DiffLayer(idx, kb, blocks(vc, f"layer {layer} V payload"), vidx))
+    (vl,) = struct.unpack("<I", take(4, "valid_len trailer"))
+    if pos != len(buf):
+        raise WireError("trailing bytes after diff")
+    nbk = block_count(total, bs)
+    for ld in layers:
+        for a in (ld.indices, ld.v_indices):
+            if a is not None and a.size and (a.min() < 0 or a.max() >= nbk):
+                raise ValueError("block index out of range")
+    if vl != valid_len(total, bs):
+        raise WireError("valid_len disagrees with token count")
+    return (nl, bs, h, d, total), layers
+
+
+# ---------------------------------------------------------------------------
+# restores -- restore.py:29-139
+
+
+def fused_restore(master_k: np.ndarray, master_v: np.ndarray,
+                  layers: Sequence[DiffLayer], block_size: int,
+                  old_positions: np.ndarray, new_positions: np.ndarray,
+                  slots: np.ndarray, pool_k: np.ndarray, pool_v: np.ndarray,
+                  base: float) -> None:
+    """Per layer: master planes, diff overlaid BEFORE rotation (restore.py:5-8,
+    88), rope_recover on K, rows written to ``pool[l, slots]``."""
+    for layer, ld in enumerate(layers):
+        k = master_k[layer].copy()
+        v = master_v[layer].copy()
+        _overlay(k, ld.indices, ld.k_blocks, block_size)
+        _overlay(v, ld.indices if ld.v_indices is None else ld.v_indices,
+                 ld.v_blocks, block_size)
+        pool_k[layer, slots] = rope_recover(old_positions, new_positions, k, base)
+        pool_v[layer, slots] = v
+
+
+def dense_restore(master_k, master_v, layers, block_size, old_positions,
+                  new_positions, slots, pool_k, pool_v, base) -> None:
+    """Materialize first, then rotate and write (restore.py:107-139)."""
+    k, v = decode_dense(master_k, master_v, layers, block_size)
+    for layer in range(k.shape[0]):
+        pool_k[layer, slots] = rope_recover(old_positions, new_positions, k[layer], base)
+        pool_v[layer, slots] = v[layer]
+
+
+# ---------------------------------------------------------------------------
+# family election inputs -- collective.py:117-149
+
+
+def select_master(scores: dict) -> int:
+    """argmin over (score, id) (collective.py:117-121)."""
+    if not scores:
+        raise ValueError("cannot elect a master from an empty group")
+    return sorted(scores.items(), key=lambda kv: (kv[1], kv[0]))[0][0]
+
+
+def mirror_hints(member_entry: np.ndarray, member_offset: np.ndarray,
+                 master_entry: np.ndarray, master_offset: np.ndarray,
+                 member_important: np.ndarray, master_important: np.ndarray) -> np.ndarray:
+    """Positions where a mirror may differ from its master
+    (collective.py:124-149)."""
+    if member_entry.size != master_entry.size:
+        raise ValueError("hints are only defined for equal-length prompts")
+    fresh = (member_entry < 0) | (master_entry < 0)
+    moved = (member_entry != master_entry) | (member_offset != master_offset)
+    pos = np.flatnonzero(fresh | moved)
+    pos = np.union1d(pos, member_important)
+    return np.union1d(pos, master_important).astype(np.int64)
+
+
+def recompute_budget(fraction: float, shared_count: int) -> int:
+    """ceil(fraction*shared) with decimal-noise guard (pic.py:174-177)."""
+    return int(math.ceil(round(fraction * shared_count, 6)))

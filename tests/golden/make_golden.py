@@ -1,0 +1,338 @@
+"""Generate golden vectors from the reference package itself.
+
+Run in the build container (where ``/root/reference`` exists):
+
+    python tests/golden/make_golden.py
+
+It imports ``roundkv`` 0.1.0 read-only from ``/root/reference/pkg/src`` and
+records the reference's own outputs for the hot-path functions into small
+fixtures next to this script.  The fixtures are committed; nothing that runs
+on the GPU box reads ``/root/reference``.
+
+Inputs are regenerated from seeds wherever possible (numpy's PCG64 streams
+are platform-stable), so most fixtures hold only seeds plus the reference's
+integer outputs and SHA-256 digests of its float outputs.  Small realistic
+caches produced by the reference's toy model (which the oracle does not
+restate) are stored verbatim in ``family.npz``.
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+from types import SimpleNamespace
+
+import numpy as np
+
+sys.dont_write_bytecode = True
+sys.path.insert(0, "/root/reference/pkg/src")
+
+from roundkv.collective import collective_recover, form_groups  # noqa: E402
+from roundkv.core import CacheBlockConfig, LayeredKv, ModelConfig, PositionSpan  # noqa: E402
+from roundkv.diffstore import (  # noqa: E402
+    DiffStore, HintSoundnessError, MasterEntry, MirrorHandle, encode_diff,
+    serialize_diff,
+)
+from roundkv.ledger import CostLedger  # noqa: E402
+from roundkv.paged_pool import PagedPool  # noqa: E402
+from roundkv.pic import PicConfig, _skeleton, align_cached, prepare_request  # noqa: E402
+from roundkv.restore import dense_restore, fused_restore  # noqa: E402
+from roundkv.segment_index import SegmentCacheEntry, SegmentIndex  # noqa: E402
+from roundkv.toymodel import build_weights, full_prefill, rope_apply  # noqa: E402
+from roundkv.workload import WorkloadSpec, decode_context, generate_round  # noqa: E402
+from roundkv.core import token_digest  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def sha(*arrays) -> str:
+    h = hashlib.sha256()
+    for a in arrays:
+        a = np.ascontiguousarray(a)
+        h.update(str(a.dtype).encode() + str(a.shape).encode())
+        h.update(a.tobytes())
+    return h.hexdigest()
+
+
+def random_kv(rng, t, layers, heads, dim, start=0):
+    shape = (layers, t, heads, dim)
+    return LayeredKv(rng.standard_normal(shape).astype(np.float32),
+                     rng.standard_normal(shape).astype(np.float32),
+                     np.arange(start, start + t, dtype=np.int64))
+
+
+# ---------------------------------------------------------------------------
+
+
+def gen_rope():
+    """rope_apply on seeded K with deltas spanning +-8192 (toymodel.py:60-83)."""
+    cases = []
+    for seed, (t, h, d) in enumerate([(40, 2, 8), (33, 3, 16), (64, 2, 64), (17, 4, 128)]):
+        rng = np.random.default_rng(1000 + seed)
+        k = rng.standard_normal((t, h, d)).astype(np.float32)
+        pos = rng.integers(-8192, 8192, t).astype(np.int64)
+        cases.append({"seed": 1000 + seed, "shape": [t, h, d],
+                      "sha": sha(rope_apply(k, pos, 10000.0))})
+    return cases
+
+
+def gen_collector():
+    """A reference round through prepare_request + _skeleton + align_cached:
+    the K rows the Collector produces and the V rows it copies."""
+    model = ModelConfig(num_layers=2, num_heads=2, head_dim=16, vocab_size=512,
+                        weight_seed=5)
+    weights = build_weights(model)
+    spec = WorkloadSpec(num_agents=4, num_rounds=1, history_len=(9, 9, 9, 9),
+                        shared_block_len=11, token_seed=3, permutation_seed=8)
+    rnd = generate_round(spec, model, 0)
+    index = SegmentIndex(budget_bytes=1 << 30)
+    masters = []
+    for agent, seg in enumerate(rnd.shared_outputs):
+        ctx = decode_context(spec, model, 0, agent)
+        stream = list(ctx) + [model.separator_token] + list(seg.tokens)
+        kv = full_prefill(weights, stream)
+        lo = len(ctx) + 1
+        rows = LayeredKv(kv.k[:, lo:].copy(), kv.v[:, lo:].copy(), kv.positions[lo:].copy())
+        index.insert(SegmentCacheEntry(seg.digest, rows.positions, SimpleNamespace(kv=rows),
+                                       token_digest(ctx), rows.dense_nbytes))
+        masters.append(rows)
+    preps = [prepare_request(rnd.prompts[a], model, index, request_id=a) for a in range(4)]
+    contexts = [_skeleton(weights, p) for p in preps]
+    ledger = CostLedger(model.num_layers)
+    align_cached(preps, contexts, model.rope_base, ledger)
+    arrays = {}
+    meta = {"rope_calls_by_layer": ledger.rope_calls_by_layer, "agents": []}
+    for i, m in enumerate(masters):
+        arrays[f"master{i}_k"] = m.k
+        arrays[f"master{i}_v"] = m.v
+        arrays[f"master{i}_pos"] = m.positions
+    for a, (p, (ck, cv)) in enumerate(zip(preps, contexts)):
+        hits = []
+        for h in p.hits:
+            src = masters.index(h.kv)
+            hits.append({"master": src, "target": h.target_idx.tolist(),
+                         "delta": h.delta.tolist()})
+        shared = p.shared_idx
+        arrays[f"agent{a}_k_shared"] = ck[:, shared]
+        arrays[f"agent{a}_v_shared"] = cv[:, shared]
+        meta["agents"].append({"T": int(p.num_tokens), "hits": hits,
+                               "shared_idx": shared.tolist()})
+    np.savez_compressed(os.path.join(HERE, "collector.npz"), **arrays)
+    return meta
+
+
+def gen_family():
+    """collective_recover -> encode_family -> fused/dense restore on a small
+    toy-model round: the realistic diff inputs and the reference's outputs."""
+    model = ModelConfig(num_layers=3, num_heads=2, head_dim=8, vocab_size=512, weight_seed=21)
+    weights = build_weights(model)
+    spec = WorkloadSpec(num_agents=3, num_rounds=1, history_len=12, shared_block_len=6,
+                        token_seed=31, permutation_seed=None)
+    rnd = generate_round(spec, model, 0)
+    index = SegmentIndex(budget_bytes=1 << 30)
+    for agent, seg in enumerate(rnd.shared_outputs):
+        ctx = decode_context(spec, model, 0, agent)
+        stream = list(ctx) + [model.separator_token] + list(seg.tokens)
+        kv = full_prefill(weights, stream)
+        lo = len(ctx) + 1
+        rows = LayeredKv(kv.k[:, lo:].copy(), kv.v[:, lo:].copy(), kv.positions[lo:].copy())
+        index.insert(SegmentCacheEntry(seg.digest, rows.positions, SimpleNamespace(kv=rows),
+                                       token_digest(ctx), rows.dense_nbytes))
+    preps = [prepare_request(rnd.prompts[a], model, index, request_id=a) for a in range(3)]
+    groups, _ = form_groups(preps)
+    blocks = CacheBlockConfig(block_size=8)
+    results, plan = collective_recover(weights, groups[0], PicConfig(0.15, 1))
+    store = DiffStore(blocks)
+    enc = store.encode_family(plan, results)
+    arrays = {}
+    meta = {"master_id": int(plan.master_id), "block_size": 8, "rope_base": model.rope_base,
+            "stats": {"dense": enc.stats.dense_nbytes,
+                      "payload": enc.stats.diff_payload_nbytes,
+                      "serialized": enc.stats.diff_serialized_nbytes,
+                      "changed": enc.stats.changed_blocks,
+                      "ratios": enc.stats.ratios,
+                      "family_cost": enc.stats.family_cost},
+            "mirrors": []}
+    arrays["master_k"] = results[plan.master_id].kv.k
+    arrays["master_v"] = results[plan.master_id].kv.v
+    arrays["positions"] = results[plan.master_id].kv.positions
+    for rid, handle in sorted(enc.mirrors.items()):
+        arrays[f"mirror{rid}_k"] = results[rid].kv.k
+        arrays[f"mirror{rid}_v"] = results[rid].kv.v
+        arrays[f"hints{rid}"] = plan.mirror_diff_hints[rid]
+        wire = serialize_diff(handle.diff)
+        T = handle.master.kv.num_tokens
+        pool = PagedPool(4 * T + 32, 3, 2, 8, block_size=8)
+        fmap = pool.allocate(T, 1)
+        dmap = pool.allocate(T, 2)
+        span = PositionSpan.shifted(handle.positions, 16)
+        led = CostLedger(3)
+        fused_restore(handle, span, pool, fmap, model.rope_base, ledger=led)
+        dense_restore(handle, span, pool, dmap, model.rope_base)
+        fk = np.stack([pool.read_rows(fmap, l)[0] for l in range(3)])
+        fv = np.stack([pool.read_rows(fmap, l)[1] for l in range(3)])
+        meta["mirrors"].append({
+            "rid": int(rid),
+            "indices": [ld.indices.tolist() for ld in handle.diff.layers],
+            "wire_sha": hashlib.sha256(wire).hexdigest(),
+            "wire_len": len(wire),
+            "fused_slots": fmap.slots.tolist(),
+            "fused_sha": sha(fk, fv),
+            "bytes_moved": led.bytes_moved,
+            "temp_peak": led.temp_buffer_peak_bytes,
+        })
+    np.savez_compressed(os.path.join(HERE, "family.npz"), **arrays)
+    return meta
+
+
+def _perturb(rng, master, blocks, block_ids):
+    mirror = master.copy()
+    hints = []
+    for b in block_ids:
+        lo, hi = blocks.block_bounds(b, master.num_tokens)
+        mirror.k[:, lo:hi] = rng.standard_normal(mirror.k[:, lo:hi].shape).astype(np.float32)
+        mirror.v[:, lo:hi] = rng.standard_normal(mirror.v[:, lo:hi].shape).astype(np.float32)
+        hints.extend(range(lo, hi))
+    return mirror, np.asarray(sorted(hints), dtype=np.int64)
+
+
+def gen_codec_trials():
+    """C04-style randomized encode trials (acceptance test_c04) regenerated
+    from a seed; records indices, wire length and digest per trial."""
+    out = []
+    rng = np.random.default_rng(0xD1FF)
+    for trial in range(300):
+        bs = int(rng.choice([8, 16, 32]))
+        blocks = CacheBlockConfig(block_size=bs)
+        t = int(rng.integers(1, 180))
+        layers = int(rng.integers(1, 4))
+        heads = int(rng.integers(1, 3))
+        dim = 2 * int(rng.integers(1, 5))
+        start = int(rng.integers(0, 40))
+        master = random_kv(rng, t, layers, heads, dim, start=start)
+        mirror = master.copy()
+        nb = blocks.num_blocks(t)
+        count = int(rng.integers(0, nb + 1))
+        chosen = rng.choice(nb, size=count, replace=False)
+        hints = []
+        for b in sorted(int(b) for b in chosen):
+            lo, hi = blocks.block_bounds(b, t)
+            hints.extend(range(lo, hi))
+            mode = int(rng.integers(0, 4))
+            row = int(rng.integers(lo, hi))
+            if mode == 0:
+                mirror.k[:, lo:hi] += 1.0
+            elif mode == 1:
+                mirror.v[:, lo:hi] -= 1.0
+            elif mode == 2:
+                mirror.k[:, row] = rng.standard_normal(mirror.k[:, row].shape).astype(np.float32)
+        diff = encode_diff(master, mirror, np.asarray(hints, dtype=np.int64), blocks)
+        wire = serialize_diff(diff)
+        out.append({"indices": [ld.indices.tolist() for ld in diff.layers],
+                    "wire_len": len(wire), "wire_sha": hashlib.sha256(wire).hexdigest()})
+    return out
+
+
+def gen_known_answers():
+    """The worked examples of test_diffstore.py / acceptance C07."""
+    blocks = CacheBlockConfig(block_size=32)
+    res = {}
+    rng = np.random.default_rng(11)
+    master = random_kv(rng, 640, 4, 2, 8)
+    mirror, hints = _perturb(rng, master, blocks, [3, 17])
+    diff = encode_diff(master, mirror, hints, blocks)
+    wire = serialize_diff(diff)
+    res["worked"] = {"seed": 11, "payload": diff.payload_nbytes, "dense": master.dense_nbytes,
+                     "wire_len": len(wire), "wire_sha": hashlib.sha256(wire).hexdigest(),
+                     "changed": diff.changed_blocks_per_layer}
+    rng = np.random.default_rng(24)
+    master = random_kv(rng, 128, 4, 2, 8)
+    mirror, hints = _perturb(rng, master, blocks, [1])
+    mirror.v[0, 100, 0, 0] += 0.5
+    try:
+        encode_diff(master, mirror, hints, blocks)
+        raise AssertionError("expected a soundness error")
+    except HintSoundnessError as exc:
+        res["violation"] = {"seed": 24, "message": str(exc)}
+    rng = np.random.default_rng(21)
+    master = random_kv(rng, 70, 4, 2, 8)
+    mirror, hints = _perturb(rng, master, blocks, [2])
+    wire = serialize_diff(encode_diff(master, mirror, hints, blocks))
+    res["partial"] = {"seed": 21, "wire_sha": hashlib.sha256(wire).hexdigest(),
+                      "wire_len": len(wire)}
+    return res
+
+
+def gen_restores():
+    """C05-style fused restores (acceptance test_c05): pool digests."""
+    out = []
+    rng = np.random.default_rng(0xF05E)
+    blocks = CacheBlockConfig(block_size=16)
+    for trial in range(60):
+        t = int(rng.integers(8, 90))
+        start = int(rng.integers(0, 60))
+        delta = int(rng.integers(-start, 80))
+        master_kv = random_kv(rng, t, 3, 2, 8, start=start)
+        nb = blocks.num_blocks(t)
+        count = int(rng.integers(0, min(nb, 3) + 1))
+        chosen = sorted(int(b) for b in rng.choice(nb, count, replace=False))
+        mirror_kv, hints = _perturb(rng, master_kv, blocks, chosen)
+        diff = encode_diff(master_kv, mirror_kv, hints, blocks)
+        master = MasterEntry(0, master_kv)
+        master.pin_count = 1
+        handle = MirrorHandle(0, trial, master, diff)
+        span = PositionSpan.shifted(master_kv.positions, delta)
+        pool = PagedPool(128, 3, 2, 8, block_size=16)
+        smap = pool.allocate(t, request_id=trial)
+        led = CostLedger(3)
+        fused_restore(handle, span, pool, smap, 10000.0, ledger=led)
+        k = np.stack([pool.read_rows(smap, l)[0] for l in range(3)])
+        v = np.stack([pool.read_rows(smap, l)[1] for l in range(3)])
+        out.append({"t": t, "delta": delta, "slots": smap.slots.tolist(),
+                    "sha": sha(k, v), "bytes_moved": led.bytes_moved})
+    return out
+
+
+def gen_allocator():
+    """A seeded allocate/free stream through PagedPool (paged_pool.py:106-148)."""
+    pool = PagedPool(256, 1, 1, 2, block_size=32, debug=False)
+    rng = np.random.default_rng(7)
+    live, ops = [], []
+    for step in range(300):
+        if live and (rng.random() < 0.45 or pool.free_count < 20):
+            i = int(rng.integers(len(live)))
+            m = live.pop(i)
+            pool.free(m)
+            ops.append({"op": "free", "serial": m.serial})
+        else:
+            n = int(rng.integers(1, 40))
+            if n > pool.free_count:
+                ops.append({"op": "skip", "n": n})
+                continue
+            m = pool.allocate(n, request_id=step)
+            live.append(m)
+            ops.append({"op": "alloc", "n": n, "serial": m.serial, "slots": m.slots.tolist()})
+    return ops
+
+
+def main():
+    golden = {
+        "generator": "tests/golden/make_golden.py",
+        "reference": "roundkv 0.1.0 (/root/reference/pkg/src)",
+        "numpy": np.__version__,
+        "rope": gen_rope(),
+        "collector": gen_collector(),
+        "family": gen_family(),
+        "codec_trials": gen_codec_trials(),
+        "known": gen_known_answers(),
+        "restores": gen_restores(),
+        "allocator": gen_allocator(),
+    }
+    with open(os.path.join(HERE, "golden.json"), "w") as f:
+        json.dump(golden, f, indent=1, sort_keys=True)
+    print("wrote", os.path.join(HERE, "golden.json"))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,123 @@
+"""Seeded input generators shared by the CPU and GPU parity tests.
+
+The random streams match the ones the reference tests draw
+(``pkg/tests/conftest.py:54-73``) and ``tests/golden/make_golden.py``, so
+the golden digests recorded from the reference apply to these inputs.
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+GOLDEN_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def load_golden() -> dict:
+    with open(os.path.join(GOLDEN_DIR, "golden.json")) as f:
+        return json.load(f)
+
+
+def load_npz(name: str):
+    return np.load(os.path.join(GOLDEN_DIR, name))
+
+
+def sha(*arrays) -> str:
+    h = hashlib.sha256()
+    for a in arrays:
+        a = np.ascontiguousarray(a)
+        h.update(str(a.dtype).encode() + str(a.shape).encode())
+        h.update(a.tobytes())
+    return h.hexdigest()
+
+
+def random_planes(rng, t, layers=4, heads=2, dim=8, start=0):
+    shape = (layers, t, heads, dim)
+    k = rng.standard_normal(shape).astype(np.float32)
+    v = rng.standard_normal(shape).astype(np.float32)
+    return k, v, np.arange(start, start + t, dtype=np.int64)
+
+
+def perturb(rng, k, v, block_size, block_ids):
+    """Mirror = master with whole blocks re-drawn in every layer."""
+    t = k.shape[1]
+    mk, mv = k.copy(), v.copy()
+    hints = []
+    for b in block_ids:
+        lo, hi = b * block_size, min(b * block_size + block_size, t)
+        mk[:, lo:hi] = rng.standard_normal(mk[:, lo:hi].shape).astype(np.float32)
+        mv[:, lo:hi] = rng.standard_normal(mv[:, lo:hi].shape).astype(np.float32)
+        hints.extend(range(lo, hi))
+    return mk, mv, np.asarray(sorted(hints), dtype=np.int64)
+
+
+@dataclass
+class CodecTrial:
+    block_size: int
+    master_k: np.ndarray
+    master_v: np.ndarray
+    positions: np.ndarray
+    mirror_k: np.ndarray
+    mirror_v: np.ndarray
+    hints: np.ndarray
+
+
+def codec_trials(n=300):
+    """The acceptance-C04 trial stream (pkg/tests/test_acceptance.py:186-228)."""
+    rng = np.random.default_rng(0xD1FF)
+    for _ in range(n):
+        bs = int(rng.choice([8, 16, 32]))
+        t = int(rng.integers(1, 180))
+        layers = int(rng.integers(1, 4))
+        heads = int(rng.integers(1, 3))
+        dim = 2 * int(rng.integers(1, 5))
+        start = int(rng.integers(0, 40))
+        k, v, pos = random_planes(rng, t, layers, heads, dim, start)
+        mk, mv = k.copy(), v.copy()
+        nb = -(-t // bs)
+        count = int(rng.integers(0, nb + 1))
+        chosen = rng.choice(nb, size=count, replace=False)
+        hints = []
+        for b in sorted(int(b) for b in chosen):
+            lo, hi = b * bs, min(b * bs + bs, t)
+            hints.extend(range(lo, hi))
+            mode = int(rng.integers(0, 4))
+            row = int(rng.integers(lo, hi))
+            if mode == 0:
+                mk[:, lo:hi] += 1.0
+            elif mode == 1:
+                mv[:, lo:hi] -= 1.0
+            elif mode == 2:
+                mk[:, row] = rng.standard_normal(mk[:, row].shape).astype(np.float32)
+        yield CodecTrial(bs, k, v, pos, mk, mv, np.asarray(hints, dtype=np.int64))
+
+
+@dataclass
+class RestoreTrial:
+    block_size: int
+    master_k: np.ndarray
+    master_v: np.ndarray
+    positions: np.ndarray
+    mirror_k: np.ndarray
+    mirror_v: np.ndarray
+    hints: np.ndarray
+    delta: int
+
+
+def restore_trials(n=60):
+    """The acceptance-C05 trial stream (pkg/tests/test_acceptance.py:231-279)."""
+    rng = np.random.default_rng(0xF05E)
+    bs = 16
+    for _ in range(n):
+        t = int(rng.integers(8, 90))
+        start = int(rng.integers(0, 60))
+        delta = int(rng.integers(-start, 80))
+        k, v, pos = random_planes(rng, t, 3, 2, 8, start)
+        nb = -(-t // bs)
+        count = int(rng.integers(0, min(nb, 3) + 1))
+        chosen = sorted(int(b) for b in rng.choice(nb, count, replace=False))
+        mk, mv, hints = perturb(rng, k, v, bs, chosen)
+        yield RestoreTrial(bs, k, v, pos, mk, mv, hints, delta)
