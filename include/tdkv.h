@@ -1,0 +1,210 @@
+/*
+ * tdkv.h -- C-ABI of the B200 KV Collector + block-sparse diff codec.
+ *
+ * Drop-in boundary for the hot path of TokenDance's reference package
+ * ``roundkv`` 0.1.0 (paths below are relative to /root/reference/pkg/src/roundkv).
+ * The reference has no FFI layer (it is pure Python + numpy);
+ * each entry point below is what a binding for the named Python function
+ * would call.  INTEGRATION.md shows the ctypes binding.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  Pointers prefixed ``d_`` are device
+ *     pointers; everything else is host memory.  ``stream`` is a cudaStream_t
+ *     passed as void* (NULL = legacy default stream).
+ *   - Every function returns 0 on success or a TDKV_E* code; a message for
+ *     the most recent failure on the calling thread is available from
+ *     tdkv_last_error().  No call synchronizes the stream.
+ *   - KV planes are (num_layers, rows, num_heads, head_dim) with a given
+ *     layer stride in ELEMENTS; a "row" is one token's H*D elements.
+ *   - dtype: TDKV_F32 (rotation evaluated in float64 with one final
+ *     round-to-nearest, bit-compatible with toymodel.py:60-83) or TDKV_BF16
+ *     (rotation in float32 with float32 cos/sin derived from the float64
+ *     angle, result rounded to bf16).
+ *   - Rotary pairs are interleaved (2j, 2j+1) (toymodel.py:78-82).
+ *   - Reentrant: no global mutable state except a launch counter.
+ */
+#ifndef TDKV_H
+#define TDKV_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TDKV_F32 0
+#define TDKV_BF16 1
+
+#define TDKV_OK 0
+#define TDKV_EINVAL 1     /* bad argument (shape, pointer, alignment) */
+#define TDKV_EUNSUPPORTED 2
+#define TDKV_ECUDA 3      /* a CUDA launch/runtime error */
+
+#define TDKV_NO_VIOLATION 0x7f7f7f7f
+
+/* Library version, (major << 16) | minor. */
+int32_t tdkv_version(void);
+/* Message for the last failing call on this thread ("" if none). */
+const char* tdkv_last_error(void);
+/* Number of kernels this library has launched in the process so far. */
+int64_t tdkv_launch_count(void);
+
+/* ------------------------------------------------------------------------
+ * K0  rotary table.  Replaces the angle/cos/sin part of rope_apply
+ * (toymodel.py:73-77).  For each row r and pair j:
+ *     theta = (double)d_deltas[r] * d_inv_freq[j]         (IEEE mul)
+ *     table[r][j] = (cos theta, sin theta)
+ * stored as double2 (table_dtype TDKV_F32) or float2 (TDKV_BF16).
+ * d_inv_freq holds base^(-2j/D) computed by the caller (toymodel.py:74).
+ * ---------------------------------------------------------------------- */
+int32_t tdkv_rope_table(const int64_t* d_deltas, int64_t n_rows,
+                        const double* d_inv_freq, int32_t half_dim,
+                        int32_t table_dtype, void* d_table, void* stream);
+
+/* ------------------------------------------------------------------------
+ * K1  KV Collector.  Replaces pic.align_cached (pic.py:208-235) fused with
+ * the _skeleton V copy (pic.py:203-204) and PagedPool.write_rows
+ * (paged_pool.py:150-156, reached via trace._write_cache trace.py:148-152).
+ *
+ * The master arena holds every shared segment's cached rows:
+ * d_master_{k,v}[layer * master_layer_stride + row * H * D + e].
+ * A unit is a tile of <= max_rows consecutive arena rows of ONE segment
+ * plus a range of jobs [job_begin, job_end) that hold that segment; the
+ * tile is staged once in shared memory (cp.async.bulk) and written to every
+ * job.  For job j and segment-relative token i the destination row is
+ * d_dst_rows[job.dst_off + i] and the cos/sin row is
+ * job.tbl_row + i * job.tbl_stride.  rotate == 0 copies K unchanged (the
+ * reference skips rope_apply when every delta is zero, pic.py:228).
+ * ---------------------------------------------------------------------- */
+typedef struct {
+    int64_t dst_off;     /* index of token 0 of this job in d_dst_rows */
+    int32_t seg_row0;    /* arena row of token 0 of the job's segment */
+    int32_t tbl_row;     /* cos/sin row of token 0 */
+    int32_t tbl_stride;  /* 0: one delta for the whole job, 1: per token */
+    int32_t pad_;
+} tdkv_collect_job;
+
+typedef struct {
+    int32_t row0;        /* first arena row of the tile */
+    int32_t nrows;       /* rows in the tile (<= max_rows) */
+    int32_t job_begin;
+    int32_t job_end;
+} tdkv_collect_unit;
+
+int32_t tdkv_collect(const void* d_master_k, const void* d_master_v,
+                     int64_t master_layer_stride,
+                     const tdkv_collect_unit* d_units, int32_t n_units,
+                     int32_t max_rows,
+                     const tdkv_collect_job* d_jobs, const int64_t* d_dst_rows,
+                     const void* d_table, int32_t rotate,
+                     void* d_dst_k, void* d_dst_v, int64_t dst_layer_stride,
+                     int32_t num_layers, int32_t num_heads, int32_t head_dim,
+                     int32_t dtype, int32_t grid_limit, void* stream);
+/* d_master_v == d_dst_v == NULL makes a K-only collect (align_cached alone;
+ * the reference copies V in _skeleton). */
+
+/* ------------------------------------------------------------------------
+ * K2  block-diff encoder.  Replaces diffstore.encode_diff
+ * (diffstore.py:119-182) for a batch of (master, mirror) pairs of identical
+ * geometry (L, T, H, D), dense planes with layer stride T*H*D.
+ *
+ * tdkv_diff_compare: for every pair p, layer l, block b
+ *     changed[(p*L + l)*nb + b] = any(mirror != master) over K and V rows
+ * with float '!=' semantics (np.array_equal, diffstore.py:151-153).  A
+ * changed block whose d_hinted[p*nb + b] is 0 is a soundness violation:
+ * d_violation[p] receives the smallest l*nb + b (layer-major order, the
+ * reference's first raise) and d_viol_maxabs[(p*L+l)*nb + b] the block's
+ * max |mirror - master| over both planes (diffstore.py:157-160).
+ *
+ * tdkv_diff_compact: per (p, l), stream-compacts the changed blocks in
+ * ascending order: indices[l*cap + s] = b, counts[p*L + l] = n, payload
+ * block (l*cap + s) = mirror rows of block b zero-padded to block_size
+ * (_pad_rows, diffstore.py:110-116), and blkmap[l*nb + b] = l*cap + s for
+ * changed blocks, -1 otherwise.  cap must be >= the number of changed blocks
+ * of any layer (the hinted-block count is a bound when there is no
+ * violation).
+ * ---------------------------------------------------------------------- */
+typedef struct {
+    const void* master_k;
+    const void* master_v;
+    const void* mirror_k;
+    const void* mirror_v;
+} tdkv_diff_pair;
+
+typedef struct {
+    void* payload_k;     /* (L*cap, block_size, H, D) */
+    void* payload_v;
+    int32_t* indices;    /* (L*cap) */
+    int32_t* blkmap;     /* (L*nb) */
+    int32_t cap;
+    int32_t pad_;
+} tdkv_diff_out;
+
+int32_t tdkv_diff_compare(const tdkv_diff_pair* d_pairs, int32_t n_pairs,
+                          const uint8_t* d_hinted,
+                          uint8_t* d_changed, int32_t* d_violation,
+                          float* d_viol_maxabs,
+                          int32_t num_layers, int32_t num_tokens,
+                          int32_t num_heads, int32_t head_dim,
+                          int32_t block_size, int32_t dtype, void* stream);
+
+int32_t tdkv_diff_compact(const tdkv_diff_pair* d_pairs,
+                          const tdkv_diff_out* d_outs, int32_t n_pairs,
+                          const uint8_t* d_changed, int32_t* d_counts,
+                          int32_t num_layers, int32_t num_tokens,
+                          int32_t num_heads, int32_t head_dim,
+                          int32_t block_size, int32_t dtype, void* stream);
+
+/* ------------------------------------------------------------------------
+ * K3  row mover: gather -> (diff overlay) -> rotate -> scatter.
+ * Replaces restore.fused_restore (restore.py:50-104, with _apply_layer_diff
+ * :39-47 and rope_recover toymodel.py:86-96), diff_decode_dense
+ * (diffstore.py:185-203), dense_restore (restore.py:107-139), rope_apply /
+ * rope_recover, and PagedPool.write_rows / read_rows (paged_pool.py:150-164).
+ *
+ * For job j, layer l, token t (block b = t / block_size):
+ *   if map_k && map_k[l*nb + b] >= 0: K source = pay_k row
+ *        (map_k[l*nb+b] * block_size + t - b*block_size)
+ *   else K source = src_k[l*src_layer_stride + srow(t)*H*D],
+ *        srow(t) = src_rows ? src_rows[t] : t
+ *   (V likewise with map_v / pay_v; the diff overlays BEFORE rotation,
+ *   restore.py:5-8)
+ *   K is rotated with cos/sin row tbl_row + t*tbl_stride when rotate != 0,
+ *   then K and V are written to dst row drow(t) = dst_rows ? dst_rows[t] : t.
+ *   dst_v == NULL makes a K-only job (rope_apply).
+ * ---------------------------------------------------------------------- */
+typedef struct {
+    const void* src_k;
+    const void* src_v;
+    int64_t src_layer_stride;    /* elements */
+    const int64_t* src_rows;     /* NULL = identity */
+    const void* pay_k;
+    const void* pay_v;
+    const int32_t* map_k;        /* NULL = no diff */
+    const int32_t* map_v;
+    void* dst_k;
+    void* dst_v;
+    int64_t dst_layer_stride;    /* elements */
+    const int64_t* dst_rows;     /* NULL = identity */
+    int32_t num_tokens;
+    int32_t tbl_row;
+    int32_t tbl_stride;
+    int32_t rotate;
+} tdkv_rows_job;
+
+int32_t tdkv_rows(const tdkv_rows_job* d_jobs, int32_t n_jobs,
+                  int32_t max_tokens, const void* d_table,
+                  int32_t num_layers, int32_t num_heads, int32_t head_dim,
+                  int32_t block_size, int32_t dtype, int32_t grid_limit,
+                  void* stream);
+
+/* Fill rows of every layer with a value (NaN poisoning of freed slots,
+ * paged_pool.py:144-147).  value_bits is the element bit pattern. */
+int32_t tdkv_fill_rows(void* d_plane, int64_t layer_stride, int32_t num_layers,
+                       const int64_t* d_rows, int64_t n_rows, int32_t row_elems,
+                       int32_t dtype, uint32_t value_bits, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TDKV_H */

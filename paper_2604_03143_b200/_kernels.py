@@ -1,0 +1,90 @@
+"""Thin typed wrappers over the tdkv C-ABI entry points.
+
+Each wrapper takes torch device tensors, uploads the small descriptor tables
+the kernel needs, and launches on the current CUDA stream.
+"""
+from __future__ import annotations
+
+from functools import lru_cache
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._device import dtype_code, ptr, stream_handle, table_dtype, upload
+
+ROWS_BLOCK = 32          # tiling of the row mover when no diff geometry applies
+
+
+def inv_freq_host(head_dim: int, base: float) -> np.ndarray:
+    """base^(-2j/D) in float64, the expression of toymodel.py:74."""
+    return float(base) ** (-np.arange(0, head_dim, 2, dtype=np.float64) / head_dim)
+
+
+@lru_cache(maxsize=64)
+def _inv_freq_dev(device_index: int, head_dim: int, base: float) -> torch.Tensor:
+    return torch.from_numpy(inv_freq_host(head_dim, base)).to(
+        torch.device("cuda", device_index))
+
+
+def rope_table(deltas: np.ndarray, head_dim: int, base: float, kv_dtype: torch.dtype,
+               device: torch.device) -> torch.Tensor:
+    """K0: (n, D/2, 2) cos/sin rows for the given int64 deltas."""
+    deltas = np.ascontiguousarray(deltas, dtype=np.int64)
+    n = int(deltas.size)
+    tdt = table_dtype(kv_dtype)
+    out = torch.empty((max(n, 1), head_dim // 2, 2), dtype=tdt, device=device)
+    if n == 0:
+        return out
+    d_deltas = torch.from_numpy(deltas).to(device)
+    inv = _inv_freq_dev(device.index, head_dim, float(base))
+    _lib.call("tdkv_rope_table", ptr(d_deltas), n, ptr(inv), head_dim // 2,
+              dtype_code(kv_dtype), ptr(out), stream_handle(device))
+    return out
+
+
+def rope_table_from_device(d_deltas: torch.Tensor, head_dim: int, base: float,
+                           kv_dtype: torch.dtype, out: torch.Tensor) -> torch.Tensor:
+    """K0 on an already-resident delta vector (used by planned, replayable rounds)."""
+    inv = _inv_freq_dev(d_deltas.device.index, head_dim, float(base))
+    n = int(d_deltas.numel())
+    if n:
+        _lib.call("tdkv_rope_table", ptr(d_deltas), n, ptr(inv), head_dim // 2,
+                  dtype_code(kv_dtype), ptr(out), stream_handle(d_deltas.device))
+    return out
+
+
+def rows(jobs: np.ndarray, max_tokens: int, table: Optional[torch.Tensor], num_layers: int,
+         num_heads: int, head_dim: int, block_size: int, kv_dtype: torch.dtype,
+         device: torch.device, grid_limit: int = 0) -> None:
+    """K3 over a ROWS_JOB descriptor array."""
+    if jobs.size == 0 or max_tokens == 0:
+        return
+    d_jobs = upload(jobs, device)
+    _lib.call("tdkv_rows", ptr(d_jobs), int(jobs.size), int(max_tokens), ptr(table),
+              num_layers, num_heads, head_dim, block_size, dtype_code(kv_dtype), grid_limit,
+              stream_handle(device))
+
+
+def rows_job(src_k, src_v, src_layer_stride, dst_k, dst_v, dst_layer_stride, num_tokens, *,
+             src_rows=None, dst_rows=None, pay_k=None, pay_v=None, map_k=None, map_v=None,
+             tbl_row=0, tbl_stride=0, rotate=0) -> tuple:
+    return (ptr(src_k), ptr(src_v), int(src_layer_stride), ptr(src_rows), ptr(pay_k),
+            ptr(pay_v), ptr(map_k), ptr(map_v), ptr(dst_k), ptr(dst_v), int(dst_layer_stride),
+            ptr(dst_rows), int(num_tokens), int(tbl_row), int(tbl_stride), int(rotate))
+
+
+def rows_jobs(tuples) -> np.ndarray:
+    return np.array(list(tuples), dtype=_lib.ROWS_JOB)
+
+
+def fill_rows(plane: torch.Tensor, rows_dev: torch.Tensor, value: float) -> None:
+    """Write ``value`` into the given rows of every layer of a (L, cap, H, D) plane."""
+    L, cap, H, D = plane.shape
+    if plane.dtype == torch.float32:
+        bits = int(np.array([value], np.float32).view(np.uint32)[0])
+    else:
+        bits = int(torch.tensor([value], dtype=torch.bfloat16).view(torch.int16).item()) & 0xFFFF
+    _lib.call("tdkv_fill_rows", ptr(plane), cap * H * D, L, ptr(rows_dev), int(rows_dev.numel()),
+              H * D, dtype_code(plane.dtype), bits, stream_handle(plane.device))

@@ -1,0 +1,151 @@
+"""ctypes binding of libtdkv.so (the C-ABI declared in include/tdkv.h).
+
+The shared library is built in-tree by ``build_library()`` (nvcc, sm_100a)
+and loaded from this package directory.  There is no fallback: if the
+library is missing every entry point raises ``TdkvUnavailable``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+from typing import Optional
+
+import numpy as np
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG_DIR)
+LIB_PATH = os.path.join(PKG_DIR, "libtdkv.so")
+CSRC = os.path.join(PKG_DIR, "csrc")
+INCLUDE = os.path.join(ROOT, "include")
+
+TDKV_F32 = 0
+TDKV_BF16 = 1
+NO_VIOLATION = 0x7F7F7F7F
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    "-Xcompiler", "-fPIC", "-shared",
+]
+
+
+class TdkvUnavailable(RuntimeError):
+    """libtdkv.so is not built or cannot be loaded (no CPU fallback exists)."""
+
+
+class TdkvError(RuntimeError):
+    """A tdkv C-ABI call returned a non-zero status."""
+
+
+# ---------------------------------------------------------------------------
+# build
+
+
+def sources():
+    return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cu"))
+
+
+def build_library(force: bool = False, verbose: bool = False) -> str:
+    """Compile csrc/*.cu into libtdkv.so for sm_100a (cross-compiles without a GPU)."""
+    srcs = sources()
+    deps = srcs + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")]
+    deps.append(os.path.join(INCLUDE, "tdkv.h"))
+    if not force and os.path.exists(LIB_PATH):
+        built = os.path.getmtime(LIB_PATH)
+        if all(os.path.getmtime(d) <= built for d in deps):
+            return LIB_PATH
+    nvcc = os.environ.get("NVCC", "nvcc")
+    tmp = LIB_PATH + ".tmp"
+    cmd = [nvcc, *NVCC_FLAGS, "-I", INCLUDE, *srcs, "-o", tmp]
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.run(cmd, check=True)
+    os.replace(tmp, LIB_PATH)
+    return LIB_PATH
+
+
+# ---------------------------------------------------------------------------
+# descriptor layouts (must match include/tdkv.h)
+
+COLLECT_JOB = np.dtype([("dst_off", "<i8"), ("seg_row0", "<i4"), ("tbl_row", "<i4"),
+                        ("tbl_stride", "<i4"), ("pad", "<i4")])
+COLLECT_UNIT = np.dtype([("row0", "<i4"), ("nrows", "<i4"), ("job_begin", "<i4"),
+                         ("job_end", "<i4")])
+DIFF_PAIR = np.dtype([("master_k", "<u8"), ("master_v", "<u8"), ("mirror_k", "<u8"),
+                      ("mirror_v", "<u8")])
+DIFF_OUT = np.dtype([("payload_k", "<u8"), ("payload_v", "<u8"), ("indices", "<u8"),
+                     ("blkmap", "<u8"), ("cap", "<i4"), ("pad", "<i4")])
+ROWS_JOB = np.dtype([("src_k", "<u8"), ("src_v", "<u8"), ("src_layer_stride", "<i8"),
+                     ("src_rows", "<u8"), ("pay_k", "<u8"), ("pay_v", "<u8"),
+                     ("map_k", "<u8"), ("map_v", "<u8"), ("dst_k", "<u8"), ("dst_v", "<u8"),
+                     ("dst_layer_stride", "<i8"), ("dst_rows", "<u8"), ("num_tokens", "<i4"),
+                     ("tbl_row", "<i4"), ("tbl_stride", "<i4"), ("rotate", "<i4")])
+assert COLLECT_JOB.itemsize == 24 and COLLECT_UNIT.itemsize == 16
+assert DIFF_PAIR.itemsize == 32 and DIFF_OUT.itemsize == 40 and ROWS_JOB.itemsize == 112
+
+EXPORTS = (
+    "tdkv_version", "tdkv_last_error", "tdkv_launch_count", "tdkv_rope_table",
+    "tdkv_collect", "tdkv_diff_compare", "tdkv_diff_compact", "tdkv_rows",
+    "tdkv_fill_rows",
+)
+
+_P = ctypes.c_void_p
+_I32 = ctypes.c_int32
+_I64 = ctypes.c_int64
+_SIGS = {
+    "tdkv_version": (_I32, []),
+    "tdkv_last_error": (ctypes.c_char_p, []),
+    "tdkv_launch_count": (_I64, []),
+    "tdkv_rope_table": (_I32, [_P, _I64, _P, _I32, _I32, _P, _P]),
+    "tdkv_collect": (_I32, [_P, _P, _I64, _P, _I32, _I32, _P, _P, _P, _I32, _P, _P, _I64,
+                            _I32, _I32, _I32, _I32, _I32, _P]),
+    "tdkv_diff_compare": (_I32, [_P, _I32, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32,
+                                 _I32, _P]),
+    "tdkv_diff_compact": (_I32, [_P, _P, _I32, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32,
+                                 _P]),
+    "tdkv_rows": (_I32, [_P, _I32, _I32, _P, _I32, _I32, _I32, _I32, _I32, _I32, _P]),
+    "tdkv_fill_rows": (_I32, [_P, _I64, _I32, _P, _I64, _I32, _I32, ctypes.c_uint32, _P]),
+}
+
+_lib: Optional[ctypes.CDLL] = None
+_lock = threading.Lock()
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libtdkv.so (once).  Raises TdkvUnavailable when it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise TdkvUnavailable(
+                f"{path} is not built; run __graft_entry__.build() (nvcc sm_100a). "
+                "There is no CPU fallback.")
+        lib = ctypes.CDLL(path)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def call(name: str, *args) -> None:
+    """Invoke a tdkv entry point; raise TdkvError with the library's message."""
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if rc != 0:
+        msg = lib.tdkv_last_error().decode(errors="replace")
+        raise TdkvError(f"{name} failed ({rc}): {msg}")
+
+
+def launch_count() -> int:
+    return int(load().tdkv_launch_count())
+
+
+def version() -> int:
+    return int(load().tdkv_version())

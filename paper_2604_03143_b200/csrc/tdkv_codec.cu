@@ -1,0 +1,272 @@
+// K2 block-diff encoder: compare + stream compaction.
+//
+// Replaces diffstore.encode_diff (diffstore.py:119-182).  The compare pass
+// streams both dense caches once (the reference compares every block,
+// diffstore.py:149-165) and reduces a per-block "any element differs" flag
+// with float '!=' semantics; the compact pass scans each (pair, layer) row of
+// flags in block order and copies the changed mirror blocks, zero-padded,
+// into the payload in ascending index order (diffstore.py:166-173).
+#include <climits>
+
+#include "tdkv_common.cuh"
+
+namespace tdkv {
+
+struct CodecGeom {
+    int32_t num_layers;
+    int32_t num_tokens;
+    int32_t row_elems;
+    int32_t block_size;
+    int32_t nb;
+};
+
+template <typename T, int UB>
+__global__ void __launch_bounds__(256)
+    diff_compare_kernel(const tdkv_diff_pair* __restrict__ pairs, const uint8_t* __restrict__ hinted,
+                        uint8_t* __restrict__ changed, int32_t* __restrict__ violation,
+                        float* __restrict__ viol_maxabs, const CodecGeom g) {
+    using V = typename UnitBits<UB>::V;
+    constexpr int kUnroll = 2;
+    const int item = blockIdx.x;                 // (pair, layer, block)
+    const int per_pair = g.num_layers * g.nb;
+    const int pi = item / per_pair;
+    const int rem = item - pi * per_pair;
+    const int layer = rem / g.nb;
+    const int b = rem - layer * g.nb;
+    const int lo = b * g.block_size;
+    const int hi = min(lo + g.block_size, g.num_tokens);
+    const int upr = g.row_elems * (int)sizeof(T) / UB;
+    const int units = (hi - lo) * upr;
+    const size_t off_units = ((size_t)layer * g.num_tokens + lo) * upr;
+
+    const tdkv_diff_pair pr = pairs[pi];
+    const V* mk = static_cast<const V*>(pr.master_k) + off_units;
+    const V* mv = static_cast<const V*>(pr.master_v) + off_units;
+    const V* rk = static_cast<const V*>(pr.mirror_k) + off_units;
+    const V* rv = static_cast<const V*>(pr.mirror_v) + off_units;
+
+    bool diff = false;
+    int u = threadIdx.x;
+    for (; u + (kUnroll - 1) * (int)blockDim.x < units; u += kUnroll * blockDim.x) {
+        V a[kUnroll][4];
+#pragma unroll
+        for (int q = 0; q < kUnroll; ++q) {
+            const int w = u + q * blockDim.x;
+            a[q][0] = ld_stream(mk + w);
+            a[q][1] = ld_stream(rk + w);
+            a[q][2] = ld_stream(mv + w);
+            a[q][3] = ld_stream(rv + w);
+        }
+#pragma unroll
+        for (int q = 0; q < kUnroll; ++q)
+            diff |= unit_differs<T>(a[q][0], a[q][1]) | unit_differs<T>(a[q][2], a[q][3]);
+    }
+    for (; u < units; u += blockDim.x) {
+        diff |= unit_differs<T>(ld_stream(mk + u), ld_stream(rk + u)) |
+                unit_differs<T>(ld_stream(mv + u), ld_stream(rv + u));
+    }
+    const int any = __syncthreads_or(diff);
+    if (threadIdx.x == 0) changed[item] = (uint8_t)(any != 0);
+    if (!any || hinted[(size_t)pi * g.nb + b]) return;
+
+    // soundness violation (rare): max |mirror - master| over both planes
+    float m = 0.f;
+    for (int w = threadIdx.x; w < units; w += blockDim.x) {
+        m = fmaxf(m, unit_maxabs<T>(mk[w], rk[w]));
+        m = fmaxf(m, unit_maxabs<T>(mv[w], rv[w]));
+    }
+    __shared__ float red[32];
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float mm = 0.f;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mm = fmaxf(mm, red[w]);
+        viol_maxabs[item] = mm;
+        atomicMin(violation + pi, layer * g.nb + b);
+    }
+}
+
+// One CTA per (pair, layer): block-ordered scan of the change flags in
+// chunks of blockDim.x, then a cooperative copy of each changed block.
+template <typename T, int UB>
+__global__ void __launch_bounds__(256)
+    diff_compact_kernel(const tdkv_diff_pair* __restrict__ pairs, const tdkv_diff_out* __restrict__ outs,
+                        const uint8_t* __restrict__ changed, int32_t* __restrict__ counts,
+                        const CodecGeom g) {
+    using V = typename UnitBits<UB>::V;
+    const int pi = blockIdx.x / g.num_layers;
+    const int layer = blockIdx.x - pi * g.num_layers;
+    const uint8_t* flags = changed + ((size_t)pi * g.num_layers + layer) * g.nb;
+    const tdkv_diff_out out = outs[pi];
+    const tdkv_diff_pair pr = pairs[pi];
+    const int upr = g.row_elems * (int)sizeof(T) / UB;
+    const int blk_units = g.block_size * upr;
+
+    __shared__ int s_warp[32];
+    __shared__ int s_list[256];
+    __shared__ int s_total;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nwarps = blockDim.x >> 5;
+    int running = 0;
+
+    for (int base = 0; base < g.nb; base += blockDim.x) {
+        const int b = base + threadIdx.x;
+        const bool f = b < g.nb && flags[b];
+        const unsigned bal = __ballot_sync(0xffffffffu, f);
+        if (lane == 0) s_warp[warp] = __popc(bal);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int acc = 0;
+            for (int w = 0; w < nwarps; ++w) {
+                const int c = s_warp[w];
+                s_warp[w] = acc;
+                acc += c;
+            }
+            s_total = acc;
+        }
+        __syncthreads();
+        const int local = s_warp[warp] + __popc(bal & ((1u << lane) - 1u));
+        if (b < g.nb) {
+            if (f) {
+                // slots past ``cap`` only occur on a soundness violation (the
+                // host reports it); never write outside this layer's region
+                const int slot = running + local;
+                if (slot < out.cap) {
+                    out.indices[layer * out.cap + slot] = b;
+                    out.blkmap[layer * g.nb + b] = layer * out.cap + slot;
+                } else {
+                    out.blkmap[layer * g.nb + b] = -1;
+                }
+                s_list[local] = b;
+            } else {
+                out.blkmap[layer * g.nb + b] = -1;
+            }
+        }
+        __syncthreads();
+        const int n = s_total;
+        // copy the n changed blocks of this chunk
+        const int n_copy = max(0, min(n, out.cap - running));
+        for (int i = 0; i < n_copy; ++i) {
+            const int blk = s_list[i];
+            const int lo = blk * g.block_size;
+            const int rows = min(g.block_size, g.num_tokens - lo);
+            const size_t src = ((size_t)layer * g.num_tokens + lo) * upr;
+            const size_t dst = ((size_t)layer * out.cap + running + i) * blk_units;
+            const V* sk = static_cast<const V*>(pr.mirror_k) + src;
+            const V* sv = static_cast<const V*>(pr.mirror_v) + src;
+            V* pk = static_cast<V*>(out.payload_k) + dst;
+            V* pv = static_cast<V*>(out.payload_v) + dst;
+            const int valid = rows * upr;
+            for (int w = threadIdx.x; w < blk_units; w += blockDim.x) {
+                V kx, vx;
+                if (w < valid) {
+                    kx = ld_stream(sk + w);
+                    vx = ld_stream(sv + w);
+                } else {
+                    kx = V{};
+                    vx = V{};
+                }
+                pk[w] = kx;
+                pv[w] = vx;
+            }
+        }
+        running += n;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) counts[pi * g.num_layers + layer] = running;
+}
+
+}  // namespace tdkv
+
+using namespace tdkv;
+
+static int32_t codec_check(const char* who, int32_t n_pairs, int32_t L, int32_t T, int32_t H,
+                           int32_t D, int32_t bs, int32_t dtype) {
+    if (n_pairs < 0 || L <= 0 || T <= 0 || H <= 0 || D <= 0 || bs <= 0)
+        return set_error(TDKV_EINVAL, "%s: bad geometry pairs=%d L=%d T=%d H=%d D=%d bs=%d", who,
+                         n_pairs, L, T, H, D, bs);
+    if (dtype != TDKV_F32 && dtype != TDKV_BF16)
+        return set_error(TDKV_EUNSUPPORTED, "%s: dtype %d", who, dtype);
+    return TDKV_OK;
+}
+
+// unit width for the codec: 16 B when a row is a whole number of 16-byte
+// units (the caller guarantees 16-byte aligned dense planes in that case),
+// otherwise 4 bytes (rows are always a multiple of 4 bytes).
+static int codec_unit(int32_t dtype, int32_t row_elems) {
+    return (row_elems * (int)elt_size(dtype)) % 16 == 0 ? 16 : 4;
+}
+
+extern "C" int32_t tdkv_diff_compare(const tdkv_diff_pair* d_pairs, int32_t n_pairs,
+                                     const uint8_t* d_hinted, uint8_t* d_changed,
+                                     int32_t* d_violation, float* d_viol_maxabs,
+                                     int32_t num_layers, int32_t num_tokens, int32_t num_heads,
+                                     int32_t head_dim, int32_t block_size, int32_t dtype,
+                                     void* stream) {
+    int32_t rc = codec_check("tdkv_diff_compare", n_pairs, num_layers, num_tokens, num_heads,
+                             head_dim, block_size, dtype);
+    if (rc) return rc;
+    if (n_pairs == 0) return TDKV_OK;
+    if (!d_pairs || !d_hinted || !d_changed || !d_violation || !d_viol_maxabs)
+        return set_error(TDKV_EINVAL, "tdkv_diff_compare: null pointer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    CodecGeom g{num_layers, num_tokens, num_heads * head_dim, block_size,
+                ceil_div(num_tokens, block_size)};
+    const long long items = (long long)n_pairs * num_layers * g.nb;
+    if (items > INT_MAX) return set_error(TDKV_EINVAL, "tdkv_diff_compare: batch too large");
+    if (cudaMemsetAsync(d_violation, 0x7f, sizeof(int32_t) * n_pairs, s) != cudaSuccess)
+        return check_launch("tdkv_diff_compare: memset");
+    const int ub = codec_unit(dtype, g.row_elems);
+    const dim3 grid((unsigned)items);
+    if (dtype == TDKV_F32) {
+        if (ub == 16)
+            diff_compare_kernel<float, 16><<<grid, 256, 0, s>>>(d_pairs, d_hinted, d_changed,
+                                                                d_violation, d_viol_maxabs, g);
+        else
+            diff_compare_kernel<float, 4><<<grid, 256, 0, s>>>(d_pairs, d_hinted, d_changed,
+                                                               d_violation, d_viol_maxabs, g);
+    } else {
+        if (ub == 16)
+            diff_compare_kernel<__nv_bfloat16, 16><<<grid, 256, 0, s>>>(
+                d_pairs, d_hinted, d_changed, d_violation, d_viol_maxabs, g);
+        else
+            diff_compare_kernel<__nv_bfloat16, 4><<<grid, 256, 0, s>>>(
+                d_pairs, d_hinted, d_changed, d_violation, d_viol_maxabs, g);
+    }
+    count_launch();
+    return check_launch("tdkv_diff_compare");
+}
+
+extern "C" int32_t tdkv_diff_compact(const tdkv_diff_pair* d_pairs, const tdkv_diff_out* d_outs,
+                                     int32_t n_pairs, const uint8_t* d_changed, int32_t* d_counts,
+                                     int32_t num_layers, int32_t num_tokens, int32_t num_heads,
+                                     int32_t head_dim, int32_t block_size, int32_t dtype,
+                                     void* stream) {
+    int32_t rc = codec_check("tdkv_diff_compact", n_pairs, num_layers, num_tokens, num_heads,
+                             head_dim, block_size, dtype);
+    if (rc) return rc;
+    if (n_pairs == 0) return TDKV_OK;
+    if (!d_pairs || !d_outs || !d_changed || !d_counts)
+        return set_error(TDKV_EINVAL, "tdkv_diff_compact: null pointer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    CodecGeom g{num_layers, num_tokens, num_heads * head_dim, block_size,
+                ceil_div(num_tokens, block_size)};
+    const int ub = codec_unit(dtype, g.row_elems);
+    const dim3 grid((unsigned)(n_pairs * num_layers));
+    if (dtype == TDKV_F32) {
+        if (ub == 16)
+            diff_compact_kernel<float, 16><<<grid, 256, 0, s>>>(d_pairs, d_outs, d_changed, d_counts, g);
+        else
+            diff_compact_kernel<float, 4><<<grid, 256, 0, s>>>(d_pairs, d_outs, d_changed, d_counts, g);
+    } else {
+        if (ub == 16)
+            diff_compact_kernel<__nv_bfloat16, 16><<<grid, 256, 0, s>>>(d_pairs, d_outs, d_changed,
+                                                                        d_counts, g);
+        else
+            diff_compact_kernel<__nv_bfloat16, 4><<<grid, 256, 0, s>>>(d_pairs, d_outs, d_changed,
+                                                                       d_counts, g);
+    }
+    count_launch();
+    return check_launch("tdkv_diff_compact");
+}

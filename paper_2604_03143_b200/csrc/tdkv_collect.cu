@@ -1,0 +1,310 @@
+// K0 rotary table + K1 KV Collector.
+//
+// K1 replaces pic.align_cached (pic.py:208-235) + the _skeleton V copy
+// (pic.py:203-204) + PagedPool.write_rows (paged_pool.py:150-156): each
+// master tile (one segment, <= max_rows rows, K and V) is staged ONCE in
+// shared memory by the TMA engine (cp.async.bulk, double-buffered across the
+// persistent loop) and then rotated/copied to every agent that holds the
+// segment, straight into that agent's paged-pool slots.  HBM traffic is the
+// algorithmic minimum M + N*M (master read once, N agent copies written).
+#include "tdkv_common.cuh"
+
+namespace tdkv {
+
+// ---------------------------------------------------------------------------
+// K0
+
+template <typename Tbl>
+__global__ void rope_table_kernel(const int64_t* __restrict__ deltas, int64_t n_rows,
+                                  const double* __restrict__ inv_freq, int half,
+                                  Tbl* __restrict__ out) {
+    const int64_t total = n_rows * half;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / half;
+        const int j = (int)(i - r * half);
+        // numpy: pos(float64) * inv_freq(float64), one IEEE multiply
+        const double theta = __dmul_rn((double)deltas[r], inv_freq[j]);
+        double s, c;
+        sincos(theta, &s, &c);
+        if constexpr (sizeof(Tbl) == 16) {
+            out[i] = make_double2(c, s);
+        } else {
+            out[i] = make_float2((float)c, (float)s);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K1
+
+struct CollectParams {
+    const void* mk;
+    const void* mv;
+    int64_t mls;                 // master layer stride (elements)
+    const tdkv_collect_unit* units;
+    int32_t n_units;
+    int32_t max_rows;
+    const tdkv_collect_job* jobs;
+    const int64_t* dst_rows;
+    const void* table;
+    int32_t rotate;
+    void* dk;
+    void* dv;
+    int64_t dls;                 // destination layer stride (elements)
+    int32_t num_layers;
+    int32_t head_dim;
+    int32_t row_elems;
+};
+
+template <typename T, int UB, bool BULK>
+__global__ void __launch_bounds__(256) collect_kernel(const CollectParams p) {
+    using V = typename UnitBits<UB>::V;
+    using Tbl = typename Elt<T>::Table;
+    constexpr int kEpu = UB / (int)sizeof(T);      // elements per unit
+    constexpr int kPairs = kEpu / 2;
+
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ __align__(8) uint64_t bars[2];
+
+    const int tid = threadIdx.x;
+    const int nthr = blockDim.x;
+    const int row_bytes = p.row_elems * (int)sizeof(T);
+    const int tile_bytes = p.max_rows * row_bytes;      // one plane
+    const int upr = row_bytes / UB;                      // units per row
+    const int tx_n = upr < nthr ? upr : nthr;
+    const int rows_per_pass = nthr / tx_n;
+    const int tx = tid % tx_n;
+    const int ty = tid / tx_n;
+    const int n_items = p.n_units * p.num_layers;
+    const Tbl* __restrict__ table = static_cast<const Tbl*>(p.table);
+    const int half = p.head_dim >> 1;
+    const bool has_v = p.dv != nullptr;            // K-only collect (align_cached)
+
+    if constexpr (BULK) {
+        if (tid == 0) {
+            mbar_init(&bars[0], 1);
+            mbar_init(&bars[1], 1);
+            fence_mbar_init();
+        }
+        __syncthreads();
+    }
+
+    // item -> (layer, unit); units vary fastest so consecutive CTAs stream
+    // neighbouring tiles of one layer plane
+    auto stage_src = [&](int item, const T*& gk, const T*& gv, tdkv_collect_unit& u) {
+        const int layer = item / p.n_units;
+        u = p.units[item - layer * p.n_units];
+        const size_t off = (size_t)layer * p.mls + (size_t)u.row0 * p.row_elems;
+        gk = static_cast<const T*>(p.mk) + off;
+        gv = static_cast<const T*>(p.mv) + off;
+    };
+
+    int item = blockIdx.x;
+    if constexpr (BULK) {
+        if (tid == 0 && item < n_items) {
+            const T *gk, *gv;
+            tdkv_collect_unit u;
+            stage_src(item, gk, gv, u);
+            const uint32_t bytes = (uint32_t)u.nrows * row_bytes;
+            mbar_arrive_expect_tx(&bars[0], (has_v ? 2 : 1) * bytes);
+            bulk_g2s(smem, gk, bytes, &bars[0]);
+            if (has_v) bulk_g2s(smem + tile_bytes, gv, bytes, &bars[0]);
+        }
+    }
+
+    for (int iter = 0; item < n_items; item += gridDim.x, ++iter) {
+        const int b = iter & 1;
+        uint8_t* buf = smem + (size_t)b * 2 * tile_bytes;
+        const int layer = item / p.n_units;
+        const tdkv_collect_unit u = p.units[item - layer * p.n_units];
+
+        if constexpr (BULK) {
+            const int next = item + gridDim.x;
+            if (tid == 0 && next < n_items) {
+                // buffer b^1 was drained by every thread before the trailing
+                // __syncthreads of the previous iteration
+                fence_proxy_async_smem();
+                const T *gk, *gv;
+                tdkv_collect_unit un;
+                stage_src(next, gk, gv, un);
+                const uint32_t bytes = (uint32_t)un.nrows * row_bytes;
+                uint8_t* nb = smem + (size_t)(b ^ 1) * 2 * tile_bytes;
+                mbar_arrive_expect_tx(&bars[b ^ 1], (has_v ? 2 : 1) * bytes);
+                bulk_g2s(nb, gk, bytes, &bars[b ^ 1]);
+                if (has_v) bulk_g2s(nb + tile_bytes, gv, bytes, &bars[b ^ 1]);
+            }
+            mbar_wait(&bars[b], (uint32_t)((iter >> 1) & 1));
+        } else {
+            const T *gk, *gv;
+            tdkv_collect_unit un;
+            stage_src(item, gk, gv, un);
+            const int words = u.nrows * row_bytes / 4;
+            const uint32_t* sk32 = reinterpret_cast<const uint32_t*>(gk);
+            const uint32_t* sv32 = reinterpret_cast<const uint32_t*>(gv);
+            uint32_t* dk32 = reinterpret_cast<uint32_t*>(buf);
+            uint32_t* dv32 = reinterpret_cast<uint32_t*>(buf + tile_bytes);
+            for (int w = tid; w < words; w += nthr) {
+                dk32[w] = sk32[w];
+                if (has_v) dv32[w] = sv32[w];
+            }
+            __syncthreads();
+        }
+
+        const V* sk = reinterpret_cast<const V*>(buf);
+        const V* sv = reinterpret_cast<const V*>(buf + tile_bytes);
+        T* dk_l = static_cast<T*>(p.dk) + (size_t)layer * p.dls;
+        T* dv_l = static_cast<T*>(p.dv) + (size_t)layer * p.dls;
+
+        if (ty < rows_per_pass) {
+            for (int j = u.job_begin; j < u.job_end; ++j) {
+                const tdkv_collect_job job = p.jobs[j];
+                const int i0 = u.row0 - job.seg_row0;
+                const int64_t* __restrict__ drows = p.dst_rows + job.dst_off + i0;
+                for (int c = tx; c < upr; c += tx_n) {
+                    const int j0 = ((c * kEpu) % p.head_dim) >> 1;
+                    Tbl cs[kPairs];
+                    if (p.rotate && job.tbl_stride == 0) {
+                        const Tbl* trow = table + (size_t)job.tbl_row * half + j0;
+#pragma unroll
+                        for (int q = 0; q < kPairs; ++q) cs[q] = trow[q];
+                    }
+                    for (int r = ty; r < u.nrows; r += rows_per_pass) {
+                        const int64_t drow = __ldg(drows + r);
+                        V kv = sk[r * upr + c];
+                        if (p.rotate) {
+                            if (job.tbl_stride != 0) {
+                                const Tbl* trow =
+                                    table + (size_t)(job.tbl_row + (i0 + r) * job.tbl_stride) * half + j0;
+#pragma unroll
+                                for (int q = 0; q < kPairs; ++q) cs[q] = trow[q];
+                            }
+                            T* e = reinterpret_cast<T*>(&kv);
+#pragma unroll
+                            for (int q = 0; q < kPairs; ++q) rot_pair(e[2 * q], e[2 * q + 1], cs[q]);
+                        }
+                        st_stream(reinterpret_cast<V*>(dk_l + (size_t)drow * p.row_elems) + c, kv);
+                        if (has_v)
+                            st_stream(reinterpret_cast<V*>(dv_l + (size_t)drow * p.row_elems) + c,
+                                      sv[r * upr + c]);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+template <typename T, int UB, bool BULK>
+static int32_t launch_collect(const CollectParams& p, int grid_limit, cudaStream_t s) {
+    auto kern = collect_kernel<T, UB, BULK>;
+    const int threads = 256;
+    const size_t smem = (size_t)4 * p.max_rows * p.row_elems * sizeof(T);
+    if (smem > 227 * 1024)
+        return set_error(TDKV_EINVAL, "tdkv_collect: tile of %d rows needs %zu B of shared memory",
+                         p.max_rows, smem);
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return check_launch("tdkv_collect: cudaFuncSetAttribute");
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+    if (per_sm < 1) per_sm = 1;
+    const int items = p.n_units * p.num_layers;
+    int grid = sm_count() * per_sm;
+    if (grid_limit > 0 && grid > grid_limit) grid = grid_limit;
+    if (grid > items) grid = items;
+    kern<<<grid, threads, smem, s>>>(p);
+    count_launch();
+    return check_launch("tdkv_collect");
+}
+
+}  // namespace tdkv
+
+using namespace tdkv;
+
+extern "C" int32_t tdkv_rope_table(const int64_t* d_deltas, int64_t n_rows,
+                                   const double* d_inv_freq, int32_t half_dim,
+                                   int32_t table_dtype, void* d_table, void* stream) {
+    if (n_rows < 0 || half_dim <= 0) return set_error(TDKV_EINVAL, "tdkv_rope_table: bad sizes");
+    if (n_rows == 0) return TDKV_OK;
+    if (!d_deltas || !d_inv_freq || !d_table)
+        return set_error(TDKV_EINVAL, "tdkv_rope_table: null pointer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t total = n_rows * half_dim;
+    int grid = (int)((total + 255) / 256);
+    if (grid > sm_count() * 8) grid = sm_count() * 8;
+    if (table_dtype == TDKV_F32) {
+        rope_table_kernel<double2><<<grid, 256, 0, s>>>(d_deltas, n_rows, d_inv_freq, half_dim,
+                                                        static_cast<double2*>(d_table));
+    } else if (table_dtype == TDKV_BF16) {
+        rope_table_kernel<float2><<<grid, 256, 0, s>>>(d_deltas, n_rows, d_inv_freq, half_dim,
+                                                       static_cast<float2*>(d_table));
+    } else {
+        return set_error(TDKV_EUNSUPPORTED, "tdkv_rope_table: dtype %d", table_dtype);
+    }
+    count_launch();
+    return check_launch("tdkv_rope_table");
+}
+
+extern "C" int32_t tdkv_collect(const void* d_master_k, const void* d_master_v,
+                                int64_t master_layer_stride, const tdkv_collect_unit* d_units,
+                                int32_t n_units, int32_t max_rows, const tdkv_collect_job* d_jobs,
+                                const int64_t* d_dst_rows, const void* d_table, int32_t rotate,
+                                void* d_dst_k, void* d_dst_v, int64_t dst_layer_stride,
+                                int32_t num_layers, int32_t num_heads, int32_t head_dim,
+                                int32_t dtype, int32_t grid_limit, void* stream) {
+    if (n_units < 0 || num_layers <= 0 || num_heads <= 0 || head_dim <= 0 || (head_dim & 1))
+        return set_error(TDKV_EINVAL, "tdkv_collect: bad geometry L=%d H=%d D=%d", num_layers,
+                         num_heads, head_dim);
+    if (n_units == 0) return TDKV_OK;
+    if (max_rows <= 0) return set_error(TDKV_EINVAL, "tdkv_collect: max_rows must be positive");
+    if (!d_master_k || !d_units || !d_jobs || !d_dst_rows || !d_dst_k || (rotate && !d_table) ||
+        ((d_dst_v == nullptr) != (d_master_v == nullptr)))
+        return set_error(TDKV_EINVAL, "tdkv_collect: null pointer");
+    if (dtype != TDKV_F32 && dtype != TDKV_BF16)
+        return set_error(TDKV_EUNSUPPORTED, "tdkv_collect: dtype %d", dtype);
+
+    CollectParams p;
+    p.mk = d_master_k;
+    p.mv = d_master_v;
+    p.mls = master_layer_stride;
+    p.units = d_units;
+    p.n_units = n_units;
+    p.max_rows = max_rows;
+    p.jobs = d_jobs;
+    p.dst_rows = d_dst_rows;
+    p.table = d_table;
+    p.rotate = rotate;
+    p.dk = d_dst_k;
+    p.dv = d_dst_v;
+    p.dls = dst_layer_stride;
+    p.num_layers = num_layers;
+    p.head_dim = head_dim;
+    p.row_elems = num_heads * head_dim;
+
+    const size_t esz = elt_size(dtype);
+    const size_t row_bytes = (size_t)p.row_elems * esz;
+    int ub = pick_unit_bytes(dtype, head_dim, p.row_elems);
+    if (ub == 16 && !(aligned(d_dst_k, 16) && aligned(d_dst_v, 16) && aligned(d_master_k, 16) &&
+                      aligned(d_master_v, 16) &&
+                      (dst_layer_stride * esz) % 16 == 0))
+        ub = (int)(2 * esz);
+    const bool bulk = row_bytes % 16 == 0 && aligned(d_master_k, 16) && aligned(d_master_v, 16) &&
+                      (master_layer_stride * esz) % 16 == 0;
+    if (!aligned(d_master_k, 4) || !aligned(d_master_v, 4))
+        return set_error(TDKV_EINVAL, "tdkv_collect: master planes must be 4-byte aligned");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+
+    if (dtype == TDKV_F32) {
+        if (ub == 16)
+            return bulk ? launch_collect<float, 16, true>(p, grid_limit, s)
+                        : launch_collect<float, 16, false>(p, grid_limit, s);
+        return bulk ? launch_collect<float, 8, true>(p, grid_limit, s)
+                    : launch_collect<float, 8, false>(p, grid_limit, s);
+    }
+    if (ub == 16)
+        return bulk ? launch_collect<__nv_bfloat16, 16, true>(p, grid_limit, s)
+                    : launch_collect<__nv_bfloat16, 16, false>(p, grid_limit, s);
+    return bulk ? launch_collect<__nv_bfloat16, 4, true>(p, grid_limit, s)
+                : launch_collect<__nv_bfloat16, 4, false>(p, grid_limit, s);
+}

@@ -1,0 +1,532 @@
+"""Diff-aware storage: block-sparse diffs, wire format, families
+(reference: roundkv/diffstore.py).
+
+Encoding (``encode_diff`` / ``encode_batch`` / ``DiffStore.encode_family``)
+runs kernel K2 on the device: one compare pass over every (mirror, layer,
+block) with float '!=' semantics (diffstore.py:151-153) and one compaction
+pass that writes each layer's changed blocks in ascending order, zero-padded,
+into a payload slab (diffstore.py:166-173).  A whole family is encoded in
+two launches and one device->host read of the counts and indices.
+
+Decoding is fused into restores (restore.py); ``diff_decode_dense`` is the
+dense baseline (diffstore.py:185-203), one K3 launch.
+
+The wire format (diffstore.py:10-23, 210-306) is produced/parsed on the host
+and is byte-identical to the reference's (version 1, float32 payload).
+"""
+from __future__ import annotations
+
+import struct
+import threading
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _kernels, _lib
+from ._device import (default_device, dtype_code, is_host, ptr, stream_handle, to_device,
+                      to_host, upload)
+from .core import CacheBlockConfig, LayeredKv
+
+MAGIC = b"TDDF"
+VERSION = 1
+_HEADER = struct.Struct("<4sHHIIII")
+
+
+class MalformedDiffError(ValueError):
+    """A serialized diff is truncated or inconsistent."""
+
+
+class HintSoundnessError(RuntimeError):
+    """Master and mirror differ outside the hinted positions."""
+
+
+class PinnedMasterError(RuntimeError):
+    """A family whose master has live mirrors was dropped."""
+
+
+def _nbytes(x) -> int:
+    if isinstance(x, torch.Tensor):
+        return x.numel() * x.element_size()
+    return int(x.nbytes)
+
+
+def _payload_ok(x, want) -> bool:
+    if tuple(x.shape) != want:
+        return False
+    if isinstance(x, np.ndarray):
+        return x.dtype == np.float32
+    return isinstance(x, torch.Tensor) and x.dtype in (torch.float32, torch.bfloat16)
+
+
+@dataclass(eq=False)
+class LayerDiff:
+    """Changed blocks of one layer; ``v_indices`` None = K and V share
+    ``indices`` (the only form the encoder emits)."""
+
+    indices: np.ndarray
+    k_blocks: object
+    v_blocks: object
+    v_indices: Optional[np.ndarray] = None
+
+    def __post_init__(self) -> None:
+        self.indices = np.asarray(self.indices, dtype=np.int64)
+        if self.v_indices is not None:
+            self.v_indices = np.asarray(self.v_indices, dtype=np.int64)
+
+    @property
+    def payload_nbytes(self) -> int:
+        return _nbytes(self.k_blocks) + _nbytes(self.v_blocks)
+
+
+@dataclass
+class _DeviceDiff:
+    """Device form used by the fused decoder: payload slabs + block maps."""
+
+    pay_k: torch.Tensor
+    pay_v: torch.Tensor
+    map_k: torch.Tensor          # (L * nb) int32, -1 = take the master block
+    map_v: torch.Tensor
+
+
+@dataclass(eq=False)
+class BlockSparseDiff:
+    """Per-layer changed blocks of a mirror relative to its master."""
+
+    num_layers: int
+    block_size: int
+    num_heads: int
+    head_dim: int
+    total_tokens: int
+    layers: List[LayerDiff]
+    _dev: Optional[_DeviceDiff] = field(default=None, repr=False)
+
+    def __post_init__(self) -> None:
+        if len(self.layers) != self.num_layers:
+            raise ValueError("one LayerDiff per layer required")
+        nb = CacheBlockConfig(self.block_size).num_blocks(self.total_tokens)
+        for ld in self.layers:
+            for idx, payload in ((ld.indices, ld.k_blocks), (ld.v_indices, ld.v_blocks)):
+                idx = ld.indices if idx is None else idx
+                if idx.size and (idx.min() < 0 or idx.max() >= nb):
+                    raise ValueError("block index out of range")
+                if idx.size > 1 and not (np.diff(idx) > 0).all():
+                    raise ValueError("block indices must be strictly increasing")
+                want = (idx.size, self.block_size, self.num_heads, self.head_dim)
+                if not _payload_ok(payload, want):
+                    raise ValueError("payload must be float32 with one block per index")
+
+    @property
+    def payload_nbytes(self) -> int:
+        return sum(ld.payload_nbytes for ld in self.layers)
+
+    @property
+    def changed_blocks_per_layer(self) -> List[int]:
+        return [int(ld.indices.size) for ld in self.layers]
+
+    def device_form(self, device: torch.device, dtype: torch.dtype) -> _DeviceDiff:
+        """Payload slabs + block maps on the device (uploaded once for host diffs)."""
+        d = self._dev
+        if d is not None and d.pay_k.device == device and d.pay_k.dtype == dtype:
+            return d
+        nb = CacheBlockConfig(self.block_size).num_blocks(self.total_tokens)
+        maps = []
+        slabs = []
+        for plane in ("k", "v"):
+            blocks, mp = [], np.full((self.num_layers, nb), -1, np.int32)
+            off = 0
+            for layer, ld in enumerate(self.layers):
+                idx = ld.indices if (plane == "k" or ld.v_indices is None) else ld.v_indices
+                payload = ld.k_blocks if plane == "k" else ld.v_blocks
+                if idx.size:
+                    mp[layer, idx] = np.arange(off, off + idx.size, dtype=np.int32)
+                    blocks.append(to_device(payload, device, dtype))
+                off += idx.size
+            shape = (max(off, 1), self.block_size, self.num_heads, self.head_dim)
+            slab = torch.cat(blocks) if blocks else torch.zeros(shape, dtype=dtype, device=device)
+            slabs.append(slab)
+            maps.append(torch.from_numpy(mp.reshape(-1)).to(device))
+        d = _DeviceDiff(slabs[0], slabs[1], maps[0], maps[1])
+        self._dev = d
+        return d
+
+
+# ---------------------------------------------------------------------------
+# encoder (K2)
+
+
+def _check_pair(master: LayeredKv, mirror: LayeredKv) -> None:
+    if tuple(master.k.shape) != tuple(mirror.k.shape):
+        raise ValueError("master and mirror must have identical plane shapes")
+    if not np.array_equal(master.positions, mirror.positions):
+        raise ValueError("master and mirror must cover the same positions")
+
+
+def _plane_dtype(kv: LayeredKv) -> torch.dtype:
+    return kv.k.dtype if isinstance(kv.k, torch.Tensor) else torch.float32
+
+
+def encode_batch(master: LayeredKv, mirrors: Sequence[LayeredKv],
+                 hint_positions: Sequence[np.ndarray], blocks: CacheBlockConfig,
+                 device: Optional[torch.device] = None) -> List[BlockSparseDiff]:
+    """Encode many mirrors against one master in two kernel launches.
+
+    Raises HintSoundnessError for the first mirror (in list order) that
+    differs outside its hints, at that mirror's first (layer, block) in
+    layer-major order -- the block encode_diff would raise on.
+    """
+    if len(mirrors) != len(hint_positions):
+        raise ValueError("one hint array per mirror")
+    if not mirrors:
+        return []
+    total = master.num_tokens
+    nb = blocks.num_blocks(total)
+    bs = blocks.block_size
+    L, H, D = master.num_layers, master.num_heads, master.head_dim
+    hinted = np.zeros((len(mirrors), nb), np.uint8)
+    for p, (mir, hints) in enumerate(zip(mirrors, hint_positions)):
+        _check_pair(master, mir)
+        h = np.asarray(hints, dtype=np.int64)
+        if h.size and (h.min() < 0 or h.max() >= total):
+            raise ValueError("hint positions out of range")
+        hinted[p, h // bs] = 1
+    device = device or (master.k.device if master.on_device else default_device())
+    dtype = _plane_dtype(master)
+    mk = to_device(master.k, device, dtype)
+    mv = to_device(master.v, device, dtype)
+    mirrors_dev = [(to_device(m.k, device, dtype), to_device(m.v, device, dtype)) for m in mirrors]
+    P = len(mirrors)
+    pairs = np.array([(ptr(mk), ptr(mv), ptr(a), ptr(b)) for a, b in mirrors_dev],
+                     dtype=_lib.DIFF_PAIR)
+    d_pairs = upload(pairs, device)
+    d_hinted = torch.from_numpy(hinted.reshape(-1)).to(device)
+    changed = torch.empty(P * L * nb, dtype=torch.uint8, device=device)
+    violation = torch.empty(P, dtype=torch.int32, device=device)
+    viol_maxabs = torch.zeros(P * L * nb, dtype=torch.float32, device=device)
+    code = dtype_code(dtype)
+    stream = stream_handle(device)
+    _lib.call("tdkv_diff_compare", ptr(d_pairs), P, ptr(d_hinted), ptr(changed), ptr(violation),
+              ptr(viol_maxabs), L, total, H, D, bs, code, stream)
+
+    caps = np.maximum(hinted.sum(axis=1).astype(np.int64), 1)
+    slab_blocks = int((caps * L).sum())
+    pay_k = torch.empty((slab_blocks, bs, H, D), dtype=dtype, device=device)
+    pay_v = torch.empty_like(pay_k)
+    indices = torch.empty(slab_blocks, dtype=torch.int32, device=device)
+    blkmap = torch.empty(P * L * nb, dtype=torch.int32, device=device)
+    counts = torch.empty(P * L, dtype=torch.int32, device=device)
+    starts = np.concatenate([[0], np.cumsum(caps * L)[:-1]])
+    esz = pay_k.element_size()
+    blk_bytes = bs * H * D * esz
+    outs = np.array([(ptr(pay_k) + int(s) * blk_bytes, ptr(pay_v) + int(s) * blk_bytes,
+                      ptr(indices) + int(s) * 4, ptr(blkmap) + p * L * nb * 4, int(c), 0)
+                     for p, (s, c) in enumerate(zip(starts, caps))], dtype=_lib.DIFF_OUT)
+    d_outs = upload(outs, device)
+    _lib.call("tdkv_diff_compact", ptr(d_pairs), ptr(d_outs), P, ptr(changed), ptr(counts),
+              L, total, H, D, bs, code, stream)
+
+    viol_h = violation.cpu().numpy()
+    bad = np.flatnonzero(viol_h != _lib.NO_VIOLATION)
+    if bad.size:
+        p = int(bad[0])
+        v = int(viol_h[p])
+        layer, b = divmod(v, nb)
+        worst = float(viol_maxabs[(p * L + layer) * nb + b].item())
+        raise HintSoundnessError(
+            f"layer {layer} block {b} differs outside the hinted positions (max abs {worst:.3e})")
+    counts_h = counts.cpu().numpy().reshape(P, L)
+    idx_h = indices.cpu().numpy()
+    diffs = []
+    for p in range(P):
+        s, cap = int(starts[p]), int(caps[p])
+        layers = []
+        for layer in range(L):
+            n = int(counts_h[p, layer])
+            base = s + layer * cap
+            layers.append(LayerDiff(idx_h[base:base + n].astype(np.int64),
+                                    pay_k[base:base + n], pay_v[base:base + n]))
+        diff = BlockSparseDiff(L, bs, H, D, total, layers)
+        slab_k = pay_k[s:s + L * cap]
+        slab_v = pay_v[s:s + L * cap]
+        mp = blkmap[p * L * nb:(p + 1) * L * nb]
+        diff._dev = _DeviceDiff(slab_k, slab_v, mp, mp)
+        diffs.append(diff)
+    return diffs
+
+
+def encode_diff(master: LayeredKv, mirror: LayeredKv, hint_positions: np.ndarray,
+                blocks: CacheBlockConfig) -> BlockSparseDiff:
+    """Block-sparse difference of mirror against master (diffstore.py:119-182).
+
+    Host (numpy) inputs produce a diff with host numpy payloads; device
+    inputs keep the payload on the device."""
+    diff = encode_batch(master, [mirror], [hint_positions], blocks)[0]
+    if not master.on_device:
+        for ld in diff.layers:
+            ld.k_blocks = to_host(ld.k_blocks)
+            ld.v_blocks = to_host(ld.v_blocks)
+    return diff
+
+
+# ---------------------------------------------------------------------------
+# dense decode (K3 with identity rows, no rotation)
+
+
+def diff_decode_dense(master: LayeredKv, diff: BlockSparseDiff) -> LayeredKv:
+    """Materialize the mirror's full planes: master + changed blocks."""
+    if (master.num_layers != diff.num_layers or master.num_tokens != diff.total_tokens
+            or tuple(master.k.shape[2:]) != (diff.num_heads, diff.head_dim)):
+        raise ValueError("diff does not describe this master")
+    device = master.k.device if master.on_device else default_device()
+    dtype = _plane_dtype(master)
+    mk = to_device(master.k, device, dtype)
+    mv = to_device(master.v, device, dtype)
+    out_k = torch.empty_like(mk)
+    out_v = torch.empty_like(mv)
+    decode_dense_into(mk, mv, diff, out_k, out_v)
+    if master.on_device:
+        return LayeredKv(out_k, out_v, master.positions.copy())
+    return LayeredKv(to_host(out_k), to_host(out_v), master.positions.copy())
+
+
+def decode_dense_into(mk: torch.Tensor, mv: torch.Tensor, diff: BlockSparseDiff,
+                      out_k: torch.Tensor, out_v: torch.Tensor) -> None:
+    L, T, H, D = mk.shape
+    dd = diff.device_form(mk.device, mk.dtype)
+    job = _kernels.rows_job(mk, mv, T * H * D, out_k, out_v, T * H * D, T, pay_k=dd.pay_k,
+                            pay_v=dd.pay_v, map_k=dd.map_k, map_v=dd.map_v)
+    _kernels.rows(_kernels.rows_jobs([job]), T, None, L, H, D, diff.block_size, mk.dtype,
+                  mk.device)
+
+
+# ---------------------------------------------------------------------------
+# wire format (host)
+
+
+def wire_nbytes(diff: BlockSparseDiff, itemsize: int = 4) -> int:
+    """Serialized size without building the bytes: header, per layer
+    count+flag+indices(+escape fields)+payload, trailer.  itemsize=4 is the
+    reference's float32 wire (equal to len(serialize_diff(diff)))."""
+    blk = diff.block_size * diff.num_heads * diff.head_dim * itemsize
+    n = _HEADER.size + 4
+    for ld in diff.layers:
+        kc = int(ld.indices.size)
+        vc = kc if ld.v_indices is None else int(ld.v_indices.size)
+        n += 5 + 4 * kc + kc * blk + vc * blk
+        if ld.v_indices is not None:
+            n += 4 + 4 * vc
+    return n
+
+
+def _f32_bytes(x) -> bytes:
+    if isinstance(x, torch.Tensor):
+        x = to_host(x)
+    return np.ascontiguousarray(x, dtype="<f4").tobytes()
+
+
+def serialize_diff(diff: BlockSparseDiff) -> bytes:
+    parts = [_HEADER.pack(MAGIC, VERSION, diff.num_layers, diff.block_size, diff.num_heads,
+                          diff.head_dim, diff.total_tokens)]
+    for ld in diff.layers:
+        shared = ld.v_indices is None
+        parts.append(struct.pack("<IB", ld.indices.size, 1 if shared else 0))
+        parts.append(ld.indices.astype("<u4").tobytes())
+        parts.append(_f32_bytes(ld.k_blocks))
+        if not shared:
+            parts.append(struct.pack("<I", ld.v_indices.size))
+            parts.append(ld.v_indices.astype("<u4").tobytes())
+        parts.append(_f32_bytes(ld.v_blocks))
+    parts.append(struct.pack("<I", CacheBlockConfig(diff.block_size).valid_len(diff.total_tokens)))
+    return b"".join(parts)
+
+
+class _Cursor:
+    def __init__(self, buf: bytes) -> None:
+        self.buf = buf
+        self.pos = 0
+
+    def take(self, n: int, what: str) -> bytes:
+        if self.pos + n > len(self.buf):
+            raise MalformedDiffError(f"truncated diff: expected {what}")
+        out = self.buf[self.pos:self.pos + n]
+        self.pos += n
+        return out
+
+    def u32(self, what: str) -> int:
+        return struct.unpack("<I", self.take(4, what))[0]
+
+    def ids(self, count: int, what: str) -> np.ndarray:
+        a = np.frombuffer(self.take(4 * count, what), dtype="<u4").astype(np.int64)
+        if a.size > 1 and not (np.diff(a) > 0).all():
+            raise MalformedDiffError(f"{what} must be strictly increasing")
+        return a
+
+    def blocks(self, count: int, shape: tuple, what: str) -> np.ndarray:
+        n = count * int(np.prod(shape)) * 4
+        return np.frombuffer(self.take(n, what), dtype="<f4").astype(np.float32).reshape(
+            (count,) + shape)
+
+
+def deserialize_diff(buf: bytes) -> BlockSparseDiff:
+    cur = _Cursor(buf)
+    magic, version, num_layers, bs, heads, dim, total = _HEADER.unpack(
+        cur.take(_HEADER.size, "header"))
+    if magic != MAGIC:
+        raise MalformedDiffError("bad magic")
+    if version != VERSION:
+        raise MalformedDiffError(f"unsupported version {version}")
+    if min(num_layers, bs, heads, dim, total) <= 0:
+        raise MalformedDiffError("non-positive geometry field")
+    shape = (bs, heads, dim)
+    layers = []
+    for layer in range(num_layers):
+        count = cur.u32(f"layer {layer} count")
+        flag = cur.take(1, f"layer {layer} index flag")[0]
+        if flag not in (0, 1):
+            raise MalformedDiffError(f"layer {layer}: unknown index flag {flag}")
+        idx = cur.ids(count, f"layer {layer} indices")
+        kb = cur.blocks(count, shape, f"layer {layer} K payload")
+        if flag == 1:
+            layers.append(LayerDiff(idx, kb, cur.blocks(count, shape, f"layer {layer} V payload")))
+        else:
+            vc = cur.u32(f"layer {layer} V count")
+            vidx = cur.ids(vc, f"layer {layer} V indices")
+            layers.append(LayerDiff(idx, kb, cur.blocks(vc, shape, f"layer {layer} V payload"),
+                                    v_indices=vidx))
+    valid = cur.u32("valid_len trailer")
+    if cur.pos != len(buf):
+        raise MalformedDiffError("trailing bytes after diff")
+    diff = BlockSparseDiff(num_layers, bs, heads, dim, total, layers)
+    if valid != CacheBlockConfig(bs).valid_len(total):
+        raise MalformedDiffError("valid_len disagrees with token count")
+    return diff
+
+
+# ---------------------------------------------------------------------------
+# families (diffstore.py:313-457)
+
+
+@dataclass(eq=False)
+class MasterEntry:
+    family_id: int
+    kv: LayeredKv
+    tokens: Optional[tuple] = None
+    pin_count: int = 0
+
+
+@dataclass(eq=False)
+class MirrorHandle:
+    """Master reference + block-sparse diff; pins the master while live."""
+
+    family_id: int
+    request_id: int
+    master: MasterEntry
+    diff: BlockSparseDiff
+    released: bool = field(default=False, init=False)
+
+    @property
+    def positions(self) -> np.ndarray:
+        return self.master.kv.positions
+
+    def release(self) -> None:
+        if self.released:
+            raise ValueError("mirror handle already released")
+        self.released = True
+        self.master.pin_count -= 1
+
+
+@dataclass(eq=False)
+class CompressionStats:
+    dense_nbytes: int
+    diff_payload_nbytes: List[int]
+    diff_serialized_nbytes: List[int]
+    changed_blocks: List[int]
+
+    @property
+    def ratios(self) -> List[float]:
+        return [self.dense_nbytes / b for b in self.diff_serialized_nbytes]
+
+    @property
+    def family_cost(self) -> float:
+        return 1.0 + sum(b / self.dense_nbytes for b in self.diff_serialized_nbytes)
+
+
+def family_cost_from_ratio(num_members: int, ratio: float) -> float:
+    if num_members < 1:
+        raise ValueError("a family has at least one member")
+    if ratio <= 0:
+        raise ValueError("compression ratio must be positive")
+    return 1.0 + (num_members - 1) / ratio
+
+
+@dataclass(eq=False)
+class FamilyEncoding:
+    master: MasterEntry
+    mirrors: Dict[int, MirrorHandle]
+    stats: CompressionStats
+
+
+class DiffStore:
+    """Registry of cache families: dense masters and diff-encoded mirrors."""
+
+    def __init__(self, blocks: CacheBlockConfig) -> None:
+        self.blocks = blocks
+        self._families: Dict[int, FamilyEncoding] = {}
+        self._next_id = 0
+        self._lock = threading.Lock()
+
+    def __len__(self) -> int:
+        return len(self._families)
+
+    def register_dense(self, kv: LayeredKv, tokens: Optional[Sequence[int]] = None) -> MasterEntry:
+        with self._lock:
+            fid = self._next_id
+            self._next_id += 1
+            master = MasterEntry(fid, kv.copy(),
+                                 None if tokens is None else tuple(int(t) for t in tokens))
+            self._families[fid] = FamilyEncoding(master, {},
+                                                 CompressionStats(kv.dense_nbytes, [], [], []))
+            return master
+
+    def encode_family(self, plan, results, tokens: Optional[Sequence[int]] = None) -> FamilyEncoding:
+        """Master stays dense; every other member becomes a diff against it.
+        All mirrors are encoded in one batched K2 pass (ascending rid order)."""
+        master_kv = results[plan.master_id].kv
+        items = sorted(plan.mirror_diff_hints.items())
+        mirrors_kv = [results[rid].kv for rid, _ in items]
+        diffs = encode_batch(master_kv, mirrors_kv, [h for _, h in items], self.blocks)
+        if not master_kv.on_device:
+            for diff in diffs:
+                for ld in diff.layers:
+                    ld.k_blocks = to_host(ld.k_blocks)
+                    ld.v_blocks = to_host(ld.v_blocks)
+        master = self.register_dense(master_kv, tokens)
+        itemsize = 4 if _plane_dtype(master_kv) == torch.float32 else 2
+        mirrors, payload, wire, changed = {}, [], [], []
+        for (rid, _), diff in zip(items, diffs):
+            mirrors[rid] = MirrorHandle(master.family_id, rid, master, diff)
+            master.pin_count += 1
+            payload.append(diff.payload_nbytes)
+            wire.append(wire_nbytes(diff, itemsize))
+            changed.append(sum(diff.changed_blocks_per_layer))
+        enc = FamilyEncoding(master, mirrors,
+                             CompressionStats(master_kv.dense_nbytes, payload, wire, changed))
+        with self._lock:
+            self._families[master.family_id] = enc
+        return enc
+
+    def family(self, family_id: int) -> FamilyEncoding:
+        with self._lock:
+            return self._families[family_id]
+
+    def drop_family(self, family_id: int) -> None:
+        with self._lock:
+            enc = self._families[family_id]
+            if enc.master.pin_count > 0:
+                raise PinnedMasterError(
+                    f"family {family_id} has {enc.master.pin_count} live mirrors")
+            del self._families[family_id]
+
+    def is_pinned(self, ref: object) -> bool:
+        return isinstance(ref, MasterEntry) and ref.pin_count > 0

@@ -1,0 +1,142 @@
+"""Restoring mirror caches into the paged pool (reference: roundkv/restore.py).
+
+``fused_restore`` is Algorithm 1 of the paper as one K3 launch over every
+(layer, block): the source block is the diff payload when the block changed
+and the master's rows otherwise (the overlay precedes rotation,
+restore.py:5-8), K is re-encoded from span.old to span.new, and K and V go
+straight to the pool slots.  No staging planes and no dense mirror exist on
+the device.  The ledger receives the reference's accounting
+(restore.py:70-104) so the byte laws of the reference tests still hold.
+
+``dense_restore`` is the baseline (restore.py:107-139): materialize the
+mirror (K3, identity rows), then rotate + scatter it (K3).
+
+``fused_restore_many`` restores a batch of mirrors in one K0 + one K3
+launch (the round-level form used by the benchmark).
+"""
+from __future__ import annotations
+
+from typing import List, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _kernels
+from ._device import to_device
+from .core import CacheBlockConfig, PositionSpan
+from .diffstore import MirrorHandle, decode_dense_into
+from .ledger import CostLedger
+from .paged_pool import PagedPool, SlotMap
+
+_EVENTS = ("load", "swap", "diff", "rope", "write")
+
+
+def _check_restore_args(mirror: MirrorHandle, span: PositionSpan, slot_map: SlotMap) -> None:
+    if mirror.released:
+        raise ValueError("cannot restore from a released mirror handle")
+    master = mirror.master.kv
+    if not np.array_equal(span.old_positions, master.positions):
+        raise ValueError("span must start at the mirror's source positions")
+    if len(slot_map) != master.num_tokens:
+        raise ValueError("slot map must cover one slot per token")
+
+
+def _delta_rows(delta: np.ndarray):
+    """cos/sin rows for a span: one row if the delta is constant, else one per
+    token.  Returns (deltas, stride, rotate)."""
+    if delta.size == 0 or not delta.any():
+        return np.zeros(1, np.int64), 0, 0
+    if (delta == delta[0]).all():
+        return delta[:1].copy(), 0, 1
+    return delta.copy(), 1, 1
+
+
+def _master_planes(mirror: MirrorHandle, pool: PagedPool):
+    kv = mirror.master.kv
+    # device masters are used in place; host masters are uploaded per call
+    return to_device(kv.k, pool.device, pool.dtype), to_device(kv.v, pool.device, pool.dtype)
+
+
+def fused_restore_many(mirrors: Sequence[MirrorHandle], spans: Sequence[PositionSpan],
+                       pool: PagedPool, slot_maps: Sequence[SlotMap], rope_base: float,
+                       ledger: Optional[CostLedger] = None, grid_limit: int = 0) -> int:
+    """Restore every mirror with one table launch and one K3 launch."""
+    if not mirrors:
+        return 0
+    recs, deltas, tbl_row = [], [], 0
+    max_t, L, H, D = 0, pool.num_layers, pool.num_heads, pool.head_dim
+    bs = mirrors[0].diff.block_size
+    for mirror, span, smap in zip(mirrors, spans, slot_maps):
+        _check_restore_args(mirror, span, smap)
+        if mirror.diff.block_size != bs:
+            raise ValueError("batched restores must share a block size")
+        kv = mirror.master.kv
+        T = kv.num_tokens
+        mk, mv = _master_planes(mirror, pool)
+        dd = mirror.diff.device_form(pool.device, pool.dtype)
+        rows, stride, rotate = _delta_rows(span.delta)
+        recs.append(_kernels.rows_job(mk, mv, T * H * D, pool.k, pool.v, pool.layer_stride, T,
+                                      dst_rows=smap.device_slots(pool.device), pay_k=dd.pay_k,
+                                      pay_v=dd.pay_v, map_k=dd.map_k, map_v=dd.map_v,
+                                      tbl_row=tbl_row, tbl_stride=stride, rotate=rotate))
+        deltas.append(rows)
+        tbl_row += rows.size
+        max_t = max(max_t, T)
+    table = _kernels.rope_table(np.concatenate(deltas), D, rope_base, pool.dtype, pool.device)
+    _kernels.rows(_kernels.rows_jobs(recs), max_t, table, L, H, D, bs, pool.dtype, pool.device,
+                  grid_limit)
+    for mirror, smap in zip(mirrors, slot_maps):
+        pool.mark_written(smap)
+        if ledger is not None:
+            _fused_ledger(mirror, ledger)
+    return 2
+
+
+def _fused_ledger(mirror: MirrorHandle, ledger: CostLedger) -> None:
+    kv = mirror.master.kv
+    layer_pair = 2 * kv.dense_nbytes // (2 * kv.num_layers)   # one layer's K+V planes
+    ledger.record_temp_buffer(2 * layer_pair)
+    for layer in range(kv.num_layers):
+        ledger.record_moved(layer_pair + mirror.diff.layers[layer].payload_nbytes)
+
+
+def fused_restore(mirror: MirrorHandle, span: PositionSpan, pool: PagedPool, slot_map: SlotMap,
+                  rope_base: float, ledger: Optional[CostLedger] = None,
+                  trace: Optional[list] = None) -> None:
+    """Load, patch, re-encode and write each layer without a dense mirror."""
+    _check_restore_args(mirror, span, slot_map)
+    fused_restore_many([mirror], [span], pool, [slot_map], rope_base, ledger)
+    if trace is not None:
+        for layer in range(mirror.master.kv.num_layers):
+            trace.extend((event, layer) for event in _EVENTS)
+
+
+def dense_restore(mirror: MirrorHandle, span: PositionSpan, pool: PagedPool, slot_map: SlotMap,
+                  rope_base: float, ledger: Optional[CostLedger] = None,
+                  trace: Optional[list] = None) -> None:
+    """Baseline: materialize the dense mirror, then rotate and write it."""
+    _check_restore_args(mirror, span, slot_map)
+    kv = mirror.master.kv
+    diff = mirror.diff
+    mk, mv = _master_planes(mirror, pool)
+    dense_k = torch.empty_like(mk)
+    dense_v = torch.empty_like(mv)
+    decode_dense_into(mk, mv, diff, dense_k, dense_v)
+    if trace is not None:
+        trace.append(("materialize", -1))
+    if ledger is not None:
+        ledger.record_dense_mirror()
+        ledger.record_temp_buffer(kv.dense_nbytes)
+        ledger.record_moved(kv.dense_nbytes + diff.payload_nbytes + 2 * kv.dense_nbytes)
+    L, T, H, D = dense_k.shape
+    rows, stride, rotate = _delta_rows(span.delta)
+    table = _kernels.rope_table(rows, D, rope_base, pool.dtype, pool.device)
+    job = _kernels.rows_job(dense_k, dense_v, T * H * D, pool.k, pool.v, pool.layer_stride, T,
+                            dst_rows=slot_map.device_slots(pool.device), tbl_row=0,
+                            tbl_stride=stride, rotate=rotate)
+    _kernels.rows(_kernels.rows_jobs([job]), T, table, L, H, D, _kernels.ROWS_BLOCK, pool.dtype,
+                  pool.device)
+    pool.mark_written(slot_map)
+    if trace is not None:
+        for layer in range(L):
+            trace.extend([("rope", layer), ("write", layer)])

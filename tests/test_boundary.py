@@ -1,0 +1,134 @@
+"""CPU-side checks of the drop-in boundary: the C-ABI library loads and
+exports every symbol include/tdkv.h declares, descriptor layouts match the
+header, host-side planning (allocator policy, collect plan tiling) matches
+the reference, and the product package never imports the oracle."""
+import ast
+import os
+import re
+
+import numpy as np
+import pytest
+
+from helpers import load_golden
+from oracle import roundkv_port as ref
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PKG = os.path.join(ROOT, "paper_2604_03143_b200")
+
+
+def _header_functions():
+    text = open(os.path.join(ROOT, "include", "tdkv.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int32_t|int64_t|const char\*)\s+(tdkv_\w+)\s*\(",
+                                 text, re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    from paper_2604_03143_b200 import _lib
+    _lib.build_library()
+    lib = _lib.load()
+    declared = _header_functions()
+    assert declared, "no functions parsed from tdkv.h"
+    assert set(declared) == set(_lib.EXPORTS)
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert _lib.version() == (1 << 16)
+    assert _lib.launch_count() >= 0
+
+
+def test_descriptor_layouts_match_header():
+    from paper_2604_03143_b200 import _lib
+    text = open(os.path.join(ROOT, "include", "tdkv.h")).read()
+    for struct, dt in [("tdkv_collect_job", _lib.COLLECT_JOB),
+                       ("tdkv_collect_unit", _lib.COLLECT_UNIT),
+                       ("tdkv_diff_pair", _lib.DIFF_PAIR), ("tdkv_diff_out", _lib.DIFF_OUT),
+                       ("tdkv_rows_job", _lib.ROWS_JOB)]:
+        body = re.search(r"typedef struct \{([^{}]*)\}\s*" + struct + ";", text).group(1)
+        # field count and total size (pointers / int64 = 8 B, int32 = 4 B)
+        sizes = []
+        for line in body.strip().splitlines():
+            line = line.split("/*")[0].strip()
+            if not line:
+                continue
+            sizes.append(8 if ("*" in line or "int64_t" in line) else 4)
+        assert sum(sizes) == dt.itemsize, struct
+        assert len(sizes) == len(dt.names), struct
+
+
+def test_allocator_policy_matches_reference_stream():
+    from paper_2604_03143_b200.paged_pool import choose_slots
+    free = np.ones(256, bool)
+    live = {}
+    for op in load_golden()["allocator"]:
+        if op["op"] == "alloc":
+            got = choose_slots(free, op["n"], 32)
+            assert got.tolist() == op["slots"]
+            free[got] = False
+            live[op["serial"]] = got
+        elif op["op"] == "free":
+            free[live.pop(op["serial"])] = True
+
+
+def test_allocator_randomized_against_oracle():
+    from paper_2604_03143_b200.paged_pool import choose_slots
+    rng = np.random.default_rng(5)
+    for cap, bs in [(100, 32), (257, 16), (64, 8), (1000, 32)]:
+        free_a = np.ones(cap, bool)
+        live = []
+        for step in range(300):
+            if live and rng.random() < 0.4:
+                m = live.pop(int(rng.integers(len(live))))
+                free_a[m] = True
+                continue
+            n = int(rng.integers(1, cap // 4))
+            if n > free_a.sum():
+                continue
+            want = ref.allocate_slots(free_a.copy(), n, bs)
+            got = choose_slots(free_a, n, bs)
+            assert got.tolist() == want.tolist()
+            free_a[got] = False
+            live.append(got)
+
+
+def test_product_never_imports_oracle():
+    for dirpath, _, files in os.walk(PKG):
+        for f in files:
+            if not f.endswith(".py"):
+                continue
+            tree = ast.parse(open(os.path.join(dirpath, f)).read())
+            for node in ast.walk(tree):
+                if isinstance(node, ast.Import):
+                    assert all(not a.name.startswith("oracle") for a in node.names), f
+                if isinstance(node, ast.ImportFrom):
+                    assert not (node.module or "").startswith("oracle"), f
+
+
+def test_wire_size_formula_matches_serialization():
+    from paper_2604_03143_b200.diffstore import BlockSparseDiff, LayerDiff, serialize_diff, wire_nbytes
+    rng = np.random.default_rng(3)
+    layers = []
+    for c in (0, 2, 1):
+        idx = np.sort(rng.choice(5, c, replace=False))
+        kb = rng.standard_normal((c, 8, 2, 4)).astype(np.float32)
+        layers.append(LayerDiff(idx, kb, kb.copy()))
+    diff = BlockSparseDiff(3, 8, 2, 4, 37, layers)
+    assert wire_nbytes(diff) == len(serialize_diff(diff))
+    want = ref.serialize([ref.DiffLayer(l.indices, l.k_blocks, l.v_blocks) for l in layers],
+                         8, 2, 4, 37)
+    assert serialize_diff(diff) == want
+
+
+def test_deserialize_rejects_malformed_like_reference():
+    from paper_2604_03143_b200.diffstore import MalformedDiffError, deserialize_diff
+    rng = np.random.default_rng(41)
+    k = rng.standard_normal((4, 64, 2, 8)).astype(np.float32)
+    v = rng.standard_normal((4, 64, 2, 8)).astype(np.float32)
+    mk, mv = k.copy(), v.copy()
+    mk[:, :32] += 1
+    wire = ref.serialize(ref.encode_diff(k, v, mk, mv, np.arange(32), 32), 32, 2, 8, 64)
+    back = deserialize_diff(wire)
+    assert back.changed_blocks_per_layer == [1, 1, 1, 1]
+    for bad, what in [(b"XXXX" + wire[4:], "magic"), (wire[:4] + b"\xff\x00" + wire[6:], "version"),
+                      (wire[:10], "truncated"), (wire[:-6], "truncated"),
+                      (wire + b"\x00", "trailing"), (b"", "truncated")]:
+        with pytest.raises(MalformedDiffError, match=what):
+            deserialize_diff(bad)
