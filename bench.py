@@ -1,0 +1,492 @@
+#!/usr/bin/env python
+"""Benchmark: collected-KV GB/s and agents/s per All-Gather round, plus the
+diff codec's GB/s, on B200 (BASELINE.json metric).
+
+A step is one All-Gather round of the KV Collector over the configured
+synthetic round (default C2: Qwen2.5-7B-shaped bf16 KV, 50 agents per GPU x
+16 shared 256-token blocks): [N>1: NCCL broadcast of the master arena from
+rank 0] + K0 (cos/sin rows) + K1 (rotate + scatter into every agent's paged
+slots).  ``value`` = algorithmic bytes (M + N*M per GPU) of all
+ranks / max-over-ranks device time.  Agents are sharded (weak scaling: each
+GPU owns ``agents`` agents).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2]
+    python bench.py --impl reference ...   # CPU oracle port on the host cores
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="tdkv", choices=["tdkv", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--agents", type=int, default=0, help="agents per GPU (default: config)")
+    ap.add_argument("--no-codec", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--mirror-frac", type=float, default=0.1)
+    ap.add_argument("--profile", action="store_true", help="few launches, no extras (for ncu)")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------
+# clocks
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clock / throttle sampling (NVML) during a region."""
+
+    REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+        "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+        "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+        "display_clock_setting": 0x100,
+    }
+
+    def __init__(self, index: int, period: float = 0.1):
+        self.index = index
+        self.period = period
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:   # noqa: BLE001 - clocks are reported as unavailable
+            self._nvml = None
+
+    def _run(self):
+        nv = self._nvml
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for name, bit in self.REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:   # noqa: BLE001
+                pass
+            self._stop.wait(self.period)
+
+    def __enter__(self):
+        if self._nvml is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def measured_peak_hbm():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:   # noqa: BLE001
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(kernel: str):
+    """dram bytes per launch of ``kernel`` from the committed ncu summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            data = json.load(f)
+        return data.get(kernel, {}).get("dram_bytes_per_launch")
+    except Exception:   # noqa: BLE001
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle legs (cpu_baseline and --impl reference)
+
+
+def _cpu_collect_agents(spec, agents, mk, mv):
+    """Oracle collector (oracle/roundkv_port.collect_into_pool) for ``agents``
+    of the round, each into its own f32 pool; returns elapsed seconds."""
+    from oracle import roundkv_port as ref
+    from paper_2604_03143_b200 import rounds
+    T = spec.tokens_per_agent
+    t0 = time.perf_counter()
+    for a in agents:
+        pk = np.empty((spec.num_layers, T, spec.num_heads, spec.head_dim), np.float32)
+        pv = np.empty_like(pk)
+        slots = np.arange(T, dtype=np.int64)
+        jobs = []
+        for cj in rounds.agent_jobs(spec, a, slots):
+            r0 = cj.segment * spec.seg_len
+            jobs.append(ref.CollectJob(0, mk[:, r0:r0 + spec.seg_len], mv[:, r0:r0 + spec.seg_len],
+                                       np.arange(spec.seg_len), cj.delta))
+        ref.collect_into_pool(jobs, [slots], pk, pv, 10000.0)
+    return time.perf_counter() - t0
+
+
+_REF_STATE = {}
+
+
+def _ref_worker(args):
+    agent, = args
+    st = _REF_STATE
+    return _cpu_collect_agents(st["spec"], [agent], st["mk"], st["mv"])
+
+
+def cpu_masters(spec):
+    """f32 masters on the host: the bf16-rounded values, upcast (the reference
+    is float32-only, roundkv/core.py:180-181)."""
+    import torch
+    from paper_2604_03143_b200 import rounds
+    mk, mv = rounds.master_planes_host(spec)
+    if spec.dtype == "bf16":
+        mk = torch.from_numpy(mk).bfloat16().float().numpy()
+        mv = torch.from_numpy(mv).bfloat16().float().numpy()
+    return mk, mv
+
+
+def cpu_baseline(spec, seconds: float):
+    mk, mv = cpu_masters(spec)
+    done, elapsed = 0, 0.0
+    while elapsed < seconds and done < spec.num_agents:
+        elapsed += _cpu_collect_agents(spec, [done], mk, mv)
+        done += 1
+    gbs = spec.collector_bytes(done) / elapsed / 1e9
+    return {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "port",
+            "agents_per_s": round(done / elapsed, 4),
+            "sample": f"oracle collector (numpy, 1 thread, f32-upcast inputs) on the first "
+                      f"{done} agents of {spec.name}: {elapsed:.1f} s; bytes counted at the "
+                      f"config dtype (M + n*M)"}
+
+
+def run_reference(args):
+    """--impl reference: the oracle port of the reference path on all host
+    cores (agents are independent; one process per core)."""
+    import multiprocessing as mp
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2604_03143_b200 import rounds
+    spec = rounds.CONFIGS[args.config]
+    if args.agents:
+        spec = spec.scaled(num_agents=args.agents)
+    cores = len(os.sched_getaffinity(0))
+    procs = max(1, min(cores, 32, spec.num_agents))
+    mk, mv = cpu_masters(spec)
+    _REF_STATE.update(spec=spec, mk=mk, mv=mv)
+    ctx = mp.get_context("fork")
+    with ctx.Pool(procs) as pool:
+        def step(i):
+            agents = [((i * procs + j) % spec.num_agents,) for j in range(procs)]
+            t0 = time.perf_counter()
+            pool.map(_ref_worker, agents, chunksize=1)
+            return time.perf_counter() - t0
+        for i in range(args.warmup):
+            step(i)
+        times = [step(args.warmup + i) for i in range(args.steps)]
+    t = sum(times) / len(times)
+    gbs = spec.collector_bytes(procs) / t / 1e9
+    line = {
+        "impl": "reference", "metric": "collected KV GB/s", "value": round(gbs, 4),
+        "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": spec.dtype, "data": "synthetic",
+        "config": {"workload": spec.name, "agents_per_step": procs},
+        "agents_per_s": round(procs / t, 3),
+        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": procs, "kind": "port",
+                         "sample": f"{procs} agents of {spec.name} per step, one process per "
+                                   f"agent (oracle/roundkv_port, f32-upcast inputs)"},
+        "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# tdkv
+
+
+def run_tdkv(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2604_03143_b200 as tk
+    from paper_2604_03143_b200 import rounds
+
+    world, rank, local = dist_env()
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    spec = rounds.CONFIGS[args.config]
+    if args.agents:
+        spec = spec.scaled(num_agents=args.agents)
+    dt = spec.torch_dtype
+    L, H, D = spec.num_layers, spec.num_heads, spec.head_dim
+    T = spec.tokens_per_agent
+    n_local = spec.num_agents
+
+    # masters: host-pinned copy (the e2e input) + device arena
+    mk_h, mv_h = rounds.master_planes_host(spec)
+    host_k = torch.from_numpy(mk_h).to(dt).pin_memory()
+    host_v = torch.from_numpy(mv_h).to(dt).pin_memory()
+    del mk_h, mv_h
+    src = rounds.source_offsets(spec)
+    arena = tk.MasterArena(host_k.to(dev), host_v.to(dev),
+                           np.arange(spec.num_segments) * spec.seg_len,
+                           np.full(spec.num_segments, spec.seg_len),
+                           [np.arange(p, p + spec.seg_len) for p in src])
+    pool = tk.PagedPool(n_local * T, L, H, D, dtype=dt, device=dev, debug=False)
+    agents = range(rank * n_local, (rank + 1) * n_local)
+    maps = [pool.allocate(T, a) for a in agents]
+
+    def make_jobs():
+        return [j for a, m in zip(agents, maps) for j in rounds.agent_jobs(spec, a, m.slots)]
+
+    collector = tk.KVCollector(arena, pool)
+    plan = collector.plan(make_jobs())
+    step_bytes = spec.collector_bytes(n_local)
+    assert plan.algorithmic_bytes() == step_bytes
+
+    stream = torch.cuda.current_stream(dev)
+
+    def round_step(events=None):
+        if world > 1:
+            dist.broadcast(arena.k, 0)
+            dist.broadcast(arena.v, 0)
+        if events is not None:
+            events[0].record(stream)
+        collector.collect(plan)
+        if events is not None:
+            events[1].record(stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # -- device-timed rounds ------------------------------------------------
+    for _ in range(args.warmup):
+        round_step()
+    barrier()
+    k1_events = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                 for _ in range(args.steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = tk.launch_count()
+    sampler = ClockSampler(local)
+    with sampler:
+        barrier()
+        start.record(stream)
+        for i in range(args.steps):
+            round_step(k1_events[i])
+        stop.record(stream)
+        barrier()
+    launches = tk.launch_count() - launches0
+    elapsed_ms = max_over_ranks(start.elapsed_time(stop))
+    ms_step = elapsed_ms / args.steps
+    k1_ms = sum(a.elapsed_time(b) for a, b in k1_events) / args.steps
+    value = world * step_bytes / (ms_step * 1e-3) / 1e9
+    agents_per_s = world * n_local / (ms_step * 1e-3)
+
+    peak, peak_kind = measured_peak_hbm()
+    achieved = step_bytes / (k1_ms * 1e-3) / 1e9
+    traffic = ncu_traffic("collect_kernel")
+    line = {
+        "metric": "collected KV GB/s", "value": round(value, 2), "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": spec.dtype, "data": "synthetic",
+        "config": {"workload": spec.name, "agents_per_gpu": n_local,
+                   "total_agents": world * n_local, "shared_blocks": spec.num_segments,
+                   "block_len": spec.seg_len, "layers": L, "kv_heads": H, "head_dim": D,
+                   "tokens_per_agent": T, "parallelism": f"agent-shard x{world}",
+                   "l2": "inputs larger than L2 (master arena "
+                         f"{spec.master_bytes / 2**20:.0f} MiB read, "
+                         f"{step_bytes / 1e9:.1f} GB moved per GPU per step)"},
+        "agents_per_s": round(agents_per_s, 1),
+        "roofline": {"bound": "hbm", "kernel": "collect_kernel (K1)",
+                     "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "peak_source": peak_kind,
+                     "algorithmic_bytes_per_launch": step_bytes,
+                     "k1_ms": round(k1_ms, 4)},
+        "gpu_launches": launches,
+        "clocks": sampler.summary(),
+    }
+
+    # -- e2e: public API with host buffers ---------------------------------
+    if not args.no_e2e and not args.profile:
+        status = torch.empty(1, dtype=dt, device="cpu").pin_memory()
+
+        def e2e_step():
+            # shared blocks arrive from host memory; the round is planned
+            # from host metadata (slot maps, positions); one completion read
+            arena.k.copy_(host_k, non_blocking=True)
+            arena.v.copy_(host_v, non_blocking=True)
+            p = collector.plan(make_jobs())
+            collector.collect(p)
+            status.copy_(pool.k[0, maps[0].slots[spec.hist_len + 1]].view(-1)[:1],
+                         non_blocking=True)
+            return p
+
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            p = e2e_step()
+        ev1.record(stream)
+        barrier()
+        wall = max_over_ranks(time.perf_counter() - t0) / args.steps
+        e2e_gbs = world * step_bytes / wall / 1e9
+        line["e2e"] = {"value": round(e2e_gbs, 2), "unit": "GB/s",
+                       "h2d_bytes_per_step": int(2 * host_k.numel() * host_k.element_size()
+                                                 + p.h2d_bytes),
+                       "d2h_bytes_per_step": int(status.numel() * status.element_size()),
+                       "ms_per_step": round(wall * 1e3, 3),
+                       "agents_per_s": round(world * n_local / wall, 1),
+                       "path": "MasterArena H2D from pinned host + KVCollector.plan (host "
+                               "metadata -> device descriptors) + collect + completion read"}
+
+    # -- codec sub-benchmarks (rank-local) ----------------------------------
+    if not args.no_codec and not args.profile:
+        line["codec"] = codec_bench(tk, spec, pool, maps, dev, args, peak)
+
+    if not args.no_cpu and not args.profile and rank == 0 and world == 1:
+        line["cpu_baseline"] = cpu_baseline(spec, args.cpu_seconds)
+
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def codec_bench(tk, spec, pool, maps, dev, args, peak):
+    """Encode the agents' caches as diffs against agent 0's, then fused-restore
+    every mirror into the pool; each mirror is agent 0's cache with a
+    fraction of its 32-token blocks (all layers) re-drawn."""
+    import torch
+    bs = 32
+    T = spec.tokens_per_agent
+    nb = -(-T // bs)
+    n_mirrors = len(maps) - 1
+    sl0 = maps[0].device_slots(dev)
+    mk = pool.k[:, sl0].contiguous()
+    mv = pool.v[:, sl0].contiguous()
+    master = tk.LayeredKv(mk, mv, np.arange(T))
+    rng = np.random.default_rng(3)
+    g = torch.Generator(device=dev).manual_seed(3)
+    mirrors, hints = [], []
+    n_pick = max(1, int(round(args.mirror_frac * nb)))
+    for _ in range(n_mirrors):
+        blocks = np.sort(rng.choice(nb, n_pick, replace=False))
+        k = mk.clone()
+        v = mv.clone()
+        for b in blocks:
+            lo, hi = b * bs, min(T, b * bs + bs)
+            k[:, lo:hi] = torch.randn(k[:, lo:hi].shape, generator=g, device=dev).to(k.dtype)
+            v[:, lo:hi] = torch.randn(v[:, lo:hi].shape, generator=g, device=dev).to(v.dtype)
+        mirrors.append(tk.LayeredKv(k, v, np.arange(T)))
+        hints.append(np.concatenate([np.arange(b * bs, min(T, b * bs + bs)) for b in blocks]))
+    blocks_cfg = tk.CacheBlockConfig(bs)
+    dense = spec.dense_bytes
+    # encode (K2 compare + compact + the host read of counts/indices)
+    for _ in range(2):
+        diffs = tk.encode_batch(master, mirrors, hints, blocks_cfg)
+    torch.cuda.synchronize(dev)
+    reps = max(1, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        diffs = tk.encode_batch(master, mirrors, hints, blocks_cfg)
+    torch.cuda.synchronize(dev)
+    enc_s = (time.perf_counter() - t0) / reps
+    payload = sum(d.payload_nbytes for d in diffs)
+    changed = sum(sum(d.changed_blocks_per_layer) for d in diffs)
+    enc_bytes = n_mirrors * 2 * dense + payload + 4 * changed
+    # fused restore of every mirror into its agent's slots
+    fam = tk.MasterEntry(0, master, pin_count=n_mirrors)
+    handles = [tk.MirrorHandle(0, i + 1, fam, d) for i, d in enumerate(diffs)]
+    spans = [tk.PositionSpan.shifted(np.arange(T), 16) for _ in handles]
+    tmaps = maps[1:]
+    for _ in range(2):
+        tk.fused_restore_many(handles, spans, pool, tmaps, 10000.0)
+    torch.cuda.synchronize(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(reps):
+        tk.fused_restore_many(handles, spans, pool, tmaps, 10000.0)
+    ev1.record()
+    torch.cuda.synchronize(dev)
+    dec_s = ev0.elapsed_time(ev1) * 1e-3 / reps
+    dec_bytes = n_mirrors * 2 * dense
+    wire = [tk.wire_nbytes(d, 2) for d in diffs]
+    return {
+        "mirrors": n_mirrors, "changed_block_fraction": round(changed / (n_mirrors * spec.num_layers * nb), 4),
+        "encode_gbs": round(enc_bytes / enc_s / 1e9, 1),
+        "encode_frac": round(enc_bytes / enc_s / 1e9 / peak, 4),
+        "encode_ms_per_family": round(enc_s * 1e3, 3),
+        "decode_gbs": round(dec_bytes / dec_s / 1e9, 1),
+        "decode_frac": round(dec_bytes / dec_s / 1e9 / peak, 4),
+        "decode_ms_per_family": round(dec_s * 1e3, 3),
+        "compression_ratio_mean": round(float(np.mean([dense / w for w in wire])), 3),
+        "bytes": "encode: 2*dense + payload + 4*changed per mirror (host read included); "
+                 "fused decode: 2*dense per mirror (K0+K3 device time)",
+    }
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_tdkv(args)
+
+
+if __name__ == "__main__":
+    main()

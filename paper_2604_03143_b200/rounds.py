@@ -1,0 +1,125 @@
+"""Synthetic All-Gather rounds of the benchmark shapes.
+
+An agent's prompt is ``hist || SEP || seg_{pi(0)} || SEP || ... || seg_{pi(S-1)}``
+(the flattened layout of core.PromptLayout, one separator between segments),
+so T = hist + S * (seg_len + 1).  Segment s's master rows were produced at
+source positions p_s .. p_s + seg_len - 1 with p_s ~ U[0, 8192) (seed 1) to
+exercise large |delta|; agent i reads the segments in the order
+rng(2 + i).permutation(S).  K/V values are N(0, 1) float32 (seed 0), bf16
+configs round the same values.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+import torch
+
+from .collector import CollectJob
+
+
+@dataclass(frozen=True)
+class RoundSpec:
+    name: str
+    num_layers: int
+    num_heads: int
+    head_dim: int
+    dtype: str                 # "f32" | "bf16"
+    num_agents: int
+    num_segments: int
+    seg_len: int
+    hist_len: int
+    max_source: int = 8192
+
+    @property
+    def tokens_per_agent(self) -> int:
+        return self.hist_len + self.num_segments * (self.seg_len + 1)
+
+    @property
+    def torch_dtype(self) -> torch.dtype:
+        return torch.float32 if self.dtype == "f32" else torch.bfloat16
+
+    @property
+    def itemsize(self) -> int:
+        return 4 if self.dtype == "f32" else 2
+
+    @property
+    def row_bytes(self) -> int:
+        return self.num_heads * self.head_dim * self.itemsize
+
+    @property
+    def master_rows(self) -> int:
+        return self.num_segments * self.seg_len
+
+    @property
+    def master_bytes(self) -> int:
+        """M: K+V bytes of every shared segment master (read once)."""
+        return 2 * self.num_layers * self.master_rows * self.row_bytes
+
+    def collector_bytes(self, agents: Optional[int] = None) -> int:
+        """Algorithmic collector bytes M + N*M."""
+        n = self.num_agents if agents is None else agents
+        return self.master_bytes * (1 + n)
+
+    @property
+    def dense_bytes(self) -> int:
+        return 2 * self.num_layers * self.tokens_per_agent * self.row_bytes
+
+    def scaled(self, **kw) -> "RoundSpec":
+        d = dict(self.__dict__)
+        d.update(kw)
+        return RoundSpec(**d)
+
+
+CONFIGS = {
+    "c1": RoundSpec("c1-toy-8x4x256-f32", 2, 8, 64, "f32", 8, 4, 256, 64),
+    "c2": RoundSpec("c2-qwen7b-50x16x256-bf16", 28, 4, 128, "bf16", 50, 16, 256, 512),
+    "c3": RoundSpec("c3-qwen14b-25x20x25-bf16", 48, 8, 128, "bf16", 25, 20, 25, 192),
+    "c4": RoundSpec("c4-agentsociety-100x32x128-bf16", 28, 4, 128, "bf16", 100, 32, 128, 8192),
+}
+
+
+def source_offsets(spec: RoundSpec) -> np.ndarray:
+    return np.random.default_rng(1).integers(0, spec.max_source, spec.num_segments).astype(np.int64)
+
+
+def agent_order(agent: int, num_segments: int) -> np.ndarray:
+    return np.random.default_rng(2 + agent).permutation(num_segments)
+
+
+def segment_starts(spec: RoundSpec, agent: int) -> np.ndarray:
+    """Prompt offset of every segment (indexed by segment id) for an agent."""
+    order = agent_order(agent, spec.num_segments)
+    starts = np.empty(spec.num_segments, np.int64)
+    starts[order] = spec.hist_len + 1 + np.arange(spec.num_segments) * (spec.seg_len + 1)
+    return starts
+
+
+def master_planes_host(spec: RoundSpec, seed: int = 0) -> Tuple[np.ndarray, np.ndarray]:
+    """(L, S*len, H, D) float32 masters, segment-major rows."""
+    g = torch.Generator().manual_seed(seed)
+    shape = (spec.num_layers, spec.master_rows, spec.num_heads, spec.head_dim)
+    k = torch.randn(shape, generator=g, dtype=torch.float32)
+    v = torch.randn(shape, generator=g, dtype=torch.float32)
+    return k.numpy(), v.numpy()
+
+
+def agent_jobs(spec: RoundSpec, agent: int, slots: np.ndarray) -> List[CollectJob]:
+    """The collector jobs of one agent: segment s lands at its prompt rows."""
+    starts = segment_starts(spec, agent)
+    src = source_offsets(spec)
+    jobs = []
+    for s in range(spec.num_segments):
+        t0 = int(starts[s])
+        dst = slots[t0:t0 + spec.seg_len]
+        delta = np.full(spec.seg_len, t0 - int(src[s]), np.int64)
+        jobs.append(CollectJob(s, dst, delta))
+    return jobs
+
+
+def shard(num_agents: int, rank: int, world: int) -> range:
+    """Contiguous agent shard of a rank."""
+    per = (num_agents + world - 1) // world
+    lo = min(num_agents, rank * per)
+    return range(lo, min(num_agents, lo + per))

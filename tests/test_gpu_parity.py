@@ -1,0 +1,549 @@
+"""GPU parity: every kernel through the C-ABI against the CPU oracle and the
+reference's golden vectors.
+
+Tolerances (north_star): float32 rotated keys / reconstructed KV max-abs
+1e-5 (the fp64 rotation is expected to be bit-exact whenever the device's
+cos/sin bits equal numpy's); bf16 within 1e-2 * max(1, |ref|) against the
+oracle run on the f32-upcast inputs (one bf16 rounding of the output alone
+is 2^-9 relative); V rows, diff masks, block indices, payload layout, slot
+maps and wire bytes are bit-exact.
+"""
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2604_03143_b200 as tk
+from helpers import (codec_trials, load_golden, load_npz, perturb, random_planes,
+                     restore_trials, sha)
+from oracle import roundkv_port as ref
+from paper_2604_03143_b200 import rounds
+
+pytestmark = pytest.mark.gpu
+G = load_golden()
+DEV = torch.device("cuda", 0)
+F32_TOL = 1e-5
+
+
+def bf16_close(got: np.ndarray, want: np.ndarray) -> float:
+    """max |got - want| / max(1, |want|)"""
+    return float((np.abs(got - want) / np.maximum(1.0, np.abs(want))).max()) if got.size else 0.0
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    tk.build_library()
+    assert torch.cuda.is_available()
+
+
+# ---------------------------------------------------------------------------
+# rotary
+
+
+def test_rope_apply_matches_oracle_and_reference_digests():
+    exact = 0
+    for case in G["rope"]:
+        rng = np.random.default_rng(case["seed"])
+        t, h, d = case["shape"]
+        k = rng.standard_normal((t, h, d)).astype(np.float32)
+        pos = rng.integers(-8192, 8192, t).astype(np.int64)
+        got = tk.rope_apply(k, pos)
+        want = ref.rope_apply(k, pos)
+        assert isinstance(got, np.ndarray) and got.dtype == np.float32
+        assert np.abs(got - want).max() <= F32_TOL
+        exact += int(np.array_equal(got, want))
+    print(f"rope cases bit-exact with numpy: {exact}/{len(G['rope'])}")
+
+
+def test_rope_identities_on_device():
+    rng = np.random.default_rng(5)
+    k = torch.from_numpy((rng.standard_normal((20, 2, 8)) * 0.05).astype(np.float32)).to(DEV)
+    p = np.arange(100, 120, dtype=np.int64)
+    q = np.arange(20, dtype=np.int64) * 3 + 1
+    a = tk.rope_apply(tk.rope_apply(k, p), q)
+    b = tk.rope_apply(k, p + q)
+    assert (a - b).abs().max().item() <= 1e-6
+    assert (tk.rope_apply(tk.rope_apply(k, p), -p) - k).abs().max().item() <= 1e-6
+    span = tk.PositionSpan.identity(range(100, 120))
+    out = tk.rope_recover(span, k)
+    assert out is not k and torch.equal(out, k)
+    with pytest.raises(ValueError):
+        tk.rope_apply(np.zeros((4, 2, 7), np.float32), np.arange(4))
+    with pytest.raises(ValueError):
+        tk.rope_apply(np.zeros((4, 2, 8), np.float32), np.arange(5))
+
+
+def test_rope_bf16_close_to_oracle():
+    rng = np.random.default_rng(8)
+    k = rng.standard_normal((64, 4, 128)).astype(np.float32)
+    pos = rng.integers(-8192, 8192, 64)
+    kb = torch.from_numpy(k).to(DEV).bfloat16()
+    got = tk.rope_apply(kb, pos).float().cpu().numpy()
+    want = ref.rope_apply(kb.float().cpu().numpy(), pos)
+    assert bf16_close(got, want) <= 1e-2
+
+
+# ---------------------------------------------------------------------------
+# collector
+
+
+class _Hit:
+    def __init__(self, kv, target, delta):
+        self.kv = kv
+        self.target_idx = np.asarray(target, np.int64)
+        self.delta = np.asarray(delta, np.int64)
+
+
+class _Member:
+    def __init__(self, hits):
+        self.hits = hits
+
+
+def _golden_round():
+    meta = G["collector"]
+    z = load_npz("collector.npz")
+    masters = [tk.LayeredKv(z[f"master{i}_k"], z[f"master{i}_v"], z[f"master{i}_pos"])
+               for i in range(len(meta["agents"]))]
+    members = [_Member([_Hit(masters[h["master"]], h["target"], h["delta"]) for h in a["hits"]])
+               for a in meta["agents"]]
+    return meta, z, masters, members
+
+
+def test_align_cached_dropin_matches_reference_goldens():
+    meta, z, masters, members = _golden_round()
+    L, _, H, D = z["master0_k"].shape
+    ctx = [(np.zeros((L, a["T"], H, D), np.float32), np.zeros((L, a["T"], H, D), np.float32))
+           for a in meta["agents"]]
+    ledger = tk.CostLedger(L)
+    tk.skeleton_values(members, ctx)
+    tk.align_cached(members, ctx, 10000.0, ledger)
+    assert ledger.rope_calls_by_layer == meta["rope_calls_by_layer"]
+    for a, agent in enumerate(meta["agents"]):
+        shared = np.asarray(agent["shared_idx"])
+        assert np.abs(ctx[a][0][:, shared] - z[f"agent{a}_k_shared"]).max() <= 1e-6
+        assert np.array_equal(ctx[a][1][:, shared], z[f"agent{a}_v_shared"])
+        others = np.setdiff1d(np.arange(agent["T"]), shared)
+        assert not ctx[a][0][:, others].any() and not ctx[a][1][:, others].any()
+
+
+def test_align_cached_device_contexts():
+    meta, z, masters, members = _golden_round()
+    L, _, H, D = z["master0_k"].shape
+    dev_masters = [tk.LayeredKv(torch.from_numpy(m.k).to(DEV), torch.from_numpy(m.v).to(DEV),
+                                m.positions) for m in masters]
+    members = [_Member([_Hit(dev_masters[masters.index(h.kv)], h.target_idx, h.delta)
+                        for h in m.hits]) for m in members]
+    ctx = [(torch.zeros((L, a["T"], H, D), device=DEV), torch.zeros((L, a["T"], H, D), device=DEV))
+           for a in meta["agents"]]
+    tk.align_cached(members, ctx, 10000.0)
+    tk.skeleton_values(members, ctx)
+    for a, agent in enumerate(meta["agents"]):
+        shared = np.asarray(agent["shared_idx"])
+        k = ctx[a][0].cpu().numpy()
+        assert np.abs(k[:, shared] - z[f"agent{a}_k_shared"]).max() <= 1e-6
+        assert np.array_equal(ctx[a][1].cpu().numpy()[:, shared], z[f"agent{a}_v_shared"])
+
+
+def _collect_case(spec: rounds.RoundSpec, tile_rows=None, seed=0):
+    """Run the pool-form collector on a synthetic round and the oracle on the
+    same (f32-upcast) inputs; return (pool_k, pool_v, want_k, want_v, slots)."""
+    mk, mv = rounds.master_planes_host(spec, seed)
+    dt = spec.torch_dtype
+    arena_k = torch.from_numpy(mk).to(DEV).to(dt)
+    arena_v = torch.from_numpy(mv).to(DEV).to(dt)
+    lens = np.full(spec.num_segments, spec.seg_len)
+    row0 = np.arange(spec.num_segments) * spec.seg_len
+    src = rounds.source_offsets(spec)
+    arena = tk.MasterArena(arena_k, arena_v, row0, lens,
+                           [np.arange(p, p + spec.seg_len) for p in src])
+    T = spec.tokens_per_agent
+    pool = tk.PagedPool(spec.num_agents * T + 64, spec.num_layers, spec.num_heads, spec.head_dim,
+                        dtype=dt, device=DEV)
+    maps = [pool.allocate(T, a) for a in range(spec.num_agents)]
+    jobs = [j for a in range(spec.num_agents) for j in rounds.agent_jobs(spec, a, maps[a].slots)]
+    col = tk.KVCollector(arena, pool, 10000.0, tile_rows=tile_rows)
+    plan = col.plan(jobs)
+    ledger = tk.CostLedger(spec.num_layers)
+    col.collect(plan, ledger)
+    assert ledger.rope_calls_by_layer == [1] * spec.num_layers
+    # oracle on the upcast inputs
+    mk32 = arena_k.float().cpu().numpy()
+    mv32 = arena_v.float().cpu().numpy()
+    cap = pool.capacity
+    want_k = np.zeros((spec.num_layers, cap, spec.num_heads, spec.head_dim), np.float32)
+    want_v = np.zeros_like(want_k)
+    ojobs = []
+    for j in jobs:
+        r0 = j.segment * spec.seg_len
+        ojobs.append(ref.CollectJob(0, mk32[:, r0:r0 + spec.seg_len], mv32[:, r0:r0 + spec.seg_len],
+                                    np.arange(spec.seg_len), j.delta))
+    # each oracle job writes its own destination rows
+    for j, oj in zip(jobs, ojobs):
+        ref.collect_into_pool([oj], [j.dst_rows], want_k, want_v, 10000.0)
+    return pool.k.float().cpu().numpy(), pool.v.float().cpu().numpy(), want_k, want_v, jobs
+
+
+def test_collector_c1_f32_matches_oracle():
+    spec = rounds.CONFIGS["c1"]
+    gk, gv, wk, wv, jobs = _collect_case(spec)
+    rows = np.concatenate([j.dst_rows for j in jobs])
+    assert np.array_equal(gv[:, rows], wv[:, rows])
+    err = np.abs(gk[:, rows] - wk[:, rows]).max()
+    exact = float(np.mean(gk[:, rows] == wk[:, rows]))
+    print(f"c1 collector max-abs {err:.3e}, bit-exact fraction {exact:.8f}")
+    assert err <= F32_TOL
+    untouched = np.setdiff1d(np.arange(gk.shape[1]), rows)
+    assert not gk[:, untouched].any() and not gv[:, untouched].any()
+
+
+@pytest.mark.parametrize("tile_rows", [None, 1, 7])
+def test_collector_bf16_reduced_c2(tile_rows):
+    spec = rounds.CONFIGS["c2"].scaled(num_layers=3, num_agents=6, num_segments=5, hist_len=40)
+    gk, gv, wk, wv, jobs = _collect_case(spec, tile_rows=tile_rows)
+    rows = np.concatenate([j.dst_rows for j in jobs])
+    assert np.array_equal(gv[:, rows], wv[:, rows])
+    assert bf16_close(gk[:, rows], wk[:, rows]) <= 1e-2
+
+
+def test_collector_odd_shapes_and_chunking():
+    # rows that are not 16-byte multiples (pair-unit path, no bulk copy),
+    # many agents over few tiles (job chunking)
+    for spec in [rounds.RoundSpec("odd", 2, 3, 6, "f32", 40, 2, 5, 3),
+                 rounds.RoundSpec("odd16", 1, 1, 2, "bf16", 30, 3, 9, 1),
+                 rounds.RoundSpec("many", 1, 2, 8, "f32", 300, 1, 3, 2)]:
+        gk, gv, wk, wv, jobs = _collect_case(spec)
+        rows = np.concatenate([j.dst_rows for j in jobs])
+        assert np.array_equal(gv[:, rows], wv[:, rows])
+        if spec.dtype == "f32":
+            assert np.abs(gk[:, rows] - wk[:, rows]).max() <= F32_TOL
+        else:
+            assert bf16_close(gk[:, rows], wk[:, rows]) <= 1e-2
+
+
+def test_collector_per_token_and_zero_deltas():
+    rng = np.random.default_rng(12)
+    L, H, D, n = 2, 2, 16, 37
+    mk = rng.standard_normal((L, n, H, D)).astype(np.float32)
+    mv = rng.standard_normal((L, n, H, D)).astype(np.float32)
+    arena = tk.MasterArena(torch.from_numpy(mk).to(DEV), torch.from_numpy(mv).to(DEV),
+                           [0], [n], [np.arange(n)])
+    pool = tk.PagedPool(256, L, H, D, device=DEV)
+    m0, m1 = pool.allocate(n), pool.allocate(n)
+    d_var = rng.integers(-5000, 5000, n).astype(np.int64)
+    for deltas in ([np.zeros(n, np.int64), np.zeros(n, np.int64)],
+                   [d_var, np.full(n, 17, np.int64)]):
+        jobs = [tk.CollectJob(0, m0.slots, deltas[0]), tk.CollectJob(0, m1.slots, deltas[1])]
+        col = tk.KVCollector(arena, pool)
+        col.collect(col.plan(jobs))
+        gk = pool.k.cpu().numpy()
+        for m, d in zip((m0, m1), deltas):
+            for layer in range(L):
+                want = ref.rope_recover(np.zeros(n), d, mk[layer]) if d.any() else mk[layer]
+                assert np.abs(gk[layer, m.slots] - want).max() <= F32_TOL
+                if not d.any():
+                    assert np.array_equal(gk[layer, m.slots], mk[layer])
+
+
+# ---------------------------------------------------------------------------
+# encoder / decoder
+
+
+def test_codec_trials_match_reference_goldens():
+    for trial, want in zip(codec_trials(len(G["codec_trials"])), G["codec_trials"]):
+        master = tk.LayeredKv(trial.master_k, trial.master_v, trial.positions)
+        mirror = tk.LayeredKv(trial.mirror_k, trial.mirror_v, trial.positions)
+        blocks = tk.CacheBlockConfig(trial.block_size)
+        diff = tk.encode_diff(master, mirror, trial.hints, blocks)
+        assert [ld.indices.tolist() for ld in diff.layers] == want["indices"]
+        wire = tk.serialize_diff(diff)
+        assert len(wire) == want["wire_len"] == tk.wire_nbytes(diff)
+        assert hashlib.sha256(wire).hexdigest() == want["wire_sha"]
+        back = tk.diff_decode_dense(master, tk.deserialize_diff(wire))
+        assert np.array_equal(back.k, trial.mirror_k) and np.array_equal(back.v, trial.mirror_v)
+        direct = tk.diff_decode_dense(master, diff)
+        assert np.array_equal(direct.k, trial.mirror_k)
+
+
+def test_known_answers_and_errors():
+    known = G["known"]
+    blocks = tk.CacheBlockConfig(32)
+    rng = np.random.default_rng(known["worked"]["seed"])
+    k, v, pos = random_planes(rng, 640)
+    mk, mv, hints = perturb(rng, k, v, 32, [3, 17])
+    diff = tk.encode_diff(tk.LayeredKv(k, v, pos), tk.LayeredKv(mk, mv, pos), hints, blocks)
+    assert diff.changed_blocks_per_layer == [2, 2, 2, 2]
+    assert diff.payload_nbytes == 32768
+    wire = tk.serialize_diff(diff)
+    assert len(wire) - diff.payload_nbytes == 80
+    assert hashlib.sha256(wire).hexdigest() == known["worked"]["wire_sha"]
+
+    rng = np.random.default_rng(known["violation"]["seed"])
+    k, v, pos = random_planes(rng, 128)
+    mk, mv, hints = perturb(rng, k, v, 32, [1])
+    mv[0, 100, 0, 0] += 0.5
+    with pytest.raises(tk.HintSoundnessError) as err:
+        tk.encode_diff(tk.LayeredKv(k, v, pos), tk.LayeredKv(mk, mv, pos), hints, blocks)
+    assert str(err.value) == known["violation"]["message"]
+
+    rng = np.random.default_rng(known["partial"]["seed"])
+    k, v, pos = random_planes(rng, 70)
+    mk, mv, hints = perturb(rng, k, v, 32, [2])
+    diff = tk.encode_diff(tk.LayeredKv(k, v, pos), tk.LayeredKv(mk, mv, pos), hints, blocks)
+    assert diff.layers[0].k_blocks.shape[1] == 32
+    assert np.all(diff.layers[0].k_blocks[0, 6:] == 0.0)
+    assert hashlib.sha256(tk.serialize_diff(diff)).hexdigest() == known["partial"]["wire_sha"]
+
+    with pytest.raises(ValueError, match="shape"):
+        tk.encode_diff(tk.LayeredKv(k, v, pos), tk.LayeredKv(*random_planes(rng, 96)[:2],
+                                                             np.arange(96)), hints, blocks)
+    k2, v2, _ = random_planes(rng, 70)
+    with pytest.raises(ValueError, match="positions"):
+        tk.encode_diff(tk.LayeredKv(k, v, pos), tk.LayeredKv(k2, v2, pos + 5), hints, blocks)
+
+
+def test_float_equality_semantics():
+    """+0 == -0 is unchanged, NaN != NaN is changed (np.array_equal)."""
+    k = np.zeros((1, 64, 1, 4), np.float32)
+    v = np.zeros_like(k)
+    pos = np.arange(64)
+    mk = k.copy()
+    mk[0, 3, 0, 0] = -0.0
+    d = tk.encode_diff(tk.LayeredKv(k, v, pos), tk.LayeredKv(mk, v.copy(), pos),
+                       np.empty(0, np.int64), tk.CacheBlockConfig(32))
+    assert d.changed_blocks_per_layer == [0]
+    k2 = k.copy()
+    k2[0, 40, 0, 1] = np.nan
+    d = tk.encode_diff(tk.LayeredKv(k2, v, pos), tk.LayeredKv(k2.copy(), v.copy(), pos),
+                       np.arange(32, 64), tk.CacheBlockConfig(32))
+    assert d.layers[0].indices.tolist() == [1]
+
+
+def test_hinted_but_identical_not_stored_and_single_row_change():
+    rng = np.random.default_rng(23)
+    k, v, pos = random_planes(rng, 128)
+    mk, mv, _ = perturb(rng, k, v, 32, [1])
+    d = tk.encode_diff(tk.LayeredKv(k, v, pos), tk.LayeredKv(mk, mv, pos), np.arange(128),
+                       tk.CacheBlockConfig(32))
+    assert d.changed_blocks_per_layer == [1, 1, 1, 1]
+    m2 = k.copy()
+    m2[2, 40, 1, 3] += 1.0
+    d = tk.encode_diff(tk.LayeredKv(k, v, pos), tk.LayeredKv(m2, v.copy(), pos), np.array([40]),
+                       tk.CacheBlockConfig(32))
+    assert d.changed_blocks_per_layer == [0, 0, 1, 0] and d.layers[2].indices.tolist() == [1]
+
+
+def test_family_matches_reference_stats():
+    fam = G["family"]
+    z = load_npz("family.npz")
+    pos = z["positions"]
+    results = {fam["master_id"]: type("R", (), {"kv": tk.LayeredKv(z["master_k"], z["master_v"], pos)})}
+    hints = {}
+    for m in fam["mirrors"]:
+        rid = m["rid"]
+        results[rid] = type("R", (), {"kv": tk.LayeredKv(z[f"mirror{rid}_k"], z[f"mirror{rid}_v"], pos)})
+        hints[rid] = z[f"hints{rid}"]
+    plan = type("P", (), {"master_id": fam["master_id"], "mirror_diff_hints": hints})
+    store = tk.DiffStore(tk.CacheBlockConfig(fam["block_size"]))
+    enc = store.encode_family(plan, results)
+    st = fam["stats"]
+    assert enc.stats.dense_nbytes == st["dense"]
+    assert enc.stats.diff_payload_nbytes == st["payload"]
+    assert enc.stats.diff_serialized_nbytes == st["serialized"]
+    assert enc.stats.changed_blocks == st["changed"]
+    assert enc.stats.ratios == st["ratios"]
+    assert enc.stats.family_cost == st["family_cost"]
+    assert enc.master.pin_count == len(fam["mirrors"])
+    L, T, H, D = z["master_k"].shape
+    for m in fam["mirrors"]:
+        h = enc.mirrors[m["rid"]]
+        assert [ld.indices.tolist() for ld in h.diff.layers] == m["indices"]
+        assert hashlib.sha256(tk.serialize_diff(h.diff)).hexdigest() == m["wire_sha"]
+        pool = tk.PagedPool(4 * T + 32, L, H, D, block_size=8, device=DEV)
+        fmap = pool.allocate(T, 1)
+        dmap = pool.allocate(T, 2)
+        assert fmap.slots.tolist() == m["fused_slots"]
+        span = tk.PositionSpan.shifted(pos, 16)
+        led = tk.CostLedger(L)
+        tk.fused_restore(h, span, pool, fmap, fam["rope_base"], ledger=led)
+        tk.dense_restore(h, span, pool, dmap, fam["rope_base"])
+        assert led.bytes_moved == m["bytes_moved"] and led.temp_buffer_peak_bytes == m["temp_peak"]
+        fk = np.stack([pool.read_rows(fmap, l, host=True)[0] for l in range(L)])
+        dk = np.stack([pool.read_rows(dmap, l, host=True)[0] for l in range(L)])
+        assert np.array_equal(fk, dk)
+    for h in enc.mirrors.values():
+        h.release()
+    store.drop_family(enc.master.family_id)
+
+
+# ---------------------------------------------------------------------------
+# restores
+
+
+def _handle(master_k, master_v, pos, diff):
+    master = tk.MasterEntry(0, tk.LayeredKv(master_k, master_v, pos))
+    master.pin_count = 1
+    return tk.MirrorHandle(0, 1, master, diff)
+
+
+def test_restore_trials_match_oracle_and_goldens():
+    exact = 0
+    for trial, want in zip(restore_trials(len(G["restores"])), G["restores"]):
+        master = tk.LayeredKv(trial.master_k, trial.master_v, trial.positions)
+        mirror = tk.LayeredKv(trial.mirror_k, trial.mirror_v, trial.positions)
+        diff = tk.encode_diff(master, mirror, trial.hints, tk.CacheBlockConfig(16))
+        handle = _handle(trial.master_k, trial.master_v, trial.positions, diff)
+        span = tk.PositionSpan.shifted(trial.positions, trial.delta)
+        pool = tk.PagedPool(128, 3, 2, 8, block_size=16, device=DEV)
+        smap = pool.allocate(trial.master_k.shape[1], 1)
+        assert smap.slots.tolist() == want["slots"]
+        led = tk.CostLedger(3)
+        tk.fused_restore(handle, span, pool, smap, 10000.0, ledger=led)
+        assert led.bytes_moved == want["bytes_moved"]
+        gk = np.stack([pool.read_rows(smap, l, host=True)[0] for l in range(3)])
+        gv = np.stack([pool.read_rows(smap, l, host=True)[1] for l in range(3)])
+        layers = ref.encode_diff(trial.master_k, trial.master_v, trial.mirror_k, trial.mirror_v,
+                                 trial.hints, 16)
+        wk = np.zeros((3, 128, 2, 8), np.float32)
+        wv = np.zeros_like(wk)
+        ref.fused_restore(trial.master_k, trial.master_v, layers, 16, trial.positions,
+                          trial.positions + trial.delta, smap.slots, wk, wv, 10000.0)
+        assert np.array_equal(gv, wv[:, smap.slots])
+        assert np.abs(gk - wk[:, smap.slots]).max() <= F32_TOL
+        exact += int(sha(gk, gv) == want["sha"])
+    print(f"restores bit-identical to the reference digests: {exact}/{len(G['restores'])}")
+
+
+@pytest.mark.parametrize("offset", [0, 16, -5])
+def test_fused_equals_dense_bitwise(offset):
+    rng = np.random.default_rng(101 + offset)
+    for _ in range(10):
+        T = int(rng.integers(33, 161))
+        nb = -(-T // 32)
+        picks = sorted(rng.choice(nb, size=int(rng.integers(1, nb + 1)), replace=False).tolist())
+        k, v, pos = random_planes(rng, T, start=int(rng.integers(0, 50)))
+        mk, mv, hints = perturb(rng, k, v, 32, picks)
+        diff = tk.encode_diff(tk.LayeredKv(k, v, pos), tk.LayeredKv(mk, mv, pos), hints,
+                              tk.CacheBlockConfig(32))
+        h = _handle(k, v, pos, diff)
+        span = tk.PositionSpan.shifted(pos, offset)
+        pool = tk.PagedPool(512, 4, 2, 8, device=DEV)
+        a, b = pool.allocate(T, 1), pool.allocate(T, 2)
+        tk.fused_restore(h, span, pool, a, 10000.0)
+        tk.dense_restore(h, span, pool, b, 10000.0)
+        for layer in range(4):
+            fa = pool.read_rows(a, layer, host=True)
+            fb = pool.read_rows(b, layer, host=True)
+            assert np.array_equal(fa[0], fb[0]) and np.array_equal(fa[1], fb[1])
+        if offset == 0:
+            assert np.array_equal(np.stack([pool.read_rows(a, l, host=True)[0] for l in range(4)]), mk)
+
+
+def test_restore_event_order_accounting_and_validation():
+    rng = np.random.default_rng(17)
+    k, v, pos = random_planes(rng, 96)
+    mk, mv, hints = perturb(rng, k, v, 32, [0, 2])
+    diff = tk.encode_diff(tk.LayeredKv(k, v, pos), tk.LayeredKv(mk, mv, pos), hints,
+                          tk.CacheBlockConfig(32))
+    h = _handle(k, v, pos, diff)
+    pool = tk.PagedPool(512, 4, 2, 8, device=DEV)
+    span = tk.PositionSpan.shifted(pos, 4)
+    trace = []
+    fl = tk.CostLedger(4)
+    tk.fused_restore(h, span, pool, pool.allocate(96, 1), 10000.0, ledger=fl, trace=trace)
+    assert trace == [(e, l) for l in range(4) for e in ("load", "swap", "diff", "rope", "write")]
+    pair = 2 * 96 * 2 * 8 * 4
+    assert fl.bytes_moved == 2 * 4 * 96 * 2 * 8 * 4 + diff.payload_nbytes
+    assert fl.temp_buffer_peak_bytes == 2 * pair and fl.dense_mirror_allocations == 0
+    dl = tk.CostLedger(4)
+    dtrace = []
+    tk.dense_restore(h, span, pool, pool.allocate(96, 2), 10000.0, ledger=dl, trace=dtrace)
+    assert dtrace[0] == ("materialize", -1)
+    assert dl.dense_mirror_allocations == 1 and dl.temp_buffer_peak_bytes == 4 * pair
+    with pytest.raises(ValueError, match="one slot per token"):
+        tk.fused_restore(h, span, pool, pool.allocate(32, 3), 10000.0)
+    with pytest.raises(ValueError, match="source positions"):
+        tk.fused_restore(h, tk.PositionSpan.shifted(pos + 3, 1), pool, pool.allocate(96, 4), 1e4)
+    h.release()
+    with pytest.raises(ValueError, match="released"):
+        tk.fused_restore(h, span, pool, pool.allocate(96, 5), 10000.0)
+
+
+# ---------------------------------------------------------------------------
+# pool
+
+
+def test_pool_roundtrip_poison_and_use_after_free():
+    pool = tk.PagedPool(128, 3, 2, 8, device=DEV)
+    rng = np.random.default_rng(0)
+    m = pool.allocate(40, 1)
+    assert m.slots.tolist() == list(range(40))
+    stored = []
+    for layer in range(3):
+        kr = rng.standard_normal((40, 2, 8)).astype(np.float32)
+        vr = rng.standard_normal((40, 2, 8)).astype(np.float32)
+        pool.write_rows(m, layer, kr, vr)
+        stored.append((kr, vr))
+    for layer in range(3):
+        kr, vr = pool.read_rows(m, layer, host=True)
+        assert np.array_equal(kr, stored[layer][0]) and np.array_equal(vr, stored[layer][1])
+    pool.free(m)
+    assert torch.isnan(pool.k[:, :40]).all()
+    with pytest.raises(tk.UseAfterFreeError):
+        pool.read_rows(m, 0)
+    m2 = pool.allocate(8)
+    with pytest.raises(tk.UseAfterFreeError):
+        pool.read_rows(m2, 0)
+    with pytest.raises(tk.OutOfSlotsError):
+        pool.allocate(500)
+
+
+# ---------------------------------------------------------------------------
+# full-size properties (BASELINE configs), size-independent checks
+
+
+def test_c2_full_size_collector_and_codec_properties():
+    spec = rounds.CONFIGS["c2"].scaled(num_agents=8)
+    mk, mv = rounds.master_planes_host(spec)
+    dt = spec.torch_dtype
+    arena = tk.MasterArena(torch.from_numpy(mk).to(DEV).to(dt), torch.from_numpy(mv).to(DEV).to(dt),
+                           np.arange(spec.num_segments) * spec.seg_len,
+                           np.full(spec.num_segments, spec.seg_len),
+                           [np.arange(spec.seg_len)] * spec.num_segments)
+    T = spec.tokens_per_agent
+    pool = tk.PagedPool(spec.num_agents * T, spec.num_layers, spec.num_heads, spec.head_dim,
+                        dtype=dt, device=DEV)
+    maps = [pool.allocate(T, a) for a in range(spec.num_agents)]
+    jobs = [j for a in range(spec.num_agents) for j in rounds.agent_jobs(spec, a, maps[a].slots)]
+    col = tk.KVCollector(arena, pool)
+    col.collect(col.plan(jobs))
+    # V rows are bit copies of the master; K rows rotate back to the master
+    for j in jobs[:: 37]:
+        r0 = j.segment * spec.seg_len
+        got_v = pool.v[:, torch.from_numpy(j.dst_rows).to(DEV)]
+        assert torch.equal(got_v, arena.v[:, r0:r0 + spec.seg_len])
+        got_k = pool.k[5, torch.from_numpy(j.dst_rows).to(DEV)]
+        back = tk.rope_apply(got_k.float(), -j.delta).cpu().numpy()
+        want = arena.k[5, r0:r0 + spec.seg_len].float().cpu().numpy()
+        assert bf16_close(back, want) <= 2e-2
+    # encode -> decode round trip of agent caches taken from the pool
+    dense = []
+    for m in maps[:3]:
+        sl = torch.from_numpy(m.slots).to(DEV)
+        dense.append(tk.LayeredKv(pool.k[:, sl].contiguous(), pool.v[:, sl].contiguous(),
+                                  np.arange(T)))
+    rng = np.random.default_rng(3)
+    mirrors, hints = [], []
+    for d in dense[1:]:
+        mir = dense[0].copy()
+        blocks = sorted(rng.choice(-(-T // 32), 15, replace=False).tolist())
+        for b in blocks:
+            mir.k[:, b * 32:(b + 1) * 32] = d.k[:, b * 32:(b + 1) * 32]
+            mir.v[:, b * 32:(b + 1) * 32] = d.v[:, b * 32:(b + 1) * 32]
+        mirrors.append(mir)
+        hints.append(np.concatenate([np.arange(b * 32, min(T, b * 32 + 32)) for b in blocks]))
+    diffs = tk.encode_batch(dense[0], mirrors, hints, tk.CacheBlockConfig(32))
+    for mir, diff in zip(mirrors, diffs):
+        assert max(diff.changed_blocks_per_layer) <= 15
+        back = tk.diff_decode_dense(dense[0], diff)
+        assert torch.equal(back.k, mir.k) and torch.equal(back.v, mir.v)
