@@ -192,11 +192,17 @@ typedef struct {
     int32_t rotate;
 } tdkv_rows_job;
 
+/* flags: TDKV_ROWS_CONTIGUOUS promises that every job has src_rows == NULL
+ * and 16-byte aligned planes, payloads and strides; rows that are whole
+ * 16-byte units then take the TMA-staged path (tiles of tile_rows rows,
+ * 0 = block_size, double-buffered in shared memory by cp.async.bulk). */
+#define TDKV_ROWS_CONTIGUOUS 1
+
 int32_t tdkv_rows(const tdkv_rows_job* d_jobs, int32_t n_jobs,
                   int32_t max_tokens, const void* d_table,
                   int32_t num_layers, int32_t num_heads, int32_t head_dim,
-                  int32_t block_size, int32_t dtype, int32_t grid_limit,
-                  void* stream);
+                  int32_t block_size, int32_t dtype, int32_t flags,
+                  int32_t tile_rows, int32_t grid_limit, void* stream);
 
 /* Fill rows of every layer with a value (NaN poisoning of freed slots,
  * paged_pool.py:144-147).  value_bits is the element bit pattern. */

@@ -61,10 +61,38 @@ def rows(jobs: np.ndarray, max_tokens: int, table: Optional[torch.Tensor], num_l
     """K3 over a ROWS_JOB descriptor array."""
     if jobs.size == 0 or max_tokens == 0:
         return
+    esz = 4 if kv_dtype == torch.float32 else 2
+    flags, tile = 0, 0
+    if _contiguous(jobs, esz):
+        flags = _lib.ROWS_CONTIGUOUS
+        tile = min(block_size, tile_rows_for(num_heads * head_dim * esz))
     d_jobs = upload(jobs, device)
     _lib.call("tdkv_rows", ptr(d_jobs), int(jobs.size), int(max_tokens), ptr(table),
-              num_layers, num_heads, head_dim, block_size, dtype_code(kv_dtype), grid_limit,
-              stream_handle(device))
+              num_layers, num_heads, head_dim, block_size, dtype_code(kv_dtype), flags, tile,
+              grid_limit, stream_handle(device))
+
+
+def tile_rows_for(row_bytes: int, budget: int = 72 * 1024) -> int:
+    """Rows per staged tile: double-buffered K+V within ``budget`` bytes."""
+    rows = max(1, budget // (4 * row_bytes))
+    p = 1
+    while p * 2 <= min(rows, 32):
+        p *= 2
+    return p
+
+
+def _contiguous(jobs: np.ndarray, esz: int) -> bool:
+    """Every job reads whole contiguous source rows from 16-byte aligned
+    planes/payloads (the TMA-staged K3 path)."""
+    if (jobs["src_rows"] != 0).any():
+        return False
+    for f in ("src_k", "src_v", "pay_k", "pay_v", "dst_k", "dst_v"):
+        if (jobs[f] % 16 != 0).any():
+            return False
+    for f in ("src_layer_stride", "dst_layer_stride"):
+        if ((jobs[f] * esz) % 16 != 0).any():
+            return False
+    return True
 
 
 def rows_job(src_k, src_v, src_layer_stride, dst_k, dst_v, dst_layer_stride, num_tokens, *,

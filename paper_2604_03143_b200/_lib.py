@@ -23,6 +23,7 @@ INCLUDE = os.path.join(ROOT, "include")
 TDKV_F32 = 0
 TDKV_BF16 = 1
 NO_VIOLATION = 0x7F7F7F7F
+ROWS_CONTIGUOUS = 1
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -105,7 +106,8 @@ _SIGS = {
                                  _I32, _P]),
     "tdkv_diff_compact": (_I32, [_P, _P, _I32, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32,
                                  _P]),
-    "tdkv_rows": (_I32, [_P, _I32, _I32, _P, _I32, _I32, _I32, _I32, _I32, _I32, _P]),
+    "tdkv_rows": (_I32, [_P, _I32, _I32, _P, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32,
+                         _P]),
     "tdkv_fill_rows": (_I32, [_P, _I64, _I32, _P, _I64, _I32, _I32, ctypes.c_uint32, _P]),
 }
 
