@@ -90,23 +90,40 @@ class _DeviceDiff:
     map_v: torch.Tensor
 
 
-@dataclass(eq=False)
+@dataclass
+class _EncodedSlab:
+    """Encoder output kept in its device layout: layer l's changed blocks are
+    slab rows [l*cap, l*cap + counts[l]) with block ids idx[l*cap:...]."""
+
+    counts: np.ndarray           # (L,) int
+    idx: np.ndarray              # (L*cap,) int32, host copy
+    cap: int
+    pay_k: torch.Tensor          # (L*cap, bs, H, D)
+    pay_v: torch.Tensor
+
+
 class BlockSparseDiff:
-    """Per-layer changed blocks of a mirror relative to its master."""
+    """Per-layer changed blocks of a mirror relative to its master.
 
-    num_layers: int
-    block_size: int
-    num_heads: int
-    head_dim: int
-    total_tokens: int
-    layers: List[LayerDiff]
-    _dev: Optional[_DeviceDiff] = field(default=None, repr=False)
+    Constructed from ``layers`` (validated like diffstore.py:84-99), or by the
+    encoder from its device slab, in which case the per-layer ``LayerDiff``
+    views are only materialized when ``layers`` is first read.
+    """
 
-    def __post_init__(self) -> None:
-        if len(self.layers) != self.num_layers:
+    def __init__(self, num_layers: int, block_size: int, num_heads: int, head_dim: int,
+                 total_tokens: int, layers: List[LayerDiff]) -> None:
+        self.num_layers = num_layers
+        self.block_size = block_size
+        self.num_heads = num_heads
+        self.head_dim = head_dim
+        self.total_tokens = total_tokens
+        self._layers = list(layers)
+        self._slab: Optional[_EncodedSlab] = None
+        self._dev: Optional[_DeviceDiff] = None
+        if len(self._layers) != self.num_layers:
             raise ValueError("one LayerDiff per layer required")
         nb = CacheBlockConfig(self.block_size).num_blocks(self.total_tokens)
-        for ld in self.layers:
+        for ld in self._layers:
             for idx, payload in ((ld.indices, ld.k_blocks), (ld.v_indices, ld.v_blocks)):
                 idx = ld.indices if idx is None else idx
                 if idx.size and (idx.min() < 0 or idx.max() >= nb):
@@ -117,13 +134,67 @@ class BlockSparseDiff:
                 if not _payload_ok(payload, want):
                     raise ValueError("payload must be float32 with one block per index")
 
+    @classmethod
+    def _from_slab(cls, num_layers: int, block_size: int, num_heads: int, head_dim: int,
+                   total_tokens: int, slab: _EncodedSlab, dev: _DeviceDiff) -> "BlockSparseDiff":
+        self = cls.__new__(cls)
+        self.num_layers = num_layers
+        self.block_size = block_size
+        self.num_heads = num_heads
+        self.head_dim = head_dim
+        self.total_tokens = total_tokens
+        self._layers = None
+        self._slab = slab
+        self._dev = dev
+        return self
+
+    @property
+    def layers(self) -> List[LayerDiff]:
+        if self._layers is None:
+            s = self._slab
+            out = []
+            for layer in range(self.num_layers):
+                n = int(s.counts[layer])
+                base = layer * s.cap
+                out.append(LayerDiff(s.idx[base:base + n].astype(np.int64),
+                                     s.pay_k[base:base + n], s.pay_v[base:base + n]))
+            self._layers = out
+        return self._layers
+
+    @layers.setter
+    def layers(self, value: List[LayerDiff]) -> None:
+        self._layers = list(value)
+
     @property
     def payload_nbytes(self) -> int:
-        return sum(ld.payload_nbytes for ld in self.layers)
+        if self._layers is None:
+            s = self._slab
+            blk = self.block_size * self.num_heads * self.head_dim * s.pay_k.element_size()
+            return int(2 * blk * int(s.counts.sum()))
+        return sum(ld.payload_nbytes for ld in self._layers)
 
     @property
     def changed_blocks_per_layer(self) -> List[int]:
-        return [int(ld.indices.size) for ld in self.layers]
+        if self._layers is None:
+            return [int(c) for c in self._slab.counts]
+        return [int(ld.indices.size) for ld in self._layers]
+
+    def _plane_counts(self):
+        """Per layer (k_count, v_count, escape)."""
+        if self._layers is None:
+            return [(int(c), int(c), False) for c in self._slab.counts]
+        return [(int(ld.indices.size),
+                 int(ld.indices.size if ld.v_indices is None else ld.v_indices.size),
+                 ld.v_indices is not None) for ld in self._layers]
+
+    def to_host(self) -> "BlockSparseDiff":
+        """Bring the payload to host numpy (the reference's representation)."""
+        for ld in self.layers:
+            if isinstance(ld.k_blocks, torch.Tensor):
+                ld.k_blocks = to_host(ld.k_blocks)
+            if isinstance(ld.v_blocks, torch.Tensor):
+                ld.v_blocks = to_host(ld.v_blocks)
+        return self
 
     def device_form(self, device: torch.device, dtype: torch.dtype) -> _DeviceDiff:
         """Payload slabs + block maps on the device (uploaded once for host diffs)."""
@@ -201,21 +272,23 @@ def encode_batch(master: LayeredKv, mirrors: Sequence[LayeredKv],
                      dtype=_lib.DIFF_PAIR)
     d_pairs = upload(pairs, device)
     d_hinted = torch.from_numpy(hinted.reshape(-1)).to(device)
+    caps = np.maximum(hinted.sum(axis=1).astype(np.int64), 1)
+    slab_blocks = int((caps * L).sum())
+    # one int32 buffer for everything the host reads back: one D2H copy
+    meta = torch.empty(P + P * L + slab_blocks, dtype=torch.int32, device=device)
+    violation = meta[:P]
+    counts = meta[P:P + P * L]
+    indices = meta[P + P * L:]
     changed = torch.empty(P * L * nb, dtype=torch.uint8, device=device)
-    violation = torch.empty(P, dtype=torch.int32, device=device)
     viol_maxabs = torch.zeros(P * L * nb, dtype=torch.float32, device=device)
     code = dtype_code(dtype)
     stream = stream_handle(device)
     _lib.call("tdkv_diff_compare", ptr(d_pairs), P, ptr(d_hinted), ptr(changed), ptr(violation),
               ptr(viol_maxabs), L, total, H, D, bs, code, stream)
 
-    caps = np.maximum(hinted.sum(axis=1).astype(np.int64), 1)
-    slab_blocks = int((caps * L).sum())
     pay_k = torch.empty((slab_blocks, bs, H, D), dtype=dtype, device=device)
     pay_v = torch.empty_like(pay_k)
-    indices = torch.empty(slab_blocks, dtype=torch.int32, device=device)
     blkmap = torch.empty(P * L * nb, dtype=torch.int32, device=device)
-    counts = torch.empty(P * L, dtype=torch.int32, device=device)
     starts = np.concatenate([[0], np.cumsum(caps * L)[:-1]])
     esz = pay_k.element_size()
     blk_bytes = bs * H * D * esz
@@ -226,7 +299,8 @@ def encode_batch(master: LayeredKv, mirrors: Sequence[LayeredKv],
     _lib.call("tdkv_diff_compact", ptr(d_pairs), ptr(d_outs), P, ptr(changed), ptr(counts),
               L, total, H, D, bs, code, stream)
 
-    viol_h = violation.cpu().numpy()
+    meta_h = meta.cpu().numpy()
+    viol_h = meta_h[:P]
     bad = np.flatnonzero(viol_h != _lib.NO_VIOLATION)
     if bad.size:
         p = int(bad[0])
@@ -235,23 +309,16 @@ def encode_batch(master: LayeredKv, mirrors: Sequence[LayeredKv],
         worst = float(viol_maxabs[(p * L + layer) * nb + b].item())
         raise HintSoundnessError(
             f"layer {layer} block {b} differs outside the hinted positions (max abs {worst:.3e})")
-    counts_h = counts.cpu().numpy().reshape(P, L)
-    idx_h = indices.cpu().numpy()
+    counts_h = meta_h[P:P + P * L].reshape(P, L)
+    idx_h = meta_h[P + P * L:]
     diffs = []
     for p in range(P):
         s, cap = int(starts[p]), int(caps[p])
-        layers = []
-        for layer in range(L):
-            n = int(counts_h[p, layer])
-            base = s + layer * cap
-            layers.append(LayerDiff(idx_h[base:base + n].astype(np.int64),
-                                    pay_k[base:base + n], pay_v[base:base + n]))
-        diff = BlockSparseDiff(L, bs, H, D, total, layers)
-        slab_k = pay_k[s:s + L * cap]
-        slab_v = pay_v[s:s + L * cap]
+        slab = _EncodedSlab(counts_h[p], idx_h[s:s + L * cap], cap, pay_k[s:s + L * cap],
+                            pay_v[s:s + L * cap])
         mp = blkmap[p * L * nb:(p + 1) * L * nb]
-        diff._dev = _DeviceDiff(slab_k, slab_v, mp, mp)
-        diffs.append(diff)
+        diffs.append(BlockSparseDiff._from_slab(L, bs, H, D, total, slab,
+                                                _DeviceDiff(slab.pay_k, slab.pay_v, mp, mp)))
     return diffs
 
 
@@ -262,11 +329,7 @@ def encode_diff(master: LayeredKv, mirror: LayeredKv, hint_positions: np.ndarray
     Host (numpy) inputs produce a diff with host numpy payloads; device
     inputs keep the payload on the device."""
     diff = encode_batch(master, [mirror], [hint_positions], blocks)[0]
-    if not master.on_device:
-        for ld in diff.layers:
-            ld.k_blocks = to_host(ld.k_blocks)
-            ld.v_blocks = to_host(ld.v_blocks)
-    return diff
+    return diff if master.on_device else diff.to_host()
 
 
 # ---------------------------------------------------------------------------
@@ -310,11 +373,9 @@ def wire_nbytes(diff: BlockSparseDiff, itemsize: int = 4) -> int:
     reference's float32 wire (equal to len(serialize_diff(diff)))."""
     blk = diff.block_size * diff.num_heads * diff.head_dim * itemsize
     n = _HEADER.size + 4
-    for ld in diff.layers:
-        kc = int(ld.indices.size)
-        vc = kc if ld.v_indices is None else int(ld.v_indices.size)
+    for kc, vc, escape in diff._plane_counts():
         n += 5 + 4 * kc + kc * blk + vc * blk
-        if ld.v_indices is not None:
+        if escape:
             n += 4 + 4 * vc
     return n
 
@@ -497,10 +558,7 @@ class DiffStore:
         mirrors_kv = [results[rid].kv for rid, _ in items]
         diffs = encode_batch(master_kv, mirrors_kv, [h for _, h in items], self.blocks)
         if not master_kv.on_device:
-            for diff in diffs:
-                for ld in diff.layers:
-                    ld.k_blocks = to_host(ld.k_blocks)
-                    ld.v_blocks = to_host(ld.v_blocks)
+            diffs = [d.to_host() for d in diffs]
         master = self.register_dense(master_kv, tokens)
         itemsize = 4 if _plane_dtype(master_kv) == torch.float32 else 2
         mirrors, payload, wire, changed = {}, [], [], []
