@@ -108,131 +108,194 @@ class CollectJob:
     delta: np.ndarray
 
 
+def _excl_cumsum(a: np.ndarray) -> np.ndarray:
+    out = np.zeros_like(a)
+    np.cumsum(a[:-1], out=out[1:])
+    return out
+
+
+@dataclass
+class HostPlan:
+    """Host half of a CollectPlan (pure numpy; what gets uploaded)."""
+
+    units: np.ndarray            # COLLECT_UNIT records
+    jobs: np.ndarray             # COLLECT_JOB records (segment-sorted)
+    dst_rows: np.ndarray         # int64, job-major
+    deltas: np.ndarray           # int64, one per cos/sin table row
+    rotate: bool
+    rows_written: int
+    master_rows: int
+
+
+def plan_host(seg_row0: np.ndarray, seg_len: np.ndarray, segments: np.ndarray,
+              dst_rows: np.ndarray, deltas: np.ndarray, num_layers: int, tile_rows: int,
+              target_items: int = 4 * _SMS * 3) -> HostPlan:
+    """Vectorized round planning.  ``segments`` (J,) names each job's
+    segment; ``dst_rows``/``deltas`` are the jobs' per-token rows and deltas
+    concatenated in job order (job j covers seg_len[segments[j]] tokens)."""
+    segments = np.asarray(segments, np.int64)
+    dst_rows = np.asarray(dst_rows, np.int64)
+    deltas = np.asarray(deltas, np.int64)
+    J = segments.size
+    if J == 0:
+        return HostPlan(np.zeros(0, _lib.COLLECT_UNIT), np.zeros(0, _lib.COLLECT_JOB),
+                        np.zeros(0, np.int64), np.zeros(0, np.int64), False, 0, 0)
+    lens = np.asarray(seg_len, np.int64)[segments]
+    total = int(lens.sum())
+    if dst_rows.shape != (total,) or deltas.shape != (total,):
+        raise ValueError("job rows/deltas must cover the whole segment")
+    if (lens <= 0).any():
+        raise ValueError("segments must be non-empty")
+    order = np.argsort(segments, kind="stable")
+    lens_o = lens[order]
+    src_off = _excl_cumsum(lens)[order]
+    dst_off = _excl_cumsum(lens_o)
+    gather = np.repeat(src_off - dst_off, lens_o) + np.arange(total)
+    dst_o = dst_rows[gather]
+    delta_o = deltas[gather]
+    const = np.minimum.reduceat(delta_o, dst_off) == np.maximum.reduceat(delta_o, dst_off)
+    tbl_count = np.where(const, 1, lens_o)
+    tbl_row = _excl_cumsum(tbl_count)
+    keep = np.repeat(~const, lens_o)
+    keep[dst_off] = True
+    seg_o = segments[order]
+    jobs = np.zeros(J, dtype=_lib.COLLECT_JOB)
+    jobs["dst_off"] = dst_off
+    jobs["seg_row0"] = np.asarray(seg_row0, np.int64)[seg_o]
+    jobs["tbl_row"] = tbl_row
+    jobs["tbl_stride"] = (~const).astype(np.int32)
+
+    # (tile, job-chunk) units: enough independent (layer, tile, chunk) items
+    # to fill every SM, without re-reading master tiles more than needed
+    useg, first, njobs = np.unique(seg_o, return_index=True, return_counts=True)
+    n_s = np.asarray(seg_len, np.int64)[useg]
+    r0_s = np.asarray(seg_row0, np.int64)[useg]
+    nt = (n_s + tile_rows - 1) // tile_rows                 # tiles per segment
+    tile_seg = np.repeat(np.arange(useg.size), nt)
+    tile_i = np.arange(int(nt.sum())) - np.repeat(_excl_cumsum(nt), nt)
+    base_items = max(1, num_layers * tile_seg.size)
+    nchunk = min(int(njobs.max()), max(1, math.ceil(target_items / base_items)))
+    per = np.maximum(1, -(-njobs // nchunk))                # jobs per chunk, per segment
+    nc = -(-njobs // per)                                   # chunks per segment
+    nc_t = nc[tile_seg]
+    unit_tile = np.repeat(np.arange(tile_seg.size), nc_t)
+    unit_c = np.arange(int(nc_t.sum())) - np.repeat(_excl_cumsum(nc_t), nc_t)
+    us = tile_seg[unit_tile]
+    units = np.zeros(unit_tile.size, dtype=_lib.COLLECT_UNIT)
+    units["row0"] = r0_s[us] + tile_i[unit_tile] * tile_rows
+    units["nrows"] = np.minimum(tile_rows, n_s[us] - tile_i[unit_tile] * tile_rows)
+    jb = first[us] + unit_c * per[us]
+    units["job_begin"] = jb
+    units["job_end"] = np.minimum(jb + per[us], first[us] + njobs[us])
+    return HostPlan(units, jobs, dst_o, delta_o[keep], bool(delta_o.any()), total,
+                    int(n_s.sum()))
+
+
 class CollectPlan:
     """A round's collector work, planned once and resident on the device.
 
-    Jobs are grouped by segment (input order kept within a segment); every
-    job with a constant delta shares one cos/sin row, otherwise it gets one
-    row per token.  Master tiles of ``tile_rows`` rows pair with job chunks
-    so a launch has enough independent (layer, tile, chunk) items to fill
-    all SMs.
+    Jobs are grouped by segment (input order kept within a segment); a job
+    with a constant delta gets one cos/sin row, otherwise one per token.
+    Master tiles of ``tile_rows`` rows pair with job chunks so a launch has
+    enough independent (layer, tile, chunk) items to fill all SMs.
     """
 
     def __init__(self, arena: MasterArena, jobs: Sequence[CollectJob], rope_base: float,
                  tile_rows: Optional[int] = None, device: Optional[torch.device] = None) -> None:
+        segs = np.array([int(j.segment) for j in jobs], np.int64)
+        for j in jobs:
+            n = int(arena.seg_len[int(j.segment)])
+            if np.shape(j.dst_rows) != (n,) or np.shape(j.delta) != (n,):
+                raise ValueError("job rows/deltas must cover the whole segment")
+        dst = (np.concatenate([np.asarray(j.dst_rows, np.int64) for j in jobs]) if jobs
+               else np.zeros(0, np.int64))
+        dl = (np.concatenate([np.asarray(j.delta, np.int64) for j in jobs]) if jobs
+              else np.zeros(0, np.int64))
+        self._setup(arena, segs, dst, dl, rope_base, tile_rows, device)
+
+    @classmethod
+    def from_arrays(cls, arena: MasterArena, segments: np.ndarray, dst_rows: np.ndarray,
+                    deltas: np.ndarray, rope_base: float, tile_rows: Optional[int] = None,
+                    device: Optional[torch.device] = None) -> "CollectPlan":
+        """Plan from concatenated per-job arrays (no per-job Python objects)."""
+        self = cls.__new__(cls)
+        self._setup(arena, segments, dst_rows, deltas, rope_base, tile_rows, device)
+        return self
+
+    def _setup(self, arena, segments, dst_rows, deltas, rope_base, tile_rows, device) -> None:
         self.device = device or arena.k.device
-        self.arena_rows = int(arena.k.shape[1])
         self.num_layers = arena.num_layers
         self.num_heads = int(arena.k.shape[2])
         self.head_dim = int(arena.k.shape[3])
         self.kv_dtype = arena.k.dtype
         self.rope_base = float(rope_base)
-        self.num_jobs = len(jobs)
-        row_elems = self.num_heads * self.head_dim
-        row_bytes = row_elems * arena.k.element_size()
+        row_bytes = self.num_heads * self.head_dim * arena.k.element_size()
         self.tile_rows = tile_rows or pick_tile_rows(row_bytes)
-
-        order = sorted(range(len(jobs)), key=lambda i: jobs[i].segment)
-        jrec = np.zeros(len(jobs), dtype=_lib.COLLECT_JOB)
-        dst_parts, delta_parts = [], []
-        dst_off = 0
-        tbl_rows = 0
-        rotate = False
-        self.rows_written = 0
-        seg_jobs = {}
-        for slot, ji in enumerate(order):
-            job = jobs[ji]
-            s = int(job.segment)
-            n = int(arena.seg_len[s])
-            dst = np.asarray(job.dst_rows, np.int64)
-            delta = np.asarray(job.delta, np.int64)
-            if dst.shape != (n,) or delta.shape != (n,):
-                raise ValueError("job rows/deltas must cover the whole segment")
-            const = bool(n == 0 or (delta == delta[0]).all())
-            jrec[slot] = (dst_off, int(arena.seg_row0[s]), tbl_rows, 0 if const else 1, 0)
-            delta_parts.append(delta[:1] if const else delta)
-            tbl_rows += 1 if const else n
-            rotate |= bool(delta.any())
-            dst_parts.append(dst)
-            dst_off += n
-            self.rows_written += n
-            seg_jobs.setdefault(s, []).append(slot)
-        self.rotate = rotate
-
-        # (tile, job-chunk) units
-        tiles = []
-        for s in sorted(seg_jobs):
-            r0, n = int(arena.seg_row0[s]), int(arena.seg_len[s])
-            for t0 in range(0, n, self.tile_rows):
-                tiles.append((s, r0 + t0, min(self.tile_rows, n - t0)))
-        base_items = max(1, self.num_layers * len(tiles))
-        want = 4 * _SMS * 3
-        max_jobs = max((len(v) for v in seg_jobs.values()), default=1)
-        nchunk = min(max_jobs, max(1, math.ceil(want / base_items)))
-        units = []
-        for s, row0, nrows in tiles:
-            slots = seg_jobs[s]
-            per = max(1, math.ceil(len(slots) / nchunk))
-            for c0 in range(0, len(slots), per):
-                units.append((row0, nrows, slots[0] + c0, slots[0] + min(c0 + per, len(slots))))
-        self.units_host = np.array(units, dtype=_lib.COLLECT_UNIT)
-        self.jobs_host = jrec
-        self.dst_rows_host = (np.concatenate(dst_parts) if dst_parts
-                              else np.empty(0, np.int64))
-        self.deltas_host = (np.concatenate(delta_parts) if delta_parts
-                            else np.empty(0, np.int64))
+        host = plan_host(arena.seg_row0, arena.seg_len, segments, dst_rows, deltas,
+                         self.num_layers, self.tile_rows)
+        self.host = host
+        self.num_jobs = int(host.jobs.size)
+        self.rotate = host.rotate
+        self.rows_written = host.rows_written
+        self.units_host = host.units
         # device residency
-        self.d_units = upload(self.units_host, self.device)
-        self.d_jobs = upload(self.jobs_host, self.device)
-        self.d_dst_rows = torch.from_numpy(self.dst_rows_host).to(self.device)
-        self.d_deltas = torch.from_numpy(self.deltas_host).to(self.device)
-        self.table = torch.empty((max(tbl_rows, 1), self.head_dim // 2, 2),
+        self.d_units = upload(host.units, self.device)
+        self.d_jobs = upload(host.jobs, self.device)
+        self.d_dst_rows = torch.from_numpy(host.dst_rows).to(self.device)
+        self.d_deltas = torch.from_numpy(host.deltas).to(self.device)
+        self.table = torch.empty((max(host.deltas.size, 1), self.head_dim // 2, 2),
                                  dtype=torch.float64 if self.kv_dtype == torch.float32
                                  else torch.float32, device=self.device)
 
     @property
     def h2d_bytes(self) -> int:
-        return (self.units_host.nbytes + self.jobs_host.nbytes + self.dst_rows_host.nbytes
-                + self.deltas_host.nbytes)
+        h = self.host
+        return h.units.nbytes + h.jobs.nbytes + h.dst_rows.nbytes + h.deltas.nbytes
 
     def algorithmic_bytes(self, with_v: bool = True) -> int:
         """Master read once + every job's rows written (M + N*M)."""
         planes = 2 if with_v else 1
         row = self.num_heads * self.head_dim * torch.tensor([], dtype=self.kv_dtype).element_size()
-        return planes * row * self.num_layers * (self._master_rows() + self.rows_written)
+        return planes * row * self.num_layers * (self.host.master_rows + self.rows_written)
 
-    def _master_rows(self) -> int:
-        # rows of the arena that some job reads (each tile counted once)
-        seen = set()
-        total = 0
-        for u in self.units_host:
-            key = (int(u["row0"]), int(u["nrows"]))
-            if key not in seen:
-                seen.add(key)
-                total += key[1]
-        return total
+    def launch_table(self) -> int:
+        """K0: this round's cos/sin rows."""
+        if not (self.rotate and self.num_jobs):
+            return 0
+        _kernels.rope_table_from_device(self.d_deltas, self.head_dim, self.rope_base,
+                                        self.kv_dtype, self.table)
+        return 1
 
-    def launch(self, arena: MasterArena, dst_k: torch.Tensor, dst_v: Optional[torch.Tensor],
-               dst_layer_stride: int, grid_limit: int = 0) -> int:
-        """K0 (this round's cos/sin rows) + K1; returns the kernels launched."""
+    def launch_collect(self, arena: MasterArena, dst_k: torch.Tensor,
+                       dst_v: Optional[torch.Tensor], dst_layer_stride: int,
+                       layers: Optional[tuple] = None, grid_limit: int = 0) -> int:
+        """K1 over all layers or the layer range ``layers = (l0, l1)``."""
         if arena.k.dtype != self.kv_dtype or dst_k.dtype != self.kv_dtype:
             raise ValueError("arena, destination and plan dtypes differ")
         if self.num_jobs == 0:
             return 0
-        launched = 0
-        if self.rotate:
-            _kernels.rope_table_from_device(self.d_deltas, self.head_dim, self.rope_base,
-                                            self.kv_dtype, self.table)
-            launched += 1
+        l0, l1 = layers if layers is not None else (0, self.num_layers)
+        if not 0 <= l0 < l1 <= self.num_layers:
+            raise ValueError("layer range out of bounds")
+        esz = arena.k.element_size()
+        a_off = l0 * arena.layer_stride * esz
+        d_off = l0 * int(dst_layer_stride) * esz
         with_v = dst_v is not None
-        _lib.call("tdkv_collect", ptr(arena.k), ptr(arena.v) if with_v else 0,
+        _lib.call("tdkv_collect", ptr(arena.k) + a_off, ptr(arena.v) + a_off if with_v else 0,
                   arena.layer_stride, ptr(self.d_units), int(self.units_host.size),
                   self.tile_rows, ptr(self.d_jobs), ptr(self.d_dst_rows),
-                  ptr(self.table) if self.rotate else 0, int(self.rotate), ptr(dst_k),
-                  ptr(dst_v) if with_v else 0, int(dst_layer_stride), self.num_layers,
+                  ptr(self.table) if self.rotate else 0, int(self.rotate), ptr(dst_k) + d_off,
+                  ptr(dst_v) + d_off if with_v else 0, int(dst_layer_stride), l1 - l0,
                   self.num_heads, self.head_dim, dtype_code(self.kv_dtype), int(grid_limit),
                   stream_handle(self.device))
-        return launched + 1
+        return 1
+
+    def launch(self, arena: MasterArena, dst_k: torch.Tensor, dst_v: Optional[torch.Tensor],
+               dst_layer_stride: int, grid_limit: int = 0) -> int:
+        """K0 + K1 over every layer; returns the kernels launched."""
+        n = self.launch_table()
+        return n + self.launch_collect(arena, dst_k, dst_v, dst_layer_stride,
+                                       grid_limit=grid_limit)
 
 
 class KVCollector:
@@ -265,12 +328,48 @@ class KVCollector:
                                        np.asarray(hit.delta, np.int64)))
         return self.plan(jobs)
 
+    def plan_arrays(self, segments, dst_rows, deltas) -> CollectPlan:
+        return CollectPlan.from_arrays(self.arena, segments, dst_rows, deltas, self.rope_base,
+                                       self.tile_rows, self.pool.device)
+
     def collect(self, plan: CollectPlan, ledger: Optional[CostLedger] = None,
                 grid_limit: int = 0) -> int:
         n = plan.launch(self.arena, self.pool.k, self.pool.v, self.pool.layer_stride,
                         grid_limit)
         if ledger is not None and plan.num_jobs:
             for layer in range(plan.num_layers):
+                ledger.record_rope_call(layer)
+        return n
+
+    def collect_from_host(self, plan: CollectPlan, host_k: torch.Tensor, host_v: torch.Tensor,
+                          chunks: int = 4, copy_stream: Optional[torch.cuda.Stream] = None,
+                          ledger: Optional[CostLedger] = None) -> int:
+        """Collect a round whose master blocks arrive from (pinned) host
+        memory: the arena is filled layer-chunk by layer-chunk on a copy
+        stream while K1 runs on the chunks that have landed, so the PCIe
+        transfer overlaps the HBM-bound collector."""
+        arena = self.arena
+        L = arena.num_layers
+        cur = torch.cuda.current_stream(self.pool.device)
+        copy_stream = copy_stream or torch.cuda.Stream(self.pool.device)
+        bounds = [round(i * L / chunks) for i in range(chunks + 1)]
+        copy_stream.wait_stream(cur)             # arena reuse after the previous round
+        events = []
+        with torch.cuda.stream(copy_stream):
+            for l0, l1 in zip(bounds[:-1], bounds[1:]):
+                if l1 > l0:
+                    arena.k[l0:l1].copy_(host_k[l0:l1], non_blocking=True)
+                    arena.v[l0:l1].copy_(host_v[l0:l1], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(copy_stream)
+                    events.append((l0, l1, ev))
+        n = plan.launch_table()
+        for l0, l1, ev in events:
+            cur.wait_event(ev)
+            n += plan.launch_collect(arena, self.pool.k, self.pool.v, self.pool.layer_stride,
+                                     layers=(l0, l1))
+        if ledger is not None and plan.num_jobs:
+            for layer in range(L):
                 ledger.record_rope_call(layer)
         return n
 

@@ -1,0 +1,59 @@
+"""Agent sharding across GPUs.
+
+One process per GPU (``torch.distributed``, NCCL over NVLink on the B200
+box, gloo for the CPU tests).  Agents are independent for the collector and
+for mirror encoding, so each rank owns a contiguous agent range; the round
+has two exchange steps:
+
+* ``broadcast_arena`` -- the shared master blocks, once per round, from the
+  rank that holds them (NCCL broadcast; every rank then runs K0 + K1 for its
+  own agents);
+* ``elect_master`` -- an all-gather of every rank's (deviation, request id)
+  pairs so all ranks elect the same family master,
+  argmin over (score, id) exactly as collective.select_master
+  (collective.py:117-121).
+"""
+from __future__ import annotations
+
+from typing import Dict, Optional
+
+import torch
+import torch.distributed as dist
+
+
+def shard_range(num_agents: int, rank: int, world: int) -> range:
+    """Contiguous agent ids of ``rank`` (the last ranks may get fewer)."""
+    per = (num_agents + world - 1) // world
+    lo = min(num_agents, rank * per)
+    return range(lo, min(num_agents, lo + per))
+
+
+def broadcast_arena(arena, src: int = 0, group=None) -> int:
+    """Broadcast the master arena's K and V planes from ``src``; returns the
+    bytes each receiver gets."""
+    dist.broadcast(arena.k, src, group=group)
+    dist.broadcast(arena.v, src, group=group)
+    return 2 * arena.k.numel() * arena.k.element_size()
+
+
+def elect_master(local_scores: Dict[int, float], group=None,
+                 device: Optional[torch.device] = None) -> int:
+    """Global family master over every rank's members: lowest deviation,
+    ties to the lowest request id."""
+    world = dist.get_world_size(group)
+    device = device or (torch.device("cuda", torch.cuda.current_device())
+                        if dist.get_backend(group) == "nccl" else torch.device("cpu"))
+    n_local = torch.tensor([len(local_scores)], dtype=torch.int64, device=device)
+    counts = [torch.zeros_like(n_local) for _ in range(world)]
+    dist.all_gather(counts, n_local, group=group)
+    width = int(max(c.item() for c in counts))
+    if width == 0:
+        raise ValueError("cannot elect a master from an empty group")
+    buf = torch.full((width, 2), float("inf"), dtype=torch.float64, device=device)
+    for i, (rid, score) in enumerate(sorted(local_scores.items())):
+        buf[i, 0] = float(score)
+        buf[i, 1] = float(rid)
+    parts = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf, group=group)
+    pairs = [(float(s), int(r)) for part in parts for s, r in part.tolist() if s != float("inf")]
+    return min(pairs)[1]
