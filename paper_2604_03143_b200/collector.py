@@ -18,6 +18,7 @@ copies it into the pool later (trace.py:148-152); both forms are provided:
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 from typing import List, Optional, Sequence
 
@@ -31,7 +32,7 @@ from .core import LayeredKv
 from .ledger import CostLedger
 
 # smem budget per CTA for the double-buffered K+V master tile (3 CTAs / SM)
-_TILE_SMEM = 72 * 1024
+_TILE_SMEM = int(os.environ.get("TDKV_TILE_SMEM", 64 * 1024))
 _SMS = 148
 
 

@@ -57,6 +57,13 @@ struct CollectParams {
     int32_t row_elems;
 };
 
+// Per-job destination metadata is staged in shared memory in groups of
+// kJobGroup jobs with cp.async (double-buffered), so the scatter loop never
+// waits on a dependent global load; each thread's cos/sin values are
+// prefetched one job ahead in registers.
+constexpr int kJobGroup = 8;
+constexpr int kMaxTileRows = 32;
+
 template <typename T, int UB, bool BULK>
 __global__ void __launch_bounds__(256) collect_kernel(const CollectParams p) {
     using V = typename UnitBits<UB>::V;
@@ -66,6 +73,8 @@ __global__ void __launch_bounds__(256) collect_kernel(const CollectParams p) {
 
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ __align__(8) uint64_t bars[2];
+    __shared__ __align__(16) int64_t s_drow[2][kJobGroup * kMaxTileRows];
+    __shared__ int4 s_meta[2][kJobGroup];          // tbl_row, tbl_stride, i0
 
     const int tid = threadIdx.x;
     const int nthr = blockDim.x;
@@ -80,6 +89,7 @@ __global__ void __launch_bounds__(256) collect_kernel(const CollectParams p) {
     const Tbl* __restrict__ table = static_cast<const Tbl*>(p.table);
     const int half = p.head_dim >> 1;
     const bool has_v = p.dv != nullptr;            // K-only collect (align_cached)
+    const bool rotate = p.rotate != 0;
 
     if constexpr (BULK) {
         if (tid == 0) {
@@ -98,6 +108,28 @@ __global__ void __launch_bounds__(256) collect_kernel(const CollectParams p) {
         const size_t off = (size_t)layer * p.mls + (size_t)u.row0 * p.row_elems;
         gk = static_cast<const T*>(p.mk) + off;
         gv = static_cast<const T*>(p.mv) + off;
+    };
+    auto stage_meta = [&](const tdkv_collect_unit& u, int g, int mb) {
+        const int jbase = u.job_begin + g * kJobGroup;
+        const int ng = min(kJobGroup, u.job_end - jbase);
+        const int cnt = ng * u.nrows;
+        for (int idx = tid; idx < cnt; idx += nthr) {
+            const int jj = idx / u.nrows;
+            const int r = idx - jj * u.nrows;
+            const tdkv_collect_job* jp = p.jobs + jbase + jj;
+            const int64_t off = jp->dst_off + (u.row0 - jp->seg_row0) + r;
+            cp_async_8(&s_drow[mb][jj * kMaxTileRows + r], p.dst_rows + off);
+        }
+        if (tid < ng) {
+            const tdkv_collect_job jb = p.jobs[jbase + tid];
+            s_meta[mb][tid] = make_int4(jb.tbl_row, jb.tbl_stride, u.row0 - jb.seg_row0, 0);
+        }
+        cp_async_commit();
+    };
+    auto load_cs = [&](Tbl* cs, int tbl_row, int j0) {
+        const Tbl* trow = table + (size_t)tbl_row * half + j0;
+#pragma unroll
+        for (int q = 0; q < kPairs; ++q) cs[q] = __ldg(trow + q);
     };
 
     int item = blockIdx.x;
@@ -118,6 +150,7 @@ __global__ void __launch_bounds__(256) collect_kernel(const CollectParams p) {
         uint8_t* buf = smem + (size_t)b * 2 * tile_bytes;
         const int layer = item / p.n_units;
         const tdkv_collect_unit u = p.units[item - layer * p.n_units];
+        stage_meta(u, 0, 0);
 
         if constexpr (BULK) {
             const int next = item + gridDim.x;
@@ -148,50 +181,58 @@ __global__ void __launch_bounds__(256) collect_kernel(const CollectParams p) {
                 dk32[w] = sk32[w];
                 if (has_v) dv32[w] = sv32[w];
             }
-            __syncthreads();
         }
 
         const V* sk = reinterpret_cast<const V*>(buf);
         const V* sv = reinterpret_cast<const V*>(buf + tile_bytes);
         T* dk_l = static_cast<T*>(p.dk) + (size_t)layer * p.dls;
         T* dv_l = static_cast<T*>(p.dv) + (size_t)layer * p.dls;
+        const int ngroups = (u.job_end - u.job_begin + kJobGroup - 1) / kJobGroup;
 
-        if (ty < rows_per_pass) {
-            for (int j = u.job_begin; j < u.job_end; ++j) {
-                const tdkv_collect_job job = p.jobs[j];
-                const int i0 = u.row0 - job.seg_row0;
-                const int64_t* __restrict__ drows = p.dst_rows + job.dst_off + i0;
+        for (int g = 0; g < ngroups; ++g) {
+            const int mb = g & 1;
+            if (g + 1 < ngroups) {
+                stage_meta(u, g + 1, mb ^ 1);
+                cp_async_wait<1>();
+            } else {
+                cp_async_wait<0>();
+            }
+            __syncthreads();
+            const int ng = min(kJobGroup, u.job_end - u.job_begin - g * kJobGroup);
+            if (ty < rows_per_pass) {
                 for (int c = tx; c < upr; c += tx_n) {
                     const int j0 = ((c * kEpu) % p.head_dim) >> 1;
-                    Tbl cs[kPairs];
-                    if (p.rotate && job.tbl_stride == 0) {
-                        const Tbl* trow = table + (size_t)job.tbl_row * half + j0;
+                    Tbl cs[kPairs], csn[kPairs];
+                    int4 m = s_meta[mb][0];
+                    if (rotate && m.y == 0) load_cs(cs, m.x, j0);
+                    for (int jj = 0; jj < ng; ++jj) {
+                        const int4 mn = jj + 1 < ng ? s_meta[mb][jj + 1] : m;
+                        if (rotate && jj + 1 < ng && mn.y == 0) load_cs(csn, mn.x, j0);
+                        const int64_t* dr = &s_drow[mb][jj * kMaxTileRows];
+                        for (int r = ty; r < u.nrows; r += rows_per_pass) {
+                            const int64_t drow = dr[r];
+                            V kv = sk[r * upr + c];
+                            if (rotate) {
+                                if (m.y != 0) load_cs(cs, m.x + (m.z + r) * m.y, j0);
+                                T* e = reinterpret_cast<T*>(&kv);
 #pragma unroll
-                        for (int q = 0; q < kPairs; ++q) cs[q] = trow[q];
-                    }
-                    for (int r = ty; r < u.nrows; r += rows_per_pass) {
-                        const int64_t drow = __ldg(drows + r);
-                        V kv = sk[r * upr + c];
-                        if (p.rotate) {
-                            if (job.tbl_stride != 0) {
-                                const Tbl* trow =
-                                    table + (size_t)(job.tbl_row + (i0 + r) * job.tbl_stride) * half + j0;
-#pragma unroll
-                                for (int q = 0; q < kPairs; ++q) cs[q] = trow[q];
+                                for (int q = 0; q < kPairs; ++q)
+                                    rot_pair(e[2 * q], e[2 * q + 1], cs[q]);
                             }
-                            T* e = reinterpret_cast<T*>(&kv);
-#pragma unroll
-                            for (int q = 0; q < kPairs; ++q) rot_pair(e[2 * q], e[2 * q + 1], cs[q]);
+                            st_stream(reinterpret_cast<V*>(dk_l + (size_t)drow * p.row_elems) + c,
+                                      kv);
+                            if (has_v)
+                                st_stream(reinterpret_cast<V*>(dv_l + (size_t)drow * p.row_elems) + c,
+                                          sv[r * upr + c]);
                         }
-                        st_stream(reinterpret_cast<V*>(dk_l + (size_t)drow * p.row_elems) + c, kv);
-                        if (has_v)
-                            st_stream(reinterpret_cast<V*>(dv_l + (size_t)drow * p.row_elems) + c,
-                                      sv[r * upr + c]);
+                        m = mn;
+#pragma unroll
+                        for (int q = 0; q < kPairs; ++q) cs[q] = csn[q];
                     }
                 }
             }
+            __syncthreads();
         }
-        __syncthreads();
     }
 }
 
@@ -257,7 +298,8 @@ extern "C" int32_t tdkv_collect(const void* d_master_k, const void* d_master_v,
         return set_error(TDKV_EINVAL, "tdkv_collect: bad geometry L=%d H=%d D=%d", num_layers,
                          num_heads, head_dim);
     if (n_units == 0) return TDKV_OK;
-    if (max_rows <= 0) return set_error(TDKV_EINVAL, "tdkv_collect: max_rows must be positive");
+    if (max_rows <= 0 || max_rows > kMaxTileRows)
+        return set_error(TDKV_EINVAL, "tdkv_collect: max_rows must be in [1, %d]", kMaxTileRows);
     if (!d_master_k || !d_units || !d_jobs || !d_dst_rows || !d_dst_k || (rotate && !d_table) ||
         ((d_dst_v == nullptr) != (d_master_v == nullptr)))
         return set_error(TDKV_EINVAL, "tdkv_collect: null pointer");
