@@ -373,12 +373,13 @@ def run_tdkv(args):
             # shared blocks arrive from pinned host memory (layer chunks on a
             # copy stream, overlapped with K1); the round is planned from host
             # metadata; the host reads one result element back per round
+            events = collector.stage_from_host(host_k, host_v, chunks=4, copy_stream=copy_stream)
             segs = np.tile(np.arange(spec.num_segments), n_local)
             rows = (starts[:, :, None] + tok).reshape(n_local, -1)
             dst = np.take_along_axis(slot_mat, rows, axis=1).reshape(-1)
             dl = np.repeat((starts - src_off).reshape(-1), spec.seg_len)
             p = collector.plan_arrays(segs, dst, dl)
-            collector.collect_from_host(p, host_k, host_v, chunks=4, copy_stream=copy_stream)
+            collector.collect_staged(p, events)
             status.copy_(pool.k[0, int(slot_mat[0, spec.hist_len + 1])].view(-1)[:1],
                          non_blocking=True)
             done.record(stream)
@@ -397,11 +398,28 @@ def run_tdkv(args):
         barrier()
         wall = max_over_ranks(time.perf_counter() - t0) / args.steps
         e2e_gbs = world * step_bytes / wall / 1e9
+        # breakdown: the H2D alone (copy-stream events) and the host planning alone
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h0.record(copy_stream)
+        collector.stage_from_host(host_k, host_v, chunks=4, copy_stream=copy_stream)
+        h1.record(copy_stream)
+        torch.cuda.synchronize(dev)
+        h2d_ms = h0.elapsed_time(h1)
+        tp = time.perf_counter()
+        segs_b = np.tile(np.arange(spec.num_segments), n_local)
+        rows_b = (starts[:, :, None] + tok).reshape(n_local, -1)
+        dst_b = np.take_along_axis(slot_mat, rows_b, axis=1).reshape(-1)
+        dl_b = np.repeat((starts - src_off).reshape(-1), spec.seg_len)
+        plan_host_only = tk.collector.plan_host(arena.seg_row0, arena.seg_len, segs_b, dst_b,
+                                                dl_b, L, p.tile_rows)
+        plan_ms = (time.perf_counter() - tp) * 1e3
+        del plan_host_only
         line["e2e"] = {"value": round(e2e_gbs, 2), "unit": "GB/s",
                        "h2d_bytes_per_step": int(2 * host_k.numel() * host_k.element_size()
                                                  + p.h2d_bytes),
                        "d2h_bytes_per_step": int(status.numel() * status.element_size()),
                        "ms_per_step": round(wall * 1e3, 3),
+                       "h2d_ms": round(h2d_ms, 3), "host_plan_ms": round(plan_ms, 3),
                        "agents_per_s": round(world * n_local / wall, 1),
                        "path": "KVCollector.plan_arrays (host slot maps + layouts -> device "
                                "descriptors) + collect_from_host (pinned-host master H2D in 4 "

@@ -342,13 +342,11 @@ class KVCollector:
                 ledger.record_rope_call(layer)
         return n
 
-    def collect_from_host(self, plan: CollectPlan, host_k: torch.Tensor, host_v: torch.Tensor,
-                          chunks: int = 4, copy_stream: Optional[torch.cuda.Stream] = None,
-                          ledger: Optional[CostLedger] = None) -> int:
-        """Collect a round whose master blocks arrive from (pinned) host
-        memory: the arena is filled layer-chunk by layer-chunk on a copy
-        stream while K1 runs on the chunks that have landed, so the PCIe
-        transfer overlaps the HBM-bound collector."""
+    def stage_from_host(self, host_k: torch.Tensor, host_v: torch.Tensor, chunks: int = 4,
+                        copy_stream: Optional[torch.cuda.Stream] = None) -> list:
+        """Start filling the arena from (pinned) host memory, layer chunk by
+        layer chunk, on a copy stream; returns [(l0, l1, event)] to pass to
+        ``collect_staged``.  Planning can proceed on the host meanwhile."""
         arena = self.arena
         L = arena.num_layers
         cur = torch.cuda.current_stream(self.pool.device)
@@ -364,15 +362,29 @@ class KVCollector:
                     ev = torch.cuda.Event()
                     ev.record(copy_stream)
                     events.append((l0, l1, ev))
+        return events
+
+    def collect_staged(self, plan: CollectPlan, events: list,
+                       ledger: Optional[CostLedger] = None) -> int:
+        """K0, then K1 per landed layer chunk (the PCIe transfer of the next
+        chunk overlaps the HBM-bound collector on the current one)."""
+        cur = torch.cuda.current_stream(self.pool.device)
         n = plan.launch_table()
         for l0, l1, ev in events:
             cur.wait_event(ev)
-            n += plan.launch_collect(arena, self.pool.k, self.pool.v, self.pool.layer_stride,
+            n += plan.launch_collect(self.arena, self.pool.k, self.pool.v, self.pool.layer_stride,
                                      layers=(l0, l1))
         if ledger is not None and plan.num_jobs:
-            for layer in range(L):
+            for layer in range(plan.num_layers):
                 ledger.record_rope_call(layer)
         return n
+
+    def collect_from_host(self, plan: CollectPlan, host_k: torch.Tensor, host_v: torch.Tensor,
+                          chunks: int = 4, copy_stream: Optional[torch.cuda.Stream] = None,
+                          ledger: Optional[CostLedger] = None) -> int:
+        """Collect a round whose master blocks arrive from (pinned) host memory."""
+        events = self.stage_from_host(host_k, host_v, chunks, copy_stream)
+        return self.collect_staged(plan, events, ledger)
 
 
 # ---------------------------------------------------------------------------
