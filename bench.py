@@ -373,7 +373,7 @@ def run_tdkv(args):
             # shared blocks arrive from pinned host memory (layer chunks on a
             # copy stream, overlapped with K1); the round is planned from host
             # metadata; the host reads one result element back per round
-            events = collector.stage_from_host(host_k, host_v, chunks=4, copy_stream=copy_stream)
+            events = collector.stage_from_host(host_k, host_v, chunks=7, copy_stream=copy_stream)
             segs = np.tile(np.arange(spec.num_segments), n_local)
             rows = (starts[:, :, None] + tok).reshape(n_local, -1)
             dst = np.take_along_axis(slot_mat, rows, axis=1).reshape(-1)
@@ -401,7 +401,7 @@ def run_tdkv(args):
         # breakdown: the H2D alone (copy-stream events) and the host planning alone
         h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         h0.record(copy_stream)
-        collector.stage_from_host(host_k, host_v, chunks=4, copy_stream=copy_stream)
+        collector.stage_from_host(host_k, host_v, chunks=7, copy_stream=copy_stream)
         h1.record(copy_stream)
         torch.cuda.synchronize(dev)
         h2d_ms = h0.elapsed_time(h1)
@@ -422,8 +422,9 @@ def run_tdkv(args):
                        "h2d_ms": round(h2d_ms, 3), "host_plan_ms": round(plan_ms, 3),
                        "agents_per_s": round(world * n_local / wall, 1),
                        "path": "KVCollector.plan_arrays (host slot maps + layouts -> device "
-                               "descriptors) + collect_from_host (pinned-host master H2D in 4 "
-                               "layer chunks overlapped with K1) + synchronous result read"}
+                               "descriptors, pinned async uploads) + stage_from_host (master "
+                               "H2D in 7 layer chunks, issued before planning) + collect_staged "
+                               "(K1 per landed chunk) + synchronous result read"}
 
     # -- codec sub-benchmarks (rank-local) ----------------------------------
     if not args.no_codec and not args.profile:

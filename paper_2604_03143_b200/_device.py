@@ -68,9 +68,19 @@ def to_device(x: ArrayLike, device: Optional[torch.device] = None,
 
 def upload(arr: np.ndarray, device: Optional[torch.device] = None) -> torch.Tensor:
     """Raw bytes of a host array (e.g. a descriptor table) onto the device."""
+    return h2d(np.ascontiguousarray(arr).view(np.uint8).reshape(-1), device)
+
+
+def h2d(arr: np.ndarray, device: Optional[torch.device] = None) -> torch.Tensor:
+    """Host array -> device tensor through pinned staging, asynchronous on the
+    current stream (the caching host allocator keeps the staging buffer alive
+    until the copy has run), so descriptor uploads do not serialize behind
+    bulk pageable copies."""
     device = device or default_device()
-    raw = np.ascontiguousarray(arr).view(np.uint8).reshape(-1)
-    return torch.from_numpy(raw.copy()).to(device)
+    src = torch.from_numpy(np.ascontiguousarray(arr))
+    if src.numel() < 4096:
+        return src.to(device)
+    return src.pin_memory().to(device, non_blocking=True)
 
 
 def ptr(t: Optional[torch.Tensor]) -> int:

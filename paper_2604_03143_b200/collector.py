@@ -26,13 +26,13 @@ import numpy as np
 import torch
 
 from . import _kernels, _lib
-from ._device import (default_device, dtype_code, is_host, ptr, stream_handle, to_device,
+from ._device import (default_device, dtype_code, h2d, is_host, ptr, stream_handle, to_device,
                       to_host, upload)
 from .core import LayeredKv
 from .ledger import CostLedger
 
 # smem budget per CTA for the double-buffered K+V master tile (3 CTAs / SM)
-_TILE_SMEM = int(os.environ.get("TDKV_TILE_SMEM", 64 * 1024))
+_TILE_SMEM = int(os.environ.get("TDKV_TILE_SMEM", 32 * 1024))
 _SMS = 148
 
 
@@ -242,8 +242,8 @@ class CollectPlan:
         # device residency
         self.d_units = upload(host.units, self.device)
         self.d_jobs = upload(host.jobs, self.device)
-        self.d_dst_rows = torch.from_numpy(host.dst_rows).to(self.device)
-        self.d_deltas = torch.from_numpy(host.deltas).to(self.device)
+        self.d_dst_rows = h2d(host.dst_rows, self.device)
+        self.d_deltas = h2d(host.deltas, self.device)
         self.table = torch.empty((max(host.deltas.size, 1), self.head_dim // 2, 2),
                                  dtype=torch.float64 if self.kv_dtype == torch.float32
                                  else torch.float32, device=self.device)
