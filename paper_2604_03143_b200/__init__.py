@@ -8,8 +8,8 @@ kernels in ``libtdkv.so`` (C-ABI: include/tdkv.h); there is no CPU
 fallback -- without the library or a CUDA device the entry points raise.
 """
 from ._lib import TdkvError, TdkvUnavailable, build_library, launch_count
-from .collector import (CollectJob, CollectPlan, KVCollector, MasterArena, align_cached,
-                        skeleton_values)
+from .collector import (CollectJob, CollectPlan, KVCollector, MasterArena, SlotArena,
+                        align_cached, skeleton_values)
 from .core import CacheBlockConfig, LayeredKv, PositionSpan, kv_dense_nbytes
 from .diffstore import (BlockSparseDiff, CompressionStats, DiffStore, FamilyEncoding,
                         HintSoundnessError, LayerDiff, MalformedDiffError, MasterEntry,
@@ -28,7 +28,7 @@ __all__ = [
     "CostLedger", "DiffStore", "FamilyEncoding", "HintSoundnessError", "KVCollector",
     "LayerDiff", "LayeredKv", "MalformedDiffError", "MasterArena", "MasterEntry",
     "MirrorHandle", "OutOfSlotsError", "PagedPool", "PinnedMasterError", "PositionSpan",
-    "SlotMap", "TdkvError", "TdkvUnavailable", "UseAfterFreeError", "align_cached",
+    "SlotArena", "SlotMap", "TdkvError", "TdkvUnavailable", "UseAfterFreeError", "align_cached",
     "build_library", "dense_restore", "deserialize_diff", "diff_decode_dense", "encode_batch",
     "encode_diff", "family_cost_from_ratio", "fused_restore", "fused_restore_many",
     "kv_dense_nbytes", "launch_count", "rope_apply", "rope_recover", "serialize_diff",

@@ -166,8 +166,16 @@ def plan_host(seg_row0: np.ndarray, seg_len: np.ndarray, segments: np.ndarray,
     jobs["tbl_row"] = tbl_row
     jobs["tbl_stride"] = (~const).astype(np.int32)
 
-    # (tile, job-chunk) units: enough independent (layer, tile, chunk) items
-    # to fill every SM, without re-reading master tiles more than needed
+    units, master_rows = _build_units(seg_row0, seg_len, seg_o, num_layers, tile_rows,
+                                      target_items)
+    return HostPlan(units, jobs, dst_o, delta_o[keep], bool(delta_o.any()), total, master_rows)
+
+
+def _build_units(seg_row0, seg_len, seg_o: np.ndarray, num_layers: int, tile_rows: int,
+                 target_items: int):
+    """(tile, job-chunk) units over segment-sorted jobs: enough independent
+    (layer, tile, chunk) items to fill every SM, without re-reading master
+    tiles more than needed."""
     useg, first, njobs = np.unique(seg_o, return_index=True, return_counts=True)
     n_s = np.asarray(seg_len, np.int64)[useg]
     r0_s = np.asarray(seg_row0, np.int64)[useg]
@@ -188,8 +196,45 @@ def plan_host(seg_row0: np.ndarray, seg_len: np.ndarray, segments: np.ndarray,
     jb = first[us] + unit_c * per[us]
     units["job_begin"] = jb
     units["job_end"] = np.minimum(jb + per[us], first[us] + njobs[us])
-    return HostPlan(units, jobs, dst_o, delta_o[keep], bool(delta_o.any()), total,
-                    int(n_s.sum()))
+    return units, int(n_s.sum())
+
+
+def plan_host_offsets(seg_row0: np.ndarray, seg_len: np.ndarray, segments: np.ndarray,
+                      dst_off: np.ndarray, job_delta: np.ndarray, num_layers: int,
+                      tile_rows: int, target_items: int = 4 * _SMS * 3) -> HostPlan:
+    """Planning when every job's destination rows are a contiguous run of a
+    device-resident row table (e.g. the agents' slot maps, see SlotArena):
+    job j's token i lands at rows[dst_off[j] + i] and rotates by the
+    constant ``job_delta[j]``.  Nothing per-token is built or uploaded."""
+    segments = np.asarray(segments, np.int64)
+    J = segments.size
+    if J == 0:
+        return HostPlan(np.zeros(0, _lib.COLLECT_UNIT), np.zeros(0, _lib.COLLECT_JOB),
+                        np.zeros(0, np.int64), np.zeros(0, np.int64), False, 0, 0)
+    order = np.argsort(segments, kind="stable")
+    seg_o = segments[order]
+    job_delta = np.asarray(job_delta, np.int64)[order]
+    jobs = np.zeros(J, dtype=_lib.COLLECT_JOB)
+    jobs["dst_off"] = np.asarray(dst_off, np.int64)[order]
+    jobs["seg_row0"] = np.asarray(seg_row0, np.int64)[seg_o]
+    jobs["tbl_row"] = np.arange(J)
+    units, master_rows = _build_units(seg_row0, seg_len, seg_o, num_layers, tile_rows,
+                                      target_items)
+    total = int(np.asarray(seg_len, np.int64)[segments].sum())
+    return HostPlan(units, jobs, None, job_delta, bool(job_delta.any()), total, master_rows)
+
+
+class SlotArena:
+    """The agents' slot maps concatenated and resident on the device (pool
+    state, uploaded once at admission): a collect job then only names its
+    agent's base row and the target offset of its segment."""
+
+    def __init__(self, slot_maps, device: torch.device) -> None:
+        lens = np.array([len(m) for m in slot_maps], np.int64)
+        self.base = _excl_cumsum(lens)
+        cat = (np.concatenate([np.asarray(m.slots, np.int64) for m in slot_maps])
+               if slot_maps else np.zeros(0, np.int64))
+        self.rows = torch.from_numpy(cat).to(device)
 
 
 class CollectPlan:
@@ -223,7 +268,19 @@ class CollectPlan:
         self._setup(arena, segments, dst_rows, deltas, rope_base, tile_rows, device)
         return self
 
-    def _setup(self, arena, segments, dst_rows, deltas, rope_base, tile_rows, device) -> None:
+    @classmethod
+    def from_offsets(cls, arena: MasterArena, segments: np.ndarray, dst_off: np.ndarray,
+                     job_delta: np.ndarray, rows: torch.Tensor, rope_base: float,
+                     tile_rows: Optional[int] = None) -> "CollectPlan":
+        """Plan against a device-resident row table ``rows`` (SlotArena.rows):
+        job j's token i lands at rows[dst_off[j] + i]; one delta per job."""
+        self = cls.__new__(cls)
+        self._setup(arena, segments, None, None, rope_base, tile_rows, rows.device,
+                    offsets=(dst_off, job_delta, rows))
+        return self
+
+    def _setup(self, arena, segments, dst_rows, deltas, rope_base, tile_rows, device,
+               offsets=None) -> None:
         self.device = device or arena.k.device
         self.num_layers = arena.num_layers
         self.num_heads = int(arena.k.shape[2])
@@ -232,8 +289,12 @@ class CollectPlan:
         self.rope_base = float(rope_base)
         row_bytes = self.num_heads * self.head_dim * arena.k.element_size()
         self.tile_rows = tile_rows or pick_tile_rows(row_bytes)
-        host = plan_host(arena.seg_row0, arena.seg_len, segments, dst_rows, deltas,
-                         self.num_layers, self.tile_rows)
+        if offsets is None:
+            host = plan_host(arena.seg_row0, arena.seg_len, segments, dst_rows, deltas,
+                             self.num_layers, self.tile_rows)
+        else:
+            host = plan_host_offsets(arena.seg_row0, arena.seg_len, segments, offsets[0],
+                                     offsets[1], self.num_layers, self.tile_rows)
         self.host = host
         self.num_jobs = int(host.jobs.size)
         self.rotate = host.rotate
@@ -242,7 +303,7 @@ class CollectPlan:
         # device residency
         self.d_units = upload(host.units, self.device)
         self.d_jobs = upload(host.jobs, self.device)
-        self.d_dst_rows = h2d(host.dst_rows, self.device)
+        self.d_dst_rows = h2d(host.dst_rows, self.device) if offsets is None else offsets[2]
         self.d_deltas = h2d(host.deltas, self.device)
         self.table = torch.empty((max(host.deltas.size, 1), self.head_dim // 2, 2),
                                  dtype=torch.float64 if self.kv_dtype == torch.float32
@@ -251,7 +312,8 @@ class CollectPlan:
     @property
     def h2d_bytes(self) -> int:
         h = self.host
-        return h.units.nbytes + h.jobs.nbytes + h.dst_rows.nbytes + h.deltas.nbytes
+        dst = h.dst_rows.nbytes if h.dst_rows is not None else 0
+        return h.units.nbytes + h.jobs.nbytes + dst + h.deltas.nbytes
 
     def algorithmic_bytes(self, with_v: bool = True) -> int:
         """Master read once + every job's rows written (M + N*M)."""
@@ -328,6 +390,10 @@ class KVCollector:
                 jobs.append(CollectJob(int(segment_of(hit)), slots[np.asarray(hit.target_idx)],
                                        np.asarray(hit.delta, np.int64)))
         return self.plan(jobs)
+
+    def plan_offsets(self, segments, dst_off, job_delta, slot_arena: "SlotArena") -> CollectPlan:
+        return CollectPlan.from_offsets(self.arena, segments, dst_off, job_delta,
+                                        slot_arena.rows, self.rope_base, self.tile_rows)
 
     def plan_arrays(self, segments, dst_rows, deltas) -> CollectPlan:
         return CollectPlan.from_arrays(self.arena, segments, dst_rows, deltas, self.rope_base,

@@ -547,3 +547,34 @@ def test_c2_full_size_collector_and_codec_properties():
         assert max(diff.changed_blocks_per_layer) <= 15
         back = tk.diff_decode_dense(dense[0], diff)
         assert torch.equal(back.k, mir.k) and torch.equal(back.v, mir.v)
+
+
+def test_slot_arena_planning_equals_row_planning():
+    spec = rounds.CONFIGS["c2"].scaled(num_layers=2, num_agents=5, num_segments=4, hist_len=20)
+    mk, mv = rounds.master_planes_host(spec)
+    dt = spec.torch_dtype
+    arena = tk.MasterArena(torch.from_numpy(mk).to(DEV).to(dt), torch.from_numpy(mv).to(DEV).to(dt),
+                           np.arange(spec.num_segments) * spec.seg_len,
+                           np.full(spec.num_segments, spec.seg_len),
+                           [np.arange(spec.seg_len)] * spec.num_segments)
+    T = spec.tokens_per_agent
+    pools = []
+    for mode in ("rows", "offsets"):
+        pool = tk.PagedPool(spec.num_agents * T + 100, spec.num_layers, spec.num_heads,
+                            spec.head_dim, dtype=dt, device=DEV)
+        pool.allocate(37)            # non-trivial slot maps
+        maps = [pool.allocate(T, a) for a in range(spec.num_agents)]
+        col = tk.KVCollector(arena, pool)
+        if mode == "rows":
+            plan = col.plan([j for a in range(spec.num_agents)
+                             for j in rounds.agent_jobs(spec, a, maps[a].slots)])
+        else:
+            sa = tk.SlotArena(maps, DEV)
+            starts = np.stack([rounds.segment_starts(spec, a) for a in range(spec.num_agents)])
+            src = rounds.source_offsets(spec)
+            plan = col.plan_offsets(np.tile(np.arange(spec.num_segments), spec.num_agents),
+                                    (sa.base[:, None] + starts).reshape(-1),
+                                    (starts - src).reshape(-1), sa)
+        col.collect(plan)
+        pools.append((pool.k.clone(), pool.v.clone()))
+    assert torch.equal(pools[0][0], pools[1][0]) and torch.equal(pools[0][1], pools[1][1])
