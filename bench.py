@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--mirror-frac", type=float, default=0.1)
+    ap.add_argument("--codec-mirrors", type=int, default=49, help="mirrors per codec family")
     ap.add_argument("--profile", action="store_true", help="few launches, no extras (for ncu)")
     return ap.parse_args()
 
@@ -267,11 +268,7 @@ def run_tdkv(args):
     host_k = torch.from_numpy(mk_h).to(dt).pin_memory()
     host_v = torch.from_numpy(mv_h).to(dt).pin_memory()
     del mk_h, mv_h
-    src = rounds.source_offsets(spec)
-    arena = tk.MasterArena(host_k.to(dev), host_v.to(dev),
-                           np.arange(spec.num_segments) * spec.seg_len,
-                           np.full(spec.num_segments, spec.seg_len),
-                           [np.arange(p, p + spec.seg_len) for p in src])
+    arena = rounds.make_arena(spec, host_k.to(dev), host_v.to(dev))
     pool = tk.PagedPool(n_local * T, L, H, D, dtype=dt, device=dev, debug=False)
     agents = range(rank * n_local, (rank + 1) * n_local)
     maps = [pool.allocate(T, a) for a in agents]
@@ -363,17 +360,13 @@ def run_tdkv(args):
         # host metadata of the round: each agent's prompt layout (segment
         # start rows); the agents' slot maps are pool state, resident on the
         # device since admission (SlotArena)
-        starts = np.stack([rounds.segment_starts(spec, a) for a in agents])
-        src_off = rounds.source_offsets(spec)
         slot_arena = tk.SlotArena(maps, dev)
         first_slot = int(maps[0].slots[spec.hist_len + 1])
         copy_stream = torch.cuda.Stream(dev)
         done = torch.cuda.Event()
 
         def plan_round():
-            segs = np.tile(np.arange(spec.num_segments), n_local)
-            dst_off = (slot_arena.base[:, None] + starts).reshape(-1)
-            job_delta = (starts - src_off).reshape(-1)
+            segs, dst_off, job_delta = rounds.round_offsets(spec, agents, slot_arena.base)
             return collector.plan_offsets(segs, dst_off, job_delta, slot_arena)
 
         def e2e_step():
@@ -445,7 +438,7 @@ def codec_bench(tk, spec, pool, maps, dev, args, peak):
     bs = 32
     T = spec.tokens_per_agent
     nb = -(-T // bs)
-    n_mirrors = len(maps) - 1
+    n_mirrors = max(1, min(len(maps) - 1, args.codec_mirrors))
     sl0 = maps[0].device_slots(dev)
     mk = pool.k[:, sl0].contiguous()
     mv = pool.v[:, sl0].contiguous()
@@ -483,7 +476,7 @@ def codec_bench(tk, spec, pool, maps, dev, args, peak):
     fam = tk.MasterEntry(0, master, pin_count=n_mirrors)
     handles = [tk.MirrorHandle(0, i + 1, fam, d) for i, d in enumerate(diffs)]
     spans = [tk.PositionSpan.shifted(np.arange(T), 16) for _ in handles]
-    tmaps = maps[1:]
+    tmaps = maps[1:1 + n_mirrors]
     for _ in range(2):
         tk.fused_restore_many(handles, spans, pool, tmaps, 10000.0)
     torch.cuda.synchronize(dev)

@@ -16,7 +16,7 @@ from typing import List, Optional, Sequence, Tuple
 import numpy as np
 import torch
 
-from .collector import CollectJob
+from .collector import CollectJob, MasterArena
 
 
 @dataclass(frozen=True)
@@ -31,6 +31,18 @@ class RoundSpec:
     seg_len: int
     hist_len: int
     max_source: int = 8192
+    sessions: int = 1          # independent groups; agents and segments split evenly
+
+    @property
+    def agents_per_session(self) -> int:
+        return -(-self.num_agents // self.sessions)
+
+    @property
+    def total_segments(self) -> int:
+        return self.sessions * self.num_segments
+
+    def session_of(self, agent: int) -> int:
+        return min(self.sessions - 1, agent // self.agents_per_session)
 
     @property
     def tokens_per_agent(self) -> int:
@@ -50,17 +62,25 @@ class RoundSpec:
 
     @property
     def master_rows(self) -> int:
-        return self.num_segments * self.seg_len
+        return self.sessions * self.num_segments * self.seg_len
 
     @property
     def master_bytes(self) -> int:
         """M: K+V bytes of every shared segment master (read once)."""
         return 2 * self.num_layers * self.master_rows * self.row_bytes
 
+    @property
+    def session_master_bytes(self) -> int:
+        return self.master_bytes // self.sessions
+
     def collector_bytes(self, agents: Optional[int] = None) -> int:
-        """Algorithmic collector bytes M + N*M."""
+        """Algorithmic collector bytes: every master of the
+        sessions the first ``agents`` agents belong to, read once, plus each
+        agent's copy of its session's masters, written (M + N*M for one
+        session)."""
         n = self.num_agents if agents is None else agents
-        return self.master_bytes * (1 + n)
+        touched = len({self.session_of(a) for a in range(n)})
+        return self.session_master_bytes * (touched + n)
 
     @property
     def dense_bytes(self) -> int:
@@ -75,13 +95,16 @@ class RoundSpec:
 CONFIGS = {
     "c1": RoundSpec("c1-toy-8x4x256-f32", 2, 8, 64, "f32", 8, 4, 256, 64),
     "c2": RoundSpec("c2-qwen7b-50x16x256-bf16", 28, 4, 128, "bf16", 50, 16, 256, 512),
-    "c3": RoundSpec("c3-qwen14b-25x20x25-bf16", 48, 8, 128, "bf16", 25, 20, 25, 192),
+    "c3": RoundSpec("c3-qwen14b-250x25x20-10sessions-bf16", 48, 8, 128, "bf16", 250, 25, 20,
+                    192, sessions=10),
     "c4": RoundSpec("c4-agentsociety-100x32x128-bf16", 28, 4, 128, "bf16", 100, 32, 128, 8192),
 }
 
 
 def source_offsets(spec: RoundSpec) -> np.ndarray:
-    return np.random.default_rng(1).integers(0, spec.max_source, spec.num_segments).astype(np.int64)
+    """Source position of every (global) segment's master."""
+    return np.random.default_rng(1).integers(0, spec.max_source,
+                                             spec.total_segments).astype(np.int64)
 
 
 def agent_order(agent: int, num_segments: int) -> np.ndarray:
@@ -89,7 +112,8 @@ def agent_order(agent: int, num_segments: int) -> np.ndarray:
 
 
 def segment_starts(spec: RoundSpec, agent: int) -> np.ndarray:
-    """Prompt offset of every segment (indexed by segment id) for an agent."""
+    """Prompt offset of each of the agent's session segments (indexed by the
+    segment's index within the session)."""
     order = agent_order(agent, spec.num_segments)
     starts = np.empty(spec.num_segments, np.int64)
     starts[order] = spec.hist_len + 1 + np.arange(spec.num_segments) * (spec.seg_len + 1)
@@ -97,7 +121,7 @@ def segment_starts(spec: RoundSpec, agent: int) -> np.ndarray:
 
 
 def master_planes_host(spec: RoundSpec, seed: int = 0) -> Tuple[np.ndarray, np.ndarray]:
-    """(L, S*len, H, D) float32 masters, segment-major rows."""
+    """(L, sessions*S*len, H, D) float32 masters, rows grouped by global segment."""
     g = torch.Generator().manual_seed(seed)
     shape = (spec.num_layers, spec.master_rows, spec.num_heads, spec.head_dim)
     k = torch.randn(shape, generator=g, dtype=torch.float32)
@@ -105,17 +129,40 @@ def master_planes_host(spec: RoundSpec, seed: int = 0) -> Tuple[np.ndarray, np.n
     return k.numpy(), v.numpy()
 
 
+def make_arena(spec: RoundSpec, k, v) -> MasterArena:
+    """Wrap (L, master_rows, H, D) device planes as the round's master arena."""
+    src = source_offsets(spec)
+    n = spec.total_segments
+    return MasterArena(k, v, np.arange(n) * spec.seg_len, np.full(n, spec.seg_len),
+                       [np.arange(p, p + spec.seg_len) for p in src])
+
+
 def agent_jobs(spec: RoundSpec, agent: int, slots: np.ndarray) -> List[CollectJob]:
     """The collector jobs of one agent: segment s lands at its prompt rows."""
     starts = segment_starts(spec, agent)
     src = source_offsets(spec)
+    base = spec.session_of(agent) * spec.num_segments
     jobs = []
     for s in range(spec.num_segments):
         t0 = int(starts[s])
         dst = slots[t0:t0 + spec.seg_len]
-        delta = np.full(spec.seg_len, t0 - int(src[s]), np.int64)
-        jobs.append(CollectJob(s, dst, delta))
+        g = base + s
+        delta = np.full(spec.seg_len, t0 - int(src[g]), np.int64)
+        jobs.append(CollectJob(g, dst, delta))
     return jobs
+
+
+def round_offsets(spec: RoundSpec, agents, slot_base: np.ndarray):
+    """Vectorized job arrays of a round for ``plan_offsets``: (global segment
+    ids, destination offsets into the agents' slot arena, per-job delta)."""
+    agents = list(agents)
+    starts = np.stack([segment_starts(spec, a) for a in agents])         # (n, S)
+    sess = np.array([spec.session_of(a) for a in agents], np.int64)
+    segs = (sess[:, None] * spec.num_segments + np.arange(spec.num_segments)).reshape(-1)
+    src = source_offsets(spec)
+    dst_off = (np.asarray(slot_base, np.int64)[:, None] + starts).reshape(-1)
+    delta = (starts.reshape(-1) - src[segs])
+    return segs, dst_off, delta
 
 
 def shard(num_agents: int, rank: int, world: int) -> range:

@@ -139,19 +139,18 @@ def test_offset_planning_matches_row_planning():
     from paper_2604_03143_b200.collector import plan_host, plan_host_offsets
     spec = rounds.CONFIGS["c2"].scaled(num_agents=7)
     T = spec.tokens_per_agent
+    spec = spec.scaled(sessions=2)
     starts = np.stack([rounds.segment_starts(spec, a) for a in range(7)])
-    src = rounds.source_offsets(spec)
     slots = np.random.default_rng(0).permutation(7 * T).reshape(7, T)
-    segs = np.tile(np.arange(spec.num_segments), 7)
+    base = np.arange(7) * T
+    segs, dst_off, jd = rounds.round_offsets(spec, range(7), base)
     rows = (starts[:, :, None] + np.arange(spec.seg_len)).reshape(7, -1)
     dst = np.take_along_axis(slots, rows, axis=1).reshape(-1)
-    dl = np.repeat((starts - src).reshape(-1), spec.seg_len)
-    seg_row0 = np.arange(spec.num_segments) * spec.seg_len
-    seg_len = np.full(spec.num_segments, spec.seg_len)
+    dl = np.repeat(jd, spec.seg_len)
+    seg_row0 = np.arange(spec.total_segments) * spec.seg_len
+    seg_len = np.full(spec.total_segments, spec.seg_len)
     a = plan_host(seg_row0, seg_len, segs, dst, dl, spec.num_layers, 8)
-    base = np.arange(7) * T
-    b = plan_host_offsets(seg_row0, seg_len, segs, (base[:, None] + starts).reshape(-1),
-                          (starts - src).reshape(-1), spec.num_layers, 8)
+    b = plan_host_offsets(seg_row0, seg_len, segs, dst_off, jd, spec.num_layers, 8)
     assert np.array_equal(a.units, b.units)
     assert np.array_equal(a.jobs["seg_row0"], b.jobs["seg_row0"])
     assert np.array_equal(a.jobs["tbl_row"], b.jobs["tbl_row"])

@@ -152,11 +152,7 @@ def _collect_case(spec: rounds.RoundSpec, tile_rows=None, seed=0):
     dt = spec.torch_dtype
     arena_k = torch.from_numpy(mk).to(DEV).to(dt)
     arena_v = torch.from_numpy(mv).to(DEV).to(dt)
-    lens = np.full(spec.num_segments, spec.seg_len)
-    row0 = np.arange(spec.num_segments) * spec.seg_len
-    src = rounds.source_offsets(spec)
-    arena = tk.MasterArena(arena_k, arena_v, row0, lens,
-                           [np.arange(p, p + spec.seg_len) for p in src])
+    arena = rounds.make_arena(spec, arena_k, arena_v)
     T = spec.tokens_per_agent
     pool = tk.PagedPool(spec.num_agents * T + 64, spec.num_layers, spec.num_heads, spec.head_dim,
                         dtype=dt, device=DEV)
@@ -202,6 +198,15 @@ def test_collector_bf16_reduced_c2(tile_rows):
     spec = rounds.CONFIGS["c2"].scaled(num_layers=3, num_agents=6, num_segments=5, hist_len=40)
     gk, gv, wk, wv, jobs = _collect_case(spec, tile_rows=tile_rows)
     rows = np.concatenate([j.dst_rows for j in jobs])
+    assert np.array_equal(gv[:, rows], wv[:, rows])
+    assert bf16_close(gk[:, rows], wk[:, rows]) <= 1e-2
+
+
+def test_collector_multi_session_c3_shape():
+    spec = rounds.CONFIGS["c3"].scaled(num_layers=2, num_agents=12, sessions=3, hist_len=17)
+    gk, gv, wk, wv, jobs = _collect_case(spec)
+    rows = np.concatenate([j.dst_rows for j in jobs])
+    assert {j.segment for j in jobs} == set(range(spec.total_segments))
     assert np.array_equal(gv[:, rows], wv[:, rows])
     assert bf16_close(gk[:, rows], wk[:, rows]) <= 1e-2
 
@@ -506,10 +511,8 @@ def test_c2_full_size_collector_and_codec_properties():
     spec = rounds.CONFIGS["c2"].scaled(num_agents=8)
     mk, mv = rounds.master_planes_host(spec)
     dt = spec.torch_dtype
-    arena = tk.MasterArena(torch.from_numpy(mk).to(DEV).to(dt), torch.from_numpy(mv).to(DEV).to(dt),
-                           np.arange(spec.num_segments) * spec.seg_len,
-                           np.full(spec.num_segments, spec.seg_len),
-                           [np.arange(spec.seg_len)] * spec.num_segments)
+    arena = rounds.make_arena(spec, torch.from_numpy(mk).to(DEV).to(dt),
+                              torch.from_numpy(mv).to(DEV).to(dt))
     T = spec.tokens_per_agent
     pool = tk.PagedPool(spec.num_agents * T, spec.num_layers, spec.num_heads, spec.head_dim,
                         dtype=dt, device=DEV)
@@ -553,10 +556,8 @@ def test_slot_arena_planning_equals_row_planning():
     spec = rounds.CONFIGS["c2"].scaled(num_layers=2, num_agents=5, num_segments=4, hist_len=20)
     mk, mv = rounds.master_planes_host(spec)
     dt = spec.torch_dtype
-    arena = tk.MasterArena(torch.from_numpy(mk).to(DEV).to(dt), torch.from_numpy(mv).to(DEV).to(dt),
-                           np.arange(spec.num_segments) * spec.seg_len,
-                           np.full(spec.num_segments, spec.seg_len),
-                           [np.arange(spec.seg_len)] * spec.num_segments)
+    arena = rounds.make_arena(spec, torch.from_numpy(mk).to(DEV).to(dt),
+                              torch.from_numpy(mv).to(DEV).to(dt))
     T = spec.tokens_per_agent
     pools = []
     for mode in ("rows", "offsets"):
@@ -570,11 +571,8 @@ def test_slot_arena_planning_equals_row_planning():
                              for j in rounds.agent_jobs(spec, a, maps[a].slots)])
         else:
             sa = tk.SlotArena(maps, DEV)
-            starts = np.stack([rounds.segment_starts(spec, a) for a in range(spec.num_agents)])
-            src = rounds.source_offsets(spec)
-            plan = col.plan_offsets(np.tile(np.arange(spec.num_segments), spec.num_agents),
-                                    (sa.base[:, None] + starts).reshape(-1),
-                                    (starts - src).reshape(-1), sa)
+            plan = col.plan_offsets(*rounds.round_offsets(spec, range(spec.num_agents), sa.base),
+                                    sa)
         col.collect(plan)
         pools.append((pool.k.clone(), pool.v.clone()))
     assert torch.equal(pools[0][0], pools[1][0]) and torch.equal(pools[0][1], pools[1][1])
