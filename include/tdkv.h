@@ -204,6 +204,32 @@ int32_t tdkv_rows(const tdkv_rows_job* d_jobs, int32_t n_jobs,
                   int32_t block_size, int32_t dtype, int32_t flags,
                   int32_t tile_rows, int32_t grid_limit, void* stream);
 
+/* ------------------------------------------------------------------------
+ * K4  check-layer selection.  Replaces the batched
+ * difference pass of pic.probe_and_select (pic.py:268-281).
+ *
+ * tdkv_keydiff: mags[r] = sqrt(sum_e (fresh[r,e] - cached[row(r),e])^2)
+ * over one token's H*D elements (key_diff, pic.py:166-171); fresh is dense
+ * (n_rows, H*D), cached rows are d_cached_rows[r] (NULL = r), e.g. the pool's
+ * check-layer plane addressed by slots.  float32 difference and product as
+ * numpy, float64 accumulation, float32 result.
+ *
+ * tdkv_select_important: member m owns mags[member_off[m] .. member_off[m+1]);
+ * writes its top min(budget[m], #nonzero) positions by (-mag, index), in
+ * ascending order, to out_idx[member_off[m] ...] (select_important,
+ * pic.py:180-189), their number to out_count[m], and the float32 sum of its
+ * magnitudes to deviation[m] (pic.py:280).  At most 16384 positions per
+ * member.
+ * ---------------------------------------------------------------------- */
+int32_t tdkv_keydiff(const void* d_fresh, const void* d_cached,
+                     const int64_t* d_cached_rows, int64_t n_rows, int32_t row_elems,
+                     int32_t dtype, float* d_mags, void* stream);
+
+int32_t tdkv_select_important(const float* d_mags, const int64_t* d_member_off,
+                              const int32_t* d_budget, int32_t n_members,
+                              int32_t max_count, int32_t* d_out_idx,
+                              int32_t* d_out_count, float* d_deviation, void* stream);
+
 /* Fill rows of every layer with a value (NaN poisoning of freed slots,
  * paged_pool.py:144-147).  value_bits is the element bit pattern. */
 int32_t tdkv_fill_rows(void* d_plane, int64_t layer_stride, int32_t num_layers,

@@ -442,6 +442,25 @@ def mirror_hints(member_entry: np.ndarray, member_offset: np.ndarray,
     return np.union1d(pos, master_important).astype(np.int64)
 
 
+def key_diff(fresh: np.ndarray, cached: np.ndarray) -> np.ndarray:
+    """Per-position L2 norm of the float32 key difference (pic.py:166-171)."""
+    if fresh.shape != cached.shape:
+        raise ValueError("key tensors must have identical shapes")
+    diff = (fresh - cached).reshape(fresh.shape[0], -1)
+    return np.sqrt(np.einsum("te,te->t", diff, diff))
+
+
+def select_important(mags: np.ndarray, budget: int) -> np.ndarray:
+    """Largest magnitudes first, ties to the lower index, zeros excluded,
+    result sorted ascending (pic.py:180-189)."""
+    if mags.size == 0 or budget <= 0:
+        return np.empty(0, dtype=np.int64)
+    idx = np.arange(mags.size)
+    ranked = idx[np.lexsort((idx, -mags))]
+    ranked = ranked[mags[ranked] > 0.0][:budget]
+    return np.sort(ranked).astype(np.int64)
+
+
 def recompute_budget(fraction: float, shared_count: int) -> int:
     """ceil(fraction*shared) with decimal-noise guard (pic.py:174-177)."""
     return int(math.ceil(round(fraction * shared_count, 6)))

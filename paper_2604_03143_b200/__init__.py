@@ -20,6 +20,8 @@ from .ledger import CostLedger
 from .paged_pool import OutOfSlotsError, PagedPool, SlotMap, UseAfterFreeError, slot_maps_disjoint
 from .restore import dense_restore, fused_restore, fused_restore_many
 from .rope import rope_apply, rope_recover
+from .select import (batched_selection, key_diff, mirror_hint_positions, recompute_budget,
+                     select_important, select_master)
 
 __version__ = "0.1.0"
 
@@ -28,7 +30,8 @@ __all__ = [
     "CostLedger", "DiffStore", "FamilyEncoding", "HintSoundnessError", "KVCollector",
     "LayerDiff", "LayeredKv", "MalformedDiffError", "MasterArena", "MasterEntry",
     "MirrorHandle", "OutOfSlotsError", "PagedPool", "PinnedMasterError", "PositionSpan",
-    "SlotArena", "SlotMap", "TdkvError", "TdkvUnavailable", "UseAfterFreeError", "align_cached",
+    "SlotArena", "SlotMap", "TdkvError", "TdkvUnavailable", "UseAfterFreeError", "align_cached", "batched_selection", "key_diff",
+    "mirror_hint_positions", "recompute_budget", "select_important", "select_master",
     "build_library", "dense_restore", "deserialize_diff", "diff_decode_dense", "encode_batch",
     "encode_diff", "family_cost_from_ratio", "fused_restore", "fused_restore_many",
     "kv_dense_nbytes", "launch_count", "rope_apply", "rope_recover", "serialize_diff",

@@ -1,0 +1,146 @@
+"""Check-layer selection and family election (reference: roundkv/pic.py
+166-189, 238-281; collective.py:117-149).
+
+``batched_selection`` is the paper's "one batched difference pass"
+(PAPER.md:337-340): the fresh check-layer keys of every member's reused
+positions are compared with the cached (collector-rotated) keys in one K4
+launch, and every member's important set and deviation score come out of a
+second launch.  The cached rows can be read straight from the paged pool
+(``cached_rows`` = slots at the check layer), so the collector's output is
+never copied.  The fresh keys come from the model's probe forward, which is
+outside this path.
+
+Host helpers keep the reference's exact integer semantics:
+``recompute_budget`` (pic.py:174-177), ``select_master`` (collective.py:
+117-121) and ``mirror_hint_positions`` (collective.py:124-149).
+"""
+from __future__ import annotations
+
+import math
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._device import default_device, dtype_code, h2d, is_host, ptr, stream_handle, to_device
+from .ledger import CostLedger
+
+
+def recompute_budget(fraction: float, shared_count: int) -> int:
+    """ceil(fraction * shared_count) with the reference's decimal-noise guard."""
+    return int(math.ceil(round(fraction * shared_count, 6)))
+
+
+def _mags_device(fresh: torch.Tensor, cached: torch.Tensor,
+                 cached_rows: Optional[torch.Tensor]) -> torch.Tensor:
+    n = int(fresh.shape[0])
+    row = int(np.prod(fresh.shape[1:]))
+    out = torch.empty(n, dtype=torch.float32, device=fresh.device)
+    if n:
+        _lib.call("tdkv_keydiff", ptr(fresh), ptr(cached), ptr(cached_rows), n, row,
+                  dtype_code(fresh.dtype), ptr(out), stream_handle(fresh.device))
+    return out
+
+
+def key_diff(fresh_k, cached_k):
+    """Per-position L2 magnitude of the key difference, shape (T,)."""
+    if tuple(fresh_k.shape) != tuple(cached_k.shape):
+        raise ValueError("key tensors must have identical shapes")
+    host = is_host(fresh_k)
+    dev = fresh_k.device if isinstance(fresh_k, torch.Tensor) else default_device()
+    f = to_device(fresh_k, dev)
+    c = to_device(cached_k, dev, f.dtype)
+    out = _mags_device(f, c, None)
+    return out.cpu().numpy() if host else out
+
+
+def _select_device(mags: torch.Tensor, counts: Sequence[int], budgets: Sequence[int]):
+    counts = np.asarray(counts, np.int64)
+    off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    dev = mags.device
+    d_off = h2d(off, dev)
+    d_budget = h2d(np.asarray(budgets, np.int32), dev)
+    m = counts.size
+    out_idx = torch.empty(max(int(off[-1]), 1), dtype=torch.int32, device=dev)
+    out_cnt = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
+    dev_sum = torch.empty(max(m, 1), dtype=torch.float32, device=dev)
+    if m:
+        _lib.call("tdkv_select_important", ptr(mags), ptr(d_off), ptr(d_budget), m,
+                  int(counts.max(initial=0)), ptr(out_idx), ptr(out_cnt), ptr(dev_sum),
+                  stream_handle(dev))
+    return off, out_idx, out_cnt, dev_sum
+
+
+def select_important(magnitudes, budget: int) -> np.ndarray:
+    """Top-``budget`` magnitudes (largest first, ties to the lower index,
+    zeros never taken), returned as sorted int64 indices."""
+    n = int(magnitudes.shape[0])
+    if n == 0 or budget <= 0:
+        return np.empty(0, dtype=np.int64)
+    dev = magnitudes.device if isinstance(magnitudes, torch.Tensor) else default_device()
+    mags = to_device(magnitudes, dev, torch.float32)
+    _, idx, cnt, _ = _select_device(mags, [n], [budget])
+    k = int(cnt[0].item())
+    return idx[:k].cpu().numpy().astype(np.int64)
+
+
+def batched_selection(fresh, cached, counts: Sequence[int], fraction: float,
+                      cached_rows=None, ledger: Optional[CostLedger] = None
+                      ) -> List[Tuple[np.ndarray, float]]:
+    """One difference pass over every member's reused rows.
+
+    ``fresh`` (R, H, D): the probe forward's check-layer keys of every member's
+    shared positions, members concatenated in order with ``counts[m]`` rows
+    each; ``cached``: the matching cached keys -- dense (R, H, D), or a
+    (rows, H, D) plane (e.g. ``pool.k[check_layer]``) addressed by
+    ``cached_rows`` (R,).  Returns per member (member-relative important
+    indices ascending, deviation score); members with no rows get
+    (empty, 0.0), like probe_and_select (pic.py:244-246)."""
+    dev = fresh.device if isinstance(fresh, torch.Tensor) else default_device()
+    f = to_device(fresh, dev)
+    c = to_device(cached, dev, f.dtype)
+    rows = None if cached_rows is None else to_device(np.asarray(cached_rows, np.int64)
+                                                     if not isinstance(cached_rows, torch.Tensor)
+                                                     else cached_rows, dev)
+    if rows is None and tuple(c.shape) != tuple(f.shape):
+        raise ValueError("key tensors must have identical shapes")
+    counts = [int(x) for x in counts]
+    if sum(counts) != int(f.shape[0]):
+        raise ValueError("member counts must cover every fresh row")
+    mags = _mags_device(f, c, rows)
+    if ledger is not None:
+        ledger.record_selection_pass()
+    budgets = [recompute_budget(fraction, n) for n in counts]
+    off, idx, cnt, dev_sum = _select_device(mags, counts, budgets)
+    idx_h = idx.cpu().numpy()
+    cnt_h = cnt.cpu().numpy()
+    sums = dev_sum.cpu().numpy()
+    out = []
+    for m, n in enumerate(counts):
+        if n == 0:
+            out.append((np.empty(0, dtype=np.int64), 0.0))
+            continue
+        k = int(cnt_h[m])
+        out.append((idx_h[off[m]:off[m] + k].astype(np.int64), float(sums[m])))
+    return out
+
+
+def select_master(deviation_scores: Dict[int, float]) -> int:
+    """Request id with the lowest total deviation; ties to the lowest id."""
+    if not deviation_scores:
+        raise ValueError("cannot elect a master from an empty group")
+    return min(deviation_scores.items(), key=lambda kv: (kv[1], kv[0]))[0]
+
+
+def mirror_hint_positions(member, master, member_important: np.ndarray,
+                          master_important: np.ndarray) -> np.ndarray:
+    """Positions where a mirror may differ from its master: fresh on either
+    side, different cache entry or offset, or either side's important set."""
+    if member.num_tokens != master.num_tokens:
+        raise ValueError("hints are only defined for equal-length prompts")
+    le, lo = np.asarray(member.label_entry), np.asarray(member.label_offset)
+    me, mo = np.asarray(master.label_entry), np.asarray(master.label_offset)
+    divergent = (le == -1) | (me == -1) | (le != me) | (lo != mo)
+    hinted = np.union1d(np.flatnonzero(divergent), member_important)
+    return np.union1d(hinted, master_important).astype(np.int64)

@@ -36,7 +36,10 @@ from roundkv.diffstore import (  # noqa: E402
 )
 from roundkv.ledger import CostLedger  # noqa: E402
 from roundkv.paged_pool import PagedPool  # noqa: E402
-from roundkv.pic import PicConfig, _skeleton, align_cached, prepare_request  # noqa: E402
+from roundkv.collective import select_master  # noqa: E402
+from roundkv.pic import (PicConfig, _skeleton, align_cached, key_diff,  # noqa: E402
+                         prepare_request, probe_and_select)
+from roundkv.toymodel import _selective_forward  # noqa: E402
 from roundkv.restore import dense_restore, fused_restore  # noqa: E402
 from roundkv.segment_index import SegmentCacheEntry, SegmentIndex  # noqa: E402
 from roundkv.toymodel import build_weights, full_prefill, rope_apply  # noqa: E402
@@ -118,6 +121,30 @@ def gen_collector():
         arrays[f"agent{a}_v_shared"] = cv[:, shared]
         meta["agents"].append({"T": int(p.num_tokens), "hits": hits,
                                "shared_idx": shared.tolist()})
+    # the check-layer selection on the same round (pic.probe_and_select):
+    # fresh probe keys, cached (aligned) keys, and the reference's outputs
+    pic = PicConfig(recompute_fraction=0.15, check_layer=1)
+    fresh_rows, cached_rows, counts = [], [], []
+    for p, (ck, cv) in zip(preps, contexts):
+        shared = p.shared_idx
+        fix = np.union1d(shared, p.structural_idx)
+        k, _ = _selective_forward(weights, p.tokens, p.positions, fix, ck, cv,
+                                  max_layer=pic.check_layer + 1)
+        fresh_rows.append(k[pic.check_layer][np.searchsorted(fix, shared)])
+        cached_rows.append(ck[pic.check_layer][shared])
+        counts.append(int(shared.size))
+    sel = probe_and_select(weights, preps, contexts, pic, CostLedger(model.num_layers))
+    arrays["sel_fresh"] = np.concatenate(fresh_rows)
+    arrays["sel_cached"] = np.concatenate(cached_rows)
+    arrays["sel_mags"] = key_diff(arrays["sel_fresh"], arrays["sel_cached"])
+    meta["selection"] = {
+        "fraction": pic.recompute_fraction, "counts": counts,
+        "important": [imp.tolist() for imp, _ in sel],
+        "important_rel": [np.searchsorted(p.shared_idx, imp).tolist()
+                          for p, (imp, _) in zip(preps, sel)],
+        "deviation": [dev for _, dev in sel],
+        "master": int(select_master({i: d for i, (_, d) in enumerate(sel)})),
+    }
     np.savez_compressed(os.path.join(HERE, "collector.npz"), **arrays)
     return meta
 

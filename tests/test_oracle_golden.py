@@ -219,6 +219,35 @@ def test_allocator_stream_matches_reference():
             free[live.pop(op["serial"])] = True
 
 
+def test_selection_matches_reference_probe_and_select():
+    sel = G["collector"]["selection"]
+    z = load_npz("collector.npz")
+    mags = ref.key_diff(z["sel_fresh"], z["sel_cached"])
+    assert np.abs(mags - z["sel_mags"]).max() <= 1e-6
+    off = 0
+    devs = {}
+    for m, n in enumerate(sel["counts"]):
+        mm = mags[off:off + n]
+        imp = ref.select_important(mm, ref.recompute_budget(sel["fraction"], n))
+        assert imp.tolist() == sel["important_rel"][m]
+        devs[m] = float(mm.sum())
+        assert abs(devs[m] - sel["deviation"][m]) <= 1e-6 * max(1.0, abs(sel["deviation"][m]))
+        off += n
+    assert ref.select_master(devs) == sel["master"]
+
+
+def test_selection_known_answers():
+    fresh = np.zeros((3, 2, 4), np.float32)
+    cached = np.zeros((3, 2, 4), np.float32)
+    cached[1, 0, 0], cached[1, 1, 0] = 3.0, 4.0
+    assert ref.key_diff(fresh, cached).tolist() == [0.0, 5.0, 0.0]
+    mags = np.array([0.0, 3.0, 3.0, 1.0, 0.0, 2.0], np.float32)
+    assert ref.select_important(mags, 3).tolist() == [1, 2, 5]
+    assert ref.select_important(mags, 10).tolist() == [1, 2, 3, 5]
+    assert ref.select_important(mags, 0).tolist() == []
+    assert ref.select_important(np.array([5.0, 5.0, 5.0, 1.0], np.float32), 2).tolist() == [0, 1]
+
+
 def test_select_master_and_budget():
     assert ref.select_master({0: 2.0, 1: 1.5, 2: 3.0}) == 1
     assert ref.select_master({2: 1.5, 0: 1.5, 1: 2.0}) == 0
