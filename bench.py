@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--mirror-frac", type=float, default=0.1)
     ap.add_argument("--codec-mirrors", type=int, default=49, help="mirrors per codec family")
     ap.add_argument("--profile", action="store_true", help="few launches, no extras (for ncu)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     return ap.parse_args()
 
 
@@ -251,10 +252,15 @@ def run_tdkv(args):
     from paper_2604_03143_b200.dist import broadcast_arena
 
     world, rank, local = dist_env()
-    dev = torch.device("cuda", local)
+    # one GPU per rank; --dist-backend gloo lets a single-GPU box exercise the
+    # multi-rank flow (ranks then share the device)
+    dev = torch.device("cuda", local % torch.cuda.device_count())
     torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
     spec = rounds.CONFIGS[args.config]
     if args.agents:
         spec = spec.scaled(num_agents=args.agents)
@@ -300,7 +306,8 @@ def run_tdkv(args):
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        t = torch.tensor([x], dtype=torch.float64,
+                         device=dev if args.dist_backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
