@@ -249,7 +249,7 @@ def run_tdkv(args):
 
     import paper_2604_03143_b200 as tk
     from paper_2604_03143_b200 import rounds
-    from paper_2604_03143_b200.dist import broadcast_arena
+    from paper_2604_03143_b200.dist import broadcast_collect
 
     world, rank, local = dist_env()
     # one GPU per rank; --dist-backend gloo lets a single-GPU box exercise the
@@ -290,11 +290,13 @@ def run_tdkv(args):
     stream = torch.cuda.current_stream(dev)
 
     def round_step(events=None):
-        if world > 1:
-            broadcast_arena(arena, 0)
         if events is not None:
             events[0].record(stream)
-        collector.collect(plan)
+        if world > 1:
+            # masters broadcast from rank 0 in layer chunks, K1 per landed chunk
+            broadcast_collect(collector, plan, 0, chunks=7)
+        else:
+            collector.collect(plan)
         if events is not None:
             events[1].record(stream)
 

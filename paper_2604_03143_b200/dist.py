@@ -36,6 +36,34 @@ def broadcast_arena(arena, src: int = 0, group=None) -> int:
     return 2 * arena.k.numel() * arena.k.element_size()
 
 
+def broadcast_collect(collector, plan, src: int = 0, chunks: int = 7, group=None,
+                      ledger=None) -> int:
+    """One round on one rank: the master arena arrives from ``src`` in layer
+    chunks (NCCL broadcasts queued back to back on the communicator's
+    stream) and K1 runs on each chunk as soon as it has landed, so the
+    NVLink transfer of chunk c+1 overlaps the HBM-bound collector on chunk
+    c.  Returns the kernels launched."""
+    arena = collector.arena
+    L = arena.num_layers
+    bounds = [round(i * L / chunks) for i in range(chunks + 1)]
+    works = []
+    for l0, l1 in zip(bounds[:-1], bounds[1:]):
+        if l1 > l0:
+            wk = dist.broadcast(arena.k[l0:l1], src, group=group, async_op=True)
+            wv = dist.broadcast(arena.v[l0:l1], src, group=group, async_op=True)
+            works.append((l0, l1, wk, wv))
+    pool = collector.pool
+    n = plan.launch_table()
+    for l0, l1, wk, wv in works:
+        wk.wait()          # stream dependency for NCCL (host-blocking for gloo)
+        wv.wait()
+        n += plan.launch_collect(arena, pool.k, pool.v, pool.layer_stride, layers=(l0, l1))
+    if ledger is not None and plan.num_jobs:
+        for layer in range(L):
+            ledger.record_rope_call(layer)
+    return n
+
+
 def elect_master(local_scores: Dict[int, float], group=None,
                  device: Optional[torch.device] = None) -> int:
     """Global family master over every rank's members: lowest deviation,

@@ -1,0 +1,69 @@
+"""Multi-rank collector check (launched by tests/test_gpu_dist.py via torchrun).
+
+Each rank owns a contiguous agent shard; rank 0 alone holds the master
+blocks and broadcasts them in layer chunks while every rank collects its
+shard (dist.broadcast_collect).  Every rank then rebuilds its shard with a
+single-process collect from the true masters and requires bit equality.
+Backend: nccl on multi-GPU boxes, gloo when ranks share one GPU.
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2604_03143_b200 as tk  # noqa: E402
+from paper_2604_03143_b200 import rounds  # noqa: E402
+from paper_2604_03143_b200.dist import broadcast_collect, elect_master, shard_range  # noqa: E402
+
+
+def main():
+    backend = os.environ.get("TDKV_DIST_BACKEND", "gloo")
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)) % torch.cuda.device_count())
+    torch.cuda.set_device(dev)
+    dist.init_process_group(backend)
+    spec = rounds.CONFIGS["c2"].scaled(num_layers=5, num_agents=9, num_segments=3, hist_len=11)
+    mk, mv = rounds.master_planes_host(spec)
+    dt = spec.torch_dtype
+    k = torch.from_numpy(mk).to(dev).to(dt)
+    v = torch.from_numpy(mv).to(dev).to(dt)
+    truth = rounds.make_arena(spec, k.clone(), v.clone())
+    if rank != 0:
+        k.zero_()
+        v.zero_()
+    arena = rounds.make_arena(spec, k, v)
+    agents = shard_range(spec.num_agents, rank, world)
+    T = spec.tokens_per_agent
+    pool = tk.PagedPool(len(agents) * T + 8, spec.num_layers, spec.num_heads, spec.head_dim,
+                        dtype=dt, device=dev)
+    maps = [pool.allocate(T, a) for a in agents]
+    jobs = [j for a, m in zip(agents, maps) for j in rounds.agent_jobs(spec, a, m.slots)]
+    col = tk.KVCollector(arena, pool)
+    plan = col.plan(jobs)
+    broadcast_collect(col, plan, 0, chunks=3)
+    torch.cuda.synchronize(dev)
+    assert torch.equal(arena.k, truth.k) and torch.equal(arena.v, truth.v), "broadcast"
+    ref_pool = tk.PagedPool(len(agents) * T + 8, spec.num_layers, spec.num_heads, spec.head_dim,
+                            dtype=dt, device=dev)
+    for a in agents:
+        ref_pool.allocate(T, a)
+    rc = tk.KVCollector(truth, ref_pool)
+    rc.collect(rc.plan(jobs))
+    torch.cuda.synchronize(dev)
+    assert torch.equal(pool.k, ref_pool.k) and torch.equal(pool.v, ref_pool.v), "collect"
+    scores = {a: float((a * 7919) % 13) / 4.0 for a in agents}
+    master = elect_master(scores, device=dev if backend == "nccl" else torch.device("cpu"))
+    want = min(((float((a * 7919) % 13) / 4.0, a) for a in range(spec.num_agents)))[1]
+    assert master == want, (master, want)
+    dist.barrier()
+    if rank == 0:
+        print(f"dist_check ok: world={world} backend={backend}")
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
