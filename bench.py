@@ -427,6 +427,7 @@ def run_tdkv(args):
     # -- codec sub-benchmarks (rank-local) ----------------------------------
     if not args.no_codec and not args.profile:
         line["codec"] = codec_bench(tk, spec, pool, maps, dev, args, peak)
+        line["selection"] = selection_bench(tk, spec, pool, maps, dev, args, peak)
 
     if not args.no_cpu and not args.profile and rank == 0 and world == 1:
         line["cpu_baseline"] = cpu_baseline(spec, args.cpu_seconds)
@@ -437,6 +438,46 @@ def run_tdkv(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def selection_bench(tk, spec, pool, maps, dev, args, peak):
+    """K4 over the round: every agent's shared rows at the check layer (layer
+    1, as PicConfig's default) are compared with probe keys in one pass; the
+    cached side is read straight from the pool by slot."""
+    import torch
+    from paper_2604_03143_b200 import select as sel
+    check = 1 if spec.num_layers > 1 else 0
+    starts = np.stack([rounds_segment_starts(spec, a) for a in range(len(maps))])
+    tok = np.arange(spec.seg_len)
+    rows = np.concatenate([m.slots[(st[:, None] + tok).reshape(-1)]
+                           for m, st in zip(maps, starts)])
+    d_rows = torch.from_numpy(rows).to(dev)
+    plane = pool.k[check]
+    g = torch.Generator(device=dev).manual_seed(5)
+    fresh = plane[d_rows].clone()
+    fresh += (0.05 * torch.randn(fresh.shape, generator=g, device=dev)).to(fresh.dtype)
+    counts = [spec.num_segments * spec.seg_len] * len(maps)
+    for _ in range(2):
+        out = sel.batched_selection(fresh, plane, counts, 0.15, cached_rows=d_rows)
+    reps = max(1, min(args.steps, 5))
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        out = sel.batched_selection(fresh, plane, counts, 0.15, cached_rows=d_rows)
+    torch.cuda.synchronize(dev)
+    t = (time.perf_counter() - t0) / reps
+    nbytes = 2 * fresh.numel() * fresh.element_size() + 4 * len(rows)
+    return {"members": len(maps), "rows": int(len(rows)),
+            "important_per_member": int(len(out[0][0])),
+            "gbs": round(nbytes / t / 1e9, 1), "frac": round(nbytes / t / 1e9 / peak, 4),
+            "ms_per_round": round(t * 1e3, 3),
+            "bytes": "fresh + cached check-layer rows read once (+ magnitudes); whole API call "
+                     "incl. the host read of important sets and deviations"}
+
+
+def rounds_segment_starts(spec, a):
+    from paper_2604_03143_b200 import rounds
+    return rounds.segment_starts(spec, a)
 
 
 def codec_bench(tk, spec, pool, maps, dev, args, peak):
