@@ -218,8 +218,9 @@ int32_t tdkv_rows(const tdkv_rows_job* d_jobs, int32_t n_jobs,
  * writes its top min(budget[m], #nonzero) positions by (-mag, index), in
  * ascending order, to out_idx[member_off[m] ...] (select_important,
  * pic.py:180-189), their number to out_count[m], and the float32 sum of its
- * magnitudes to deviation[m] (pic.py:280).  At most 16384 positions per
- * member.
+ * magnitudes to deviation[m] (pic.py:280).  One CTA per member runs a
+ * radix select over the magnitudes' bit patterns; at most 49152 positions
+ * per member.
  * ---------------------------------------------------------------------- */
 int32_t tdkv_keydiff(const void* d_fresh, const void* d_cached,
                      const int64_t* d_cached_rows, int64_t n_rows, int32_t row_elems,

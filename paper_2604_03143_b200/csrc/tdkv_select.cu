@@ -39,40 +39,61 @@ __global__ void __launch_bounds__(256)
     }
 }
 
-// One CTA per member: bitonic sort of (descending magnitude, ascending
-// index) keys in shared memory, keep the first min(budget, nonzero) and emit
-// them in ascending index order.
+// One CTA per member, radix select on the magnitudes' bit patterns (a
+// non-negative float orders like its bits): four 8-bit passes find the
+// take-th largest value T; everything above T is selected, plus the
+// lowest-index elements equal to T (ties to the lower index); the flags are
+// then compacted in ascending index order.
+__device__ __forceinline__ int block_excl_scan(int v, int* s_warp, int& total) {
+    // exclusive block scan of one int per thread (blockDim.x <= 1024)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            const int c = s_warp[w];
+            s_warp[w] = acc;
+            acc += c;
+        }
+        s_warp[32] = acc;
+    }
+    __syncthreads();
+    const int out = s_warp[warp] + x - v;
+    total = s_warp[32];
+    __syncthreads();
+    return out;
+}
+
 __global__ void __launch_bounds__(512)
     select_kernel(const float* __restrict__ mags, const int64_t* __restrict__ member_off,
                   const int32_t* __restrict__ budget, int32_t* __restrict__ out_idx,
                   int32_t* __restrict__ out_count, float* __restrict__ deviation) {
-    extern __shared__ __align__(16) unsigned long long keys[];
+    extern __shared__ __align__(16) uint32_t bits[];
     __shared__ double red[32];
-    __shared__ int s_nnz;
-    __shared__ int s_warp[32];
+    __shared__ int s_warp[33];
+    __shared__ int hist[256];
+    __shared__ int s_nnz, s_sel, s_rem;
     const int m = blockIdx.x;
     const int64_t off = member_off[m];
     const int n = (int)(member_off[m + 1] - off);
-    int npad = 1;
-    while (npad < n) npad <<= 1;
     const int tid = threadIdx.x, nthr = blockDim.x;
     if (tid == 0) s_nnz = 0;
     __syncthreads();
 
     double sum = 0.0;
     int nnz = 0;
-    for (int i = tid; i < npad; i += nthr) {
-        unsigned long long key = ~0ull;
-        if (i < n) {
-            const float v = mags[off + i];
-            sum += (double)v;
-            // v >= 0: its bit pattern orders like its value; invert for a
-            // descending sort, index in the low word breaks ties ascending
-            const uint32_t bits = v > 0.f ? __float_as_uint(v) : 0u;
-            nnz += v > 0.f;
-            key = ((unsigned long long)(~bits) << 32) | (uint32_t)i;
-        }
-        keys[i] = key;
+    for (int i = tid; i < n; i += nthr) {
+        const float v = mags[off + i];
+        sum += (double)v;
+        nnz += v > 0.f;
+        bits[i] = v > 0.f ? __float_as_uint(v) : 0u;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -85,58 +106,76 @@ __global__ void __launch_bounds__(512)
     }
     __syncthreads();
     if (tid == 0) {
-        double s = 0.0;
-        for (int w = 0; w < (nthr >> 5); ++w) s += red[w];
-        deviation[m] = (float)s;
+        double acc = 0.0;
+        for (int w = 0; w < (nthr >> 5); ++w) acc += red[w];
+        deviation[m] = (float)acc;
+        s_rem = min(budget[m], s_nnz);
     }
-    // bitonic sort ascending
-    for (int k = 2; k <= npad; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = tid; i < npad; i += nthr) {
-                const int ixj = i ^ j;
-                if (ixj > i) {
-                    const unsigned long long a = keys[i], b = keys[ixj];
-                    const bool up = (i & k) == 0;
-                    if ((a > b) == up) {
-                        keys[i] = b;
-                        keys[ixj] = a;
+    __syncthreads();
+    const int take = s_rem;
+    if (take <= 0) {
+        if (tid == 0) out_count[m] = 0;
+        return;
+    }
+    // radix select of the take-th largest bit pattern
+    uint32_t prefix = 0u, mask = 0u;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        for (int b = tid; b < 256; b += nthr) hist[b] = 0;
+        __syncthreads();
+        for (int i = tid; i < n; i += nthr) {
+            const uint32_t x = bits[i];
+            if ((x & mask) == prefix) atomicAdd(&hist[(x >> shift) & 255u], 1);
+        }
+        __syncthreads();
+        if (tid < 32) {
+            // lane l owns bins 255-8l .. 248-8l (from the top)
+            int c[8], local = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                c[q] = hist[255 - 8 * tid - q];
+                local += c[q];
+            }
+            int incl = local;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (tid >= o) incl += y;
+            }
+            const int before = incl - local;
+            const int rem = s_rem;
+            if (before < rem && incl >= rem) {
+                int acc = before;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if (acc + c[q] >= rem) {
+                        s_sel = 255 - 8 * tid - q;
+                        s_rem = rem - acc;        // still needed inside the chosen bin
+                        break;
                     }
+                    acc += c[q];
                 }
             }
-            __syncthreads();
         }
+        __syncthreads();
+        prefix |= (uint32_t)s_sel << shift;
+        mask |= 255u << shift;
+        __syncthreads();
     }
-    const int take = min(budget[m], s_nnz);
-    // mark the selected indices (reuse the tail of the key array as flags is
-    // unsafe while reading keys -> two passes through a flag word array)
-    __syncthreads();
-    uint32_t* flags = reinterpret_cast<uint32_t*>(keys + npad);   // npad words after keys
-    for (int i = tid; i < npad; i += nthr) flags[i] = 0u;
-    __syncthreads();
-    for (int i = tid; i < take; i += nthr) flags[(uint32_t)(keys[i] & 0xffffffffu)] = 1u;
-    __syncthreads();
-    // block-ordered compaction of the flags (ascending indices)
-    int running = 0;
-    const int lane = tid & 31, warp = tid >> 5;
+    const uint32_t thr = prefix;
+    const int need_eq = s_rem;                     // elements equal to thr to keep
+    // pass over indices in ascending order: keep > thr, and the first
+    // need_eq elements == thr; then compact
+    int running_eq = 0, running = 0, total;
     for (int base = 0; base < n; base += nthr) {
         const int i = base + tid;
-        const bool f = i < n && flags[i];
-        const unsigned bal = __ballot_sync(0xffffffffu, f);
-        if (lane == 0) s_warp[warp] = __popc(bal);
-        __syncthreads();
-        if (tid == 0) {
-            int acc = 0;
-            for (int w = 0; w < (nthr >> 5); ++w) {
-                const int c = s_warp[w];
-                s_warp[w] = acc;
-                acc += c;
-            }
-            s_warp[31] = acc;   // nthr <= 512 -> at most 16 warps, slot 31 is free
-        }
-        __syncthreads();
-        if (f) out_idx[off + running + s_warp[warp] + __popc(bal & ((1u << lane) - 1u))] = i;
-        running += s_warp[31];
-        __syncthreads();
+        const uint32_t x = i < n ? bits[i] : 0u;
+        const int eq = (i < n && x == thr) ? 1 : 0;
+        const int eq_rank = running_eq + block_excl_scan(eq, s_warp, total);
+        running_eq += total;
+        const int keep = (i < n) && (x > thr || (eq && eq_rank < need_eq)) ? 1 : 0;
+        const int pos = running + block_excl_scan(keep, s_warp, total);
+        if (keep) out_idx[off + pos] = i;
+        running += total;
     }
     if (tid == 0) out_count[m] = take;
 }
@@ -175,14 +214,12 @@ extern "C" int32_t tdkv_select_important(const float* d_mags, const int64_t* d_m
                                          int32_t* d_out_count, float* d_deviation, void* stream) {
     if (n_members < 0 || max_count < 0) return set_error(TDKV_EINVAL, "tdkv_select_important: bad sizes");
     if (n_members == 0) return TDKV_OK;
-    if (max_count > 16384)
+    if (max_count > 49152)
         return set_error(TDKV_EUNSUPPORTED,
-                         "tdkv_select_important: %d positions per member (max 16384)", max_count);
+                         "tdkv_select_important: %d positions per member (max 49152)", max_count);
     if (!d_mags || !d_member_off || !d_budget || !d_out_idx || !d_out_count || !d_deviation)
         return set_error(TDKV_EINVAL, "tdkv_select_important: null pointer");
-    int npad = 1;
-    while (npad < max_count) npad <<= 1;
-    const size_t smem = (size_t)npad * 8 + (size_t)npad * 4;
+    const size_t smem = (size_t)(max_count > 0 ? max_count : 1) * 4;
     if (cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess)
         return check_launch("tdkv_select_important: cudaFuncSetAttribute");

@@ -62,14 +62,16 @@ def _select_device(mags: torch.Tensor, counts: Sequence[int], budgets: Sequence[
     d_off = h2d(off, dev)
     d_budget = h2d(np.asarray(budgets, np.int32), dev)
     m = counts.size
-    out_idx = torch.empty(max(int(off[-1]), 1), dtype=torch.int32, device=dev)
-    out_cnt = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
-    dev_sum = torch.empty(max(m, 1), dtype=torch.float32, device=dev)
+    # one int32 buffer [counts | deviation bits | indices] -> a single D2H
+    buf = torch.empty(2 * m + max(int(off[-1]), 1), dtype=torch.int32, device=dev)
+    out_cnt = buf[:m]
+    dev_sum = buf[m:2 * m].view(torch.float32)
+    out_idx = buf[2 * m:]
     if m:
         _lib.call("tdkv_select_important", ptr(mags), ptr(d_off), ptr(d_budget), m,
                   int(counts.max(initial=0)), ptr(out_idx), ptr(out_cnt), ptr(dev_sum),
                   stream_handle(dev))
-    return off, out_idx, out_cnt, dev_sum
+    return off, out_idx, out_cnt, dev_sum, buf
 
 
 def select_important(magnitudes, budget: int) -> np.ndarray:
@@ -80,7 +82,7 @@ def select_important(magnitudes, budget: int) -> np.ndarray:
         return np.empty(0, dtype=np.int64)
     dev = magnitudes.device if isinstance(magnitudes, torch.Tensor) else default_device()
     mags = to_device(magnitudes, dev, torch.float32)
-    _, idx, cnt, _ = _select_device(mags, [n], [budget])
+    _, idx, cnt, _, _ = _select_device(mags, [n], [budget])
     k = int(cnt[0].item())
     return idx[:k].cpu().numpy().astype(np.int64)
 
@@ -112,10 +114,12 @@ def batched_selection(fresh, cached, counts: Sequence[int], fraction: float,
     if ledger is not None:
         ledger.record_selection_pass()
     budgets = [recompute_budget(fraction, n) for n in counts]
-    off, idx, cnt, dev_sum = _select_device(mags, counts, budgets)
-    idx_h = idx.cpu().numpy()
-    cnt_h = cnt.cpu().numpy()
-    sums = dev_sum.cpu().numpy()
+    off, _, _, _, buf = _select_device(mags, counts, budgets)
+    m = len(counts)
+    host = buf.cpu().numpy()
+    cnt_h = host[:m]
+    sums = host[m:2 * m].view(np.float32)
+    idx_h = host[2 * m:]
     out = []
     for m, n in enumerate(counts):
         if n == 0:
