@@ -466,11 +466,21 @@ def selection_bench(tk, spec, pool, maps, dev, args, peak):
         out = sel.batched_selection(fresh, plane, counts, 0.15, cached_rows=d_rows)
     torch.cuda.synchronize(dev)
     t = (time.perf_counter() - t0) / reps
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        sel.selection_kernels(fresh, plane, d_rows, counts, 0.15)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    tk_s = e0.elapsed_time(e1) * 1e-3 / reps
     nbytes = 2 * fresh.numel() * fresh.element_size() + 4 * len(rows)
     return {"members": len(maps), "rows": int(len(rows)),
             "important_per_member": int(len(out[0][0])),
             "gbs": round(nbytes / t / 1e9, 1), "frac": round(nbytes / t / 1e9 / peak, 4),
             "ms_per_round": round(t * 1e3, 3),
+            "device_gbs": round(nbytes / tk_s / 1e9, 1),
+            "device_frac": round(nbytes / tk_s / 1e9 / peak, 4),
+            "device_ms": round(tk_s * 1e3, 4),
             "bytes": "fresh + cached check-layer rows read once (+ magnitudes); whole API call "
                      "incl. the host read of important sets and deviations"}
 

@@ -87,6 +87,18 @@ def select_important(magnitudes, budget: int) -> np.ndarray:
     return idx[:k].cpu().numpy().astype(np.int64)
 
 
+def selection_kernels(fresh: torch.Tensor, cached: torch.Tensor,
+                      cached_rows: Optional[torch.Tensor], counts: Sequence[int],
+                      fraction: float):
+    """The two K4 launches on device tensors, no host synchronization.
+    Returns (member offsets, int32 result buffer [counts | deviation bits |
+    indices])."""
+    mags = _mags_device(fresh, cached, cached_rows)
+    budgets = [recompute_budget(fraction, n) for n in counts]
+    off, _, _, _, buf = _select_device(mags, counts, budgets)
+    return off, buf
+
+
 def batched_selection(fresh, cached, counts: Sequence[int], fraction: float,
                       cached_rows=None, ledger: Optional[CostLedger] = None
                       ) -> List[Tuple[np.ndarray, float]]:
@@ -110,11 +122,9 @@ def batched_selection(fresh, cached, counts: Sequence[int], fraction: float,
     counts = [int(x) for x in counts]
     if sum(counts) != int(f.shape[0]):
         raise ValueError("member counts must cover every fresh row")
-    mags = _mags_device(f, c, rows)
+    off, buf = selection_kernels(f, c, rows, counts, fraction)
     if ledger is not None:
         ledger.record_selection_pass()
-    budgets = [recompute_budget(fraction, n) for n in counts]
-    off, _, _, _, buf = _select_device(mags, counts, budgets)
     m = len(counts)
     host = buf.cpu().numpy()
     cnt_h = host[:m]
