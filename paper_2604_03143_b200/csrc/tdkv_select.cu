@@ -16,22 +16,30 @@ namespace tdkv {
 // One warp per row: sum of squared differences accumulated in float64 (the
 // reference accumulates in float32 -- any order difference stays far below
 // the float32 rounding of the result), sqrt, rounded to float32.
-template <typename T>
+template <typename T, typename V>
 __global__ void __launch_bounds__(256)
     keydiff_kernel(const T* __restrict__ fresh, const T* __restrict__ cached,
                    const int64_t* __restrict__ cached_rows, int64_t n_rows, int row_elems,
                    float* __restrict__ mags) {
+    constexpr int kE = sizeof(V) / sizeof(T);          // elements per load
     const int lane = threadIdx.x & 31;
+    const int upr = row_elems / kE;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < n_rows;
          r += warps) {
-        const T* f = fresh + (size_t)r * row_elems;
+        const V* f = reinterpret_cast<const V*>(fresh + (size_t)r * row_elems);
         const int64_t cr = cached_rows ? __ldg(cached_rows + r) : r;
-        const T* c = cached + (size_t)cr * row_elems;
+        const V* c = reinterpret_cast<const V*>(cached + (size_t)cr * row_elems);
         double acc = 0.0;
-        for (int e = lane; e < row_elems; e += 32) {
-            const float d = (float)f[e] - (float)c[e];     // float32 difference, as numpy
-            acc += (double)__fmul_rn(d, d);                // float32 product, as numpy
+        for (int u = lane; u < upr; u += 32) {
+            const V fv = __ldcs(f + u), cv = __ldcs(c + u);
+            const T* fe = reinterpret_cast<const T*>(&fv);
+            const T* ce = reinterpret_cast<const T*>(&cv);
+#pragma unroll
+            for (int q = 0; q < kE; ++q) {
+                const float d = (float)fe[q] - (float)ce[q];   // float32 difference, as numpy
+                acc += (double)__fmul_rn(d, d);                // float32 product, as numpy
+            }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -122,9 +130,15 @@ __global__ void __launch_bounds__(512)
     for (int shift = 24; shift >= 0; shift -= 8) {
         for (int b = tid; b < 256; b += nthr) hist[b] = 0;
         __syncthreads();
-        for (int i = tid; i < n; i += nthr) {
-            const uint32_t x = bits[i];
-            if ((x & mask) == prefix) atomicAdd(&hist[(x >> shift) & 255u], 1);
+        // magnitudes cluster in a few exponent bins: aggregate same-bin lanes
+        // of a warp into one shared-memory atomic
+        for (int base = 0; base < n; base += nthr) {
+            const int i = base + tid;
+            const uint32_t x = i < n ? bits[i] : 0u;
+            const bool live = i < n && (x & mask) == prefix;
+            const unsigned bin = live ? (x >> shift) & 255u : 256u;
+            const unsigned peers = __match_any_sync(0xffffffffu, bin);
+            if (live && (__ffs(peers) - 1) == (tid & 31)) atomicAdd(&hist[bin], __popc(peers));
         }
         __syncthreads();
         if (tid < 32) {
@@ -193,14 +207,26 @@ extern "C" int32_t tdkv_keydiff(const void* d_fresh, const void* d_cached,
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     long long grid = (n_rows + 7) / 8;
     if (grid > sm_count() * 16) grid = sm_count() * 16;
+    const bool vec = (row_elems * elt_size(dtype)) % 16 == 0 && aligned(d_fresh, 16) &&
+                     aligned(d_cached, 16);
     if (dtype == TDKV_F32) {
-        keydiff_kernel<float><<<(unsigned)grid, 256, 0, s>>>(
-            static_cast<const float*>(d_fresh), static_cast<const float*>(d_cached), d_cached_rows,
-            n_rows, row_elems, d_mags);
+        const float* f = static_cast<const float*>(d_fresh);
+        const float* c = static_cast<const float*>(d_cached);
+        if (vec)
+            keydiff_kernel<float, uint4><<<(unsigned)grid, 256, 0, s>>>(f, c, d_cached_rows, n_rows,
+                                                                        row_elems, d_mags);
+        else
+            keydiff_kernel<float, float><<<(unsigned)grid, 256, 0, s>>>(f, c, d_cached_rows, n_rows,
+                                                                        row_elems, d_mags);
     } else if (dtype == TDKV_BF16) {
-        keydiff_kernel<__nv_bfloat16><<<(unsigned)grid, 256, 0, s>>>(
-            static_cast<const __nv_bfloat16*>(d_fresh), static_cast<const __nv_bfloat16*>(d_cached),
-            d_cached_rows, n_rows, row_elems, d_mags);
+        const __nv_bfloat16* f = static_cast<const __nv_bfloat16*>(d_fresh);
+        const __nv_bfloat16* c = static_cast<const __nv_bfloat16*>(d_cached);
+        if (vec)
+            keydiff_kernel<__nv_bfloat16, uint4><<<(unsigned)grid, 256, 0, s>>>(
+                f, c, d_cached_rows, n_rows, row_elems, d_mags);
+        else
+            keydiff_kernel<__nv_bfloat16, __nv_bfloat16><<<(unsigned)grid, 256, 0, s>>>(
+                f, c, d_cached_rows, n_rows, row_elems, d_mags);
     } else {
         return set_error(TDKV_EUNSUPPORTED, "tdkv_keydiff: dtype %d", dtype);
     }
