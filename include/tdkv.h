@@ -231,6 +231,19 @@ int32_t tdkv_select_important(const float* d_mags, const int64_t* d_member_off,
                               int32_t max_count, int32_t* d_out_idx,
                               int32_t* d_out_count, float* d_deviation, void* stream);
 
+/* ------------------------------------------------------------------------
+ * K5 building block: C[m, n] (+)= A[m, :k] . B[n, :k] on the
+ * tcgen05 tensor cores, accumulator in TMEM.  A (lda) and B (ldb) row-major
+ * (K-major), C (ldc) float32 row-major; accumulate != 0 adds into C.  For
+ * TDKV_F32 operands the product runs as 3xTF32 (hi/lo split) to stay within
+ * float32 tolerance; TDKV_BF16 runs kind::f16 with bf16 operands.  Used for
+ * the Q/K/V/mix projections of the selective recompute
+ * (toymodel._selective_forward, toymodel.py:99-151).
+ * ---------------------------------------------------------------------- */
+int32_t tdkv_gemm(const void* d_a, int32_t lda, const void* d_b, int32_t ldb,
+                  float* d_c, int32_t ldc, int32_t m, int32_t n, int32_t k,
+                  int32_t dtype, int32_t accumulate, void* stream);
+
 /* Fill rows of every layer with a value (NaN poisoning of freed slots,
  * paged_pool.py:144-147).  value_bits is the element bit pattern. */
 int32_t tdkv_fill_rows(void* d_plane, int64_t layer_stride, int32_t num_layers,

@@ -89,7 +89,7 @@ assert DIFF_PAIR.itemsize == 32 and DIFF_OUT.itemsize == 40 and ROWS_JOB.itemsiz
 EXPORTS = (
     "tdkv_version", "tdkv_last_error", "tdkv_launch_count", "tdkv_rope_table",
     "tdkv_collect", "tdkv_diff_compare", "tdkv_diff_compact", "tdkv_rows",
-    "tdkv_keydiff", "tdkv_select_important", "tdkv_fill_rows",
+    "tdkv_keydiff", "tdkv_select_important", "tdkv_gemm", "tdkv_fill_rows",
 )
 
 _P = ctypes.c_void_p
@@ -111,6 +111,7 @@ _SIGS = {
     "tdkv_fill_rows": (_I32, [_P, _I64, _I32, _P, _I64, _I32, _I32, ctypes.c_uint32, _P]),
     "tdkv_keydiff": (_I32, [_P, _P, _P, _I64, _I32, _I32, _P, _P]),
     "tdkv_select_important": (_I32, [_P, _P, _P, _I32, _I32, _P, _P, _P, _P]),
+    "tdkv_gemm": (_I32, [_P, _I32, _P, _I32, _P, _I32, _I32, _I32, _I32, _I32, _I32, _P]),
 }
 
 _lib: Optional[ctypes.CDLL] = None

@@ -1,0 +1,296 @@
+// K5 building block: C[M,N] (+)= A[M,K] * B[N,K]^T on the 5th-generation
+// tensor cores (tcgen05.mma, accumulator in TMEM).
+//
+// Used by the selective recompute of deviating tokens (reference:
+// pic.refresh -> toymodel._selective_forward, toymodel.py:99-151): the
+// Q/K/V/mix projections h @ W are K-major GEMMs with B = W^T.
+//
+//   * float32 operands run as 3xTF32 (A_hi*B_hi + A_hi*B_lo + A_lo*B_hi, each
+//     split with cvt.rna.tf32) so the products keep ~22 mantissa bits and
+//     the result stays within float32 tolerance of the reference's numpy
+//     float32 matmul; bf16 operands run as kind::f16 (bf16) directly.
+//   * one CTA = one 128 x BN output tile, 128 threads: all threads stage
+//     K-blocks of 32 elements of A and B into shared memory in the canonical
+//     no-swizzle K-major core-matrix layout (8 rows x 16 B per core matrix),
+//     one elected thread issues the MMAs and commits them to an mbarrier,
+//     double-buffered so the next K-block's staging overlaps the MMAs; the
+//     epilogue reads the accumulator with tcgen05.ld and stores (or adds, for
+//     the residual update h += mix @ Wm) float32 rows.
+#include "tdkv_common.cuh"
+
+namespace tdkv {
+
+constexpr int kGemmBM = 128;
+constexpr int kGemmBK = 32;          // elements of K per stage (128 B of tf32 per row)
+
+__device__ __forceinline__ uint32_t tf32_rna(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return r;
+}
+
+// Canonical K-major, no-swizzle UMMA shared-memory descriptor (SM100
+// version 1): LBO = byte step between core matrices along K, SBO = byte step
+// between 8-row groups.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t smem_addr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((smem_addr >> 4) & 0x3FFFu);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1 << 46;                       // descriptor version (Blackwell)
+    return d;                                     // base offset 0, layout SWIZZLE_NONE
+}
+
+// Instruction descriptor: F32 accumulate, K-major A and B, M x N tile.
+__device__ __forceinline__ uint32_t umma_idesc(int ab_format, int m, int n) {
+    return (1u << 4)                              // c_format = F32
+           | ((uint32_t)ab_format << 7)           // a_format (TF32 = 2, BF16 = 1)
+           | ((uint32_t)ab_format << 10)          // b_format
+           | ((uint32_t)(n >> 3) << 17)           // N >> 3
+           | ((uint32_t)(m >> 4) << 24);          // M >> 4
+}
+
+template <bool kTF32>
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                     uint32_t accumulate) {
+    if constexpr (kTF32) {
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+            "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+    } else {
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+            "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+    }
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::
+                     "r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_ld8(uint32_t addr, uint32_t (&r)[8]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7])
+        : "r"(addr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Core-matrix offset of 16-byte chunk ``c16`` (along K) of row ``r`` in a
+// tile whose K-block spans ``ck`` chunks.
+__device__ __forceinline__ uint32_t core_off(int r, int c16, int ck) {
+    return (uint32_t)((((r >> 3) * ck + c16) << 7) + ((r & 7) << 4));
+}
+
+// T = float (3xTF32) or __nv_bfloat16.  A: (M, lda) row-major, B: (N, ldb)
+// row-major (= K-major both), C: (M, ldc) float32.  BN <= 256, multiple of 16.
+template <typename T, int BN>
+__global__ void __launch_bounds__(128, 1)
+    gemm_tn_kernel(const T* __restrict__ A, int lda, const T* __restrict__ B, int ldb,
+                   float* __restrict__ C, int ldc, int M, int N, int K, int accumulate_c) {
+    constexpr bool kTF32 = sizeof(T) == 4;
+    constexpr int kEsz = sizeof(T);
+    constexpr int kChunkElems = 16 / kEsz;                 // elements per 16-byte chunk
+    constexpr int kCk = kGemmBK * kEsz / 16;               // chunks per row per K-block
+    constexpr int kPlanes = kTF32 ? 2 : 1;                 // hi/lo split for tf32
+    constexpr int kABytes = kGemmBM * kGemmBK * kEsz;      // one plane of an A stage
+    constexpr int kBBytes = BN * kGemmBK * kEsz;
+    constexpr int kStageBytes = kPlanes * (kABytes + kBBytes);
+    constexpr int kUmmaK = 32 / kEsz;                      // 8 tf32 or 16 bf16 per MMA
+    constexpr uint32_t kTmemCols = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ __align__(8) uint64_t bars[2];
+    __shared__ uint32_t s_tmem;
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int m0 = blockIdx.x * kGemmBM;
+    const int n0 = blockIdx.y * BN;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(&s_tmem)),
+                     "n"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_mbar_init();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = s_tmem;
+    const uint32_t idesc = umma_idesc(kTF32 ? 2 : 1, kGemmBM, BN);
+
+    const int nk = (K + kGemmBK - 1) / kGemmBK;
+    uint32_t phase[2] = {0u, 0u};
+    for (int kb = 0; kb < nk; ++kb) {
+        const int st = kb & 1;
+        uint8_t* base = smem + st * kStageBytes;
+        if (kb >= 2) {                      // the MMAs that read this stage are done
+            mbar_wait(&bars[st], phase[st]);
+            phase[st] ^= 1u;
+        }
+        // ---- stage A and B K-block kb (generic-proxy smem writes)
+        const int k0 = kb * kGemmBK;
+        auto stage = [&](const T* src, int ld, int rows_valid, int row0, int nrows,
+                         uint8_t* hi, uint8_t* lo) {
+            for (int idx = tid; idx < nrows * kCk; idx += blockDim.x) {
+                const int r = idx / kCk, c = idx - r * kCk;
+                const int gr = row0 + r, gk = k0 + c * kChunkElems;
+                uint4 v = make_uint4(0u, 0u, 0u, 0u);
+                if (gr < rows_valid) {
+                    if (gk + kChunkElems <= K) {
+                        v = *reinterpret_cast<const uint4*>(src + (size_t)gr * ld + gk);
+                    } else {
+                        T tmp[kChunkElems];
+#pragma unroll
+                        for (int q = 0; q < kChunkElems; ++q)
+                            tmp[q] = gk + q < K ? src[(size_t)gr * ld + gk + q] : T(0.f);
+                        v = *reinterpret_cast<uint4*>(tmp);
+                    }
+                }
+                const uint32_t off = core_off(r, c, kCk);
+                if constexpr (kTF32) {
+                    const float* f = reinterpret_cast<const float*>(&v);
+                    uint4 h, l;
+                    uint32_t* hp = reinterpret_cast<uint32_t*>(&h);
+                    uint32_t* lp = reinterpret_cast<uint32_t*>(&l);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        hp[q] = tf32_rna(f[q]);
+                        lp[q] = tf32_rna(f[q] - __uint_as_float(hp[q]));
+                    }
+                    *reinterpret_cast<uint4*>(hi + off) = h;
+                    *reinterpret_cast<uint4*>(lo + off) = l;
+                } else {
+                    *reinterpret_cast<uint4*>(hi + off) = v;
+                }
+            }
+        };
+        uint8_t* a_hi = base;
+        uint8_t* a_lo = base + kABytes;                        // tf32 only
+        uint8_t* b_hi = base + kPlanes * kABytes;
+        uint8_t* b_lo = b_hi + kBBytes;                        // tf32 only
+        stage(A, lda, M, m0, kGemmBM, a_hi, a_lo);
+        stage(B, ldb, N, n0, BN, b_hi, b_lo);
+        fence_proxy_async_smem();          // make the staged tiles visible to the tensor core
+        __syncthreads();
+        // ---- one thread issues the MMAs of this K-block
+        if (tid == 0) {
+            tc_fence_after();
+            const uint32_t lbo = 128, sbo = kCk * 128;
+#pragma unroll
+            for (int s = 0; s < kGemmBK / kUmmaK; ++s) {
+                const uint32_t koff = s * 2 * 128;             // two core matrices per MMA-K
+                const uint64_t dah = umma_desc(smem_u32(a_hi) + koff, lbo, sbo);
+                const uint64_t dbh = umma_desc(smem_u32(b_hi) + koff, lbo, sbo);
+                const uint32_t acc0 = (kb > 0 || s > 0) ? 1u : 0u;
+                umma<kTF32>(tmem, dah, dbh, idesc, acc0);
+                if constexpr (kTF32) {
+                    const uint64_t dal = umma_desc(smem_u32(a_lo) + koff, lbo, sbo);
+                    const uint64_t dbl = umma_desc(smem_u32(b_lo) + koff, lbo, sbo);
+                    umma<kTF32>(tmem, dah, dbl, idesc, 1u);
+                    umma<kTF32>(tmem, dal, dbh, idesc, 1u);
+                }
+            }
+            umma_commit(&bars[st]);
+        }
+        __syncwarp();
+    }
+    // wait for the last commit (it covers every earlier MMA)
+    {
+        const int st = (nk - 1) & 1;
+        mbar_wait(&bars[st], phase[st]);
+    }
+    tc_fence_after();
+
+    // ---- epilogue: thread = one output row (TMEM lane), 8 columns per load
+    const int row = m0 + tid;
+    const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 8) {
+        uint32_t r[8];
+        tmem_ld8(lane_addr + c0, r);
+        if (row < M) {
+            float* crow = C + (size_t)row * ldc;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int col = n0 + c0 + q;
+                if (col < N) {
+                    const float v = __uint_as_float(r[q]);
+                    crow[col] = accumulate_c ? crow[col] + v : v;
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "n"(kTmemCols)
+                     : "memory");
+    }
+}
+
+template <typename T, int BN>
+static int32_t launch_gemm(const void* A, int lda, const void* B, int ldb, float* C, int ldc,
+                           int M, int N, int K, int accumulate, cudaStream_t s) {
+    auto kern = gemm_tn_kernel<T, BN>;
+    constexpr int kPlanes = sizeof(T) == 4 ? 2 : 1;
+    const size_t smem = (size_t)2 * kPlanes * (kGemmBM + BN) * kGemmBK * sizeof(T);
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return check_launch("tdkv_gemm: cudaFuncSetAttribute");
+    dim3 grid((M + kGemmBM - 1) / kGemmBM, (N + BN - 1) / BN);
+    kern<<<grid, 128, smem, s>>>(static_cast<const T*>(A), lda, static_cast<const T*>(B), ldb, C,
+                                 ldc, M, N, K, accumulate);
+    return TDKV_OK;
+}
+
+}  // namespace tdkv
+
+using namespace tdkv;
+
+extern "C" int32_t tdkv_gemm(const void* d_a, int32_t lda, const void* d_b, int32_t ldb,
+                             float* d_c, int32_t ldc, int32_t m, int32_t n, int32_t k,
+                             int32_t dtype, int32_t accumulate, void* stream) {
+    if (m < 0 || n < 0 || k < 0) return set_error(TDKV_EINVAL, "tdkv_gemm: negative size");
+    if (m == 0 || n == 0) return TDKV_OK;
+    if (!d_a || !d_b || !d_c) return set_error(TDKV_EINVAL, "tdkv_gemm: null pointer");
+    const size_t esz = elt_size(dtype);
+    if (dtype != TDKV_F32 && dtype != TDKV_BF16)
+        return set_error(TDKV_EUNSUPPORTED, "tdkv_gemm: dtype %d", dtype);
+    if (!aligned(d_a, 16) || !aligned(d_b, 16) || (lda * esz) % 16 || (ldb * esz) % 16)
+        return set_error(TDKV_EINVAL, "tdkv_gemm: A/B rows must be 16-byte aligned");
+    if (k == 0) return set_error(TDKV_EINVAL, "tdkv_gemm: K must be positive");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int32_t rc;
+    if (dtype == TDKV_F32) {
+        rc = n <= 64 ? launch_gemm<float, 64>(d_a, lda, d_b, ldb, d_c, ldc, m, n, k, accumulate, s)
+                     : launch_gemm<float, 128>(d_a, lda, d_b, ldb, d_c, ldc, m, n, k, accumulate, s);
+    } else {
+        rc = n <= 64
+                 ? launch_gemm<__nv_bfloat16, 64>(d_a, lda, d_b, ldb, d_c, ldc, m, n, k, accumulate, s)
+                 : launch_gemm<__nv_bfloat16, 128>(d_a, lda, d_b, ldb, d_c, ldc, m, n, k, accumulate, s);
+    }
+    if (rc) return rc;
+    count_launch();
+    return check_launch("tdkv_gemm");
+}

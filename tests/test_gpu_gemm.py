@@ -1,0 +1,41 @@
+"""tcgen05 GEMM (K5 building block) against a float64 reference."""
+import pytest
+import torch
+
+from paper_2604_03143_b200 import gemm
+
+pytestmark = pytest.mark.gpu
+DEV = torch.device("cuda", 0)
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 8, 8), (128, 64, 32), (130, 100, 72), (300, 512, 512),
+                                   (17, 1536, 512), (256, 128, 40)])
+def test_gemm_tf32x3_matches_float64(M, N, K):
+    g = torch.Generator(device=DEV).manual_seed(M * 1000 + N + K)
+    a = torch.randn(M, K, generator=g, device=DEV)
+    b = torch.randn(N, K, generator=g, device=DEV) * 0.1
+    out = gemm.gemm_tn(a, b)
+    want = (a.double() @ b.double().T)
+    err = (out.double() - want).abs().max().item()
+    scale = want.abs().max().item()
+    assert err <= 2e-6 * max(1.0, scale) * max(1.0, (K / 64) ** 0.5), (err, scale)
+
+
+def test_gemm_accumulate_residual():
+    g = torch.Generator(device=DEV).manual_seed(7)
+    a = torch.randn(200, 64, generator=g, device=DEV)
+    b = torch.randn(96, 64, generator=g, device=DEV)
+    c = torch.randn(200, 96, generator=g, device=DEV)
+    want = c.double() + a.double() @ b.double().T
+    gemm.gemm_tn(a, b, out=c, accumulate=True)
+    assert (c.double() - want).abs().max().item() <= 1e-5
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 128, 64), (77, 200, 512)])
+def test_gemm_bf16(M, N, K):
+    g = torch.Generator(device=DEV).manual_seed(3)
+    a = torch.randn(M, K, generator=g, device=DEV).bfloat16()
+    b = torch.randn(N, K, generator=g, device=DEV).bfloat16()
+    out = gemm.gemm_tn(a, b)
+    want = a.double() @ b.double().T
+    assert (out.double() - want).abs().max().item() <= 1e-3 * max(1.0, want.abs().max().item())
