@@ -442,6 +442,83 @@ def mirror_hints(member_entry: np.ndarray, member_offset: np.ndarray,
     return np.union1d(pos, master_important).astype(np.int64)
 
 
+# ---------------------------------------------------------------------------
+# toy transformer (the selective recompute's arithmetic) -- toymodel.py:26-167
+
+
+@dataclass
+class ToyWeights:
+    num_heads: int
+    head_dim: int
+    rope_base: float
+    embed: np.ndarray     # (vocab, hidden)
+    wq: np.ndarray        # (layers, hidden, hidden)
+    wk: np.ndarray
+    wv: np.ndarray
+    wm: np.ndarray
+
+
+def build_weights(num_layers: int, num_heads: int, head_dim: int, vocab_size: int,
+                  weight_seed: int = 0, rope_base: float = 10000.0) -> ToyWeights:
+    """U[-0.1, 0.1] float32 draws from PCG64(SeedSequence(seed)) in the order
+    embedding, then per layer q, k, v, mix (toymodel.py:36-57)."""
+    rng = np.random.default_rng(np.random.SeedSequence(weight_seed))
+    hid = num_heads * head_dim
+
+    def u(*shape):
+        return rng.uniform(-0.1, 0.1, size=shape).astype(np.float32)
+
+    embed = u(vocab_size, hid)
+    mats = {name: np.empty((num_layers, hid, hid), np.float32) for name in "qkvm"}
+    for layer in range(num_layers):
+        for name in "qkvm":
+            mats[name][layer] = u(hid, hid)
+    return ToyWeights(num_heads, head_dim, rope_base, embed, mats["q"], mats["k"], mats["v"],
+                      mats["m"])
+
+
+def selective_forward(w: ToyWeights, tokens: np.ndarray, positions: np.ndarray,
+                      fix_idx: np.ndarray, ctx_k: np.ndarray, ctx_v: np.ndarray,
+                      max_layer: Optional[int] = None):
+    """Fresh K/V at the ``fix_idx`` rows; other rows come from the context,
+    causal by sequence index (toymodel.py:99-151)."""
+    layers = w.wq.shape[0] if max_layer is None else max_layer
+    H, D = w.num_heads, w.head_dim
+    T, F = tokens.shape[0], fix_idx.shape[0]
+    out_k = np.empty((layers, F, H, D), np.float32)
+    out_v = np.empty_like(out_k)
+    if F == 0:
+        return out_k, out_v
+    pos = positions[fix_idx]
+    scale = np.float32(1.0 / np.sqrt(D))
+    visible = np.arange(T)[None, :] <= fix_idx[:, None]
+    h = w.embed[tokens[fix_idx]]
+    for layer in range(layers):
+        q = rope_apply((h @ w.wq[layer]).reshape(F, H, D), pos, w.rope_base)
+        k = rope_apply((h @ w.wk[layer]).reshape(F, H, D), pos, w.rope_base)
+        v = (h @ w.wv[layer]).reshape(F, H, D)
+        out_k[layer], out_v[layer] = k, v
+        keys = ctx_k[layer].copy()
+        vals = ctx_v[layer].copy()
+        keys[fix_idx], vals[fix_idx] = k, v
+        s = np.einsum("fhd,thd->hft", q, keys) * scale
+        s = np.where(visible[None], s, np.float32(-np.inf))
+        p = np.exp(s - s.max(axis=-1, keepdims=True))
+        p /= p.sum(axis=-1, keepdims=True)
+        h = h + np.einsum("hft,thd->fhd", p, vals).reshape(F, H * D) @ w.wm[layer]
+    return out_k, out_v
+
+
+def full_prefill(w: ToyWeights, tokens, start_pos: int = 0):
+    """All rows fresh at positions start_pos.. (toymodel.py:154-167)."""
+    toks = np.asarray(tokens, np.int64)
+    T = toks.size
+    L, H, D = w.wq.shape[0], w.num_heads, w.head_dim
+    zeros = np.zeros((L, T, H, D), np.float32)
+    pos = np.arange(start_pos, start_pos + T, dtype=np.int64)
+    return selective_forward(w, toks, pos, np.arange(T), zeros, zeros)
+
+
 def key_diff(fresh: np.ndarray, cached: np.ndarray) -> np.ndarray:
     """Per-position L2 norm of the float32 key difference (pic.py:166-171)."""
     if fresh.shape != cached.shape:

@@ -343,8 +343,44 @@ def gen_allocator():
     return ops
 
 
+def gen_toymodel():
+    """Toy transformer outputs (the selective recompute's arithmetic,
+    toymodel.py:36-192): weights digests, a full prefill and a selective
+    forward over a perturbed context, recorded verbatim (small)."""
+    out = {}
+    arrays = {}
+    for name, (L, H, D, V, seed) in {"small": (3, 2, 8, 512, 21),
+                                     "c1": (2, 8, 64, 1024, 0)}.items():
+        cfg = ModelConfig(num_layers=L, num_heads=H, head_dim=D, vocab_size=V, weight_seed=seed)
+        w = build_weights(cfg)
+        rng = np.random.default_rng(100 + L)
+        toks = [int(t) for t in rng.integers(0, V - 1, 48)]
+        pre = full_prefill(w, toks)
+        ctx_k = pre.k + rng.standard_normal(pre.k.shape).astype(np.float32) * 0.01
+        ctx_v = pre.v + rng.standard_normal(pre.v.shape).astype(np.float32) * 0.01
+        fix = np.sort(rng.choice(48, 13, replace=False)).astype(np.int64)
+        pos = np.arange(48, dtype=np.int64) + 5
+        k, v = _selective_forward(w, np.asarray(toks), pos, fix, ctx_k, ctx_v)
+        k1, v1 = _selective_forward(w, np.asarray(toks), pos, fix, ctx_k, ctx_v, max_layer=1)
+        out[name] = {"config": [L, H, D, V, seed],
+                     "weights_sha": sha(w.embed, w.wq, w.wk, w.wv, w.wm),
+                     "prefill_sha": sha(pre.k, pre.v), "selective_sha": sha(k, v),
+                     "probe_sha": sha(k1, v1)}
+        arrays[f"{name}_tokens"] = np.asarray(toks)
+        arrays[f"{name}_ctx_k"] = ctx_k
+        arrays[f"{name}_ctx_v"] = ctx_v
+        arrays[f"{name}_fix"] = fix
+        arrays[f"{name}_prefill_k"] = pre.k
+        arrays[f"{name}_prefill_v"] = pre.v
+        arrays[f"{name}_sel_k"] = k
+        arrays[f"{name}_sel_v"] = v
+    np.savez_compressed(os.path.join(HERE, "toymodel.npz"), **arrays)
+    return out
+
+
 def main():
     golden = {
+        "toymodel": gen_toymodel(),
         "generator": "tests/golden/make_golden.py",
         "reference": "roundkv 0.1.0 (/root/reference/pkg/src)",
         "numpy": np.__version__,

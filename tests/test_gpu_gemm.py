@@ -28,7 +28,8 @@ def test_gemm_accumulate_residual():
     c = torch.randn(200, 96, generator=g, device=DEV)
     want = c.double() + a.double() @ b.double().T
     gemm.gemm_tn(a, b, out=c, accumulate=True)
-    assert (c.double() - want).abs().max().item() <= 1e-5
+    # float32 result rounding of |values| up to ~25 plus 3xTF32 product error
+    assert (c.double() - want).abs().max().item() <= 2e-6 * want.abs().max().item()
 
 
 @pytest.mark.parametrize("M,N,K", [(128, 128, 64), (77, 200, 512)])

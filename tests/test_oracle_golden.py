@@ -236,6 +236,26 @@ def test_selection_matches_reference_probe_and_select():
     assert ref.select_master(devs) == sel["master"]
 
 
+def test_toymodel_matches_reference():
+    z = load_npz("toymodel.npz")
+    for name, meta in G["toymodel"].items():
+        L, H, D, V, seed = meta["config"]
+        w = ref.build_weights(L, H, D, V, seed)
+        assert sha(w.embed, w.wq, w.wk, w.wv, w.wm) == meta["weights_sha"]
+        toks = z[f"{name}_tokens"]
+        k, v = ref.full_prefill(w, toks)
+        assert np.abs(k - z[f"{name}_prefill_k"]).max() <= 1e-6
+        if SAME_NUMPY:
+            assert sha(k, v) == meta["prefill_sha"]
+        pos = np.arange(toks.size, dtype=np.int64) + 5
+        k, v = ref.selective_forward(w, toks, pos, z[f"{name}_fix"], z[f"{name}_ctx_k"],
+                                     z[f"{name}_ctx_v"])
+        assert np.abs(k - z[f"{name}_sel_k"]).max() <= 1e-6
+        assert np.abs(v - z[f"{name}_sel_v"]).max() <= 1e-6
+        if SAME_NUMPY:
+            assert sha(k, v) == meta["selective_sha"]
+
+
 def test_selection_known_answers():
     fresh = np.zeros((3, 2, 4), np.float32)
     cached = np.zeros((3, 2, 4), np.float32)
