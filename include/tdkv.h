@@ -244,6 +244,22 @@ int32_t tdkv_gemm(const void* d_a, int32_t lda, const void* d_b, int32_t ldb,
                   float* d_c, int32_t ldc, int32_t m, int32_t n, int32_t k,
                   int32_t dtype, int32_t accumulate, void* stream);
 
+/* K5 non-GEMM stages of one layer of the selective forward (float32 toy
+ * model, toymodel.py:111-150):
+ *   tdkv_qkv_rope: qkv (n_rows, 3*H*D) -> q, k rotated by the row's cos/sin
+ *     (double2 table rows, one per fixed row), v copied; (n_rows, H*D) each.
+ *   tdkv_attention: mix[f, h, :] = softmax_t(q[f,h].key_t * scale) . value_t
+ *     over t <= fix_idx[f]; key/value rows come from the fresh rows where
+ *     fresh_of[t] >= 0, else from the context planes (num_tokens, H*D). */
+int32_t tdkv_qkv_rope(const float* d_qkv, const void* d_table, int32_t n_rows,
+                      int32_t num_heads, int32_t head_dim, float* d_q, float* d_k,
+                      float* d_v, void* stream);
+int32_t tdkv_attention(const float* d_q, const float* d_k_fresh, const float* d_v_fresh,
+                       const float* d_ctx_k, const float* d_ctx_v,
+                       const int32_t* d_fresh_of, const int64_t* d_fix_idx,
+                       int32_t n_fix, int32_t num_tokens, int32_t num_heads,
+                       int32_t head_dim, float scale, float* d_mix, void* stream);
+
 /* Fill rows of every layer with a value (NaN poisoning of freed slots,
  * paged_pool.py:144-147).  value_bits is the element bit pattern. */
 int32_t tdkv_fill_rows(void* d_plane, int64_t layer_stride, int32_t num_layers,

@@ -89,7 +89,8 @@ assert DIFF_PAIR.itemsize == 32 and DIFF_OUT.itemsize == 40 and ROWS_JOB.itemsiz
 EXPORTS = (
     "tdkv_version", "tdkv_last_error", "tdkv_launch_count", "tdkv_rope_table",
     "tdkv_collect", "tdkv_diff_compare", "tdkv_diff_compact", "tdkv_rows",
-    "tdkv_keydiff", "tdkv_select_important", "tdkv_gemm", "tdkv_fill_rows",
+    "tdkv_keydiff", "tdkv_select_important", "tdkv_gemm", "tdkv_qkv_rope", "tdkv_attention",
+    "tdkv_fill_rows",
 )
 
 _P = ctypes.c_void_p
@@ -112,6 +113,9 @@ _SIGS = {
     "tdkv_keydiff": (_I32, [_P, _P, _P, _I64, _I32, _I32, _P, _P]),
     "tdkv_select_important": (_I32, [_P, _P, _P, _I32, _I32, _P, _P, _P, _P]),
     "tdkv_gemm": (_I32, [_P, _I32, _P, _I32, _P, _I32, _I32, _I32, _I32, _I32, _I32, _P]),
+    "tdkv_qkv_rope": (_I32, [_P, _P, _I32, _I32, _I32, _P, _P, _P, _P]),
+    "tdkv_attention": (_I32, [_P, _P, _P, _P, _P, _P, _P, _I32, _I32, _I32, _I32,
+                              ctypes.c_float, _P, _P]),
 }
 
 _lib: Optional[ctypes.CDLL] = None

@@ -1,0 +1,154 @@
+// K5 selective recompute, non-GEMM stages (reference: toymodel._selective_
+// forward, toymodel.py:99-151).  Per layer the host runs
+//   tdkv_gemm      qkv = h @ [Wq | Wk | Wv]           (tensor cores)
+//   tdkv_qkv_rope  q, k rotated to the fixed rows' positions (float64
+//                  rotation, bit-compatible with rope_apply), k and v written
+//                  to the layer's output planes
+//   tdkv_attention causal softmax attention of every fixed row over the
+//                  context, fresh rows overriding cached ones
+//   tdkv_gemm      h += mix @ Wm                       (tensor cores)
+#include "tdkv_common.cuh"
+
+namespace tdkv {
+
+__global__ void qkv_rope_kernel(const float* __restrict__ qkv, const double2* __restrict__ table,
+                                int F, int H, int D, float* __restrict__ q_out,
+                                float* __restrict__ k_out, float* __restrict__ v_out) {
+    const int hid = H * D;
+    const int half = D >> 1;
+    const long long pairs = (long long)F * (hid >> 1);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < pairs;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int f = (int)(i / (hid >> 1));
+        const int p = (int)(i - (long long)f * (hid >> 1));    // pair index within the row
+        const int e = 2 * p;
+        const int j = (e % D) >> 1;                              // pair index within the head
+        const double2 cs = table[(size_t)f * half + j];
+        const float* row = qkv + (size_t)f * 3 * hid;
+        float qx = row[e], qy = row[e + 1];
+        float kx = row[hid + e], ky = row[hid + e + 1];
+        rot_pair(qx, qy, cs);
+        rot_pair(kx, ky, cs);
+        q_out[(size_t)f * hid + e] = qx;
+        q_out[(size_t)f * hid + e + 1] = qy;
+        k_out[(size_t)f * hid + e] = kx;
+        k_out[(size_t)f * hid + e + 1] = ky;
+        v_out[(size_t)f * hid + e] = row[2 * hid + e];
+        v_out[(size_t)f * hid + e + 1] = row[2 * hid + e + 1];
+    }
+}
+
+// One CTA per (fixed row f, head h).  Keys/values of row t come from the
+// fresh rows when fresh_of[t] >= 0, else from the context planes; row f sees
+// t <= fix_idx[f] (causal by sequence index).
+__global__ void __launch_bounds__(128)
+    attention_kernel(const float* __restrict__ q, const float* __restrict__ k_fresh,
+                     const float* __restrict__ v_fresh, const float* __restrict__ ctx_k,
+                     const float* __restrict__ ctx_v, const int32_t* __restrict__ fresh_of,
+                     const int64_t* __restrict__ fix_idx, int H, int D, float scale,
+                     float* __restrict__ mix) {
+    extern __shared__ float s_score[];
+    __shared__ float s_q[256];
+    __shared__ float s_red[32];
+    __shared__ double s_redd[32];
+    const int f = blockIdx.x, h = blockIdx.y;
+    const int hid = H * D;
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int tn = (int)fix_idx[f] + 1;
+    for (int d = tid; d < D; d += nthr) s_q[d] = q[(size_t)f * hid + h * D + d];
+    __syncthreads();
+
+    float mx = -INFINITY;
+    for (int t = tid; t < tn; t += nthr) {
+        const int fr = fresh_of[t];
+        const float* kr = fr >= 0 ? k_fresh + (size_t)fr * hid + h * D : ctx_k + (size_t)t * hid + h * D;
+        float acc = 0.f;
+        for (int d = 0; d < D; ++d) acc = fmaf(s_q[d], kr[d], acc);
+        const float sc = acc * scale;
+        s_score[t] = sc;
+        mx = fmaxf(mx, sc);
+    }
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((tid & 31) == 0) s_red[tid >> 5] = mx;
+    __syncthreads();
+    if (tid == 0) {
+        float m = -INFINITY;
+        for (int w = 0; w < (nthr >> 5); ++w) m = fmaxf(m, s_red[w]);
+        s_red[0] = m;
+    }
+    __syncthreads();
+    mx = s_red[0];
+    double sum = 0.0;
+    for (int t = tid; t < tn; t += nthr) {
+        const float e = expf(s_score[t] - mx);
+        s_score[t] = e;
+        sum += (double)e;
+    }
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    __syncthreads();
+    if ((tid & 31) == 0) s_redd[tid >> 5] = sum;
+    __syncthreads();
+    if (tid == 0) {
+        double s = 0.0;
+        for (int w = 0; w < (nthr >> 5); ++w) s += s_redd[w];
+        s_redd[0] = s;
+    }
+    __syncthreads();
+    const float total = (float)s_redd[0];
+    for (int t = tid; t < tn; t += nthr) s_score[t] = s_score[t] / total;
+    __syncthreads();
+    for (int d = tid; d < D; d += nthr) {
+        double acc = 0.0;
+        for (int t = 0; t < tn; ++t) {
+            const int fr = fresh_of[t];
+            const float vv = fr >= 0 ? v_fresh[(size_t)fr * hid + h * D + d]
+                                     : ctx_v[(size_t)t * hid + h * D + d];
+            acc += (double)s_score[t] * (double)vv;
+        }
+        mix[(size_t)f * hid + h * D + d] = (float)acc;
+    }
+}
+
+}  // namespace tdkv
+
+using namespace tdkv;
+
+extern "C" int32_t tdkv_qkv_rope(const float* d_qkv, const void* d_table, int32_t n_rows,
+                                 int32_t num_heads, int32_t head_dim, float* d_q, float* d_k,
+                                 float* d_v, void* stream) {
+    if (n_rows < 0 || num_heads <= 0 || head_dim <= 0 || (head_dim & 1))
+        return set_error(TDKV_EINVAL, "tdkv_qkv_rope: bad geometry");
+    if (n_rows == 0) return TDKV_OK;
+    if (!d_qkv || !d_table || !d_q || !d_k || !d_v)
+        return set_error(TDKV_EINVAL, "tdkv_qkv_rope: null pointer");
+    const long long pairs = (long long)n_rows * num_heads * head_dim / 2;
+    long long grid = (pairs + 255) / 256;
+    if (grid > sm_count() * 8) grid = sm_count() * 8;
+    qkv_rope_kernel<<<(unsigned)grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        d_qkv, static_cast<const double2*>(d_table), n_rows, num_heads, head_dim, d_q, d_k, d_v);
+    count_launch();
+    return check_launch("tdkv_qkv_rope");
+}
+
+extern "C" int32_t tdkv_attention(const float* d_q, const float* d_k_fresh, const float* d_v_fresh,
+                                  const float* d_ctx_k, const float* d_ctx_v,
+                                  const int32_t* d_fresh_of, const int64_t* d_fix_idx,
+                                  int32_t n_fix, int32_t num_tokens, int32_t num_heads,
+                                  int32_t head_dim, float scale, float* d_mix, void* stream) {
+    if (n_fix < 0 || num_tokens <= 0 || num_heads <= 0 || head_dim <= 0 || head_dim > 256)
+        return set_error(TDKV_EINVAL, "tdkv_attention: bad geometry");
+    if (n_fix == 0) return TDKV_OK;
+    const size_t smem = (size_t)num_tokens * sizeof(float);
+    if (smem > 200 * 1024)
+        return set_error(TDKV_EUNSUPPORTED, "tdkv_attention: %d tokens exceed shared memory",
+                         num_tokens);
+    if (cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+        return check_launch("tdkv_attention: cudaFuncSetAttribute");
+    dim3 grid(n_fix, num_heads);
+    attention_kernel<<<grid, 128, smem, static_cast<cudaStream_t>(stream)>>>(
+        d_q, d_k_fresh, d_v_fresh, d_ctx_k, d_ctx_v, d_fresh_of, d_fix_idx, num_heads, head_dim,
+        scale, d_mix);
+    count_launch();
+    return check_launch("tdkv_attention");
+}

@@ -1,0 +1,187 @@
+"""Selective recompute of deviating tokens on the B200 (reference:
+roundkv/toymodel.py:99-192 and pic.refresh, pic.py:284-300).
+
+The reference recomputes the important and structural rows of a prompt
+with its seeded toy transformer (embedding, per layer Q/K/V projections
+with rotary Q/K, causal softmax attention over the partly cached context,
+output mix folded into the residual stream; float32).  Here every
+projection is a tensor-core GEMM (``tdkv_gemm``: tcgen05, TMEM accumulator,
+3xTF32 for float32 operands), the rotary step and the attention are
+``tdkv_qkv_rope`` / ``tdkv_attention``, and the embedding gather and the
+row write-back use the row mover (K3).  The final layer's attention and
+mix are skipped: their only consumer is the next layer.
+
+Signatures follow the reference: ``selective_forward`` (= _selective_forward),
+``full_prefill``, ``recompute_positions`` and ``refresh``; ``weights`` is the
+reference's ``ModelWeights`` (or anything with ``config``, ``embed``,
+``wq/wk/wv/wm``).
+"""
+from __future__ import annotations
+
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _kernels, _lib
+from ._device import default_device, h2d, is_host, ptr, stream_handle, to_device, to_host
+from .core import LayeredKv
+from .gemm import gemm_tn
+from .ledger import CostLedger
+
+
+def _cfg(weights):
+    cfg = getattr(weights, "config", weights)
+    return (int(cfg.num_layers if hasattr(cfg, "num_layers") else weights.wq.shape[0]),
+            int(cfg.num_heads), int(cfg.head_dim), float(getattr(cfg, "rope_base", 10000.0)))
+
+
+class ToyModel:
+    """Device-resident weights: embedding, [Wq|Wk|Wv]^T per layer (3*hid, hid)
+    and Wm^T per layer (hid, hid), all float32 (K-major GEMM operands)."""
+
+    _cache: dict = {}
+
+    def __init__(self, weights, device: torch.device) -> None:
+        self.num_layers, self.num_heads, self.head_dim, self.rope_base = _cfg(weights)
+        hid = self.num_heads * self.head_dim
+        if hid % 4:
+            raise ValueError("hidden size must be a multiple of 4 (16-byte GEMM rows)")
+        self.hidden = hid
+        self.device = device
+        self.embed = to_device(np.asarray(weights.embed, np.float32), device)
+        wq, wk, wv, wm = (np.asarray(getattr(weights, n), np.float32) for n in ("wq", "wk", "wv", "wm"))
+        qkv_t = np.concatenate([wq.transpose(0, 2, 1), wk.transpose(0, 2, 1),
+                                wv.transpose(0, 2, 1)], axis=1)
+        self.wqkv_t = to_device(np.ascontiguousarray(qkv_t), device)
+        self.wm_t = to_device(np.ascontiguousarray(wm.transpose(0, 2, 1)), device)
+
+    @classmethod
+    def of(cls, weights, device: Optional[torch.device] = None) -> "ToyModel":
+        if isinstance(weights, ToyModel):
+            return weights
+        device = device or default_device()
+        key = (id(weights), device)
+        m = cls._cache.get(key)
+        if m is None or m._src is not weights:
+            m = cls(weights, device)
+            m._src = weights
+            cls._cache[key] = m
+        return m
+
+
+def selective_forward(weights, tokens, positions, fix_idx, ctx_k, ctx_v,
+                      max_layer: Optional[int] = None):
+    """Fresh K/V rows at ``fix_idx`` against the cached context; returns
+    (k, v) of shape (layers_run, F, H, D) -- numpy for numpy contexts."""
+    host = is_host(ctx_k)
+    dev = ctx_k.device if isinstance(ctx_k, torch.Tensor) else default_device()
+    m = ToyModel.of(weights, dev)
+    H, D, hid = m.num_heads, m.head_dim, m.hidden
+    toks = np.asarray(tokens, np.int64)
+    pos = np.asarray(positions, np.int64)
+    fix = np.asarray(fix_idx, np.int64)
+    T, F = toks.size, fix.size
+    layers = m.num_layers if max_layer is None else int(max_layer)
+    out_k = torch.empty((layers, F, H, D), dtype=torch.float32, device=dev)
+    out_v = torch.empty_like(out_k)
+    if F and layers:
+        ck = to_device(ctx_k, dev, torch.float32)
+        cv = to_device(ctx_v, dev, torch.float32)
+        _forward(m, toks, pos, fix, ck, cv, layers, out_k, out_v)
+    if host:
+        return to_host(out_k), to_host(out_v)
+    return out_k, out_v
+
+
+def _forward(m: ToyModel, toks, pos, fix, ck, cv, layers, out_k, out_v) -> int:
+    dev = m.device
+    H, D, hid = m.num_heads, m.head_dim, m.hidden
+    T, F = toks.size, fix.size
+    stream = stream_handle(dev)
+    d_fix = h2d(fix, dev)
+    fresh_of = np.full(T, -1, np.int32)
+    fresh_of[fix] = np.arange(F, dtype=np.int32)
+    d_fresh_of = h2d(fresh_of, dev)
+    table = _kernels.rope_table(pos[fix], D, m.rope_base, torch.float32, dev)
+    # h = embed[tokens[fix]] (row mover, K-only gather)
+    h = torch.empty((F, hid), dtype=torch.float32, device=dev)
+    d_tok = h2d(toks[fix], dev)
+    job = _kernels.rows_job(m.embed, None, 0, h, None, 0, F, src_rows=d_tok)
+    _kernels.rows(_kernels.rows_jobs([job]), F, None, 1, 1, hid, _kernels.ROWS_BLOCK,
+                  torch.float32, dev)
+    qkv = torch.empty((F, 3 * hid), dtype=torch.float32, device=dev)
+    q = torch.empty((F, hid), dtype=torch.float32, device=dev)
+    mix = torch.empty((F, hid), dtype=torch.float32, device=dev)
+    scale = float(np.float32(1.0 / np.sqrt(D)))
+    launches = 2
+    for layer in range(layers):
+        gemm_tn(h, m.wqkv_t[layer], out=qkv)
+        _lib.call("tdkv_qkv_rope", ptr(qkv), ptr(table), F, H, D, ptr(q), ptr(out_k[layer]),
+                  ptr(out_v[layer]), stream)
+        launches += 2
+        if layer == layers - 1:
+            break                       # the last layer's attention only feeds h
+        _lib.call("tdkv_attention", ptr(q), ptr(out_k[layer]), ptr(out_v[layer]),
+                  ptr(ck[layer]), ptr(cv[layer]), ptr(d_fresh_of), ptr(d_fix), F, T, H, D,
+                  scale, ptr(mix), stream)
+        gemm_tn(mix, m.wm_t[layer], out=h, accumulate=True)
+        launches += 2
+    return launches
+
+
+def full_prefill(weights, tokens: Sequence[int], start_pos: int = 0) -> LayeredKv:
+    """Ground-truth prefill of every row (toymodel.py:154-167), on the device;
+    returns host float32 planes like the reference."""
+    toks = np.asarray(tokens, dtype=np.int64)
+    L, H, D, _ = _cfg(weights)
+    vocab = int(np.asarray(weights.embed).shape[0])
+    if toks.ndim != 1 or toks.size == 0:
+        raise ValueError("tokens must be one non-empty sequence")
+    if toks.min() < 0 or toks.max() >= vocab:
+        raise ValueError("token id out of vocabulary range")
+    T = toks.size
+    positions = np.arange(start_pos, start_pos + T, dtype=np.int64)
+    zeros = np.zeros((L, T, H, D), np.float32)
+    k, v = selective_forward(weights, toks, positions, np.arange(T), zeros, zeros)
+    return LayeredKv(k, v, positions)
+
+
+def recompute_positions(weights, tokens, positions_to_fix, context_kv: LayeredKv):
+    """(sorted fix indices, k rows, v rows) against a cached context
+    (toymodel.py:170-192)."""
+    toks = np.asarray(tokens, dtype=np.int64)
+    if toks.shape[0] != context_kv.num_tokens:
+        raise ValueError("context must cover the full token sequence")
+    L = _cfg(weights)[0]
+    if context_kv.num_layers != L:
+        raise ValueError("context layer count does not match the model")
+    fix = np.unique(np.asarray(list(positions_to_fix), dtype=np.int64))
+    if fix.size and (fix[0] < 0 or fix[-1] >= toks.shape[0]):
+        raise ValueError("fix index out of range")
+    k, v = selective_forward(weights, toks, context_kv.positions, fix, context_kv.k,
+                             context_kv.v)
+    return fix, k, v
+
+
+def refresh(weights, prep, context, important: np.ndarray,
+            ledger: Optional[CostLedger] = None) -> None:
+    """Recompute important and structural positions together at all layers
+    and write them into the member's context (pic.py:284-300)."""
+    fix = np.union1d(important, prep.structural_idx).astype(np.int64)
+    if fix.size == 0:
+        return
+    ctx_k, ctx_v = context
+    k, v = selective_forward(weights, prep.tokens, prep.positions, fix, ctx_k, ctx_v)
+    if is_host(ctx_k):
+        ctx_k[:, fix] = k
+        ctx_v[:, fix] = v
+    else:
+        L, F, H, D = k.shape
+        T = int(ctx_k.shape[1])
+        d_fix = h2d(fix, ctx_k.device)
+        job = _kernels.rows_job(k, v, F * H * D, ctx_k, ctx_v, T * H * D, F, dst_rows=d_fix)
+        _kernels.rows(_kernels.rows_jobs([job]), F, None, L, H, D, _kernels.ROWS_BLOCK,
+                      ctx_k.dtype, ctx_k.device)
+    if ledger is not None:
+        ledger.record_recomputed(int(fix.size))
