@@ -38,7 +38,7 @@ from roundkv.ledger import CostLedger  # noqa: E402
 from roundkv.paged_pool import PagedPool  # noqa: E402
 from roundkv.collective import select_master  # noqa: E402
 from roundkv.pic import (PicConfig, _skeleton, align_cached, key_diff,  # noqa: E402
-                         prepare_request, probe_and_select)
+                         prepare_request, probe_and_select, recover_prepared)
 from roundkv.toymodel import _selective_forward  # noqa: E402
 from roundkv.restore import dense_restore, fused_restore  # noqa: E402
 from roundkv.segment_index import SegmentCacheEntry, SegmentIndex  # noqa: E402
@@ -378,8 +378,69 @@ def gen_toymodel():
     return out
 
 
+def gen_recovery():
+    """collective_recover (and serial recover_prepared) on two decode-seeded
+    rounds: everything a duck-typed PreparedRequest needs, and the
+    reference's results (caches, important sets, deviations, master, hints)."""
+    meta = {}
+    arrays = {}
+    for case, (agents, perm_seed, hist, blen) in {"same_order": (3, None, 12, 6),
+                                                  "permuted": (4, 17, 9, 7)}.items():
+        model = ModelConfig(num_layers=3, num_heads=2, head_dim=8, vocab_size=512,
+                            weight_seed=21)
+        weights = build_weights(model)
+        spec = WorkloadSpec(num_agents=agents, num_rounds=1, history_len=hist,
+                            shared_block_len=blen, token_seed=31, permutation_seed=perm_seed)
+        rnd = generate_round(spec, model, 0)
+        index = SegmentIndex(budget_bytes=1 << 30)
+        seg_rows = []
+        for agent, seg in enumerate(rnd.shared_outputs):
+            ctx = decode_context(spec, model, 0, agent)
+            stream = list(ctx) + [model.separator_token] + list(seg.tokens)
+            kv = full_prefill(weights, stream)
+            lo = len(ctx) + 1
+            rows = LayeredKv(kv.k[:, lo:].copy(), kv.v[:, lo:].copy(), kv.positions[lo:].copy())
+            index.insert(SegmentCacheEntry(seg.digest, rows.positions, SimpleNamespace(kv=rows),
+                                           token_digest(ctx), rows.dense_nbytes))
+            seg_rows.append(rows)
+            arrays[f"{case}_seg{agent}_k"] = rows.k
+            arrays[f"{case}_seg{agent}_v"] = rows.v
+            arrays[f"{case}_seg{agent}_pos"] = rows.positions
+        preps = [prepare_request(rnd.prompts[a], model, index, request_id=a)
+                 for a in range(agents)]
+        groups, _ = form_groups(preps)
+        pic = PicConfig(0.15, 1)
+        results, plan = collective_recover(weights, groups[0], pic, CostLedger(3))
+        serial = recover_prepared(weights, preps[0], pic, CostLedger(3))
+        m = {"agents": agents, "members": [], "master_id": int(plan.master_id),
+             "fraction": 0.15, "check_layer": 1, "model": [3, 2, 8, 512, 21]}
+        for p in preps:
+            rid = p.request_id
+            for name in ("tokens", "positions", "private_idx", "structural_idx", "label_entry",
+                         "label_offset"):
+                arrays[f"{case}_r{rid}_{name}"] = np.asarray(getattr(p, name))
+            arrays[f"{case}_r{rid}_k"] = results[rid].kv.k
+            arrays[f"{case}_r{rid}_v"] = results[rid].kv.v
+            m["members"].append({
+                "rid": rid,
+                "hits": [{"seg": seg_rows.index(h.kv), "target": h.target_idx.tolist()}
+                         for h in p.hits],
+                "important": plan.important[rid].tolist(),
+                "deviation": plan.deviation_scores[rid],
+                "hints": (plan.mirror_diff_hints[rid].tolist()
+                          if rid in plan.mirror_diff_hints else None),
+                "num_recomputed": results[rid].num_recomputed,
+            })
+        arrays[f"{case}_serial0_k"] = serial.kv.k
+        arrays[f"{case}_serial0_v"] = serial.kv.v
+        meta[case] = m
+    np.savez_compressed(os.path.join(HERE, "recovery.npz"), **arrays)
+    return meta
+
+
 def main():
     golden = {
+        "recovery": gen_recovery(),
         "toymodel": gen_toymodel(),
         "generator": "tests/golden/make_golden.py",
         "reference": "roundkv 0.1.0 (/root/reference/pkg/src)",

@@ -1,0 +1,101 @@
+"""End-to-end recovery on the GPU (Collector K1 + selective recompute K5 +
+selection K4) against the reference's own collective_recover /
+recover_prepared outputs (tests/golden/recovery.npz)."""
+import numpy as np
+import pytest
+
+from helpers import load_golden, load_npz
+from oracle import roundkv_port as ref
+from paper_2604_03143_b200 import pic
+from paper_2604_03143_b200.core import LayeredKv
+from paper_2604_03143_b200.ledger import CostLedger
+
+pytestmark = pytest.mark.gpu
+G = load_golden()["recovery"]
+TOL = 1e-5
+
+
+class _Cfg:
+    def __init__(self, L, H, D, V):
+        self.num_layers, self.num_heads, self.head_dim, self.vocab_size = L, H, D, V
+        self.rope_base = 10000.0
+
+
+class _Weights:
+    def __init__(self, L, H, D, V, seed):
+        w = ref.build_weights(L, H, D, V, seed)
+        self.config = _Cfg(L, H, D, V)
+        self.embed, self.wq, self.wk, self.wv, self.wm = w.embed, w.wq, w.wk, w.wv, w.wm
+
+
+class _Hit:
+    def __init__(self, kv, target):
+        self.kv = kv
+        self.target_idx = np.asarray(target, np.int64)
+        self.delta = self.target_idx - kv.positions
+
+    def __len__(self):
+        return int(self.target_idx.size)
+
+
+class _Prep:
+    def __init__(self, z, case, m, segs):
+        rid = m["rid"]
+        self.request_id = rid
+        for name in ("tokens", "positions", "private_idx", "structural_idx", "label_entry",
+                     "label_offset"):
+            setattr(self, name, z[f"{case}_r{rid}_{name}"])
+        self.hits = [_Hit(segs[h["seg"]], h["target"]) for h in m["hits"]]
+
+    @property
+    def num_tokens(self):
+        return int(self.tokens.size)
+
+    @property
+    def shared_idx(self):
+        if not self.hits:
+            return np.empty(0, dtype=np.int64)
+        return np.sort(np.concatenate([h.target_idx for h in self.hits]))
+
+
+class _Pic:
+    recompute_fraction = 0.15
+    check_layer = 1
+
+
+def _world(case):
+    z = load_npz("recovery.npz")
+    meta = G[case]
+    segs = [LayeredKv(z[f"{case}_seg{a}_k"], z[f"{case}_seg{a}_v"], z[f"{case}_seg{a}_pos"])
+            for a in range(meta["agents"])]
+    preps = [_Prep(z, case, m, segs) for m in meta["members"]]
+    return z, meta, preps, _Weights(*meta["model"])
+
+
+@pytest.mark.parametrize("case", ["same_order", "permuted"])
+def test_collective_recover_matches_reference(case):
+    z, meta, preps, w = _world(case)
+    group = type("G", (), {"members": preps})
+    led = CostLedger(3)
+    results, plan = pic.collective_recover(w, group, _Pic, led)
+    assert led.rope_calls_by_layer == [1, 1, 1] and led.selection_passes == 1
+    assert plan.master_id == meta["master_id"]
+    for m in meta["members"]:
+        rid = m["rid"]
+        r = results[rid]
+        assert r.important_positions.tolist() == m["important"]
+        assert abs(r.deviation_score - m["deviation"]) <= 1e-5 * max(1.0, abs(m["deviation"]))
+        assert r.num_recomputed == m["num_recomputed"]
+        assert np.abs(r.kv.k.cpu().numpy() - z[f"{case}_r{rid}_k"]).max() <= TOL
+        assert np.abs(r.kv.v.cpu().numpy() - z[f"{case}_r{rid}_v"]).max() <= TOL
+        if m["hints"] is not None:
+            assert plan.mirror_diff_hints[rid].tolist() == m["hints"]
+
+
+def test_serial_recovery_matches_reference():
+    z, meta, preps, w = _world("permuted")
+    led = CostLedger(3)
+    r = pic.recover_prepared(w, preps[0], _Pic, led)
+    assert led.rope_calls_by_layer == [1, 1, 1] and led.selection_passes == 1
+    assert np.abs(r.kv.k.cpu().numpy() - z["permuted_serial0_k"]).max() <= TOL
+    assert np.abs(r.kv.v.cpu().numpy() - z["permuted_serial0_v"]).max() <= TOL
