@@ -428,6 +428,7 @@ def run_tdkv(args):
     if not args.no_codec and not args.profile:
         line["codec"] = codec_bench(tk, spec, pool, maps, dev, args, peak)
         line["selection"] = selection_bench(tk, spec, pool, maps, dev, args, peak)
+        line["recompute"] = recompute_bench(dev, args)
 
     if not args.no_cpu and not args.profile and rank == 0 and world == 1:
         line["cpu_baseline"] = cpu_baseline(spec, args.cpu_seconds)
@@ -483,6 +484,75 @@ def selection_bench(tk, spec, pool, maps, dev, args, peak):
             "device_ms": round(tk_s * 1e3, 4),
             "bytes": "fresh + cached check-layer rows read once (+ magnitudes); whole API call "
                      "incl. the host read of important sets and deviations"}
+
+
+def recompute_bench(dev, args):
+    """K5: the tensor-core projection GEMM at a Qwen2.5-7B-shaped selective
+    recompute (2048 deviating rows x fused QKV 3584 -> 4608), bf16 and
+    3xTF32, against the measured bf16 peak; plus the toy model's refresh of
+    a C1 round (8 agents) timed against the oracle on the host."""
+    import torch
+    from paper_2604_03143_b200 import gemm, recompute
+    from oracle import roundkv_port as ref
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except Exception:   # noqa: BLE001
+        pass
+    bf16_peak = float(peaks.get("bf16_tflops", 1590.0))
+    out = {}
+    M, N, K = 2048, 4608, 3584
+    g = torch.Generator(device=dev).manual_seed(1)
+    for name, dt, rounds_ in (("bf16", torch.bfloat16, 20), ("tf32x3", torch.float32, 5)):
+        a = torch.randn(M, K, generator=g, device=dev).to(dt)
+        b = torch.randn(N, K, generator=g, device=dev).to(dt)
+        c = torch.empty(M, N, device=dev)
+        gemm.gemm_tn(a, b, out=c)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(rounds_):
+            gemm.gemm_tn(a, b, out=c)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        t = e0.elapsed_time(e1) * 1e-3 / rounds_
+        tflops = 2.0 * M * N * K / t / 1e12
+        out[f"gemm_{name}"] = {"shape": [M, N, K], "ms": round(t * 1e3, 4),
+                               "tflops": round(tflops, 1),
+                               "frac_of_bf16_peak": round(tflops / bf16_peak, 4)}
+    # toy-model refresh of a C1-shaped round (L=2, H=8, D=64), 8 agents
+    w = ref.build_weights(2, 8, 64, 1024, 0)
+
+    class _W:
+        config = type("C", (), {"num_layers": 2, "num_heads": 8, "head_dim": 64,
+                                "rope_base": 10000.0})
+        embed, wq, wk, wv, wm = w.embed, w.wq, w.wk, w.wv, w.wm
+    rng = np.random.default_rng(3)
+    T = 1092
+    toks = rng.integers(0, 1023, T)
+    ctx_k = rng.standard_normal((2, T, 8, 64)).astype(np.float32) * 0.1
+    ctx_v = rng.standard_normal((2, T, 8, 64)).astype(np.float32) * 0.1
+    fixes = [np.union1d(np.sort(rng.choice(np.arange(65, T), 154, replace=False)),
+                        [64, 321, 578, 835]).astype(np.int64) for _ in range(8)]
+    dk, dv = torch.from_numpy(ctx_k).to(dev), torch.from_numpy(ctx_v).to(dev)
+    pos = np.arange(T, dtype=np.int64)
+    for f in fixes[:2]:
+        recompute.selective_forward(_W, toks, pos, f, dk, dv)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for f in fixes:
+        recompute.selective_forward(_W, toks, pos, f, dk, dv)
+    torch.cuda.synchronize(dev)
+    gpu_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    for f in fixes[:2]:
+        ref.selective_forward(w, toks, pos, f, ctx_k, ctx_v)
+    cpu_s = (time.perf_counter() - t0) * len(fixes) / 2
+    out["toy_refresh_c1"] = {"agents": 8, "rows_per_agent": int(fixes[0].size),
+                             "gpu_ms": round(gpu_s * 1e3, 3),
+                             "cpu_oracle_ms_1core": round(cpu_s * 1e3, 1),
+                             "speedup": round(cpu_s / gpu_s, 1)}
+    return out
 
 
 def rounds_segment_starts(spec, a):

@@ -20,6 +20,9 @@ from .ledger import CostLedger
 from .paged_pool import OutOfSlotsError, PagedPool, SlotMap, UseAfterFreeError, slot_maps_disjoint
 from .restore import dense_restore, fused_restore, fused_restore_many
 from .rope import rope_apply, rope_recover
+from .gemm import gemm_tn
+from .pic import RecoveryResult, ReusePlan, collective_recover, probe_and_select, recover_prepared
+from .recompute import ToyModel, full_prefill, recompute_positions, refresh, selective_forward
 from .select import (batched_selection, key_diff, mirror_hint_positions, recompute_budget,
                      select_important, select_master)
 
@@ -30,7 +33,9 @@ __all__ = [
     "CostLedger", "DiffStore", "FamilyEncoding", "HintSoundnessError", "KVCollector",
     "LayerDiff", "LayeredKv", "MalformedDiffError", "MasterArena", "MasterEntry",
     "MirrorHandle", "OutOfSlotsError", "PagedPool", "PinnedMasterError", "PositionSpan",
-    "SlotArena", "SlotMap", "TdkvError", "TdkvUnavailable", "UseAfterFreeError", "align_cached", "batched_selection", "key_diff",
+    "SlotArena", "SlotMap", "TdkvError", "TdkvUnavailable", "UseAfterFreeError", "align_cached", "gemm_tn", "RecoveryResult", "ReusePlan",
+    "collective_recover", "probe_and_select", "recover_prepared", "ToyModel", "full_prefill",
+    "recompute_positions", "refresh", "selective_forward", "batched_selection", "key_diff",
     "mirror_hint_positions", "recompute_budget", "select_important", "select_master",
     "build_library", "dense_restore", "deserialize_diff", "diff_decode_dense", "encode_batch",
     "encode_diff", "family_cost_from_ratio", "fused_restore", "fused_restore_many",
