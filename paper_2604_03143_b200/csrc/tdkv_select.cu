@@ -157,6 +157,7 @@ __global__ void __launch_bounds__(512)
             }
             const int before = incl - local;
             const int rem = s_rem;
+            __syncwarp();                         // every lane has read s_rem before one rewrites it
             if (before < rem && incl >= rem) {
                 int acc = before;
 #pragma unroll
