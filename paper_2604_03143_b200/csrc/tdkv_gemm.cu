@@ -9,19 +9,19 @@
 //     split with cvt.rna.tf32) so the products keep ~22 mantissa bits and
 //     the result stays within float32 tolerance of the reference's numpy
 //     float32 matmul; bf16 operands run as kind::f16 (bf16) directly.
-//   * one CTA = one 128 x BN output tile, 128 threads: all threads stage
-//     K-blocks of 32 elements of A and B into shared memory in the canonical
-//     no-swizzle K-major core-matrix layout (8 rows x 16 B per core matrix),
-//     one elected thread issues the MMAs and commits them to an mbarrier,
-//     double-buffered so the next K-block's staging overlaps the MMAs; the
-//     epilogue reads the accumulator with tcgen05.ld and stores (or adds, for
-//     the residual update h += mix @ Wm) float32 rows.
+//   * one CTA = one 128 x BN output tile, 128 threads: cp.async streams
+//     128-byte K-slices of A and B (zero-filled past the edges) into a 3-4
+//     stage shared-memory ring in the canonical no-swizzle K-major
+//     core-matrix layout (8 rows x 16 B per core matrix); one elected thread
+//     issues the MMAs of a stage and commits them to that stage's mbarrier,
+//     which gates the stage's refill; the epilogue reads the accumulator with
+//     tcgen05.ld and stores (or adds, for the residual update h += mix @ Wm)
+//     float32 rows.
 #include "tdkv_common.cuh"
 
 namespace tdkv {
 
 constexpr int kGemmBM = 128;
-constexpr int kGemmBK = 32;          // elements of K per stage (128 B of tf32 per row)
 
 __device__ __forceinline__ uint32_t tf32_rna(float x) {
     uint32_t r;
@@ -94,25 +94,35 @@ __device__ __forceinline__ uint32_t core_off(int r, int c16, int ck) {
     return (uint32_t)((((r >> 3) * ck + c16) << 7) + ((r & 7) << 4));
 }
 
+__device__ __forceinline__ void cp_async_16_zfill(void* smem_dst, const void* gsrc, int src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem_dst)),
+                 "l"(gsrc), "r"(src_bytes)
+                 : "memory");
+}
+
 // T = float (3xTF32) or __nv_bfloat16.  A: (M, lda) row-major, B: (N, ldb)
-// row-major (= K-major both), C: (M, ldc) float32.  BN <= 256, multiple of 16.
-template <typename T, int BN>
+// row-major (= K-major both), C: (M, ldc) float32.  BN <= 256, multiple of
+// 16.  Each pipeline stage holds 128 bytes of K per row (32 tf32 / 64 bf16
+// elements) for A and B, filled by cp.async (zero-filled past M, N, K);
+// kStages - 1 stages are in flight while the tensor core consumes one.
+template <typename T, int BN, int kStages>
 __global__ void __launch_bounds__(128, 1)
     gemm_tn_kernel(const T* __restrict__ A, int lda, const T* __restrict__ B, int ldb,
                    float* __restrict__ C, int ldc, int M, int N, int K, int accumulate_c) {
     constexpr bool kTF32 = sizeof(T) == 4;
     constexpr int kEsz = sizeof(T);
     constexpr int kChunkElems = 16 / kEsz;                 // elements per 16-byte chunk
-    constexpr int kCk = kGemmBK * kEsz / 16;               // chunks per row per K-block
+    constexpr int kCk = 8;                                 // 16-byte chunks per row per stage
+    constexpr int kBK = kCk * kChunkElems;                 // K elements per stage
     constexpr int kPlanes = kTF32 ? 2 : 1;                 // hi/lo split for tf32
-    constexpr int kABytes = kGemmBM * kGemmBK * kEsz;      // one plane of an A stage
-    constexpr int kBBytes = BN * kGemmBK * kEsz;
+    constexpr int kABytes = kGemmBM * kCk * 16;            // one plane of an A stage
+    constexpr int kBBytes = BN * kCk * 16;
     constexpr int kStageBytes = kPlanes * (kABytes + kBBytes);
-    constexpr int kUmmaK = 32 / kEsz;                      // 8 tf32 or 16 bf16 per MMA
+    constexpr int kUmmaSteps = kCk / 2;                    // MMA-K = 32 bytes = 2 chunks
     constexpr uint32_t kTmemCols = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
 
     extern __shared__ __align__(1024) uint8_t smem[];
-    __shared__ __align__(8) uint64_t bars[2];
+    __shared__ __align__(8) uint64_t bars[kStages];
     __shared__ uint32_t s_tmem;
 
     const int tid = threadIdx.x;
@@ -128,8 +138,7 @@ __global__ void __launch_bounds__(128, 1)
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     if (tid == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
+        for (int i = 0; i < kStages; ++i) mbar_init(&bars[i], 1);
         fence_mbar_init();
     }
     tc_fence_before();
@@ -137,88 +146,93 @@ __global__ void __launch_bounds__(128, 1)
     tc_fence_after();
     const uint32_t tmem = s_tmem;
     const uint32_t idesc = umma_idesc(kTF32 ? 2 : 1, kGemmBM, BN);
+    const int nk = (K + kBK - 1) / kBK;
 
-    const int nk = (K + kGemmBK - 1) / kGemmBK;
-    uint32_t phase[2] = {0u, 0u};
-    for (int kb = 0; kb < nk; ++kb) {
-        const int st = kb & 1;
-        uint8_t* base = smem + st * kStageBytes;
-        if (kb >= 2) {                      // the MMAs that read this stage are done
-            mbar_wait(&bars[st], phase[st]);
-            phase[st] ^= 1u;
-        }
-        // ---- stage A and B K-block kb (generic-proxy smem writes)
-        const int k0 = kb * kGemmBK;
-        auto stage = [&](const T* src, int ld, int rows_valid, int row0, int nrows,
-                         uint8_t* hi, uint8_t* lo) {
-            for (int idx = tid; idx < nrows * kCk; idx += blockDim.x) {
-                const int r = idx / kCk, c = idx - r * kCk;
+    auto a_hi = [&](int st) { return smem + st * kStageBytes; };
+    auto a_lo = [&](int st) { return smem + st * kStageBytes + kABytes; };
+    auto b_hi = [&](int st) { return smem + st * kStageBytes + kPlanes * kABytes; };
+    auto b_lo = [&](int st) { return smem + st * kStageBytes + kPlanes * kABytes + kBBytes; };
+
+    // issue the cp.async loads of K-block kb into stage st
+    auto load_stage = [&](int kb, int st) {
+        const int k0 = kb * kBK;
+        auto tile = [&](const T* src, int ld, int rows_valid, int row0, int nrows, uint8_t* dst) {
+            for (int idx = tid; idx < nrows * kCk; idx += 128) {
+                const int r = idx >> 3, c = idx & 7;
                 const int gr = row0 + r, gk = k0 + c * kChunkElems;
-                uint4 v = make_uint4(0u, 0u, 0u, 0u);
-                if (gr < rows_valid) {
-                    if (gk + kChunkElems <= K) {
-                        v = *reinterpret_cast<const uint4*>(src + (size_t)gr * ld + gk);
-                    } else {
-                        T tmp[kChunkElems];
-#pragma unroll
-                        for (int q = 0; q < kChunkElems; ++q)
-                            tmp[q] = gk + q < K ? src[(size_t)gr * ld + gk + q] : T(0.f);
-                        v = *reinterpret_cast<uint4*>(tmp);
-                    }
+                int bytes = 0;
+                const T* g = src;
+                if (gr < rows_valid && gk < K) {
+                    bytes = min(kChunkElems, K - gk) * kEsz;
+                    g = src + (size_t)gr * ld + gk;
                 }
-                const uint32_t off = core_off(r, c, kCk);
-                if constexpr (kTF32) {
-                    const float* f = reinterpret_cast<const float*>(&v);
-                    uint4 h, l;
-                    uint32_t* hp = reinterpret_cast<uint32_t*>(&h);
-                    uint32_t* lp = reinterpret_cast<uint32_t*>(&l);
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        hp[q] = tf32_rna(f[q]);
-                        lp[q] = tf32_rna(f[q] - __uint_as_float(hp[q]));
-                    }
-                    *reinterpret_cast<uint4*>(hi + off) = h;
-                    *reinterpret_cast<uint4*>(lo + off) = l;
-                } else {
-                    *reinterpret_cast<uint4*>(hi + off) = v;
-                }
+                cp_async_16_zfill(dst + core_off(r, c, kCk), g, bytes);
             }
         };
-        uint8_t* a_hi = base;
-        uint8_t* a_lo = base + kABytes;                        // tf32 only
-        uint8_t* b_hi = base + kPlanes * kABytes;
-        uint8_t* b_lo = b_hi + kBBytes;                        // tf32 only
-        stage(A, lda, M, m0, kGemmBM, a_hi, a_lo);
-        stage(B, ldb, N, n0, BN, b_hi, b_lo);
-        fence_proxy_async_smem();          // make the staged tiles visible to the tensor core
+        tile(A, lda, M, m0, kGemmBM, a_hi(st));
+        tile(B, ldb, N, n0, BN, b_hi(st));
+    };
+    // tf32: split this thread's own chunks of stage st into hi (in place) / lo
+    auto split_stage = [&](int st) {
+        auto split = [&](uint8_t* hi, uint8_t* lo, int nrows) {
+            for (int idx = tid; idx < nrows * kCk; idx += 128) {
+                const uint32_t off = core_off(idx >> 3, idx & 7, kCk);
+                uint4 v = *reinterpret_cast<uint4*>(hi + off);
+                float* f = reinterpret_cast<float*>(&v);
+                uint4 h, l;
+                uint32_t* hp = reinterpret_cast<uint32_t*>(&h);
+                uint32_t* lp = reinterpret_cast<uint32_t*>(&l);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    hp[q] = tf32_rna(f[q]);
+                    lp[q] = tf32_rna(f[q] - __uint_as_float(hp[q]));
+                }
+                *reinterpret_cast<uint4*>(hi + off) = h;
+                *reinterpret_cast<uint4*>(lo + off) = l;
+            }
+        };
+        split(a_hi(st), a_lo(st), kGemmBM);
+        split(b_hi(st), b_lo(st), BN);
+    };
+
+    for (int s = 0; s < kStages - 1; ++s) {
+        if (s < nk) load_stage(s, s);
+        cp_async_commit();
+    }
+    for (int kb = 0; kb < nk; ++kb) {
+        const int st = kb % kStages;
+        cp_async_wait<kStages - 2>();          // this thread's chunks of K-block kb landed
+        if constexpr (kTF32) split_stage(st);
+        fence_proxy_async_smem();              // generic-proxy smem writes -> tensor core
         __syncthreads();
-        // ---- one thread issues the MMAs of this K-block
         if (tid == 0) {
             tc_fence_after();
             const uint32_t lbo = 128, sbo = kCk * 128;
 #pragma unroll
-            for (int s = 0; s < kGemmBK / kUmmaK; ++s) {
+            for (int s = 0; s < kUmmaSteps; ++s) {
                 const uint32_t koff = s * 2 * 128;             // two core matrices per MMA-K
-                const uint64_t dah = umma_desc(smem_u32(a_hi) + koff, lbo, sbo);
-                const uint64_t dbh = umma_desc(smem_u32(b_hi) + koff, lbo, sbo);
-                const uint32_t acc0 = (kb > 0 || s > 0) ? 1u : 0u;
-                umma<kTF32>(tmem, dah, dbh, idesc, acc0);
+                const uint64_t dah = umma_desc(smem_u32(a_hi(st)) + koff, lbo, sbo);
+                const uint64_t dbh = umma_desc(smem_u32(b_hi(st)) + koff, lbo, sbo);
+                umma<kTF32>(tmem, dah, dbh, idesc, (kb > 0 || s > 0) ? 1u : 0u);
                 if constexpr (kTF32) {
-                    const uint64_t dal = umma_desc(smem_u32(a_lo) + koff, lbo, sbo);
-                    const uint64_t dbl = umma_desc(smem_u32(b_lo) + koff, lbo, sbo);
+                    const uint64_t dal = umma_desc(smem_u32(a_lo(st)) + koff, lbo, sbo);
+                    const uint64_t dbl = umma_desc(smem_u32(b_lo(st)) + koff, lbo, sbo);
                     umma<kTF32>(tmem, dah, dbl, idesc, 1u);
                     umma<kTF32>(tmem, dal, dbh, idesc, 1u);
                 }
             }
             umma_commit(&bars[st]);
         }
-        __syncwarp();
+        // refill the stage consumed one iteration ago once its MMAs are done
+        const int next = kb + kStages - 1;
+        if (next < nk) {
+            const int ns = next % kStages;
+            if (kb >= 1) mbar_wait(&bars[ns], (uint32_t)(((kb - 1) / kStages) & 1));
+            load_stage(next, ns);
+        }
+        cp_async_commit();
     }
-    // wait for the last commit (it covers every earlier MMA)
-    {
-        const int st = (nk - 1) & 1;
-        mbar_wait(&bars[st], phase[st]);
-    }
+    mbar_wait(&bars[(nk - 1) % kStages], (uint32_t)(((nk - 1) / kStages) & 1));
     tc_fence_after();
 
     // ---- epilogue: thread = one output row (TMEM lane), 8 columns per load
@@ -252,9 +266,10 @@ __global__ void __launch_bounds__(128, 1)
 template <typename T, int BN>
 static int32_t launch_gemm(const void* A, int lda, const void* B, int ldb, float* C, int ldc,
                            int M, int N, int K, int accumulate, cudaStream_t s) {
-    auto kern = gemm_tn_kernel<T, BN>;
+    constexpr int kStages = sizeof(T) == 4 ? 3 : 4;
+    auto kern = gemm_tn_kernel<T, BN, kStages>;
     constexpr int kPlanes = sizeof(T) == 4 ? 2 : 1;
-    const size_t smem = (size_t)2 * kPlanes * (kGemmBM + BN) * kGemmBK * sizeof(T);
+    const size_t smem = (size_t)kStages * kPlanes * (kGemmBM + BN) * 128;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
         return check_launch("tdkv_gemm: cudaFuncSetAttribute");
