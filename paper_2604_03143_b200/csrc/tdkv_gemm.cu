@@ -301,9 +301,15 @@ extern "C" int32_t tdkv_gemm(const void* d_a, int32_t lda, const void* d_b, int3
         rc = n <= 64 ? launch_gemm<float, 64>(d_a, lda, d_b, ldb, d_c, ldc, m, n, k, accumulate, s)
                      : launch_gemm<float, 128>(d_a, lda, d_b, ldb, d_c, ldc, m, n, k, accumulate, s);
     } else {
-        rc = n <= 64
-                 ? launch_gemm<__nv_bfloat16, 64>(d_a, lda, d_b, ldb, d_c, ldc, m, n, k, accumulate, s)
-                 : launch_gemm<__nv_bfloat16, 128>(d_a, lda, d_b, ldb, d_c, ldc, m, n, k, accumulate, s);
+        // 128 x 256 tiles halve the L2 operand traffic per flop when the
+        // grid still fills the SMs
+        const long long tiles256 = (long long)((m + 127) / 128) * ((n + 255) / 256);
+        if (n <= 64)
+            rc = launch_gemm<__nv_bfloat16, 64>(d_a, lda, d_b, ldb, d_c, ldc, m, n, k, accumulate, s);
+        else if (n >= 256 && tiles256 >= sm_count())
+            rc = launch_gemm<__nv_bfloat16, 256>(d_a, lda, d_b, ldb, d_c, ldc, m, n, k, accumulate, s);
+        else
+            rc = launch_gemm<__nv_bfloat16, 128>(d_a, lda, d_b, ldb, d_c, ldc, m, n, k, accumulate, s);
     }
     if (rc) return rc;
     count_launch();
