@@ -229,7 +229,7 @@ def gen_codec_trials():
     from a seed; records indices, wire length and digest per trial."""
     out = []
     rng = np.random.default_rng(0xD1FF)
-    for trial in range(300):
+    for trial in range(1000):          # the acceptance C04 count
         bs = int(rng.choice([8, 16, 32]))
         blocks = CacheBlockConfig(block_size=bs)
         t = int(rng.integers(1, 180))
@@ -296,7 +296,7 @@ def gen_restores():
     out = []
     rng = np.random.default_rng(0xF05E)
     blocks = CacheBlockConfig(block_size=16)
-    for trial in range(60):
+    for trial in range(200):           # the acceptance C05 count
         t = int(rng.integers(8, 90))
         start = int(rng.integers(0, 60))
         delta = int(rng.integers(-start, 80))

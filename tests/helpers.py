@@ -65,7 +65,7 @@ class CodecTrial:
     hints: np.ndarray
 
 
-def codec_trials(n=300):
+def codec_trials(n=1000):
     """The acceptance-C04 trial stream (pkg/tests/test_acceptance.py:186-228)."""
     rng = np.random.default_rng(0xD1FF)
     for _ in range(n):
@@ -107,7 +107,7 @@ class RestoreTrial:
     delta: int
 
 
-def restore_trials(n=60):
+def restore_trials(n=200):
     """The acceptance-C05 trial stream (pkg/tests/test_acceptance.py:231-279)."""
     rng = np.random.default_rng(0xF05E)
     bs = 16
