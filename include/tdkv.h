@@ -39,6 +39,7 @@ extern "C" {
 #define TDKV_EINVAL 1     /* bad argument (shape, pointer, alignment) */
 #define TDKV_EUNSUPPORTED 2
 #define TDKV_ECUDA 3      /* a CUDA launch/runtime error */
+#define TDKV_ENOSLOTS 4   /* allocator: not enough free slots */
 
 #define TDKV_NO_VIOLATION 0x7f7f7f7f
 
@@ -259,6 +260,18 @@ int32_t tdkv_attention(const float* d_q, const float* d_k_fresh, const float* d_
                        const int32_t* d_fresh_of, const int64_t* d_fix_idx,
                        int32_t n_fix, int32_t num_tokens, int32_t num_heads,
                        int32_t head_dim, float scale, float* d_mix, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Host slot allocator of the paged pool, policy of
+ * PagedPool.allocate (paged_pool.py:106-135): whole free blocks ascending
+ * first (a prefix of the last), then the lowest free slots.  Host memory
+ * only; thread-safe.  take() writes n slots to out_slots or returns
+ * TDKV_ENOSLOTS; release() rejects slots that are not allocated. */
+void* tdkv_alloc_create(int64_t capacity, int32_t block_size);
+void tdkv_alloc_destroy(void* handle);
+int64_t tdkv_alloc_free_count(void* handle);
+int32_t tdkv_alloc_take(void* handle, int64_t n, int64_t* out_slots);
+int32_t tdkv_alloc_release(void* handle, const int64_t* slots, int64_t n);
 
 /* Fill rows of every layer with a value (NaN poisoning of freed slots,
  * paged_pool.py:144-147).  value_bits is the element bit pattern. */

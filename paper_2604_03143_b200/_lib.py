@@ -90,7 +90,8 @@ EXPORTS = (
     "tdkv_version", "tdkv_last_error", "tdkv_launch_count", "tdkv_rope_table",
     "tdkv_collect", "tdkv_diff_compare", "tdkv_diff_compact", "tdkv_rows",
     "tdkv_keydiff", "tdkv_select_important", "tdkv_gemm", "tdkv_qkv_rope", "tdkv_attention",
-    "tdkv_fill_rows",
+    "tdkv_fill_rows", "tdkv_alloc_create", "tdkv_alloc_destroy", "tdkv_alloc_free_count",
+    "tdkv_alloc_take", "tdkv_alloc_release",
 )
 
 _P = ctypes.c_void_p
@@ -114,6 +115,11 @@ _SIGS = {
     "tdkv_select_important": (_I32, [_P, _P, _P, _I32, _I32, _P, _P, _P, _P]),
     "tdkv_gemm": (_I32, [_P, _I32, _P, _I32, _P, _I32, _I32, _I32, _I32, _I32, _I32, _P]),
     "tdkv_qkv_rope": (_I32, [_P, _P, _I32, _I32, _I32, _P, _P, _P, _P]),
+    "tdkv_alloc_create": (_P, [_I64, _I32]),
+    "tdkv_alloc_destroy": (None, [_P]),
+    "tdkv_alloc_free_count": (_I64, [_P]),
+    "tdkv_alloc_take": (_I32, [_P, _I64, _P]),
+    "tdkv_alloc_release": (_I32, [_P, _P, _I64]),
     "tdkv_attention": (_I32, [_P, _P, _P, _P, _P, _P, _P, _I32, _I32, _I32, _I32,
                               ctypes.c_float, _P, _P]),
 }

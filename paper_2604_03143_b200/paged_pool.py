@@ -8,8 +8,10 @@ any slot order stores fully coalesced.
 
 The allocator keeps the reference policy exactly (paged_pool.py:106-135):
 whole free blocks in ascending order first, then the lowest scattered free
-slots -- vectorized over a numpy free mask so slot maps are bit-identical
-to the reference's without its O(capacity) Python loop.  Slot maps are host
+slots -- in native code over free-slot / whole-block bitmaps
+(``tdkv_alloc_*``), so slot maps are bit-identical to the reference's
+without its O(capacity) Python loop.  ``choose_slots`` is the same policy in
+numpy, kept as an executable statement of it for the host-side tests.  Slot maps are host
 metadata; their device copies are cached on the SlotMap.
 """
 from __future__ import annotations
@@ -97,6 +99,45 @@ def choose_slots(free: np.ndarray, num_tokens: int, block_size: int) -> np.ndarr
     return np.concatenate(parts).astype(np.int64) if parts else np.empty(0, np.int64)
 
 
+class SlotAllocator:
+    """The native (C++) slot allocator behind PagedPool: the reference policy
+    (paged_pool.py:106-135) over free-slot / whole-block bitmaps."""
+
+    def __init__(self, capacity: int, block_size: int) -> None:
+        import ctypes
+        from . import _lib
+        self._lib = _lib.load()
+        self._ct = ctypes
+        self._h = self._lib.tdkv_alloc_create(int(capacity), int(block_size))
+        if not self._h:
+            raise ValueError(self._lib.tdkv_last_error().decode())
+
+    def __del__(self) -> None:
+        h = getattr(self, "_h", None)
+        if h:
+            self._lib.tdkv_alloc_destroy(h)
+            self._h = None
+
+    @property
+    def free_count(self) -> int:
+        return int(self._lib.tdkv_alloc_free_count(self._h))
+
+    def take(self, n: int) -> np.ndarray:
+        out = np.empty(int(n), dtype=np.int64)
+        rc = self._lib.tdkv_alloc_take(self._h, int(n), out.ctypes.data_as(self._ct.c_void_p))
+        if rc == 4:
+            raise OutOfSlotsError(int(n), self.free_count)
+        if rc:
+            raise ValueError(self._lib.tdkv_last_error().decode())
+        return out
+
+    def release(self, slots: np.ndarray) -> None:
+        s = np.ascontiguousarray(slots, dtype=np.int64)
+        rc = self._lib.tdkv_alloc_release(self._h, s.ctypes.data_as(self._ct.c_void_p), s.size)
+        if rc:
+            raise ValueError(self._lib.tdkv_last_error().decode())
+
+
 class PagedPool:
     """Fixed-capacity slot pool with per-layer K and V planes in HBM."""
 
@@ -112,7 +153,7 @@ class PagedPool:
         shape = (num_layers, self.capacity, num_heads, head_dim)
         self.k = torch.zeros(shape, dtype=dtype, device=self.device)
         self.v = torch.zeros(shape, dtype=dtype, device=self.device)
-        self._free = np.ones(self.capacity, dtype=bool)
+        self._alloc = SlotAllocator(self.capacity, self.block_size)
         self._nfree = self.capacity
         self._written = np.zeros((num_layers, self.capacity), dtype=bool)
         self._peak = 0
@@ -165,8 +206,7 @@ class PagedPool:
         with self._lock:
             if num_tokens > self._nfree:
                 raise OutOfSlotsError(num_tokens, self._nfree)
-            chosen = choose_slots(self._free, num_tokens, self.block_size)
-            self._free[chosen] = False
+            chosen = self._alloc.take(num_tokens)
             self._nfree -= chosen.size
             self._written[:, chosen] = False
             self._peak = max(self._peak, self.allocated_count)
@@ -187,7 +227,7 @@ class PagedPool:
                 _kernels.fill_rows(self.k, rows, float("nan"))
                 _kernels.fill_rows(self.v, rows, float("nan"))
             self._written[:, slots] = False
-            self._free[slots] = True
+            self._alloc.release(slots)
             self._nfree += slots.size
 
     def mark_written(self, slot_map: SlotMap, layers: Optional[Sequence[int]] = None,
@@ -238,5 +278,5 @@ class PagedPool:
 
     def check_conservation(self) -> None:
         assert 0 <= self._nfree <= self.capacity
-        assert int(self._free.sum()) == self._nfree
+        assert self._alloc.free_count == self._nfree
         assert self.allocated_count + self.free_count == self.capacity

@@ -18,7 +18,7 @@ PKG = os.path.join(ROOT, "paper_2604_03143_b200")
 
 def _header_functions():
     text = open(os.path.join(ROOT, "include", "tdkv.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int32_t|int64_t|const char\*)\s+(tdkv_\w+)\s*\(",
+    return sorted(set(re.findall(r"^\s*(?:int32_t|int64_t|const char\*|void\*?)\s+(tdkv_\w+)\s*\(",
                                  text, re.M)))
 
 
@@ -161,3 +161,41 @@ def test_offset_planning_matches_row_planning():
         assert np.array_equal(a.dst_rows[a.jobs["dst_off"][j]:a.jobs["dst_off"][j] + n],
                               flat[b.jobs["dst_off"][j]:b.jobs["dst_off"][j] + n])
     assert a.rows_written == b.rows_written and a.master_rows == b.master_rows
+
+
+def test_native_allocator_matches_reference_policy():
+    """tdkv_alloc_* (host C++) against the reference's recorded allocator
+    stream and the oracle policy under random alloc/free churn."""
+    from paper_2604_03143_b200.paged_pool import OutOfSlotsError, SlotAllocator
+    a = SlotAllocator(256, 32)
+    live = {}
+    for op in load_golden()["allocator"]:
+        if op["op"] == "alloc":
+            got = a.take(op["n"])
+            assert got.tolist() == op["slots"]
+            live[op["serial"]] = got
+        elif op["op"] == "free":
+            a.release(live.pop(op["serial"]))
+    rng = np.random.default_rng(9)
+    for cap, bs in [(1000, 32), (777, 16), (64, 64)]:
+        al = SlotAllocator(cap, bs)
+        free = np.ones(cap, bool)
+        held = []
+        for _ in range(400):
+            if held and rng.random() < 0.45:
+                m = held.pop(int(rng.integers(len(held))))
+                al.release(m)
+                free[m] = True
+                continue
+            n = int(rng.integers(1, max(2, cap // 5)))
+            if n > free.sum():
+                with pytest.raises(OutOfSlotsError):
+                    al.take(n)
+                continue
+            want = ref.allocate_slots(free, n, bs)
+            got = al.take(n)
+            assert got.tolist() == want.tolist()
+            held.append(got)
+        assert al.free_count == int(free.sum())
+    with pytest.raises(ValueError, match="not allocated"):
+        al.release(np.array([0, 0]))
