@@ -599,6 +599,16 @@ def codec_bench(tk, spec, pool, maps, dev, args, peak):
         diffs = tk.encode_batch(master, mirrors, hints, blocks_cfg)
     torch.cuda.synchronize(dev)
     enc_s = (time.perf_counter() - t0) / reps
+    # the two K2 launches alone (CUDA events; descriptor upload included)
+    from paper_2604_03143_b200 import diffstore as _ds
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        st = _ds.encode_launch(master, mirrors, hints, blocks_cfg)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    enc_dev_s = e0.elapsed_time(e1) * 1e-3 / reps
+    del st
     payload = sum(d.payload_nbytes for d in diffs)
     changed = sum(sum(d.changed_blocks_per_layer) for d in diffs)
     enc_bytes = n_mirrors * 2 * dense + payload + 4 * changed
@@ -624,6 +634,8 @@ def codec_bench(tk, spec, pool, maps, dev, args, peak):
         "encode_gbs": round(enc_bytes / enc_s / 1e9, 1),
         "encode_frac": round(enc_bytes / enc_s / 1e9 / peak, 4),
         "encode_ms_per_family": round(enc_s * 1e3, 3),
+        "encode_device_gbs": round(enc_bytes / enc_dev_s / 1e9, 1),
+        "encode_device_frac": round(enc_bytes / enc_dev_s / 1e9 / peak, 4),
         "decode_gbs": round(dec_bytes / dec_s / 1e9, 1),
         "decode_frac": round(dec_bytes / dec_s / 1e9 / peak, 4),
         "decode_ms_per_family": round(dec_s * 1e3, 3),

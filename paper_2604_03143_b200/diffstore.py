@@ -238,6 +238,97 @@ def _plane_dtype(kv: LayeredKv) -> torch.dtype:
     return kv.k.dtype if isinstance(kv.k, torch.Tensor) else torch.float32
 
 
+def encode_launch(master: LayeredKv, mirrors: Sequence[LayeredKv],
+                  hint_positions: Sequence[np.ndarray], blocks: CacheBlockConfig,
+                  device: Optional[torch.device] = None) -> "_EncodeState":
+    """Validate, upload the descriptors and launch K2 (compare + compact) for
+    a family without reading anything back; ``encode_finish`` completes it."""
+    if len(mirrors) != len(hint_positions) or not mirrors:
+        raise ValueError("one hint array per mirror, at least one mirror")
+    total = master.num_tokens
+    nb = blocks.num_blocks(total)
+    bs = blocks.block_size
+    L, H, D = master.num_layers, master.num_heads, master.head_dim
+    hinted = np.zeros((len(mirrors), nb), np.uint8)
+    shape = tuple(master.k.shape)
+    for mir in mirrors:
+        if tuple(mir.k.shape) != shape:
+            raise ValueError("master and mirror must have identical plane shapes")
+        if mir.positions is not master.positions and not np.array_equal(master.positions,
+                                                                         mir.positions):
+            raise ValueError("master and mirror must cover the same positions")
+    # every mirror's hint positions -> its hinted-block row, in one scatter
+    hs = [np.asarray(h, dtype=np.int64).reshape(-1) for h in hint_positions]
+    cat = np.concatenate(hs) if hs else np.zeros(0, np.int64)
+    if cat.size and (cat.min() < 0 or cat.max() >= total):
+        raise ValueError("hint positions out of range")
+    owner = np.repeat(np.arange(len(hs)), [h.size for h in hs])
+    hinted[owner, cat // bs] = 1
+    device = device or (master.k.device if master.on_device else default_device())
+    dtype = _plane_dtype(master)
+    mk = to_device(master.k, device, dtype)
+    mv = to_device(master.v, device, dtype)
+    mirrors_dev = [(to_device(m.k, device, dtype), to_device(m.v, device, dtype)) for m in mirrors]
+    P = len(mirrors)
+    caps = np.maximum(hinted.sum(axis=1).astype(np.int64), 1)
+    slab_blocks = int((caps * L).sum())
+    # one int32 buffer for everything the host reads back: one D2H copy
+    meta = torch.empty(P + P * L + slab_blocks, dtype=torch.int32, device=device)
+    violation = meta[:P]
+    counts = meta[P:P + P * L]
+    indices = meta[P + P * L:]
+    changed = torch.empty(P * L * nb, dtype=torch.uint8, device=device)
+    viol_maxabs = torch.empty(P * L * nb, dtype=torch.float32, device=device)  # violations only
+    pay_k = torch.empty((slab_blocks, bs, H, D), dtype=dtype, device=device)
+    pay_v = torch.empty_like(pay_k)
+    blkmap = torch.empty(P * L * nb, dtype=torch.int32, device=device)
+    starts = np.concatenate([[0], np.cumsum(caps * L)[:-1]])
+    blk_bytes = bs * H * D * pay_k.element_size()
+    # descriptors (pairs, outputs) and the hinted-block mask in ONE upload
+    desc = np.zeros(P * (_lib.DIFF_PAIR.itemsize + _lib.DIFF_OUT.itemsize) + P * nb, np.uint8)
+    pairs = desc[:P * 32].view(_lib.DIFF_PAIR)
+    outs = desc[P * 32:P * 72].view(_lib.DIFF_OUT)
+    pairs["master_k"], pairs["master_v"] = ptr(mk), ptr(mv)
+    pairs["mirror_k"] = [ptr(a) for a, _ in mirrors_dev]
+    pairs["mirror_v"] = [ptr(b) for _, b in mirrors_dev]
+    outs["payload_k"] = ptr(pay_k) + starts * blk_bytes
+    outs["payload_v"] = ptr(pay_v) + starts * blk_bytes
+    outs["indices"] = ptr(indices) + starts * 4
+    outs["blkmap"] = ptr(blkmap) + np.arange(P, dtype=np.int64) * (L * nb * 4)
+    outs["cap"] = caps
+    desc[P * 72:] = hinted.reshape(-1)
+    d_desc = upload(desc, device)
+    d_pairs, d_outs, d_hinted = ptr(d_desc), ptr(d_desc) + P * 32, ptr(d_desc) + P * 72
+    code = dtype_code(dtype)
+    stream = stream_handle(device)
+    _lib.call("tdkv_diff_compare", d_pairs, P, d_hinted, ptr(changed), ptr(violation),
+              ptr(viol_maxabs), L, total, H, D, bs, code, stream)
+    _lib.call("tdkv_diff_compact", d_pairs, d_outs, P, ptr(changed), ptr(counts),
+              L, total, H, D, bs, code, stream)
+    return _EncodeState(P, L, H, D, bs, nb, total, caps, starts, meta, viol_maxabs, pay_k,
+                        pay_v, blkmap)
+
+
+@dataclass
+class _EncodeState:
+    """Launched-but-unread encoder outputs (see encode_launch)."""
+
+    P: int
+    L: int
+    H: int
+    D: int
+    bs: int
+    nb: int
+    total: int
+    caps: np.ndarray
+    starts: np.ndarray
+    meta: torch.Tensor
+    viol_maxabs: torch.Tensor
+    pay_k: torch.Tensor
+    pay_v: torch.Tensor
+    blkmap: torch.Tensor
+
+
 def encode_batch(master: LayeredKv, mirrors: Sequence[LayeredKv],
                  hint_positions: Sequence[np.ndarray], blocks: CacheBlockConfig,
                  device: Optional[torch.device] = None) -> List[BlockSparseDiff]:
@@ -251,54 +342,15 @@ def encode_batch(master: LayeredKv, mirrors: Sequence[LayeredKv],
         raise ValueError("one hint array per mirror")
     if not mirrors:
         return []
-    total = master.num_tokens
-    nb = blocks.num_blocks(total)
-    bs = blocks.block_size
-    L, H, D = master.num_layers, master.num_heads, master.head_dim
-    hinted = np.zeros((len(mirrors), nb), np.uint8)
-    for p, (mir, hints) in enumerate(zip(mirrors, hint_positions)):
-        _check_pair(master, mir)
-        h = np.asarray(hints, dtype=np.int64)
-        if h.size and (h.min() < 0 or h.max() >= total):
-            raise ValueError("hint positions out of range")
-        hinted[p, h // bs] = 1
-    device = device or (master.k.device if master.on_device else default_device())
-    dtype = _plane_dtype(master)
-    mk = to_device(master.k, device, dtype)
-    mv = to_device(master.v, device, dtype)
-    mirrors_dev = [(to_device(m.k, device, dtype), to_device(m.v, device, dtype)) for m in mirrors]
-    P = len(mirrors)
-    pairs = np.array([(ptr(mk), ptr(mv), ptr(a), ptr(b)) for a, b in mirrors_dev],
-                     dtype=_lib.DIFF_PAIR)
-    d_pairs = upload(pairs, device)
-    d_hinted = torch.from_numpy(hinted.reshape(-1)).to(device)
-    caps = np.maximum(hinted.sum(axis=1).astype(np.int64), 1)
-    slab_blocks = int((caps * L).sum())
-    # one int32 buffer for everything the host reads back: one D2H copy
-    meta = torch.empty(P + P * L + slab_blocks, dtype=torch.int32, device=device)
-    violation = meta[:P]
-    counts = meta[P:P + P * L]
-    indices = meta[P + P * L:]
-    changed = torch.empty(P * L * nb, dtype=torch.uint8, device=device)
-    viol_maxabs = torch.zeros(P * L * nb, dtype=torch.float32, device=device)
-    code = dtype_code(dtype)
-    stream = stream_handle(device)
-    _lib.call("tdkv_diff_compare", ptr(d_pairs), P, ptr(d_hinted), ptr(changed), ptr(violation),
-              ptr(viol_maxabs), L, total, H, D, bs, code, stream)
+    return encode_finish(encode_launch(master, mirrors, hint_positions, blocks, device))
 
-    pay_k = torch.empty((slab_blocks, bs, H, D), dtype=dtype, device=device)
-    pay_v = torch.empty_like(pay_k)
-    blkmap = torch.empty(P * L * nb, dtype=torch.int32, device=device)
-    starts = np.concatenate([[0], np.cumsum(caps * L)[:-1]])
-    esz = pay_k.element_size()
-    blk_bytes = bs * H * D * esz
-    outs = np.array([(ptr(pay_k) + int(s) * blk_bytes, ptr(pay_v) + int(s) * blk_bytes,
-                      ptr(indices) + int(s) * 4, ptr(blkmap) + p * L * nb * 4, int(c), 0)
-                     for p, (s, c) in enumerate(zip(starts, caps))], dtype=_lib.DIFF_OUT)
-    d_outs = upload(outs, device)
-    _lib.call("tdkv_diff_compact", ptr(d_pairs), ptr(d_outs), P, ptr(changed), ptr(counts),
-              L, total, H, D, bs, code, stream)
 
+def encode_finish(st: "_EncodeState") -> List[BlockSparseDiff]:
+    """The one device->host read of an encode (violations, counts, indices)
+    and the diffs as views of the device payload slab."""
+    P, L, H, D, bs, nb, total = st.P, st.L, st.H, st.D, st.bs, st.nb, st.total
+    caps, starts, meta, viol_maxabs = st.caps, st.starts, st.meta, st.viol_maxabs
+    pay_k, pay_v, blkmap = st.pay_k, st.pay_v, st.blkmap
     meta_h = meta.cpu().numpy()
     viol_h = meta_h[:P]
     bad = np.flatnonzero(viol_h != _lib.NO_VIOLATION)
