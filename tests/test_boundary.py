@@ -199,3 +199,31 @@ def test_native_allocator_matches_reference_policy():
         assert al.free_count == int(free.sum())
     with pytest.raises(ValueError, match="not allocated"):
         al.release(np.array([0, 0]))
+
+
+def test_c_abi_rejects_bad_arguments_without_a_gpu():
+    """Argument validation happens before any CUDA call: the status codes and
+    messages are observable on a CPU-only host."""
+    import ctypes
+    from paper_2604_03143_b200 import _lib
+    lib = _lib.load()
+    null = ctypes.c_void_p(0)
+    rc = lib.tdkv_collect(null, null, 0, null, 1, 8, null, null, null, 0, null, null, 0,
+                          2, 2, 7, 0, 0, null)
+    assert rc == 1 and b"geometry" in lib.tdkv_last_error()
+    rc = lib.tdkv_collect(null, null, 0, null, 1, 8, null, null, null, 0, null, null, 0,
+                          2, 2, 8, 0, 0, null)
+    assert rc == 1 and b"null pointer" in lib.tdkv_last_error()
+    rc = lib.tdkv_collect(null, null, 0, null, 1, 64, null, null, null, 0, null, null, 0,
+                          2, 2, 8, 0, 0, null)
+    assert rc == 1 and b"max_rows" in lib.tdkv_last_error()
+    assert lib.tdkv_diff_compare(null, 1, null, null, null, null, 1, 8, 1, 8, 0, 0, null) == 1
+    assert lib.tdkv_diff_compare(null, 1, null, null, null, null, 1, 8, 1, 8, 8, 7, null) == 2
+    assert lib.tdkv_rows(null, 1, 8, null, 1, 1, 8, 8, 0, 0, 0, 0, null) == 1
+    assert lib.tdkv_gemm(null, 8, null, 8, null, 8, 4, 4, 4, 0, 0, null) == 1
+    assert lib.tdkv_select_important(null, null, null, 1, 100000, null, null, null, null) == 2
+    assert lib.tdkv_rope_table(null, 4, null, 4, 0, null, null) == 1
+    # zero-size work is a successful no-op
+    assert lib.tdkv_collect(null, null, 0, null, 0, 8, null, null, null, 0, null, null, 0,
+                            2, 2, 8, 0, 0, null) == 0
+    assert lib.tdkv_rows(null, 0, 8, null, 1, 1, 8, 8, 0, 0, 0, 0, null) == 0
