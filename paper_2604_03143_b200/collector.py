@@ -453,6 +453,44 @@ class KVCollector:
         return self.collect_staged(plan, events, ledger)
 
 
+class RoundPipeline:
+    """Steady-state rounds whose masters arrive from host memory: two arenas
+    alternate, so round r+1's masters stream over PCIe (copy stream) while
+    round r is collected from the other arena (compute stream)."""
+
+    def __init__(self, arena: MasterArena, pool, rope_base: float = 10000.0,
+                 chunks: int = 7) -> None:
+        twin = MasterArena(torch.empty_like(arena.k), torch.empty_like(arena.v), arena.seg_row0,
+                           arena.seg_len, arena.source_positions)
+        self.collectors = [KVCollector(arena, pool, rope_base), KVCollector(twin, pool, rope_base)]
+        self.chunks = chunks
+        self.copy_stream = torch.cuda.Stream(pool.device)
+        self._pending = None          # (collector index, staged chunk events)
+        self._round = 0
+
+    def prime(self, host_k: torch.Tensor, host_v: torch.Tensor) -> None:
+        """Start streaming the first round's masters."""
+        c = self.collectors[self._round % 2]
+        self._pending = (self._round % 2,
+                         c.stage_from_host(host_k, host_v, self.chunks, self.copy_stream))
+
+    def step(self, plan: CollectPlan, next_host_k: Optional[torch.Tensor],
+             next_host_v: Optional[torch.Tensor], ledger: Optional[CostLedger] = None) -> int:
+        """Collect the primed round with ``plan`` (planned against either arena:
+        both share the segment table); start streaming the next round's masters
+        (if given) into the other arena first, so the transfers overlap."""
+        if self._pending is None:
+            raise RuntimeError("prime() the pipeline first")
+        idx, events = self._pending
+        nxt = (idx + 1) % 2
+        self._pending = None
+        if next_host_k is not None:
+            self._pending = (nxt, self.collectors[nxt].stage_from_host(
+                next_host_k, next_host_v, self.chunks, self.copy_stream))
+        self._round += 1
+        return self.collectors[idx].collect_staged(plan, events, ledger)
+
+
 # ---------------------------------------------------------------------------
 # reference-shaped drop-ins (pic.py:192-235)
 
