@@ -209,9 +209,23 @@ __global__ void __launch_bounds__(256)
         }
     };
 
+    // the tile's destination rows are staged in shared memory with cp.async
+    // (issued with the next tile's bulk copy), so the scatter loop never
+    // waits on a dependent global load
+    __shared__ __align__(16) int64_t s_drow[2][32];
+    auto stage_rows = [&](const Item& x, int b) {
+        const int64_t* dr = jobs[x.ji].dst_rows;
+        if (tid < x.n) {
+            if (dr) cp_async_8(&s_drow[b][tid], dr + x.lo + tid);
+            else s_drow[b][tid] = x.lo + tid;
+        }
+        cp_async_commit();
+    };
+
     Item cur, nxt;
     long long it = next_valid(blockIdx.x, cur);
     if (tid == 0 && it < n_items) issue(cur, 0);
+    if (it < n_items) stage_rows(cur, 0);
     uint32_t phase0 = 0, phase1 = 0;
     int bi = 0;
     while (it < n_items) {
@@ -220,8 +234,15 @@ __global__ void __launch_bounds__(256)
             fence_proxy_async_smem();
             issue(nxt, bi ^ 1);
         }
+        if (nx < n_items) {
+            stage_rows(nxt, bi ^ 1);
+            cp_async_wait<1>();            // this tile's rows (the older group) landed
+        } else {
+            cp_async_wait<0>();
+        }
         mbar_wait(&bars[bi], bi ? phase1 : phase0);
         if (bi) phase1 ^= 1u; else phase0 ^= 1u;
+        __syncthreads();                   // staged rows visible to every thread
 
         const tdkv_rows_job* job = jobs + cur.ji;
         const V* sk = reinterpret_cast<const V*>(smem + (size_t)bi * 2 * tile_bytes);
@@ -229,7 +250,6 @@ __global__ void __launch_bounds__(256)
         T* dk = static_cast<T*>(job->dst_k) + (size_t)cur.layer * job->dst_layer_stride;
         T* dv = static_cast<T*>(job->dst_v) + (size_t)cur.layer * job->dst_layer_stride;
         const bool has_v = job->dst_v != nullptr;
-        const int64_t* drows = job->dst_rows;
         const int rotate = job->rotate, tbl_row = job->tbl_row, tbl_stride = job->tbl_stride;
         if (ty < rows_per_pass) {
             for (int c = tx; c < upr; c += tx_n) {
@@ -242,7 +262,7 @@ __global__ void __launch_bounds__(256)
                 }
                 for (int r = ty; r < cur.n; r += rows_per_pass) {
                     const int t = cur.lo + r;
-                    const int64_t drow = drows ? __ldg(drows + t) : t;
+                    const int64_t drow = s_drow[bi][r];
                     V kx = sk[r * upr + c];
                     if (rotate) {
                         if (tbl_stride != 0) {
@@ -335,6 +355,7 @@ extern "C" int32_t tdkv_rows(const tdkv_rows_job* d_jobs, int32_t n_jobs, int32_
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if ((flags & TDKV_ROWS_CONTIGUOUS) && ub == 16) {
         if (tile_rows <= 0 || tile_rows > block_size) tile_rows = block_size;
+        if (tile_rows > 32) tile_rows = 32;        // staged destination rows per tile
         if ((size_t)4 * tile_rows * g.row_elems * elt_size(dtype) > 227 * 1024)
             return set_error(TDKV_EINVAL, "tdkv_rows: tile of %d rows exceeds shared memory",
                              tile_rows);
