@@ -72,7 +72,10 @@ def rows(jobs: np.ndarray, max_tokens: int, table: Optional[torch.Tensor], num_l
               grid_limit, stream_handle(device))
 
 
-def tile_rows_for(row_bytes: int, budget: int = 72 * 1024) -> int:
+_ROWS_SMEM = int(__import__("os").environ.get("TDKV_ROWS_SMEM", 72 * 1024))
+
+
+def tile_rows_for(row_bytes: int, budget: int = _ROWS_SMEM) -> int:
     """Rows per staged tile: double-buffered K+V within ``budget`` bytes."""
     rows = max(1, budget // (4 * row_bytes))
     p = 1
