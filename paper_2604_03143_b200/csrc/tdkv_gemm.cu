@@ -17,6 +17,10 @@
 //     which gates the stage's refill; the epilogue reads the accumulator with
 //     tcgen05.ld and stores (or adds, for the residual update h += mix @ Wm)
 //     float32 rows.
+#include <cstdlib>
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "tdkv_common.cuh"
 
 namespace tdkv {
@@ -279,6 +283,231 @@ static int32_t launch_gemm(const void* A, int lda, const void* B, int ldb, float
     return TDKV_OK;
 }
 
+// ---------------------------------------------------------------------------
+// TMA + warp-specialized variant.  Operand tiles arrive by TMA
+// (cp.async.bulk.tensor, 128-byte swizzle, zero fill past the edges) into a
+// kStages-deep ring; warp 0 produces, warp 1 issues the MMAs (one elected
+// lane) and releases each stage with tcgen05.commit, warps 2-5 split tf32
+// stages into hi/lo (3xTF32) and run the epilogue.  UMMA reads the stages
+// through SWIZZLE_128B K-major descriptors (SBO = 1024 B, 8-row atoms).
+
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((smem_addr >> 4) & 0x3FFFu);
+    d |= (uint64_t)1 << 16;                       // LBO (unused for swizzled K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;             // SBO: 8 rows x 128 B
+    d |= (uint64_t)1 << 46;                       // version
+    d |= (uint64_t)2 << 61;                       // SWIZZLE_128B
+    return d;
+}
+
+__device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map, uint64_t* bar,
+                                            int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, "
+        "{%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <typename T, int BN, int kStages>
+__global__ void __launch_bounds__(192, 1)
+    gemm_tma_kernel(const __grid_constant__ CUtensorMap map_a,
+                    const __grid_constant__ CUtensorMap map_b, float* __restrict__ C, int ldc,
+                    int M, int N, int K, int accumulate_c) {
+    constexpr bool kTF32 = sizeof(T) == 4;
+    constexpr int kBK = 128 / (int)sizeof(T);              // one 128-byte atom of K
+    constexpr int kABytes = kGemmBM * 128;
+    constexpr int kBBytes = BN * 128;
+    constexpr int kPlanes = kTF32 ? 2 : 1;
+    constexpr int kStageBytes = kPlanes * (kABytes + kBBytes);
+    constexpr uint32_t kTmemCols = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // SWIZZLE_128B stages need 1024-byte alignment
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ __align__(8) uint64_t full[kStages], empty[kStages], split[kStages], accum;
+    __shared__ uint32_t s_tmem;
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int m0 = blockIdx.x * kGemmBM;
+    const int n0 = blockIdx.y * BN;
+    const int nk = (K + kBK - 1) / kBK;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(&s_tmem)),
+                     "n"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) {
+        for (int i = 0; i < kStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+            mbar_init(&split[i], 128);
+        }
+        mbar_init(&accum, 1);
+        fence_mbar_init();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = s_tmem;
+
+    auto a_hi = [&](int st) { return smem + st * kStageBytes; };
+    auto b_hi = [&](int st) { return smem + st * kStageBytes + kABytes; };
+    auto a_lo = [&](int st) { return smem + st * kStageBytes + kABytes + kBBytes; };
+    auto b_lo = [&](int st) { return smem + st * kStageBytes + 2 * kABytes + kBBytes; };
+
+    if (warp == 0) {
+        if (lane == 0) {                                     // ---- TMA producer
+            for (int kb = 0; kb < nk; ++kb) {
+                const int st = kb % kStages;
+                if (kb >= kStages) mbar_wait(&empty[st], (uint32_t)((kb / kStages - 1) & 1));
+                mbar_arrive_expect_tx(&full[st], kABytes + kBBytes);
+                tma_load_2d(a_hi(st), &map_a, &full[st], kb * kBK, m0);
+                tma_load_2d(b_hi(st), &map_b, &full[st], kb * kBK, n0);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {                                     // ---- MMA issuer
+            const uint32_t idesc = umma_idesc(kTF32 ? 2 : 1, kGemmBM, BN);
+            for (int kb = 0; kb < nk; ++kb) {
+                const int st = kb % kStages;
+                mbar_wait(kTF32 ? &split[st] : &full[st], (uint32_t)((kb / kStages) & 1));
+                tc_fence_after();
+#pragma unroll
+                for (int s = 0; s < 4; ++s) {                // 4 x 32 bytes of K per atom
+                    const uint64_t dah = umma_desc_sw128(smem_u32(a_hi(st)) + 32 * s);
+                    const uint64_t dbh = umma_desc_sw128(smem_u32(b_hi(st)) + 32 * s);
+                    umma<kTF32>(tmem, dah, dbh, idesc, (kb > 0 || s > 0) ? 1u : 0u);
+                    if constexpr (kTF32) {
+                        const uint64_t dal = umma_desc_sw128(smem_u32(a_lo(st)) + 32 * s);
+                        const uint64_t dbl = umma_desc_sw128(smem_u32(b_lo(st)) + 32 * s);
+                        umma<kTF32>(tmem, dah, dbl, idesc, 1u);
+                        umma<kTF32>(tmem, dal, dbh, idesc, 1u);
+                    }
+                }
+                umma_commit(&empty[st]);                     // frees the stage when done
+            }
+            umma_commit(&accum);
+        }
+    } else {
+        const int et = tid - 64;                             // 0..127
+        if constexpr (kTF32) {                               // ---- 3xTF32 split
+            for (int kb = 0; kb < nk; ++kb) {
+                const int st = kb % kStages;
+                mbar_wait(&full[st], (uint32_t)((kb / kStages) & 1));
+                auto run = [&](uint8_t* hi, uint8_t* lo, int bytes) {
+                    for (int off = et * 16; off < bytes; off += 128 * 16) {
+                        uint4 v = *reinterpret_cast<uint4*>(hi + off);
+                        float* f = reinterpret_cast<float*>(&v);
+                        uint4 h, l;
+                        uint32_t* hp = reinterpret_cast<uint32_t*>(&h);
+                        uint32_t* lp = reinterpret_cast<uint32_t*>(&l);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            hp[q] = tf32_rna(f[q]);
+                            lp[q] = tf32_rna(f[q] - __uint_as_float(hp[q]));
+                        }
+                        *reinterpret_cast<uint4*>(hi + off) = h;
+                        *reinterpret_cast<uint4*>(lo + off) = l;
+                    }
+                };
+                run(a_hi(st), a_lo(st), kABytes);
+                run(b_hi(st), b_lo(st), kBBytes);
+                fence_proxy_async_smem();
+                mbar_arrive(&split[st]);
+            }
+        }
+        // ---- epilogue: TMEM lane quarter of this warp = warp % 4
+        mbar_wait(&accum, 0u);
+        tc_fence_after();
+        const int q = warp & 3;
+        const int row = m0 + q * 32 + lane;
+        const uint32_t lane_addr = tmem + ((uint32_t)(q * 32) << 16);
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 8) {
+            uint32_t r[8];
+            tmem_ld8(lane_addr + c0, r);
+            if (row < M) {
+                float* crow = C + (size_t)row * ldc;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int col = n0 + c0 + j;
+                    if (col < N) {
+                        const float v = __uint_as_float(r[j]);
+                        crow[col] = accumulate_c ? crow[col] + v : v;
+                    }
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "n"(kTmemCols)
+                     : "memory");
+    }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// 2-D K-major tensor map: dims (K, rows), box (128 bytes of K, box_rows), 128 B swizzle
+static bool make_map(CUtensorMap* map, const void* base, int dtype, int rows, int K, int ld,
+                     int box_rows) {
+    auto enc = tensor_map_encoder();
+    if (!enc) return false;
+    const size_t esz = elt_size(dtype);
+    const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld * esz};
+    const cuuint32_t box[2] = {(cuuint32_t)(128 / esz), (cuuint32_t)box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = enc(map, dtype == TDKV_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                                  : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                           2, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <typename T, int BN, int kStages>
+static int32_t launch_gemm_tma(const void* A, int lda, const void* B, int ldb, float* C, int ldc,
+                               int M, int N, int K, int accumulate, int dtype, cudaStream_t s,
+                               bool* ok) {
+    CUtensorMap ma, mb;
+    *ok = make_map(&ma, A, dtype, M, K, lda, kGemmBM) && make_map(&mb, B, dtype, N, K, ldb, BN);
+    if (!*ok) return TDKV_OK;
+    auto kern = gemm_tma_kernel<T, BN, kStages>;
+    constexpr int kPlanes = sizeof(T) == 4 ? 2 : 1;
+    const size_t smem = (size_t)kStages * kPlanes * (kGemmBM + BN) * 128 + 1024;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return check_launch("tdkv_gemm: cudaFuncSetAttribute");
+    dim3 grid((M + kGemmBM - 1) / kGemmBM, (N + BN - 1) / BN);
+    kern<<<grid, 192, smem, s>>>(ma, mb, C, ldc, M, N, K, accumulate);
+    return TDKV_OK;
+}
+
 }  // namespace tdkv
 
 using namespace tdkv;
@@ -297,6 +526,31 @@ extern "C" int32_t tdkv_gemm(const void* d_a, int32_t lda, const void* d_b, int3
     if (k == 0) return set_error(TDKV_EINVAL, "tdkv_gemm: K must be positive");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     int32_t rc;
+    bool tma = false;
+    if (!getenv("TDKV_GEMM_NO_TMA")) {
+        if (dtype == TDKV_F32) {
+            rc = n <= 64 ? launch_gemm_tma<float, 64, 4>(d_a, lda, d_b, ldb, d_c, ldc, m, n, k,
+                                                          accumulate, dtype, s, &tma)
+                         : launch_gemm_tma<float, 128, 3>(d_a, lda, d_b, ldb, d_c, ldc, m, n, k,
+                                                           accumulate, dtype, s, &tma);
+        } else {
+            const long long tiles256 = (long long)((m + 127) / 128) * ((n + 255) / 256);
+            if (n <= 64)
+                rc = launch_gemm_tma<__nv_bfloat16, 64, 6>(d_a, lda, d_b, ldb, d_c, ldc, m, n, k,
+                                                            accumulate, dtype, s, &tma);
+            else if (n >= 256 && tiles256 >= sm_count())
+                rc = launch_gemm_tma<__nv_bfloat16, 256, 4>(d_a, lda, d_b, ldb, d_c, ldc, m, n, k,
+                                                             accumulate, dtype, s, &tma);
+            else
+                rc = launch_gemm_tma<__nv_bfloat16, 128, 5>(d_a, lda, d_b, ldb, d_c, ldc, m, n, k,
+                                                             accumulate, dtype, s, &tma);
+        }
+        if (rc) return rc;
+        if (tma) {
+            count_launch();
+            return check_launch("tdkv_gemm");
+        }
+    }
     if (dtype == TDKV_F32) {
         rc = n <= 64 ? launch_gemm<float, 64>(d_a, lda, d_b, ldb, d_c, ldc, m, n, k, accumulate, s)
                      : launch_gemm<float, 128>(d_a, lda, d_b, ldb, d_c, ldc, m, n, k, accumulate, s);
