@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--mirror-frac", type=float, default=0.1)
     ap.add_argument("--codec-mirrors", type=int, default=49, help="mirrors per codec family")
+    ap.add_argument("--codec-sweep", action="store_true",
+                    help="encode/decode sweep over changed-block fractions (C4)")
     ap.add_argument("--profile", action="store_true", help="few launches, no extras (for ncu)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     return ap.parse_args()
@@ -455,6 +457,8 @@ def run_tdkv(args):
         line["codec"] = codec_bench(tk, spec, pool, maps, dev, args, peak)
         line["selection"] = selection_bench(tk, spec, pool, maps, dev, args, peak)
         line["recompute"] = recompute_bench(dev, args)
+        if args.codec_sweep:
+            line["codec_sweep"] = codec_sweep(tk, spec, pool, maps, dev, args, peak)
 
     if not args.no_cpu and not args.profile and rank == 0 and world == 1:
         line["cpu_baseline"] = cpu_baseline(spec, args.cpu_seconds)
@@ -586,7 +590,26 @@ def rounds_segment_starts(spec, a):
     return rounds.segment_starts(spec, a)
 
 
-def codec_bench(tk, spec, pool, maps, dev, args, peak):
+def codec_sweep(tk, spec, pool, maps, dev, args, peak):
+    """The diff-aware storage sweep of SURVEY §8d: changed-block fractions
+    0 .. 1, plus the 'hint everything' variant at 10%."""
+    out = []
+    for frac, hint_all in ((0.0, False), (0.05, False), (0.1, False), (0.2, False),
+                           (0.5, False), (1.0, False), (0.1, True)):
+        r = codec_bench(tk, spec, pool, maps, dev, args, peak, frac=frac, hint_all=hint_all)
+        out.append({"changed_fraction": frac, "hint_all": hint_all,
+                    "encode_gbs": r["encode_gbs"], "encode_device_gbs": r["encode_device_gbs"],
+                    "decode_gbs": r["decode_gbs"], "compression_ratio": r["compression_ratio_mean"]})
+        torch_empty_cache()
+    return out
+
+
+def torch_empty_cache():
+    import torch
+    torch.cuda.empty_cache()
+
+
+def codec_bench(tk, spec, pool, maps, dev, args, peak, frac=None, hint_all=False):
     """Encode the agents' caches as diffs against agent 0's, then fused-restore
     every mirror into the pool; each mirror is agent 0's cache with a
     fraction of its 32-token blocks (all layers) re-drawn."""
@@ -594,6 +617,7 @@ def codec_bench(tk, spec, pool, maps, dev, args, peak):
     bs = 32
     T = spec.tokens_per_agent
     nb = -(-T // bs)
+    frac = args.mirror_frac if frac is None else frac
     n_mirrors = max(1, min(len(maps) - 1, args.codec_mirrors))
     sl0 = maps[0].device_slots(dev)
     mk = pool.k[:, sl0].contiguous()
@@ -602,17 +626,22 @@ def codec_bench(tk, spec, pool, maps, dev, args, peak):
     rng = np.random.default_rng(3)
     g = torch.Generator(device=dev).manual_seed(3)
     mirrors, hints = [], []
-    n_pick = max(1, int(round(args.mirror_frac * nb)))
+    n_pick = int(round(frac * nb))
+    tok_block = torch.arange(T, device=dev) // bs
     for _ in range(n_mirrors):
         blocks = np.sort(rng.choice(nb, n_pick, replace=False))
-        k = mk.clone()
-        v = mv.clone()
-        for b in blocks:
-            lo, hi = b * bs, min(T, b * bs + bs)
-            k[:, lo:hi] = torch.randn(k[:, lo:hi].shape, generator=g, device=dev).to(k.dtype)
-            v[:, lo:hi] = torch.randn(v[:, lo:hi].shape, generator=g, device=dev).to(v.dtype)
+        sel = torch.zeros(nb, dtype=torch.bool, device=dev)
+        if n_pick:
+            sel[torch.from_numpy(blocks).to(dev)] = True
+        row = sel[tok_block].view(1, T, 1, 1)
+        k = torch.where(row, torch.randn(mk.shape, generator=g, device=dev).to(mk.dtype), mk)
+        v = torch.where(row, torch.randn(mv.shape, generator=g, device=dev).to(mv.dtype), mv)
         mirrors.append(tk.LayeredKv(k, v, np.arange(T)))
-        hints.append(np.concatenate([np.arange(b * bs, min(T, b * bs + bs)) for b in blocks]))
+        if hint_all:
+            hints.append(np.arange(T))
+        else:
+            hints.append(np.concatenate([np.arange(b * bs, min(T, b * bs + bs)) for b in blocks])
+                         if n_pick else np.zeros(0, np.int64))
     blocks_cfg = tk.CacheBlockConfig(bs)
     dense = spec.dense_bytes
     # encode (K2 compare + compact + the host read of counts/indices)
