@@ -156,6 +156,20 @@ int32_t tdkv_diff_compact(const tdkv_diff_pair* d_pairs,
                           int32_t num_heads, int32_t head_dim,
                           int32_t block_size, int32_t dtype, void* stream);
 
+/* Single-pass form of the two calls above (what the encoder uses): compare,
+ * stream compaction and payload copy in one launch.  Tiles (pair, layer,
+ * block) are handed out by an atomic ticket (d_ticket, 1 int32 scratch); a
+ * block publishes its status in d_flags (n_pairs*L*nb int32 scratch) and a
+ * changed, hinted block finds its payload slot by looking back over the
+ * flags of the earlier blocks of its layer.  Same outputs and violation
+ * reporting as tdkv_diff_compare + tdkv_diff_compact. */
+int32_t tdkv_diff_encode(const tdkv_diff_pair* d_pairs, const tdkv_diff_out* d_outs,
+                         int32_t n_pairs, const uint8_t* d_hinted, int32_t* d_flags,
+                         int32_t* d_ticket, int32_t* d_counts, int32_t* d_violation,
+                         float* d_viol_maxabs, int32_t num_layers, int32_t num_tokens,
+                         int32_t num_heads, int32_t head_dim, int32_t block_size,
+                         int32_t dtype, void* stream);
+
 /* ------------------------------------------------------------------------
  * K3  row mover: gather -> (diff overlay) -> rotate -> scatter.
  * Replaces restore.fused_restore (restore.py:50-104, with _apply_layer_diff

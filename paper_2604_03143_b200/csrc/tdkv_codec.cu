@@ -177,6 +177,136 @@ __global__ void __launch_bounds__(256)
     if (threadIdx.x == 0) counts[pi * g.num_layers + layer] = running;
 }
 
+// Single-pass encoder: compare, stream compaction and payload copy in one
+// launch.  Tiles are (pair, layer, block) in row-major order and are handed
+// out by an atomic ticket, so a CTA only ever waits on tiles that started
+// before it (no deadlock).  Each CTA compares its block, publishes
+// "unchanged" (1) or "stored" (2) with release semantics, and a stored block
+// computes its payload slot as the number of stored blocks before it in the
+// same (pair, layer) -- a look-back over the published flags -- then copies
+// the mirror block (still L2-resident: it was read microseconds ago) to the
+// slot, zero-padded.  DRAM traffic is the algorithmic 2 x dense + payload.
+template <typename T, int UB>
+__global__ void __launch_bounds__(256)
+    diff_encode_kernel(const tdkv_diff_pair* __restrict__ pairs,
+                       const tdkv_diff_out* __restrict__ outs, const uint8_t* __restrict__ hinted,
+                       int32_t* flags, int32_t* ticket, int32_t* __restrict__ counts,
+                       int32_t* __restrict__ violation, float* __restrict__ viol_maxabs,
+                       const CodecGeom g) {
+    using V = typename UnitBits<UB>::V;
+    constexpr int kUnroll = 2;
+    __shared__ int s_tile, s_before;
+    __shared__ float red[32];
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
+    __syncthreads();
+    const int item = s_tile;
+    const int per_pair = g.num_layers * g.nb;
+    const int pi = item / per_pair;
+    const int rem = item - pi * per_pair;
+    const int layer = rem / g.nb;
+    const int b = rem - layer * g.nb;
+    const int lo = b * g.block_size;
+    const int hi = min(lo + g.block_size, g.num_tokens);
+    const int upr = g.row_elems * (int)sizeof(T) / UB;
+    const int units = (hi - lo) * upr;
+    const size_t off_units = ((size_t)layer * g.num_tokens + lo) * upr;
+    const tdkv_diff_pair pr = pairs[pi];
+    const V* mk = static_cast<const V*>(pr.master_k) + off_units;
+    const V* mv = static_cast<const V*>(pr.master_v) + off_units;
+    const V* rk = static_cast<const V*>(pr.mirror_k) + off_units;
+    const V* rv = static_cast<const V*>(pr.mirror_v) + off_units;
+
+    bool diff = false;
+    int u = threadIdx.x;
+    for (; u + (kUnroll - 1) * (int)blockDim.x < units; u += kUnroll * blockDim.x) {
+        V a[kUnroll][4];
+#pragma unroll
+        for (int q = 0; q < kUnroll; ++q) {
+            const int w = u + q * blockDim.x;
+            a[q][0] = ld_stream(mk + w);
+            a[q][1] = __ldcg(rk + w);          // mirror stays in L2 for the copy
+            a[q][2] = ld_stream(mv + w);
+            a[q][3] = __ldcg(rv + w);
+        }
+#pragma unroll
+        for (int q = 0; q < kUnroll; ++q)
+            diff |= unit_differs<T>(a[q][0], a[q][1]) | unit_differs<T>(a[q][2], a[q][3]);
+    }
+    for (; u < units; u += blockDim.x)
+        diff |= unit_differs<T>(ld_stream(mk + u), __ldcg(rk + u)) |
+                unit_differs<T>(ld_stream(mv + u), __ldcg(rv + u));
+    const int any = __syncthreads_or(diff);
+    const bool is_hinted = hinted[(size_t)pi * g.nb + b] != 0;
+    const bool stored = any && is_hinted;
+    const size_t row = ((size_t)pi * g.num_layers + layer) * g.nb;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicExch(flags + row + b, stored ? 2 : 1);        // publish
+    }
+    const tdkv_diff_out out = outs[pi];
+    if (any && !is_hinted) {
+        // soundness violation (rare): max |mirror - master| over both planes
+        float m = 0.f;
+        for (int w = threadIdx.x; w < units; w += blockDim.x) {
+            m = fmaxf(m, unit_maxabs<T>(mk[w], rk[w]));
+            m = fmaxf(m, unit_maxabs<T>(mv[w], rv[w]));
+        }
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            float mm = 0.f;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mm = fmaxf(mm, red[w]);
+            viol_maxabs[row + b] = mm;
+            atomicMin(violation + pi, layer * g.nb + b);
+        }
+    }
+    const bool last = b == g.nb - 1;
+    if (!stored && !last) {
+        if (threadIdx.x == 0) out.blkmap[layer * g.nb + b] = -1;
+        return;
+    }
+    // look-back: stored blocks before b in this (pair, layer); predecessors
+    // hold lower tickets, so they are running or done
+    int before = 0;
+    for (int j = threadIdx.x; j < b; j += blockDim.x) {
+        int f;
+        volatile int32_t* fp = flags + row + j;
+        while ((f = *fp) == 0) {}
+        before += f == 2;
+    }
+    __threadfence();
+    for (int o = 16; o > 0; o >>= 1) before += __shfl_xor_sync(0xffffffffu, before, o);
+    if (threadIdx.x == 0) s_before = 0;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0 && before) atomicAdd(&s_before, before);
+    __syncthreads();
+    const int slot = s_before;
+    if (last && threadIdx.x == 0) counts[pi * g.num_layers + layer] = slot + (stored ? 1 : 0);
+    if (!stored) {
+        if (threadIdx.x == 0) out.blkmap[layer * g.nb + b] = -1;
+        return;
+    }
+    if (slot >= out.cap) return;                     // only after a violation
+    if (threadIdx.x == 0) {
+        out.indices[layer * out.cap + slot] = b;
+        out.blkmap[layer * g.nb + b] = layer * out.cap + slot;
+    }
+    const int blk_units = g.block_size * upr;
+    const size_t dst = ((size_t)layer * out.cap + slot) * blk_units;
+    V* pk = static_cast<V*>(out.payload_k) + dst;
+    V* pv = static_cast<V*>(out.payload_v) + dst;
+    for (int w = threadIdx.x; w < blk_units; w += blockDim.x) {
+        V kx{}, vx{};
+        if (w < units) {
+            kx = ld_stream(rk + w);
+            vx = ld_stream(rv + w);
+        }
+        pk[w] = kx;
+        pv[w] = vx;
+    }
+}
+
 }  // namespace tdkv
 
 using namespace tdkv;
@@ -269,4 +399,51 @@ extern "C" int32_t tdkv_diff_compact(const tdkv_diff_pair* d_pairs, const tdkv_d
     }
     count_launch();
     return check_launch("tdkv_diff_compact");
+}
+
+extern "C" int32_t tdkv_diff_encode(const tdkv_diff_pair* d_pairs, const tdkv_diff_out* d_outs,
+                                    int32_t n_pairs, const uint8_t* d_hinted, int32_t* d_flags,
+                                    int32_t* d_ticket, int32_t* d_counts, int32_t* d_violation,
+                                    float* d_viol_maxabs, int32_t num_layers, int32_t num_tokens,
+                                    int32_t num_heads, int32_t head_dim, int32_t block_size,
+                                    int32_t dtype, void* stream) {
+    int32_t rc = codec_check("tdkv_diff_encode", n_pairs, num_layers, num_tokens, num_heads,
+                             head_dim, block_size, dtype);
+    if (rc) return rc;
+    if (n_pairs == 0) return TDKV_OK;
+    if (!d_pairs || !d_outs || !d_hinted || !d_flags || !d_ticket || !d_counts || !d_violation ||
+        !d_viol_maxabs)
+        return set_error(TDKV_EINVAL, "tdkv_diff_encode: null pointer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    CodecGeom g{num_layers, num_tokens, num_heads * head_dim, block_size,
+                ceil_div(num_tokens, block_size)};
+    const long long items = (long long)n_pairs * num_layers * g.nb;
+    if (items > INT_MAX) return set_error(TDKV_EINVAL, "tdkv_diff_encode: batch too large");
+    if (cudaMemsetAsync(d_flags, 0, sizeof(int32_t) * items, s) != cudaSuccess ||
+        cudaMemsetAsync(d_ticket, 0, sizeof(int32_t), s) != cudaSuccess ||
+        cudaMemsetAsync(d_violation, 0x7f, sizeof(int32_t) * n_pairs, s) != cudaSuccess)
+        return check_launch("tdkv_diff_encode: memset");
+    const int ub = codec_unit(dtype, g.row_elems);
+    const dim3 grid((unsigned)items);
+    if (dtype == TDKV_F32) {
+        if (ub == 16)
+            diff_encode_kernel<float, 16><<<grid, 256, 0, s>>>(d_pairs, d_outs, d_hinted, d_flags,
+                                                               d_ticket, d_counts, d_violation,
+                                                               d_viol_maxabs, g);
+        else
+            diff_encode_kernel<float, 4><<<grid, 256, 0, s>>>(d_pairs, d_outs, d_hinted, d_flags,
+                                                              d_ticket, d_counts, d_violation,
+                                                              d_viol_maxabs, g);
+    } else {
+        if (ub == 16)
+            diff_encode_kernel<__nv_bfloat16, 16><<<grid, 256, 0, s>>>(
+                d_pairs, d_outs, d_hinted, d_flags, d_ticket, d_counts, d_violation, d_viol_maxabs,
+                g);
+        else
+            diff_encode_kernel<__nv_bfloat16, 4><<<grid, 256, 0, s>>>(
+                d_pairs, d_outs, d_hinted, d_flags, d_ticket, d_counts, d_violation, d_viol_maxabs,
+                g);
+    }
+    count_launch();
+    return check_launch("tdkv_diff_encode");
 }

@@ -31,6 +31,9 @@ from .core import CacheBlockConfig, LayeredKv
 
 MAGIC = b"TDDF"
 VERSION = 1
+# single-pass encoder (tdkv_diff_encode); TDKV_TWO_PASS_ENCODE=1 selects the
+# compare + compact pair
+_SINGLE_PASS = not __import__("os").environ.get("TDKV_TWO_PASS_ENCODE")
 _HEADER = struct.Struct("<4sHHIIII")
 
 
@@ -277,7 +280,7 @@ def encode_launch(master: LayeredKv, mirrors: Sequence[LayeredKv],
     violation = meta[:P]
     counts = meta[P:P + P * L]
     indices = meta[P + P * L:]
-    changed = torch.empty(P * L * nb, dtype=torch.uint8, device=device)
+    changed = None if _SINGLE_PASS else torch.empty(P * L * nb, dtype=torch.uint8, device=device)
     viol_maxabs = torch.empty(P * L * nb, dtype=torch.float32, device=device)  # violations only
     pay_k = torch.empty((slab_blocks, bs, H, D), dtype=dtype, device=device)
     pay_v = torch.empty_like(pay_k)
@@ -301,10 +304,17 @@ def encode_launch(master: LayeredKv, mirrors: Sequence[LayeredKv],
     d_pairs, d_outs, d_hinted = ptr(d_desc), ptr(d_desc) + P * 32, ptr(d_desc) + P * 72
     code = dtype_code(dtype)
     stream = stream_handle(device)
-    _lib.call("tdkv_diff_compare", d_pairs, P, d_hinted, ptr(changed), ptr(violation),
-              ptr(viol_maxabs), L, total, H, D, bs, code, stream)
-    _lib.call("tdkv_diff_compact", d_pairs, d_outs, P, ptr(changed), ptr(counts),
-              L, total, H, D, bs, code, stream)
+    if _SINGLE_PASS:
+        # one launch: compare + look-back compaction + payload copy
+        flags = torch.empty(P * L * nb + 1, dtype=torch.int32, device=device)
+        _lib.call("tdkv_diff_encode", d_pairs, d_outs, P, d_hinted, ptr(flags),
+                  ptr(flags) + 4 * P * L * nb, ptr(counts), ptr(violation), ptr(viol_maxabs),
+                  L, total, H, D, bs, code, stream)
+    else:
+        _lib.call("tdkv_diff_compare", d_pairs, P, d_hinted, ptr(changed), ptr(violation),
+                  ptr(viol_maxabs), L, total, H, D, bs, code, stream)
+        _lib.call("tdkv_diff_compact", d_pairs, d_outs, P, ptr(changed), ptr(counts),
+                  L, total, H, D, bs, code, stream)
     return _EncodeState(P, L, H, D, bs, nb, total, caps, starts, meta, viol_maxabs, pay_k,
                         pay_v, blkmap)
 
