@@ -296,14 +296,31 @@ __global__ void __launch_bounds__(256)
     const size_t dst = ((size_t)layer * out.cap + slot) * blk_units;
     V* pk = static_cast<V*>(out.payload_k) + dst;
     V* pv = static_cast<V*>(out.payload_v) + dst;
-    for (int w = threadIdx.x; w < blk_units; w += blockDim.x) {
+    // the mirror tile was just read with .cg, so these loads mostly hit L2;
+    // 4 independent 16-byte loads per plane per thread before any store
+    constexpr int kCopy = 4;
+    int w = threadIdx.x;
+    for (; w + (kCopy - 1) * (int)blockDim.x < units; w += kCopy * blockDim.x) {
+        V kx[kCopy], vx[kCopy];
+#pragma unroll
+        for (int q = 0; q < kCopy; ++q) {
+            kx[q] = ld_stream(rk + w + q * blockDim.x);
+            vx[q] = ld_stream(rv + w + q * blockDim.x);
+        }
+#pragma unroll
+        for (int q = 0; q < kCopy; ++q) {
+            st_stream(pk + w + q * blockDim.x, kx[q]);
+            st_stream(pv + w + q * blockDim.x, vx[q]);
+        }
+    }
+    for (; w < blk_units; w += blockDim.x) {
         V kx{}, vx{};
         if (w < units) {
             kx = ld_stream(rk + w);
             vx = ld_stream(rv + w);
         }
-        pk[w] = kx;
-        pv[w] = vx;
+        st_stream(pk + w, kx);
+        st_stream(pv + w, vx);
     }
 }
 
