@@ -8,6 +8,11 @@ has two exchange steps:
 * ``broadcast_arena`` -- the shared master blocks, once per round, from the
   rank that holds them (NCCL broadcast; every rank then runs K0 + K1 for its
   own agents);
+* ``exchange_collect`` -- multi-session rounds sharded by agent
+  (strong scaling): each session's masters live on the rank that runs the
+  session's first agent and travel point-to-point (NCCL send/recv over
+  NVLink) only to the other ranks whose shard touches that session, layer
+  chunk by layer chunk, overlapped with K1 like ``broadcast_collect``;
 * ``elect_master`` -- an all-gather of every rank's (deviation, request id)
   pairs so all ranks elect the same family master,
   argmin over (score, id) exactly as collective.select_master
@@ -22,10 +27,9 @@ import torch.distributed as dist
 
 
 def shard_range(num_agents: int, rank: int, world: int) -> range:
-    """Contiguous agent ids of ``rank`` (the last ranks may get fewer)."""
-    per = (num_agents + world - 1) // world
-    lo = min(num_agents, rank * per)
-    return range(lo, min(num_agents, lo + per))
+    """Contiguous agent ids of ``rank``; shard sizes differ by at most one."""
+    lo = rank * num_agents // world
+    return range(lo, (rank + 1) * num_agents // world)
 
 
 def broadcast_arena(arena, src: int = 0, group=None) -> int:
@@ -61,6 +65,54 @@ def broadcast_collect(collector, plan, src: int = 0, chunks: int = 7, group=None
     if ledger is not None and plan.num_jobs:
         for layer in range(L):
             ledger.record_rope_call(layer)
+    return n
+
+
+def _layer_chunks(L: int, chunks: int):
+    bounds = [round(i * L / chunks) for i in range(chunks + 1)]
+    return [(l0, l1) for l0, l1 in zip(bounds[:-1], bounds[1:]) if l1 > l0]
+
+
+def session_transfers(owners, needs):
+    """(session, src, dst) for every rank that needs a session it does not
+    own -- the round's whole exchange."""
+    return [(s, owners[s], r) for r, ss in enumerate(needs) for s in ss if owners[s] != r]
+
+
+def exchange_sessions(arena, session_rows, transfers, rank: int, layers=None, group=None):
+    """Post the point-to-point transfers of ``layers`` (default: all) of the
+    sessions in ``transfers``; returns the requests (empty if this rank takes
+    no part).  One op per (layer, plane, transfer): a layer's session rows
+    are contiguous in the (L, rows, H, D) arena."""
+    l0, l1 = layers or (0, arena.num_layers)
+    ops = []
+    for s, src, dst in transfers:
+        if rank not in (src, dst):
+            continue
+        r0, r1 = session_rows[s]
+        for layer in range(l0, l1):
+            for plane in (arena.k, arena.v):
+                t = plane[layer, r0:r1]
+                ops.append(dist.P2POp(dist.isend if rank == src else dist.irecv, t,
+                                      dst if rank == src else src, group=group))
+    return dist.batch_isend_irecv(ops) if ops else []
+
+
+def exchange_collect(collector, plans, session_rows, transfers, rank: int, chunks: int = 4,
+                     group=None) -> int:
+    """One multi-session round on one rank: K0 for every plan, then per layer
+    chunk the chunk's session transfers (send or receive) and K1 for the
+    plans once the chunk has landed.  ``plans`` are this rank's sub-batches.
+    Returns the kernels launched."""
+    arena, pool = collector.arena, collector.pool
+    n = sum(p.launch_table() for p in plans)
+    pending = [(l0, l1, exchange_sessions(arena, session_rows, transfers, rank, (l0, l1), group))
+               for l0, l1 in _layer_chunks(arena.num_layers, chunks)]
+    for l0, l1, reqs in pending:
+        for r in reqs:
+            r.wait()
+        for p in plans:
+            n += p.launch_collect(arena, pool.k, pool.v, pool.layer_stride, layers=(l0, l1))
     return n
 
 

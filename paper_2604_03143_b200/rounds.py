@@ -32,6 +32,9 @@ class RoundSpec:
     hist_len: int
     max_source: int = 8192
     sessions: int = 1          # independent groups; agents and segments split evenly
+    strong: bool = False       # multi-GPU: total agents fixed and sharded (else per-GPU fixed)
+    sub_batch: int = 0         # >0: a GPU's pool holds this many agents; its shard is
+                               # collected in sub-batches (C5 at small GPU counts)
 
     @property
     def agents_per_session(self) -> int:
@@ -82,6 +85,21 @@ class RoundSpec:
         touched = len({self.session_of(a) for a in range(n)})
         return self.session_master_bytes * (touched + n)
 
+    def collector_bytes_for(self, agents: Sequence[int]) -> int:
+        """Algorithmic collector bytes of an arbitrary agent set: the masters
+        of every session it touches read once, one copy written per agent."""
+        agents = list(agents)
+        touched = len({self.session_of(a) for a in agents})
+        return self.session_master_bytes * (touched + len(agents))
+
+    def session_rows(self, session: int) -> Tuple[int, int]:
+        """Arena row range [r0, r1) of a session's masters."""
+        n = self.num_segments * self.seg_len
+        return session * n, (session + 1) * n
+
+    def sessions_of(self, agents: Sequence[int]) -> List[int]:
+        return sorted({self.session_of(a) for a in agents})
+
     @property
     def dense_bytes(self) -> int:
         return 2 * self.num_layers * self.tokens_per_agent * self.row_bytes
@@ -96,8 +114,10 @@ CONFIGS = {
     "c1": RoundSpec("c1-toy-8x4x256-f32", 2, 8, 64, "f32", 8, 4, 256, 64),
     "c2": RoundSpec("c2-qwen7b-50x16x256-bf16", 28, 4, 128, "bf16", 50, 16, 256, 512),
     "c3": RoundSpec("c3-qwen14b-250x25x20-10sessions-bf16", 48, 8, 128, "bf16", 250, 25, 20,
-                    192, sessions=10),
+                    192, sessions=10, strong=True),
     "c4": RoundSpec("c4-agentsociety-100x32x128-bf16", 28, 4, 128, "bf16", 100, 32, 128, 8192),
+    "c5": RoundSpec("c5-qwen7b-1000-agent-shard-bf16", 28, 4, 128, "bf16", 1000, 16, 256, 512,
+                    strong=True, sub_batch=125),
 }
 
 
@@ -166,7 +186,22 @@ def round_offsets(spec: RoundSpec, agents, slot_base: np.ndarray):
 
 
 def shard(num_agents: int, rank: int, world: int) -> range:
-    """Contiguous agent shard of a rank."""
-    per = (num_agents + world - 1) // world
-    lo = min(num_agents, rank * per)
-    return range(lo, min(num_agents, lo + per))
+    """Contiguous agent shard of a rank: sizes differ by at
+    most one, so a session spans as few ranks as possible."""
+    lo = rank * num_agents // world
+    return range(lo, (rank + 1) * num_agents // world)
+
+
+def session_owners(spec: RoundSpec, world: int) -> List[int]:
+    """The rank holding each session's masters: the rank of the session's
+    first agent (the masters are produced where that session runs)."""
+    owners = []
+    for s in range(spec.sessions):
+        first = s * spec.agents_per_session
+        owners.append(next(r for r in range(world) if first in shard(spec.num_agents, r, world)))
+    return owners
+
+
+def session_needs(spec: RoundSpec, world: int) -> List[List[int]]:
+    """Per rank, the sessions whose masters its agent shard reads."""
+    return [spec.sessions_of(shard(spec.num_agents, r, world)) for r in range(world)]
