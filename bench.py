@@ -7,8 +7,10 @@ synthetic round (default C2: Qwen2.5-7B-shaped bf16 KV, 50 agents per GPU x
 16 shared 256-token blocks): [N>1: NCCL broadcast of the master arena from
 rank 0] + K0 (cos/sin rows) + K1 (rotate + scatter into every agent's paged
 slots).  ``value`` = algorithmic bytes (M + N*M per GPU) of all
-ranks / max-over-ranks device time.  Agents are sharded (weak scaling: each
-GPU owns ``agents`` agents).
+ranks / max-over-ranks device time.  Agents are sharded: weak scaling (each
+GPU owns a config's worth of agents: C1, C2, C4) or strong scaling (the
+config's agents split over the GPUs: C3's 250 agents in 10 sessions, C5's
+1000 agents collected in pool sub-batches of 125).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2]
     python bench.py --impl reference ...   # CPU oracle port on the host cores
@@ -47,6 +49,9 @@ def parse():
                     help="encode/decode sweep over changed-block fractions (C4)")
     ap.add_argument("--profile", action="store_true", help="few launches, no extras (for ncu)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--scaling", default="auto", choices=["auto", "weak", "strong"],
+                    help="strong: the config's agents are sharded over the GPUs (C3, C5); "
+                         "weak: every GPU owns a config's worth of agents (auto: per config)")
     return ap.parse_args()
 
 
@@ -251,7 +256,9 @@ def run_tdkv(args):
 
     import paper_2604_03143_b200 as tk
     from paper_2604_03143_b200 import rounds
-    from paper_2604_03143_b200.dist import broadcast_collect
+    from paper_2604_03143_b200.dist import (broadcast_arena, broadcast_collect,
+                                            exchange_collect, exchange_sessions,
+                                            session_transfers)
 
     world, rank, local = dist_env()
     # one GPU per rank; --dist-backend gloo lets a single-GPU box exercise the
@@ -266,10 +273,20 @@ def run_tdkv(args):
     spec = rounds.CONFIGS[args.config]
     if args.agents:
         spec = spec.scaled(num_agents=args.agents)
+    strong = spec.strong if args.scaling == "auto" else args.scaling == "strong"
     dt = spec.torch_dtype
     L, H, D = spec.num_layers, spec.num_heads, spec.head_dim
     T = spec.tokens_per_agent
-    n_local = spec.num_agents
+    # strong: the config's agents are sharded over the ranks (contiguous, so a
+    # session spans as few ranks as possible); weak: every rank owns a full
+    # config's worth of agents
+    if strong:
+        agents = list(rounds.shard(spec.num_agents, rank, world))
+    else:
+        agents = list(range(rank * spec.num_agents, (rank + 1) * spec.num_agents))
+    n_local = len(agents)
+    sb = min(n_local, spec.sub_batch) if spec.sub_batch else n_local
+    batches = [agents[i:i + sb] for i in range(0, n_local, sb)]
 
     # masters: host-pinned copy (the e2e input) + device arena
     mk_h, mv_h = rounds.master_planes_host(spec)
@@ -277,28 +294,44 @@ def run_tdkv(args):
     host_v = torch.from_numpy(mv_h).to(dt).pin_memory()
     del mk_h, mv_h
     arena = rounds.make_arena(spec, host_k.to(dev), host_v.to(dev))
-    pool = tk.PagedPool(n_local * T, L, H, D, dtype=dt, device=dev, debug=False)
-    agents = range(rank * n_local, (rank + 1) * n_local)
-    maps = [pool.allocate(T, a) for a in agents]
-
-    def make_jobs():
-        return [j for a, m in zip(agents, maps) for j in rounds.agent_jobs(spec, a, m.slots)]
+    # the pool holds one sub-batch of agents; sub-batch j reuses its slots
+    pool = tk.PagedPool(sb * T, L, H, D, dtype=dt, device=dev, debug=False)
+    maps = [pool.allocate(T, a) for a in batches[0]]
 
     collector = tk.KVCollector(arena, pool)
-    plan = collector.plan(make_jobs())
-    step_bytes = spec.collector_bytes(n_local)
-    assert plan.algorithmic_bytes() == step_bytes
+    plans = [collector.plan([j for a, m in zip(b, maps) for j in rounds.agent_jobs(spec, a, m.slots)])
+             for b in batches]
+    plan = plans[0]
+    step_bytes = sum(spec.collector_bytes_for(b) for b in batches)
+    assert sum(p.algorithmic_bytes() for p in plans) == step_bytes
+
+    # the round's one exchange (N>1): a single-session round broadcasts its
+    # masters from rank 0; a multi-session round sends each session only to
+    # the ranks whose shard reads it (point-to-point, NCCL over NVLink)
+    owners = rounds.session_owners(spec, world) if strong else [0] * spec.sessions
+    needs = (rounds.session_needs(spec, world) if strong
+             else [list(range(spec.sessions))] * world)
+    transfers = session_transfers(owners, needs)
+    use_broadcast = spec.sessions == 1 or not strong
+    session_rows = [spec.session_rows(s) for s in range(spec.sessions)]
+    if use_broadcast:
+        recv_bytes = spec.master_bytes if rank != 0 else 0
+    else:
+        recv_bytes = sum(spec.session_master_bytes for s, _, d in transfers if d == rank)
 
     stream = torch.cuda.current_stream(dev)
 
     def round_step(events=None):
         if events is not None:
             events[0].record(stream)
-        if world > 1:
+        if world > 1 and use_broadcast:
             # masters broadcast from rank 0 in layer chunks, K1 per landed chunk
-            broadcast_collect(collector, plan, 0, chunks=7)
+            broadcast_collect(collector, plans, 0, chunks=7)
+        elif world > 1:
+            exchange_collect(collector, plans, session_rows, transfers, rank, chunks=4)
         else:
-            collector.collect(plan)
+            for p in plans:
+                collector.collect(p)
         if events is not None:
             events[1].record(stream)
 
@@ -307,13 +340,19 @@ def run_tdkv(args):
             dist.barrier()
         torch.cuda.synchronize(dev)
 
-    def max_over_ranks(x: float) -> float:
+    def reduce_over_ranks(x: float, op) -> float:
         if world == 1:
             return x
         t = torch.tensor([x], dtype=torch.float64,
                          device=dev if args.dist_backend == "nccl" else "cpu")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=op)
         return float(t.item())
+
+    def max_over_ranks(x: float) -> float:
+        return reduce_over_ranks(x, dist.ReduceOp.MAX if world > 1 else None)
+
+    total_bytes = int(reduce_over_ranks(float(step_bytes), dist.ReduceOp.SUM if world > 1 else None))
+    total_agents = int(reduce_over_ranks(float(n_local), dist.ReduceOp.SUM if world > 1 else None))
 
     # -- device-timed rounds ------------------------------------------------
     for _ in range(args.warmup):
@@ -335,8 +374,33 @@ def run_tdkv(args):
     elapsed_ms = max_over_ranks(start.elapsed_time(stop))
     ms_step = elapsed_ms / args.steps
     k1_ms = sum(a.elapsed_time(b) for a, b in k1_events) / args.steps
-    value = world * step_bytes / (ms_step * 1e-3) / 1e9
-    agents_per_s = world * n_local / (ms_step * 1e-3)
+    value = total_bytes / (ms_step * 1e-3) / 1e9
+    agents_per_s = total_agents / (ms_step * 1e-3)
+
+    # the exchange alone (N>1): NVLink receive roofline of the busiest rank
+    exchange = None
+    if world > 1 and not args.profile:
+        x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        x0.record(stream)
+        for _ in range(args.steps):
+            if use_broadcast:
+                broadcast_arena(arena, 0)
+            else:
+                for r in exchange_sessions(arena, session_rows, transfers, rank):
+                    r.wait()
+        x1.record(stream)
+        barrier()
+        x_ms = max_over_ranks(x0.elapsed_time(x1)) / args.steps
+        busiest = int(max_over_ranks(float(recv_bytes)))
+        nvlink_peak = 900.0          # NVLink 5, GB/s per direction per GPU (nominal)
+        exchange = {"kind": "broadcast" if use_broadcast else "session p2p",
+                    "recv_bytes_max_rank": busiest, "ms": round(x_ms, 4),
+                    "achieved": round(busiest / (x_ms * 1e-3) / 1e9, 1) if x_ms > 0 else None,
+                    "peak": nvlink_peak, "unit": "GB/s",
+                    "frac": round(busiest / (x_ms * 1e-3) / 1e9 / nvlink_peak, 4)
+                    if x_ms > 0 else None,
+                    "backend": args.dist_backend}
 
     peak, peak_kind = measured_peak_hbm()
     achieved = step_bytes / (k1_ms * 1e-3) / 1e9
@@ -344,10 +408,12 @@ def run_tdkv(args):
     line = {
         "metric": "collected KV GB/s", "value": round(value, 2), "unit": "GB/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+        "scaling": "strong" if strong else "weak",
         "vs_baseline": None, "dtype": spec.dtype, "data": "synthetic",
         "config": {"workload": spec.name, "agents_per_gpu": n_local,
-                   "total_agents": world * n_local, "shared_blocks": spec.num_segments,
+                   "total_agents": total_agents, "sessions": spec.sessions,
+                   "sub_batches_per_gpu": len(batches), "shared_blocks": spec.num_segments,
                    "block_len": spec.seg_len, "layers": L, "kv_heads": H, "head_dim": D,
                    "tokens_per_agent": T, "parallelism": f"agent-shard x{world}",
                    "l2": "inputs larger than L2 (master arena "
@@ -363,9 +429,14 @@ def run_tdkv(args):
         "gpu_launches": launches,
         "clocks": sampler.summary(),
     }
+    if exchange is not None:
+        line["exchange"] = exchange
 
     # -- e2e: public API with host buffers ---------------------------------
-    if not args.no_e2e and not args.profile:
+    if len(batches) > 1 and not args.no_e2e:
+        line["e2e_note"] = ("e2e measured for single-sub-batch shards only (this shard is "
+                            f"collected in {len(batches)} pool sub-batches)")
+    if not args.no_e2e and not args.profile and len(batches) == 1:
         status = torch.empty(1, dtype=dt, device="cpu").pin_memory()
 
         # host metadata of the round: each agent's prompt layout (segment
@@ -424,7 +495,7 @@ def run_tdkv(args):
             p = pipe_step()
         barrier()                      # includes the last in-flight H2D
         wall = max_over_ranks(time.perf_counter() - t0) / args.steps
-        e2e_gbs = world * step_bytes / wall / 1e9
+        e2e_gbs = total_bytes / wall / 1e9
         # breakdown: the H2D alone (copy-stream events) and the host planning alone
         h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         h0.record(copy_stream)
@@ -443,7 +514,7 @@ def run_tdkv(args):
                        "ms_per_step": round(wall * 1e3, 3),
                        "h2d_ms": round(h2d_ms, 3), "plan_ms": round(plan_ms, 3),
                        "single_round_ms": round(single_wall * 1e3, 3),
-                       "agents_per_s": round(world * n_local / wall, 1),
+                       "agents_per_s": round(total_agents / wall, 1),
                        "path": "per step: KVCollector.plan_offsets (host layouts -> job "
                                "records against the device-resident slot maps; ~30 KB "
                                "uploaded) + RoundPipeline.step (the next round's pinned-host "

@@ -46,23 +46,24 @@ def broadcast_collect(collector, plan, src: int = 0, chunks: int = 7, group=None
     chunks (NCCL broadcasts queued back to back on the communicator's
     stream) and K1 runs on each chunk as soon as it has landed, so the
     NVLink transfer of chunk c+1 overlaps the HBM-bound collector on chunk
-    c.  Returns the kernels launched."""
+    c.  ``plan`` may be a list (a rank's pool sub-batches).  Returns the
+    kernels launched."""
     arena = collector.arena
     L = arena.num_layers
-    bounds = [round(i * L / chunks) for i in range(chunks + 1)]
+    plans = plan if isinstance(plan, (list, tuple)) else [plan]
     works = []
-    for l0, l1 in zip(bounds[:-1], bounds[1:]):
-        if l1 > l0:
-            wk = dist.broadcast(arena.k[l0:l1], src, group=group, async_op=True)
-            wv = dist.broadcast(arena.v[l0:l1], src, group=group, async_op=True)
-            works.append((l0, l1, wk, wv))
+    for l0, l1 in _layer_chunks(L, chunks):
+        wk = dist.broadcast(arena.k[l0:l1], src, group=group, async_op=True)
+        wv = dist.broadcast(arena.v[l0:l1], src, group=group, async_op=True)
+        works.append((l0, l1, wk, wv))
     pool = collector.pool
-    n = plan.launch_table()
+    n = sum(p.launch_table() for p in plans)
     for l0, l1, wk, wv in works:
         wk.wait()          # stream dependency for NCCL (host-blocking for gloo)
         wv.wait()
-        n += plan.launch_collect(arena, pool.k, pool.v, pool.layer_stride, layers=(l0, l1))
-    if ledger is not None and plan.num_jobs:
+        for p in plans:
+            n += p.launch_collect(arena, pool.k, pool.v, pool.layer_stride, layers=(l0, l1))
+    if ledger is not None and any(p.num_jobs for p in plans):
         for layer in range(L):
             ledger.record_rope_call(layer)
     return n
@@ -79,13 +80,27 @@ def session_transfers(owners, needs):
     return [(s, owners[s], r) for r, ss in enumerate(needs) for s in ss if owners[s] != r]
 
 
+class _StagedRecv:
+    """A gloo receive of a CUDA tensor: lands in host memory, copied to the
+    device on wait() (gloo point-to-point moves CPU tensors only; NCCL moves
+    device memory directly)."""
+
+    def __init__(self, work, host: torch.Tensor, dst: torch.Tensor) -> None:
+        self.work, self.host, self.dst = work, host, dst
+
+    def wait(self) -> None:
+        self.work.wait()
+        self.dst.copy_(self.host)
+
+
 def exchange_sessions(arena, session_rows, transfers, rank: int, layers=None, group=None):
     """Post the point-to-point transfers of ``layers`` (default: all) of the
-    sessions in ``transfers``; returns the requests (empty if this rank takes
-    no part).  One op per (layer, plane, transfer): a layer's session rows
-    are contiguous in the (L, rows, H, D) arena."""
+    sessions in ``transfers``; returns the requests to wait on (empty if this
+    rank takes no part).  One op per (layer, plane, transfer): a layer's
+    session rows are contiguous in the (L, rows, H, D) arena."""
     l0, l1 = layers or (0, arena.num_layers)
-    ops = []
+    staged = dist.get_backend(group) == "gloo" and arena.k.is_cuda
+    ops, fixups = [], []
     for s, src, dst in transfers:
         if rank not in (src, dst):
             continue
@@ -93,9 +108,19 @@ def exchange_sessions(arena, session_rows, transfers, rank: int, layers=None, gr
         for layer in range(l0, l1):
             for plane in (arena.k, arena.v):
                 t = plane[layer, r0:r1]
-                ops.append(dist.P2POp(dist.isend if rank == src else dist.irecv, t,
-                                      dst if rank == src else src, group=group))
-    return dist.batch_isend_irecv(ops) if ops else []
+                if rank == src:
+                    ops.append(dist.P2POp(dist.isend, t.cpu() if staged else t, dst, group=group))
+                else:
+                    buf = torch.empty(t.shape, dtype=t.dtype) if staged else t
+                    ops.append(dist.P2POp(dist.irecv, buf, src, group=group))
+                    if staged:
+                        fixups.append((len(ops) - 1, buf, t))
+    if not ops:
+        return []
+    reqs = list(dist.batch_isend_irecv(ops))
+    for i, buf, t in fixups:
+        reqs[i] = _StagedRecv(reqs[i], buf, t)
+    return reqs
 
 
 def exchange_collect(collector, plans, session_rows, transfers, rank: int, chunks: int = 4,

@@ -16,7 +16,8 @@ import torch.distributed as dist
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2604_03143_b200 as tk  # noqa: E402
 from paper_2604_03143_b200 import rounds  # noqa: E402
-from paper_2604_03143_b200.dist import broadcast_collect, elect_master, shard_range  # noqa: E402
+from paper_2604_03143_b200.dist import (broadcast_collect, elect_master, exchange_collect,  # noqa: E402
+                                        session_transfers, shard_range)
 
 
 def main():
@@ -59,10 +60,59 @@ def main():
     master = elect_master(scores, device=dev if backend == "nccl" else torch.device("cpu"))
     want = min(((float((a * 7919) % 13) / 4.0, a) for a in range(spec.num_agents)))[1]
     assert master == want, (master, want)
+    check_sessions(rank, world, dev)
     dist.barrier()
     if rank == 0:
         print(f"dist_check ok: world={world} backend={backend}")
     dist.destroy_process_group()
+
+
+def check_sessions(rank, world, dev):
+    """Strong-scaling multi-session round: each rank starts with only the
+    sessions it owns; exchange_collect moves the others point-to-point, layer
+    chunk by layer chunk, and collects two pool sub-batches."""
+    spec = rounds.CONFIGS["c3"].scaled(num_layers=3, num_agents=11, num_segments=2, seg_len=20,
+                                       hist_len=5, sessions=4)
+    mk, mv = rounds.master_planes_host(spec)
+    dt = spec.torch_dtype
+    k = torch.from_numpy(mk).to(dev).to(dt)
+    v = torch.from_numpy(mv).to(dev).to(dt)
+    truth = rounds.make_arena(spec, k.clone(), v.clone())
+    owners = rounds.session_owners(spec, world)
+    needs = rounds.session_needs(spec, world)
+    for s in range(spec.sessions):
+        if owners[s] != rank:
+            r0, r1 = spec.session_rows(s)
+            k[:, r0:r1] = 0
+            v[:, r0:r1] = 0
+    arena = rounds.make_arena(spec, k, v)
+    agents = list(rounds.shard(spec.num_agents, rank, world))
+    T = spec.tokens_per_agent
+    sb = max(1, (len(agents) + 1) // 2)
+    batches = [agents[i:i + sb] for i in range(0, len(agents), sb)]
+    pools, plans = [], []
+    for b in batches:
+        pool = tk.PagedPool(len(b) * T + 8, spec.num_layers, spec.num_heads, spec.head_dim,
+                            dtype=dt, device=dev)
+        maps = [pool.allocate(T, a) for a in b]
+        pools.append(pool)
+        plans.append([j for a, m in zip(b, maps) for j in rounds.agent_jobs(spec, a, m.slots)])
+    transfers = session_transfers(owners, needs)
+    rows = [spec.session_rows(s) for s in range(spec.sessions)]
+    for pool, jobs in zip(pools, plans):
+        col = tk.KVCollector(arena, pool)
+        exchange_collect(col, [col.plan(jobs)], rows, transfers, rank, chunks=2)
+    torch.cuda.synchronize(dev)
+    for s in needs[rank]:
+        r0, r1 = spec.session_rows(s)
+        assert torch.equal(arena.k[:, r0:r1], truth.k[:, r0:r1]), ("session", s)
+    for pool, jobs in zip(pools, plans):
+        ref_pool = tk.PagedPool(pool.capacity, spec.num_layers, spec.num_heads, spec.head_dim,
+                                dtype=dt, device=dev)
+        rc = tk.KVCollector(truth, ref_pool)
+        rc.collect(rc.plan(jobs))
+        torch.cuda.synchronize(dev)
+        assert torch.equal(pool.k, ref_pool.k) and torch.equal(pool.v, ref_pool.v), "sessions"
 
 
 if __name__ == "__main__":

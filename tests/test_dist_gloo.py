@@ -99,3 +99,87 @@ def test_shard_ranges_cover_agents():
         for world in (1, 2, 4, 8):
             got = [a for r in range(world) for a in shard_range(n, r, world)]
             assert got == list(range(n))
+
+
+class _LayeredArena(_Arena):
+    @property
+    def num_layers(self):
+        return self.k.shape[0]
+
+
+def _exchange_worker(rank, world, port, spec, results):
+    from paper_2604_03143_b200.dist import exchange_sessions, session_transfers
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        mk, mv = rounds.master_planes_host(spec)
+        owners = rounds.session_owners(spec, world)
+        needs = rounds.session_needs(spec, world)
+        k, v = torch.zeros(mk.shape), torch.zeros(mv.shape)
+        for s in range(spec.sessions):          # a rank starts with the masters it owns
+            if owners[s] == rank:
+                r0, r1 = spec.session_rows(s)
+                k[:, r0:r1] = torch.from_numpy(mk[:, r0:r1])
+                v[:, r0:r1] = torch.from_numpy(mv[:, r0:r1])
+        arena = _LayeredArena(k, v)
+        transfers = session_transfers(owners, needs)
+        rows = [spec.session_rows(s) for s in range(spec.sessions)]
+        dist.barrier()
+        # two layer chunks, as exchange_collect posts them
+        for chunk in ((0, 1), (1, spec.num_layers)):
+            for r in exchange_sessions(arena, rows, transfers, rank, chunk):
+                r.wait()
+        have = []
+        for s in range(spec.sessions):
+            r0, r1 = spec.session_rows(s)
+            have.append(bool(torch.equal(k[:, r0:r1], torch.from_numpy(mk[:, r0:r1]))
+                             and torch.equal(v[:, r0:r1], torch.from_numpy(mv[:, r0:r1]))))
+        agents = list(rounds.shard(spec.num_agents, rank, world))
+        shard = _oracle_shard(spec, agents, k.numpy(), v.numpy())
+        results[rank] = (agents, have, transfers,
+                         {a: (kk.sum(), vv.sum()) for a, (kk, vv) in shard.items()})
+    finally:
+        dist.destroy_process_group()
+
+
+def test_session_exchange_strong_shards():
+    """Multi-session round sharded by agent (strong scaling): every rank ends
+    with exactly the sessions its shard reads, and the shards' collector
+    outputs equal a single-process round."""
+    world = 3
+    spec = rounds.RoundSpec("gloo-sessions", 2, 2, 8, "f32", 11, 2, 5, 3, sessions=4, strong=True)
+    port = _free_port()
+    with mp.Manager() as manager:
+        results = manager.dict()
+        mp.spawn(_exchange_worker, args=(world, port, spec, results), nprocs=world, join=True)
+        results = dict(results)
+    needs = rounds.session_needs(spec, world)
+    owners = rounds.session_owners(spec, world)
+    assert results[0][2], "the test round must exercise at least one transfer"
+    for r in range(world):
+        agents, have, _, sums = results[r]
+        assert agents == list(rounds.shard(spec.num_agents, r, world))
+        for s in range(spec.sessions):
+            if s in needs[r] or owners[s] == r:
+                assert have[s], (r, s)
+            else:
+                assert not have[s], (r, s)      # nothing beyond what the shard reads
+    mk, mv = rounds.master_planes_host(spec)
+    whole = _oracle_shard(spec, list(range(spec.num_agents)), mk, mv)
+    for r in range(world):
+        for a, (ks, vs) in results[r][3].items():
+            assert ks == whole[a][0].sum() and vs == whole[a][1].sum()
+
+
+def test_session_owners_and_bytes():
+    spec = rounds.CONFIGS["c3"]
+    for world in (1, 2, 4, 8):
+        owners = rounds.session_owners(spec, world)
+        needs = rounds.session_needs(spec, world)
+        for s, o in enumerate(owners):
+            assert s in needs[o]
+        # contiguous shards: a rank reads at most one session beyond its share
+        assert max(len(n) for n in needs) <= -(-spec.sessions // world) + 1
+        total = sum(spec.collector_bytes_for(rounds.shard(spec.num_agents, r, world))
+                    for r in range(world))
+        assert total >= spec.collector_bytes()
