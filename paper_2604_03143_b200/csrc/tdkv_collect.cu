@@ -7,6 +7,8 @@
 // persistent loop) and then rotated/copied to every agent that holds the
 // segment, straight into that agent's paged-pool slots.  HBM traffic is the
 // algorithmic minimum M + N*M (master read once, N agent copies written).
+#include <cstdlib>
+
 #include "tdkv_common.cuh"
 
 namespace tdkv {
@@ -55,6 +57,7 @@ struct CollectParams {
     int32_t num_layers;
     int32_t head_dim;
     int32_t row_elems;
+    int32_t v_bulk;              // V rows leave by TMA bulk stores straight from the tile
 };
 
 // Per-job destination metadata is staged in shared memory in groups of
@@ -90,6 +93,10 @@ __global__ void __launch_bounds__(256) collect_kernel(const CollectParams p) {
     const int half = p.head_dim >> 1;
     const bool has_v = p.dv != nullptr;            // K-only collect (align_cached)
     const bool rotate = p.rotate != 0;
+    // V is position-free: with v_bulk its rows go from the staged tile to the
+    // agents' slots by TMA bulk stores (one per job when the job's slots are
+    // contiguous, else one per row) and the threads only handle K
+    const bool v_tma = BULK && has_v && p.v_bulk != 0;
 
     if constexpr (BULK) {
         if (tid == 0) {
@@ -199,6 +206,24 @@ __global__ void __launch_bounds__(256) collect_kernel(const CollectParams p) {
             }
             __syncthreads();
             const int ng = min(kJobGroup, u.job_end - u.job_begin - g * kJobGroup);
+            if constexpr (BULK) {
+                if (v_tma && tid < ng) {
+                    const int64_t* dr = &s_drow[mb][tid * kMaxTileRows];
+                    const int64_t r0 = dr[0];
+                    bool contig = true;
+                    for (int r = 1; r < u.nrows; ++r) contig &= dr[r] == r0 + r;
+                    const uint8_t* src = buf + tile_bytes;
+                    if (contig) {
+                        bulk_s2g(dv_l + (size_t)r0 * p.row_elems, src,
+                                 (uint32_t)(u.nrows * row_bytes));
+                    } else {
+                        for (int r = 0; r < u.nrows; ++r)
+                            bulk_s2g(dv_l + (size_t)dr[r] * p.row_elems, src + r * row_bytes,
+                                     (uint32_t)row_bytes);
+                    }
+                    bulk_commit();
+                }
+            }
             if (ty < rows_per_pass) {
                 for (int c = tx; c < upr; c += tx_n) {
                     const int j0 = ((c * kEpu) % p.head_dim) >> 1;
@@ -221,7 +246,7 @@ __global__ void __launch_bounds__(256) collect_kernel(const CollectParams p) {
                             }
                             st_stream(reinterpret_cast<V*>(dk_l + (size_t)drow * p.row_elems) + c,
                                       kv);
-                            if (has_v)
+                            if (has_v && !v_tma)
                                 st_stream(reinterpret_cast<V*>(dv_l + (size_t)drow * p.row_elems) + c,
                                           sv[r * upr + c]);
                         }
@@ -231,8 +256,13 @@ __global__ void __launch_bounds__(256) collect_kernel(const CollectParams p) {
                     }
                 }
             }
+            if (g + 1 == ngroups && v_tma && tid < kJobGroup)
+                bulk_wait_read<0>();    // the tile buffer is refilled next iteration
             __syncthreads();
         }
+    }
+    if constexpr (BULK) {
+        if (v_tma && tid < kJobGroup) bulk_wait<0>();
     }
 }
 
@@ -323,6 +353,10 @@ extern "C" int32_t tdkv_collect(const void* d_master_k, const void* d_master_v,
     p.num_layers = num_layers;
     p.head_dim = head_dim;
     p.row_elems = num_heads * head_dim;
+    static const bool v_bulk_env = [] {
+        const char* e = getenv("TDKV_COLLECT_V_BULK");
+        return !(e && e[0] == '0');
+    }();
 
     const size_t esz = elt_size(dtype);
     const size_t row_bytes = (size_t)p.row_elems * esz;
@@ -333,6 +367,7 @@ extern "C" int32_t tdkv_collect(const void* d_master_k, const void* d_master_v,
         ub = (int)(2 * esz);
     const bool bulk = row_bytes % 16 == 0 && aligned(d_master_k, 16) && aligned(d_master_v, 16) &&
                       (master_layer_stride * esz) % 16 == 0;
+    p.v_bulk = v_bulk_env && bulk && ub == 16 && d_dst_v != nullptr;
     if (!aligned(d_master_k, 4) || !aligned(d_master_v, 4))
         return set_error(TDKV_EINVAL, "tdkv_collect: master planes must be 4-byte aligned");
     cudaStream_t s = static_cast<cudaStream_t>(stream);

@@ -1,0 +1,128 @@
+// Direction-resolved HBM ceilings with hand-written 16-byte streaming kernels
+// (context for the rooflines; the reported denominator stays
+// MEASURED_PEAKS.json's copy figure).  Not part of the product.
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o gpurun_out/hbm_probe scripts/hbm_probe.cu
+//   gpurun_out/hbm_probe            -> one JSON line
+//
+// read:   every byte of an 8 GiB buffer loaded once (ld.global.cs, xor-reduced)
+// write:  8 GiB stored once (st.global.cs)
+// copy:   4 GiB -> 4 GiB
+// fanout: the collector's pattern -- a 224 MiB source read once, each 16-byte
+//         unit stored to 50 destinations (11.2 GiB written)
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { \
+    fprintf(stderr, "%s: %s\n", #x, cudaGetErrorString(e)); return 1; } } while (0)
+
+__global__ void read_k(const uint4* __restrict__ p, size_t n, uint4* sink) {
+    uint4 acc = make_uint4(0, 0, 0, 0);
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x) {
+        uint4 v = __ldcs(p + i);
+        acc.x ^= v.x; acc.y ^= v.y; acc.z ^= v.z; acc.w ^= v.w;
+    }
+    if ((acc.x & acc.y & acc.z & acc.w) == 0xFFFFFFFFu) sink[threadIdx.x] = acc;
+}
+
+__global__ void write_k(uint4* __restrict__ p, size_t n) {
+    const uint4 v = make_uint4(threadIdx.x, 1, 2, 3);
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x)
+        __stcs(p + i, v);
+}
+
+__global__ void write_wb_k(uint4* __restrict__ p, size_t n) {
+    const uint4 v = make_uint4(threadIdx.x, 1, 2, 3);
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
+// TMA bulk store: each CTA fills a 16 KiB smem tile once and streams it out
+// with cp.async.bulk.global.shared::cta in `chunk`-byte pieces
+__global__ void write_bulk_k(char* __restrict__ p, size_t nbytes, int chunk) {
+    __shared__ __align__(128) uint4 tile[1024];
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) tile[i] = make_uint4(i, 1, 2, 3);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    const size_t pieces = nbytes / chunk;
+    const unsigned saddr = (unsigned)__cvta_generic_to_shared(tile);
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < pieces;
+         i += (size_t)gridDim.x * blockDim.x) {
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                     :: "l"(p + i * chunk), "r"(saddr + (unsigned)((i * chunk) % 16384)), "r"(chunk)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 8;" ::: "memory");
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+__global__ void copy_k(const uint4* __restrict__ s, uint4* __restrict__ d, size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x)
+        __stcs(d + i, __ldcs(s + i));
+}
+
+__global__ void fanout_k(const uint4* __restrict__ s, uint4* __restrict__ d, size_t n, int fan) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x) {
+        const uint4 v = __ldcs(s + i);
+        for (int f = 0; f < fan; ++f) __stcs(d + (size_t)f * n + i, v);
+    }
+}
+
+template <typename F>
+static float best_ms(F launch, int reps = 10) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    launch();
+    cudaDeviceSynchronize();
+    float best = 1e30f;
+    for (int r = 0; r < reps; ++r) {
+        cudaEventRecord(a);
+        launch();
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        if (ms < best) best = ms;
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return best;
+}
+
+int main() {
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    const size_t big = 8ull << 30;
+    uint4 *x, *y, *sink;
+    CK(cudaMalloc(&x, big));
+    CK(cudaMalloc(&y, big));
+    CK(cudaMalloc(&sink, 4096));
+    CK(cudaMemset(x, 1, big));
+    const size_t n = big / 16;
+    const dim3 grid(sms * 8), block(256);
+    const float r = best_ms([&] { read_k<<<grid, block>>>(x, n, sink); });
+    const float w = best_ms([&] { write_k<<<grid, block>>>(y, n); });
+    const float c = best_ms([&] { copy_k<<<grid, block>>>(x, y, n / 2); });
+    const float wb = best_ms([&] { write_wb_k<<<grid, block>>>(y, n); });
+    const float b1 = best_ms([&] { write_bulk_k<<<sms * 2, 32>>>((char*)y, big, 1024); });
+    const float b4 = best_ms([&] { write_bulk_k<<<sms * 2, 32>>>((char*)y, big, 4096); });
+    const size_t src = 224ull << 20;
+    const int fan = 50;
+    const float f = best_ms([&] { fanout_k<<<grid, block>>>(x, y, src / 16, fan); }, 5);
+    CK(cudaGetLastError());
+    printf("{\"read_gbs\": %.1f, \"write_gbs\": %.1f, \"copy_gbs\": %.1f, "
+           "\"write_default_gbs\": %.1f, \"write_bulk1k_gbs\": %.1f, \"write_bulk4k_gbs\": %.1f, "
+           "\"fanout50_gbs\": %.1f, \"fanout50_bytes\": %zu, \"bytes\": %zu, \"sms\": %d}\n",
+           big / (r * 1e-3) / 1e9, big / (w * 1e-3) / 1e9, big / (c * 1e-3) / 1e9,
+           big / (wb * 1e-3) / 1e9, big / (b1 * 1e-3) / 1e9, big / (b4 * 1e-3) / 1e9,
+           (src * (fan + 1)) / (f * 1e-3) / 1e9, src * (fan + 1), big, sms);
+    return 0;
+}
