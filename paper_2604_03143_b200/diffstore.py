@@ -93,16 +93,47 @@ class _DeviceDiff:
     map_v: torch.Tensor
 
 
-@dataclass
 class _EncodedSlab:
     """Encoder output kept in its device layout: layer l's changed blocks are
-    slab rows [l*cap, l*cap + counts[l]) with block ids idx[l*cap:...]."""
+    slab rows [l*cap, l*cap + counts[l]) with block ids idx[l*cap:...].  The
+    mirror's views of the family tensors are cut on first use (an encode of
+    a 49-mirror family then builds no tensor views on the host)."""
 
-    counts: np.ndarray           # (L,) int
-    idx: np.ndarray              # (L*cap,) int32, host copy
-    cap: int
-    pay_k: torch.Tensor          # (L*cap, bs, H, D)
-    pay_v: torch.Tensor
+    __slots__ = ("counts", "idx", "cap", "_fam", "_row0", "_map", "_map_n", "_views")
+
+    def __init__(self, counts, idx, cap, fam_k, fam_v, row0, fam_map, map0, map_n):
+        self.counts = counts         # (L,) int
+        self.idx = idx               # (L*cap,) int32, host copy
+        self.cap = cap
+        self._fam = (fam_k, fam_v, fam_map)
+        self._row0 = row0
+        self._map = map0
+        self._map_n = map_n
+        self._views = None
+
+    def _cut(self):
+        if self._views is None:
+            fk, fv, fm = self._fam
+            r0, n = self._row0, self.cap * len(self.counts)
+            mp = fm[self._map:self._map + self._map_n]
+            self._views = (fk[r0:r0 + n], fv[r0:r0 + n], mp)
+        return self._views
+
+    @property
+    def pay_k(self) -> torch.Tensor:    # (L*cap, bs, H, D)
+        return self._cut()[0]
+
+    @property
+    def pay_v(self) -> torch.Tensor:
+        return self._cut()[1]
+
+    @property
+    def elt_size(self) -> int:
+        return self._fam[0].element_size()
+
+    def device_diff(self) -> _DeviceDiff:
+        k, v, mp = self._cut()
+        return _DeviceDiff(k, v, mp, mp)
 
 
 class BlockSparseDiff:
@@ -139,7 +170,8 @@ class BlockSparseDiff:
 
     @classmethod
     def _from_slab(cls, num_layers: int, block_size: int, num_heads: int, head_dim: int,
-                   total_tokens: int, slab: _EncodedSlab, dev: _DeviceDiff) -> "BlockSparseDiff":
+                   total_tokens: int, slab: _EncodedSlab,
+                   dev: Optional[_DeviceDiff] = None) -> "BlockSparseDiff":
         self = cls.__new__(cls)
         self.num_layers = num_layers
         self.block_size = block_size
@@ -167,12 +199,14 @@ class BlockSparseDiff:
     @layers.setter
     def layers(self, value: List[LayerDiff]) -> None:
         self._layers = list(value)
+        self._slab = None            # the encoder's device form no longer describes it
+        self._dev = None
 
     @property
     def payload_nbytes(self) -> int:
         if self._layers is None:
             s = self._slab
-            blk = self.block_size * self.num_heads * self.head_dim * s.pay_k.element_size()
+            blk = self.block_size * self.num_heads * self.head_dim * s.elt_size
             return int(2 * blk * int(s.counts.sum()))
         return sum(ld.payload_nbytes for ld in self._layers)
 
@@ -201,6 +235,8 @@ class BlockSparseDiff:
 
     def device_form(self, device: torch.device, dtype: torch.dtype) -> _DeviceDiff:
         """Payload slabs + block maps on the device (uploaded once for host diffs)."""
+        if self._dev is None and self._slab is not None:
+            self._dev = self._slab.device_diff()
         d = self._dev
         if d is not None and d.pay_k.device == device and d.pay_k.dtype == dtype:
             return d
@@ -244,8 +280,8 @@ def _plane_dtype(kv: LayeredKv) -> torch.dtype:
 def encode_launch(master: LayeredKv, mirrors: Sequence[LayeredKv],
                   hint_positions: Sequence[np.ndarray], blocks: CacheBlockConfig,
                   device: Optional[torch.device] = None) -> "_EncodeState":
-    """Validate, upload the descriptors and launch K2 (compare + compact) for
-    a family without reading anything back; ``encode_finish`` completes it."""
+    """Validate, upload the descriptors and launch K2 for a family without
+    reading anything back; ``encode_finish`` completes it."""
     if len(mirrors) != len(hint_positions) or not mirrors:
         raise ValueError("one hint array per mirror, at least one mirror")
     total = master.num_tokens
@@ -254,24 +290,25 @@ def encode_launch(master: LayeredKv, mirrors: Sequence[LayeredKv],
     L, H, D = master.num_layers, master.num_heads, master.head_dim
     hinted = np.zeros((len(mirrors), nb), np.uint8)
     shape = tuple(master.k.shape)
-    for mir in mirrors:
-        if tuple(mir.k.shape) != shape:
-            raise ValueError("master and mirror must have identical plane shapes")
-        if mir.positions is not master.positions and not np.array_equal(master.positions,
-                                                                         mir.positions):
-            raise ValueError("master and mirror must cover the same positions")
+    if any(tuple(mir.k.shape) != shape for mir in mirrors):
+        raise ValueError("master and mirror must have identical plane shapes")
+    others = [mir.positions for mir in mirrors if mir.positions is not master.positions]
+    if others and not (np.stack(others) == master.positions).all():   # one vectorized compare
+        raise ValueError("master and mirror must cover the same positions")
     # every mirror's hint positions -> its hinted-block row (a 1-D scatter per
     # mirror is ~4x faster than one 2-D fancy-index scatter over the family)
-    shift = bs.bit_length() - 1 if bs & (bs - 1) == 0 else -1
-    for p, h in enumerate(hint_positions):
-        h = np.asarray(h).reshape(-1)
-        if not h.size:
-            continue
-        if not np.issubdtype(h.dtype, np.integer):
-            h = h.astype(np.int64)
-        if h.min() < 0 or h.max() >= total:
+    hs = [np.asarray(h).reshape(-1) for h in hint_positions]
+    hs = [h if np.issubdtype(h.dtype, np.integer) else h.astype(np.int64) for h in hs]
+    sizes = [h.size for h in hs]
+    if any(sizes):
+        cat = np.concatenate([h for h in hs if h.size])
+        if cat.min() < 0 or cat.max() >= total:
             raise ValueError("hint positions out of range")
-        hinted[p, (h >> shift) if shift >= 0 else (h // bs)] = 1
+        blk = (cat >> (bs.bit_length() - 1)) if bs & (bs - 1) == 0 else cat // bs
+        offs = np.cumsum([0] + sizes)
+        for p in range(len(hs)):
+            if sizes[p]:
+                hinted[p, blk[offs[p]:offs[p + 1]]] = 1
     device = device or (master.k.device if master.on_device else default_device())
     dtype = _plane_dtype(master)
     mk = to_device(master.k, device, dtype)
@@ -381,11 +418,9 @@ def encode_finish(st: "_EncodeState") -> List[BlockSparseDiff]:
     diffs = []
     for p in range(P):
         s, cap = int(starts[p]), int(caps[p])
-        slab = _EncodedSlab(counts_h[p], idx_h[s:s + L * cap], cap, pay_k[s:s + L * cap],
-                            pay_v[s:s + L * cap])
-        mp = blkmap[p * L * nb:(p + 1) * L * nb]
-        diffs.append(BlockSparseDiff._from_slab(L, bs, H, D, total, slab,
-                                                _DeviceDiff(slab.pay_k, slab.pay_v, mp, mp)))
+        slab = _EncodedSlab(counts_h[p], idx_h[s:s + L * cap], cap, pay_k, pay_v, s,
+                            blkmap, p * L * nb, L * nb)
+        diffs.append(BlockSparseDiff._from_slab(L, bs, H, D, total, slab))
     return diffs
 
 

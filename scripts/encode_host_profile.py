@@ -1,0 +1,38 @@
+"""cProfile of the encoder's host side (encode_launch + encode_finish) at the
+C2 codec-bench shape: 49 mirrors, 10% changed blocks (diagnostic)."""
+import cProfile
+import pstats
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+import paper_2604_03143_b200 as tk  # noqa: E402
+from paper_2604_03143_b200 import diffstore as ds  # noqa: E402
+
+L, T, H, D, bs, P = 28, 4624, 4, 128, 32, 49
+dev = torch.device("cuda:0")
+g = torch.Generator(device=dev).manual_seed(0)
+mk = torch.randn(L, T, H, D, generator=g, device=dev).bfloat16()
+mv = torch.randn(L, T, H, D, generator=g, device=dev).bfloat16()
+master = tk.LayeredKv(mk, mv, np.arange(T))
+nb = -(-T // bs)
+rng = np.random.default_rng(1)
+mirrors, hints = [], []
+for _ in range(P):
+    blocks = np.sort(rng.choice(nb, nb // 10, replace=False))
+    mirrors.append(tk.LayeredKv(mk.clone(), mv.clone(), np.arange(T)))
+    hints.append(np.concatenate([np.arange(b * bs, min(T, b * bs + bs)) for b in blocks]))
+cfg = tk.CacheBlockConfig(bs)
+for _ in range(3):
+    ds.encode_batch(master, mirrors, hints, cfg)
+torch.cuda.synchronize()
+pr = cProfile.Profile()
+pr.enable()
+for _ in range(20):
+    st = ds.encode_launch(master, mirrors, hints, cfg)
+    torch.cuda.synchronize()
+    d = ds.encode_finish(st)
+pr.disable()
+pstats.Stats(pr).sort_stats("tottime").print_stats(18)
