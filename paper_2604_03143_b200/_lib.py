@@ -130,9 +130,11 @@ _lib: Optional[ctypes.CDLL] = None
 _lock = threading.Lock()
 
 
-def load(path: str = LIB_PATH) -> ctypes.CDLL:
-    """Load libtdkv.so (once).  Raises TdkvUnavailable when it is missing."""
+def load(path: Optional[str] = None) -> ctypes.CDLL:
+    """Load libtdkv.so (once; ``TDKV_LIBRARY`` overrides the in-tree path for
+    A/B builds).  Raises TdkvUnavailable when it is missing."""
     global _lib
+    path = path or os.environ.get("TDKV_LIBRARY") or LIB_PATH
     if _lib is not None:
         return _lib
     with _lock:

@@ -1,0 +1,50 @@
+"""A/B timing of the fused restore (K0 + K3) at the C2 codec-bench shape:
+run once per library build (TDKV_LIBRARY=...), prints median GB/s of 15
+repetitions of a 49-mirror family restore (diagnostic)."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+import paper_2604_03143_b200 as tk  # noqa: E402
+
+L, T, H, D, bs, P = 28, 4624, 4, 128, 32, 49
+dev = torch.device("cuda:0")
+g = torch.Generator(device=dev).manual_seed(0)
+mk = torch.randn(L, T, H, D, generator=g, device=dev).bfloat16()
+mv = torch.randn(L, T, H, D, generator=g, device=dev).bfloat16()
+master = tk.LayeredKv(mk, mv, np.arange(T))
+nb = -(-T // bs)
+rng = np.random.default_rng(1)
+mirrors, hints = [], []
+for _ in range(P):
+    blocks = np.sort(rng.choice(nb, nb // 10, replace=False))
+    k, v = mk.clone(), mv.clone()
+    for b in blocks:
+        k[:, b * bs:(b + 1) * bs] += 1
+    mirrors.append(tk.LayeredKv(k, v, np.arange(T)))
+    hints.append(np.concatenate([np.arange(b * bs, min(T, b * bs + bs)) for b in blocks]))
+del k, v
+diffs = tk.encode_batch(master, mirrors, hints, tk.CacheBlockConfig(bs))
+del mirrors
+pool = tk.PagedPool(P * T + 64, L, H, D, dtype=torch.bfloat16, device=dev, debug=False)
+maps = [pool.allocate(T, i) for i in range(P)]
+fam = tk.MasterEntry(0, master, pin_count=P)
+handles = [tk.MirrorHandle(0, i + 1, fam, d) for i, d in enumerate(diffs)]
+spans = [tk.PositionSpan.shifted(np.arange(T), 16) for _ in handles]
+for _ in range(3):
+    tk.fused_restore_many(handles, spans, pool, maps, 10000.0)
+torch.cuda.synchronize()
+res = []
+for _ in range(15):
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    tk.fused_restore_many(handles, spans, pool, maps, 10000.0)
+    b.record()
+    torch.cuda.synchronize()
+    res.append(a.elapsed_time(b) * 1e-3)
+dense = 2 * L * T * H * D * 2
+print(os.environ.get("TDKV_LIBRARY", "in-tree"), "fused restore GB/s median",
+      round(P * 2 * dense / np.median(res) / 1e9, 1), "best", round(P * 2 * dense / min(res) / 1e9, 1))
