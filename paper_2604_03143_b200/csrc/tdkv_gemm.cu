@@ -459,6 +459,170 @@ __global__ void __launch_bounds__(192, 1)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Persistent bf16 variant: one CTA per SM walks the output tiles
+// (t = blockIdx.x, blockIdx.x + gridDim.x, ...; m-blocks fastest so the
+// CTAs in flight share B tiles in L2).  Three pipelines: the smem ring
+// (TMA producer <-> MMA issuer, continuous across tiles), and a
+// double-buffered TMEM accumulator (2 x BN columns) between the MMA issuer
+// and the four epilogue warps, so tile i's epilogue (tcgen05.ld -> float4
+// stores) overlaps tile i+1's main loop.
+
+__device__ __forceinline__ void tmem_ld32(uint32_t addr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+        "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+        "%28, %29, %30, %31}, [%32];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+          "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+          "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(addr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+template <int BN, int kStages>
+__global__ void __launch_bounds__(192, 1)
+    gemm_persistent_kernel(const __grid_constant__ CUtensorMap map_a,
+                           const __grid_constant__ CUtensorMap map_b, float* __restrict__ C,
+                           int ldc, int M, int N, int K, int accumulate_c) {
+    constexpr int kBK = 64;                                 // one 128-byte bf16 atom of K
+    constexpr int kABytes = kGemmBM * 128;
+    constexpr int kBBytes = BN * 128;
+    constexpr int kStageBytes = kABytes + kBBytes;
+    constexpr uint32_t kTmemCols = 2 * BN;                  // two accumulators
+
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ __align__(8) uint64_t full[kStages], empty[kStages], tfull[2], tempty[2];
+    __shared__ uint32_t s_tmem;
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int nk = (K + kBK - 1) / kBK;
+    const int tiles_m = (M + kGemmBM - 1) / kGemmBM;
+    const int n_tiles = tiles_m * ((N + BN - 1) / BN);
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(&s_tmem)),
+                     "n"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) {
+        for (int i = 0; i < kStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 4);                       // one arrive per epilogue warp
+        }
+        fence_mbar_init();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = s_tmem;
+
+    if (warp == 0) {
+        if (lane == 0) {                                     // ---- TMA producer
+            int g = 0;
+            for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+                const int m0 = (t % tiles_m) * kGemmBM, n0 = (t / tiles_m) * BN;
+                for (int kb = 0; kb < nk; ++kb, ++g) {
+                    const int st = g % kStages;
+                    if (g >= kStages) mbar_wait(&empty[st], (uint32_t)((g / kStages - 1) & 1));
+                    uint8_t* a = smem + st * kStageBytes;
+                    mbar_arrive_expect_tx(&full[st], kStageBytes);
+                    tma_load_2d(a, &map_a, &full[st], kb * kBK, m0);
+                    tma_load_2d(a + kABytes, &map_b, &full[st], kb * kBK, n0);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {                                     // ---- MMA issuer
+            const uint32_t idesc = umma_idesc(1, kGemmBM, BN);
+            int g = 0, i = 0;
+            for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+                const int acc = i & 1;
+                if (i >= 2) mbar_wait(&tempty[acc], (uint32_t)((i / 2 - 1) & 1));
+                tc_fence_after();
+                const uint32_t d = tmem + (uint32_t)(acc * BN);
+                for (int kb = 0; kb < nk; ++kb, ++g) {
+                    const int st = g % kStages;
+                    mbar_wait(&full[st], (uint32_t)((g / kStages) & 1));
+                    tc_fence_after();
+                    const uint32_t a = smem_u32(smem + st * kStageBytes);
+#pragma unroll
+                    for (int s = 0; s < 4; ++s)
+                        umma<false>(d, umma_desc_sw128(a + 32 * s),
+                                    umma_desc_sw128(a + kABytes + 32 * s), idesc,
+                                    (kb > 0 || s > 0) ? 1u : 0u);
+                    umma_commit(&empty[st]);                 // frees the stage when done
+                }
+                umma_commit(&tfull[acc]);                    // accumulator ready
+            }
+        }
+    } else {                                                 // ---- epilogue warps 2-5
+        const int q = warp & 3;                              // TMEM lane quarter
+        int i = 0;
+        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+            const int acc = i & 1;
+            const int m0 = (t % tiles_m) * kGemmBM, n0 = (t / tiles_m) * BN;
+            mbar_wait(&tfull[acc], (uint32_t)((i / 2) & 1));
+            tc_fence_after();
+            const int row = m0 + q * 32 + lane;
+            const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
+            float* crow = C + (size_t)row * ldc;
+            const bool vec = (ldc & 3) == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0;
+#pragma unroll 1
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+                uint32_t r[32];
+                tmem_ld32(taddr + c0, r);
+                if (row >= M) continue;
+                const int col0 = n0 + c0;
+                if (vec && col0 + 32 <= N) {
+                    float4* dst = reinterpret_cast<float4*>(crow + col0);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        float4 v = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                               __uint_as_float(r[4 * j + 2]),
+                                               __uint_as_float(r[4 * j + 3]));
+                        if (accumulate_c) {
+                            const float4 o = dst[j];
+                            v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+                        }
+                        dst[j] = v;
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int col = col0 + j;
+                        if (col < N) {
+                            const float v = __uint_as_float(r[j]);
+                            crow[col] = accumulate_c ? crow[col] + v : v;
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);        // accumulator drained
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "n"(kTmemCols)
+                     : "memory");
+    }
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     if (!fn) {
@@ -508,6 +672,25 @@ static int32_t launch_gemm_tma(const void* A, int lda, const void* B, int ldb, f
     return TDKV_OK;
 }
 
+template <int BN, int kStages>
+static int32_t launch_gemm_persistent(const void* A, int lda, const void* B, int ldb, float* C,
+                                      int ldc, int M, int N, int K, int accumulate,
+                                      cudaStream_t s, bool* ok) {
+    CUtensorMap ma, mb;
+    *ok = make_map(&ma, A, TDKV_BF16, M, K, lda, kGemmBM) &&
+          make_map(&mb, B, TDKV_BF16, N, K, ldb, BN);
+    if (!*ok) return TDKV_OK;
+    auto kern = gemm_persistent_kernel<BN, kStages>;
+    const size_t smem = (size_t)kStages * (kGemmBM + BN) * 128 + 1024;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return check_launch("tdkv_gemm: cudaFuncSetAttribute");
+    const long long tiles = (long long)((M + kGemmBM - 1) / kGemmBM) * ((N + BN - 1) / BN);
+    const int grid = (int)(tiles < sm_count() ? tiles : sm_count());
+    kern<<<grid, 192, smem, s>>>(ma, mb, C, ldc, M, N, K, accumulate);
+    return TDKV_OK;
+}
+
 }  // namespace tdkv
 
 using namespace tdkv;
@@ -533,6 +716,13 @@ extern "C" int32_t tdkv_gemm(const void* d_a, int32_t lda, const void* d_b, int3
                                                           accumulate, dtype, s, &tma)
                          : launch_gemm_tma<float, 128, 3>(d_a, lda, d_b, ldb, d_c, ldc, m, n, k,
                                                            accumulate, dtype, s, &tma);
+        } else if (n > 64 && !getenv("TDKV_GEMM_NO_PERSISTENT")) {
+            const long long tiles256 = (long long)((m + 127) / 128) * ((n + 255) / 256);
+            rc = (n >= 256 && tiles256 >= sm_count())
+                     ? launch_gemm_persistent<256, 4>(d_a, lda, d_b, ldb, d_c, ldc, m, n, k,
+                                                      accumulate, s, &tma)
+                     : launch_gemm_persistent<128, 6>(d_a, lda, d_b, ldb, d_c, ldc, m, n, k,
+                                                      accumulate, s, &tma);
         } else {
             const long long tiles256 = (long long)((m + 127) / 128) * ((n + 255) / 256);
             if (n <= 64)

@@ -40,3 +40,26 @@ def test_gemm_bf16(M, N, K):
     out = gemm.gemm_tn(a, b)
     want = a.double() @ b.double().T
     assert (out.double() - want).abs().max().item() <= 1e-3 * max(1.0, want.abs().max().item())
+
+
+@pytest.mark.parametrize("M,N,K", [(300, 512, 512), (2048, 4608, 256), (130, 300, 72),
+                                   (129, 257, 1000), (4096, 4096, 128)])
+def test_gemm_bf16_persistent(M, N, K):
+    """Shapes that put several output tiles on one persistent CTA (both TMEM
+    accumulator buffers in use), ragged M/N/K edges and the scalar tail."""
+    g = torch.Generator(device=DEV).manual_seed(M + N + K)
+    a = torch.randn(M, K, generator=g, device=DEV).bfloat16()
+    b = torch.randn(N, K, generator=g, device=DEV).bfloat16()
+    out = gemm.gemm_tn(a, b)
+    want = a.double() @ b.double().T
+    assert (out.double() - want).abs().max().item() <= 1e-5 * max(1.0, want.abs().max().item()) * K ** 0.5
+
+
+def test_gemm_bf16_persistent_accumulate():
+    g = torch.Generator(device=DEV).manual_seed(11)
+    a = torch.randn(1000, 192, generator=g, device=DEV).bfloat16()
+    b = torch.randn(1000, 192, generator=g, device=DEV).bfloat16()
+    c = torch.randn(1000, 1000, generator=g, device=DEV)
+    want = c.double() + a.double() @ b.double().T
+    gemm.gemm_tn(a, b, out=c, accumulate=True)
+    assert (c.double() - want).abs().max().item() <= 1e-5 * want.abs().max().item() * 192 ** 0.5
