@@ -623,6 +623,207 @@ __global__ void __launch_bounds__(192, 1)
     }
 }
 
+// ---------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2): a cluster of two CTAs on one TPC computes
+// a 256 x BN tile.  Each CTA stages its own 128 rows of A and its half of B
+// (BN/2 rows) -- 2/3 of the single-CTA operand traffic per flop -- and the
+// leader CTA's one elected thread issues M=256 MMAs that read both CTAs'
+// shared memory and write each CTA's TMEM.  Both producers signal the
+// leader's full barrier; the leader's commits multicast to both CTAs' empty
+// and TMEM-full barriers; both CTAs' epilogue warps release the accumulator
+// on the leader's TMEM-empty barrier.
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of ``p`` (a local smem address) in CTA ``rank``
+__device__ __forceinline__ uint32_t map_to_rank(const void* p, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const CUtensorMap* map,
+                                                 uint32_t leader_bar, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(x), "r"(y)
+        : "memory");
+}
+__device__ __forceinline__ void umma_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+        "[%0], %1;" ::"r"(smem_u32(bar)),
+        "h"((uint16_t)0x3)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+                 : "memory");
+}
+
+template <int BN, int kStages>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+    gemm_pair_kernel(const __grid_constant__ CUtensorMap map_a,
+                     const __grid_constant__ CUtensorMap map_b, float* __restrict__ C, int ldc,
+                     int M, int N, int K, int accumulate_c) {
+    constexpr int kBK = 64;
+    constexpr int kABytes = kGemmBM * 128;                  // this CTA's 128 rows of A
+    constexpr int kBBytes = (BN / 2) * 128;                 // this CTA's half of B
+    constexpr int kStageBytes = kABytes + kBBytes;
+    constexpr uint32_t kTmemCols = 2 * BN;
+
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ __align__(8) uint64_t full[kStages], empty[kStages], tfull[2], tempty[2];
+    __shared__ uint32_t s_tmem;
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+    const int nk = (K + kBK - 1) / kBK;
+    const int tiles_m = (M + 2 * kGemmBM - 1) / (2 * kGemmBM);
+    const int n_tiles = tiles_m * ((N + BN - 1) / BN);
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(&s_tmem)),
+                     "n"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) {
+        for (int i = 0; i < kStages; ++i) {
+            mbar_init(&full[i], 1);                         // the leader producer's arrive
+            mbar_init(&empty[i], 1);                        // the leader's multicast commit
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 8);                       // 4 epilogue warps x 2 CTAs
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    tc_fence_before();
+    cluster_sync_all();                                      // peer barriers initialized
+    tc_fence_after();
+    const uint32_t tmem = s_tmem;
+
+    if (warp == 0) {
+        if (lane == 0) {                                     // ---- TMA producer (both CTAs)
+            int g = 0;
+            for (int t = pair; t < n_tiles; t += n_pairs) {
+                const int m0 = (t % tiles_m) * 2 * kGemmBM + (int)rank * kGemmBM;
+                const int n0 = (t / tiles_m) * BN + (int)rank * (BN / 2);
+                for (int kb = 0; kb < nk; ++kb, ++g) {
+                    const int st = g % kStages;
+                    if (g >= kStages) mbar_wait(&empty[st], (uint32_t)((g / kStages - 1) & 1));
+                    if (leader) mbar_arrive_expect_tx(&full[st], 2 * kStageBytes);
+                    const uint32_t bar = map_to_rank(&full[st], 0);
+                    uint8_t* a = smem + st * kStageBytes;
+                    tma_load_2d_pair(a, &map_a, bar, kb * kBK, m0);
+                    tma_load_2d_pair(a + kABytes, &map_b, bar, kb * kBK, n0);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader && lane == 0) {                           // ---- MMA issuer (leader)
+            const uint32_t idesc = umma_idesc(1, 2 * kGemmBM, BN);
+            int g = 0, i = 0;
+            for (int t = pair; t < n_tiles; t += n_pairs, ++i) {
+                const int acc = i & 1;
+                if (i >= 2) mbar_wait(&tempty[acc], (uint32_t)((i / 2 - 1) & 1));
+                tc_fence_after();
+                const uint32_t d = tmem + (uint32_t)(acc * BN);
+                for (int kb = 0; kb < nk; ++kb, ++g) {
+                    const int st = g % kStages;
+                    mbar_wait(&full[st], (uint32_t)((g / kStages) & 1));
+                    tc_fence_after();
+                    const uint32_t a = smem_u32(smem + st * kStageBytes);
+#pragma unroll
+                    for (int s = 0; s < 4; ++s)
+                        umma_pair(d, umma_desc_sw128(a + 32 * s),
+                                  umma_desc_sw128(a + kABytes + 32 * s), idesc,
+                                  (kb > 0 || s > 0) ? 1u : 0u);
+                    umma_commit_pair(&empty[st]);            // frees the stage in both CTAs
+                }
+                umma_commit_pair(&tfull[acc]);               // both CTAs' accumulators ready
+            }
+        }
+    } else {                                                 // ---- epilogue warps 2-5
+        const int q = warp & 3;
+        const uint32_t tempty_leader0 = map_to_rank(&tempty[0], 0);
+        const uint32_t tempty_leader1 = map_to_rank(&tempty[1], 0);
+        int i = 0;
+        for (int t = pair; t < n_tiles; t += n_pairs, ++i) {
+            const int acc = i & 1;
+            const int m0 = (t % tiles_m) * 2 * kGemmBM + (int)rank * kGemmBM;
+            const int n0 = (t / tiles_m) * BN;
+            mbar_wait(&tfull[acc], (uint32_t)((i / 2) & 1));
+            tc_fence_after();
+            const int row = m0 + q * 32 + lane;
+            const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
+            float* crow = C + (size_t)row * ldc;
+            const bool vec = (ldc & 3) == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0;
+#pragma unroll 1
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+                uint32_t r[32];
+                tmem_ld32(taddr + c0, r);
+                if (row >= M) continue;
+                const int col0 = n0 + c0;
+                if (vec && col0 + 32 <= N) {
+                    float4* dst = reinterpret_cast<float4*>(crow + col0);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        float4 v = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                               __uint_as_float(r[4 * j + 2]),
+                                               __uint_as_float(r[4 * j + 3]));
+                        if (accumulate_c) {
+                            const float4 o = dst[j];
+                            v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+                        }
+                        dst[j] = v;
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int col = col0 + j;
+                        if (col < N) {
+                            const float v = __uint_as_float(r[j]);
+                            crow[col] = accumulate_c ? crow[col] + v : v;
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(acc ? tempty_leader1 : tempty_leader0);
+        }
+    }
+    tc_fence_before();
+    cluster_sync_all();                                      // both CTAs done with TMEM
+    if (warp == 0) {
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "n"(kTmemCols)
+                     : "memory");
+    }
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     if (!fn) {
@@ -691,6 +892,24 @@ static int32_t launch_gemm_persistent(const void* A, int lda, const void* B, int
     return TDKV_OK;
 }
 
+template <int BN, int kStages>
+static int32_t launch_gemm_pair(const void* A, int lda, const void* B, int ldb, float* C, int ldc,
+                                int M, int N, int K, int accumulate, cudaStream_t s, bool* ok) {
+    CUtensorMap ma, mb;
+    *ok = make_map(&ma, A, TDKV_BF16, M, K, lda, kGemmBM) &&
+          make_map(&mb, B, TDKV_BF16, N, K, ldb, BN / 2);
+    if (!*ok) return TDKV_OK;
+    auto kern = gemm_pair_kernel<BN, kStages>;
+    const size_t smem = (size_t)kStages * (kGemmBM + BN / 2) * 128 + 1024;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return check_launch("tdkv_gemm: cudaFuncSetAttribute");
+    const long long tiles = (long long)((M + 255) / 256) * ((N + BN - 1) / BN);
+    const int pairs = (int)(tiles < sm_count() / 2 ? tiles : sm_count() / 2);
+    kern<<<2 * pairs, 192, smem, s>>>(ma, mb, C, ldc, M, N, K, accumulate);
+    return TDKV_OK;
+}
+
 }  // namespace tdkv
 
 using namespace tdkv;
@@ -716,6 +935,11 @@ extern "C" int32_t tdkv_gemm(const void* d_a, int32_t lda, const void* d_b, int3
                                                           accumulate, dtype, s, &tma)
                          : launch_gemm_tma<float, 128, 3>(d_a, lda, d_b, ldb, d_c, ldc, m, n, k,
                                                            accumulate, dtype, s, &tma);
+        } else if (n >= 256 && m > 128 && !getenv("TDKV_GEMM_NO_PAIR") &&
+                   (long long)((m + 255) / 256) * ((n + 255) / 256) >= sm_count() / 2) {
+            // enough 256 x 256 tiles to give every CTA pair work: cta_group::2
+            rc = launch_gemm_pair<256, 6>(d_a, lda, d_b, ldb, d_c, ldc, m, n, k, accumulate, s,
+                                          &tma);
         } else if (n > 64 && !getenv("TDKV_GEMM_NO_PERSISTENT")) {
             const long long tiles256 = (long long)((m + 127) / 128) * ((n + 255) / 256);
             rc = (n >= 256 && tiles256 >= sm_count())

@@ -1,8 +1,8 @@
 """tdkv_gemm variants vs cuBLAS (torch.matmul) on a few shapes (diagnostic).
 
-Prints TFLOP/s for: persistent TMEM-double-buffered kernel (default), the
-non-persistent TMA kernel (TDKV_GEMM_NO_PERSISTENT=1), and torch bf16 matmul
-with float32 output semantics (bf16 in, fp32 out via out_dtype)."""
+Prints TFLOP/s for: the CTA-pair kernel (default for large shapes), the
+single-CTA persistent kernel (TDKV_GEMM_NO_PAIR=1), the non-persistent TMA
+kernel (+ TDKV_GEMM_NO_PERSISTENT=1), and cuBLAS via torch.matmul (bf16 out)."""
 import os
 import sys
 
@@ -30,14 +30,15 @@ for M, N, K in [(2048, 4608, 3584), (2048, 3584, 3584), (4096, 4096, 4096), (819
     c = torch.empty(M, N, device="cuda")
     fl = 2.0 * M * N * K
     row = [f"{M}x{N}x{K}"]
-    for mode in ("persistent", "tma"):
-        if mode == "tma":
-            os.environ["TDKV_GEMM_NO_PERSISTENT"] = "1"
-        else:
-            os.environ.pop("TDKV_GEMM_NO_PERSISTENT", None)
+    for mode, env in (("pair", {}), ("persistent", {"TDKV_GEMM_NO_PAIR": "1"}),
+                      ("tma", {"TDKV_GEMM_NO_PAIR": "1", "TDKV_GEMM_NO_PERSISTENT": "1"})):
+        for key in ("TDKV_GEMM_NO_PAIR", "TDKV_GEMM_NO_PERSISTENT"):
+            os.environ.pop(key, None)
+        os.environ.update(env)
         t = timeit(lambda: gemm.gemm_tn(a, b, out=c))
         row.append(f"{mode} {fl / t / 1e12:.0f}")
-    os.environ.pop("TDKV_GEMM_NO_PERSISTENT", None)
+    for key in ("TDKV_GEMM_NO_PAIR", "TDKV_GEMM_NO_PERSISTENT"):
+        os.environ.pop(key, None)
     t = timeit(lambda: torch.matmul(a, b.T))
     row.append(f"cublas(bf16 out) {fl / t / 1e12:.0f}")
     print("  ".join(row), flush=True)

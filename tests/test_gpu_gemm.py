@@ -63,3 +63,19 @@ def test_gemm_bf16_persistent_accumulate():
     want = c.double() + a.double() @ b.double().T
     gemm.gemm_tn(a, b, out=c, accumulate=True)
     assert (c.double() - want).abs().max().item() <= 1e-5 * want.abs().max().item() * 192 ** 0.5
+
+
+@pytest.mark.parametrize("M,N,K", [(2048, 4608, 320), (4096, 2560, 64), (2100, 4700, 104)])
+def test_gemm_bf16_cta_pair(M, N, K):
+    """Shapes large enough for the cta_group::2 kernel (every CTA pair busy),
+    including ragged M/N/K."""
+    g = torch.Generator(device=DEV).manual_seed(M ^ N ^ K)
+    a = torch.randn(M, K, generator=g, device=DEV).bfloat16()
+    b = torch.randn(N, K, generator=g, device=DEV).bfloat16()
+    c = torch.randn(M, N, generator=g, device=DEV)
+    want = a.double() @ b.double().T
+    out = gemm.gemm_tn(a, b)
+    assert (out.double() - want).abs().max().item() <= 1e-5 * max(1.0, want.abs().max().item()) * K ** 0.5
+    want = want + c.double()
+    gemm.gemm_tn(a, b, out=c, accumulate=True)
+    assert (c.double() - want).abs().max().item() <= 1e-5 * max(1.0, want.abs().max().item()) * K ** 0.5
