@@ -760,6 +760,20 @@ def codec_bench(tk, spec, pool, maps, dev, args, peak, frac=None, hint_all=False
     dec_s = ev0.elapsed_time(ev1) * 1e-3 / reps
     dec_bytes = n_mirrors * 2 * dense
     wire = [tk.wire_nbytes(d, 2) for d in diffs]
+    # TDDF wire images (float32 payload, the reference format): GPU pack of
+    # the whole family + one D2H, and GPU unpack of one image into device
+    # slabs (H2D included); bytes = wire image bytes
+    t0 = time.perf_counter()
+    images = tk.serialize_many(diffs)
+    pack_s = time.perf_counter() - t0
+    wire_total = sum(len(w) for w in images)
+    t0 = time.perf_counter()
+    for w in images[:8]:
+        tk.deserialize_to_device(w, dev, pool.k.dtype)
+    torch.cuda.synchronize(dev)
+    unpack_s = time.perf_counter() - t0
+    unpack_bytes = sum(len(w) for w in images[:8])
+    del images
     return {
         "mirrors": n_mirrors, "changed_block_fraction": round(changed / (n_mirrors * spec.num_layers * nb), 4),
         "encode_gbs": round(enc_bytes / enc_s / 1e9, 1),
@@ -771,6 +785,11 @@ def codec_bench(tk, spec, pool, maps, dev, args, peak, frac=None, hint_all=False
         "decode_frac": round(dec_bytes / dec_s / 1e9 / peak, 4),
         "decode_ms_per_family": round(dec_s * 1e3, 3),
         "compression_ratio_mean": round(float(np.mean([dense / w for w in wire])), 3),
+        "wire_pack_gbs": round(wire_total / pack_s / 1e9, 2),
+        "wire_unpack_gbs": round(unpack_bytes / unpack_s / 1e9, 2),
+        "wire_note": "serialize_many of the family (GPU pack, one D2H, Python bytes) and "
+                     "deserialize_to_device of 8 images (host parse, one H2D each, GPU "
+                     "unpack); wall clock, float32 wire bytes",
         "bytes": "encode: 2*dense + payload + 4*changed per mirror (host read included); "
                  "fused decode: 2*dense per mirror (K0+K3 device time)",
     }

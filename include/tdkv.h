@@ -293,6 +293,41 @@ int32_t tdkv_fill_rows(void* d_plane, int64_t layer_stride, int32_t num_layers,
                        const int64_t* d_rows, int64_t n_rows, int32_t row_elems,
                        int32_t dtype, uint32_t value_bits, void* stream);
 
+/* ------------------------------------------------------------------------
+ * Wire format (TDDF) on the GPU.  Replaces the byte assembly of
+ * serialize_diff (diffstore.py:210-239) and the payload extraction of
+ * deserialize_diff (diffstore.py:242-306); the host keeps the structural
+ * parse and the validation (magic, version, flags, ascending indices,
+ * truncation, trailing bytes, valid_len), which are O(layers).
+ *
+ * An image is described by byte segments.  tdkv_wire_pack writes, for each
+ * segment, ``nbytes`` bytes at byte ``offset`` of d_out taken from ``ptr``:
+ * kind TDKV_WIRE_RAW copies bytes; TDKV_WIRE_BF16_TO_F32 reads nbytes/4
+ * bf16 values and writes their float32 encodings (exact).  Segments must not
+ * overlap; d_out must be 4-byte aligned.  tdkv_wire_unpack reads, for each
+ * segment, nbytes (a multiple of 4) of d_in starting at byte ``offset`` and
+ * writes them to ``ptr`` (TDKV_WIRE_RAW: 32-bit words, e.g. block indices)
+ * or converts float32 -> bf16 (TDKV_WIRE_F32_TO_BF16, round to nearest
+ * even); d_in must be 4-byte aligned with >= 4 readable bytes past the last
+ * segment.  max_seg_bytes = the largest segment (sizes the grid).
+ * ---------------------------------------------------------------------- */
+#define TDKV_WIRE_RAW 0
+#define TDKV_WIRE_BF16_TO_F32 1
+#define TDKV_WIRE_F32_TO_BF16 2
+
+typedef struct {
+    uint64_t offset;       /* byte offset in the wire image */
+    uint64_t nbytes;       /* bytes of the wire image covered */
+    const void* ptr;       /* pack: source; unpack: destination (device) */
+    int32_t kind;
+    int32_t pad;
+} tdkv_wire_seg;           /* 32 bytes */
+
+int32_t tdkv_wire_pack(const tdkv_wire_seg* d_segs, int32_t n_segs, int64_t max_seg_bytes,
+                       void* d_out, void* stream);
+int32_t tdkv_wire_unpack(const tdkv_wire_seg* d_segs, int32_t n_segs, int64_t max_seg_bytes,
+                         const void* d_in, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -15,6 +15,7 @@ from .diffstore import (BlockSparseDiff, CompressionStats, DiffStore, FamilyEnco
                         HintSoundnessError, LayerDiff, MalformedDiffError, MasterEntry,
                         MirrorHandle, PinnedMasterError, deserialize_diff, diff_decode_dense,
                         encode_batch, encode_diff, family_cost_from_ratio, serialize_diff,
+                        deserialize_to_device, serialize_many,
                         wire_nbytes)
 from .ledger import CostLedger
 from .paged_pool import OutOfSlotsError, PagedPool, SlotMap, UseAfterFreeError, slot_maps_disjoint
@@ -40,5 +41,6 @@ __all__ = [
     "build_library", "dense_restore", "deserialize_diff", "diff_decode_dense", "encode_batch",
     "encode_diff", "family_cost_from_ratio", "fused_restore", "fused_restore_many",
     "kv_dense_nbytes", "launch_count", "rope_apply", "rope_recover", "serialize_diff",
+    "serialize_many", "deserialize_to_device",
     "skeleton_values", "slot_maps_disjoint", "wire_nbytes",
 ]

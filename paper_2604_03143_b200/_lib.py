@@ -83,6 +83,10 @@ ROWS_JOB = np.dtype([("src_k", "<u8"), ("src_v", "<u8"), ("src_layer_stride", "<
                      ("map_k", "<u8"), ("map_v", "<u8"), ("dst_k", "<u8"), ("dst_v", "<u8"),
                      ("dst_layer_stride", "<i8"), ("dst_rows", "<u8"), ("num_tokens", "<i4"),
                      ("tbl_row", "<i4"), ("tbl_stride", "<i4"), ("rotate", "<i4")])
+WIRE_SEG = np.dtype([("offset", "<u8"), ("nbytes", "<u8"), ("ptr", "<u8"), ("kind", "<i4"),
+                     ("pad", "<i4")])
+WIRE_RAW, WIRE_BF16_TO_F32, WIRE_F32_TO_BF16 = 0, 1, 2
+assert WIRE_SEG.itemsize == 32
 assert COLLECT_JOB.itemsize == 24 and COLLECT_UNIT.itemsize == 16
 assert DIFF_PAIR.itemsize == 32 and DIFF_OUT.itemsize == 40 and ROWS_JOB.itemsize == 112
 
@@ -91,7 +95,7 @@ EXPORTS = (
     "tdkv_collect", "tdkv_diff_compare", "tdkv_diff_compact", "tdkv_diff_encode", "tdkv_rows",
     "tdkv_keydiff", "tdkv_select_important", "tdkv_gemm", "tdkv_qkv_rope", "tdkv_attention",
     "tdkv_fill_rows", "tdkv_alloc_create", "tdkv_alloc_destroy", "tdkv_alloc_free_count",
-    "tdkv_alloc_take", "tdkv_alloc_release",
+    "tdkv_alloc_take", "tdkv_alloc_release", "tdkv_wire_pack", "tdkv_wire_unpack",
 )
 
 _P = ctypes.c_void_p
@@ -122,6 +126,8 @@ _SIGS = {
     "tdkv_alloc_free_count": (_I64, [_P]),
     "tdkv_alloc_take": (_I32, [_P, _I64, _P]),
     "tdkv_alloc_release": (_I32, [_P, _P, _I64]),
+    "tdkv_wire_pack": (_I32, [_P, _I32, _I64, _P, _P]),
+    "tdkv_wire_unpack": (_I32, [_P, _I32, _I64, _P, _P]),
     "tdkv_attention": (_I32, [_P, _P, _P, _P, _P, _P, _P, _I32, _I32, _I32, _I32,
                               ctypes.c_float, _P, _P]),
 }

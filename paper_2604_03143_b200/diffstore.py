@@ -4,15 +4,18 @@
 Encoding (``encode_diff`` / ``encode_batch`` / ``DiffStore.encode_family``)
 runs kernel K2 on the device: one compare pass over every (mirror, layer,
 block) with float '!=' semantics (diffstore.py:151-153) and one compaction
-pass that writes each layer's changed blocks in ascending order, zero-padded,
-into a payload slab (diffstore.py:166-173).  A whole family is encoded in
-two launches and one device->host read of the counts and indices.
+that writes each layer's changed blocks in ascending order, zero-padded, into
+a payload slab (diffstore.py:166-173).  A whole family is encoded in one
+launch and one device->host read of the counts and indices.
 
 Decoding is fused into restores (restore.py); ``diff_decode_dense`` is the
 dense baseline (diffstore.py:185-203), one K3 launch.
 
-The wire format (diffstore.py:10-23, 210-306) is produced/parsed on the host
-and is byte-identical to the reference's (version 1, float32 payload).
+The wire format (diffstore.py:10-23, 210-306) is byte-identical to the
+reference's (version 1, float32 payload): encoder output is packed on the GPU
+(tdkv_wire_pack, one D2H per batch of diffs) and an image can be unpacked
+straight into device slabs for the fused restore (tdkv_wire_unpack); host
+diffs keep the host path.
 """
 from __future__ import annotations
 
@@ -488,7 +491,7 @@ def _f32_bytes(x) -> bytes:
     return np.ascontiguousarray(x, dtype="<f4").tobytes()
 
 
-def serialize_diff(diff: BlockSparseDiff) -> bytes:
+def _serialize_host(diff: BlockSparseDiff) -> bytes:
     parts = [_HEADER.pack(MAGIC, VERSION, diff.num_layers, diff.block_size, diff.num_heads,
                           diff.head_dim, diff.total_tokens)]
     for ld in diff.layers:
@@ -504,6 +507,88 @@ def serialize_diff(diff: BlockSparseDiff) -> bytes:
     return b"".join(parts)
 
 
+def _gpu_packable(diff: BlockSparseDiff) -> bool:
+    """Encoder-produced diffs (payload in a device slab, shared K/V indices)
+    are packed on the GPU; anything else takes the host path."""
+    return diff._slab is not None and diff._slab.pay_k.is_cuda
+
+
+def _pack_segments(diff: BlockSparseDiff, base: int, lit: bytearray, segs: list) -> int:
+    """Append the wire segments of one slab-backed diff at image offset
+    ``base``; literal bytes (header, counts, flags, indices, trailer) go to
+    ``lit`` (uploaded once) and are referenced by their offset there.
+    Returns the image length."""
+    s = diff._slab
+    pay_k, pay_v = s.pay_k, s.pay_v
+    esz = pay_k.element_size()
+    blk = diff.block_size * diff.num_heads * diff.head_dim
+    kind = _lib.WIRE_BF16_TO_F32 if pay_k.dtype == torch.bfloat16 else _lib.WIRE_RAW
+    off = base
+
+    def literal(b: bytes) -> None:
+        nonlocal off
+        segs.append((off, len(b), -1 - len(lit), _lib.WIRE_RAW))   # negative = literal
+        lit.extend(b)
+        off += len(b)
+
+    literal(_HEADER.pack(MAGIC, VERSION, diff.num_layers, diff.block_size, diff.num_heads,
+                         diff.head_dim, diff.total_tokens))
+    for layer in range(diff.num_layers):
+        c = int(s.counts[layer])
+        row0 = layer * s.cap
+        idx = s.idx[row0:row0 + c].astype("<u4").tobytes()
+        literal(struct.pack("<IB", c, 1) + idx)
+        for plane in (pay_k, pay_v):
+            if c:
+                segs.append((off, c * blk * 4, ptr(plane) + row0 * blk * esz, kind))
+                off += c * blk * 4
+    literal(struct.pack("<I", CacheBlockConfig(diff.block_size).valid_len(diff.total_tokens)))
+    return off - base
+
+
+def serialize_many(diffs: Sequence[BlockSparseDiff]) -> List[bytes]:
+    """Wire images of several diffs.  Encoder-produced (device) diffs are
+    packed by one tdkv_wire_pack launch into one device buffer (payload
+    converted to float32 on the fly) and read back with one copy; the
+    bytes are identical to serialize_diff (diffstore.py:210-239)."""
+    out: List[Optional[bytes]] = [None] * len(diffs)
+    gpu = [i for i, d in enumerate(diffs) if _gpu_packable(d)]
+    for i, d in enumerate(diffs):
+        if i not in gpu:
+            out[i] = _serialize_host(d)
+    if not gpu:
+        return out
+    device = diffs[gpu[0]]._slab.pay_k.device
+    lit = bytearray()
+    segs: list = []
+    spans = []
+    base = 0
+    for i in gpu:
+        n = _pack_segments(diffs[i], base, lit, segs)
+        spans.append((base, n))
+        base += (n + 15) & ~15
+    d_lit = upload(np.frombuffer(lit, np.uint8), device)
+    table = np.zeros(len(segs), _lib.WIRE_SEG)
+    for j, (o, n, p, k) in enumerate(segs):
+        table[j] = (o, n, p if p >= 0 else ptr(d_lit) + (-1 - p), k, 0)
+    d_table = upload(table.view(np.uint8), device)
+    image = torch.empty(base + 16, dtype=torch.uint8, device=device)
+    _lib.call("tdkv_wire_pack", ptr(d_table), len(segs), int(table["nbytes"].max()), ptr(image),
+              stream_handle(device))
+    host = torch.empty(base, dtype=torch.uint8, pin_memory=base >= 1 << 16)
+    host.copy_(image[:base])
+    buf = host.numpy()
+    for i, (o, n) in zip(gpu, spans):
+        out[i] = buf[o:o + n].tobytes()
+    return out
+
+
+def serialize_diff(diff: BlockSparseDiff) -> bytes:
+    """The TDDF wire image (diffstore.py:210-239): GPU-packed for encoder
+    output, host-assembled otherwise; byte-identical either way."""
+    return serialize_many([diff])[0]
+
+
 class _Cursor:
     def __init__(self, buf: bytes) -> None:
         self.buf = buf
@@ -516,6 +601,13 @@ class _Cursor:
         self.pos += n
         return out
 
+    def skip(self, n: int, what: str) -> int:
+        if self.pos + n > len(self.buf):
+            raise MalformedDiffError(f"truncated diff: expected {what}")
+        at = self.pos
+        self.pos += n
+        return at
+
     def u32(self, what: str) -> int:
         return struct.unpack("<I", self.take(4, what))[0]
 
@@ -525,13 +617,19 @@ class _Cursor:
             raise MalformedDiffError(f"{what} must be strictly increasing")
         return a
 
-    def blocks(self, count: int, shape: tuple, what: str) -> np.ndarray:
-        n = count * int(np.prod(shape)) * 4
-        return np.frombuffer(self.take(n, what), dtype="<f4").astype(np.float32).reshape(
-            (count,) + shape)
+
+@dataclass
+class _WireLayer:
+    indices: np.ndarray
+    k_off: int                   # byte offset of the K payload in the image
+    v_indices: Optional[np.ndarray]
+    v_off: int
 
 
-def deserialize_diff(buf: bytes) -> BlockSparseDiff:
+def _parse_wire(buf: bytes):
+    """Structural parse + every check of deserialize_diff (diffstore.py:242-306)
+    without touching the payload bytes: geometry and per-layer index arrays
+    and payload offsets."""
     cur = _Cursor(buf)
     magic, version, num_layers, bs, heads, dim, total = _HEADER.unpack(
         cur.take(_HEADER.size, "header"))
@@ -541,7 +639,7 @@ def deserialize_diff(buf: bytes) -> BlockSparseDiff:
         raise MalformedDiffError(f"unsupported version {version}")
     if min(num_layers, bs, heads, dim, total) <= 0:
         raise MalformedDiffError("non-positive geometry field")
-    shape = (bs, heads, dim)
+    blk_bytes = bs * heads * dim * 4
     layers = []
     for layer in range(num_layers):
         count = cur.u32(f"layer {layer} count")
@@ -549,21 +647,103 @@ def deserialize_diff(buf: bytes) -> BlockSparseDiff:
         if flag not in (0, 1):
             raise MalformedDiffError(f"layer {layer}: unknown index flag {flag}")
         idx = cur.ids(count, f"layer {layer} indices")
-        kb = cur.blocks(count, shape, f"layer {layer} K payload")
+        k_off = cur.skip(count * blk_bytes, f"layer {layer} K payload")
         if flag == 1:
-            layers.append(LayerDiff(idx, kb, cur.blocks(count, shape, f"layer {layer} V payload")))
+            v_off = cur.skip(count * blk_bytes, f"layer {layer} V payload")
+            layers.append(_WireLayer(idx, k_off, None, v_off))
         else:
             vc = cur.u32(f"layer {layer} V count")
             vidx = cur.ids(vc, f"layer {layer} V indices")
-            layers.append(LayerDiff(idx, kb, cur.blocks(vc, shape, f"layer {layer} V payload"),
-                                    v_indices=vidx))
+            v_off = cur.skip(vc * blk_bytes, f"layer {layer} V payload")
+            layers.append(_WireLayer(idx, k_off, vidx, v_off))
     valid = cur.u32("valid_len trailer")
     if cur.pos != len(buf):
         raise MalformedDiffError("trailing bytes after diff")
-    diff = BlockSparseDiff(num_layers, bs, heads, dim, total, layers)
+    nb = CacheBlockConfig(bs).num_blocks(total)
+    for wl in layers:
+        for ids in (wl.indices, wl.v_indices):
+            if ids is not None and ids.size and ids.max() >= nb:
+                raise ValueError("block index out of range")
     if valid != CacheBlockConfig(bs).valid_len(total):
         raise MalformedDiffError("valid_len disagrees with token count")
+    return (num_layers, bs, heads, dim, total), layers
+
+
+def deserialize_diff(buf: bytes) -> BlockSparseDiff:
+    """Parse a wire image into a host (numpy float32) diff (diffstore.py:242-306)."""
+    (num_layers, bs, heads, dim, total), wls = _parse_wire(buf)
+    shape = (bs, heads, dim)
+    blk = bs * heads * dim
+
+    def blocks(off: int, count: int) -> np.ndarray:
+        return np.frombuffer(buf, dtype="<f4", count=count * blk, offset=off).astype(
+            np.float32).reshape((count,) + shape)
+
+    layers = []
+    for wl in wls:
+        vc = wl.indices.size if wl.v_indices is None else wl.v_indices.size
+        layers.append(LayerDiff(wl.indices, blocks(wl.k_off, wl.indices.size),
+                                blocks(wl.v_off, vc), v_indices=wl.v_indices))
+    return BlockSparseDiff(num_layers, bs, heads, dim, total, layers)
+
+
+def deserialize_to_device(buf: bytes, device: Optional[torch.device] = None,
+                          dtype: torch.dtype = torch.bfloat16) -> BlockSparseDiff:
+    """Parse a wire image straight into a device diff ready for the fused
+    restore: the host validates the structure (same errors as
+    deserialize_diff), the image crosses PCIe once and one tdkv_wire_unpack
+    launch scatters every payload block into a K and a V slab (float32 wire
+    -> ``dtype``); the block maps are built on the host from the indices."""
+    device = device or default_device()
+    (num_layers, bs, heads, dim, total), wls = _parse_wire(buf)
+    nb = CacheBlockConfig(bs).num_blocks(total)
+    blk = bs * heads * dim
+    kc = [wl.indices.size for wl in wls]
+    vc = [wl.indices.size if wl.v_indices is None else wl.v_indices.size for wl in wls]
+    k_rows, v_rows = _excl(kc), _excl(vc)
+    pay_k = torch.empty((max(1, sum(kc)), bs, heads, dim), dtype=dtype, device=device)
+    pay_v = torch.empty((max(1, sum(vc)), bs, heads, dim), dtype=dtype, device=device)
+    kind = _lib.WIRE_F32_TO_BF16 if dtype == torch.bfloat16 else _lib.WIRE_RAW
+    esz = pay_k.element_size()
+    maps = np.full((2, num_layers, nb), -1, np.int32)
+    segs = []
+    for layer, wl in enumerate(wls):
+        vidx = wl.indices if wl.v_indices is None else wl.v_indices
+        maps[0, layer, wl.indices] = k_rows[layer] + np.arange(kc[layer], dtype=np.int32)
+        maps[1, layer, vidx] = v_rows[layer] + np.arange(vc[layer], dtype=np.int32)
+        if kc[layer]:
+            segs.append((wl.k_off, kc[layer] * blk * 4, ptr(pay_k) + k_rows[layer] * blk * esz,
+                         kind, 0))
+        if vc[layer]:
+            segs.append((wl.v_off, vc[layer] * blk * 4, ptr(pay_v) + v_rows[layer] * blk * esz,
+                         kind, 0))
+    # the image (+ 4 bytes of padding for the funnel-shift reads) in one copy
+    staged = torch.empty(len(buf) + 8, dtype=torch.uint8, pin_memory=True)
+    staged.numpy()[:len(buf)] = np.frombuffer(buf, np.uint8)
+    image = staged.to(device, non_blocking=True)
+    table = np.array(segs, dtype=_lib.WIRE_SEG) if segs else np.zeros(0, _lib.WIRE_SEG)
+    d_maps = torch.from_numpy(maps.reshape(2, -1)).to(device, non_blocking=True)
+    if segs:
+        d_table = upload(table.view(np.uint8), device)
+        _lib.call("tdkv_wire_unpack", ptr(d_table), len(segs), int(table["nbytes"].max()),
+                  ptr(image), stream_handle(device))
+    layers = []
+    for layer, wl in enumerate(wls):
+        k0, v0 = k_rows[layer], v_rows[layer]
+        layers.append(LayerDiff(wl.indices, pay_k[k0:k0 + kc[layer]], pay_v[v0:v0 + vc[layer]],
+                                v_indices=wl.v_indices))
+    diff = BlockSparseDiff(num_layers, bs, heads, dim, total, layers)
+    diff._dev = _DeviceDiff(pay_k, pay_v, d_maps[0], d_maps[1])
+    diff._keepalive = (image, staged)             # until the unpack has run
     return diff
+
+
+def _excl(counts) -> List[int]:
+    out, acc = [], 0
+    for c in counts:
+        out.append(acc)
+        acc += c
+    return out
 
 
 # ---------------------------------------------------------------------------

@@ -41,6 +41,7 @@ def test_descriptor_layouts_match_header():
     for struct, dt in [("tdkv_collect_job", _lib.COLLECT_JOB),
                        ("tdkv_collect_unit", _lib.COLLECT_UNIT),
                        ("tdkv_diff_pair", _lib.DIFF_PAIR), ("tdkv_diff_out", _lib.DIFF_OUT),
+                       ("tdkv_wire_seg", _lib.WIRE_SEG),
                        ("tdkv_rows_job", _lib.ROWS_JOB)]:
         body = re.search(r"typedef struct \{([^{}]*)\}\s*" + struct + ";", text).group(1)
         # field count and total size (pointers / int64 = 8 B, int32 = 4 B)
