@@ -764,7 +764,7 @@ def codec_bench(tk, spec, pool, maps, dev, args, peak, frac=None, hint_all=False
     # the whole family + one D2H, and GPU unpack of one image into device
     # slabs (H2D included); bytes = wire image bytes
     t0 = time.perf_counter()
-    images = tk.serialize_many(diffs)
+    images = tk.serialize_many(diffs, copy=False)
     pack_s = time.perf_counter() - t0
     wire_total = sum(len(w) for w in images)
     t0 = time.perf_counter()
@@ -787,7 +787,8 @@ def codec_bench(tk, spec, pool, maps, dev, args, peak, frac=None, hint_all=False
         "compression_ratio_mean": round(float(np.mean([dense / w for w in wire])), 3),
         "wire_pack_gbs": round(wire_total / pack_s / 1e9, 2),
         "wire_unpack_gbs": round(unpack_bytes / unpack_s / 1e9, 2),
-        "wire_note": "serialize_many of the family (GPU pack, one D2H, Python bytes) and "
+        "wire_note": "serialize_many of the family (GPU pack, one D2H into pinned memory, "
+                     "images as memoryviews) and "
                      "deserialize_to_device of 8 images (host parse, one H2D each, GPU "
                      "unpack); wall clock, float32 wire bytes",
         "bytes": "encode: 2*dense + payload + 4*changed per mirror (host read included); "

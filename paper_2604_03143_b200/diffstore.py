@@ -546,12 +546,16 @@ def _pack_segments(diff: BlockSparseDiff, base: int, lit: bytearray, segs: list)
     return off - base
 
 
-def serialize_many(diffs: Sequence[BlockSparseDiff]) -> List[bytes]:
+def serialize_many(diffs: Sequence[BlockSparseDiff], copy: bool = True) -> list:
     """Wire images of several diffs.  Encoder-produced (device) diffs are
     packed by one tdkv_wire_pack launch into one device buffer (payload
     converted to float32 on the fly) and read back with one copy; the
-    bytes are identical to serialize_diff (diffstore.py:210-239)."""
-    out: List[Optional[bytes]] = [None] * len(diffs)
+    bytes are identical to serialize_diff (diffstore.py:210-239).
+
+    ``copy=False`` returns the GPU-packed images as read-only memoryviews
+    of one pinned host buffer (no per-image bytes object: building Python
+    bytes from a fresh buffer runs at ~2 GB/s, the PCIe read at ~50)."""
+    out: list = [None] * len(diffs)
     gpu = [i for i, d in enumerate(diffs) if _gpu_packable(d)]
     for i, d in enumerate(diffs):
         if i not in gpu:
@@ -578,8 +582,9 @@ def serialize_many(diffs: Sequence[BlockSparseDiff]) -> List[bytes]:
     host = torch.empty(base, dtype=torch.uint8, pin_memory=base >= 1 << 16)
     host.copy_(image[:base])
     buf = host.numpy()
+    view = memoryview(buf).toreadonly()
     for i, (o, n) in zip(gpu, spans):
-        out[i] = buf[o:o + n].tobytes()
+        out[i] = buf[o:o + n].tobytes() if copy else view[o:o + n]
     return out
 
 

@@ -116,3 +116,13 @@ def test_unpack_rejects_malformed_images_like_the_host_parser():
         with pytest.raises(tk.MalformedDiffError) as e2:
             tk.deserialize_to_device(b, DEV)
         assert str(e1.value) == str(e2.value)
+
+
+def test_serialize_many_views_equal_bytes():
+    rng = np.random.default_rng(3)
+    _, _, diffs = _family(rng, torch.bfloat16, 100, 2, 2, 16, 16, 3, 0.4)
+    views = tk.serialize_many(diffs, copy=False)
+    owned = tk.serialize_many(diffs)
+    assert [bytes(v) for v in views] == owned
+    back = tk.deserialize_to_device(views[1], DEV)
+    assert all(np.array_equal(a.indices, b.indices) for a, b in zip(diffs[1].layers, back.layers))
