@@ -328,6 +328,39 @@ int32_t tdkv_wire_pack(const tdkv_wire_seg* d_segs, int32_t n_segs, int64_t max_
 int32_t tdkv_wire_unpack(const tdkv_wire_seg* d_segs, int32_t n_segs, int64_t max_seg_bytes,
                          const void* d_in, void* stream);
 
+/* ------------------------------------------------------------------------
+ * Host segment index.  Replaces segment_index.SegmentIndex
+ * (segment_index.py:86-183): content-digest (16-byte token_digest) keyed
+ * entries, the most recent entry per digest wins a lookup, byte-budget LRU
+ * eviction that skips pinned entries.  Pins are queried at eviction time
+ * through ``pinned(ctx, entry_id)`` (nonzero = pinned; may be NULL).  The
+ * index keeps ids and sizes; evicted ids are returned LRU-first so the
+ * owner can release its objects (the reference's on_evict order).
+ * ---------------------------------------------------------------------- */
+typedef int32_t (*tdkv_pinned_fn)(void* ctx, int64_t entry_id);
+
+void* tdkv_segidx_create(int64_t budget_bytes);
+void tdkv_segidx_destroy(void* handle);
+int64_t tdkv_segidx_count(void* handle);
+int64_t tdkv_segidx_total(void* handle);
+/* Insert, then evict LRU-first down to the budget (ids into evicted[cap]). */
+int32_t tdkv_segidx_insert(void* handle, const uint8_t* digest16, int64_t entry_id,
+                           int64_t nbytes, tdkv_pinned_fn pinned, void* ctx, int64_t* evicted,
+                           int32_t cap, int32_t* n_evicted);
+/* n digests (16 bytes each) -> most recent entry id or -1; refresh != 0
+ * moves each hit to most-recently-used (SegmentIndex.lookup), 0 does not
+ * (SegmentIndex.__contains__). */
+int32_t tdkv_segidx_lookup(void* handle, const uint8_t* digests16, int32_t n, int32_t refresh,
+                           int64_t* out_ids);
+/* Remove an entry; for an id that is not present the reference still
+ * subtracts the entry's size (segment_index.py:172-181), so nbytes is
+ * subtracted then too. */
+int32_t tdkv_segidx_remove(void* handle, int64_t entry_id, int64_t nbytes);
+int32_t tdkv_segidx_evict(void* handle, int64_t budget_bytes, tdkv_pinned_fn pinned, void* ctx,
+                          int64_t* evicted, int32_t cap, int32_t* n_evicted);
+/* Live entry ids, least recently used first. */
+int32_t tdkv_segidx_entries(void* handle, int64_t* out_ids, int64_t cap, int64_t* n_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -541,3 +541,85 @@ def select_important(mags: np.ndarray, budget: int) -> np.ndarray:
 def recompute_budget(fraction: float, shared_count: int) -> int:
     """ceil(fraction*shared) with decimal-noise guard (pic.py:174-177)."""
     return int(math.ceil(round(fraction * shared_count, 6)))
+
+
+# ---------------------------------------------------------------------------
+# segment index (segment_index.py:86-183)
+
+
+class SegmentIndexPort:
+    """Digest -> entries cache with byte-budget LRU eviction, restated from
+    segment_index.SegmentIndex: per digest a stack of entries (lookup takes
+    the newest, :125-135); recency = insertion-ordered map keyed by entry_id,
+    refreshed by lookup (:131-134); insert adds then evicts to the budget
+    (:137-143); eviction walks oldest-first, skipping pinned refs, until the
+    total fits (:159-170); removal subtracts the size and reports on_evict
+    even for an entry that is not present (:172-181)."""
+
+    def __init__(self, budget_bytes, is_pinned=None, on_evict=None):
+        if budget_bytes < 0:
+            raise ValueError("budget must be non-negative")
+        self.budget_bytes = int(budget_bytes)
+        self.is_pinned = is_pinned or (lambda ref: False)
+        self.on_evict = on_evict
+        self.stacks = {}
+        self.order = {}
+        self.total = 0
+
+    def __len__(self):
+        return len(self.order)
+
+    def __contains__(self, digest):
+        return bool(self.stacks.get(digest))
+
+    @property
+    def total_bytes(self):
+        return self.total
+
+    def entries(self):
+        return tuple(self.order.values())
+
+    def lookup(self, digest):
+        stack = self.stacks.get(digest)
+        if not stack:
+            return None
+        e = stack[-1]
+        self.order.pop(e.entry_id, None)
+        self.order[e.entry_id] = e
+        return e
+
+    def insert(self, e):
+        self.stacks.setdefault(e.digest, []).append(e)
+        self.order[e.entry_id] = e
+        self.total += e.nbytes
+        self._evict(self.budget_bytes)
+
+    def remove(self, e):
+        if self.is_pinned(e.kv_ref):
+            raise RuntimeError("entry is pinned by live mirrors")
+        self._drop(e)
+
+    def evict_to_budget(self, budget=None):
+        return self._evict(self.budget_bytes if budget is None else budget)
+
+    def _evict(self, budget):
+        n = 0
+        for e in list(self.order.values()):
+            if self.total <= budget:
+                break
+            if self.is_pinned(e.kv_ref):
+                continue
+            self._drop(e)
+            n += 1
+        return n
+
+    def _drop(self, e):
+        stack = self.stacks.get(e.digest, [])
+        if e in stack:
+            stack.remove(e)
+            if not stack:
+                del self.stacks[e.digest]
+        self.order.pop(e.entry_id, None)
+        self.total -= e.nbytes
+        if self.on_evict is not None:
+            self.on_evict(e)

@@ -21,6 +21,8 @@ from .ledger import CostLedger
 from .paged_pool import OutOfSlotsError, PagedPool, SlotMap, UseAfterFreeError, slot_maps_disjoint
 from .restore import dense_restore, fused_restore, fused_restore_many
 from .rope import rope_apply, rope_recover
+from .segment_index import (EmptySegmentError, PinnedEntryError, SegmentCacheEntry,
+                            SegmentIndex)
 from .gemm import gemm_tn
 from .pic import RecoveryResult, ReusePlan, collective_recover, probe_and_select, recover_prepared
 from .recompute import ToyModel, full_prefill, recompute_positions, refresh, selective_forward
@@ -41,6 +43,7 @@ __all__ = [
     "build_library", "dense_restore", "deserialize_diff", "diff_decode_dense", "encode_batch",
     "encode_diff", "family_cost_from_ratio", "fused_restore", "fused_restore_many",
     "kv_dense_nbytes", "launch_count", "rope_apply", "rope_recover", "serialize_diff",
-    "serialize_many", "deserialize_to_device",
+    "serialize_many", "deserialize_to_device", "EmptySegmentError", "PinnedEntryError",
+    "SegmentCacheEntry", "SegmentIndex",
     "skeleton_values", "slot_maps_disjoint", "wire_nbytes",
 ]

@@ -96,6 +96,9 @@ EXPORTS = (
     "tdkv_keydiff", "tdkv_select_important", "tdkv_gemm", "tdkv_qkv_rope", "tdkv_attention",
     "tdkv_fill_rows", "tdkv_alloc_create", "tdkv_alloc_destroy", "tdkv_alloc_free_count",
     "tdkv_alloc_take", "tdkv_alloc_release", "tdkv_wire_pack", "tdkv_wire_unpack",
+    "tdkv_segidx_create", "tdkv_segidx_destroy", "tdkv_segidx_count", "tdkv_segidx_total",
+    "tdkv_segidx_insert", "tdkv_segidx_lookup", "tdkv_segidx_remove", "tdkv_segidx_evict",
+    "tdkv_segidx_entries",
 )
 
 _P = ctypes.c_void_p
@@ -127,6 +130,15 @@ _SIGS = {
     "tdkv_alloc_take": (_I32, [_P, _I64, _P]),
     "tdkv_alloc_release": (_I32, [_P, _P, _I64]),
     "tdkv_wire_pack": (_I32, [_P, _I32, _I64, _P, _P]),
+    "tdkv_segidx_create": (_P, [_I64]),
+    "tdkv_segidx_destroy": (None, [_P]),
+    "tdkv_segidx_count": (_I64, [_P]),
+    "tdkv_segidx_total": (_I64, [_P]),
+    "tdkv_segidx_insert": (_I32, [_P, _P, _I64, _I64, _P, _P, _P, _I32, _P]),
+    "tdkv_segidx_lookup": (_I32, [_P, _P, _I32, _I32, _P]),
+    "tdkv_segidx_remove": (_I32, [_P, _I64, _I64]),
+    "tdkv_segidx_evict": (_I32, [_P, _I64, _P, _P, _P, _I32, _P]),
+    "tdkv_segidx_entries": (_I32, [_P, _P, _I64, _P]),
     "tdkv_wire_unpack": (_I32, [_P, _I32, _I64, _P, _P]),
     "tdkv_attention": (_I32, [_P, _P, _P, _P, _P, _P, _P, _I32, _I32, _I32, _I32,
                               ctypes.c_float, _P, _P]),
@@ -166,6 +178,9 @@ def call(name: str, *args) -> None:
     if rc != 0:
         msg = lib.tdkv_last_error().decode(errors="replace")
         raise TdkvError(f"{name} failed ({rc}): {msg}")
+
+
+PINNED_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64)
 
 
 def launch_count() -> int:

@@ -29,7 +29,7 @@ sys.dont_write_bytecode = True
 sys.path.insert(0, "/root/reference/pkg/src")
 
 from roundkv.collective import collective_recover, form_groups  # noqa: E402
-from roundkv.core import CacheBlockConfig, LayeredKv, ModelConfig, PositionSpan  # noqa: E402
+from roundkv.core import CacheBlockConfig, LayeredKv, ModelConfig, PositionSpan, token_digest  # noqa: E402
 from roundkv.diffstore import (  # noqa: E402
     DiffStore, HintSoundnessError, MasterEntry, MirrorHandle, encode_diff,
     serialize_diff,
@@ -343,6 +343,55 @@ def gen_allocator():
     return ops
 
 
+def gen_segment_index():
+    """A seeded insert / lookup / pin / remove / evict stream through
+    segment_index.SegmentIndex (segment_index.py:86-183); entries are
+    labelled by creation order, state recorded after every step."""
+    from roundkv.segment_index import PinnedEntryError, SegmentCacheEntry, SegmentIndex
+
+    class Ref:
+        def __init__(self):
+            self.pinned = False
+
+    rng = np.random.default_rng(23)
+    made, label = [], {}
+    evicted = []
+    idx = SegmentIndex(2000, is_pinned=lambda r: r.pinned,
+                       on_evict=lambda e: evicted.append(label[id(e)]))
+    ops = []
+    for _ in range(1500):
+        r = int(rng.integers(0, 10))
+        if r < 4:
+            tok, nb = int(rng.integers(0, 30)), int(rng.integers(1, 300))
+            e = SegmentCacheEntry(token_digest([tok]), np.arange(1), Ref(), b"c" * 16, nb)
+            label[id(e)] = len(made)
+            made.append(e)
+            idx.insert(e)
+            op = {"op": "insert", "tok": tok, "nbytes": nb}
+        elif r < 7:
+            tok = int(rng.integers(0, 30))
+            hit = idx.lookup(token_digest([tok]))
+            op = {"op": "lookup", "tok": tok, "hit": -1 if hit is None else label[id(hit)]}
+        elif r == 7 and made:
+            i = int(rng.integers(0, len(made)))
+            made[i].kv_ref.pinned = not made[i].kv_ref.pinned
+            op = {"op": "pin", "label": i}
+        elif r == 8 and made:
+            i = int(rng.integers(0, len(made)))
+            try:
+                idx.remove(made[i])
+                op = {"op": "remove", "label": i, "raised": False}
+            except PinnedEntryError:
+                op = {"op": "remove", "label": i, "raised": True}
+        else:
+            b = int(rng.integers(0, 3000))
+            op = {"op": "evict", "budget": b, "n": idx.evict_to_budget(b)}
+        op.update(evicted=list(evicted), total=idx.total_bytes, len=len(idx),
+                  lru=[label[id(e)] for e in idx.entries()])
+        ops.append(op)
+    return ops
+
+
 def gen_toymodel():
     """Toy transformer outputs (the selective recompute's arithmetic,
     toymodel.py:36-192): weights digests, a full prefill and a selective
@@ -452,6 +501,7 @@ def main():
         "known": gen_known_answers(),
         "restores": gen_restores(),
         "allocator": gen_allocator(),
+        "segment_index": gen_segment_index(),
     }
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump(golden, f, indent=1, sort_keys=True)

@@ -121,3 +121,44 @@ def restore_trials(n=200):
         chosen = sorted(int(b) for b in rng.choice(nb, count, replace=False))
         mk, mv, hints = perturb(rng, k, v, bs, chosen)
         yield RestoreTrial(bs, k, v, pos, mk, mv, hints, delta)
+
+
+def replay_segment_index(make_index, entry_factory, ops):
+    """Replay the reference's recorded segment-index stream (golden.json
+    'segment_index') on ``make_index(budget, is_pinned, on_evict)`` and check
+    every recorded outcome; ``entry_factory(tok, nbytes, ref)`` builds an
+    entry for a 1-token segment."""
+    import hashlib
+
+    class Ref:
+        def __init__(self):
+            self.pinned = False
+
+    def digest(tok):
+        return hashlib.blake2b(np.asarray([tok], dtype="<u4").tobytes(), digest_size=16).digest()
+
+    made, label, evicted = [], {}, []
+    idx = make_index(2000, lambda r: r.pinned, lambda e: evicted.append(label[id(e)]))
+    for step, op in enumerate(ops):
+        if op["op"] == "insert":
+            e = entry_factory(op["tok"], op["nbytes"], Ref())
+            label[id(e)] = len(made)
+            made.append(e)
+            idx.insert(e)
+        elif op["op"] == "lookup":
+            hit = idx.lookup(digest(op["tok"]))
+            assert (-1 if hit is None else label[id(hit)]) == op["hit"], step
+        elif op["op"] == "pin":
+            made[op["label"]].kv_ref.pinned = not made[op["label"]].kv_ref.pinned
+        elif op["op"] == "remove":
+            raised = False
+            try:
+                idx.remove(made[op["label"]])
+            except Exception:                     # the pinned-entry error of each API
+                raised = True
+            assert raised == op["raised"], step
+        else:
+            assert idx.evict_to_budget(op["budget"]) == op["n"], step
+        assert evicted == op["evicted"], step
+        assert idx.total_bytes == op["total"] and len(idx) == op["len"], step
+        assert [label[id(e)] for e in idx.entries()] == op["lru"], step

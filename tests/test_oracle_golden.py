@@ -273,3 +273,20 @@ def test_select_master_and_budget():
     assert ref.select_master({2: 1.5, 0: 1.5, 1: 2.0}) == 0
     assert ref.recompute_budget(0.15, 20) == 3
     assert ref.recompute_budget(0.15, 21) == 4
+
+
+def test_segment_index_port_matches_reference_stream():
+    from helpers import replay_segment_index
+
+    class E:
+        _n = 0
+
+        def __init__(self, tok, nbytes, kv_ref):
+            import hashlib
+            self.digest = hashlib.blake2b(np.asarray([tok], dtype="<u4").tobytes(),
+                                          digest_size=16).digest()
+            self.nbytes, self.kv_ref = nbytes, kv_ref
+            E._n += 1
+            self.entry_id = E._n
+
+    replay_segment_index(lambda b, p, ev: ref.SegmentIndexPort(b, p, ev), E, G["segment_index"])
