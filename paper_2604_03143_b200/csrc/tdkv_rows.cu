@@ -9,6 +9,8 @@
 // 164); with rotate == 0 and identity destinations it is diff_decode_dense
 // (diffstore.py:185-203).  No dense mirror is ever materialized on the fused
 // path.
+#include <cstdlib>
+
 #include "tdkv_common.cuh"
 
 namespace tdkv {
@@ -126,13 +128,26 @@ __global__ void __launch_bounds__(256, 3)
     }
 }
 
-// TMA-staged variant (contiguous sources): a persistent CTA double-buffers
-// row tiles of <= tile_rows rows (never straddling a diff block) into shared
-// memory with cp.async.bulk while the threads rotate and scatter the
-// previous tile -- loads are decoupled from the scattered stores exactly as
-// in K1.
-template <typename T>
-__global__ void __launch_bounds__(256)
+// TMA-staged variant (contiguous sources), warp-specialized: warp 8 is the
+// producer -- it resolves each work item (job fields, block-map entry,
+// source/destination addresses), loads the tile's destination rows into the
+// stage's metadata and issues the bulk copies of the tile's K and V rows
+// (never straddling a diff block) -- while warps 0-7 rotate and scatter the
+// tiles of earlier stages.  A kStages ring with full/empty mbarriers links
+// them, so the dependent metadata loads and the copies run ahead of the
+// consumers and the loop has no CTA-wide barrier.
+constexpr int kRowsConsumers = 256;
+
+struct RowsItem {
+    int valid;                // 0 = no more items (sentinel stage)
+    int lo, n;                // token range of the tile
+    int rotate, tbl_row, tbl_stride;
+    void* dk;                 // destination planes of the item's layer
+    void* dv;
+};
+
+template <typename T, int S>
+__global__ void __launch_bounds__(kRowsConsumers + 32)
     rows_tma_kernel(const tdkv_rows_job* __restrict__ jobs, const void* __restrict__ table_v,
                     const RowsGeom g, const int tile_rows) {
     using V = uint4;
@@ -140,133 +155,127 @@ __global__ void __launch_bounds__(256)
     constexpr int kEpu = 16 / (int)sizeof(T);
     constexpr int kPairs = kEpu / 2;
     extern __shared__ __align__(128) uint8_t smem[];
-    __shared__ __align__(8) uint64_t bars[2];
+    __shared__ __align__(8) uint64_t full[S], empty[S];
+    __shared__ __align__(16) int64_t s_drow[S][32];
+    __shared__ RowsItem s_it[S];
 
     const Tbl* __restrict__ table = static_cast<const Tbl*>(table_v);
-    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
     const int row_bytes = g.row_elems * (int)sizeof(T);
     const int upr = row_bytes / 16;
     const int tile_bytes = tile_rows * row_bytes;
     const int half = g.head_dim >> 1;
-    const int tx_n = upr < nthr ? upr : nthr;
-    const int rows_per_pass = nthr / tx_n;
-    const int tx = tid % tx_n, ty = tid / tx_n;
     const int tpb = (g.block_size + tile_rows - 1) / tile_rows;     // tiles per block
     const long long per_job = (long long)g.num_layers * g.nb_max * tpb;
     const long long n_items = (long long)g.n_jobs * per_job;
     const size_t re = (size_t)g.row_elems;
 
     if (tid == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full[i], 32);                        // every producer lane arrives
+            mbar_init(&empty[i], kRowsConsumers / 32);      // one arrive per consumer warp
+        }
         fence_mbar_init();
     }
     __syncthreads();
 
-    struct Item {
-        int ji, layer, b, lo, n;
-    };
-    auto decode = [&](long long it, Item& x) -> bool {
-        x.ji = (int)(it / per_job);
-        long long rem = it - (long long)x.ji * per_job;
-        const int per_layer = g.nb_max * tpb;
-        x.layer = (int)(rem / per_layer);
-        const int r2 = (int)(rem - (long long)x.layer * per_layer);
-        x.b = r2 / tpb;
-        const int sub = r2 - x.b * tpb;
-        const int T_ = __ldg(&jobs[x.ji].num_tokens);
-        const int blo = x.b * g.block_size;
-        const int bhi = min(blo + g.block_size, T_);
-        x.lo = blo + sub * tile_rows;
-        x.n = min(tile_rows, bhi - x.lo);
-        return x.n > 0;
-    };
-    auto next_valid = [&](long long it, Item& x) -> long long {
-        while (it < n_items && !decode(it, x)) it += gridDim.x;
-        return it;
-    };
-    // thread 0 only: stage an item's K (and V) rows into buffer ``bi``
-    auto issue = [&](const Item& x, int bi) {
-        const tdkv_rows_job* job = jobs + x.ji;
-        const int T_ = job->num_tokens;
-        const int nbj = (T_ + g.block_size - 1) / g.block_size;
-        const int mk_i = job->map_k ? job->map_k[x.layer * nbj + x.b] : -1;
-        const int mv_i = job->map_v ? job->map_v[x.layer * nbj + x.b] : -1;
-        const int in_blk = x.lo - x.b * g.block_size;
-        const T* ks = mk_i >= 0
-            ? static_cast<const T*>(job->pay_k) + ((size_t)mk_i * g.block_size + in_blk) * re
-            : static_cast<const T*>(job->src_k) + (size_t)x.layer * job->src_layer_stride + (size_t)x.lo * re;
-        const uint32_t bytes = (uint32_t)x.n * row_bytes;
-        uint8_t* dst = smem + (size_t)bi * 2 * tile_bytes;
-        const bool has_v = job->dst_v != nullptr;
-        mbar_arrive_expect_tx(&bars[bi], (has_v ? 2u : 1u) * bytes);
-        bulk_g2s(dst, ks, bytes, &bars[bi]);
-        if (has_v) {
-            const T* vs = mv_i >= 0
-                ? static_cast<const T*>(job->pay_v) + ((size_t)mv_i * g.block_size + in_blk) * re
-                : static_cast<const T*>(job->src_v) + (size_t)x.layer * job->src_layer_stride + (size_t)x.lo * re;
-            bulk_g2s(dst + tile_bytes, vs, bytes, &bars[bi]);
+    if (warp == kRowsConsumers / 32) {                      // ---- producer warp
+        int k = 0;
+        for (long long it = blockIdx.x;; it += gridDim.x) {
+            // next valid item (tiles past a job's last token are skipped)
+            int ji = 0, layer = 0, b = 0, lo = 0, n = 0, T_ = 0;
+            const tdkv_rows_job* job = nullptr;
+            for (; it < n_items; it += gridDim.x) {
+                ji = (int)(it / per_job);
+                const long long rem = it - (long long)ji * per_job;
+                const int per_layer = g.nb_max * tpb;
+                layer = (int)(rem / per_layer);
+                const int r2 = (int)(rem - (long long)layer * per_layer);
+                b = r2 / tpb;
+                job = jobs + ji;
+                T_ = job->num_tokens;
+                const int blo = b * g.block_size;
+                lo = blo + (r2 - b * tpb) * tile_rows;
+                n = min(tile_rows, min(blo + g.block_size, T_) - lo);
+                if (n > 0) break;
+            }
+            const int st = k % S;
+            if (k >= S) mbar_wait(&empty[st], (uint32_t)((k / S - 1) & 1));
+            if (it >= n_items) {                             // sentinel: consumers stop
+                if (lane == 0) s_it[st].valid = 0;
+                __syncwarp();
+                mbar_arrive(&full[st]);
+                break;
+            }
+            const int nbj = (T_ + g.block_size - 1) / g.block_size;
+            if (lane < n) s_drow[st][lane] = job->dst_rows ? __ldg(job->dst_rows + lo + lane) : lo + lane;
+            if (lane == 0) {
+                const int mk_i = job->map_k ? job->map_k[layer * nbj + b] : -1;
+                const int mv_i = job->map_v ? job->map_v[layer * nbj + b] : -1;
+                const int in_blk = lo - b * g.block_size;
+                const T* ks = mk_i >= 0
+                    ? static_cast<const T*>(job->pay_k) + ((size_t)mk_i * g.block_size + in_blk) * re
+                    : static_cast<const T*>(job->src_k) + (size_t)layer * job->src_layer_stride + (size_t)lo * re;
+                RowsItem& o = s_it[st];
+                o.valid = 1;
+                o.lo = lo;
+                o.n = n;
+                o.rotate = job->rotate;
+                o.tbl_row = job->tbl_row;
+                o.tbl_stride = job->tbl_stride;
+                o.dk = static_cast<T*>(job->dst_k) + (size_t)layer * job->dst_layer_stride;
+                o.dv = job->dst_v ? static_cast<T*>(job->dst_v) + (size_t)layer * job->dst_layer_stride
+                                  : nullptr;
+                const uint32_t bytes = (uint32_t)n * row_bytes;
+                uint8_t* dst = smem + (size_t)st * 2 * tile_bytes;
+                fence_proxy_async_smem();                    // consumers' reads of this stage done
+                mbar_arrive_expect_tx(&full[st], (job->dst_v ? 2u : 1u) * bytes);
+                bulk_g2s(dst, ks, bytes, &full[st]);
+                if (job->dst_v) {
+                    const T* vs = mv_i >= 0
+                        ? static_cast<const T*>(job->pay_v) + ((size_t)mv_i * g.block_size + in_blk) * re
+                        : static_cast<const T*>(job->src_v) + (size_t)layer * job->src_layer_stride + (size_t)lo * re;
+                    bulk_g2s(dst + tile_bytes, vs, bytes, &full[st]);
+                }
+            } else {
+                mbar_arrive(&full[st]);
+            }
+            ++k;
         }
-    };
+        return;
+    }
 
-    // the tile's destination rows are staged in shared memory with cp.async
-    // (issued with the next tile's bulk copy), so the scatter loop never
-    // waits on a dependent global load
-    __shared__ __align__(16) int64_t s_drow[2][32];
-    auto stage_rows = [&](const Item& x, int b) {
-        const int64_t* dr = jobs[x.ji].dst_rows;
-        if (tid < x.n) {
-            if (dr) cp_async_8(&s_drow[b][tid], dr + x.lo + tid);
-            else s_drow[b][tid] = x.lo + tid;
-        }
-        cp_async_commit();
-    };
-
-    Item cur, nxt;
-    long long it = next_valid(blockIdx.x, cur);
-    if (tid == 0 && it < n_items) issue(cur, 0);
-    if (it < n_items) stage_rows(cur, 0);
-    uint32_t phase0 = 0, phase1 = 0;
-    int bi = 0;
-    while (it < n_items) {
-        const long long nx = next_valid(it + gridDim.x, nxt);
-        if (tid == 0 && nx < n_items) {
-            fence_proxy_async_smem();
-            issue(nxt, bi ^ 1);
-        }
-        if (nx < n_items) {
-            stage_rows(nxt, bi ^ 1);
-            cp_async_wait<1>();            // this tile's rows (the older group) landed
-        } else {
-            cp_async_wait<0>();
-        }
-        mbar_wait(&bars[bi], bi ? phase1 : phase0);
-        if (bi) phase1 ^= 1u; else phase0 ^= 1u;
-        __syncthreads();                   // staged rows visible to every thread
-
-        const tdkv_rows_job* job = jobs + cur.ji;
-        const V* sk = reinterpret_cast<const V*>(smem + (size_t)bi * 2 * tile_bytes);
-        const V* sv = reinterpret_cast<const V*>(smem + (size_t)bi * 2 * tile_bytes + tile_bytes);
-        T* dk = static_cast<T*>(job->dst_k) + (size_t)cur.layer * job->dst_layer_stride;
-        T* dv = static_cast<T*>(job->dst_v) + (size_t)cur.layer * job->dst_layer_stride;
-        const bool has_v = job->dst_v != nullptr;
-        const int rotate = job->rotate, tbl_row = job->tbl_row, tbl_stride = job->tbl_stride;
+    // ---- consumer warps 0-7
+    const int tx_n = upr < kRowsConsumers ? upr : kRowsConsumers;
+    const int rows_per_pass = kRowsConsumers / tx_n;
+    const int tx = tid % tx_n, ty = tid / tx_n;
+    for (int k = 0;; ++k) {
+        const int st = k % S;
+        mbar_wait(&full[st], (uint32_t)((k / S) & 1));
+        const RowsItem x = s_it[st];
+        if (!x.valid) break;
+        const V* sk = reinterpret_cast<const V*>(smem + (size_t)st * 2 * tile_bytes);
+        const V* sv = reinterpret_cast<const V*>(smem + (size_t)st * 2 * tile_bytes + tile_bytes);
+        T* dk = static_cast<T*>(x.dk);
+        T* dv = static_cast<T*>(x.dv);
+        const bool has_v = dv != nullptr;
         if (ty < rows_per_pass) {
             for (int c = tx; c < upr; c += tx_n) {
                 const int j0 = ((c * kEpu) % g.head_dim) >> 1;
                 Tbl cs[kPairs];
-                if (rotate && tbl_stride == 0) {
-                    const Tbl* trow = table + (size_t)tbl_row * half + j0;
+                if (x.rotate && x.tbl_stride == 0) {
+                    const Tbl* trow = table + (size_t)x.tbl_row * half + j0;
 #pragma unroll
                     for (int q = 0; q < kPairs; ++q) cs[q] = __ldg(trow + q);
                 }
-                for (int r = ty; r < cur.n; r += rows_per_pass) {
-                    const int t = cur.lo + r;
-                    const int64_t drow = s_drow[bi][r];
+                for (int r = ty; r < x.n; r += rows_per_pass) {
+                    const int64_t drow = s_drow[st][r];
                     V kx = sk[r * upr + c];
-                    if (rotate) {
-                        if (tbl_stride != 0) {
-                            const Tbl* trow = table + (size_t)(tbl_row + t * tbl_stride) * half + j0;
+                    if (x.rotate) {
+                        if (x.tbl_stride != 0) {
+                            const Tbl* trow =
+                                table + (size_t)(x.tbl_row + (x.lo + r) * x.tbl_stride) * half + j0;
 #pragma unroll
                             for (int q = 0; q < kPairs; ++q) cs[q] = __ldg(trow + q);
                         }
@@ -279,31 +288,43 @@ __global__ void __launch_bounds__(256)
                 }
             }
         }
-        __syncthreads();
-        it = nx;
-        cur = nxt;
-        bi ^= 1;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);              // this warp is done with the stage
     }
 }
 
-template <typename T>
-static int32_t launch_rows_tma(const tdkv_rows_job* jobs, const void* table, const RowsGeom& g,
-                               int tile_rows, int grid_limit, cudaStream_t s) {
-    auto kern = rows_tma_kernel<T>;
-    const size_t smem = (size_t)4 * tile_rows * g.row_elems * sizeof(T);
+template <typename T, int S>
+static int32_t launch_rows_tma_s(const tdkv_rows_job* jobs, const void* table, const RowsGeom& g,
+                                 int tile_rows, int grid_limit, cudaStream_t s) {
+    auto kern = rows_tma_kernel<T, S>;
+    const size_t smem = (size_t)2 * S * tile_rows * g.row_elems * sizeof(T);
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
         return check_launch("tdkv_rows: cudaFuncSetAttribute");
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRowsConsumers + 32, smem);
     if (per_sm < 1) per_sm = 1;
     const int tpb = (g.block_size + tile_rows - 1) / tile_rows;
     const long long items = (long long)g.n_jobs * g.num_layers * g.nb_max * tpb;
     long long grid = (long long)sm_count() * per_sm;
     if (grid_limit > 0 && grid > grid_limit) grid = grid_limit;
     if (grid > items) grid = items;
-    kern<<<(unsigned)grid, 256, smem, s>>>(jobs, table, g, tile_rows);
+    kern<<<(unsigned)grid, kRowsConsumers + 32, smem, s>>>(jobs, table, g, tile_rows);
     return TDKV_OK;
+}
+
+// ring depth: TDKV_ROWS_STAGES (2-4, default 2) stages of tile_rows K+V rows
+template <typename T>
+static int32_t launch_rows_tma(const tdkv_rows_job* jobs, const void* table, const RowsGeom& g,
+                               int tile_rows, int grid_limit, cudaStream_t s) {
+    static const int stages = [] {
+        const char* e = getenv("TDKV_ROWS_STAGES");
+        const int v = e ? atoi(e) : 2;
+        return v < 2 ? 2 : v > 4 ? 4 : v;
+    }();
+    if (stages == 4) return launch_rows_tma_s<T, 4>(jobs, table, g, tile_rows, grid_limit, s);
+    if (stages == 3) return launch_rows_tma_s<T, 3>(jobs, table, g, tile_rows, grid_limit, s);
+    return launch_rows_tma_s<T, 2>(jobs, table, g, tile_rows, grid_limit, s);
 }
 
 template <typename T>
