@@ -432,6 +432,25 @@ def run_tdkv(args):
     if exchange is not None:
         line["exchange"] = exchange
 
+    # -- the same rounds replayed from a captured CUDA graph (N=1) -----------
+    if world == 1 and len(plans) == 1 and not args.profile:
+        graph = collector.capture(plan)
+        for _ in range(args.warmup):
+            graph.replay()
+        torch.cuda.synchronize(dev)
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(args.steps):
+            graph.replay()
+        g1.record(stream)
+        torch.cuda.synchronize(dev)
+        g_ms = g0.elapsed_time(g1) / args.steps
+        line["graph"] = {"value": round(step_bytes / (g_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+                         "ms_per_step": round(g_ms, 4), "kernels_per_replay": graph.kernels,
+                         "note": "KVCollector.capture(plan): the round (K0 + K1) as one CUDA "
+                                 "graph, replayed; not counted in gpu_launches"}
+        del graph
+
     # -- e2e: public API with host buffers ---------------------------------
     if len(batches) > 1 and not args.no_e2e:
         line["e2e_note"] = ("e2e measured for single-sub-batch shards only (this shard is "

@@ -8,7 +8,7 @@ kernels in ``libtdkv.so`` (C-ABI: include/tdkv.h); there is no CPU
 fallback -- without the library or a CUDA device the entry points raise.
 """
 from ._lib import TdkvError, TdkvUnavailable, build_library, launch_count
-from .collector import (CollectJob, CollectPlan, KVCollector, MasterArena, RoundPipeline,
+from .collector import (CollectJob, CollectPlan, KVCollector, MasterArena, RoundGraph, RoundPipeline,
                         SlotArena, align_cached, skeleton_values)
 from .core import CacheBlockConfig, LayeredKv, PositionSpan, kv_dense_nbytes
 from .diffstore import (BlockSparseDiff, CompressionStats, DiffStore, FamilyEncoding,
@@ -36,7 +36,7 @@ __all__ = [
     "CostLedger", "DiffStore", "FamilyEncoding", "HintSoundnessError", "KVCollector",
     "LayerDiff", "LayeredKv", "MalformedDiffError", "MasterArena", "MasterEntry",
     "MirrorHandle", "OutOfSlotsError", "PagedPool", "PinnedMasterError", "PositionSpan",
-    "RoundPipeline", "SlotArena", "SlotMap", "TdkvError", "TdkvUnavailable", "UseAfterFreeError", "align_cached", "gemm_tn", "RecoveryResult", "ReusePlan",
+    "RoundGraph", "RoundPipeline", "SlotArena", "SlotMap", "TdkvError", "TdkvUnavailable", "UseAfterFreeError", "align_cached", "gemm_tn", "RecoveryResult", "ReusePlan",
     "collective_recover", "probe_and_select", "recover_prepared", "ToyModel", "full_prefill",
     "recompute_positions", "refresh", "selective_forward", "batched_selection", "key_diff",
     "mirror_hint_positions", "recompute_budget", "select_important", "select_master",

@@ -379,6 +379,10 @@ class KVCollector:
     def plan(self, jobs: Sequence[CollectJob]) -> CollectPlan:
         return CollectPlan(self.arena, jobs, self.rope_base, self.tile_rows, self.pool.device)
 
+    def capture(self, plan: CollectPlan) -> "RoundGraph":
+        """The round as a replayable CUDA graph (see RoundGraph)."""
+        return RoundGraph(self, plan)
+
     def plan_members(self, members, segment_of) -> CollectPlan:
         """Jobs from reference-shaped requests: ``members[i].hits`` (each with
         ``.target_idx`` and ``.delta``) and ``members[i].slot_map``;
@@ -451,6 +455,32 @@ class KVCollector:
         """Collect a round whose master blocks arrive from (pinned) host memory."""
         events = self.stage_from_host(host_k, host_v, chunks, copy_stream)
         return self.collect_staged(plan, events, ledger)
+
+
+class RoundGraph:
+    """A planned round captured once as a CUDA graph (K0 + K1 with every
+    pointer and size baked in).  ``replay()`` re-runs the round on the
+    current stream -- on whatever the arena holds at that moment -- with one
+    graph launch instead of the per-kernel launch path; for small rounds
+    (C1: two kernels, 38 us) the launch overhead is a visible share."""
+
+    def __init__(self, collector: "KVCollector", plan: CollectPlan) -> None:
+        self.collector = collector
+        self.plan = plan                 # keeps the descriptor buffers alive
+        device = collector.pool.device
+        side = torch.cuda.Stream(device)
+        side.wait_stream(torch.cuda.current_stream(device))
+        with torch.cuda.stream(side):    # first launches outside capture (attributes set)
+            collector.collect(plan)
+        torch.cuda.current_stream(device).wait_stream(side)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.kernels = collector.collect(plan)
+
+    def replay(self) -> int:
+        """Run the captured round; returns the kernels it launches."""
+        self.graph.replay()
+        return self.kernels
 
 
 class RoundPipeline:

@@ -576,3 +576,30 @@ def test_slot_arena_planning_equals_row_planning():
         col.collect(plan)
         pools.append((pool.k.clone(), pool.v.clone()))
     assert torch.equal(pools[0][0], pools[1][0]) and torch.equal(pools[0][1], pools[1][1])
+
+
+def test_round_graph_replay_equals_eager_collect():
+    """A captured round (CUDA graph: K0 + K1) replays to the same pool bytes
+    as the eager launches, and reads the arena at replay time."""
+    spec = rounds.CONFIGS["c2"].scaled(num_layers=3, num_agents=5, num_segments=4, hist_len=33)
+    mk, mv = rounds.master_planes_host(spec)
+    dt = spec.torch_dtype
+    dev = torch.device("cuda", 0)
+    arena = rounds.make_arena(spec, torch.from_numpy(mk).to(dev).to(dt),
+                              torch.from_numpy(mv).to(dev).to(dt))
+    T = spec.tokens_per_agent
+    pools = []
+    for _ in range(2):
+        pool = tk.PagedPool(spec.num_agents * T, spec.num_layers, spec.num_heads, spec.head_dim,
+                            dtype=dt, device=dev)
+        maps = [pool.allocate(T, a) for a in range(spec.num_agents)]
+        jobs = [j for a, m in enumerate(maps) for j in rounds.agent_jobs(spec, a, m.slots)]
+        pools.append((pool, tk.KVCollector(arena, pool), jobs))
+    (pa, ca, ja), (pb, cb, jb) = pools
+    graph = cb.capture(cb.plan(jb))
+    for step in range(3):
+        arena.k.mul_(-1) if step else None          # new master contents every round
+        ca.collect(ca.plan(ja))
+        assert graph.replay() == 2
+        torch.cuda.synchronize()
+        assert torch.equal(pa.k, pb.k) and torch.equal(pa.v, pb.v), step
