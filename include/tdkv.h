@@ -104,6 +104,29 @@ int32_t tdkv_collect(const void* d_master_k, const void* d_master_v,
 /* d_master_v == d_dst_v == NULL makes a K-only collect (align_cached alone;
  * the reference copies V in _skeleton). */
 
+/* K1 over several master sources: the All-Gather round fused with the
+ * collector.  Replaces the exchange the reference does not have
+ * (every segment master sits in one process, trace.py:161-184) followed by
+ * align_cached (pic.py:208-235) + the _skeleton V copy (pic.py:203-204) +
+ * write_rows (paged_pool.py:150-156): unit u's master tile is read from
+ * source d_unit_src[u], whose K/V bases are h_src_k/h_src_v[d_unit_src[u]]
+ * (host arrays of n_src <= 16 device pointers, each an arena of the same
+ * layout -- typically a peer GPU's arena mapped over NVLink by CUDA IPC, or
+ * the local one).  Every other argument is tdkv_collect's; the tiles are
+ * TMA-staged from the peer straight into shared memory, so no received copy
+ * of the masters is ever written to local HBM.  All sources must be 16-byte
+ * aligned. */
+int32_t tdkv_collect_sources(const void* const* h_src_k, const void* const* h_src_v,
+                             int32_t n_src, const uint8_t* d_unit_src,
+                             int64_t master_layer_stride,
+                             const tdkv_collect_unit* d_units, int32_t n_units,
+                             int32_t max_rows,
+                             const tdkv_collect_job* d_jobs, const int64_t* d_dst_rows,
+                             const void* d_table, int32_t rotate,
+                             void* d_dst_k, void* d_dst_v, int64_t dst_layer_stride,
+                             int32_t num_layers, int32_t num_heads, int32_t head_dim,
+                             int32_t dtype, int32_t grid_limit, void* stream);
+
 /* ------------------------------------------------------------------------
  * K2  block-diff encoder.  Replaces diffstore.encode_diff
  * (diffstore.py:119-182) for a batch of (master, mirror) pairs of identical

@@ -92,7 +92,7 @@ assert DIFF_PAIR.itemsize == 32 and DIFF_OUT.itemsize == 40 and ROWS_JOB.itemsiz
 
 EXPORTS = (
     "tdkv_version", "tdkv_last_error", "tdkv_launch_count", "tdkv_rope_table",
-    "tdkv_collect", "tdkv_diff_compare", "tdkv_diff_compact", "tdkv_diff_encode", "tdkv_rows",
+    "tdkv_collect", "tdkv_collect_sources", "tdkv_diff_compare", "tdkv_diff_compact", "tdkv_diff_encode", "tdkv_rows",
     "tdkv_keydiff", "tdkv_select_important", "tdkv_gemm", "tdkv_qkv_rope", "tdkv_attention",
     "tdkv_fill_rows", "tdkv_alloc_create", "tdkv_alloc_destroy", "tdkv_alloc_free_count",
     "tdkv_alloc_take", "tdkv_alloc_release", "tdkv_wire_pack", "tdkv_wire_unpack",
@@ -111,6 +111,8 @@ _SIGS = {
     "tdkv_rope_table": (_I32, [_P, _I64, _P, _I32, _I32, _P, _P]),
     "tdkv_collect": (_I32, [_P, _P, _I64, _P, _I32, _I32, _P, _P, _P, _I32, _P, _P, _I64,
                             _I32, _I32, _I32, _I32, _I32, _P]),
+    "tdkv_collect_sources": (_I32, [_P, _P, _I32, _P, _I64, _P, _I32, _I32, _P, _P, _P, _I32,
+                                    _P, _P, _I64, _I32, _I32, _I32, _I32, _I32, _P]),
     "tdkv_diff_compare": (_I32, [_P, _I32, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32,
                                  _I32, _P]),
     "tdkv_diff_compact": (_I32, [_P, _P, _I32, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32,

@@ -17,6 +17,7 @@ copies it into the pool later (trace.py:148-152); both forms are provided:
 """
 from __future__ import annotations
 
+import ctypes
 import math
 import os
 from dataclasses import dataclass
@@ -224,6 +225,24 @@ def plan_host_offsets(seg_row0: np.ndarray, seg_len: np.ndarray, segments: np.nd
     return HostPlan(units, jobs, None, job_delta, bool(job_delta.any()), total, master_rows)
 
 
+def unit_sources(unit_row0: np.ndarray, seg_row0: np.ndarray, seg_len: np.ndarray,
+                 seg_source: np.ndarray) -> np.ndarray:
+    """uint8 source of each collect unit: the source of the segment whose row
+    range [seg_row0[s], seg_row0[s] + seg_len[s]) holds the unit's first row."""
+    seg_row0 = np.asarray(seg_row0, np.int64)
+    seg_len = np.asarray(seg_len, np.int64)
+    seg_source = np.asarray(seg_source, np.int64)
+    if seg_source.size and (seg_source.min() < 0 or seg_source.max() > 255):
+        raise ValueError("segment sources must be in [0, 255]")
+    live = np.flatnonzero(seg_len > 0)
+    order = live[np.argsort(seg_row0[live], kind="stable")]
+    r0 = np.asarray(unit_row0, np.int64)
+    pos = np.searchsorted(seg_row0[order], r0, side="right") - 1
+    if r0.size and (pos.min() < 0 or np.any(r0 >= seg_row0[order[pos]] + seg_len[order[pos]])):
+        raise ValueError("a unit lies outside every segment")
+    return seg_source[order[pos]].astype(np.uint8)
+
+
 class SlotArena:
     """The agents' slot maps concatenated and resident on the device (pool
     state, uploaded once at admission): a collect job then only names its
@@ -349,6 +368,37 @@ class CollectPlan:
                   self.tile_rows, ptr(self.d_jobs), ptr(self.d_dst_rows),
                   ptr(self.table) if self.rotate else 0, int(self.rotate), ptr(dst_k) + d_off,
                   ptr(dst_v) + d_off if with_v else 0, int(dst_layer_stride), l1 - l0,
+                  self.num_heads, self.head_dim, dtype_code(self.kv_dtype), int(grid_limit),
+                  stream_handle(self.device))
+        return 1
+
+    def unit_sources(self, seg_source: np.ndarray, seg_row0: np.ndarray,
+                     seg_len: np.ndarray) -> np.ndarray:
+        """Source index of every unit (see ``unit_sources``)."""
+        return unit_sources(self.units_host["row0"], seg_row0, seg_len, seg_source)
+
+    def launch_collect_sources(self, sources: Sequence[MasterArena], d_unit_src: torch.Tensor,
+                               dst_k: torch.Tensor, dst_v: Optional[torch.Tensor],
+                               dst_layer_stride: int, grid_limit: int = 0) -> int:
+        """K1 over every layer, unit u's tile read from ``sources[unit_src[u]]``
+        (arenas of identical layout: the local one or peer GPUs' arenas
+        mapped over NVLink); ``d_unit_src`` from ``unit_sources``."""
+        if not sources or any(a.k.shape != sources[0].k.shape or a.k.dtype != self.kv_dtype
+                              for a in sources):
+            raise ValueError("sources must be arenas of one layout and the plan's dtype")
+        if dst_k.dtype != self.kv_dtype:
+            raise ValueError("destination and plan dtypes differ")
+        if self.num_jobs == 0:
+            return 0
+        with_v = dst_v is not None
+        n = len(sources)
+        src_k = (ctypes.c_void_p * n)(*[ptr(a.k) for a in sources])
+        src_v = (ctypes.c_void_p * n)(*[ptr(a.v) for a in sources])
+        _lib.call("tdkv_collect_sources", src_k, src_v if with_v else None, n, ptr(d_unit_src),
+                  sources[0].layer_stride, ptr(self.d_units), int(self.units_host.size),
+                  self.tile_rows, ptr(self.d_jobs), ptr(self.d_dst_rows),
+                  ptr(self.table) if self.rotate else 0, int(self.rotate), ptr(dst_k),
+                  ptr(dst_v) if with_v else 0, int(dst_layer_stride), self.num_layers,
                   self.num_heads, self.head_dim, dtype_code(self.kv_dtype), int(grid_limit),
                   stream_handle(self.device))
         return 1

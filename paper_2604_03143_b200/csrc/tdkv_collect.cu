@@ -40,6 +40,8 @@ __global__ void rope_table_kernel(const int64_t* __restrict__ deltas, int64_t n_
 // ---------------------------------------------------------------------------
 // K1
 
+constexpr int kMaxSources = 16;
+
 struct CollectParams {
     const void* mk;
     const void* mv;
@@ -58,6 +60,12 @@ struct CollectParams {
     int32_t head_dim;
     int32_t row_elems;
     int32_t v_bulk;              // V rows leave by TMA bulk stores straight from the tile
+    // multi-source rounds (tdkv_collect_sources): unit u's master tile is read
+    // from source unit_src[u] -- a peer GPU's arena over NVLink, or the local
+    // one -- instead of mk/mv; every source shares the arena layout
+    const uint8_t* unit_src;
+    const void* src_k[kMaxSources];
+    const void* src_v[kMaxSources];
 };
 
 // Per-job destination metadata is staged in shared memory in groups of
@@ -111,10 +119,18 @@ __global__ void __launch_bounds__(256) collect_kernel(const CollectParams p) {
     // neighbouring tiles of one layer plane
     auto stage_src = [&](int item, const T*& gk, const T*& gv, tdkv_collect_unit& u) {
         const int layer = item / p.n_units;
-        u = p.units[item - layer * p.n_units];
+        const int ui = item - layer * p.n_units;
+        u = p.units[ui];
         const size_t off = (size_t)layer * p.mls + (size_t)u.row0 * p.row_elems;
-        gk = static_cast<const T*>(p.mk) + off;
-        gv = static_cast<const T*>(p.mv) + off;
+        const void* bk = p.mk;
+        const void* bv = p.mv;
+        if (p.unit_src) {
+            const int src = p.unit_src[ui];
+            bk = p.src_k[src];
+            bv = p.src_v[src];
+        }
+        gk = static_cast<const T*>(bk) + off;
+        gv = static_cast<const T*>(bv) + off;
     };
     auto stage_meta = [&](const tdkv_collect_unit& u, int g, int mb) {
         const int jbase = u.job_begin + g * kJobGroup;
@@ -317,13 +333,15 @@ extern "C" int32_t tdkv_rope_table(const int64_t* d_deltas, int64_t n_rows,
     return check_launch("tdkv_rope_table");
 }
 
-extern "C" int32_t tdkv_collect(const void* d_master_k, const void* d_master_v,
-                                int64_t master_layer_stride, const tdkv_collect_unit* d_units,
-                                int32_t n_units, int32_t max_rows, const tdkv_collect_job* d_jobs,
-                                const int64_t* d_dst_rows, const void* d_table, int32_t rotate,
-                                void* d_dst_k, void* d_dst_v, int64_t dst_layer_stride,
-                                int32_t num_layers, int32_t num_heads, int32_t head_dim,
-                                int32_t dtype, int32_t grid_limit, void* stream) {
+static int32_t collect_impl(const void* d_master_k, const void* d_master_v,
+                            int64_t master_layer_stride, const tdkv_collect_unit* d_units,
+                            int32_t n_units, int32_t max_rows, const tdkv_collect_job* d_jobs,
+                            const int64_t* d_dst_rows, const void* d_table, int32_t rotate,
+                            void* d_dst_k, void* d_dst_v, int64_t dst_layer_stride,
+                            int32_t num_layers, int32_t num_heads, int32_t head_dim,
+                            int32_t dtype, int32_t grid_limit, void* stream,
+                            const uint8_t* d_unit_src, const void* const* h_src_k,
+                            const void* const* h_src_v, int32_t n_src) {
     if (n_units < 0 || num_layers <= 0 || num_heads <= 0 || head_dim <= 0 || (head_dim & 1))
         return set_error(TDKV_EINVAL, "tdkv_collect: bad geometry L=%d H=%d D=%d", num_layers,
                          num_heads, head_dim);
@@ -353,6 +371,11 @@ extern "C" int32_t tdkv_collect(const void* d_master_k, const void* d_master_v,
     p.num_layers = num_layers;
     p.head_dim = head_dim;
     p.row_elems = num_heads * head_dim;
+    p.unit_src = d_unit_src;
+    for (int i = 0; i < kMaxSources; ++i) {
+        p.src_k[i] = i < n_src ? h_src_k[i] : nullptr;
+        p.src_v[i] = i < n_src && h_src_v ? h_src_v[i] : nullptr;
+    }
     static const bool v_bulk_env = [] {
         const char* e = getenv("TDKV_COLLECT_V_BULK");
         return !(e && e[0] == '0');
@@ -384,4 +407,49 @@ extern "C" int32_t tdkv_collect(const void* d_master_k, const void* d_master_v,
                     : launch_collect<__nv_bfloat16, 16, false>(p, grid_limit, s);
     return bulk ? launch_collect<__nv_bfloat16, 4, true>(p, grid_limit, s)
                 : launch_collect<__nv_bfloat16, 4, false>(p, grid_limit, s);
+}
+
+extern "C" int32_t tdkv_collect(const void* d_master_k, const void* d_master_v,
+                                int64_t master_layer_stride, const tdkv_collect_unit* d_units,
+                                int32_t n_units, int32_t max_rows, const tdkv_collect_job* d_jobs,
+                                const int64_t* d_dst_rows, const void* d_table, int32_t rotate,
+                                void* d_dst_k, void* d_dst_v, int64_t dst_layer_stride,
+                                int32_t num_layers, int32_t num_heads, int32_t head_dim,
+                                int32_t dtype, int32_t grid_limit, void* stream) {
+    return collect_impl(d_master_k, d_master_v, master_layer_stride, d_units, n_units, max_rows,
+                        d_jobs, d_dst_rows, d_table, rotate, d_dst_k, d_dst_v, dst_layer_stride,
+                        num_layers, num_heads, head_dim, dtype, grid_limit, stream, nullptr,
+                        nullptr, nullptr, 0);
+}
+
+extern "C" int32_t tdkv_collect_sources(const void* const* h_src_k, const void* const* h_src_v,
+                                        int32_t n_src, const uint8_t* d_unit_src,
+                                        int64_t master_layer_stride,
+                                        const tdkv_collect_unit* d_units, int32_t n_units,
+                                        int32_t max_rows, const tdkv_collect_job* d_jobs,
+                                        const int64_t* d_dst_rows, const void* d_table,
+                                        int32_t rotate, void* d_dst_k, void* d_dst_v,
+                                        int64_t dst_layer_stride, int32_t num_layers,
+                                        int32_t num_heads, int32_t head_dim, int32_t dtype,
+                                        int32_t grid_limit, void* stream) {
+    if (n_src <= 0 || n_src > kMaxSources || !h_src_k || !d_unit_src)
+        return set_error(TDKV_EINVAL, "tdkv_collect_sources: %d sources (1..%d) and a unit "
+                         "source map are required", n_src, kMaxSources);
+    if ((h_src_v == nullptr) != (d_dst_v == nullptr))
+        return set_error(TDKV_EINVAL, "tdkv_collect_sources: null pointer");
+    // every source must pass the alignment tests the single-source launch
+    // makes on its master pointer: test them all through the first slot
+    const void* k0 = h_src_k[0];
+    const void* v0 = h_src_v ? h_src_v[0] : nullptr;
+    for (int i = 0; i < n_src; ++i) {
+        if (!h_src_k[i] || (h_src_v && !h_src_v[i]))
+            return set_error(TDKV_EINVAL, "tdkv_collect_sources: source %d is null", i);
+        if (!aligned(h_src_k[i], 16) || (h_src_v && !aligned(h_src_v[i], 16)))
+            return set_error(TDKV_EINVAL, "tdkv_collect_sources: source %d not 16-byte aligned",
+                             i);
+    }
+    return collect_impl(k0, v0, master_layer_stride, d_units, n_units, max_rows, d_jobs,
+                        d_dst_rows, d_table, rotate, d_dst_k, d_dst_v, dst_layer_stride,
+                        num_layers, num_heads, head_dim, dtype, grid_limit, stream, d_unit_src,
+                        h_src_k, h_src_v, n_src);
 }

@@ -61,6 +61,7 @@ def main():
     want = min(((float((a * 7919) % 13) / 4.0, a) for a in range(spec.num_agents)))[1]
     assert master == want, (master, want)
     check_sessions(rank, world, dev)
+    check_peer(rank, world, dev)
     dist.barrier()
     if rank == 0:
         print(f"dist_check ok: world={world} backend={backend}")
@@ -113,6 +114,55 @@ def check_sessions(rank, world, dev):
         rc.collect(rc.plan(jobs))
         torch.cuda.synchronize(dev)
         assert torch.equal(pool.k, ref_pool.k) and torch.equal(pool.v, ref_pool.v), "sessions"
+
+
+def check_peer(rank, world, dev):
+    """Peer-read rounds (peer.PeerRound): each rank holds only the segments it
+    produced; K1 stages every other segment's tiles straight from the owner's
+    arena (CUDA IPC mapping; NVLink between GPUs, the same HBM when the ranks
+    share one GPU).  Two rounds with fresh masters check the ready/done
+    protocol; every rank's pool must equal a single-process collect."""
+    from paper_2604_03143_b200.peer import PeerRound, contiguous_owners
+    spec = rounds.CONFIGS["c2"].scaled(num_layers=4, num_agents=7, num_segments=5, hist_len=9)
+    dt = spec.torch_dtype
+    owners = contiguous_owners(spec.num_segments, world)
+    mk, mv = rounds.master_planes_host(spec)
+    k = torch.zeros(mk.shape, dtype=dt, device=dev)
+    v = torch.zeros(mv.shape, dtype=dt, device=dev)
+    arena = rounds.make_arena(spec, k, v)
+    agents = shard_range(spec.num_agents, rank, world)
+    T = spec.tokens_per_agent
+    pool = tk.PagedPool(len(agents) * T + 8, spec.num_layers, spec.num_heads, spec.head_dim,
+                        dtype=dt, device=dev)
+    maps = [pool.allocate(T, a) for a in agents]
+    jobs = [j for a, m in zip(agents, maps) for j in rounds.agent_jobs(spec, a, m.slots)]
+    col = tk.KVCollector(arena, pool)
+    plan = col.plan(jobs)
+    peer = PeerRound(col, owners)
+    for rnd in range(2):
+        full_k = torch.from_numpy(mk).to(dev).to(dt) * (1 + rnd)
+        full_v = torch.from_numpy(mv).to(dev).to(dt) - rnd
+        for s in range(spec.num_segments):        # this rank "produces" its segments
+            if owners[s] == rank:
+                r0 = int(arena.seg_row0[s])
+                r1 = r0 + int(arena.seg_len[s])
+                k[:, r0:r1] = full_k[:, r0:r1]
+                v[:, r0:r1] = full_v[:, r0:r1]
+        peer.round(plan)
+        torch.cuda.synchronize(dev)
+        truth = rounds.make_arena(spec, full_k, full_v)
+        ref_pool = tk.PagedPool(pool.capacity, spec.num_layers, spec.num_heads, spec.head_dim,
+                                dtype=dt, device=dev)
+        for a in agents:
+            ref_pool.allocate(T, a)
+        rc = tk.KVCollector(truth, ref_pool)
+        rc.collect(rc.plan(jobs))
+        torch.cuda.synchronize(dev)
+        assert torch.equal(pool.k, ref_pool.k) and torch.equal(pool.v, ref_pool.v), ("peer", rnd)
+    want = sum(int(arena.seg_len[s]) for s in range(spec.num_segments) if owners[s] != rank)
+    row = spec.num_heads * spec.head_dim * k.element_size()
+    assert peer.peer_bytes(plan) == 2 * spec.num_layers * row * want
+    dist.barrier()
 
 
 if __name__ == "__main__":

@@ -183,3 +183,24 @@ def test_session_owners_and_bytes():
         total = sum(spec.collector_bytes_for(rounds.shard(spec.num_agents, r, world))
                     for r in range(world))
         assert total >= spec.collector_bytes()
+
+
+def test_peer_unit_sources_follow_segment_owners():
+    """Peer-read rounds: every collect unit is read from the rank owning its
+    segment (host planning only; the IPC mapping and the multi-source K1 are
+    exercised by tests/test_gpu_dist.py)."""
+    from paper_2604_03143_b200.collector import _build_units, unit_sources
+    from paper_2604_03143_b200.peer import contiguous_owners
+    assert contiguous_owners(16, 8).tolist() == [0, 0, 1, 1, 2, 2, 3, 3, 4, 4, 5, 5, 6, 6, 7, 7]
+    assert contiguous_owners(5, 2).tolist() == [0, 0, 0, 1, 1]
+    seg_len = np.array([40, 0, 17, 256, 3], np.int64)
+    seg_row0 = np.concatenate([[0], np.cumsum(seg_len)[:-1]])
+    owners = np.array([1, 0, 0, 3, 2])
+    jobs_seg = np.sort(np.random.default_rng(0).choice([0, 2, 3, 4], 30))
+    units, _ = _build_units(seg_row0, seg_len, jobs_seg, 3, 8, 64)
+    src = unit_sources(units["row0"], seg_row0, seg_len, owners)
+    seg_of = np.searchsorted(np.cumsum(seg_len), units["row0"], side="right")
+    assert src.dtype == np.uint8
+    assert src.tolist() == owners[seg_of].tolist()
+    with pytest.raises(ValueError):
+        unit_sources(np.array([int(seg_len.sum())]), seg_row0, seg_len, owners)
