@@ -78,8 +78,9 @@ def h2d(arr: np.ndarray, device: Optional[torch.device] = None) -> torch.Tensor:
     bulk pageable copies."""
     device = device or default_device()
     src = torch.from_numpy(np.ascontiguousarray(arr))
-    if src.numel() < 4096:
-        return src.to(device)
+    # never .to(device) from pageable memory: torch follows that copy with a
+    # stream synchronize, which would stall the host behind every queued
+    # kernel (and serialize back-to-back rounds)
     return src.pin_memory().to(device, non_blocking=True)
 
 

@@ -12,7 +12,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._device import dtype_code, ptr, stream_handle, table_dtype, upload
+from ._device import dtype_code, h2d, ptr, stream_handle, table_dtype, upload
 
 ROWS_BLOCK = 32          # tiling of the row mover when no diff geometry applies
 
@@ -37,7 +37,7 @@ def rope_table(deltas: np.ndarray, head_dim: int, base: float, kv_dtype: torch.d
     out = torch.empty((max(n, 1), head_dim // 2, 2), dtype=tdt, device=device)
     if n == 0:
         return out
-    d_deltas = torch.from_numpy(deltas).to(device)
+    d_deltas = h2d(deltas, device)
     inv = _inv_freq_dev(device.index, head_dim, float(base))
     _lib.call("tdkv_rope_table", ptr(d_deltas), n, ptr(inv), head_dim // 2,
               dtype_code(kv_dtype), ptr(out), stream_handle(device))

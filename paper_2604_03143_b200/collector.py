@@ -253,7 +253,7 @@ class SlotArena:
         self.base = _excl_cumsum(lens)
         cat = (np.concatenate([np.asarray(m.slots, np.int64) for m in slot_maps])
                if slot_maps else np.zeros(0, np.int64))
-        self.rows = torch.from_numpy(cat).to(device)
+        self.rows = h2d(cat, device)
 
 
 class CollectPlan:

@@ -47,11 +47,6 @@ __global__ void __launch_bounds__(256)
     }
 }
 
-// One CTA per member, radix select on the magnitudes' bit patterns (a
-// non-negative float orders like its bits): four 8-bit passes find the
-// take-th largest value T; everything above T is selected, plus the
-// lowest-index elements equal to T (ties to the lower index); the flags are
-// then compacted in ascending index order.
 __device__ __forceinline__ int block_excl_scan(int v, int* s_warp, int& total) {
     // exclusive block scan of one int per thread (blockDim.x <= 1024)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -79,30 +74,58 @@ __device__ __forceinline__ int block_excl_scan(int v, int* s_warp, int& total) {
     return out;
 }
 
-__global__ void __launch_bounds__(512)
-    select_kernel(const float* __restrict__ mags, const int64_t* __restrict__ member_off,
-                  const int32_t* __restrict__ budget, int32_t* __restrict__ out_idx,
-                  int32_t* __restrict__ out_count, float* __restrict__ deviation) {
-    extern __shared__ __align__(16) uint32_t bits[];
-    __shared__ double red[32];
-    __shared__ int s_warp[33];
-    __shared__ int hist[256];
-    __shared__ int s_nnz, s_sel, s_rem;
-    const int m = blockIdx.x;
-    const int64_t off = member_off[m];
-    const int n = (int)(member_off[m + 1] - off);
+// ---------------------------------------------------------------------------
+// Selection of one member by one CTA: radix select on the magnitudes' bit
+// patterns (a non-negative float orders like its bits) -- four 8-bit passes
+// find the take-th largest value T; everything above T is selected, plus
+// the lowest-index elements equal to T (ties to the lower index), compacted
+// in ascending index order.  STAGED: the magnitudes are first copied into
+// shared memory (one pass over L2 with 16-byte loads).
+
+// bits(i): the magnitude's bit pattern, 0 for zero / NaN (never selected)
+__device__ __forceinline__ uint32_t mag_bits(float v) { return v > 0.f ? __float_as_uint(v) : 0u; }
+
+template <bool STAGED>
+__device__ __forceinline__ void select_member_global(const float* __restrict__ mags, int n,
+                                                     int budget, int32_t* __restrict__ out_idx,
+                                                     int32_t* out_count, float* deviation,
+                                                     int* hist, int* s_warp, double* red,
+                                                     int& s_nnz, int& s_sel, int& s_rem,
+                                                     uint32_t* staged) {
     const int tid = threadIdx.x, nthr = blockDim.x;
     if (tid == 0) s_nnz = 0;
     __syncthreads();
-
     double sum = 0.0;
     int nnz = 0;
-    for (int i = tid; i < n; i += nthr) {
-        const float v = mags[off + i];
-        sum += (double)v;
-        nnz += v > 0.f;
-        bits[i] = v > 0.f ? __float_as_uint(v) : 0u;
+    if (STAGED) {
+        // one pass over L2 with 16-byte loads; every later pass reads smem
+        const int n4 = ((reinterpret_cast<uintptr_t>(mags) & 15) == 0) ? n / 4 : 0;
+        for (int i = tid; i < n4; i += nthr) {
+            const float4 v = __ldcg(reinterpret_cast<const float4*>(mags) + i);
+            sum += (double)v.x;
+            sum += (double)v.y;
+            sum += (double)v.z;
+            sum += (double)v.w;
+            nnz += (v.x > 0.f) + (v.y > 0.f) + (v.z > 0.f) + (v.w > 0.f);
+            reinterpret_cast<uint4*>(staged)[i] =
+                make_uint4(mag_bits(v.x), mag_bits(v.y), mag_bits(v.z), mag_bits(v.w));
+        }
+        for (int i = 4 * n4 + tid; i < n; i += nthr) {
+            const float v = __ldcg(mags + i);
+            sum += (double)v;
+            nnz += v > 0.f;
+            staged[i] = mag_bits(v);
+        }
+    } else {
+        for (int i = tid; i < n; i += nthr) {
+            const float v = __ldcg(mags + i);
+            sum += (double)v;
+            nnz += v > 0.f;
+        }
     }
+    auto bits_at = [&](int i) -> uint32_t {
+        return STAGED ? staged[i] : mag_bits(__ldcg(mags + i));
+    };
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         sum += __shfl_xor_sync(0xffffffffu, sum, o);
@@ -116,25 +139,23 @@ __global__ void __launch_bounds__(512)
     if (tid == 0) {
         double acc = 0.0;
         for (int w = 0; w < (nthr >> 5); ++w) acc += red[w];
-        deviation[m] = (float)acc;
-        s_rem = min(budget[m], s_nnz);
+        *deviation = (float)acc;
+        s_rem = min(budget, s_nnz);
     }
     __syncthreads();
     const int take = s_rem;
     if (take <= 0) {
-        if (tid == 0) out_count[m] = 0;
+        if (tid == 0) *out_count = 0;
+        __syncthreads();
         return;
     }
-    // radix select of the take-th largest bit pattern
     uint32_t prefix = 0u, mask = 0u;
     for (int shift = 24; shift >= 0; shift -= 8) {
         for (int b = tid; b < 256; b += nthr) hist[b] = 0;
         __syncthreads();
-        // magnitudes cluster in a few exponent bins: aggregate same-bin lanes
-        // of a warp into one shared-memory atomic
         for (int base = 0; base < n; base += nthr) {
             const int i = base + tid;
-            const uint32_t x = i < n ? bits[i] : 0u;
+            const uint32_t x = i < n ? bits_at(i) : 0u;
             const bool live = i < n && (x & mask) == prefix;
             const unsigned bin = live ? (x >> shift) & 255u : 256u;
             const unsigned peers = __match_any_sync(0xffffffffu, bin);
@@ -142,7 +163,6 @@ __global__ void __launch_bounds__(512)
         }
         __syncthreads();
         if (tid < 32) {
-            // lane l owns bins 255-8l .. 248-8l (from the top)
             int c[8], local = 0;
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
@@ -157,14 +177,14 @@ __global__ void __launch_bounds__(512)
             }
             const int before = incl - local;
             const int rem = s_rem;
-            __syncwarp();                         // every lane has read s_rem before one rewrites it
+            __syncwarp();
             if (before < rem && incl >= rem) {
                 int acc = before;
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
                     if (acc + c[q] >= rem) {
                         s_sel = 255 - 8 * tid - q;
-                        s_rem = rem - acc;        // still needed inside the chosen bin
+                        s_rem = rem - acc;
                         break;
                     }
                     acc += c[q];
@@ -176,23 +196,54 @@ __global__ void __launch_bounds__(512)
         mask |= 255u << shift;
         __syncthreads();
     }
+    // keep everything above the threshold pattern plus the first need_eq
+    // elements equal to it (ties to the lower index), compacted ascending:
+    // each thread owns a contiguous run of indices, so two block scans place
+    // every kept index
     const uint32_t thr = prefix;
-    const int need_eq = s_rem;                     // elements equal to thr to keep
-    // pass over indices in ascending order: keep > thr, and the first
-    // need_eq elements == thr; then compact
-    int running_eq = 0, running = 0, total;
-    for (int base = 0; base < n; base += nthr) {
-        const int i = base + tid;
-        const uint32_t x = i < n ? bits[i] : 0u;
-        const int eq = (i < n && x == thr) ? 1 : 0;
-        const int eq_rank = running_eq + block_excl_scan(eq, s_warp, total);
-        running_eq += total;
-        const int keep = (i < n) && (x > thr || (eq && eq_rank < need_eq)) ? 1 : 0;
-        const int pos = running + block_excl_scan(keep, s_warp, total);
-        if (keep) out_idx[off + pos] = i;
-        running += total;
+    const int need_eq = s_rem;
+    const int per = (n + nthr - 1) / nthr;
+    const int i0 = min(n, tid * per), i1 = min(n, i0 + per);
+    int eq_cnt = 0;
+    for (int i = i0; i < i1; ++i) eq_cnt += bits_at(i) == thr;
+    int total;
+    const int eq_before = block_excl_scan(eq_cnt, s_warp, total);
+    int keep_cnt = 0, eqr = eq_before;
+    for (int i = i0; i < i1; ++i) {
+        const uint32_t x = bits_at(i);
+        if (x > thr) {
+            ++keep_cnt;
+        } else if (x == thr) {
+            keep_cnt += eqr < need_eq;
+            ++eqr;
+        }
     }
-    if (tid == 0) out_count[m] = take;
+    int pos = block_excl_scan(keep_cnt, s_warp, total);
+    eqr = eq_before;
+    for (int i = i0; i < i1; ++i) {
+        const uint32_t x = bits_at(i);
+        bool keep = x > thr;
+        if (x == thr) keep = eqr++ < need_eq;
+        if (keep) out_idx[pos++] = i;
+    }
+    if (tid == 0) *out_count = take;
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(512)
+    select_kernel(const float* __restrict__ mags, const int64_t* __restrict__ member_off,
+                  const int32_t* __restrict__ budget, int32_t* __restrict__ out_idx,
+                  int32_t* __restrict__ out_count, float* __restrict__ deviation) {
+    extern __shared__ __align__(16) uint32_t bits[];
+    __shared__ double red[32];
+    __shared__ int s_warp[33];
+    __shared__ int hist[256];
+    __shared__ int s_nnz, s_sel, s_rem;
+    const int m = blockIdx.x;
+    const int64_t off = member_off[m];
+    const int n = (int)(member_off[m + 1] - off);
+    select_member_global<true>(mags + off, n, budget[m], out_idx + off, out_count + m,
+                               deviation + m, hist, s_warp, red, s_nnz, s_sel, s_rem, bits);
 }
 
 }  // namespace tdkv
@@ -256,3 +307,4 @@ extern "C" int32_t tdkv_select_important(const float* d_mags, const int64_t* d_m
     count_launch();
     return check_launch("tdkv_select_important");
 }
+

@@ -28,7 +28,7 @@ import numpy as np
 import torch
 
 from . import _kernels, _lib
-from ._device import (default_device, dtype_code, is_host, ptr, stream_handle, to_device,
+from ._device import (default_device, dtype_code, h2d, is_host, ptr, stream_handle, to_device,
                       to_host, upload)
 from .core import CacheBlockConfig, LayeredKv
 
@@ -259,7 +259,7 @@ class BlockSparseDiff:
             shape = (max(off, 1), self.block_size, self.num_heads, self.head_dim)
             slab = torch.cat(blocks) if blocks else torch.zeros(shape, dtype=dtype, device=device)
             slabs.append(slab)
-            maps.append(torch.from_numpy(mp.reshape(-1)).to(device))
+            maps.append(h2d(mp.reshape(-1), device))
         d = _DeviceDiff(slabs[0], slabs[1], maps[0], maps[1])
         self._dev = d
         return d

@@ -23,7 +23,7 @@ import numpy as np
 import torch
 
 from . import _kernels
-from ._device import default_device, is_host, to_device, to_host
+from ._device import default_device, h2d, is_host, to_device, to_host
 
 
 class OutOfSlotsError(RuntimeError):
@@ -57,7 +57,7 @@ class SlotMap:
     def device_slots(self, device: torch.device) -> torch.Tensor:
         d = self._dev
         if d is None or d.device != device:
-            d = torch.from_numpy(self.slots).to(device)
+            d = h2d(self.slots, device)
             self._dev = d
         return d
 

@@ -55,23 +55,55 @@ def key_diff(fresh_k, cached_k):
     return out.cpu().numpy() if host else out
 
 
-def _select_device(mags: torch.Tensor, counts: Sequence[int], budgets: Sequence[int]):
-    counts = np.asarray(counts, np.int64)
-    off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+class _SelectPlan:
+    """Member offsets and budgets of one round shape, resident on the device
+    (uploaded once; rounds of the same shape reuse it)."""
+
+    def __init__(self, counts: Sequence[int], budgets: Sequence[int], device) -> None:
+        counts = np.asarray(counts, np.int64)
+        self.m = int(counts.size)
+        self.off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        self.total = int(self.off[-1])
+        self.max_count = int(counts.max(initial=0))
+        self.d_off = h2d(self.off, device)
+        self.d_budget = h2d(np.asarray(budgets, np.int32), device)
+
+
+_PLANS: Dict[tuple, _SelectPlan] = {}
+
+
+def _plan(counts: Sequence[int], device, budgets: Optional[Sequence[int]] = None,
+          fraction: Optional[float] = None) -> _SelectPlan:
+    """The resident plan of a round shape: budgets given, or ceil(r * n)."""
+    counts = tuple(int(c) for c in counts)
+    key = (device.index, counts, tuple(int(b) for b in budgets) if budgets is not None
+           else ("r", float(fraction)))
+    p = _PLANS.get(key)
+    if p is None:
+        if budgets is None:
+            budgets = [recompute_budget(fraction, n) for n in counts]
+        if len(_PLANS) >= 64:
+            _PLANS.clear()
+        p = _PLANS[key] = _SelectPlan(counts, budgets, device)
+    return p
+
+
+def _launch_select(mags: torch.Tensor, p: _SelectPlan):
     dev = mags.device
-    d_off = h2d(off, dev)
-    d_budget = h2d(np.asarray(budgets, np.int32), dev)
-    m = counts.size
+    m = p.m
     # one int32 buffer [counts | deviation bits | indices] -> a single D2H
-    buf = torch.empty(2 * m + max(int(off[-1]), 1), dtype=torch.int32, device=dev)
+    buf = torch.empty(2 * m + max(p.total, 1), dtype=torch.int32, device=dev)
     out_cnt = buf[:m]
     dev_sum = buf[m:2 * m].view(torch.float32)
     out_idx = buf[2 * m:]
     if m:
-        _lib.call("tdkv_select_important", ptr(mags), ptr(d_off), ptr(d_budget), m,
-                  int(counts.max(initial=0)), ptr(out_idx), ptr(out_cnt), ptr(dev_sum),
-                  stream_handle(dev))
-    return off, out_idx, out_cnt, dev_sum, buf
+        _lib.call("tdkv_select_important", ptr(mags), ptr(p.d_off), ptr(p.d_budget), m,
+                  p.max_count, ptr(out_idx), ptr(out_cnt), ptr(dev_sum), stream_handle(dev))
+    return p.off, out_idx, out_cnt, dev_sum, buf
+
+
+def _select_device(mags: torch.Tensor, counts: Sequence[int], budgets: Sequence[int]):
+    return _launch_select(mags, _plan(counts, mags.device, budgets=budgets))
 
 
 def select_important(magnitudes, budget: int) -> np.ndarray:
@@ -94,8 +126,7 @@ def selection_kernels(fresh: torch.Tensor, cached: torch.Tensor,
     Returns (member offsets, int32 result buffer [counts | deviation bits |
     indices])."""
     mags = _mags_device(fresh, cached, cached_rows)
-    budgets = [recompute_budget(fraction, n) for n in counts]
-    off, _, _, _, buf = _select_device(mags, counts, budgets)
+    off, _, _, _, buf = _launch_select(mags, _plan(counts, fresh.device, fraction=fraction))
     return off, buf
 
 
@@ -126,7 +157,11 @@ def batched_selection(fresh, cached, counts: Sequence[int], fraction: float,
     if ledger is not None:
         ledger.record_selection_pass()
     m = len(counts)
-    host = buf.cpu().numpy()
+    # results through pinned memory (a pageable D2H runs several times slower)
+    staged = torch.empty(buf.shape, dtype=buf.dtype, pin_memory=True)
+    staged.copy_(buf, non_blocking=True)
+    torch.cuda.current_stream(buf.device).synchronize()
+    host = staged.numpy()
     cnt_h = host[:m]
     sums = host[m:2 * m].view(np.float32)
     idx_h = host[2 * m:]

@@ -85,3 +85,28 @@ def test_bf16_keys():
     for (imp, dev), (lo, n) in zip(out, [(0, 100), (100, 200)]):
         mm = mags[lo:lo + n]
         assert imp.tolist() == ref.select_important(mm, ref.recompute_budget(0.15, n)).tolist()
+
+
+def test_ragged_members_and_repeated_passes():
+    """Ragged members incl. empty ones and members of one row, ties, zero
+    rows, repeated passes: every member's important set and deviation equal
+    the oracle's."""
+    rng = np.random.default_rng(7)
+    counts = [0, 1, 63, 64, 65, 700, 0, 4096, 5, 129]
+    R = sum(counts)
+    fresh = rng.standard_normal((R, 2, 64)).astype(np.float32)
+    cached = fresh.copy()
+    moved = rng.random(R) > 0.4
+    cached[moved] += np.round(rng.standard_normal((int(moved.sum()), 2, 64)) * 4) / 4
+    f = torch.from_numpy(fresh).to(DEV)
+    c = torch.from_numpy(cached).to(DEV)
+    mags = ref.key_diff(fresh, cached)
+    off = np.concatenate([[0], np.cumsum(counts)])
+    for _ in range(3):
+        out = sel.batched_selection(f, c, counts, 0.2)
+        for m, (imp, dv) in enumerate(out):
+            mm = mags[off[m]:off[m + 1]]
+            want = ref.select_important(mm, ref.recompute_budget(0.2, counts[m])) if counts[m] \
+                else np.zeros(0, np.int64)
+            assert imp.tolist() == want.tolist(), m
+            assert abs(dv - float(mm.sum())) <= 1e-5 * max(1.0, abs(float(mm.sum())))
