@@ -28,10 +28,30 @@ def _inv_freq_dev(device_index: int, head_dim: int, base: float) -> torch.Tensor
         torch.device("cuda", device_index))
 
 
+_ONE_ROW_TABLES: dict = {}
+
+
 def rope_table(deltas: np.ndarray, head_dim: int, base: float, kv_dtype: torch.dtype,
                device: torch.device) -> torch.Tensor:
-    """K0: (n, D/2, 2) cos/sin rows for the given int64 deltas."""
+    """K0: (n, D/2, 2) cos/sin rows for the given int64 deltas.  One-row
+    tables (a constant span shift, the common restore case) are kept per
+    (stream, delta, geometry): a repeated shift costs no upload and no launch."""
     deltas = np.ascontiguousarray(deltas, dtype=np.int64)
+    n = int(deltas.size)
+    if n == 1:
+        key = (device.index, torch.cuda.current_stream(device).cuda_stream, int(deltas[0]),
+               head_dim, float(base), kv_dtype)
+        hit = _ONE_ROW_TABLES.get(key)
+        if hit is None:
+            if len(_ONE_ROW_TABLES) >= 512:
+                _ONE_ROW_TABLES.clear()
+            hit = _ONE_ROW_TABLES[key] = _rope_table(deltas, head_dim, base, kv_dtype, device)
+        return hit
+    return _rope_table(deltas, head_dim, base, kv_dtype, device)
+
+
+def _rope_table(deltas: np.ndarray, head_dim: int, base: float, kv_dtype: torch.dtype,
+                device: torch.device) -> torch.Tensor:
     n = int(deltas.size)
     tdt = table_dtype(kv_dtype)
     out = torch.empty((max(n, 1), head_dim // 2, 2), dtype=tdt, device=device)

@@ -232,7 +232,10 @@ class PagedPool:
 
     def mark_written(self, slot_map: SlotMap, layers: Optional[Sequence[int]] = None,
                      token_idx: Optional[np.ndarray] = None) -> None:
-        """Record device-side writes (collector / restore kernels)."""
+        """Record device-side writes (collector / restore kernels); the
+        written map is only consulted by debug-mode reads."""
+        if not self.debug:
+            return
         slots = slot_map.slots if token_idx is None else slot_map.slots[token_idx]
         if layers is None:
             self._written[:, slots] = True
