@@ -869,7 +869,7 @@ def codec_bench(tk, spec, pool, maps, dev, args, peak, frac=None, hint_all=False
         "restore_ms_per_mirror": {"fused": round(per["fused"], 4), "dense": round(per["dense"], 4),
                                   "dense_over_fused": round(per["dense"] / per["fused"], 2),
                                   "note": "one mirror per API call (host planning included), "
-                                          "CUDA events around the 49 calls"},
+                                          f"CUDA events around the {n_mirrors} calls"},
         "compression_ratio_mean": round(float(np.mean([dense / w for w in wire])), 3),
         "wire_pack_gbs": round(wire_total / pack_s / 1e9, 2),
         "wire_unpack_gbs": round(unpack_bytes / unpack_s / 1e9, 2),

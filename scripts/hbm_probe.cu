@@ -75,6 +75,48 @@ __global__ void fanout_k(const uint4* __restrict__ s, uint4* __restrict__ d, siz
     }
 }
 
+// 256-bit accesses (sm_100: LDG/STG .256)
+struct alignas(32) u8x32 { uint32_t w[8]; };
+
+__device__ __forceinline__ u8x32 ld256(const u8x32* p) {
+    u8x32 r;
+    asm volatile("ld.global.cs.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(r.w[4]),
+                   "=r"(r.w[5]), "=r"(r.w[6]), "=r"(r.w[7])
+                 : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ void st256(u8x32* p, const u8x32& v) {
+    asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                 :: "l"(p), "r"(v.w[0]), "r"(v.w[1]), "r"(v.w[2]), "r"(v.w[3]), "r"(v.w[4]),
+                    "r"(v.w[5]), "r"(v.w[6]), "r"(v.w[7])
+                 : "memory");
+}
+
+__global__ void write256_k(u8x32* __restrict__ p, size_t n) {
+    u8x32 v;
+    for (int q = 0; q < 8; ++q) v.w[q] = threadIdx.x + q;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x)
+        st256(p + i, v);
+}
+
+__global__ void copy256_k(const u8x32* __restrict__ s, u8x32* __restrict__ d, size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x)
+        st256(d + i, ld256(s + i));
+}
+
+__global__ void fanout256_k(const u8x32* __restrict__ s, u8x32* __restrict__ d, size_t n,
+                            int fan) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x) {
+        const u8x32 v = ld256(s + i);
+        for (int f = 0; f < fan; ++f) st256(d + (size_t)f * n + i, v);
+    }
+}
+
 template <typename F>
 static float best_ms(F launch, int reps = 10) {
     cudaEvent_t a, b;
@@ -117,7 +159,17 @@ int main() {
     const size_t src = 224ull << 20;
     const int fan = 50;
     const float f = best_ms([&] { fanout_k<<<grid, block>>>(x, y, src / 16, fan); }, 5);
+    const float w32 = best_ms([&] { write256_k<<<grid, block>>>((u8x32*)y, big / 32); });
+    const float c32 = best_ms([&] { copy256_k<<<grid, block>>>((const u8x32*)x, (u8x32*)y,
+                                                               big / 64); });
+    const float f32 = best_ms([&] { fanout256_k<<<grid, block>>>((const u8x32*)x, (u8x32*)y,
+                                                                 src / 32, fan); }, 5);
+    float cm = best_ms([&] { cudaMemcpyAsync(y, x, big / 2, cudaMemcpyDeviceToDevice); });
     CK(cudaGetLastError());
+    printf("{\"write256_gbs\": %.1f, \"copy256_gbs\": %.1f, \"fanout50_256_gbs\": %.1f, "
+           "\"memcpy_d2d_gbs\": %.1f}\n",
+           big / (w32 * 1e-3) / 1e9, big / (c32 * 1e-3) / 1e9,
+           (src * (fan + 1)) / (f32 * 1e-3) / 1e9, big / (cm * 1e-3) / 1e9);
     printf("{\"read_gbs\": %.1f, \"write_gbs\": %.1f, \"copy_gbs\": %.1f, "
            "\"write_default_gbs\": %.1f, \"write_bulk1k_gbs\": %.1f, \"write_bulk4k_gbs\": %.1f, "
            "\"fanout50_gbs\": %.1f, \"fanout50_bytes\": %zu, \"bytes\": %zu, \"sms\": %d}\n",
