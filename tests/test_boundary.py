@@ -228,3 +228,29 @@ def test_c_abi_rejects_bad_arguments_without_a_gpu():
     assert lib.tdkv_collect(null, null, 0, null, 0, 8, null, null, null, 0, null, null, 0,
                             2, 2, 8, 0, 0, null) == 0
     assert lib.tdkv_rows(null, 0, 8, null, 1, 1, 8, 8, 0, 0, 0, 0, null) == 0
+
+
+def test_collect_sources_rejects_bad_arguments_without_a_gpu():
+    """tdkv_collect_sources (the peer-read K1) validates its source table
+    before any CUDA call."""
+    import ctypes
+    from paper_2604_03143_b200 import _lib
+    lib = _lib.load()
+    null = ctypes.c_void_p(0)
+    fake = ctypes.c_void_p(0x100000)              # never dereferenced: validation fails first
+    tbl = (ctypes.c_void_p * 2)(fake.value, fake.value)
+    tail = [null, 1, 8, null, null, null, 0, null, null, 0, 2, 2, 8, 1, 0, null]
+    assert lib.tdkv_collect_sources(tbl, tbl, 0, null, 0, *tail) == 1
+    assert b"sources" in lib.tdkv_last_error()
+    assert lib.tdkv_collect_sources(tbl, tbl, 17, fake, 0, *tail) == 1
+    assert lib.tdkv_collect_sources(tbl, tbl, 2, null, 0, *tail) == 1      # no unit map
+    tail_v = tail[:8] + [fake] + tail[9:]         # a V destination for the K+V form
+    odd = (ctypes.c_void_p * 2)(fake.value, fake.value + 8)
+    assert lib.tdkv_collect_sources(odd, odd, 2, fake, 0, *tail_v) == 1
+    assert b"aligned" in lib.tdkv_last_error()
+    holes = (ctypes.c_void_p * 2)(fake.value, None)
+    assert lib.tdkv_collect_sources(holes, tbl, 2, fake, 0, *tail_v) == 1
+    assert b"null" in lib.tdkv_last_error()
+    # K+V sources with a K-only destination (and the converse) are rejected
+    assert lib.tdkv_collect_sources(tbl, None, 2, fake, 0, *tail_v) == 1
+    assert lib.tdkv_collect_sources(tbl, tbl, 2, fake, 0, *tail) == 1
