@@ -117,6 +117,71 @@ __global__ void fanout256_k(const u8x32* __restrict__ s, u8x32* __restrict__ d, 
     }
 }
 
+// TMA both ways: one thread per CTA streams chunks global -> smem (bulk load,
+// mbarrier) -> global (bulk store) through an S-stage ring
+__device__ __forceinline__ unsigned sm32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+
+template <int S>
+__global__ void copy_tma_k(const char* __restrict__ src, char* __restrict__ dst, size_t nbytes,
+                           int chunk) {
+    extern __shared__ __align__(128) char buf[];
+    __shared__ __align__(8) uint64_t bar[S];
+    if (threadIdx.x != 0) return;
+    for (int s = 0; s < S; ++s)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sm32(&bar[s])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const size_t n = nbytes / chunk;
+    auto load = [&](size_t c, int s) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                     ::"r"(sm32(&bar[s])), "r"(chunk) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+                     "[%0], [%1], %2, [%3];"
+                     ::"r"(sm32(buf + (size_t)s * chunk)), "l"(src + c * chunk), "r"(chunk),
+                       "r"(sm32(&bar[s])) : "memory");
+    };
+    for (int s = 0; s < S; ++s) {
+        const size_t c = blockIdx.x + (size_t)s * gridDim.x;
+        if (c < n) load(c, s);
+    }
+    for (size_t k = 0;; ++k) {
+        const size_t c = blockIdx.x + k * gridDim.x;
+        if (c >= n) break;
+        const int s = (int)(k % S);
+        const unsigned phase = (unsigned)((k / S) & 1);
+        asm volatile("{\n.reg .pred p;\nW%=:\n"
+                     "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+                     "@!p bra W%=;\n}\n" ::"r"(sm32(&bar[s])), "r"(phase) : "memory");
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                     ::"l"(dst + c * chunk), "r"(sm32(buf + (size_t)s * chunk)), "r"(chunk)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        if (k >= 1) {
+            // the previous stage's store has read its smem: refill it
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            const size_t c2 = blockIdx.x + (k - 1 + S) * gridDim.x;
+            if (c2 < n) load(c2, (int)((k - 1) % S));
+        }
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// more memory-level parallelism per thread: 4 independent 16-byte loads, then
+// their 4 stores
+__global__ void copy4_k(const uint4* __restrict__ s, uint4* __restrict__ d, size_t n) {
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += 4 * stride) {
+        uint4 v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (i + q * stride < n) v[q] = __ldcs(s + i + q * stride);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (i + q * stride < n) __stcs(d + i + q * stride, v[q]);
+    }
+}
+
 template <typename F>
 static float best_ms(F launch, int reps = 10) {
     cudaEvent_t a, b;
@@ -165,6 +230,25 @@ int main() {
     const float f32 = best_ms([&] { fanout256_k<<<grid, block>>>((const u8x32*)x, (u8x32*)y,
                                                                  src / 32, fan); }, 5);
     float cm = best_ms([&] { cudaMemcpyAsync(y, x, big / 2, cudaMemcpyDeviceToDevice); });
+    float tma[4];
+    const int chunks[4] = {8192, 16384, 32768, 49152};
+    for (int q = 0; q < 4; ++q) {
+        const int ch = chunks[q];
+        const int S = 4;
+        const size_t smem = (size_t)S * ch;
+        CK(cudaFuncSetAttribute(copy_tma_k<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, copy_tma_k<4>, 32, smem));
+        tma[q] = best_ms([&] { copy_tma_k<4><<<sms * per_sm, 32, smem>>>((const char*)x,
+                                                                          (char*)y, big / 2, ch); });
+    }
+    const float c4 = best_ms([&] { copy4_k<<<grid, block>>>(x, y, n / 2); });
+    CK(cudaGetLastError());
+    printf("{\"copy_tma_8k_gbs\": %.1f, \"copy_tma_16k_gbs\": %.1f, \"copy_tma_32k_gbs\": %.1f, "
+           "\"copy_tma_48k_gbs\": %.1f, \"copy_4x16b_gbs\": %.1f}\n",
+           big / (tma[0] * 1e-3) / 1e9, big / (tma[1] * 1e-3) / 1e9, big / (tma[2] * 1e-3) / 1e9,
+           big / (tma[3] * 1e-3) / 1e9, big / (c4 * 1e-3) / 1e9);
     CK(cudaGetLastError());
     printf("{\"write256_gbs\": %.1f, \"copy256_gbs\": %.1f, \"fanout50_256_gbs\": %.1f, "
            "\"memcpy_d2d_gbs\": %.1f}\n",
