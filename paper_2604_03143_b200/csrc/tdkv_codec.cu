@@ -69,20 +69,30 @@ __global__ void __launch_bounds__(256)
     if (threadIdx.x == 0) changed[item] = (uint8_t)(any != 0);
     if (!any || hinted[(size_t)pi * g.nb + b]) return;
 
-    // soundness violation (rare): max |mirror - master| over both planes
-    float m = 0.f;
+    // soundness violation (rare): max |mirror - master| per plane, combined
+    // as the reference does
+    float mk_ = 0.f, mv_ = 0.f;
     for (int w = threadIdx.x; w < units; w += blockDim.x) {
-        m = fmaxf(m, unit_maxabs<T>(mk[w], rk[w]));
-        m = fmaxf(m, unit_maxabs<T>(mv[w], rv[w]));
+        mk_ = nanmax(mk_, unit_maxabs_nan<T>(mk[w], rk[w]));
+        mv_ = nanmax(mv_, unit_maxabs_nan<T>(mv[w], rv[w]));
     }
-    __shared__ float red[32];
-    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __shared__ float red[2][32];
+    for (int o = 16; o > 0; o >>= 1) {
+        mk_ = nanmax(mk_, __shfl_xor_sync(0xffffffffu, mk_, o));
+        mv_ = nanmax(mv_, __shfl_xor_sync(0xffffffffu, mv_, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = mk_;
+        red[1][threadIdx.x >> 5] = mv_;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
-        float mm = 0.f;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mm = fmaxf(mm, red[w]);
-        viol_maxabs[item] = mm;
+        float a = 0.f, c = 0.f;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            a = nanmax(a, red[0][w]);
+            c = nanmax(c, red[1][w]);
+        }
+        viol_maxabs[item] = py_max_kv(a, c);
         atomicMin(violation + pi, layer * g.nb + b);
     }
 }
@@ -245,19 +255,30 @@ __global__ void __launch_bounds__(256)
     }
     const tdkv_diff_out out = outs[pi];
     if (any && !is_hinted) {
-        // soundness violation (rare): max |mirror - master| over both planes
-        float m = 0.f;
+        // soundness violation (rare): max |mirror - master| per plane, combined
+        // as the reference does
+        float mk_ = 0.f, mv_ = 0.f;
         for (int w = threadIdx.x; w < units; w += blockDim.x) {
-            m = fmaxf(m, unit_maxabs<T>(mk[w], rk[w]));
-            m = fmaxf(m, unit_maxabs<T>(mv[w], rv[w]));
+            mk_ = nanmax(mk_, unit_maxabs_nan<T>(mk[w], rk[w]));
+            mv_ = nanmax(mv_, unit_maxabs_nan<T>(mv[w], rv[w]));
         }
-        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+        for (int o = 16; o > 0; o >>= 1) {
+            mk_ = nanmax(mk_, __shfl_xor_sync(0xffffffffu, mk_, o));
+            mv_ = nanmax(mv_, __shfl_xor_sync(0xffffffffu, mv_, o));
+        }
+        __shared__ float red2[32];
+        if ((threadIdx.x & 31) == 0) {
+            red[threadIdx.x >> 5] = mk_;
+            red2[threadIdx.x >> 5] = mv_;
+        }
         __syncthreads();
         if (threadIdx.x == 0) {
-            float mm = 0.f;
-            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mm = fmaxf(mm, red[w]);
-            viol_maxabs[row + b] = mm;
+            float a = 0.f, c = 0.f;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+                a = nanmax(a, red[w]);
+                c = nanmax(c, red2[w]);
+            }
+            viol_maxabs[row + b] = py_max_kv(a, c);
             atomicMin(violation + pi, layer * g.nb + b);
         }
     }

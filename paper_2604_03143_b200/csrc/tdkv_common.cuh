@@ -86,16 +86,28 @@ __device__ __forceinline__ bool unit_differs(const V& a, const V& b) {
     return d;
 }
 
+// max that propagates NaN like numpy's ndarray.max()
+__device__ __forceinline__ float nanmax(float a, float b) {
+    return (a != a || b != b) ? __int_as_float(0x7fc00000) : fmaxf(a, b);
+}
+
+// The reference's violation magnitude, max(float(|dK|.max()), float(|dV|.max()))
+// (diffstore.py:157-160): numpy's max propagates NaN within a plane; Python's
+// max(k, v) returns v only when v > k, so a NaN in K wins and a NaN in V alone
+// is dropped.
+__device__ __forceinline__ float py_max_kv(float k, float v) { return v > k ? v : k; }
+
 template <typename T, typename V>
-__device__ __forceinline__ float unit_maxabs(const V& a, const V& b) {
+__device__ __forceinline__ float unit_maxabs_nan(const V& a, const V& b) {
     constexpr int kN = sizeof(V) / sizeof(T);
     const T* x = reinterpret_cast<const T*>(&a);
     const T* y = reinterpret_cast<const T*>(&b);
     float m = 0.f;
 #pragma unroll
-    for (int i = 0; i < kN; ++i) m = fmaxf(m, fabsf((float)x[i] - (float)y[i]));
+    for (int i = 0; i < kN; ++i) m = nanmax(m, fabsf((float)x[i] - (float)y[i]));
     return m;
 }
+
 
 // ---------------------------------------------------------------------------
 // global memory access with cache hints

@@ -261,6 +261,16 @@ def gen_codec_trials():
     return out
 
 
+# (plane, index, value or None = +2.5, edit the master instead of the mirror)
+VIOLATION_CASES = {
+    "nan_k": [("k", (0, 100, 0, 0), float("nan"), False)],
+    "nan_v_and_k": [("v", (0, 100, 0, 0), float("nan"), False), ("k", (0, 101, 1, 3), None, False)],
+    "nan_both_v": [("v", (2, 99, 1, 1), float("nan"), False), ("v", (2, 99, 1, 1), float("nan"), True)],
+    "neg_inf_k": [("k", (3, 127, 0, 7), float("-inf"), False)],
+    "signed_zero": [("k", (1, 110, 1, 2), 0.0, True), ("k", (1, 110, 1, 2), -0.0, False)],
+}
+
+
 def gen_known_answers():
     """The worked examples of test_diffstore.py / acceptance C07."""
     blocks = CacheBlockConfig(block_size=32)
@@ -282,6 +292,24 @@ def gen_known_answers():
         raise AssertionError("expected a soundness error")
     except HintSoundnessError as exc:
         res["violation"] = {"seed": 24, "message": str(exc)}
+    # the violation magnitude with NaN / inf outside the hints: numpy's max
+    # propagates NaN within a plane, Python's max(k, v) keeps K's NaN and drops
+    # V's (diffstore.py:157-160)
+    res["violation_special"] = []
+    for case, edits in VIOLATION_CASES.items():
+        rng = np.random.default_rng(24)
+        master = random_kv(rng, 128, 4, 2, 8)
+        mirror, hints = _perturb(rng, master, blocks, [1])
+        for plane, idx, value, on_master in edits:
+            tgt = master if on_master else mirror
+            getattr(tgt, plane)[idx] = value if value is not None else \
+                getattr(tgt, plane)[idx] + 2.5
+        try:
+            encode_diff(master, mirror, hints, blocks)
+            message = None
+        except HintSoundnessError as exc:
+            message = str(exc)
+        res["violation_special"].append({"case": case, "message": message})
     rng = np.random.default_rng(21)
     master = random_kv(rng, 70, 4, 2, 8)
     mirror, hints = _perturb(rng, master, blocks, [2])
@@ -509,4 +537,13 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["--known-only"]:      # refresh one section in place
+        path = os.path.join(HERE, "golden.json")
+        with open(path) as f:
+            golden = json.load(f)
+        golden["known"] = gen_known_answers()
+        with open(path, "w") as f:
+            json.dump(golden, f, indent=1, sort_keys=True)
+        print("updated known answers in", path)
+    else:
+        main()

@@ -162,3 +162,27 @@ def replay_segment_index(make_index, entry_factory, ops):
         assert evicted == op["evicted"], step
         assert idx.total_bytes == op["total"] and len(idx) == op["len"], step
         assert [label[id(e)] for e in idx.entries()] == op["lru"], step
+
+
+# soundness-violation magnitudes with NaN / inf / signed zeros outside the
+# hints; the same cases as tests/golden/make_golden.py VIOLATION_CASES:
+# (plane, index, value or None = +2.5, edit the master instead of the mirror)
+VIOLATION_CASES = {
+    "nan_k": [("k", (0, 100, 0, 0), float("nan"), False)],
+    "nan_v_and_k": [("v", (0, 100, 0, 0), float("nan"), False), ("k", (0, 101, 1, 3), None, False)],
+    "nan_both_v": [("v", (2, 99, 1, 1), float("nan"), False), ("v", (2, 99, 1, 1), float("nan"), True)],
+    "neg_inf_k": [("k", (3, 127, 0, 7), float("-inf"), False)],
+    "signed_zero": [("k", (1, 110, 1, 2), 0.0, True), ("k", (1, 110, 1, 2), -0.0, False)],
+}
+
+
+def violation_case(case):
+    """(master k, master v, mirror k, mirror v, hints) of a special case."""
+    rng = np.random.default_rng(24)
+    k, v, _ = random_planes(rng, 128)
+    mk, mv, hints = perturb(rng, k, v, 32, [1])
+    planes = {("k", True): k, ("v", True): v, ("k", False): mk, ("v", False): mv}
+    for plane, idx, value, on_master in VIOLATION_CASES[case]:
+        arr = planes[(plane, on_master)]
+        arr[idx] = value if value is not None else arr[idx] + np.float32(2.5)
+    return k, v, mk, mv, hints

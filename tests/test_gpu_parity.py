@@ -15,7 +15,7 @@ import pytest
 import torch
 
 import paper_2604_03143_b200 as tk
-from helpers import (codec_trials, load_golden, load_npz, perturb, random_planes,
+from helpers import (violation_case, codec_trials, load_golden, load_npz, perturb, random_planes,
                      restore_trials, sha)
 from oracle import roundkv_port as ref
 from paper_2604_03143_b200 import rounds
@@ -305,6 +305,26 @@ def test_known_answers_and_errors():
     k2, v2, _ = random_planes(rng, 70)
     with pytest.raises(ValueError, match="positions"):
         tk.encode_diff(tk.LayeredKv(k, v, pos), tk.LayeredKv(k2, v2, pos + 5), hints, blocks)
+
+
+def test_violation_magnitudes_with_nan_inf_and_signed_zero():
+    """K2's soundness error for NaN / inf / -0.0 outside the hints equals the
+    reference's message byte for byte: numpy's per-plane max propagates NaN,
+    Python's max(k, v) keeps K's NaN and drops V's (diffstore.py:157-160)."""
+    blocks = tk.CacheBlockConfig(32)
+    for entry in G["known"]["violation_special"]:
+        k, v, mk, mv, hints = violation_case(entry["case"])
+        pos = np.arange(k.shape[1])
+        for dev in (False, True):
+            conv = (lambda a: torch.from_numpy(a).to(DEV)) if dev else (lambda a: a)
+            master = tk.LayeredKv(conv(k), conv(v), pos)
+            mirror = tk.LayeredKv(conv(mk), conv(mv), pos)
+            if entry["message"] is None:
+                tk.encode_diff(master, mirror, hints, blocks)
+                continue
+            with pytest.raises(tk.HintSoundnessError) as err:
+                tk.encode_diff(master, mirror, hints, blocks)
+            assert str(err.value) == entry["message"], (entry["case"], dev)
 
 
 def test_float_equality_semantics():

@@ -11,7 +11,7 @@ import hashlib
 import numpy as np
 import pytest
 
-from helpers import (codec_trials, load_golden, load_npz, perturb, random_planes,
+from helpers import (violation_case, codec_trials, load_golden, load_npz, perturb, random_planes,
                      restore_trials, sha)
 from oracle import roundkv_port as ref
 
@@ -290,3 +290,16 @@ def test_segment_index_port_matches_reference_stream():
             self.entry_id = E._n
 
     replay_segment_index(lambda b, p, ev: ref.SegmentIndexPort(b, p, ev), E, G["segment_index"])
+
+
+def test_oracle_violation_magnitudes_with_nan_inf_and_signed_zero():
+    """NaN / inf / -0.0 outside the hints: the oracle's soundness message is
+    the reference's, byte for byte (golden.json known.violation_special)."""
+    for entry in G["known"]["violation_special"]:
+        k, v, mk, mv, hints = violation_case(entry["case"])
+        if entry["message"] is None:
+            ref.encode_diff(k, v, mk, mv, hints, 32)
+            continue
+        with pytest.raises(ref.HintViolation) as err:
+            ref.encode_diff(k, v, mk, mv, hints, 32)
+        assert str(err.value) == entry["message"], entry["case"]
