@@ -205,3 +205,134 @@ def session_owners(spec: RoundSpec, world: int) -> List[int]:
 def session_needs(spec: RoundSpec, world: int) -> List[List[int]]:
     """Per rank, the sessions whose masters its agent shard reads."""
     return [spec.sessions_of(shard(spec.num_agents, r, world)) for r in range(world)]
+
+
+# ---------------------------------------------------------------------------
+# toy-model recovery rounds (the caller of the Collector: collective_recover)
+
+
+@dataclass
+class ToyConfig:
+    num_layers: int
+    num_heads: int
+    head_dim: int
+    vocab_size: int
+    rope_base: float = 10000.0
+
+
+@dataclass
+class ToyWeights:
+    """Synthetic toy-transformer weights with the reference's shapes and
+    distribution (U[-0.1, 0.1] float32; toymodel.py:36-57): ``embed`` (V, hid),
+    ``wq/wk/wv/wm`` (L, hid, hid)."""
+
+    config: ToyConfig
+    embed: np.ndarray
+    wq: np.ndarray
+    wk: np.ndarray
+    wv: np.ndarray
+    wm: np.ndarray
+
+
+def toy_weights(num_layers: int, num_heads: int, head_dim: int, vocab_size: int,
+                seed: int = 0) -> ToyWeights:
+    rng = np.random.default_rng(seed)
+    hid = num_heads * head_dim
+
+    def u(*shape):
+        return rng.uniform(-0.1, 0.1, size=shape).astype(np.float32)
+
+    return ToyWeights(ToyConfig(num_layers, num_heads, head_dim, vocab_size), u(vocab_size, hid),
+                      u(num_layers, hid, hid), u(num_layers, hid, hid), u(num_layers, hid, hid),
+                      u(num_layers, hid, hid))
+
+
+@dataclass(eq=False)
+class ToyHit:
+    """A shared segment resolved against the cache (pic.py:51-64)."""
+
+    kv: object                  # LayeredKv of the segment master
+    target_idx: np.ndarray
+
+    @property
+    def delta(self) -> np.ndarray:
+        return self.target_idx - np.asarray(self.kv.positions, np.int64)
+
+    def __len__(self) -> int:
+        return int(self.target_idx.size)
+
+
+@dataclass(eq=False)
+class ToyRequest:
+    """The fields of the reference's PreparedRequest (pic.py:67-98) that the
+    recovery path reads."""
+
+    request_id: int
+    tokens: np.ndarray
+    positions: np.ndarray
+    private_idx: np.ndarray
+    structural_idx: np.ndarray
+    hits: list
+    label_entry: np.ndarray
+    label_offset: np.ndarray
+
+    @property
+    def num_tokens(self) -> int:
+        return int(self.tokens.size)
+
+    @property
+    def shared_idx(self) -> np.ndarray:
+        if not self.hits:
+            return np.empty(0, dtype=np.int64)
+        return np.sort(np.concatenate([h.target_idx for h in self.hits]))
+
+
+@dataclass(eq=False)
+class ToyGroup:
+    members: list
+
+
+def toy_round(weights: ToyWeights, num_agents: int = 8, num_segments: int = 4,
+              seg_len: int = 256, hist_len: int = 64, separator: int = 0, seed: int = 0):
+    """One All-Gather round of the toy model (BASELINE configs[0]: 8 agents x
+    4 shared 256-token blocks).  Segment s is agent (s mod N)'s output,
+    prefilled after that agent's history and a separator, so its master rows
+    carry source positions hist+1 .. hist+seg_len; agent i's prompt is
+    hist_i || SEP || seg_pi(0) || SEP || ... with pi = rng(2+i).permutation(S)
+    (prepare_request's layout, pic.py:110-163).  Returns the members (one
+    group: equal lengths, one digest set)."""
+    from .recompute import full_prefill
+    rng = np.random.default_rng(seed)
+    V = weights.config.vocab_size
+    hists = [rng.integers(1, V, hist_len) for _ in range(num_agents)]
+    outputs = [rng.integers(1, V, seg_len) for _ in range(num_segments)]
+    segs = []
+    for s in range(num_segments):
+        producer = np.concatenate([hists[s % num_agents], [separator], outputs[s]])
+        kv = full_prefill(weights, producer)
+        lo = hist_len + 1
+        segs.append(type(kv)(kv.k[:, lo:].copy(), kv.v[:, lo:].copy(), kv.positions[lo:].copy()))
+    members = []
+    for i in range(num_agents):
+        order = np.random.default_rng(2 + i).permutation(num_segments)
+        toks = [hists[i]]
+        T = hist_len
+        starts = []
+        for j, s in enumerate(order):
+            toks += [[separator], outputs[s]]
+            starts.append(T + 1)
+            T += seg_len + 1
+        tokens = np.concatenate(toks).astype(np.int64)
+        label_entry = np.full(T, -1, np.int64)
+        label_offset = np.full(T, -1, np.int64)
+        hits = []
+        for s, st in zip(order, starts):
+            idx = np.arange(st, st + seg_len, dtype=np.int64)
+            hits.append(ToyHit(segs[s], idx))
+            label_entry[idx] = s
+            label_offset[idx] = np.arange(seg_len)
+        members.append(ToyRequest(i, tokens, np.arange(T, dtype=np.int64),
+                                  np.arange(hist_len, dtype=np.int64),
+                                  np.asarray([st - 1 for st in starts], np.int64), hits,
+                                  label_entry, label_offset))
+    return members

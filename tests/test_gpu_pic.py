@@ -99,3 +99,28 @@ def test_serial_recovery_matches_reference():
     assert led.rope_calls_by_layer == [1, 1, 1] and led.selection_passes == 1
     assert np.abs(r.kv.k.cpu().numpy() - z["permuted_serial0_k"]).max() <= TOL
     assert np.abs(r.kv.v.cpu().numpy() - z["permuted_serial0_v"]).max() <= TOL
+
+
+def test_grouped_equals_serial_on_a_c1_round():
+    """BASELINE configs[0] (8 agents x 4 shared 256-token blocks, 2-layer toy
+    model, 8 heads, d=64): grouped recovery is bit-identical to serial
+    recovery of every member -- caches, important sets, deviation scores
+    (the reference's acceptance C01, test_acceptance.py:80-114) -- with one
+    rotation and one selection pass per layer instead of one per member (C02)."""
+    import torch
+    from paper_2604_03143_b200 import rounds
+    w = rounds.toy_weights(2, 8, 64, 1024, seed=3)
+    members = rounds.toy_round(w, seed=5)
+    led_g, led_s = CostLedger(2), CostLedger(2)
+    results, plan = pic.collective_recover(w, rounds.ToyGroup(members), _Pic, led_g)
+    for m in members:
+        r = pic.recover_prepared(w, m, _Pic, led_s)
+        g = results[m.request_id]
+        assert torch.equal(g.kv.k, r.kv.k) and torch.equal(g.kv.v, r.kv.v)
+        assert g.important_positions.tolist() == r.important_positions.tolist()
+        assert g.deviation_score == r.deviation_score
+        assert plan.deviation_scores[m.request_id] == r.deviation_score
+    assert led_g.rope_calls_per_layer == 1
+    assert led_s.rope_calls_per_layer == len(members)
+    assert led_g.selection_passes == 1 and led_s.selection_passes == len(members)
+    assert plan.master_id == min(plan.deviation_scores.items(), key=lambda kv: (kv[1], kv[0]))[0]
