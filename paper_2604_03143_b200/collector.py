@@ -21,7 +21,7 @@ import ctypes
 import math
 import os
 from dataclasses import dataclass
-from typing import List, Optional, Sequence
+from typing import Optional, Sequence
 
 import numpy as np
 import torch

@@ -28,7 +28,7 @@ import numpy as np
 import torch
 
 from . import _kernels, _lib
-from ._device import (default_device, dtype_code, h2d, is_host, ptr, stream_handle, to_device,
+from ._device import (default_device, dtype_code, h2d, ptr, stream_handle, to_device,
                       to_host, upload)
 from .core import CacheBlockConfig, LayeredKv
 

@@ -23,7 +23,7 @@ import numpy as np
 import torch
 
 from . import _kernels
-from ._device import default_device, h2d, is_host, to_device, to_host
+from ._device import default_device, h2d, to_device, to_host
 
 
 class OutOfSlotsError(RuntimeError):

@@ -16,7 +16,7 @@ pass per recovery unit (C02), ``record_recomputed`` per refresh.
 from __future__ import annotations
 
 from dataclasses import dataclass
-from typing import Dict, List, Optional
+from typing import Dict, Optional
 
 import numpy as np
 import torch

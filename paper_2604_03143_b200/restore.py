@@ -16,14 +16,14 @@ launch (the round-level form used by the benchmark).
 """
 from __future__ import annotations
 
-from typing import List, Optional, Sequence
+from typing import Optional, Sequence
 
 import numpy as np
 import torch
 
 from . import _kernels
 from ._device import to_device
-from .core import CacheBlockConfig, PositionSpan
+from .core import PositionSpan
 from .diffstore import MirrorHandle, decode_dense_into
 from .ledger import CostLedger
 from .paged_pool import PagedPool, SlotMap

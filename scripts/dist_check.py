@@ -9,7 +9,6 @@ Backend: nccl on multi-GPU boxes, gloo when ranks share one GPU.
 import os
 import sys
 
-import numpy as np
 import torch
 import torch.distributed as dist
 
