@@ -26,9 +26,18 @@ def default_device() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def stream_handle(device: Optional[torch.device] = None) -> ctypes.c_void_p:
-    s = torch.cuda.current_stream(device)
-    return ctypes.c_void_p(s.cuda_stream)
+    """The current CUDA stream of ``device`` as a cudaStream_t (the raw
+    accessor skips building a torch.cuda.Stream object: ~10x cheaper, and it
+    is on every launch path)."""
+    if _raw_stream is not None:
+        idx = device.index if isinstance(device, torch.device) and device.index is not None \
+            else (device if isinstance(device, int) else torch.cuda.current_device())
+        return ctypes.c_void_p(_raw_stream(idx))
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
 
 def dtype_code(dt: torch.dtype) -> int:

@@ -28,6 +28,12 @@ def _inv_freq_dev(device_index: int, head_dim: int, base: float) -> torch.Tensor
         torch.device("cuda", device_index))
 
 
+def inv_freq_device(device: torch.device, head_dim: int, base: float) -> torch.Tensor:
+    """The float64 inverse frequencies, resident on ``device`` (cached)."""
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    return _inv_freq_dev(idx, head_dim, float(base))
+
+
 _ONE_ROW_TABLES: dict = {}
 
 

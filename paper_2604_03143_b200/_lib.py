@@ -178,8 +178,13 @@ def call(name: str, *args) -> None:
     lib = load()
     rc = getattr(lib, name)(*args)
     if rc != 0:
-        msg = lib.tdkv_last_error().decode(errors="replace")
-        raise TdkvError(f"{name} failed ({rc}): {msg}")
+        raise_last(name, rc)
+
+
+def raise_last(name: str, rc: int = -1) -> None:
+    """Raise TdkvError with the library's last message for a failed ``name``."""
+    msg = load().tdkv_last_error().decode(errors="replace")
+    raise TdkvError(f"{name} failed ({rc}): {msg}")
 
 
 PINNED_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64)
