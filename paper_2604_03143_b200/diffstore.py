@@ -295,23 +295,29 @@ def encode_launch(master: LayeredKv, mirrors: Sequence[LayeredKv],
     shape = tuple(master.k.shape)
     if any(tuple(mir.k.shape) != shape for mir in mirrors):
         raise ValueError("master and mirror must have identical plane shapes")
-    others = [mir.positions for mir in mirrors if mir.positions is not master.positions]
-    if others and not (np.stack(others) == master.positions).all():   # one vectorized compare
-        raise ValueError("master and mirror must cover the same positions")
-    # every mirror's hint positions -> its hinted-block row (a 1-D scatter per
-    # mirror is ~4x faster than one 2-D fancy-index scatter over the family)
+    mpos = np.asarray(master.positions)
+    mbytes = mpos.tobytes()
+    for mir in mirrors:              # byte compare of equal-typed vectors: ~2.5x np.stack ==
+        pos = mir.positions
+        if pos is mpos:
+            continue
+        pos = np.asarray(pos)
+        same = (pos.tobytes() == mbytes if pos.dtype == mpos.dtype and pos.shape == mpos.shape
+                else np.array_equal(pos, mpos))
+        if not same:
+            raise ValueError("master and mirror must cover the same positions")
+    # every mirror's hint positions -> its hinted-block row: one flat scatter
+    # of (mirror * nb + block) over the concatenated hints
     hs = [np.asarray(h).reshape(-1) for h in hint_positions]
-    hs = [h if np.issubdtype(h.dtype, np.integer) else h.astype(np.int64) for h in hs]
-    sizes = [h.size for h in hs]
-    if any(sizes):
-        cat = np.concatenate([h for h in hs if h.size])
+    sizes = np.fromiter((h.size for h in hs), np.int64, len(hs))
+    if sizes.sum():
+        cat = np.concatenate(hs)
+        if cat.dtype.kind not in "iu":
+            cat = cat.astype(np.int64)
         if cat.min() < 0 or cat.max() >= total:
             raise ValueError("hint positions out of range")
         blk = (cat >> (bs.bit_length() - 1)) if bs & (bs - 1) == 0 else cat // bs
-        offs = np.cumsum([0] + sizes)
-        for p in range(len(hs)):
-            if sizes[p]:
-                hinted[p, blk[offs[p]:offs[p + 1]]] = 1
+        hinted.reshape(-1)[blk + np.repeat(np.arange(len(hs), dtype=np.int64) * nb, sizes)] = 1
     device = device or (master.k.device if master.on_device else default_device())
     dtype = _plane_dtype(master)
     mk = to_device(master.k, device, dtype)
