@@ -35,4 +35,4 @@ for _ in range(20):
     torch.cuda.synchronize()
     d = ds.encode_finish(st)
 pr.disable()
-pstats.Stats(pr).sort_stats("tottime").print_stats(18)
+pstats.Stats(pr).sort_stats("tottime").print_stats(22)
