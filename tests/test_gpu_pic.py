@@ -124,3 +124,40 @@ def test_grouped_equals_serial_on_a_c1_round():
     assert led_s.rope_calls_per_layer == len(members)
     assert led_g.selection_passes == 1 and led_s.selection_passes == len(members)
     assert plan.master_id == min(plan.deviation_scores.items(), key=lambda kv: (kv[1], kv[0]))[0]
+
+
+def test_segment_reuse_is_position_independent():
+    """Acceptance C08 (test_acceptance.py:335-361) on the GPU: a segment
+    produced at offset 10 is reused at offset 400 of another prompt; with
+    recompute fraction 1 the recovered cache equals a full prefill of that
+    prompt (GPU prefill within 1e-6, the oracle's within the model tolerance)."""
+    import torch
+    from paper_2604_03143_b200 import recompute, rounds
+    w = rounds.toy_weights(4, 2, 8, 1024, seed=9)
+    rng = np.random.default_rng(88)
+    segment = rng.integers(1, 1024, 16)
+    producer = np.concatenate([rng.integers(1, 1024, 9), [0], segment])
+    consumer = np.concatenate([rng.integers(1, 1024, 399), [0], segment])
+    kv = recompute.full_prefill(w, producer)
+    seg_kv = type(kv)(kv.k[:, 10:].copy(), kv.v[:, 10:].copy(), kv.positions[10:].copy())
+    assert seg_kv.positions[0] == 10
+    T = consumer.size
+    target = np.arange(400, 416, dtype=np.int64)
+    le = np.full(T, -1, np.int64)
+    lo = np.full(T, -1, np.int64)
+    le[target], lo[target] = 0, np.arange(16)
+    prep = rounds.ToyRequest(0, consumer.astype(np.int64), np.arange(T, dtype=np.int64),
+                             np.arange(399, dtype=np.int64), np.array([399], np.int64),
+                             [rounds.ToyHit(seg_kv, target)], le, lo)
+
+    class _Full:
+        recompute_fraction = 1.0
+        check_layer = 1
+    res = pic.recover_prepared(w, prep, _Full, CostLedger(4))
+    full = recompute.full_prefill(w, consumer)
+    got_k = res.kv.k.cpu().numpy()
+    got_v = res.kv.v.cpu().numpy()
+    assert np.abs(got_k - full.k).max() <= 1e-6 and np.abs(got_v - full.v).max() <= 1e-6
+    ow = ref.ToyWeights(2, 8, 10000.0, w.embed, w.wq, w.wk, w.wv, w.wm)
+    ok, ov = ref.full_prefill(ow, consumer)
+    assert np.abs(got_k - ok).max() <= TOL and np.abs(got_v - ov).max() <= TOL
