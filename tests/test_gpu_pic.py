@@ -101,6 +101,26 @@ def test_serial_recovery_matches_reference():
     assert np.abs(r.kv.v.cpu().numpy() - z["permuted_serial0_v"]).max() <= TOL
 
 
+@pytest.mark.parametrize("agents", [2, 3, 5, 10])
+def test_grouped_equals_serial_across_group_sizes(agents):
+    """Acceptance C01 (test_acceptance.py:80-114) on the GPU over group sizes
+    {2, 3, 5, 10}: grouped == serial bit for bit, one rotation per layer."""
+    import torch
+    from paper_2604_03143_b200 import rounds
+    w = rounds.toy_weights(3, 2, 16, 512, seed=agents)
+    members = rounds.toy_round(w, num_agents=agents, num_segments=3, seg_len=24, hist_len=10,
+                               seed=100 + agents)
+    led = CostLedger(3)
+    results, plan = pic.collective_recover(w, rounds.ToyGroup(members), _Pic, led)
+    assert led.rope_calls_per_layer == 1 and led.selection_passes == 1
+    for m in members:
+        r = pic.recover_prepared(w, m, _Pic)
+        g = results[m.request_id]
+        assert torch.equal(g.kv.k, r.kv.k) and torch.equal(g.kv.v, r.kv.v)
+        assert g.important_positions.tolist() == r.important_positions.tolist()
+        assert g.deviation_score == r.deviation_score
+
+
 def test_grouped_equals_serial_on_a_c1_round():
     """BASELINE configs[0] (8 agents x 4 shared 256-token blocks, 2-layer toy
     model, 8 heads, d=64): grouped recovery is bit-identical to serial
@@ -161,3 +181,57 @@ def test_segment_reuse_is_position_independent():
     ow = ref.ToyWeights(2, 8, 10000.0, w.embed, w.wq, w.wk, w.wv, w.wm)
     ok, ov = ref.full_prefill(ow, consumer)
     assert np.abs(got_k - ok).max() <= TOL and np.abs(got_v - ov).max() <= TOL
+
+
+def _reuse_request(w, consumer_hist, segments):
+    """A one-member request reading ``segments`` [(tokens, producer history)]
+    after ``consumer_hist``; each segment's master is its producer's prefill
+    (history || SEP || segment), i.e. cached at offset len(history) + 1."""
+    from paper_2604_03143_b200 import recompute, rounds
+    toks = [np.asarray(consumer_hist, np.int64)]
+    T = len(consumer_hist)
+    hits, structural = [], []
+    le, lo = [], []
+    for e, (seg, hist) in enumerate(segments):
+        kv = recompute.full_prefill(w, np.concatenate([hist, [0], seg]))
+        a = len(hist) + 1
+        seg_kv = type(kv)(kv.k[:, a:].copy(), kv.v[:, a:].copy(), kv.positions[a:].copy())
+        structural.append(T)
+        toks += [np.array([0]), np.asarray(seg, np.int64)]
+        target = np.arange(T + 1, T + 1 + len(seg), dtype=np.int64)
+        hits.append(rounds.ToyHit(seg_kv, target))
+        le.append((target, e))
+        T += 1 + len(seg)
+    label_entry = np.full(T, -1, np.int64)
+    label_offset = np.full(T, -1, np.int64)
+    for target, e in le:
+        label_entry[target] = e
+        label_offset[target] = np.arange(target.size)
+    tokens = np.concatenate(toks)
+    return rounds.ToyRequest(0, tokens, np.arange(T, dtype=np.int64),
+                             np.arange(len(consumer_hist), dtype=np.int64),
+                             np.asarray(structural, np.int64), hits, label_entry, label_offset)
+
+
+def test_fidelity_brackets_with_recompute_fraction():
+    """Acceptance C03 (test_acceptance.py:149-183) on the GPU: two outputs read
+    in swapped order drift off their cached offsets; the mean K error against
+    a full prefill is > 0 at r=0, non-increasing over r in {0, .15, .5, 1},
+    and <= 1e-6 at r=1."""
+    from paper_2604_03143_b200 import recompute, rounds
+    w = rounds.toy_weights(4, 2, 8, 1024, seed=77)
+    rng = np.random.default_rng(77)
+    hist0, hist1 = rng.integers(1, 1024, 12), rng.integers(1, 1024, 14)
+    out0, out1 = rng.integers(1, 1024, 10), rng.integers(1, 1024, 10)
+    prep = _reuse_request(w, hist0, [(out1, hist1), (out0, hist0)])
+    assert prep.hits[0].kv.positions[0] == 15 and prep.hits[1].kv.positions[0] == 13
+    full = recompute.full_prefill(w, prep.tokens)
+    errors = []
+    for fraction in (0.0, 0.15, 0.5, 1.0):
+        cfg = type("Cfg", (), {"recompute_fraction": fraction, "check_layer": 1})
+        res = pic.recover_prepared(w, prep, cfg, CostLedger(4))
+        dk = res.kv.k.cpu().numpy() - full.k
+        errors.append(float(np.sqrt(np.einsum("lthd,lthd->lt", dk, dk)).mean()))
+    assert errors[0] > 0.0
+    assert all(b <= a for a, b in zip(errors, errors[1:])), errors
+    assert errors[-1] <= 1e-6
