@@ -298,6 +298,29 @@ int32_t tdkv_attention(const float* d_q, const float* d_k_fresh, const float* d_
                        int32_t n_fix, int32_t num_tokens, int32_t num_heads,
                        int32_t head_dim, float scale, float* d_mix, void* stream);
 
+/* tdkv_attention over several members' fixed rows in one launch (grouped
+ * recovery batches the members' forwards, collective.py:152-187): the rows
+ * of q / fresh K,V / mix are the members' rows concatenated; member m owns
+ * rows [row0, row0 + n_rows), attends over its own context (layer ``layer``
+ * of planes with ctx_layer_stride elements per layer), and its fresh_of
+ * indexes its own slice of the fresh rows.  d_members sorted by row0. */
+typedef struct {
+    const float* ctx_k;          /* (L, num_tokens, H*D) context planes */
+    const float* ctx_v;
+    const int32_t* fresh_of;     /* (num_tokens,) member-local fresh row or -1 */
+    const int64_t* fix_idx;      /* (n_rows,) token index of each fixed row */
+    int64_t ctx_layer_stride;
+    int32_t row0;
+    int32_t n_rows;
+    int32_t num_tokens;
+    int32_t pad;
+} tdkv_attn_member;
+
+int32_t tdkv_attention_many(const float* d_q, const float* d_k_fresh, const float* d_v_fresh,
+                            const tdkv_attn_member* d_members, int32_t n_members, int32_t layer,
+                            int32_t total_rows, int32_t max_tokens, int32_t num_heads,
+                            int32_t head_dim, float scale, float* d_mix, void* stream);
+
 /* ------------------------------------------------------------------------
  * Host slot allocator of the paged pool, policy of
  * PagedPool.allocate (paged_pool.py:106-135): whole free blocks ascending

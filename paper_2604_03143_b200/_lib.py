@@ -85,8 +85,11 @@ ROWS_JOB = np.dtype([("src_k", "<u8"), ("src_v", "<u8"), ("src_layer_stride", "<
                      ("tbl_row", "<i4"), ("tbl_stride", "<i4"), ("rotate", "<i4")])
 WIRE_SEG = np.dtype([("offset", "<u8"), ("nbytes", "<u8"), ("ptr", "<u8"), ("kind", "<i4"),
                      ("pad", "<i4")])
+ATTN_MEMBER = np.dtype([("ctx_k", "<u8"), ("ctx_v", "<u8"), ("fresh_of", "<u8"),
+                        ("fix_idx", "<u8"), ("ctx_layer_stride", "<i8"), ("row0", "<i4"),
+                        ("n_rows", "<i4"), ("num_tokens", "<i4"), ("pad", "<i4")])
 WIRE_RAW, WIRE_BF16_TO_F32, WIRE_F32_TO_BF16 = 0, 1, 2
-assert WIRE_SEG.itemsize == 32
+assert WIRE_SEG.itemsize == 32 and ATTN_MEMBER.itemsize == 56
 assert COLLECT_JOB.itemsize == 24 and COLLECT_UNIT.itemsize == 16
 assert DIFF_PAIR.itemsize == 32 and DIFF_OUT.itemsize == 40 and ROWS_JOB.itemsize == 112
 
@@ -94,6 +97,7 @@ EXPORTS = (
     "tdkv_version", "tdkv_last_error", "tdkv_launch_count", "tdkv_rope_table",
     "tdkv_collect", "tdkv_collect_sources", "tdkv_diff_compare", "tdkv_diff_compact", "tdkv_diff_encode", "tdkv_rows",
     "tdkv_keydiff", "tdkv_select_important", "tdkv_gemm", "tdkv_qkv_rope", "tdkv_attention",
+    "tdkv_attention_many",
     "tdkv_fill_rows", "tdkv_alloc_create", "tdkv_alloc_destroy", "tdkv_alloc_free_count",
     "tdkv_alloc_take", "tdkv_alloc_release", "tdkv_wire_pack", "tdkv_wire_unpack",
     "tdkv_segidx_create", "tdkv_segidx_destroy", "tdkv_segidx_count", "tdkv_segidx_total",
@@ -142,6 +146,8 @@ _SIGS = {
     "tdkv_segidx_evict": (_I32, [_P, _I64, _P, _P, _P, _I32, _P]),
     "tdkv_segidx_entries": (_I32, [_P, _P, _I64, _P]),
     "tdkv_wire_unpack": (_I32, [_P, _I32, _I64, _P, _P]),
+    "tdkv_attention_many": (_I32, [_P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32,
+                                   ctypes.c_float, _P, _P]),
     "tdkv_attention": (_I32, [_P, _P, _P, _P, _P, _P, _P, _I32, _I32, _I32, _I32,
                               ctypes.c_float, _P, _P]),
 }

@@ -38,24 +38,24 @@ __global__ void qkv_rope_kernel(const float* __restrict__ qkv, const double2* __
     }
 }
 
-// One CTA per (fixed row f, head h).  Keys/values of row t come from the
-// fresh rows when fresh_of[t] >= 0, else from the context planes; row f sees
-// t <= fix_idx[f] (causal by sequence index).
-__global__ void __launch_bounds__(128)
-    attention_kernel(const float* __restrict__ q, const float* __restrict__ k_fresh,
-                     const float* __restrict__ v_fresh, const float* __restrict__ ctx_k,
-                     const float* __restrict__ ctx_v, const int32_t* __restrict__ fresh_of,
-                     const int64_t* __restrict__ fix_idx, int H, int D, float scale,
-                     float* __restrict__ mix) {
-    extern __shared__ float s_score[];
+// Attention of one fixed row over its context, for one head (one CTA).
+// Keys/values of token t come from the fresh rows when fresh_of[t] >= 0,
+// else from the context planes; the row sees t < tn (causal by sequence
+// index, tn = fix_idx + 1).
+__device__ __forceinline__ void attend_row(const float* __restrict__ q_row,
+                                           const float* __restrict__ k_fresh,
+                                           const float* __restrict__ v_fresh,
+                                           const float* __restrict__ ctx_k,
+                                           const float* __restrict__ ctx_v,
+                                           const int32_t* __restrict__ fresh_of, int tn, int h,
+                                           int H, int D, float scale, float* __restrict__ mix_row,
+                                           float* s_score) {
     __shared__ float s_q[256];
     __shared__ float s_red[32];
     __shared__ double s_redd[32];
-    const int f = blockIdx.x, h = blockIdx.y;
     const int hid = H * D;
     const int tid = threadIdx.x, nthr = blockDim.x;
-    const int tn = (int)fix_idx[f] + 1;
-    for (int d = tid; d < D; d += nthr) s_q[d] = q[(size_t)f * hid + h * D + d];
+    for (int d = tid; d < D; d += nthr) s_q[d] = q_row[h * D + d];
     __syncthreads();
 
     float mx = -INFINITY;
@@ -105,8 +105,45 @@ __global__ void __launch_bounds__(128)
                                      : ctx_v[(size_t)t * hid + h * D + d];
             acc += (double)s_score[t] * (double)vv;
         }
-        mix[(size_t)f * hid + h * D + d] = (float)acc;
+        mix_row[h * D + d] = (float)acc;
     }
+}
+
+// One CTA per (fixed row f, head h) of one context.
+__global__ void __launch_bounds__(128)
+    attention_kernel(const float* __restrict__ q, const float* __restrict__ k_fresh,
+                     const float* __restrict__ v_fresh, const float* __restrict__ ctx_k,
+                     const float* __restrict__ ctx_v, const int32_t* __restrict__ fresh_of,
+                     const int64_t* __restrict__ fix_idx, int H, int D, float scale,
+                     float* __restrict__ mix) {
+    extern __shared__ float s_score[];
+    const int f = blockIdx.x, h = blockIdx.y;
+    const size_t hid = (size_t)H * D;
+    attend_row(q + f * hid, k_fresh, v_fresh, ctx_k, ctx_v, fresh_of, (int)fix_idx[f] + 1, h, H,
+               D, scale, mix + f * hid, s_score);
+}
+
+// Several members' fixed rows in one launch (grouped recovery): row r
+// belongs to the member whose [row0, row0 + n_rows) holds it; its fresh rows
+// are the member's slice of the concatenated fresh planes.
+__global__ void __launch_bounds__(128)
+    attention_many_kernel(const float* __restrict__ q, const float* __restrict__ k_fresh,
+                          const float* __restrict__ v_fresh,
+                          const tdkv_attn_member* __restrict__ members, int n_members, int layer,
+                          int H, int D, float scale, float* __restrict__ mix) {
+    extern __shared__ float s_score[];
+    const int r = blockIdx.x, h = blockIdx.y;
+    int lo = 0, hi = n_members - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (members[mid].row0 <= r) lo = mid; else hi = mid - 1;
+    }
+    const tdkv_attn_member m = members[lo];
+    const size_t hid = (size_t)H * D;
+    const size_t lofs = (size_t)layer * m.ctx_layer_stride;
+    attend_row(q + r * hid, k_fresh + (size_t)m.row0 * hid, v_fresh + (size_t)m.row0 * hid,
+               m.ctx_k + lofs, m.ctx_v + lofs, m.fresh_of, (int)m.fix_idx[r - m.row0] + 1, h, H,
+               D, scale, mix + r * hid, s_score);
 }
 
 }  // namespace tdkv
@@ -151,4 +188,29 @@ extern "C" int32_t tdkv_attention(const float* d_q, const float* d_k_fresh, cons
         scale, d_mix);
     count_launch();
     return check_launch("tdkv_attention");
+}
+
+extern "C" int32_t tdkv_attention_many(const float* d_q, const float* d_k_fresh,
+                                       const float* d_v_fresh, const tdkv_attn_member* d_members,
+                                       int32_t n_members, int32_t layer, int32_t total_rows,
+                                       int32_t max_tokens, int32_t num_heads, int32_t head_dim,
+                                       float scale, float* d_mix, void* stream) {
+    if (n_members < 0 || total_rows < 0 || layer < 0 || max_tokens <= 0 || num_heads <= 0 ||
+        head_dim <= 0 || head_dim > 256)
+        return set_error(TDKV_EINVAL, "tdkv_attention_many: bad geometry");
+    if (n_members == 0 || total_rows == 0) return TDKV_OK;
+    if (!d_q || !d_k_fresh || !d_v_fresh || !d_members || !d_mix)
+        return set_error(TDKV_EINVAL, "tdkv_attention_many: null pointer");
+    const size_t smem = (size_t)max_tokens * sizeof(float);
+    if (smem > 200 * 1024)
+        return set_error(TDKV_EUNSUPPORTED, "tdkv_attention_many: %d tokens exceed shared memory",
+                         max_tokens);
+    if (cudaFuncSetAttribute(attention_many_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+        return check_launch("tdkv_attention_many: cudaFuncSetAttribute");
+    dim3 grid(total_rows, num_heads);
+    attention_many_kernel<<<grid, 128, smem, static_cast<cudaStream_t>(stream)>>>(
+        d_q, d_k_fresh, d_v_fresh, d_members, n_members, layer, num_heads, head_dim, scale, d_mix);
+    count_launch();
+    return check_launch("tdkv_attention_many");
 }

@@ -24,7 +24,8 @@ import numpy as np
 import torch
 
 from . import _kernels, _lib
-from ._device import default_device, h2d, is_host, ptr, stream_handle, to_device, to_host
+from ._device import (default_device, h2d, is_host, ptr, stream_handle, to_device, to_host,
+                      upload)
 from .core import LayeredKv
 from .gemm import gemm_tn
 from .ledger import CostLedger
@@ -128,6 +129,77 @@ def _forward(m: ToyModel, toks, pos, fix, ck, cv, layers, out_k, out_v) -> int:
         gemm_tn(mix, m.wm_t[layer], out=h, accumulate=True)
         launches += 2
     return launches
+
+
+def forward_many(m: ToyModel, items, layers: int):
+    """The selective forward of several independent requests as ONE batch:
+    ``items`` = [(tokens, positions, fix_idx, ctx_k, ctx_v)] (host integer
+    arrays; device float32 context planes of shape (L, T_i, H, D), or None
+    when every attended row is fresh).  Per layer one QKV GEMM, one rotary
+    launch, one attention launch and one mix GEMM cover every item's fixed
+    rows (grouped recovery, collective.py:152-187, batches its members this
+    way); row results do not depend on the batch (rows are independent in
+    the GEMMs and attend only to their own item's context).
+
+    Returns (out_k, out_v, row0): planes (layers, sum F_i, H, D) with item i's
+    rows at [row0[i], row0[i] + F_i)."""
+    dev = m.device
+    H, D, hid = m.num_heads, m.head_dim, m.hidden
+    fixes = [np.asarray(it[2], np.int64) for it in items]
+    F = np.array([f.size for f in fixes], np.int64)
+    row0 = np.concatenate([[0], np.cumsum(F)[:-1]]).astype(np.int64)
+    R = int(F.sum())
+    out_k = torch.empty((layers, max(R, 1), H, D), dtype=torch.float32, device=dev)
+    out_v = torch.empty_like(out_k)
+    if R == 0 or layers == 0:
+        return out_k, out_v, row0
+    toks = [np.asarray(it[0], np.int64) for it in items]
+    pos = [np.asarray(it[1], np.int64) for it in items]
+    Ts = [t.size for t in toks]
+    # one upload: every item's fix indices (int64) then fresh_of maps (int32)
+    fresh_of = np.full(int(sum(Ts)), -1, np.int32)
+    t0 = np.concatenate([[0], np.cumsum(Ts)[:-1]]).astype(np.int64)
+    for i, f in enumerate(fixes):
+        fresh_of[t0[i] + f] = np.arange(f.size, dtype=np.int32)
+    meta = np.concatenate([np.concatenate(fixes).view(np.uint8), fresh_of.view(np.uint8)])
+    d_meta = h2d(meta, dev)
+    fix_base = ptr(d_meta)
+    fo_base = fix_base + 8 * R
+    table = _kernels.rope_table(np.concatenate([p[f] for p, f in zip(pos, fixes)]), D,
+                                m.rope_base, torch.float32, dev)
+    h = torch.empty((R, hid), dtype=torch.float32, device=dev)
+    d_tok = h2d(np.concatenate([t[f] for t, f in zip(toks, fixes)]), dev)
+    job = _kernels.rows_job(m.embed, None, 0, h, None, 0, R, src_rows=d_tok)
+    _kernels.rows(_kernels.rows_jobs([job]), R, None, 1, 1, hid, _kernels.ROWS_BLOCK,
+                  torch.float32, dev)
+    qkv = torch.empty((R, 3 * hid), dtype=torch.float32, device=dev)
+    q = torch.empty((R, hid), dtype=torch.float32, device=dev)
+    mix = torch.empty((R, hid), dtype=torch.float32, device=dev)
+    members = np.zeros(len(items), _lib.ATTN_MEMBER)
+    for i, it in enumerate(items):
+        ck, cv = it[3], it[4]
+        if ck is None:                       # every attended row is fresh: never read
+            ck = cv = out_k
+            stride = 0
+        else:
+            stride = int(ck.shape[1]) * hid
+        members[i] = (ptr(ck), ptr(cv), fo_base + 4 * int(t0[i]), fix_base + 8 * int(row0[i]),
+                      stride, int(row0[i]), int(F[i]), Ts[i], 0)
+    live = F > 0
+    d_members = upload(members[live], dev)
+    n_live = int(live.sum())
+    scale = float(np.float32(1.0 / np.sqrt(D)))
+    stream = stream_handle(dev)
+    for layer in range(layers):
+        gemm_tn(h, m.wqkv_t[layer], out=qkv)
+        _lib.call("tdkv_qkv_rope", ptr(qkv), ptr(table), R, H, D, ptr(q), ptr(out_k[layer]),
+                  ptr(out_v[layer]), stream)
+        if layer == layers - 1:
+            break                       # the last layer's attention only feeds h
+        _lib.call("tdkv_attention_many", ptr(q), ptr(out_k[layer]), ptr(out_v[layer]),
+                  ptr(d_members), n_live, layer, R, max(Ts), H, D, scale, ptr(mix), stream)
+        gemm_tn(mix, m.wm_t[layer], out=h, accumulate=True)
+    return out_k, out_v, row0
 
 
 def full_prefill(weights, tokens: Sequence[int], start_pos: int = 0) -> LayeredKv:
