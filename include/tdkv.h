@@ -303,7 +303,12 @@ int32_t tdkv_attention(const float* d_q, const float* d_k_fresh, const float* d_
  * of q / fresh K,V / mix are the members' rows concatenated; member m owns
  * rows [row0, row0 + n_rows), attends over its own context (layer ``layer``
  * of planes with ctx_layer_stride elements per layer), and its fresh_of
- * indexes its own slice of the fresh rows.  d_members sorted by row0. */
+ * indexes its own slice of the fresh rows.  d_members sorted by row0.
+ * n_tiles > 0 selects the query-tiled kernel (head_dim <= 128): member m's
+ * rows form ceil(n_rows / 8) tiles starting at tile index tile0
+ * (n_tiles in total), each CTA serving 8 rows of
+ * one member with every staged key/value tile; n_tiles == 0 runs one CTA per
+ * row. */
 typedef struct {
     const float* ctx_k;          /* (L, num_tokens, H*D) context planes */
     const float* ctx_v;
@@ -313,13 +318,14 @@ typedef struct {
     int32_t row0;
     int32_t n_rows;
     int32_t num_tokens;
-    int32_t pad;
+    int32_t tile0;               /* first query tile (n_tiles > 0) */
 } tdkv_attn_member;
 
 int32_t tdkv_attention_many(const float* d_q, const float* d_k_fresh, const float* d_v_fresh,
                             const tdkv_attn_member* d_members, int32_t n_members, int32_t layer,
-                            int32_t total_rows, int32_t max_tokens, int32_t num_heads,
-                            int32_t head_dim, float scale, float* d_mix, void* stream);
+                            int32_t total_rows, int32_t n_tiles, int32_t max_tokens,
+                            int32_t num_heads, int32_t head_dim, float scale, float* d_mix,
+                            void* stream);
 
 /* ------------------------------------------------------------------------
  * Host slot allocator of the paged pool, policy of

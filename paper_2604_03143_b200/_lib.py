@@ -87,7 +87,7 @@ WIRE_SEG = np.dtype([("offset", "<u8"), ("nbytes", "<u8"), ("ptr", "<u8"), ("kin
                      ("pad", "<i4")])
 ATTN_MEMBER = np.dtype([("ctx_k", "<u8"), ("ctx_v", "<u8"), ("fresh_of", "<u8"),
                         ("fix_idx", "<u8"), ("ctx_layer_stride", "<i8"), ("row0", "<i4"),
-                        ("n_rows", "<i4"), ("num_tokens", "<i4"), ("pad", "<i4")])
+                        ("n_rows", "<i4"), ("num_tokens", "<i4"), ("tile0", "<i4")])
 WIRE_RAW, WIRE_BF16_TO_F32, WIRE_F32_TO_BF16 = 0, 1, 2
 assert WIRE_SEG.itemsize == 32 and ATTN_MEMBER.itemsize == 56
 assert COLLECT_JOB.itemsize == 24 and COLLECT_UNIT.itemsize == 16
@@ -146,7 +146,7 @@ _SIGS = {
     "tdkv_segidx_evict": (_I32, [_P, _I64, _P, _P, _P, _I32, _P]),
     "tdkv_segidx_entries": (_I32, [_P, _P, _I64, _P]),
     "tdkv_wire_unpack": (_I32, [_P, _I32, _I64, _P, _P]),
-    "tdkv_attention_many": (_I32, [_P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32,
+    "tdkv_attention_many": (_I32, [_P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _I32,
                                    ctypes.c_float, _P, _P]),
     "tdkv_attention": (_I32, [_P, _P, _P, _P, _P, _P, _P, _I32, _I32, _I32, _I32,
                               ctypes.c_float, _P, _P]),

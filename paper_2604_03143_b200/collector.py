@@ -703,15 +703,18 @@ def _scatter_back(jobs, offs, staged: torch.Tensor, contexts, plane: int) -> Non
             contexts[i][plane][:, np.asarray(hit.target_idx)] = host[:, off:off + n]
         return
     L, R, H, D = staged.shape
-    recs = []
-    for (i, hit), off in zip(jobs, offs):
+    hd = H * D
+    esz = staged.element_size()
+    # every hit's target rows in one upload; sources are contiguous runs of
+    # the staged plane (an address offset, no source index array)
+    targets = [np.asarray(hit.target_idx, np.int64) for _, hit in jobs]
+    d_rows = h2d(np.concatenate(targets), staged.device)
+    base = ptr(d_rows)
+    recs, t_off = [], 0
+    for (i, hit), off, tgt in zip(jobs, offs, targets):
         ctx = contexts[i][plane]
-        n = len(hit.target_idx)
-        src_rows = torch.arange(off, off + n, device=staged.device, dtype=torch.int64)
-        dst_rows = torch.as_tensor(np.asarray(hit.target_idx, np.int64), device=staged.device)
-        recs.append((_kernels.rows_job(staged, None, R * H * D, ctx, None,
-                                       int(ctx.shape[1]) * H * D, n, src_rows=src_rows,
-                                       dst_rows=dst_rows), src_rows, dst_rows))
-    arr = _kernels.rows_jobs([r[0] for r in recs])
-    _kernels.rows(arr, max(len(h.target_idx) for _, h in jobs), None, L, H, D,
+        recs.append((ptr(staged) + esz * hd * off, 0, R * hd, 0, 0, 0, 0, 0, ptr(ctx), 0,
+                     int(ctx.shape[1]) * hd, base + 8 * t_off, tgt.size, 0, 0, 0))
+        t_off += tgt.size
+    _kernels.rows(_kernels.rows_jobs(recs), max(t.size for t in targets), None, L, H, D,
                   _kernels.ROWS_BLOCK, staged.dtype, staged.device)

@@ -41,7 +41,18 @@ __global__ void qkv_rope_kernel(const float* __restrict__ qkv, const double2* __
 // Attention of one fixed row over its context, for one head (one CTA).
 // Keys/values of token t come from the fresh rows when fresh_of[t] >= 0,
 // else from the context planes; the row sees t < tn (causal by sequence
-// index, tn = fix_idx + 1).
+// index, tn = fix_idx + 1).  Key and value rows are staged kTile tokens at
+// a time in shared memory with coalesced loads (rows padded to D+1 floats:
+// conflict-free column reads); every score is one sequential fmaf chain over
+// d and every output one sequential float64 sum over t, so the arithmetic is
+// the same whatever the tiling.
+constexpr int kAttnTile = 32;
+
+// fixed rows per CTA of the query-tiled attention (the host tiles with the
+// same rule)
+// (16-row tiles measured slower: 80 registers and 70 KB of scores per CTA)
+__host__ __device__ inline int attn_rows_per_tile(int) { return 8; }
+
 __device__ __forceinline__ void attend_row(const float* __restrict__ q_row,
                                            const float* __restrict__ k_fresh,
                                            const float* __restrict__ v_fresh,
@@ -49,24 +60,39 @@ __device__ __forceinline__ void attend_row(const float* __restrict__ q_row,
                                            const float* __restrict__ ctx_v,
                                            const int32_t* __restrict__ fresh_of, int tn, int h,
                                            int H, int D, float scale, float* __restrict__ mix_row,
-                                           float* s_score) {
+                                           float* s_score, float* s_tile) {
     __shared__ float s_q[256];
     __shared__ float s_red[32];
     __shared__ double s_redd[32];
     const int hid = H * D;
     const int tid = threadIdx.x, nthr = blockDim.x;
+    const int pitch = D + 1;
     for (int d = tid; d < D; d += nthr) s_q[d] = q_row[h * D + d];
-    __syncthreads();
+    // stage rows [t0, t0 + kAttnTile) of the K or V plane (fresh or cached)
+    auto stage = [&](const float* fresh, const float* ctx, int t0) {
+        const int n = min(kAttnTile, tn - t0);
+        for (int i = tid; i < n * D; i += nthr) {
+            const int t = i / D, d = i - t * D;
+            const int fr = fresh_of[t0 + t];
+            const float* src = fr >= 0 ? fresh + (size_t)fr * hid : ctx + (size_t)(t0 + t) * hid;
+            s_tile[t * pitch + d] = src[h * D + d];
+        }
+    };
 
     float mx = -INFINITY;
-    for (int t = tid; t < tn; t += nthr) {
-        const int fr = fresh_of[t];
-        const float* kr = fr >= 0 ? k_fresh + (size_t)fr * hid + h * D : ctx_k + (size_t)t * hid + h * D;
-        float acc = 0.f;
-        for (int d = 0; d < D; ++d) acc = fmaf(s_q[d], kr[d], acc);
-        const float sc = acc * scale;
-        s_score[t] = sc;
-        mx = fmaxf(mx, sc);
+    for (int t0 = 0; t0 < tn; t0 += kAttnTile) {
+        __syncthreads();                   // s_q ready / previous tile consumed
+        stage(k_fresh, ctx_k, t0);
+        __syncthreads();
+        const int n = min(kAttnTile, tn - t0);
+        for (int t = tid; t < n; t += nthr) {
+            const float* kr = s_tile + t * pitch;
+            float acc = 0.f;
+            for (int d = 0; d < D; ++d) acc = fmaf(s_q[d], kr[d], acc);
+            const float sc = acc * scale;
+            s_score[t0 + t] = sc;
+            mx = fmaxf(mx, sc);
+        }
     }
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if ((tid & 31) == 0) s_red[tid >> 5] = mx;
@@ -96,17 +122,22 @@ __device__ __forceinline__ void attend_row(const float* __restrict__ q_row,
     __syncthreads();
     const float total = (float)s_redd[0];
     for (int t = tid; t < tn; t += nthr) s_score[t] = s_score[t] / total;
-    __syncthreads();
-    for (int d = tid; d < D; d += nthr) {
-        double acc = 0.0;
-        for (int t = 0; t < tn; ++t) {
-            const int fr = fresh_of[t];
-            const float vv = fr >= 0 ? v_fresh[(size_t)fr * hid + h * D + d]
-                                     : ctx_v[(size_t)t * hid + h * D + d];
-            acc += (double)s_score[t] * (double)vv;
-        }
-        mix_row[h * D + d] = (float)acc;
+    double acc0 = 0.0, acc1 = 0.0;         // output elements d = tid, tid + nthr (D <= 256)
+    const int d0 = tid, d1 = tid + nthr;
+    for (int t0 = 0; t0 < tn; t0 += kAttnTile) {
+        __syncthreads();                   // probabilities written / previous tile consumed
+        stage(v_fresh, ctx_v, t0);
+        __syncthreads();
+        const int n = min(kAttnTile, tn - t0);
+        if (d0 < D)
+            for (int t = 0; t < n; ++t)
+                acc0 += (double)s_score[t0 + t] * (double)s_tile[t * pitch + d0];
+        if (d1 < D)
+            for (int t = 0; t < n; ++t)
+                acc1 += (double)s_score[t0 + t] * (double)s_tile[t * pitch + d1];
     }
+    if (d0 < D) mix_row[h * D + d0] = (float)acc0;
+    if (d1 < D) mix_row[h * D + d1] = (float)acc1;
 }
 
 // One CTA per (fixed row f, head h) of one context.
@@ -116,11 +147,11 @@ __global__ void __launch_bounds__(128)
                      const float* __restrict__ ctx_v, const int32_t* __restrict__ fresh_of,
                      const int64_t* __restrict__ fix_idx, int H, int D, float scale,
                      float* __restrict__ mix) {
-    extern __shared__ float s_score[];
+    extern __shared__ float s_dyn[];      // [tile (kAttnTile x D+1) | scores]
     const int f = blockIdx.x, h = blockIdx.y;
     const size_t hid = (size_t)H * D;
     attend_row(q + f * hid, k_fresh, v_fresh, ctx_k, ctx_v, fresh_of, (int)fix_idx[f] + 1, h, H,
-               D, scale, mix + f * hid, s_score);
+               D, scale, mix + f * hid, s_dyn + kAttnTile * (D + 1), s_dyn);
 }
 
 // Several members' fixed rows in one launch (grouped recovery): row r
@@ -131,7 +162,7 @@ __global__ void __launch_bounds__(128)
                           const float* __restrict__ v_fresh,
                           const tdkv_attn_member* __restrict__ members, int n_members, int layer,
                           int H, int D, float scale, float* __restrict__ mix) {
-    extern __shared__ float s_score[];
+    extern __shared__ float s_dyn[];      // [tile (kAttnTile x D+1) | scores]
     const int r = blockIdx.x, h = blockIdx.y;
     int lo = 0, hi = n_members - 1;
     while (lo < hi) {
@@ -143,7 +174,134 @@ __global__ void __launch_bounds__(128)
     const size_t lofs = (size_t)layer * m.ctx_layer_stride;
     attend_row(q + r * hid, k_fresh + (size_t)m.row0 * hid, v_fresh + (size_t)m.row0 * hid,
                m.ctx_k + lofs, m.ctx_v + lofs, m.fresh_of, (int)m.fix_idx[r - m.row0] + 1, h, H,
-               D, scale, mix + r * hid, s_score);
+               D, scale, mix + r * hid, s_dyn + kAttnTile * (D + 1), s_dyn);
+}
+
+// Query-tiled form of attention_many_kernel: one CTA per (4 * QW consecutive
+// fixed rows of one member, head).  Every staged key/value tile serves all
+// 4 * QW queries, so staging and index work are amortized that many times and
+// each thread carries several independent accumulators.  Warp w owns queries
+// w, w + 4, ... (scores, max, softmax); thread i owns outputs (q, d) for
+// q * D + d = i, i + 128, ... .  Scores are sequential fmaf chains over d and
+// outputs sequential float64 sums over t, as in attend_row.
+template <int QW>   // queries per warp; kQ = 4 * QW rows per CTA
+__global__ void __launch_bounds__(128)
+    attention_tiles_kernel(const float* __restrict__ q, const float* __restrict__ k_fresh,
+                           const float* __restrict__ v_fresh,
+                           const tdkv_attn_member* __restrict__ members, int n_members, int layer,
+                           int H, int D, float scale, int max_tokens, float* __restrict__ mix) {
+    constexpr int kAttnQ = 4 * QW;
+    extern __shared__ float s_dyn[];   // [tile kAttnTile x (D+1) | q kAttnQ x D | p kAttnQ x max_tokens]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int h = blockIdx.y;
+    int lo = 0, hi = n_members - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (members[mid].tile0 <= (int)blockIdx.x) lo = mid; else hi = mid - 1;
+    }
+    const tdkv_attn_member m = members[lo];
+    const int r0 = ((int)blockIdx.x - m.tile0) * kAttnQ;          // member-local first row
+    const int nq = min(kAttnQ, m.n_rows - r0);
+    const int hid = H * D;
+    const int pitch = D + 1;
+    float* s_tile = s_dyn;
+    float* s_q = s_tile + kAttnTile * pitch;
+    float* s_p = s_q + kAttnQ * D;
+    const size_t lofs = (size_t)layer * m.ctx_layer_stride;
+    const float* ctx_k = m.ctx_k + lofs;
+    const float* ctx_v = m.ctx_v + lofs;
+    const float* kf = k_fresh + (size_t)m.row0 * hid;
+    const float* vf = v_fresh + (size_t)m.row0 * hid;
+    const int32_t* fresh_of = m.fresh_of;
+    int tnq[QW];                                                 // this warp's queries' lengths
+#pragma unroll
+    for (int j = 0; j < QW; ++j) {
+        const int qi = warp + 4 * j;
+        tnq[j] = qi < nq ? (int)m.fix_idx[r0 + qi] + 1 : 0;
+    }
+    const int tn = (int)m.fix_idx[r0 + nq - 1] + 1;              // rows ascend: the longest
+    for (int i = tid; i < nq * D; i += blockDim.x) {
+        const int qi = i / D, d = i - qi * D;
+        s_q[i] = q[(size_t)(m.row0 + r0 + qi) * hid + h * D + d];
+    }
+    auto stage = [&](const float* fresh, const float* ctx, int t0, int n) {
+        for (int t = warp; t < n; t += 4) {
+            const int fr = fresh_of[t0 + t];
+            const float* src = (fr >= 0 ? fresh + (size_t)fr * hid : ctx + (size_t)(t0 + t) * hid) + h * D;
+            for (int d = lane; d < D; d += 32) s_tile[t * pitch + d] = src[d];
+        }
+    };
+    // scores
+    float mx[QW];
+#pragma unroll
+    for (int j = 0; j < QW; ++j) mx[j] = -INFINITY;
+    for (int t0 = 0; t0 < tn; t0 += kAttnTile) {
+        const int n = min(kAttnTile, tn - t0);
+        __syncthreads();
+        stage(kf, ctx_k, t0, n);
+        __syncthreads();
+        if (lane < n) {
+            const float* kr = s_tile + lane * pitch;
+#pragma unroll
+            for (int j = 0; j < QW; ++j) {
+                const int qi = warp + 4 * j;
+                if (t0 + lane < tnq[j]) {
+                    const float* qq = s_q + qi * D;
+                    float acc = 0.f;
+                    for (int d = 0; d < D; ++d) acc = fmaf(qq[d], kr[d], acc);
+                    const float sc = acc * scale;
+                    s_p[qi * max_tokens + t0 + lane] = sc;
+                    mx[j] = fmaxf(mx[j], sc);
+                }
+            }
+        }
+    }
+    // softmax of this warp's queries
+#pragma unroll
+    for (int j = 0; j < QW; ++j) {
+        const int qi = warp + 4 * j;
+        if (qi >= nq) continue;
+        float mj = mx[j];
+        for (int o = 16; o > 0; o >>= 1) mj = fmaxf(mj, __shfl_xor_sync(0xffffffffu, mj, o));
+        float* p = s_p + qi * max_tokens;
+        double sum = 0.0;
+        for (int t = lane; t < tnq[j]; t += 32) {
+            const float e = expf(p[t] - mj);
+            p[t] = e;
+            sum += (double)e;
+        }
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        const float total = (float)sum;
+        for (int t = lane; t < tnq[j]; t += 32) p[t] = p[t] / total;
+    }
+    // outputs
+    // thread outputs i = tid + 128 k < kAttnQ * D (D <= 128: at most kAttnQ)
+    double acc[kAttnQ];
+#pragma unroll
+    for (int k = 0; k < kAttnQ; ++k) acc[k] = 0.0;
+    for (int t0 = 0; t0 < tn; t0 += kAttnTile) {
+        const int n = min(kAttnTile, tn - t0);
+        __syncthreads();
+        stage(vf, ctx_v, t0, n);
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kAttnQ; ++k) {
+            const int i = tid + k * 128;
+            if (i >= nq * D) break;
+            const int qi = i / D, d = i - qi * D;
+            const int tq = (int)m.fix_idx[r0 + qi] + 1;
+            const float* p = s_p + qi * max_tokens + t0;
+            const int nn = min(n, tq - t0);
+            for (int t = 0; t < nn; ++t) acc[k] += (double)p[t] * (double)s_tile[t * pitch + d];
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < kAttnQ; ++k) {
+        const int i = tid + k * 128;
+        if (i >= nq * D) break;
+        const int qi = i / D, d = i - qi * D;
+        mix[(size_t)(m.row0 + r0 + qi) * hid + h * D + d] = (float)acc[k];
+    }
 }
 
 }  // namespace tdkv
@@ -175,7 +333,7 @@ extern "C" int32_t tdkv_attention(const float* d_q, const float* d_k_fresh, cons
     if (n_fix < 0 || num_tokens <= 0 || num_heads <= 0 || head_dim <= 0 || head_dim > 256)
         return set_error(TDKV_EINVAL, "tdkv_attention: bad geometry");
     if (n_fix == 0) return TDKV_OK;
-    const size_t smem = (size_t)num_tokens * sizeof(float);
+    const size_t smem = ((size_t)num_tokens + (size_t)kAttnTile * (head_dim + 1)) * sizeof(float);
     if (smem > 200 * 1024)
         return set_error(TDKV_EUNSUPPORTED, "tdkv_attention: %d tokens exceed shared memory",
                          num_tokens);
@@ -193,18 +351,37 @@ extern "C" int32_t tdkv_attention(const float* d_q, const float* d_k_fresh, cons
 extern "C" int32_t tdkv_attention_many(const float* d_q, const float* d_k_fresh,
                                        const float* d_v_fresh, const tdkv_attn_member* d_members,
                                        int32_t n_members, int32_t layer, int32_t total_rows,
-                                       int32_t max_tokens, int32_t num_heads, int32_t head_dim,
-                                       float scale, float* d_mix, void* stream) {
-    if (n_members < 0 || total_rows < 0 || layer < 0 || max_tokens <= 0 || num_heads <= 0 ||
-        head_dim <= 0 || head_dim > 256)
+                                       int32_t n_tiles, int32_t max_tokens, int32_t num_heads,
+                                       int32_t head_dim, float scale, float* d_mix,
+                                       void* stream) {
+    if (n_members < 0 || total_rows < 0 || n_tiles < 0 || layer < 0 || max_tokens <= 0 ||
+        num_heads <= 0 || head_dim <= 0 || head_dim > 256)
         return set_error(TDKV_EINVAL, "tdkv_attention_many: bad geometry");
     if (n_members == 0 || total_rows == 0) return TDKV_OK;
     if (!d_q || !d_k_fresh || !d_v_fresh || !d_members || !d_mix)
         return set_error(TDKV_EINVAL, "tdkv_attention_many: null pointer");
-    const size_t smem = (size_t)max_tokens * sizeof(float);
+    const size_t smem = ((size_t)max_tokens + (size_t)kAttnTile * (head_dim + 1)) * sizeof(float);
     if (smem > 200 * 1024)
         return set_error(TDKV_EUNSUPPORTED, "tdkv_attention_many: %d tokens exceed shared memory",
                          max_tokens);
+    if (n_tiles > 0 && head_dim <= 128) {
+        const int kq = attn_rows_per_tile(head_dim);
+        const size_t tsmem = ((size_t)kAttnTile * (head_dim + 1) + (size_t)kq * head_dim +
+                              (size_t)kq * max_tokens) * sizeof(float);
+        if (tsmem > 200 * 1024)
+            return set_error(TDKV_EUNSUPPORTED,
+                             "tdkv_attention_many: %d tokens exceed shared memory", max_tokens);
+        auto kern = attention_tiles_kernel<2>;
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)tsmem) != cudaSuccess)
+            return check_launch("tdkv_attention_many: cudaFuncSetAttribute");
+        dim3 tgrid(n_tiles, num_heads);
+        kern<<<tgrid, 128, tsmem, static_cast<cudaStream_t>(stream)>>>(
+            d_q, d_k_fresh, d_v_fresh, d_members, n_members, layer, num_heads, head_dim, scale,
+            max_tokens, d_mix);
+        count_launch();
+        return check_launch("tdkv_attention_many");
+    }
     if (cudaFuncSetAttribute(attention_many_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess)
         return check_launch("tdkv_attention_many: cudaFuncSetAttribute");

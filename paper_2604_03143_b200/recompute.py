@@ -131,6 +131,11 @@ def _forward(m: ToyModel, toks, pos, fix, ck, cv, layers, out_k, out_v) -> int:
     return launches
 
 
+def _attn_rows_per_tile(head_dim: int) -> int:
+    """Fixed rows per CTA of the query-tiled attention (attn_rows_per_tile)."""
+    return 8
+
+
 def forward_many(m: ToyModel, items, layers: int):
     """The selective forward of several independent requests as ONE batch:
     ``items`` = [(tokens, positions, fix_idx, ctx_k, ctx_v)] (host integer
@@ -176,6 +181,9 @@ def forward_many(m: ToyModel, items, layers: int):
     q = torch.empty((R, hid), dtype=torch.float32, device=dev)
     mix = torch.empty((R, hid), dtype=torch.float32, device=dev)
     members = np.zeros(len(items), _lib.ATTN_MEMBER)
+    tiles = -(-F // _attn_rows_per_tile(D))       # query tiles per member
+    tile0 = np.concatenate([[0], np.cumsum(tiles)[:-1]]).astype(np.int64)
+    n_tiles = int(tiles.sum()) if D <= 128 else 0
     for i, it in enumerate(items):
         ck, cv = it[3], it[4]
         if ck is None:                       # every attended row is fresh: never read
@@ -184,7 +192,7 @@ def forward_many(m: ToyModel, items, layers: int):
         else:
             stride = int(ck.shape[1]) * hid
         members[i] = (ptr(ck), ptr(cv), fo_base + 4 * int(t0[i]), fix_base + 8 * int(row0[i]),
-                      stride, int(row0[i]), int(F[i]), Ts[i], 0)
+                      stride, int(row0[i]), int(F[i]), Ts[i], int(tile0[i]))
     live = F > 0
     d_members = upload(members[live], dev)
     n_live = int(live.sum())
@@ -197,7 +205,8 @@ def forward_many(m: ToyModel, items, layers: int):
         if layer == layers - 1:
             break                       # the last layer's attention only feeds h
         _lib.call("tdkv_attention_many", ptr(q), ptr(out_k[layer]), ptr(out_v[layer]),
-                  ptr(d_members), n_live, layer, R, max(Ts), H, D, scale, ptr(mix), stream)
+                  ptr(d_members), n_live, layer, R, n_tiles, max(Ts), H, D, scale, ptr(mix),
+                  stream)
         gemm_tn(mix, m.wm_t[layer], out=h, accumulate=True)
     return out_k, out_v, row0
 
