@@ -84,51 +84,16 @@ def selective_forward(weights, tokens, positions, fix_idx, ctx_k, ctx_v,
     fix = np.asarray(fix_idx, np.int64)
     T, F = toks.size, fix.size
     layers = m.num_layers if max_layer is None else int(max_layer)
-    out_k = torch.empty((layers, F, H, D), dtype=torch.float32, device=dev)
-    out_v = torch.empty_like(out_k)
     if F and layers:
         ck = to_device(ctx_k, dev, torch.float32)
         cv = to_device(ctx_v, dev, torch.float32)
-        _forward(m, toks, pos, fix, ck, cv, layers, out_k, out_v)
+        out_k, out_v, _ = forward_many(m, [(toks, pos, fix, ck, cv)], layers)
+    else:
+        out_k = torch.empty((layers, F, H, D), dtype=torch.float32, device=dev)
+        out_v = torch.empty_like(out_k)
     if host:
         return to_host(out_k), to_host(out_v)
     return out_k, out_v
-
-
-def _forward(m: ToyModel, toks, pos, fix, ck, cv, layers, out_k, out_v) -> int:
-    dev = m.device
-    H, D, hid = m.num_heads, m.head_dim, m.hidden
-    T, F = toks.size, fix.size
-    stream = stream_handle(dev)
-    d_fix = h2d(fix, dev)
-    fresh_of = np.full(T, -1, np.int32)
-    fresh_of[fix] = np.arange(F, dtype=np.int32)
-    d_fresh_of = h2d(fresh_of, dev)
-    table = _kernels.rope_table(pos[fix], D, m.rope_base, torch.float32, dev)
-    # h = embed[tokens[fix]] (row mover, K-only gather)
-    h = torch.empty((F, hid), dtype=torch.float32, device=dev)
-    d_tok = h2d(toks[fix], dev)
-    job = _kernels.rows_job(m.embed, None, 0, h, None, 0, F, src_rows=d_tok)
-    _kernels.rows(_kernels.rows_jobs([job]), F, None, 1, 1, hid, _kernels.ROWS_BLOCK,
-                  torch.float32, dev)
-    qkv = torch.empty((F, 3 * hid), dtype=torch.float32, device=dev)
-    q = torch.empty((F, hid), dtype=torch.float32, device=dev)
-    mix = torch.empty((F, hid), dtype=torch.float32, device=dev)
-    scale = float(np.float32(1.0 / np.sqrt(D)))
-    launches = 2
-    for layer in range(layers):
-        gemm_tn(h, m.wqkv_t[layer], out=qkv)
-        _lib.call("tdkv_qkv_rope", ptr(qkv), ptr(table), F, H, D, ptr(q), ptr(out_k[layer]),
-                  ptr(out_v[layer]), stream)
-        launches += 2
-        if layer == layers - 1:
-            break                       # the last layer's attention only feeds h
-        _lib.call("tdkv_attention", ptr(q), ptr(out_k[layer]), ptr(out_v[layer]),
-                  ptr(ck[layer]), ptr(cv[layer]), ptr(d_fresh_of), ptr(d_fix), F, T, H, D,
-                  scale, ptr(mix), stream)
-        gemm_tn(mix, m.wm_t[layer], out=h, accumulate=True)
-        launches += 2
-    return launches
 
 
 def _attn_rows_per_tile(head_dim: int) -> int:

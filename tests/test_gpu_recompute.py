@@ -91,3 +91,55 @@ def test_refresh_on_device_context_matches_oracle():
     assert np.abs(dv.cpu().numpy()[:, fix] - wv).max() <= TOL
     others = np.setdiff1d(np.arange(T), fix)
     assert np.array_equal(got_k[:, others], ctx_k[:, others])
+
+
+@pytest.mark.parametrize("D", [8, 64, 128, 256])
+def test_attention_entry_points_agree(D):
+    """tdkv_attention (one context, one CTA per row) and tdkv_attention_many
+    (per-row CTAs and the query-tiled kernel) compute the same attention over
+    ragged members with mixed fresh / cached rows (head_dim 256 has no tiled
+    form)."""
+    from paper_2604_03143_b200 import _lib
+    from paper_2604_03143_b200._device import ptr, stream_handle
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(D)
+    H, L, layer = 2, 2, 1
+    hid = H * D
+    Ts, fixes = [37, 90, 5], []
+    for T in Ts:
+        fixes.append(np.sort(rng.choice(T, max(1, T // 3), replace=False)).astype(np.int64))
+    F = [f.size for f in fixes]
+    R = sum(F)
+    row0 = np.concatenate([[0], np.cumsum(F)[:-1]])
+    q = torch.randn(R, hid, device=dev)
+    kf = torch.randn(R, hid, device=dev)
+    vf = torch.randn(R, hid, device=dev)
+    ctx = [(torch.randn(L, T, hid, device=dev), torch.randn(L, T, hid, device=dev)) for T in Ts]
+    fresh_of = []
+    for T, f in zip(Ts, fixes):
+        fo = np.full(T, -1, np.int32)
+        fo[f] = np.arange(f.size, dtype=np.int32)
+        fresh_of.append(torch.from_numpy(fo).to(dev))
+    d_fix = [torch.from_numpy(f).to(dev) for f in fixes]
+    scale = float(np.float32(1.0 / np.sqrt(D)))
+    stream = stream_handle(dev)
+    want = torch.empty(R, hid, device=dev)
+    for i in range(len(Ts)):
+        sl = slice(int(row0[i]), int(row0[i]) + F[i])
+        _lib.call("tdkv_attention", ptr(q[sl]), ptr(kf[sl]), ptr(vf[sl]), ptr(ctx[i][0][layer]),
+                  ptr(ctx[i][1][layer]), ptr(fresh_of[i]), ptr(d_fix[i]), F[i], Ts[i], H, D,
+                  scale, ptr(want[sl]), stream)
+    members = np.zeros(len(Ts), _lib.ATTN_MEMBER)
+    tiles = -(-np.asarray(F) // 8)
+    tile0 = np.concatenate([[0], np.cumsum(tiles)[:-1]])
+    for i in range(len(Ts)):
+        members[i] = (ptr(ctx[i][0]), ptr(ctx[i][1]), ptr(fresh_of[i]), ptr(d_fix[i]),
+                      Ts[i] * hid, int(row0[i]), F[i], Ts[i], int(tile0[i]))
+    d_members = torch.from_numpy(members.view(np.uint8)).to(dev)
+    for n_tiles in (0, int(tiles.sum())):
+        got = torch.full((R, hid), float("nan"), device=dev)
+        _lib.call("tdkv_attention_many", ptr(q), ptr(kf), ptr(vf), ptr(d_members), len(Ts), layer,
+                  R, n_tiles, max(Ts), H, D, scale, ptr(got), stream)
+        torch.cuda.synchronize()
+        assert torch.isfinite(got).all()
+        assert (got - want).abs().max().item() <= 1e-6, n_tiles
