@@ -293,14 +293,17 @@ class ToyGroup:
 
 
 def toy_round(weights: ToyWeights, num_agents: int = 8, num_segments: int = 4,
-              seg_len: int = 256, hist_len: int = 64, separator: int = 0, seed: int = 0):
+              seg_len: int = 256, hist_len: int = 64, separator: int = 0, seed: int = 0,
+              device: Optional[torch.device] = None):
     """One All-Gather round of the toy model (BASELINE configs[0]: 8 agents x
     4 shared 256-token blocks).  Segment s is agent (s mod N)'s output,
     prefilled after that agent's history and a separator, so its master rows
     carry source positions hist+1 .. hist+seg_len; agent i's prompt is
     hist_i || SEP || seg_pi(0) || SEP || ... with pi = rng(2+i).permutation(S)
     (prepare_request's layout, pic.py:110-163).  Returns the members (one
-    group: equal lengths, one digest set)."""
+    group: equal lengths, one digest set).  ``device``: keep the segment
+    masters resident there (as a B200 deployment does) instead of host numpy
+    planes like the reference's cache entries."""
     from .recompute import full_prefill
     rng = np.random.default_rng(seed)
     V = weights.config.vocab_size
@@ -311,7 +314,10 @@ def toy_round(weights: ToyWeights, num_agents: int = 8, num_segments: int = 4,
         producer = np.concatenate([hists[s % num_agents], [separator], outputs[s]])
         kv = full_prefill(weights, producer)
         lo = hist_len + 1
-        segs.append(type(kv)(kv.k[:, lo:].copy(), kv.v[:, lo:].copy(), kv.positions[lo:].copy()))
+        k, v = kv.k[:, lo:].copy(), kv.v[:, lo:].copy()
+        if device is not None:
+            k, v = torch.from_numpy(k).to(device), torch.from_numpy(v).to(device)
+        segs.append(type(kv)(k, v, kv.positions[lo:].copy()))
     members = []
     for i in range(num_agents):
         order = np.random.default_rng(2 + i).permutation(num_segments)
