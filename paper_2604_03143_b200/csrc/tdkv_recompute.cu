@@ -42,11 +42,33 @@ __global__ void qkv_rope_kernel(const float* __restrict__ qkv, const double2* __
 // Keys/values of token t come from the fresh rows when fresh_of[t] >= 0,
 // else from the context planes; the row sees t < tn (causal by sequence
 // index, tn = fix_idx + 1).  Key and value rows are staged kTile tokens at
-// a time in shared memory with coalesced loads (rows padded to D+1 floats:
-// conflict-free column reads); every score is one sequential fmaf chain over
+// a time in shared memory with coalesced loads (rows padded to an even pitch:
+// at most 2-way conflicted column reads); every score is one sequential fmaf chain over
 // d and every output one sequential float64 sum over t, so the arithmetic is
 // the same whatever the tiling.
 constexpr int kAttnTile = 32;
+
+// staged rows are padded to an even pitch: 8-byte async copies stay aligned
+// and column reads by 32 lanes (one token each) are at most 2-way conflicted
+__host__ __device__ inline int attn_pitch(int D) { return D + 2; }
+
+// Stage head h of rows [t0, t0 + n) of the K or V plane (fresh row when
+// fresh_of[t] >= 0, else the context row) into s_tile: one warp per row, each
+// lane issuing 8-byte async copies, every copy of the tile in flight at once.
+__device__ __forceinline__ void stage_rows(float* s_tile, int pitch, const float* fresh,
+                                           const float* ctx, const int32_t* fresh_of, int t0,
+                                           int n, int h, int D, int hid) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nwarps = blockDim.x >> 5;
+    for (int t = warp; t < n; t += nwarps) {
+        const int fr = __ldg(fresh_of + t0 + t);
+        const float* src = (fr >= 0 ? fresh + (size_t)fr * hid : ctx + (size_t)(t0 + t) * hid) + h * D;
+        float* dst = s_tile + t * pitch;
+        for (int d = 2 * lane; d < D; d += 64) cp_async_8(dst + d, src + d);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+}
 
 // fixed rows per CTA of the query-tiled attention (the host tiles with the
 // same rule)
@@ -66,17 +88,11 @@ __device__ __forceinline__ void attend_row(const float* __restrict__ q_row,
     __shared__ double s_redd[32];
     const int hid = H * D;
     const int tid = threadIdx.x, nthr = blockDim.x;
-    const int pitch = D + 1;
+    const int pitch = attn_pitch(D);
     for (int d = tid; d < D; d += nthr) s_q[d] = q_row[h * D + d];
     // stage rows [t0, t0 + kAttnTile) of the K or V plane (fresh or cached)
     auto stage = [&](const float* fresh, const float* ctx, int t0) {
-        const int n = min(kAttnTile, tn - t0);
-        for (int i = tid; i < n * D; i += nthr) {
-            const int t = i / D, d = i - t * D;
-            const int fr = fresh_of[t0 + t];
-            const float* src = fr >= 0 ? fresh + (size_t)fr * hid : ctx + (size_t)(t0 + t) * hid;
-            s_tile[t * pitch + d] = src[h * D + d];
-        }
+        stage_rows(s_tile, pitch, fresh, ctx, fresh_of, t0, min(kAttnTile, tn - t0), h, D, hid);
     };
 
     float mx = -INFINITY;
@@ -147,11 +163,11 @@ __global__ void __launch_bounds__(128)
                      const float* __restrict__ ctx_v, const int32_t* __restrict__ fresh_of,
                      const int64_t* __restrict__ fix_idx, int H, int D, float scale,
                      float* __restrict__ mix) {
-    extern __shared__ float s_dyn[];      // [tile (kAttnTile x D+1) | scores]
+    extern __shared__ float s_dyn[];      // [tile (kAttnTile x pitch) | scores]
     const int f = blockIdx.x, h = blockIdx.y;
     const size_t hid = (size_t)H * D;
     attend_row(q + f * hid, k_fresh, v_fresh, ctx_k, ctx_v, fresh_of, (int)fix_idx[f] + 1, h, H,
-               D, scale, mix + f * hid, s_dyn + kAttnTile * (D + 1), s_dyn);
+               D, scale, mix + f * hid, s_dyn + kAttnTile * attn_pitch(D), s_dyn);
 }
 
 // Several members' fixed rows in one launch (grouped recovery): row r
@@ -162,7 +178,7 @@ __global__ void __launch_bounds__(128)
                           const float* __restrict__ v_fresh,
                           const tdkv_attn_member* __restrict__ members, int n_members, int layer,
                           int H, int D, float scale, float* __restrict__ mix) {
-    extern __shared__ float s_dyn[];      // [tile (kAttnTile x D+1) | scores]
+    extern __shared__ float s_dyn[];      // [tile (kAttnTile x pitch) | scores]
     const int r = blockIdx.x, h = blockIdx.y;
     int lo = 0, hi = n_members - 1;
     while (lo < hi) {
@@ -174,7 +190,7 @@ __global__ void __launch_bounds__(128)
     const size_t lofs = (size_t)layer * m.ctx_layer_stride;
     attend_row(q + r * hid, k_fresh + (size_t)m.row0 * hid, v_fresh + (size_t)m.row0 * hid,
                m.ctx_k + lofs, m.ctx_v + lofs, m.fresh_of, (int)m.fix_idx[r - m.row0] + 1, h, H,
-               D, scale, mix + r * hid, s_dyn + kAttnTile * (D + 1), s_dyn);
+               D, scale, mix + r * hid, s_dyn + kAttnTile * attn_pitch(D), s_dyn);
 }
 
 // Query-tiled form of attention_many_kernel: one CTA per (4 * QW consecutive
@@ -191,7 +207,7 @@ __global__ void __launch_bounds__(128)
                            const tdkv_attn_member* __restrict__ members, int n_members, int layer,
                            int H, int D, float scale, int max_tokens, float* __restrict__ mix) {
     constexpr int kAttnQ = 4 * QW;
-    extern __shared__ float s_dyn[];   // [tile kAttnTile x (D+1) | q kAttnQ x D | p kAttnQ x max_tokens]
+    extern __shared__ float s_dyn[];   // [tile kAttnTile x pitch | q kAttnQ x D | p kAttnQ x max_tokens]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int h = blockIdx.y;
     int lo = 0, hi = n_members - 1;
@@ -203,7 +219,7 @@ __global__ void __launch_bounds__(128)
     const int r0 = ((int)blockIdx.x - m.tile0) * kAttnQ;          // member-local first row
     const int nq = min(kAttnQ, m.n_rows - r0);
     const int hid = H * D;
-    const int pitch = D + 1;
+    const int pitch = attn_pitch(D);
     float* s_tile = s_dyn;
     float* s_q = s_tile + kAttnTile * pitch;
     float* s_p = s_q + kAttnQ * D;
@@ -225,11 +241,7 @@ __global__ void __launch_bounds__(128)
         s_q[i] = q[(size_t)(m.row0 + r0 + qi) * hid + h * D + d];
     }
     auto stage = [&](const float* fresh, const float* ctx, int t0, int n) {
-        for (int t = warp; t < n; t += 4) {
-            const int fr = fresh_of[t0 + t];
-            const float* src = (fr >= 0 ? fresh + (size_t)fr * hid : ctx + (size_t)(t0 + t) * hid) + h * D;
-            for (int d = lane; d < D; d += 32) s_tile[t * pitch + d] = src[d];
-        }
+        stage_rows(s_tile, pitch, fresh, ctx, fresh_of, t0, n, h, D, hid);
     };
     // scores
     float mx[QW];
@@ -333,7 +345,7 @@ extern "C" int32_t tdkv_attention(const float* d_q, const float* d_k_fresh, cons
     if (n_fix < 0 || num_tokens <= 0 || num_heads <= 0 || head_dim <= 0 || head_dim > 256)
         return set_error(TDKV_EINVAL, "tdkv_attention: bad geometry");
     if (n_fix == 0) return TDKV_OK;
-    const size_t smem = ((size_t)num_tokens + (size_t)kAttnTile * (head_dim + 1)) * sizeof(float);
+    const size_t smem = ((size_t)num_tokens + (size_t)kAttnTile * attn_pitch(head_dim)) * sizeof(float);
     if (smem > 200 * 1024)
         return set_error(TDKV_EUNSUPPORTED, "tdkv_attention: %d tokens exceed shared memory",
                          num_tokens);
@@ -360,13 +372,13 @@ extern "C" int32_t tdkv_attention_many(const float* d_q, const float* d_k_fresh,
     if (n_members == 0 || total_rows == 0) return TDKV_OK;
     if (!d_q || !d_k_fresh || !d_v_fresh || !d_members || !d_mix)
         return set_error(TDKV_EINVAL, "tdkv_attention_many: null pointer");
-    const size_t smem = ((size_t)max_tokens + (size_t)kAttnTile * (head_dim + 1)) * sizeof(float);
+    const size_t smem = ((size_t)max_tokens + (size_t)kAttnTile * attn_pitch(head_dim)) * sizeof(float);
     if (smem > 200 * 1024)
         return set_error(TDKV_EUNSUPPORTED, "tdkv_attention_many: %d tokens exceed shared memory",
                          max_tokens);
     if (n_tiles > 0 && head_dim <= 128) {
         const int kq = attn_rows_per_tile(head_dim);
-        const size_t tsmem = ((size_t)kAttnTile * (head_dim + 1) + (size_t)kq * head_dim +
+        const size_t tsmem = ((size_t)kAttnTile * attn_pitch(head_dim) + (size_t)kq * head_dim +
                               (size_t)kq * max_tokens) * sizeof(float);
         if (tsmem > 200 * 1024)
             return set_error(TDKV_EUNSUPPORTED,
