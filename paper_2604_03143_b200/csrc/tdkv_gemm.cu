@@ -935,15 +935,9 @@ extern "C" int32_t tdkv_gemm(const void* d_a, int32_t lda, const void* d_b, int3
         } else if (n >= 256 && m > 128 && !getenv("TDKV_GEMM_NO_PAIR") &&
                    (long long)((m + 255) / 256) * ((n + 255) / 256) >= sm_count() / 2) {
             // enough 256 x 256 tiles to give every CTA pair work: cta_group::2
-            static const int pair_bn = [] {
-                const char* e = getenv("TDKV_GEMM_PAIR_BN");
-                return e ? atoi(e) : 256;
-            }();
-            rc = pair_bn == 128
-                     ? launch_gemm_pair<128, 8>(d_a, lda, d_b, ldb, d_c, ldc, m, n, k, accumulate,
-                                                s, &tma)
-                     : launch_gemm_pair<256, 6>(d_a, lda, d_b, ldb, d_c, ldc, m, n, k, accumulate,
-                                                s, &tma);
+            // (256 x 128 pair tiles measured 0.67x: more operand traffic per flop)
+            rc = launch_gemm_pair<256, 6>(d_a, lda, d_b, ldb, d_c, ldc, m, n, k, accumulate, s,
+                                          &tma);
         } else if (n > 64 && !getenv("TDKV_GEMM_NO_PERSISTENT")) {
             const long long tiles256 = (long long)((m + 127) / 128) * ((n + 255) / 256);
             rc = (n >= 256 && tiles256 >= sm_count())
