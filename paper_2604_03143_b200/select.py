@@ -162,16 +162,17 @@ def batched_selection(fresh, cached, counts: Sequence[int], fraction: float,
     staged.copy_(buf, non_blocking=True)
     torch.cuda.current_stream(buf.device).synchronize()
     host = staged.numpy()
-    cnt_h = host[:m]
-    sums = host[m:2 * m].view(np.float32)
+    cnt_h = host[:m].tolist()
+    sums = host[m:2 * m].view(np.float32).tolist()
     idx_h = host[2 * m:]
+    starts = off.tolist()
     out = []
-    for m, n in enumerate(counts):
+    for i, n in enumerate(counts):
         if n == 0:
             out.append((np.empty(0, dtype=np.int64), 0.0))
             continue
-        k = int(cnt_h[m])
-        out.append((idx_h[off[m]:off[m] + k].astype(np.int64), float(sums[m])))
+        a = starts[i]
+        out.append((idx_h[a:a + cnt_h[i]].astype(np.int64), sums[i]))
     return out
 
 
