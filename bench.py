@@ -4,16 +4,21 @@ diff codec's GB/s, on B200 (BASELINE.json metric).
 
 A step is one All-Gather round of the KV Collector over the configured
 synthetic round (default C2: Qwen2.5-7B-shaped bf16 KV, 50 agents per GPU x
-16 shared 256-token blocks): [N>1: NCCL broadcast of the master arena from
-rank 0] + K0 (cos/sin rows) + K1 (rotate + scatter into every agent's paged
-slots).  ``value`` = algorithmic bytes (M + N*M per GPU) of all
+16 shared 256-token blocks): [N>1: the masters' exchange -- NCCL broadcast
+from rank 0 overlapped with K1 per layer chunk, or with --exchange p2p no
+transfer at all: K1 reads every tile from its owner over NVLink] + K0
+(cos/sin rows) + K1 (rotate + scatter into every agent's paged slots).  ``value`` = algorithmic bytes (M + N*M per GPU) of all
 ranks / max-over-ranks device time.  Agents are sharded: weak scaling (each
 GPU owns a config's worth of agents: C1, C2, C4) or strong scaling (the
 config's agents split over the GPUs: C3's 250 agents in 10 sessions, C5's
 1000 agents collected in pool sub-batches of 125).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--exchange p2p]
     python bench.py --impl reference ...   # CPU oracle port on the host cores
+
+Sub-benchmarks on the same line: the diff codec (encode, fused and dense
+restore, TDDF wire), the check-layer selection (K4), the tensor-core
+recompute (K5) and the grouped-vs-serial recovery of BASELINE configs[0].
 """
 from __future__ import annotations
 
