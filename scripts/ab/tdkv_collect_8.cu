@@ -72,14 +72,7 @@ struct CollectParams {
 // kJobGroup jobs with cp.async (double-buffered), so the scatter loop never
 // waits on a dependent global load; each thread's cos/sin values are
 // prefetched one job ahead in registers.
-constexpr int kJobGroup = 16;                      // capacity; groups are balanced
-
-// jobs per group for a unit of nj jobs: the fewest groups of <= kJobGroup,
-// evenly filled (50 jobs -> 4 x 13, not 3 x 16 + 2)
-__device__ __forceinline__ int job_group_size(int nj) {
-    const int groups = (nj + kJobGroup - 1) / kJobGroup;
-    return groups > 0 ? (nj + groups - 1) / groups : 1;
-}
+constexpr int kJobGroup = 8;
 constexpr int kMaxTileRows = 32;
 
 template <typename T, int UB, bool BULK>
@@ -140,9 +133,8 @@ __global__ void __launch_bounds__(256) collect_kernel(const CollectParams p) {
         gv = static_cast<const T*>(bv) + off;
     };
     auto stage_meta = [&](const tdkv_collect_unit& u, int g, int mb) {
-        const int gsz = job_group_size(u.job_end - u.job_begin);
-        const int jbase = u.job_begin + g * gsz;
-        const int ng = min(gsz, u.job_end - jbase);
+        const int jbase = u.job_begin + g * kJobGroup;
+        const int ng = min(kJobGroup, u.job_end - jbase);
         const int cnt = ng * u.nrows;
         for (int idx = tid; idx < cnt; idx += nthr) {
             const int jj = idx / u.nrows;
@@ -218,8 +210,7 @@ __global__ void __launch_bounds__(256) collect_kernel(const CollectParams p) {
         const V* sv = reinterpret_cast<const V*>(buf + tile_bytes);
         T* dk_l = static_cast<T*>(p.dk) + (size_t)layer * p.dls;
         T* dv_l = static_cast<T*>(p.dv) + (size_t)layer * p.dls;
-        const int gsz = job_group_size(u.job_end - u.job_begin);
-        const int ngroups = (u.job_end - u.job_begin + gsz - 1) / gsz;
+        const int ngroups = (u.job_end - u.job_begin + kJobGroup - 1) / kJobGroup;
 
         for (int g = 0; g < ngroups; ++g) {
             const int mb = g & 1;
@@ -230,7 +221,7 @@ __global__ void __launch_bounds__(256) collect_kernel(const CollectParams p) {
                 cp_async_wait<0>();
             }
             __syncthreads();
-            const int ng = min(gsz, u.job_end - u.job_begin - g * gsz);
+            const int ng = min(kJobGroup, u.job_end - u.job_begin - g * kJobGroup);
             if constexpr (BULK) {
                 if (v_tma && tid < ng) {
                     const int64_t* dr = &s_drow[mb][tid * kMaxTileRows];
