@@ -1,4 +1,5 @@
-# K1 A/B: the in-tree build vs scripts/ab/tdkv_collect_<variant>.cu (run under gpurun)
+# K1 A/B: the in-tree build vs scripts/ab/tdkv_collect_<variant>.cu (run under gpurun;
+# scripts/ab/ is git-ignored scratch, e.g. git show HEAD~1:paper_2604_03143_b200/csrc/tdkv_collect.cu)
 set -e
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
 mkdir -p /tmp/ab_build
