@@ -253,15 +253,23 @@ __global__ void __launch_bounds__(128)
         stage(kf, ctx_k, t0, n);
         __syncthreads();
         if (lane < n) {
+            // the warp's queries advance together over d: each key element is
+            // read once and the QW chains are independent (each chain is still
+            // one sequential fmaf over d)
             const float* kr = s_tile + lane * pitch;
+            float acc[QW];
+#pragma unroll
+            for (int j = 0; j < QW; ++j) acc[j] = 0.f;
+            for (int d = 0; d < D; ++d) {
+                const float kv = kr[d];
+#pragma unroll
+                for (int j = 0; j < QW; ++j) acc[j] = fmaf(s_q[(warp + 4 * j) * D + d], kv, acc[j]);
+            }
 #pragma unroll
             for (int j = 0; j < QW; ++j) {
                 const int qi = warp + 4 * j;
                 if (t0 + lane < tnq[j]) {
-                    const float* qq = s_q + qi * D;
-                    float acc = 0.f;
-                    for (int d = 0; d < D; ++d) acc = fmaf(qq[d], kr[d], acc);
-                    const float sc = acc * scale;
+                    const float sc = acc[j] * scale;
                     s_p[qi * max_tokens + t0 + lane] = sc;
                     mx[j] = fmaxf(mx[j], sc);
                 }
