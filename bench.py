@@ -766,6 +766,26 @@ def recovery_bench(dev, args):
         out[f"{name}_selection_passes"] = led.selection_passes
     out["speedup"] = round(out["serial_ms"] / out["grouped_ms"], 2)
     out["agents_per_s"] = round(len(members) / (out["grouped_ms"] * 1e-3), 1)
+    # group-size sweep, as the paper's Q2 (3 / 5 / 10 / 15 / 20 agents)
+    sweep = []
+    for n in (3, 5, 10, 15, 20):
+        mem = rounds.toy_round(w, num_agents=n, seed=2, device=dev)
+        grp = rounds.ToyGroup(mem)
+        row = {"agents": n}
+        for name, fn in (("grouped", lambda: pic.collective_recover(w, grp, _Pic)),
+                         ("serial", lambda: [pic.recover_prepared(w, x, _Pic) for x in mem])):
+            fn()
+            torch.cuda.synchronize(dev)
+            times = []
+            for _ in range(5):
+                t0 = time.perf_counter()
+                fn()
+                torch.cuda.synchronize(dev)
+                times.append(time.perf_counter() - t0)
+            row[f"{name}_ms"] = round(float(np.median(times)) * 1e3, 3)
+        row["speedup"] = round(row["serial_ms"] / row["grouped_ms"], 2)
+        sweep.append(row)
+    out["group_size_sweep"] = sweep
     out["note"] = ("wall clock (median of 11) incl. host control flow and the selection "
                    "read-back; segment masters resident in HBM; the paper reports up to 2.57x "
                    "collective over serial on A100 + vLLM")
