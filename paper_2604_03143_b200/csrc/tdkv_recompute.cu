@@ -60,8 +60,10 @@ __device__ __forceinline__ void stage_rows(float* s_tile, int pitch, const float
                                            int n, int h, int D, int hid) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nwarps = blockDim.x >> 5;
+    // the tile's fresh-row map in one coalesced load per warp (n <= 32)
+    const int fr_lane = lane < n ? __ldg(fresh_of + t0 + lane) : -1;
     for (int t = warp; t < n; t += nwarps) {
-        const int fr = __ldg(fresh_of + t0 + t);
+        const int fr = __shfl_sync(0xffffffffu, fr_lane, t);
         const float* src = (fr >= 0 ? fresh + (size_t)fr * hid : ctx + (size_t)(t0 + t) * hid) + h * D;
         float* dst = s_tile + t * pitch;
         for (int d = 2 * lane; d < D; d += 64) cp_async_8(dst + d, src + d);
