@@ -22,7 +22,7 @@ rng = np.random.default_rng(1)
 mirrors, hints = [], []
 for _ in range(P):
     blocks = np.sort(rng.choice(nb, nb // 10, replace=False))
-    mirrors.append(tk.LayeredKv(mk.clone(), mv.clone(), np.arange(T)))
+    mirrors.append(tk.LayeredKv(mk.clone(), mv.clone(), np.arange(T)))  # own positions
     hints.append(np.concatenate([np.arange(b * bs, min(T, b * bs + bs)) for b in blocks]))
 cfg = tk.CacheBlockConfig(bs)
 for _ in range(3):
