@@ -936,7 +936,7 @@ extern "C" int32_t tdkv_gemm(const void* d_a, int32_t lda, const void* d_b, int3
                    (long long)((m + 255) / 256) * ((n + 255) / 256) >= sm_count() / 2) {
             // enough 256 x 256 tiles to give every CTA pair work: cta_group::2
             // (256 x 128 pair tiles measured 0.67x: more operand traffic per flop)
-            rc = launch_gemm_pair<256, 6>(d_a, lda, d_b, ldb, d_c, ldc, m, n, k, accumulate, s,
+            rc = launch_gemm_pair<256, 7>(d_a, lda, d_b, ldb, d_c, ldc, m, n, k, accumulate, s,
                                           &tma);
         } else if (n > 64 && !getenv("TDKV_GEMM_NO_PERSISTENT")) {
             const long long tiles256 = (long long)((m + 127) / 128) * ((n + 255) / 256);
