@@ -25,7 +25,7 @@ from . import select as _select
 from . import _kernels
 from ._device import default_device, h2d, ptr
 from .collector import align_cached, skeleton_values
-from .core import LayeredKv
+from .core import LayeredKv, union_sorted
 from .ledger import CostLedger
 from .recompute import ToyModel, forward_many
 
@@ -118,7 +118,7 @@ def probe_and_select(weights, members, contexts, cfg, ledger: Optional[CostLedge
     fresh = torch.empty((R, H, D), dtype=torch.float32, device=device)
     cached = torch.empty_like(fresh)
     shared = [np.asarray(members[i].shared_idx, np.int64) for i in live]
-    fixes = [np.union1d(sh, members[i].structural_idx).astype(np.int64)
+    fixes = [union_sorted(sh, members[i].structural_idx)
              for i, sh in zip(live, shared)]
     items = [(np.asarray(members[i].tokens, np.int64), np.asarray(members[i].positions, np.int64),
               fx, contexts[i][0], contexts[i][1]) for i, fx in zip(live, fixes)]
@@ -158,7 +158,7 @@ def refresh_many(weights, preps, contexts, importants,
     device = contexts[0][0].device
     m = ToyModel.of(weights, device)
     hd = m.num_heads * m.head_dim
-    fixes = [np.union1d(imp, p.structural_idx).astype(np.int64)
+    fixes = [union_sorted(imp, p.structural_idx)
              for p, imp in zip(preps, importants)]
     items = [(np.asarray(p.tokens, np.int64), np.asarray(p.positions, np.int64), fx, ck, cv)
              for p, fx, (ck, cv) in zip(preps, fixes, contexts)]
@@ -185,7 +185,7 @@ def recover_prepared(weights, prep, cfg, ledger: Optional[CostLedger] = None,
     align_cached([prep], [context], ToyModel.of(weights, device).rope_base, ledger)
     (important, deviation), = probe_and_select(weights, [prep], [context], cfg, ledger)
     refresh_many(weights, [prep], [context], [important], ledger)
-    num = int(np.union1d(important, prep.structural_idx).size)
+    num = int(union_sorted(important, prep.structural_idx).size)
     kv = LayeredKv(context[0], context[1], np.asarray(prep.positions, np.int64))
     return RecoveryResult(prep.request_id, kv, important, deviation, num)
 
@@ -208,7 +208,7 @@ def collective_recover(weights, group, cfg, ledger: Optional[CostLedger] = None,
     important: Dict[int, np.ndarray] = {}
     for prep, context, (imp, dev) in zip(members, contexts, selections):
         kv = LayeredKv(context[0], context[1], np.asarray(prep.positions, np.int64))
-        num = int(np.union1d(imp, prep.structural_idx).size)
+        num = int(union_sorted(imp, prep.structural_idx).size)
         results[prep.request_id] = RecoveryResult(prep.request_id, kv, imp, dev, num)
         scores[prep.request_id] = dev
         important[prep.request_id] = imp

@@ -26,7 +26,7 @@ import torch
 from . import _kernels, _lib
 from ._device import (default_device, h2d, is_host, ptr, stream_handle, to_device, to_host,
                       upload)
-from .core import LayeredKv
+from .core import LayeredKv, union_sorted
 from .gemm import gemm_tn
 from .ledger import CostLedger
 
@@ -214,7 +214,7 @@ def refresh(weights, prep, context, important: np.ndarray,
             ledger: Optional[CostLedger] = None) -> None:
     """Recompute important and structural positions together at all layers
     and write them into the member's context (pic.py:284-300)."""
-    fix = np.union1d(important, prep.structural_idx).astype(np.int64)
+    fix = union_sorted(important, prep.structural_idx)
     if fix.size == 0:
         return
     ctx_k, ctx_v = context

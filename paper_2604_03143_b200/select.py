@@ -24,6 +24,7 @@ import torch
 
 from . import _lib
 from ._device import default_device, dtype_code, h2d, is_host, ptr, stream_handle, to_device
+from .core import union_sorted
 from .ledger import CostLedger
 
 
@@ -192,5 +193,4 @@ def mirror_hint_positions(member, master, member_important: np.ndarray,
     le, lo = np.asarray(member.label_entry), np.asarray(member.label_offset)
     me, mo = np.asarray(master.label_entry), np.asarray(master.label_offset)
     divergent = (le == -1) | (me == -1) | (le != me) | (lo != mo)
-    hinted = np.union1d(np.flatnonzero(divergent), member_important)
-    return np.union1d(hinted, master_important).astype(np.int64)
+    return union_sorted(np.flatnonzero(divergent), member_important, master_important)
