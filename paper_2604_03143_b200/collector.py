@@ -694,7 +694,45 @@ def skeleton_values(members, contexts) -> None:
     _scatter_back(jobs, offs, staged, contexts, plane=1)
 
 
-def _scatter_back(jobs, offs, staged: torch.Tensor, contexts, plane: int) -> None:
+def collect_into_contexts(members, contexts, rope_base: float,
+                          ledger: Optional[CostLedger] = None) -> None:
+    """``skeleton_values`` + ``align_cached`` in one pass for CUDA contexts:
+    one master arena, one plan, one K0 + K1 launch moving K (rotated) and V,
+    one scatter of both planes into the members' contexts.  Same results and
+    ledger law (one rotation per layer) as the two reference-shaped calls."""
+    jobs = [(i, hit) for i, prep in enumerate(members) for hit in prep.hits]
+    if not jobs:
+        return
+    ctx0 = contexts[jobs[0][0]][0]
+    if is_host(ctx0):
+        skeleton_values(members, contexts)
+        align_cached(members, contexts, rope_base, ledger)
+        return
+    num_layers = jobs[0][1].kv.num_layers
+    ids, segs = _unique_masters(jobs)
+    device, dtype = ctx0.device, ctx0.dtype
+    arena = MasterArena.from_segments(segs, dtype=dtype, device=device)
+    cjobs, offs = [], []
+    off = 0
+    for _, hit in jobs:
+        n = len(hit.target_idx)
+        cjobs.append(CollectJob(ids[id(hit.kv)], np.arange(off, off + n, dtype=np.int64),
+                                np.asarray(hit.delta, np.int64)))
+        offs.append(off)
+        off += n
+    plan = CollectPlan(arena, cjobs, rope_base, device=device)
+    L, _, H, D = arena.k.shape
+    staged_k = torch.empty((L, off, H, D), dtype=dtype, device=device)
+    staged_v = torch.empty_like(staged_k)
+    plan.launch(arena, staged_k, staged_v, off * H * D)
+    if ledger is not None:
+        for layer in range(num_layers):
+            ledger.record_rope_call(layer)
+    _scatter_back(jobs, offs, staged_k, contexts, plane=0, staged_v=staged_v)
+
+
+def _scatter_back(jobs, offs, staged: torch.Tensor, contexts, plane: int,
+                  staged_v: Optional[torch.Tensor] = None) -> None:
     first = contexts[jobs[0][0]][plane]
     if is_host(first):
         host = to_host(staged)
@@ -713,7 +751,10 @@ def _scatter_back(jobs, offs, staged: torch.Tensor, contexts, plane: int) -> Non
     recs, t_off = [], 0
     for (i, hit), off, tgt in zip(jobs, offs, targets):
         ctx = contexts[i][plane]
-        recs.append((ptr(staged) + esz * hd * off, 0, R * hd, 0, 0, 0, 0, 0, ptr(ctx), 0,
+        # staged_v given: K to contexts[i][0] and V to contexts[i][1] in one record
+        src_v = ptr(staged_v) + esz * hd * off if staged_v is not None else 0
+        dst_v = ptr(contexts[i][1]) if staged_v is not None else 0
+        recs.append((ptr(staged) + esz * hd * off, src_v, R * hd, 0, 0, 0, 0, 0, ptr(ctx), dst_v,
                      int(ctx.shape[1]) * hd, base + 8 * t_off, tgt.size, 0, 0, 0))
         t_off += tgt.size
     _kernels.rows(_kernels.rows_jobs(recs), max(t.size for t in targets), None, L, H, D,

@@ -24,7 +24,7 @@ import torch
 from . import select as _select
 from . import _kernels
 from ._device import default_device, h2d, ptr
-from .collector import align_cached, skeleton_values
+from .collector import collect_into_contexts
 from .core import LayeredKv, union_sorted
 from .ledger import CostLedger
 from .recompute import ToyModel, forward_many
@@ -181,8 +181,7 @@ def recover_prepared(weights, prep, cfg, ledger: Optional[CostLedger] = None,
     """Serial recovery of one prepared request (pic.py:303-316)."""
     device = device or default_device()
     context, = _skeletons(weights, [prep], device)
-    skeleton_values([prep], [context])
-    align_cached([prep], [context], ToyModel.of(weights, device).rope_base, ledger)
+    collect_into_contexts([prep], [context], ToyModel.of(weights, device).rope_base, ledger)
     (important, deviation), = probe_and_select(weights, [prep], [context], cfg, ledger)
     refresh_many(weights, [prep], [context], [important], ledger)
     num = int(union_sorted(important, prep.structural_idx).size)
@@ -199,8 +198,7 @@ def collective_recover(weights, group, cfg, ledger: Optional[CostLedger] = None,
     members = group.members
     model = ToyModel.of(weights, device)
     contexts = _skeletons(weights, members, device)
-    skeleton_values(members, contexts)
-    align_cached(members, contexts, model.rope_base, ledger)
+    collect_into_contexts(members, contexts, model.rope_base, ledger)
     selections = probe_and_select(weights, members, contexts, cfg, ledger)
     refresh_many(weights, members, contexts, [imp for imp, _ in selections], ledger)
     results: Dict[int, RecoveryResult] = {}
