@@ -136,27 +136,6 @@ def rows_jobs(tuples) -> np.ndarray:
     return np.array(list(tuples), dtype=_lib.ROWS_JOB)
 
 
-def move_rows(src: torch.Tensor, dst: torch.Tensor, src_rows=None, dst_rows=None) -> None:
-    """dst[l, dst_rows[i]] = src[l, src_rows[i]] for every layer l (K3 copy).
-
-    ``src``/``dst`` are (L, rows, H, D) or (rows, H, D) CUDA planes; the row
-    index arrays are host int64 (None = identity)."""
-    s = src if src.dim() == 4 else src.unsqueeze(0)
-    d = dst if dst.dim() == 4 else dst.unsqueeze(0)
-    L, _, H, D = s.shape
-    n = len(src_rows) if src_rows is not None else (len(dst_rows) if dst_rows is not None
-                                                      else int(s.shape[1]))
-    if n == 0:
-        return
-    dev = src.device
-    from ._device import h2d
-    sr = None if src_rows is None else h2d(np.asarray(src_rows, np.int64), dev)
-    dr = None if dst_rows is None else h2d(np.asarray(dst_rows, np.int64), dev)
-    job = rows_job(s, None, int(s.shape[1]) * H * D, d, None, int(d.shape[1]) * H * D, n,
-                   src_rows=sr, dst_rows=dr)
-    rows(rows_jobs([job]), n, None, L, H, D, ROWS_BLOCK, src.dtype, dev)
-
-
 def fill_rows(plane: torch.Tensor, rows_dev: torch.Tensor, value: float) -> None:
     """Write ``value`` into the given rows of every layer of a (L, cap, H, D) plane."""
     L, cap, H, D = plane.shape
