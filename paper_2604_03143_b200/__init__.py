@@ -10,7 +10,7 @@ fallback -- without the library or a CUDA device the entry points raise.
 from ._lib import TdkvError, TdkvUnavailable, build_library, launch_count
 from .collector import (CollectJob, CollectPlan, KVCollector, MasterArena, RoundGraph, RoundPipeline,
                         SlotArena, align_cached, skeleton_values)
-from .core import CacheBlockConfig, LayeredKv, PositionSpan, kv_dense_nbytes
+from .core import CacheBlockConfig, LayeredKv, ModelConfig, PositionSpan, kv_dense_nbytes
 from .diffstore import (BlockSparseDiff, CompressionStats, DiffStore, FamilyEncoding,
                         HintSoundnessError, LayerDiff, MalformedDiffError, MasterEntry,
                         MirrorHandle, PinnedMasterError, deserialize_diff, diff_decode_dense,
@@ -24,8 +24,10 @@ from .rope import rope_apply, rope_recover
 from .segment_index import (EmptySegmentError, PinnedEntryError, SegmentCacheEntry,
                             SegmentIndex)
 from .gemm import gemm_tn
-from .pic import RecoveryResult, ReusePlan, collective_recover, probe_and_select, recover_prepared
-from .recompute import ToyModel, full_prefill, recompute_positions, refresh, selective_forward
+from .pic import (PicConfig, RecoveryResult, ReuseGroup, ReusePlan, collective_recover,
+                  probe_and_select, recover_prepared)
+from .recompute import (ModelWeights, ToyModel, build_weights, full_prefill, recompute_positions,
+                        refresh, selective_forward)
 from .select import (batched_selection, key_diff, mirror_hint_positions, recompute_budget,
                      select_important, select_master)
 
@@ -45,5 +47,6 @@ __all__ = [
     "kv_dense_nbytes", "launch_count", "rope_apply", "rope_recover", "serialize_diff",
     "serialize_many", "deserialize_to_device", "EmptySegmentError", "PinnedEntryError",
     "SegmentCacheEntry", "SegmentIndex",
-    "skeleton_values", "slot_maps_disjoint", "wire_nbytes",
+    "skeleton_values", "slot_maps_disjoint", "wire_nbytes", "ModelConfig", "ModelWeights",
+    "build_weights", "PicConfig", "ReuseGroup",
 ]

@@ -1,8 +1,9 @@
 """Value types of the hot path (reference: roundkv/core.py).
 
-``LayeredKv`` (core.py:164-201), ``PositionSpan`` (core.py:204-237) and
-``CacheBlockConfig`` (core.py:240-263) keep the reference's constructors,
-validation and error messages.  KV planes may be host numpy float32 arrays
+``LayeredKv`` (core.py:164-201), ``PositionSpan`` (core.py:204-237),
+``CacheBlockConfig`` (core.py:240-263) and the toy model's ``ModelConfig``
+(core.py:38-66) keep the reference's constructors, validation and error
+messages.  KV planes may be host numpy float32 arrays
 (the reference's contract) or CUDA tensors in float32 or bfloat16 (the
 B200-resident form); positions are always host int64 metadata.
 """
@@ -161,3 +162,34 @@ class CacheBlockConfig:
     def valid_len(self, num_tokens: int) -> int:
         rem = num_tokens % self.block_size
         return rem if rem else min(self.block_size, num_tokens)
+
+
+@dataclass(frozen=True)
+class ModelConfig:
+    """Dimensions and seeds of the deterministic toy transformer (core.py:38-66)."""
+
+    num_layers: int = 4
+    num_heads: int = 2
+    head_dim: int = 8
+    vocab_size: int = 1024
+    rope_base: float = 10000.0
+    weight_seed: int = 0
+
+    def __post_init__(self) -> None:
+        if self.num_layers < 1 or self.num_heads < 1:
+            raise ValueError("num_layers and num_heads must be positive")
+        if self.head_dim < 2 or self.head_dim % 2 != 0:
+            raise ValueError("head_dim must be a positive even integer")
+        if self.vocab_size < 2:
+            raise ValueError("vocab_size must leave room for the separator id")
+        if self.rope_base <= 0:
+            raise ValueError("rope_base must be positive")
+
+    @property
+    def hidden_dim(self) -> int:
+        return self.num_heads * self.head_dim
+
+    @property
+    def separator_token(self) -> int:
+        # the highest id is reserved (the reference's workload draws below it)
+        return self.vocab_size - 1

@@ -30,6 +30,43 @@ from .ledger import CostLedger
 from .recompute import ToyModel, forward_many
 
 
+@dataclass(frozen=True)
+class PicConfig:
+    """Selective-recompute knobs (pic.py:36-48): fraction of reused positions
+    to refresh and the layer whose key differences rank them."""
+
+    recompute_fraction: float = 0.15
+    check_layer: int = 1
+
+    def __post_init__(self) -> None:
+        if not 0.0 <= self.recompute_fraction <= 1.0:
+            raise ValueError("recompute_fraction must be within [0, 1]")
+        if self.check_layer < 0:
+            raise ValueError("check_layer must be non-negative")
+
+
+@dataclass(eq=False)
+class ReuseGroup:
+    """Two or more prepared requests that recover together (collective.py:40-59)."""
+
+    group_id: int
+    members: list
+
+    def __post_init__(self) -> None:
+        if len(self.members) < 2:
+            raise ValueError("a reuse group needs at least two members")
+        ids = [m.request_id for m in self.members]
+        if len(set(ids)) != len(ids):
+            raise ValueError("group member request ids must be distinct")
+
+    @property
+    def member_ids(self) -> list:
+        return [m.request_id for m in self.members]
+
+    def __len__(self) -> int:
+        return len(self.members)
+
+
 @dataclass(eq=False)
 class RecoveryResult:
     request_id: int

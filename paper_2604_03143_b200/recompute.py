@@ -18,6 +18,7 @@ reference's ``ModelWeights`` (or anything with ``config``, ``embed``,
 """
 from __future__ import annotations
 
+from dataclasses import dataclass
 from typing import Optional, Sequence
 
 import numpy as np
@@ -26,9 +27,41 @@ import torch
 from . import _kernels, _lib
 from ._device import (default_device, h2d, is_host, ptr, stream_handle, to_device, to_host,
                       upload)
-from .core import LayeredKv, union_sorted
+from .core import LayeredKv, ModelConfig, union_sorted
 from .gemm import gemm_tn
 from .ledger import CostLedger
+
+
+@dataclass(eq=False)
+class ModelWeights:
+    """The toy transformer's weights (toymodel.py:26-33): embedding (vocab,
+    hidden) and per-layer q / k / v / mix matrices (layers, hidden, hidden),
+    float32 on the host; ``ToyModel.of`` keeps the device copies."""
+
+    config: ModelConfig
+    embed: np.ndarray
+    wq: np.ndarray
+    wk: np.ndarray
+    wv: np.ndarray
+    wm: np.ndarray
+
+
+def build_weights(config: ModelConfig) -> ModelWeights:
+    """U[-0.1, 0.1] float32 draws from one PCG64(SeedSequence(weight_seed))
+    stream in the reference's order -- embedding, then per layer q, k, v, mix
+    (toymodel.py:36-57) -- so the weights are the reference's bit for bit."""
+    rng = np.random.default_rng(np.random.SeedSequence(config.weight_seed))
+    hid = config.hidden_dim
+
+    def draw(*shape: int) -> np.ndarray:
+        return rng.uniform(-0.1, 0.1, size=shape).astype(np.float32)
+
+    embed = draw(config.vocab_size, hid)
+    mats = [np.empty((config.num_layers, hid, hid), dtype=np.float32) for _ in range(4)]
+    for layer in range(config.num_layers):
+        for mat in mats:
+            mat[layer] = draw(hid, hid)
+    return ModelWeights(config, embed, *mats)
 
 
 def _cfg(weights):

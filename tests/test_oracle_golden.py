@@ -303,3 +303,33 @@ def test_oracle_violation_magnitudes_with_nan_inf_and_signed_zero():
         with pytest.raises(ref.HintViolation) as err:
             ref.encode_diff(k, v, mk, mv, hints, 32)
         assert str(err.value) == entry["message"], entry["case"]
+
+
+def test_product_value_types_match_the_reference():
+    """ModelConfig / build_weights / PicConfig / ReuseGroup are the reference's
+    (toymodel.py:36-57, core.py:38-66, pic.py:36-48, collective.py:40-59):
+    weights bit-identical to the oracle's pinned restatement, same validation."""
+    import paper_2604_03143_b200 as tk
+    cfg = tk.ModelConfig(num_layers=3, num_heads=2, head_dim=8, vocab_size=64, weight_seed=7)
+    assert cfg.hidden_dim == 16 and cfg.separator_token == 63
+    w = tk.build_weights(cfg)
+    o = ref.build_weights(3, 2, 8, 64, 7)
+    for name in ("embed", "wq", "wk", "wv", "wm"):
+        assert np.array_equal(getattr(w, name), getattr(o, name)), name
+    for bad in (dict(head_dim=7), dict(num_layers=0), dict(vocab_size=1), dict(rope_base=0.0)):
+        with pytest.raises(ValueError):
+            tk.ModelConfig(**bad)
+    assert tk.PicConfig().recompute_fraction == 0.15 and tk.PicConfig().check_layer == 1
+    for bad in (dict(recompute_fraction=1.5), dict(check_layer=-1)):
+        with pytest.raises(ValueError):
+            tk.PicConfig(**bad)
+
+    class _M:
+        def __init__(self, rid):
+            self.request_id = rid
+    g = tk.ReuseGroup(3, [_M(1), _M(4)])
+    assert g.member_ids == [1, 4] and len(g) == 2
+    with pytest.raises(ValueError):
+        tk.ReuseGroup(0, [_M(1)])
+    with pytest.raises(ValueError):
+        tk.ReuseGroup(0, [_M(1), _M(1)])
