@@ -751,8 +751,10 @@ def recovery_bench(dev, args):
         return led
 
     out = {"agents": len(members), "tokens_per_agent": int(members[0].num_tokens)}
+    torch.cuda.empty_cache()         # the codec sub-benchmarks leave large cached blocks
     for name, fn in (("grouped", grouped), ("serial", serial)):
-        fn()
+        for _ in range(3):
+            fn()
         torch.cuda.synchronize(dev)
         times = []
         for _ in range(11):

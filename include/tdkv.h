@@ -304,11 +304,13 @@ int32_t tdkv_attention(const float* d_q, const float* d_k_fresh, const float* d_
  * rows [row0, row0 + n_rows), attends over its own context (layer ``layer``
  * of planes with ctx_layer_stride elements per layer), and its fresh_of
  * indexes its own slice of the fresh rows.  d_members sorted by row0.
- * n_tiles > 0 selects the query-tiled kernel (head_dim <= 128): member m's
- * rows form ceil(n_rows / 8) tiles starting at tile index tile0
- * (n_tiles in total), each CTA serving 8 rows of
- * one member with every staged key/value tile; n_tiles == 0 runs one CTA per
- * row. */
+ * n_tiles > 0 selects a query-tiled kernel: member m's rows form
+ * ceil(n_rows / rows_per_tile) tiles starting at tile index tile0 (n_tiles in
+ * total), each CTA serving one tile of one member with every staged
+ * key/value tile.  rows_per_tile 8 (head_dim <= 128): two-pass softmax over a
+ * stored score row; rows_per_tile 16 (head_dim <= 64): online softmax
+ * (running max / sum, float64 accumulators rescaled per 32-token tile).
+ * n_tiles == 0 runs one CTA per row. */
 typedef struct {
     const float* ctx_k;          /* (L, num_tokens, H*D) context planes */
     const float* ctx_v;
@@ -323,9 +325,9 @@ typedef struct {
 
 int32_t tdkv_attention_many(const float* d_q, const float* d_k_fresh, const float* d_v_fresh,
                             const tdkv_attn_member* d_members, int32_t n_members, int32_t layer,
-                            int32_t total_rows, int32_t n_tiles, int32_t max_tokens,
-                            int32_t num_heads, int32_t head_dim, float scale, float* d_mix,
-                            void* stream);
+                            int32_t total_rows, int32_t n_tiles, int32_t rows_per_tile,
+                            int32_t max_tokens, int32_t num_heads, int32_t head_dim, float scale,
+                            float* d_mix, void* stream);
 
 /* ------------------------------------------------------------------------
  * Host slot allocator of the paged pool, policy of

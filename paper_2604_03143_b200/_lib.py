@@ -147,7 +147,7 @@ _SIGS = {
     "tdkv_segidx_entries": (_I32, [_P, _P, _I64, _P]),
     "tdkv_wire_unpack": (_I32, [_P, _I32, _I64, _P, _P]),
     "tdkv_attention_many": (_I32, [_P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _I32,
-                                   ctypes.c_float, _P, _P]),
+                                   _I32, ctypes.c_float, _P, _P]),
     "tdkv_attention": (_I32, [_P, _P, _P, _P, _P, _P, _P, _I32, _I32, _I32, _I32,
                               ctypes.c_float, _P, _P]),
 }

@@ -72,10 +72,7 @@ __device__ __forceinline__ void stage_rows(float* s_tile, int pitch, const float
     cp_async_wait<0>();
 }
 
-// fixed rows per CTA of the query-tiled attention (the host tiles with the
-// same rule)
-// (16-row tiles measured slower: 80 registers and 70 KB of scores per CTA)
-__host__ __device__ inline int attn_rows_per_tile(int) { return 8; }
+
 
 __device__ __forceinline__ void attend_row(const float* __restrict__ q_row,
                                            const float* __restrict__ k_fresh,
@@ -326,6 +323,126 @@ __global__ void __launch_bounds__(128)
     }
 }
 
+// Online-softmax form of the query-tiled attention (head_dim <= 64): one CTA
+// per (32 fixed rows of one member, head) streams the member's keys/values
+// once in 32-token tiles (K and V staged together), keeping a running max and
+// sum per query and rescaling its float64 output accumulators per tile, so
+// no full score row is stored and every staged tile serves 32 queries.
+// Warp w owns queries w, w + 4, ..., (QW per warp); thread i owns outputs
+// (q, d) for q * D + d = i + 128 k.
+template <int QW>
+__global__ void __launch_bounds__(128)
+    attention_online_kernel(const float* __restrict__ q, const float* __restrict__ k_fresh,
+                            const float* __restrict__ v_fresh,
+                            const tdkv_attn_member* __restrict__ members, int n_members,
+                            int layer, int H, int D, float scale, float* __restrict__ mix) {
+    constexpr int kQ = 4 * QW;
+    constexpr int kOut = kQ * 64 / 128;                         // outputs per thread (D <= 64)
+    extern __shared__ float s_dyn[];   // [K tile | V tile | q kQ x D | p kQ x kAttnTile | corr kQ | l kQ]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int h = blockIdx.y;
+    int lo = 0, hi = n_members - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (members[mid].tile0 <= (int)blockIdx.x) lo = mid; else hi = mid - 1;
+    }
+    const tdkv_attn_member m = members[lo];
+    const int r0 = ((int)blockIdx.x - m.tile0) * kQ;
+    const int nq = min(kQ, m.n_rows - r0);
+    const int hid = H * D;
+    const int pitch = attn_pitch(D);
+    float* s_k = s_dyn;
+    float* s_v = s_k + kAttnTile * pitch;
+    float* s_q = s_v + kAttnTile * pitch;
+    float* s_pt = s_q + kQ * D;
+    float* s_corr = s_pt + kQ * kAttnTile;
+    float* s_l = s_corr + kQ;
+    const size_t lofs = (size_t)layer * m.ctx_layer_stride;
+    const float* ctx_k = m.ctx_k + lofs;
+    const float* ctx_v = m.ctx_v + lofs;
+    const float* kf = k_fresh + (size_t)m.row0 * hid;
+    const float* vf = v_fresh + (size_t)m.row0 * hid;
+    for (int i = tid; i < nq * D; i += blockDim.x) {
+        const int qi = i / D, d = i - qi * D;
+        s_q[i] = q[(size_t)(m.row0 + r0 + qi) * hid + h * D + d];
+    }
+    int tnq[QW];
+    float mrun[QW];
+    double lrun[QW];
+#pragma unroll
+    for (int j = 0; j < QW; ++j) {
+        const int qi = warp + 4 * j;
+        tnq[j] = qi < nq ? (int)m.fix_idx[r0 + qi] + 1 : 0;
+        mrun[j] = -INFINITY;
+        lrun[j] = 0.0;
+    }
+    const int tn = (int)m.fix_idx[r0 + nq - 1] + 1;
+    double acc[kOut];
+#pragma unroll
+    for (int k = 0; k < kOut; ++k) acc[k] = 0.0;
+    for (int t0 = 0; t0 < tn; t0 += kAttnTile) {
+        const int n = min(kAttnTile, tn - t0);
+        __syncthreads();                                     // previous tile consumed
+        stage_rows(s_k, pitch, kf, ctx_k, m.fresh_of, t0, n, h, D, hid);
+        stage_rows(s_v, pitch, vf, ctx_v, m.fresh_of, t0, n, h, D, hid);
+        __syncthreads();
+        float sc[QW];
+        {
+            float a[QW];
+#pragma unroll
+            for (int j = 0; j < QW; ++j) a[j] = 0.f;
+            if (lane < n) {
+                const float* kr = s_k + lane * pitch;
+                for (int d = 0; d < D; ++d) {
+                    const float kv = kr[d];
+#pragma unroll
+                    for (int j = 0; j < QW; ++j) a[j] = fmaf(s_q[(warp + 4 * j) * D + d], kv, a[j]);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < QW; ++j)
+                sc[j] = (lane < n && t0 + lane < tnq[j]) ? a[j] * scale : -INFINITY;
+        }
+#pragma unroll
+        for (int j = 0; j < QW; ++j) {
+            const int qi = warp + 4 * j;
+            float tmax = sc[j];
+            for (int o = 16; o > 0; o >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+            const float mnew = fmaxf(mrun[j], tmax);
+            const float corr = (mrun[j] == -INFINITY) ? 1.f : expf(mrun[j] - mnew);
+            const float p = sc[j] == -INFINITY ? 0.f : expf(sc[j] - mnew);
+            double ps = (double)p;
+            for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
+            lrun[j] = lrun[j] * (double)corr + ps;
+            mrun[j] = mnew;
+            s_pt[qi * kAttnTile + lane] = p;
+            if (lane == 0) s_corr[qi] = corr;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kOut; ++k) {
+            const int i = tid + k * 128;
+            if (i >= nq * D) break;
+            const int qi = i / D, d = i - qi * D;
+            const float* pq = s_pt + qi * kAttnTile;
+            double a = acc[k] * (double)s_corr[qi];
+            for (int t = 0; t < n; ++t) a += (double)pq[t] * (double)s_v[t * pitch + d];
+            acc[k] = a;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < QW; ++j)
+        if (lane == 0 && warp + 4 * j < nq) s_l[warp + 4 * j] = (float)lrun[j];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kOut; ++k) {
+        const int i = tid + k * 128;
+        if (i >= nq * D) break;
+        const int qi = i / D, d = i - qi * D;
+        mix[(size_t)(m.row0 + r0 + qi) * hid + h * D + d] = (float)(acc[k] / (double)s_l[qi]);
+    }
+}
+
 }  // namespace tdkv
 
 using namespace tdkv;
@@ -373,7 +490,8 @@ extern "C" int32_t tdkv_attention(const float* d_q, const float* d_k_fresh, cons
 extern "C" int32_t tdkv_attention_many(const float* d_q, const float* d_k_fresh,
                                        const float* d_v_fresh, const tdkv_attn_member* d_members,
                                        int32_t n_members, int32_t layer, int32_t total_rows,
-                                       int32_t n_tiles, int32_t max_tokens, int32_t num_heads,
+                                       int32_t n_tiles, int32_t rows_per_tile,
+                                       int32_t max_tokens, int32_t num_heads,
                                        int32_t head_dim, float scale, float* d_mix,
                                        void* stream) {
     if (n_members < 0 || total_rows < 0 || n_tiles < 0 || layer < 0 || max_tokens <= 0 ||
@@ -386,8 +504,30 @@ extern "C" int32_t tdkv_attention_many(const float* d_q, const float* d_k_fresh,
     if (smem > 200 * 1024)
         return set_error(TDKV_EUNSUPPORTED, "tdkv_attention_many: %d tokens exceed shared memory",
                          max_tokens);
-    if (n_tiles > 0 && head_dim <= 128) {
-        const int kq = attn_rows_per_tile(head_dim);
+    if (n_tiles > 0 && rows_per_tile == 16) {
+        if (head_dim > 64)
+            return set_error(TDKV_EINVAL, "tdkv_attention_many: 16-row tiles need head_dim <= 64");
+        const int pitch = attn_pitch(head_dim);
+        const size_t osmem = ((size_t)2 * kAttnTile * pitch + (size_t)16 * head_dim +
+                              (size_t)16 * kAttnTile + 2 * 16) * sizeof(float);
+        if (cudaFuncSetAttribute(attention_online_kernel<4>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)osmem) !=
+            cudaSuccess)
+            return check_launch("tdkv_attention_many: cudaFuncSetAttribute");
+        dim3 ogrid(n_tiles, num_heads);
+        attention_online_kernel<4><<<ogrid, 128, osmem, static_cast<cudaStream_t>(stream)>>>(
+            d_q, d_k_fresh, d_v_fresh, d_members, n_members, layer, num_heads, head_dim, scale,
+            d_mix);
+        count_launch();
+        return check_launch("tdkv_attention_many");
+    }
+    if (n_tiles > 0) {
+        if (rows_per_tile != 8 || head_dim > 128)
+            return set_error(TDKV_EINVAL,
+                             "tdkv_attention_many: tiles of %d rows with head_dim %d (8 rows and "
+                             "head_dim <= 128, or 16 rows and head_dim <= 64)",
+                             rows_per_tile, head_dim);
+        const int kq = 8;
         const size_t tsmem = ((size_t)kAttnTile * attn_pitch(head_dim) + (size_t)kq * head_dim +
                               (size_t)kq * max_tokens) * sizeof(float);
         if (tsmem > 200 * 1024)
