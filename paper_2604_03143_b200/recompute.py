@@ -26,8 +26,7 @@ import numpy as np
 import torch
 
 from . import _kernels, _lib
-from ._device import (default_device, h2d, is_host, ptr, stream_handle, to_device, to_host,
-                      upload)
+from ._device import default_device, h2d, is_host, ptr, stream_handle, to_device, to_host
 from .core import LayeredKv, ModelConfig, union_sorted
 from .gemm import gemm_tn
 from .ledger import CostLedger
@@ -165,42 +164,60 @@ def forward_many(m: ToyModel, items, layers: int):
     toks = [np.asarray(it[0], np.int64) for it in items]
     pos = [np.asarray(it[1], np.int64) for it in items]
     Ts = [t.size for t in toks]
-    # one upload: every item's fix indices (int64) then fresh_of maps (int32)
-    fresh_of = np.full(int(sum(Ts)), -1, np.int32)
+    # ONE upload per forward: [fix indices | tokens | positions (int64, R each) |
+    # attention member table | fresh_of maps (int32)]; device addresses inside
+    # the table point back into the same buffer
+    sumT = int(sum(Ts))
+    live = F > 0
+    n_live = int(live.sum())
+    mt = _lib.ATTN_MEMBER.itemsize
+    nbytes = 24 * R + mt * n_live + 4 * sumT
+    d_blob = torch.empty(nbytes + 8, dtype=torch.uint8, device=dev)
+    base = ptr(d_blob)
+    fix_base, tok_base, pos_base = base, base + 8 * R, base + 16 * R
+    mem_base = base + 24 * R
+    fo_base = mem_base + mt * n_live
+    blob = np.zeros(nbytes, np.uint8)
+    i64 = blob[:24 * R].view(np.int64)
+    i64[:R] = np.concatenate(fixes)
+    i64[R:2 * R] = np.concatenate([t[f] for t, f in zip(toks, fixes)])
+    i64[2 * R:] = np.concatenate([p[f] for p, f in zip(pos, fixes)])
+    fresh_of = blob[24 * R + mt * n_live:].view(np.int32)
+    fresh_of[:] = -1
     t0 = np.concatenate([[0], np.cumsum(Ts)[:-1]]).astype(np.int64)
     for i, f in enumerate(fixes):
         fresh_of[t0[i] + f] = np.arange(f.size, dtype=np.int32)
-    meta = np.concatenate([np.concatenate(fixes).view(np.uint8), fresh_of.view(np.uint8)])
-    d_meta = h2d(meta, dev)
-    fix_base = ptr(d_meta)
-    fo_base = fix_base + 8 * R
-    table = _kernels.rope_table(np.concatenate([p[f] for p, f in zip(pos, fixes)]), D,
-                                m.rope_base, torch.float32, dev)
-    h = torch.empty((R, hid), dtype=torch.float32, device=dev)
-    d_tok = h2d(np.concatenate([t[f] for t, f in zip(toks, fixes)]), dev)
-    job = _kernels.rows_job(m.embed, None, 0, h, None, 0, R, src_rows=d_tok)
-    _kernels.rows(_kernels.rows_jobs([job]), R, None, 1, 1, hid, _kernels.ROWS_BLOCK,
-                  torch.float32, dev)
-    qkv = torch.empty((R, 3 * hid), dtype=torch.float32, device=dev)
-    q = torch.empty((R, hid), dtype=torch.float32, device=dev)
-    mix = torch.empty((R, hid), dtype=torch.float32, device=dev)
-    members = np.zeros(len(items), _lib.ATTN_MEMBER)
     rows_per_tile = _attn_rows_per_tile(D)
     tiles = -(-F // rows_per_tile)                # query tiles per member
     tile0 = np.concatenate([[0], np.cumsum(tiles)[:-1]]).astype(np.int64)
     n_tiles = int(tiles.sum()) if D <= 128 else 0
+    members = blob[24 * R:24 * R + mt * n_live].view(_lib.ATTN_MEMBER)
+    j = 0
     for i, it in enumerate(items):
+        if not live[i]:
+            continue
         ck, cv = it[3], it[4]
         if ck is None:                       # every attended row is fresh: never read
             ck = cv = out_k
             stride = 0
         else:
             stride = int(ck.shape[1]) * hid
-        members[i] = (ptr(ck), ptr(cv), fo_base + 4 * int(t0[i]), fix_base + 8 * int(row0[i]),
+        members[j] = (ptr(ck), ptr(cv), fo_base + 4 * int(t0[i]), fix_base + 8 * int(row0[i]),
                       stride, int(row0[i]), int(F[i]), Ts[i], int(tile0[i]))
-    live = F > 0
-    d_members = upload(members[live], dev)
-    n_live = int(live.sum())
+        j += 1
+    staged = torch.from_numpy(blob).pin_memory()
+    d_blob[:nbytes].copy_(staged, non_blocking=True)
+    d_i64 = d_blob[:24 * R].view(torch.int64)
+    table = torch.empty((R, D // 2, 2), dtype=torch.float64, device=dev)
+    _kernels.rope_table_from_device(d_i64[2 * R:], D, m.rope_base, torch.float32, table)
+    h = torch.empty((R, hid), dtype=torch.float32, device=dev)
+    job = _kernels.rows_job(m.embed, None, 0, h, None, 0, R, src_rows=d_i64[R:2 * R])
+    _kernels.rows(_kernels.rows_jobs([job]), R, None, 1, 1, hid, _kernels.ROWS_BLOCK,
+                  torch.float32, dev)
+    qkv = torch.empty((R, 3 * hid), dtype=torch.float32, device=dev)
+    q = torch.empty((R, hid), dtype=torch.float32, device=dev)
+    mix = torch.empty((R, hid), dtype=torch.float32, device=dev)
+    d_members = mem_base
     scale = float(np.float32(1.0 / np.sqrt(D)))
     stream = stream_handle(dev)
     for layer in range(layers):
@@ -210,7 +227,7 @@ def forward_many(m: ToyModel, items, layers: int):
         if layer == layers - 1:
             break                       # the last layer's attention only feeds h
         _lib.call("tdkv_attention_many", ptr(q), ptr(out_k[layer]), ptr(out_v[layer]),
-                  ptr(d_members), n_live, layer, R, n_tiles, rows_per_tile, max(Ts), H, D,
+                  d_members, n_live, layer, R, n_tiles, rows_per_tile, max(Ts), H, D,
                   scale, ptr(mix), stream)
         gemm_tn(mix, m.wm_t[layer], out=h, accumulate=True)
     return out_k, out_v, row0
