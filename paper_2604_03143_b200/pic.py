@@ -159,7 +159,7 @@ def probe_and_select(weights, members, contexts, cfg, ledger: Optional[CostLedge
              for i, sh in zip(live, shared)]
     items = [(np.asarray(members[i].tokens, np.int64), np.asarray(members[i].positions, np.int64),
               fx, contexts[i][0], contexts[i][1]) for i, fx in zip(live, fixes)]
-    pk, _, row0 = forward_many(model, items, cfg.check_layer + 1)
+    pk, _, row0 = forward_many(model, items, cfg.check_layer + 1, k_only_last=True)
     # the probe's check-layer rows of the shared positions, and the cached
     # (collector-rotated) rows they are compared with, gathered in one launch
     offs = np.concatenate([[0], np.cumsum(counts)[:-1]])

@@ -139,7 +139,7 @@ def _attn_rows_per_tile(head_dim: int) -> int:
     return 16 if _ATTN_ONLINE and head_dim <= 64 else 8
 
 
-def forward_many(m: ToyModel, items, layers: int):
+def forward_many(m: ToyModel, items, layers: int, k_only_last: bool = False):
     """The selective forward of several independent requests as ONE batch:
     ``items`` = [(tokens, positions, fix_idx, ctx_k, ctx_v)] (host integer
     arrays; device float32 context planes of shape (L, T_i, H, D), or None
@@ -148,6 +148,10 @@ def forward_many(m: ToyModel, items, layers: int):
     rows (grouped recovery, collective.py:152-187, batches its members this
     way); row results do not depend on the batch (rows are independent in
     the GEMMs and attend only to their own item's context).
+
+    ``k_only_last``: the caller reads only K of the last layer (the probe's
+    check layer), so that layer projects K alone (a third of its QKV GEMM);
+    its V plane is then undefined.
 
     Returns (out_k, out_v, row0): planes (layers, sum F_i, H, D) with item i's
     rows at [row0[i], row0[i] + F_i)."""
@@ -221,7 +225,11 @@ def forward_many(m: ToyModel, items, layers: int):
     scale = float(np.float32(1.0 / np.sqrt(D)))
     stream = stream_handle(dev)
     for layer in range(layers):
-        gemm_tn(h, m.wqkv_t[layer], out=qkv)
+        if k_only_last and layer == layers - 1:
+            # K columns only; Q and V of this layer are never read
+            gemm_tn(h, m.wqkv_t[layer][hid:2 * hid], out=qkv[:, hid:2 * hid])
+        else:
+            gemm_tn(h, m.wqkv_t[layer], out=qkv)
         _lib.call("tdkv_qkv_rope", ptr(qkv), ptr(table), R, H, D, ptr(q), ptr(out_k[layer]),
                   ptr(out_v[layer]), stream)
         if layer == layers - 1:
