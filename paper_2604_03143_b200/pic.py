@@ -4,7 +4,10 @@
 Every numeric stage runs on the device: the private prefix prefill and the
 probe/refresh forwards (K5: tcgen05 GEMMs + attention), the V copy and the
 batched K rotation (K1, the Collector), the check-layer difference pass and
-top-k (K4).  Host code keeps the reference's control flow and integer
+top-k (K4).  A group's members share every launch: one Collector pass, one
+batched forward each for the private prefixes, the probe and the refresh,
+one selection pass -- results are bit-identical to serial recovery because
+every row's arithmetic is independent of the batch.  Host code keeps the reference's control flow and integer
 metadata, so ``recover_prepared`` / ``collective_recover`` are drop-ins that
 take the reference's ``PreparedRequest`` / ``ReuseGroup`` objects (or
 anything with the same attributes) and return ``RecoveryResult`` /

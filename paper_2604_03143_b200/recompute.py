@@ -7,9 +7,12 @@ with rotary Q/K, causal softmax attention over the partly cached context,
 output mix folded into the residual stream; float32).  Here every
 projection is a tensor-core GEMM (``tdkv_gemm``: tcgen05, TMEM accumulator,
 3xTF32 for float32 operands), the rotary step and the attention are
-``tdkv_qkv_rope`` / ``tdkv_attention``, and the embedding gather and the
-row write-back use the row mover (K3).  The final layer's attention and
-mix are skipped: their only consumer is the next layer.
+``tdkv_qkv_rope`` / ``tdkv_attention_many`` (query-tiled; online softmax for
+head_dim <= 64), and the embedding gather and the row write-back use the row
+mover (K3).  The final layer's attention and mix are skipped: their only
+consumer is the next layer.  ``forward_many`` runs several requests' forwards
+as one batch (grouped recovery); ``selective_forward`` is its one-request
+case.
 
 Signatures follow the reference: ``selective_forward`` (= _selective_forward),
 ``full_prefill``, ``recompute_positions`` and ``refresh``; ``weights`` is the
