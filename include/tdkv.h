@@ -254,7 +254,8 @@ int32_t tdkv_rows(const tdkv_rows_job* d_jobs, int32_t n_jobs,
  *
  * tdkv_select_important: member m owns mags[member_off[m] .. member_off[m+1]);
  * writes its top min(budget[m], #nonzero) positions by (-mag, index), in
- * ascending order, to out_idx[member_off[m] ...] (select_important,
+ * ascending order, to out_idx[out_off[m] ...] (out_off NULL: member_off;
+ * an exclusive prefix of the budgets packs the results densely) (select_important,
  * pic.py:180-189), their number to out_count[m], and the float32 sum of its
  * magnitudes to deviation[m] (pic.py:280).  One CTA per member runs a
  * radix select over the magnitudes' bit patterns; at most 49152 positions
@@ -265,7 +266,8 @@ int32_t tdkv_keydiff(const void* d_fresh, const void* d_cached,
                      int32_t dtype, float* d_mags, void* stream);
 
 int32_t tdkv_select_important(const float* d_mags, const int64_t* d_member_off,
-                              const int32_t* d_budget, int32_t n_members,
+                              const int32_t* d_budget, const int64_t* d_out_off,
+                              int32_t n_members,
                               int32_t max_count, int32_t* d_out_idx,
                               int32_t* d_out_count, float* d_deviation, void* stream);
 

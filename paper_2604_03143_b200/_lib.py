@@ -127,7 +127,7 @@ _SIGS = {
                                 _I32, _I32, _P]),
     "tdkv_fill_rows": (_I32, [_P, _I64, _I32, _P, _I64, _I32, _I32, ctypes.c_uint32, _P]),
     "tdkv_keydiff": (_I32, [_P, _P, _P, _I64, _I32, _I32, _P, _P]),
-    "tdkv_select_important": (_I32, [_P, _P, _P, _I32, _I32, _P, _P, _P, _P]),
+    "tdkv_select_important": (_I32, [_P, _P, _P, _P, _I32, _I32, _P, _P, _P, _P]),
     "tdkv_gemm": (_I32, [_P, _I32, _P, _I32, _P, _I32, _I32, _I32, _I32, _I32, _I32, _P]),
     "tdkv_qkv_rope": (_I32, [_P, _P, _I32, _I32, _I32, _P, _P, _P, _P]),
     "tdkv_alloc_create": (_P, [_I64, _I32]),

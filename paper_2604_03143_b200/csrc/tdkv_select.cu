@@ -232,8 +232,9 @@ __device__ __forceinline__ void select_member_global(const float* __restrict__ m
 
 __global__ void __launch_bounds__(512)
     select_kernel(const float* __restrict__ mags, const int64_t* __restrict__ member_off,
-                  const int32_t* __restrict__ budget, int32_t* __restrict__ out_idx,
-                  int32_t* __restrict__ out_count, float* __restrict__ deviation) {
+                  const int32_t* __restrict__ budget, const int64_t* __restrict__ out_off,
+                  int32_t* __restrict__ out_idx, int32_t* __restrict__ out_count,
+                  float* __restrict__ deviation) {
     extern __shared__ __align__(16) uint32_t bits[];
     __shared__ double red[32];
     __shared__ int s_warp[33];
@@ -242,7 +243,8 @@ __global__ void __launch_bounds__(512)
     const int m = blockIdx.x;
     const int64_t off = member_off[m];
     const int n = (int)(member_off[m + 1] - off);
-    select_member_global<true>(mags + off, n, budget[m], out_idx + off, out_count + m,
+    select_member_global<true>(mags + off, n, budget[m], out_idx + (out_off ? out_off[m] : off),
+                               out_count + m,
                                deviation + m, hist, s_warp, red, s_nnz, s_sel, s_rem, bits);
 }
 
@@ -287,7 +289,8 @@ extern "C" int32_t tdkv_keydiff(const void* d_fresh, const void* d_cached,
 }
 
 extern "C" int32_t tdkv_select_important(const float* d_mags, const int64_t* d_member_off,
-                                         const int32_t* d_budget, int32_t n_members,
+                                         const int32_t* d_budget, const int64_t* d_out_off,
+                                         int32_t n_members,
                                          int32_t max_count, int32_t* d_out_idx,
                                          int32_t* d_out_count, float* d_deviation, void* stream) {
     if (n_members < 0 || max_count < 0) return set_error(TDKV_EINVAL, "tdkv_select_important: bad sizes");
@@ -302,7 +305,8 @@ extern "C" int32_t tdkv_select_important(const float* d_mags, const int64_t* d_m
                              (int)smem) != cudaSuccess)
         return check_launch("tdkv_select_important: cudaFuncSetAttribute");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    select_kernel<<<n_members, 512, smem, s>>>(d_mags, d_member_off, d_budget, d_out_idx,
+    select_kernel<<<n_members, 512, smem, s>>>(d_mags, d_member_off, d_budget, d_out_off,
+                                               d_out_idx,
                                                d_out_count, d_deviation);
     count_launch();
     return check_launch("tdkv_select_important");

@@ -68,6 +68,11 @@ class _SelectPlan:
         self.max_count = int(counts.max(initial=0))
         self.d_off = h2d(self.off, device)
         self.d_budget = h2d(np.asarray(budgets, np.int32), device)
+        # results packed densely: member m's indices at the prefix of the budgets
+        budgets = np.maximum(np.asarray(budgets, np.int64), 0)
+        self.out_off = np.concatenate([[0], np.cumsum(budgets)]).astype(np.int64)
+        self.d_out_off = h2d(self.out_off[:-1].copy(), device)
+        self.packed = int(self.out_off[-1])
 
 
 _PLANS: Dict[tuple, _SelectPlan] = {}
@@ -92,15 +97,16 @@ def _plan(counts: Sequence[int], device, budgets: Optional[Sequence[int]] = None
 def _launch_select(mags: torch.Tensor, p: _SelectPlan):
     dev = mags.device
     m = p.m
-    # one int32 buffer [counts | deviation bits | indices] -> a single D2H
-    buf = torch.empty(2 * m + max(p.total, 1), dtype=torch.int32, device=dev)
+    # one int32 buffer [counts | deviation bits | packed indices] -> a single D2H
+    buf = torch.empty(2 * m + max(p.packed, 1), dtype=torch.int32, device=dev)
     out_cnt = buf[:m]
     dev_sum = buf[m:2 * m].view(torch.float32)
     out_idx = buf[2 * m:]
     if m:
-        _lib.call("tdkv_select_important", ptr(mags), ptr(p.d_off), ptr(p.d_budget), m,
-                  p.max_count, ptr(out_idx), ptr(out_cnt), ptr(dev_sum), stream_handle(dev))
-    return p.off, out_idx, out_cnt, dev_sum, buf
+        _lib.call("tdkv_select_important", ptr(mags), ptr(p.d_off), ptr(p.d_budget),
+                  ptr(p.d_out_off), m, p.max_count, ptr(out_idx), ptr(out_cnt), ptr(dev_sum),
+                  stream_handle(dev))
+    return p.out_off, out_idx, out_cnt, dev_sum, buf
 
 
 def _select_device(mags: torch.Tensor, counts: Sequence[int], budgets: Sequence[int]):
@@ -124,8 +130,9 @@ def selection_kernels(fresh: torch.Tensor, cached: torch.Tensor,
                       cached_rows: Optional[torch.Tensor], counts: Sequence[int],
                       fraction: float):
     """The two K4 launches on device tensors, no host synchronization.
-    Returns (member offsets, int32 result buffer [counts | deviation bits |
-    indices])."""
+    Returns (result offsets, int32 result buffer [counts | deviation bits |
+    indices]); member m's indices start at result offset m (the prefix of
+    the budgets)."""
     mags = _mags_device(fresh, cached, cached_rows)
     off, _, _, _, buf = _launch_select(mags, _plan(counts, fresh.device, fraction=fraction))
     return off, buf
@@ -165,7 +172,7 @@ def batched_selection(fresh, cached, counts: Sequence[int], fraction: float,
     host = staged.numpy()
     cnt_h = host[:m].tolist()
     sums = host[m:2 * m].view(np.float32).tolist()
-    idx_h = host[2 * m:]
+    idx_h = host[2 * m:].astype(np.int64)        # one widening for every member
     starts = off.tolist()
     out = []
     for i, n in enumerate(counts):
@@ -173,7 +180,7 @@ def batched_selection(fresh, cached, counts: Sequence[int], fraction: float,
             out.append((np.empty(0, dtype=np.int64), 0.0))
             continue
         a = starts[i]
-        out.append((idx_h[a:a + cnt_h[i]].astype(np.int64), sums[i]))
+        out.append((idx_h[a:a + cnt_h[i]], sums[i]))
     return out
 
 

@@ -37,7 +37,7 @@ buf = torch.empty(2 * M + M * N, dtype=torch.int32, device=dev)
 
 def two():
     mags = sel._mags_device(fresh, plane, rows)
-    sel._lib.call("tdkv_select_important", sel.ptr(mags), sel.ptr(d_off), sel.ptr(d_bud), M, N,
+    sel._lib.call("tdkv_select_important", sel.ptr(mags), sel.ptr(d_off), sel.ptr(d_bud), 0, M, N,
                   sel.ptr(buf) + 8 * M, sel.ptr(buf), sel.ptr(buf) + 4 * M,
                   sel.stream_handle(dev))
 

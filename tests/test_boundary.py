@@ -222,7 +222,8 @@ def test_c_abi_rejects_bad_arguments_without_a_gpu():
     assert lib.tdkv_diff_compare(null, 1, null, null, null, null, 1, 8, 1, 8, 8, 7, null) == 2
     assert lib.tdkv_rows(null, 1, 8, null, 1, 1, 8, 8, 0, 0, 0, 0, null) == 1
     assert lib.tdkv_gemm(null, 8, null, 8, null, 8, 4, 4, 4, 0, 0, null) == 1
-    assert lib.tdkv_select_important(null, null, null, 1, 100000, null, null, null, null) == 2
+    assert lib.tdkv_select_important(null, null, null, null, 1, 100000, null, null, null,
+                                     null) == 2
     assert lib.tdkv_rope_table(null, 4, null, 4, 0, null, null) == 1
     # zero-size work is a successful no-op
     assert lib.tdkv_collect(null, null, 0, null, 0, 8, null, null, null, 0, null, null, 0,
