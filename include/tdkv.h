@@ -310,7 +310,7 @@ int32_t tdkv_attention(const float* d_q, const float* d_k_fresh, const float* d_
  * ceil(n_rows / rows_per_tile) tiles starting at tile index tile0 (n_tiles in
  * total), each CTA serving one tile of one member with every staged
  * key/value tile.  rows_per_tile 8 (head_dim <= 128): two-pass softmax over a
- * stored score row; rows_per_tile 16 (head_dim <= 64): online softmax
+ * stored score row; rows_per_tile 16 (head_dim <= 128): online softmax
  * (running max / sum, float64 accumulators rescaled per 32-token tile).
  * n_tiles == 0 runs one CTA per row. */
 typedef struct {

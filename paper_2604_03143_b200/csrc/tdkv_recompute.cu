@@ -323,21 +323,21 @@ __global__ void __launch_bounds__(128)
     }
 }
 
-// Online-softmax form of the query-tiled attention (head_dim <= 64): one CTA
+// Online-softmax form of the query-tiled attention (head_dim <= 128): one CTA
 // per (32 fixed rows of one member, head) streams the member's keys/values
 // once in 32-token tiles (K and V staged together), keeping a running max and
 // sum per query and rescaling its float64 output accumulators per tile, so
 // no full score row is stored and every staged tile serves 32 queries.
 // Warp w owns queries w, w + 4, ..., (QW per warp); thread i owns outputs
 // (q, d) for q * D + d = i + 128 k.
-template <int QW>
+template <int QW, int DMAX>   // DMAX: largest head_dim served (64 or 128)
 __global__ void __launch_bounds__(128)
     attention_online_kernel(const float* __restrict__ q, const float* __restrict__ k_fresh,
                             const float* __restrict__ v_fresh,
                             const tdkv_attn_member* __restrict__ members, int n_members,
                             int layer, int H, int D, float scale, float* __restrict__ mix) {
     constexpr int kQ = 4 * QW;
-    constexpr int kOut = kQ * 64 / 128;                         // outputs per thread (D <= 64)
+    constexpr int kOut = kQ * DMAX / 128;                       // outputs per thread (D <= DMAX)
     extern __shared__ float s_dyn[];   // [K tile | V tile | q kQ x D | p kQ x kAttnTile | corr kQ | l kQ]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int h = blockIdx.y;
@@ -505,17 +505,17 @@ extern "C" int32_t tdkv_attention_many(const float* d_q, const float* d_k_fresh,
         return set_error(TDKV_EUNSUPPORTED, "tdkv_attention_many: %d tokens exceed shared memory",
                          max_tokens);
     if (n_tiles > 0 && rows_per_tile == 16) {
-        if (head_dim > 64)
-            return set_error(TDKV_EINVAL, "tdkv_attention_many: 16-row tiles need head_dim <= 64");
+        if (head_dim > 128)
+            return set_error(TDKV_EINVAL, "tdkv_attention_many: 16-row tiles need head_dim <= 128");
         const int pitch = attn_pitch(head_dim);
         const size_t osmem = ((size_t)2 * kAttnTile * pitch + (size_t)16 * head_dim +
                               (size_t)16 * kAttnTile + 2 * 16) * sizeof(float);
-        if (cudaFuncSetAttribute(attention_online_kernel<4>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)osmem) !=
+        auto kern = head_dim <= 64 ? attention_online_kernel<4, 64> : attention_online_kernel<4, 128>;
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)osmem) !=
             cudaSuccess)
             return check_launch("tdkv_attention_many: cudaFuncSetAttribute");
         dim3 ogrid(n_tiles, num_heads);
-        attention_online_kernel<4><<<ogrid, 128, osmem, static_cast<cudaStream_t>(stream)>>>(
+        kern<<<ogrid, 128, osmem, static_cast<cudaStream_t>(stream)>>>(
             d_q, d_k_fresh, d_v_fresh, d_members, n_members, layer, num_heads, head_dim, scale,
             d_mix);
         count_launch();
@@ -524,8 +524,8 @@ extern "C" int32_t tdkv_attention_many(const float* d_q, const float* d_k_fresh,
     if (n_tiles > 0) {
         if (rows_per_tile != 8 || head_dim > 128)
             return set_error(TDKV_EINVAL,
-                             "tdkv_attention_many: tiles of %d rows with head_dim %d (8 rows and "
-                             "head_dim <= 128, or 16 rows and head_dim <= 64)",
+                             "tdkv_attention_many: tiles of %d rows with head_dim %d (8 or 16 "
+                             "rows, head_dim <= 128)",
                              rows_per_tile, head_dim);
         const int kq = 8;
         const size_t tsmem = ((size_t)kAttnTile * attn_pitch(head_dim) + (size_t)kq * head_dim +

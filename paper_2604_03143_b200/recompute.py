@@ -8,7 +8,7 @@ output mix folded into the residual stream; float32).  Here every
 projection is a tensor-core GEMM (``tdkv_gemm``: tcgen05, TMEM accumulator,
 3xTF32 for float32 operands), the rotary step and the attention are
 ``tdkv_qkv_rope`` / ``tdkv_attention_many`` (query-tiled; online softmax for
-head_dim <= 64), and the embedding gather and the row write-back use the row
+head_dim <= 128), and the embedding gather and the row write-back use the row
 mover (K3).  The final layer's attention and mix are skipped: their only
 consumer is the next layer.  ``forward_many`` runs several requests' forwards
 as one batch (grouped recovery); ``selective_forward`` is its one-request
@@ -138,8 +138,8 @@ _ATTN_ONLINE = os.environ.get("TDKV_ATTN_ONLINE", "1") != "0"
 
 def _attn_rows_per_tile(head_dim: int) -> int:
     """Fixed rows per CTA of the query-tiled attention: 16 with the online
-    softmax (head_dim <= 64; 11% faster on the recovery round), else 8."""
-    return 16 if _ATTN_ONLINE and head_dim <= 64 else 8
+    softmax (head_dim <= 128; 11% faster on the recovery round), else 8."""
+    return 16 if _ATTN_ONLINE and head_dim <= 128 else 8
 
 
 def forward_many(m: ToyModel, items, layers: int, k_only_last: bool = False):

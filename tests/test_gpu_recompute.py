@@ -129,8 +129,7 @@ def test_attention_entry_points_agree(D):
         _lib.call("tdkv_attention", ptr(q[sl]), ptr(kf[sl]), ptr(vf[sl]), ptr(ctx[i][0][layer]),
                   ptr(ctx[i][1][layer]), ptr(fresh_of[i]), ptr(d_fix[i]), F[i], Ts[i], H, D,
                   scale, ptr(want[sl]), stream)
-    forms = ([(0, 8)] + ([(8, 8)] if D <= 128 else [])              # (tile rows, rows arg)
-             + ([(16, 16)] if D <= 64 else []))
+    forms = [(0, 8)] + ([(8, 8), (16, 16)] if D <= 128 else [])   # (tile rows, rows arg)
     for tile, rows_arg in forms:
         members = np.zeros(len(Ts), _lib.ATTN_MEMBER)
         tiles = -(-np.asarray(F) // max(tile, 1)) if tile else np.zeros(len(Ts), np.int64)
