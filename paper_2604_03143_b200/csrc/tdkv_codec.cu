@@ -196,6 +196,39 @@ __global__ void __launch_bounds__(256)
 // same (pair, layer) -- a look-back over the published flags -- then copies
 // the mirror block (still L2-resident: it was read microseconds ago) to the
 // slot, zero-padded.  DRAM traffic is the algorithmic 2 x dense + payload.
+// The violation magnitude of one block (max |mirror - master| per plane,
+// combined as the reference does) and the pair's first violating block;
+// every thread of the CTA calls it.
+template <typename T, typename V>
+__device__ __noinline__ void record_violation(const V* mk, const V* mv, const V* rk, const V* rv,
+                                              int units, float* maxabs, int32_t* violation,
+                                              int block_index) {
+    __shared__ float red_k[32], red_v[32];
+    float mk_ = 0.f, mv_ = 0.f;
+    for (int w = threadIdx.x; w < units; w += blockDim.x) {
+        mk_ = nanmax(mk_, unit_maxabs_nan<T>(mk[w], rk[w]));
+        mv_ = nanmax(mv_, unit_maxabs_nan<T>(mv[w], rv[w]));
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        mk_ = nanmax(mk_, __shfl_xor_sync(0xffffffffu, mk_, o));
+        mv_ = nanmax(mv_, __shfl_xor_sync(0xffffffffu, mv_, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        red_k[threadIdx.x >> 5] = mk_;
+        red_v[threadIdx.x >> 5] = mv_;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float a = 0.f, c = 0.f;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            a = nanmax(a, red_k[w]);
+            c = nanmax(c, red_v[w]);
+        }
+        *maxabs = py_max_kv(a, c);
+        atomicMin(violation, block_index);
+    }
+}
+
 template <typename T, int UB>
 __global__ void __launch_bounds__(256)
     diff_encode_kernel(const tdkv_diff_pair* __restrict__ pairs,
@@ -206,7 +239,6 @@ __global__ void __launch_bounds__(256)
     using V = typename UnitBits<UB>::V;
     constexpr int kUnroll = 2;
     __shared__ int s_tile, s_before;
-    __shared__ float red[32];
     if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
     __syncthreads();
     const int item = s_tile;
@@ -254,34 +286,9 @@ __global__ void __launch_bounds__(256)
         atomicExch(flags + row + b, stored ? 2 : 1);        // publish
     }
     const tdkv_diff_out out = outs[pi];
-    if (any && !is_hinted) {
-        // soundness violation (rare): max |mirror - master| per plane, combined
-        // as the reference does
-        float mk_ = 0.f, mv_ = 0.f;
-        for (int w = threadIdx.x; w < units; w += blockDim.x) {
-            mk_ = nanmax(mk_, unit_maxabs_nan<T>(mk[w], rk[w]));
-            mv_ = nanmax(mv_, unit_maxabs_nan<T>(mv[w], rv[w]));
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-            mk_ = nanmax(mk_, __shfl_xor_sync(0xffffffffu, mk_, o));
-            mv_ = nanmax(mv_, __shfl_xor_sync(0xffffffffu, mv_, o));
-        }
-        __shared__ float red2[32];
-        if ((threadIdx.x & 31) == 0) {
-            red[threadIdx.x >> 5] = mk_;
-            red2[threadIdx.x >> 5] = mv_;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            float a = 0.f, c = 0.f;
-            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-                a = nanmax(a, red[w]);
-                c = nanmax(c, red2[w]);
-            }
-            viol_maxabs[row + b] = py_max_kv(a, c);
-            atomicMin(violation + pi, layer * g.nb + b);
-        }
-    }
+    if (any && !is_hinted)   // soundness violation (rare): out of line, off the register budget
+        record_violation<T, V>(mk, mv, rk, rv, units, viol_maxabs + row + b, violation + pi,
+                               layer * g.nb + b);
     const bool last = b == g.nb - 1;
     if (!stored && !last) {
         if (threadIdx.x == 0) out.blkmap[layer * g.nb + b] = -1;
