@@ -255,3 +255,23 @@ def test_collect_sources_rejects_bad_arguments_without_a_gpu():
     # K+V sources with a K-only destination (and the converse) are rejected
     assert lib.tdkv_collect_sources(tbl, None, 2, fake, 0, *tail_v) == 1
     assert lib.tdkv_collect_sources(tbl, tbl, 2, fake, 0, *tail) == 1
+
+
+def test_missing_library_fails_loudly():
+    """No CPU fallback: with the library absent the entry points raise
+    TdkvUnavailable instead of computing anything on the host."""
+    import subprocess
+    import sys
+    code = (
+        "import paper_2604_03143_b200 as p\n"
+        "for fn in (p.launch_count, lambda: p.SegmentIndex(4)):\n"
+        "    try:\n"
+        "        fn()\n"
+        "    except p.TdkvUnavailable:\n"
+        "        continue\n"
+        "    raise SystemExit('entry point ran without libtdkv.so')\n"
+        "print('ok')\n")
+    env = dict(os.environ, TDKV_LIBRARY=os.path.join(ROOT, "no-such-dir", "libtdkv.so"))
+    out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True,
+                         text=True, timeout=300)
+    assert out.returncode == 0 and out.stdout.strip() == "ok", out.stdout + out.stderr
