@@ -275,3 +275,45 @@ def test_missing_library_fails_loudly():
     out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True,
                          text=True, timeout=300)
     assert out.returncode == 0 and out.stdout.strip() == "ok", out.stdout + out.stderr
+
+
+def test_integration_binding_matches_library_signatures():
+    """The ctypes stub INTEGRATION.md shows a maintainer declares the same
+    argument types as the repo's own binding (and so as include/tdkv.h)."""
+    import ctypes
+    from paper_2604_03143_b200 import _lib
+    text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    names = {"_P": ctypes.c_void_p, "_I32": ctypes.c_int32, "_I64": ctypes.c_int64,
+             "ctypes.c_float": ctypes.c_float, "ctypes.c_uint32": ctypes.c_uint32}
+    found = re.findall(r"_lib\.(tdkv_\w+)\.argtypes = \[([^\]]*)\]", text, re.S)
+    assert len(found) >= 15
+    for fn, body in found:
+        args = [names[a.strip()] for a in re.sub(r"#[^\n]*", "", body).split(",") if a.strip()]
+        assert args == _lib._SIGS[fn][1], fn
+
+
+def test_binding_signatures_match_header_prototypes():
+    """Every prototype in include/tdkv.h and its ctypes declaration agree
+    argument by argument (pointer / int32 / int64 / float), so a stale
+    binding cannot shift arguments silently."""
+    import ctypes
+    from paper_2604_03143_b200 import _lib
+    text = open(os.path.join(ROOT, "include", "tdkv.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    text = re.sub(r"//[^\n]*", "", text)
+
+    def ctype(decl):
+        decl = decl.strip()
+        if "*" in decl:
+            return ctypes.c_void_p
+        base = decl.replace("const ", "").split()[0]
+        return {"int32_t": ctypes.c_int32, "int64_t": ctypes.c_int64, "float": ctypes.c_float,
+                "uint32_t": ctypes.c_uint32, "tdkv_pinned_fn": ctypes.c_void_p}[base]
+
+    seen = set()
+    for fn, body in re.findall(r"(?<!\*)\b(tdkv_\w+)\s*\(([^;{]*?)\)\s*;", text, re.S):
+        body = body.strip()
+        args = [] if body in ("", "void") else [ctype(a) for a in body.split(",")]
+        assert args == _lib._SIGS[fn][1], fn
+        seen.add(fn)
+    assert seen == set(_lib.EXPORTS)
