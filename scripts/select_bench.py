@@ -55,3 +55,16 @@ for name, fn in (("selection_kernels", api), ("direct", two)):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
     print(f"M={M} N={N} frac={FRAC} {name}: {ms * 1e3:.1f} us, {nbytes / ms / 1e6:.0f} GB/s")
+
+# keydiff alone (the gather-read half of K4)
+for _ in range(3):
+    sel._mags_device(fresh, plane, rows)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(20):
+    sel._mags_device(fresh, plane, rows)
+e1.record()
+torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / 20
+print(f"M={M} N={N} keydiff: {ms * 1e3:.1f} us, {nbytes / ms / 1e6:.0f} GB/s")
