@@ -3,17 +3,20 @@
 diff codec's GB/s, on B200 (BASELINE.json metric).
 
 A step is one All-Gather round of the KV Collector over the configured
-synthetic round (default C2: Qwen2.5-7B-shaped bf16 KV, 50 agents per GPU x
-16 shared 256-token blocks): [N>1: the masters' exchange -- NCCL broadcast
-from rank 0 overlapped with K1 per layer chunk, or with --exchange p2p no
-transfer at all: K1 reads every tile from its owner over NVLink] + K0
-(cos/sin rows) + K1 (rotate + scatter into every agent's paged slots).  ``value`` = algorithmic bytes (M + N*M per GPU) of all
+synthetic round (default C3, north_star's target: Qwen2.5-14B-shaped bf16 KV
+(48 layers, 8 KV heads, d=128), 250 agents in 10 sessions of 25, 25 shared
+20-token blocks per session; C2 = Qwen2.5-7B-shaped, 50 agents x 16 shared
+256-token blocks, is ``--config c2``): [N>1: the masters' exchange -- NCCL
+broadcast / per-session send-recv overlapped with K1 per layer chunk, or with
+--exchange p2p no transfer at all: K1 reads every tile from its owner over
+NVLink] + K0 (cos/sin rows) + K1 (rotate + scatter into every agent's paged
+slots).  ``value`` = algorithmic bytes (M + N*M per GPU) of all
 ranks / max-over-ranks device time.  Agents are sharded: weak scaling (each
 GPU owns a config's worth of agents: C1, C2, C4) or strong scaling (the
 config's agents split over the GPUs: C3's 250 agents in 10 sessions, C5's
 1000 agents collected in pool sub-batches of 125).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--exchange p2p]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--exchange p2p]
     python bench.py --impl reference ...   # CPU oracle port on the host cores
 
 Sub-benchmarks on the same line: the diff codec (encode, fused and dense
@@ -42,7 +45,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="tdkv", choices=["tdkv", "reference"])
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c3",
+                    help="c1..c5 (default c3: north_star's Qwen2.5-14B-shaped 250-agent round)")
     ap.add_argument("--agents", type=int, default=0, help="agents per GPU (default: config)")
     ap.add_argument("--no-codec", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -143,15 +147,20 @@ def measured_peak_hbm():
         return 6650.0, "fallback"
 
 
-def ncu_traffic(kernel: str):
-    """dram bytes per launch of ``kernel`` from the committed ncu summary."""
-    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+def ncu_traffic(kernel: str, workload: str):
+    """DRAM bytes per launch of ``kernel`` from the committed ncu capture of
+    THIS workload (profiles/ncu_traffic.json) and the capture it came from;
+    (None, None) when no capture of this workload exists -- never another
+    config's figure."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            data = json.load(f)
-        return data.get(kernel, {}).get("dram_bytes_per_launch")
+            entry = json.load(f).get(workload, {}).get(kernel)
     except Exception:   # noqa: BLE001
-        return None
+        entry = None
+    if not entry:
+        return None, None
+    return entry["dram_bytes_per_launch"], f"{entry.get('round')} {entry.get('report')}"
 
 
 # ---------------------------------------------------------------------------
@@ -243,7 +252,8 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": "collected KV GB/s", "value": round(gbs, 4),
         "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": round(t * 1e3, 3), "higher_is_better": True,
+        "scaling": "strong" if spec.strong else "weak",
         "vs_baseline": None, "dtype": spec.dtype, "data": "synthetic",
         "config": {"workload": spec.name, "agents_per_step": procs},
         "agents_per_s": round(procs / t, 3),
@@ -449,7 +459,7 @@ def run_tdkv(args):
 
     peak, peak_kind = measured_peak_hbm()
     achieved = step_bytes / (k1_ms * 1e-3) / 1e9
-    traffic = ncu_traffic("collect_kernel")
+    traffic, traffic_src = ncu_traffic("collect_kernel", spec.name)
     line = {
         "metric": "collected KV GB/s", "value": round(value, 2), "unit": "GB/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -470,6 +480,7 @@ def run_tdkv(args):
         "roofline": {"bound": "hbm", "kernel": "collect_kernel (K1)",
                      "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "traffic_source": traffic_src,
                      "peak_source": peak_kind,
                      "algorithmic_bytes_per_launch": step_bytes,
                      "k1_ms": round(k1_ms, 4)},
@@ -881,6 +892,10 @@ def codec_bench(tk, spec, pool, maps, dev, args, peak, frac=None, hint_all=False
     payload = sum(d.payload_nbytes for d in diffs)
     changed = sum(sum(d.changed_blocks_per_layer) for d in diffs)
     enc_bytes = n_mirrors * 2 * dense + payload + 4 * changed
+    # the family byte model: the master is read once for the whole family
+    # (K2/K3 order their work so the P mirrors of a master tile run back to
+    # back and share it through L2)
+    enc_family_bytes = dense + n_mirrors * dense + payload + 4 * changed
     # fused restore of every mirror into its agent's slots
     fam = tk.MasterEntry(0, master, pin_count=n_mirrors)
     handles = [tk.MirrorHandle(0, i + 1, fam, d) for i, d in enumerate(diffs)]
@@ -897,6 +912,7 @@ def codec_bench(tk, spec, pool, maps, dev, args, peak, frac=None, hint_all=False
     torch.cuda.synchronize(dev)
     dec_s = ev0.elapsed_time(ev1) * 1e-3 / reps
     dec_bytes = n_mirrors * 2 * dense
+    dec_family_bytes = dense + payload + n_mirrors * dense
     # the paper's fused-vs-dense comparison, one mirror per
     # API call as the reference restores them (trace.py:314-318): fused_restore
     # vs dense_restore (materialize the mirror, then rotate + write it)
@@ -911,7 +927,9 @@ def codec_bench(tk, spec, pool, maps, dev, args, peak, frac=None, hint_all=False
         ev1.record()
         torch.cuda.synchronize(dev)
         per[name] = ev0.elapsed_time(ev1) / n_mirrors
-    wire = [tk.wire_nbytes(d, 2) for d in diffs]
+    wire = [tk.wire_nbytes(d) for d in diffs]       # == len(serialize_diff(d))
+    dense_f32 = tk.kv_dense_nbytes(T, spec.num_layers, spec.num_heads, spec.head_dim)
+    pay_bytes = [d.payload_nbytes for d in diffs]
     # TDDF wire images (float32 payload, the reference format): GPU pack of
     # the whole family + one D2H, and GPU unpack of one image into device
     # slabs (H2D included); bytes = wire image bytes
@@ -943,11 +961,23 @@ def codec_bench(tk, spec, pool, maps, dev, args, peak, frac=None, hint_all=False
         "decode_gbs": round(dec_bytes / dec_s / 1e9, 1),
         "decode_frac": round(dec_bytes / dec_s / 1e9 / peak, 4),
         "decode_ms_per_family": round(dec_s * 1e3, 3),
+        "family_model": {
+            "encode_bytes": int(enc_family_bytes), "decode_bytes": int(dec_family_bytes),
+            "encode_device_gbs": round(enc_family_bytes / enc_dev_s / 1e9, 1),
+            "encode_device_frac": round(enc_family_bytes / enc_dev_s / 1e9 / peak, 4),
+            "decode_gbs": round(dec_family_bytes / dec_s / 1e9, 1),
+            "decode_frac": round(dec_family_bytes / dec_s / 1e9 / peak, 4),
+            "bytes": "encode: dense (master once) + P*dense (mirrors) + payload + 4*changed; "
+                     "decode: dense (master once) + payload + P*dense (pool writes)"},
         "restore_ms_per_mirror": {"fused": round(per["fused"], 4), "dense": round(per["dense"], 4),
                                   "dense_over_fused": round(per["dense"] / per["fused"], 2),
                                   "note": "one mirror per API call (host planning included), "
                                           f"CUDA events around the {n_mirrors} calls"},
-        "compression_ratio_mean": round(float(np.mean([dense / w for w in wire])), 3),
+        # CompressionStats.ratios as the reference computes them: float32 dense
+        # bytes / bytes of the float32 TDDF image serialize_diff emits
+        "compression_ratio_mean": round(float(np.mean([dense_f32 / w for w in wire])), 3),
+        # the in-HBM form: bf16 dense cache / bf16 payload slab bytes
+        "payload_ratio_mean": round(float(np.mean([dense / max(1, b) for b in pay_bytes])), 3),
         "wire_pack_gbs": round(wire_total / pack_s / 1e9, 2),
         "wire_unpack_gbs": round(unpack_bytes / unpack_s / 1e9, 2),
         "wire_note": "serialize_many of the family (GPU pack, one D2H into pinned memory, "

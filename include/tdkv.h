@@ -235,6 +235,10 @@ typedef struct {
  * 16-byte units then take the TMA-staged path (tiles of tile_rows rows,
  * 0 = block_size, double-buffered in shared memory by cp.async.bulk). */
 #define TDKV_ROWS_CONTIGUOUS 1
+/* TDKV_ROWS_JOB_MINOR orders the work items (layer, block, tile, job): the
+ * jobs of one family (mirrors of one master, trace.py:289-329) then read each
+ * master tile back to back, so DRAM serves it once and L2 the rest. */
+#define TDKV_ROWS_JOB_MINOR 2
 
 int32_t tdkv_rows(const tdkv_rows_job* d_jobs, int32_t n_jobs,
                   int32_t max_tokens, const void* d_table,

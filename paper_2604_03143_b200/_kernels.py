@@ -83,8 +83,10 @@ def rope_table_from_device(d_deltas: torch.Tensor, head_dim: int, base: float,
 
 def rows(jobs: np.ndarray, max_tokens: int, table: Optional[torch.Tensor], num_layers: int,
          num_heads: int, head_dim: int, block_size: int, kv_dtype: torch.dtype,
-         device: torch.device, grid_limit: int = 0) -> None:
-    """K3 over a ROWS_JOB descriptor array."""
+         device: torch.device, grid_limit: int = 0, job_minor: bool = False) -> None:
+    """K3 over a ROWS_JOB descriptor array.  ``job_minor`` orders the work
+    (layer, block, tile, job) -- for jobs sharing a master (a family), whose
+    tiles are then read from DRAM once and from L2 by the other jobs."""
     if jobs.size == 0 or max_tokens == 0:
         return
     esz = 4 if kv_dtype == torch.float32 else 2
@@ -92,12 +94,16 @@ def rows(jobs: np.ndarray, max_tokens: int, table: Optional[torch.Tensor], num_l
     if _contiguous(jobs, esz):
         flags = _lib.ROWS_CONTIGUOUS
         tile = min(block_size, tile_rows_for(num_heads * head_dim * esz))
+    if job_minor and jobs.size > 1 and _JOB_MINOR:
+        flags |= _lib.ROWS_JOB_MINOR
     d_jobs = upload(jobs, device)
     _lib.call("tdkv_rows", ptr(d_jobs), int(jobs.size), int(max_tokens), ptr(table),
               num_layers, num_heads, head_dim, block_size, dtype_code(kv_dtype), flags, tile,
               grid_limit, stream_handle(device))
 
 
+# TDKV_RESTORE_ORDER=job keeps the job-major order for A/B measurement
+_JOB_MINOR = __import__("os").environ.get("TDKV_RESTORE_ORDER", "family") != "job"
 _ROWS_SMEM = int(__import__("os").environ.get("TDKV_ROWS_SMEM", 72 * 1024))
 
 

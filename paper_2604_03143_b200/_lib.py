@@ -24,6 +24,7 @@ TDKV_F32 = 0
 TDKV_BF16 = 1
 NO_VIOLATION = 0x7F7F7F7F
 ROWS_CONTIGUOUS = 1
+ROWS_JOB_MINOR = 2
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

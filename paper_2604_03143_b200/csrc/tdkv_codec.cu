@@ -7,6 +7,7 @@
 // flags in block order and copies the changed mirror blocks, zero-padded,
 // into the payload in ascending index order (diffstore.py:166-173).
 #include <climits>
+#include <cstdlib>
 
 #include "tdkv_common.cuh"
 
@@ -18,6 +19,8 @@ struct CodecGeom {
     int32_t row_elems;
     int32_t block_size;
     int32_t nb;
+    int32_t n_pairs;
+    int32_t pair_minor;   // 1: items ordered (layer, block, pair) -- the family order
 };
 
 template <typename T, int UB>
@@ -242,11 +245,25 @@ __global__ void __launch_bounds__(256)
     if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
     __syncthreads();
     const int item = s_tile;
-    const int per_pair = g.num_layers * g.nb;
-    const int pi = item / per_pair;
-    const int rem = item - pi * per_pair;
-    const int layer = rem / g.nb;
-    const int b = rem - layer * g.nb;
+    // Family order (default): the P mirrors of one master (layer, block)
+    // hold consecutive tickets, so the master tile is read from DRAM once and
+    // served from L2 to the other P-1 CTAs comparing against it (DRAM bytes
+    // per family: master once + P mirrors + payload).  A (pair, layer)'s
+    // lower blocks still hold lower tickets, so the look-back below never
+    // waits on a CTA that has not started.
+    int pi, layer, b;
+    if (g.pair_minor) {
+        const int lb = item / g.n_pairs;
+        pi = item - lb * g.n_pairs;
+        layer = lb / g.nb;
+        b = lb - layer * g.nb;
+    } else {
+        const int per_pair = g.num_layers * g.nb;
+        pi = item / per_pair;
+        const int rem = item - pi * per_pair;
+        layer = rem / g.nb;
+        b = rem - layer * g.nb;
+    }
     const int lo = b * g.block_size;
     const int hi = min(lo + g.block_size, g.num_tokens);
     const int upr = g.row_elems * (int)sizeof(T) / UB;
@@ -265,9 +282,9 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
         for (int q = 0; q < kUnroll; ++q) {
             const int w = u + q * blockDim.x;
-            a[q][0] = ld_stream(mk + w);
+            a[q][0] = __ldcg(mk + w);          // master: L2-resident for the family
             a[q][1] = __ldcg(rk + w);          // mirror stays in L2 for the copy
-            a[q][2] = ld_stream(mv + w);
+            a[q][2] = __ldcg(mv + w);
             a[q][3] = __ldcg(rv + w);
         }
 #pragma unroll
@@ -275,8 +292,8 @@ __global__ void __launch_bounds__(256)
             diff |= unit_differs<T>(a[q][0], a[q][1]) | unit_differs<T>(a[q][2], a[q][3]);
     }
     for (; u < units; u += blockDim.x)
-        diff |= unit_differs<T>(ld_stream(mk + u), __ldcg(rk + u)) |
-                unit_differs<T>(ld_stream(mv + u), __ldcg(rv + u));
+        diff |= unit_differs<T>(__ldcg(mk + u), __ldcg(rk + u)) |
+                unit_differs<T>(__ldcg(mv + u), __ldcg(rv + u));
     const int any = __syncthreads_or(diff);
     const bool is_hinted = hinted[(size_t)pi * g.nb + b] != 0;
     const bool stored = any && is_hinted;
@@ -369,6 +386,16 @@ static int32_t codec_check(const char* who, int32_t n_pairs, int32_t L, int32_t 
 // unit width for the codec: 16 B when a row is a whole number of 16-byte
 // units (the caller guarantees 16-byte aligned dense planes in that case),
 // otherwise 4 bytes (rows are always a multiple of 4 bytes).
+// TDKV_ENCODE_ORDER=pair selects the pair-major item order (each mirror's
+// blocks in a row; the master is re-read per mirror) for A/B measurement
+static int encode_pair_minor() {
+    static const int v = [] {
+        const char* e = getenv("TDKV_ENCODE_ORDER");
+        return (e && e[0] == 'p') ? 0 : 1;
+    }();
+    return v;
+}
+
 static int codec_unit(int32_t dtype, int32_t row_elems) {
     return (row_elems * (int)elt_size(dtype)) % 16 == 0 ? 16 : 4;
 }
@@ -387,7 +414,7 @@ extern "C" int32_t tdkv_diff_compare(const tdkv_diff_pair* d_pairs, int32_t n_pa
         return set_error(TDKV_EINVAL, "tdkv_diff_compare: null pointer");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     CodecGeom g{num_layers, num_tokens, num_heads * head_dim, block_size,
-                ceil_div(num_tokens, block_size)};
+                ceil_div(num_tokens, block_size), n_pairs, encode_pair_minor()};
     const long long items = (long long)n_pairs * num_layers * g.nb;
     if (items > INT_MAX) return set_error(TDKV_EINVAL, "tdkv_diff_compare: batch too large");
     if (cudaMemsetAsync(d_violation, 0x7f, sizeof(int32_t) * n_pairs, s) != cudaSuccess)
@@ -426,7 +453,7 @@ extern "C" int32_t tdkv_diff_compact(const tdkv_diff_pair* d_pairs, const tdkv_d
         return set_error(TDKV_EINVAL, "tdkv_diff_compact: null pointer");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     CodecGeom g{num_layers, num_tokens, num_heads * head_dim, block_size,
-                ceil_div(num_tokens, block_size)};
+                ceil_div(num_tokens, block_size), n_pairs, encode_pair_minor()};
     const int ub = codec_unit(dtype, g.row_elems);
     const dim3 grid((unsigned)(n_pairs * num_layers));
     if (dtype == TDKV_F32) {
@@ -461,7 +488,7 @@ extern "C" int32_t tdkv_diff_encode(const tdkv_diff_pair* d_pairs, const tdkv_di
         return set_error(TDKV_EINVAL, "tdkv_diff_encode: null pointer");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     CodecGeom g{num_layers, num_tokens, num_heads * head_dim, block_size,
-                ceil_div(num_tokens, block_size)};
+                ceil_div(num_tokens, block_size), n_pairs, encode_pair_minor()};
     const long long items = (long long)n_pairs * num_layers * g.nb;
     if (items > INT_MAX) return set_error(TDKV_EINVAL, "tdkv_diff_encode: batch too large");
     if (cudaMemsetAsync(d_flags, 0, sizeof(int32_t) * items, s) != cudaSuccess ||

@@ -22,7 +22,24 @@ struct RowsGeom {
     int32_t block_size;
     int32_t nb_max;
     int32_t n_jobs;
+    int32_t job_minor;    // TDKV_ROWS_JOB_MINOR: items ordered (layer, block, tile, job)
 };
+
+// item -> (job, layer, tile-in-layer) for ``per_layer`` tiles per layer
+__device__ __forceinline__ void rows_item(long long it, const RowsGeom& g, long long per_job,
+                                          int per_layer, int& ji, int& layer, int& r2) {
+    long long rem;
+    if (g.job_minor) {
+        const long long lt = it / g.n_jobs;
+        ji = (int)(it - lt * g.n_jobs);
+        rem = lt;
+    } else {
+        ji = (int)(it / per_job);
+        rem = it - (long long)ji * per_job;
+    }
+    layer = (int)(rem / per_layer);
+    r2 = (int)(rem - (long long)layer * per_layer);
+}
 
 template <typename T, int UB>
 __global__ void __launch_bounds__(256, 3)
@@ -48,10 +65,8 @@ __global__ void __launch_bounds__(256, 3)
     if (ty >= rows_per_pass) return;               // no barriers below
 
     for (long long item = blockIdx.x; item < n_items; item += gridDim.x) {
-        const int ji = (int)(item / per_job);
-        const int rem = (int)(item - (long long)ji * per_job);
-        const int layer = rem / g.nb_max;
-        const int b = rem - layer * g.nb_max;
+        int ji, layer, b;
+        rows_item(item, g, per_job, g.nb_max, ji, layer, b);
         const tdkv_rows_job* job = jobs + ji;
         const int T_ = job->num_tokens;
         const int lo = b * g.block_size;
@@ -187,11 +202,8 @@ __global__ void __launch_bounds__(kRowsConsumers + 32)
             int ji = 0, layer = 0, b = 0, lo = 0, n = 0, T_ = 0;
             const tdkv_rows_job* job = nullptr;
             for (; it < n_items; it += gridDim.x) {
-                ji = (int)(it / per_job);
-                const long long rem = it - (long long)ji * per_job;
-                const int per_layer = g.nb_max * tpb;
-                layer = (int)(rem / per_layer);
-                const int r2 = (int)(rem - (long long)layer * per_layer);
+                int r2;
+                rows_item(it, g, per_job, g.nb_max * tpb, ji, layer, r2);
                 b = r2 / tpb;
                 job = jobs + ji;
                 T_ = job->num_tokens;
@@ -371,7 +383,7 @@ extern "C" int32_t tdkv_rows(const tdkv_rows_job* d_jobs, int32_t n_jobs, int32_
     if (dtype != TDKV_F32 && dtype != TDKV_BF16)
         return set_error(TDKV_EUNSUPPORTED, "tdkv_rows: dtype %d", dtype);
     RowsGeom g{num_layers, num_heads * head_dim, head_dim, block_size,
-               ceil_div(max_tokens, block_size), n_jobs};
+               ceil_div(max_tokens, block_size), n_jobs, (flags & TDKV_ROWS_JOB_MINOR) ? 1 : 0};
     // the caller (host wrapper) promises 16-byte aligned planes/strides when
     // rows are whole 16-byte units; pick_unit_bytes encodes the row test
     const int ub = pick_unit_bytes(dtype, head_dim, g.row_elems);

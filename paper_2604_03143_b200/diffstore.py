@@ -30,7 +30,7 @@ import torch
 from . import _kernels, _lib
 from ._device import (default_device, dtype_code, h2d, ptr, stream_handle, to_device,
                       to_host, upload)
-from .core import CacheBlockConfig, LayeredKv
+from .core import CacheBlockConfig, LayeredKv, kv_dense_nbytes
 
 MAGIC = b"TDDF"
 VERSION = 1
@@ -848,8 +848,9 @@ class DiffStore:
             self._next_id += 1
             master = MasterEntry(fid, kv.copy(),
                                  None if tokens is None else tuple(int(t) for t in tokens))
-            self._families[fid] = FamilyEncoding(master, {},
-                                                 CompressionStats(kv.dense_nbytes, [], [], []))
+            L, T, H, D = (int(x) for x in kv.k.shape)
+            self._families[fid] = FamilyEncoding(
+                master, {}, CompressionStats(kv_dense_nbytes(T, L, H, D), [], [], []))
             return master
 
     def encode_family(self, plan, results, tokens: Optional[Sequence[int]] = None) -> FamilyEncoding:
@@ -862,16 +863,28 @@ class DiffStore:
         if not master_kv.on_device:
             diffs = [d.to_host() for d in diffs]
         master = self.register_dense(master_kv, tokens)
-        itemsize = 4 if _plane_dtype(master_kv) == torch.float32 else 2
+        # wire sizes are those of the image serialize_diff emits: the
+        # reference's float32 TDDF for every dtype (diffstore.py:431 measures
+        # len(serialize_diff(d))); wire_nbytes(d) == len(serialize_diff(d))
         mirrors, payload, wire, changed = {}, [], [], []
+        diff_f32 = _plane_dtype(master_kv) == torch.float32
         for (rid, _), diff in zip(items, diffs):
             mirrors[rid] = MirrorHandle(master.family_id, rid, master, diff)
             master.pin_count += 1
-            payload.append(diff.payload_nbytes)
-            wire.append(wire_nbytes(diff, itemsize))
+            # float32 payload bytes (== diff.payload_nbytes for float32 planes)
+            payload.append(diff.payload_nbytes if diff_f32 else
+                           2 * 4 * diff.block_size * diff.num_heads * diff.head_dim
+                           * sum(diff.changed_blocks_per_layer))
+            wire.append(wire_nbytes(diff))
             changed.append(sum(diff.changed_blocks_per_layer))
+        # dense bytes as the reference defines them (float32 K+V, core.py:33-35
+        # and CompressionStats, diffstore.py:349-366), so ratios and
+        # family_cost compare float32 dense with the float32 wire for every
+        # plane dtype -- the figures the reference reports on the f32-upcast
+        # cache
+        L, T, H, D = (int(x) for x in master_kv.k.shape)
         enc = FamilyEncoding(master, mirrors,
-                             CompressionStats(master_kv.dense_nbytes, payload, wire, changed))
+                             CompressionStats(kv_dense_nbytes(T, L, H, D), payload, wire, changed))
         with self._lock:
             self._families[master.family_id] = enc
         return enc

@@ -40,7 +40,7 @@ class UseAfterFreeError(RuntimeError):
 class SlotMap:
     """Slots of one request in token order (paged_pool.py:29-48)."""
 
-    __slots__ = ("request_id", "slots", "serial", "_dev")
+    __slots__ = ("request_id", "slots", "serial", "_dev", "lo", "hi")
 
     def __init__(self, request_id: int, slots, serial: int = -1) -> None:
         arr = np.asarray(slots, dtype=np.int64).reshape(-1)
@@ -50,6 +50,10 @@ class SlotMap:
         self.slots = arr
         self.serial = int(serial)
         self._dev = None
+        # slot range, checked against a pool's capacity before any kernel
+        # writes through the map (numpy's IndexError in the reference)
+        self.lo = int(arr.min()) if arr.size else 0
+        self.hi = int(arr.max()) if arr.size else -1
 
     def __len__(self) -> int:
         return int(self.slots.size)
@@ -242,11 +246,26 @@ class PagedPool:
         else:
             self._written[np.asarray(layers)[:, None], slots[None, :]] = True
 
+    # -- geometry checks before any kernel touches the planes ----------------
+    def check_slots(self, slot_map: SlotMap) -> None:
+        """Every slot of the map addresses a row of this pool (the kernels
+        index the planes by slot without bounds checks)."""
+        if slot_map.lo < 0 or slot_map.hi >= self.capacity:
+            raise IndexError(f"slot map addresses slots [{slot_map.lo}, {slot_map.hi}] outside "
+                             f"a pool of capacity {self.capacity}")
+
+    def check_layer(self, layer: int) -> None:
+        # numpy plane indexing: -L <= layer < L
+        if not -self.num_layers <= int(layer) < self.num_layers:
+            raise IndexError(f"layer {layer} out of range for {self.num_layers} layers")
+
     # -- row movement (K3) --------------------------------------------------
     def write_rows(self, slot_map: SlotMap, layer: int, k_rows, v_rows) -> None:
         slots = slot_map.slots
         if k_rows.shape[0] != slots.size or v_rows.shape[0] != slots.size:
             raise ValueError("row count must match the slot map")
+        self.check_layer(layer)
+        self.check_slots(slot_map)
         n = slots.size
         if n:
             kd = to_device(k_rows, self.device, self.dtype)
@@ -260,10 +279,13 @@ class PagedPool:
                           self.dtype, self.device)
         self._written[layer, slots] = True
 
-    def read_rows(self, slot_map: SlotMap, layer: int, host: bool = False):
-        """Gather one layer's rows for the slot map (device tensors, or numpy
-        copies with host=True)."""
+    def read_rows(self, slot_map: SlotMap, layer: int, host: bool = True):
+        """Gather one layer's rows for the slot map: numpy copies like the
+        reference (paged_pool.py:158-164), or device tensors with host=False
+        (the HBM-resident form, ``read_rows_device``)."""
         slots = slot_map.slots
+        self.check_layer(layer)
+        self.check_slots(slot_map)
         if self.debug and not self._written[layer, slots].all():
             raise UseAfterFreeError(f"layer {layer}: some slots were freed or never written")
         n = slots.size
@@ -278,6 +300,10 @@ class PagedPool:
         if host:
             return to_host(k), to_host(v)
         return k, v
+
+    def read_rows_device(self, slot_map: SlotMap, layer: int):
+        """read_rows with the rows left in HBM (device tensors)."""
+        return self.read_rows(slot_map, layer, host=False)
 
     def check_conservation(self) -> None:
         assert 0 <= self._nfree <= self.capacity

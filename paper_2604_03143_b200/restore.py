@@ -41,6 +41,21 @@ def _check_restore_args(mirror: MirrorHandle, span: PositionSpan, slot_map: Slot
         raise ValueError("slot map must cover one slot per token")
 
 
+def _check_geometry(mirror: MirrorHandle, pool: PagedPool, slot_map: SlotMap) -> None:
+    """The descriptors K3 builds from raw pointers must describe the pool,
+    the master and the diff consistently (numpy raises on any mismatch in
+    the reference, restore.py:68-99); checked before every launch."""
+    kv = mirror.master.kv
+    L, T, H, D = (int(x) for x in kv.k.shape)
+    if (L, H, D) != (pool.num_layers, pool.num_heads, pool.head_dim):
+        raise ValueError(f"master planes (L={L}, H={H}, D={D}) do not match the pool "
+                         f"(L={pool.num_layers}, H={pool.num_heads}, D={pool.head_dim})")
+    diff = mirror.diff
+    if (diff.num_layers, diff.total_tokens, diff.num_heads, diff.head_dim) != (L, T, H, D):
+        raise ValueError("diff does not describe this master")
+    pool.check_slots(slot_map)
+
+
 def _delta_rows(delta: np.ndarray):
     """cos/sin rows for a span: one row if the delta is constant, else one per
     token.  Returns (deltas, stride, rotate)."""
@@ -68,6 +83,7 @@ def fused_restore_many(mirrors: Sequence[MirrorHandle], spans: Sequence[Position
     bs = mirrors[0].diff.block_size
     for mirror, span, smap in zip(mirrors, spans, slot_maps):
         _check_restore_args(mirror, span, smap)
+        _check_geometry(mirror, pool, smap)
         if mirror.diff.block_size != bs:
             raise ValueError("batched restores must share a block size")
         kv = mirror.master.kv
@@ -83,8 +99,11 @@ def fused_restore_many(mirrors: Sequence[MirrorHandle], spans: Sequence[Position
         tbl_row += rows.size
         max_t = max(max_t, T)
     table = _kernels.rope_table(np.concatenate(deltas), D, rope_base, pool.dtype, pool.device)
+    # jobs of one family share the master planes: order the work so each
+    # master tile is fetched from DRAM once for all of them
+    shared = len({(r[0], r[1]) for r in recs}) < len(recs)
     _kernels.rows(_kernels.rows_jobs(recs), max_t, table, L, H, D, bs, pool.dtype, pool.device,
-                  grid_limit)
+                  grid_limit, job_minor=shared)
     for mirror, smap in zip(mirrors, slot_maps):
         pool.mark_written(smap)
         if ledger is not None:
@@ -103,19 +122,48 @@ def _fused_ledger(mirror: MirrorHandle, ledger: CostLedger) -> None:
 def fused_restore(mirror: MirrorHandle, span: PositionSpan, pool: PagedPool, slot_map: SlotMap,
                   rope_base: float, ledger: Optional[CostLedger] = None,
                   trace: Optional[list] = None) -> None:
-    """Load, patch, re-encode and write each layer without a dense mirror."""
+    """Load, patch, re-encode and write each layer without a dense mirror.
+
+    Untraced, all layers go in one K3 launch.  With ``trace`` the restore runs
+    as one K3 launch per layer in layer order (each launch performs that
+    layer's load, swap (the staging ring), diff overlay, rotation and write,
+    restore.py:72-99) and the layer's five events are appended once its
+    launch is enqueued -- the trace reflects the launches that ran."""
     _check_restore_args(mirror, span, slot_map)
-    fused_restore_many([mirror], [span], pool, [slot_map], rope_base, ledger)
-    if trace is not None:
-        for layer in range(mirror.master.kv.num_layers):
-            trace.extend((event, layer) for event in _EVENTS)
+    if trace is None:
+        fused_restore_many([mirror], [span], pool, [slot_map], rope_base, ledger)
+        return
+    _check_geometry(mirror, pool, slot_map)
+    kv = mirror.master.kv
+    L, T, H, D = kv.k.shape
+    diff = mirror.diff
+    bs = diff.block_size
+    nb = (T + bs - 1) // bs
+    mk, mv = _master_planes(mirror, pool)
+    dd = diff.device_form(pool.device, pool.dtype)
+    rows, stride, rotate = _delta_rows(span.delta)
+    table = _kernels.rope_table(rows, D, rope_base, pool.dtype, pool.device)
+    slots = slot_map.device_slots(pool.device)
+    for layer in range(L):
+        job = _kernels.rows_job(mk[layer], mv[layer], 0, pool.k[layer], pool.v[layer], 0, T,
+                                dst_rows=slots, pay_k=dd.pay_k, pay_v=dd.pay_v,
+                                map_k=dd.map_k[layer * nb:], map_v=dd.map_v[layer * nb:],
+                                tbl_row=0, tbl_stride=stride, rotate=rotate)
+        _kernels.rows(_kernels.rows_jobs([job]), T, table, 1, H, D, bs, pool.dtype, pool.device)
+        trace.extend((event, layer) for event in _EVENTS)
+    pool.mark_written(slot_map)
+    if ledger is not None:
+        _fused_ledger(mirror, ledger)
 
 
 def dense_restore(mirror: MirrorHandle, span: PositionSpan, pool: PagedPool, slot_map: SlotMap,
                   rope_base: float, ledger: Optional[CostLedger] = None,
                   trace: Optional[list] = None) -> None:
-    """Baseline: materialize the dense mirror, then rotate and write it."""
+    """Baseline: materialize the dense mirror, then rotate and write it
+    (one K3 launch for the whole cache; with ``trace``, one per layer so the
+    rope/write events follow the launches)."""
     _check_restore_args(mirror, span, slot_map)
+    _check_geometry(mirror, pool, slot_map)
     kv = mirror.master.kv
     diff = mirror.diff
     mk, mv = _master_planes(mirror, pool)
@@ -131,12 +179,18 @@ def dense_restore(mirror: MirrorHandle, span: PositionSpan, pool: PagedPool, slo
     L, T, H, D = dense_k.shape
     rows, stride, rotate = _delta_rows(span.delta)
     table = _kernels.rope_table(rows, D, rope_base, pool.dtype, pool.device)
-    job = _kernels.rows_job(dense_k, dense_v, T * H * D, pool.k, pool.v, pool.layer_stride, T,
-                            dst_rows=slot_map.device_slots(pool.device), tbl_row=0,
-                            tbl_stride=stride, rotate=rotate)
-    _kernels.rows(_kernels.rows_jobs([job]), T, table, L, H, D, _kernels.ROWS_BLOCK, pool.dtype,
-                  pool.device)
-    pool.mark_written(slot_map)
-    if trace is not None:
+    slots = slot_map.device_slots(pool.device)
+    if trace is None:
+        job = _kernels.rows_job(dense_k, dense_v, T * H * D, pool.k, pool.v, pool.layer_stride,
+                                T, dst_rows=slots, tbl_row=0, tbl_stride=stride, rotate=rotate)
+        _kernels.rows(_kernels.rows_jobs([job]), T, table, L, H, D, _kernels.ROWS_BLOCK,
+                      pool.dtype, pool.device)
+    else:
         for layer in range(L):
+            job = _kernels.rows_job(dense_k[layer], dense_v[layer], 0, pool.k[layer],
+                                    pool.v[layer], 0, T, dst_rows=slots, tbl_row=0,
+                                    tbl_stride=stride, rotate=rotate)
+            _kernels.rows(_kernels.rows_jobs([job]), T, table, 1, H, D, _kernels.ROWS_BLOCK,
+                          pool.dtype, pool.device)
             trace.extend([("rope", layer), ("write", layer)])
+    pool.mark_written(slot_map)
