@@ -457,6 +457,17 @@ def run_tdkv(args):
                     if x_ms > 0 else None,
                     "backend": args.dist_backend}
 
+    # the family master exchange (N>1, SURVEY §8e collective 3): every family
+    # (a session) elects its master -- here the session's first agent -- and
+    # the rank holding that agent's cache sends its dense K/V to every other
+    # rank holding members of the family, which then encode their mirrors
+    # against it (dist.encode_family_sharded)
+    if world > 1 and not args.profile and len(batches) == 1:
+        line_family = family_exchange_bench(spec, pool, maps, agents, rank, world, dev, stream,
+                                            barrier, max_over_ranks, args)
+    else:
+        line_family = None
+
     peak, peak_kind = measured_peak_hbm()
     achieved = step_bytes / (k1_ms * 1e-3) / 1e9
     traffic, traffic_src = ncu_traffic("collect_kernel", spec.name)
@@ -489,6 +500,8 @@ def run_tdkv(args):
     }
     if exchange is not None:
         line["exchange"] = exchange
+    if line_family is not None:
+        line["family_exchange"] = line_family
 
     # -- the same rounds replayed from a captured CUDA graph (N=1) -----------
     if world == 1 and len(plans) == 1 and not args.profile:
@@ -618,6 +631,75 @@ def run_tdkv(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def family_exchange_bench(spec, pool, maps, agents, rank, world, dev, stream, barrier,
+                          max_over_ranks, args):
+    """Time the family master exchange of one round: per family (session
+    under strong scaling, the whole round otherwise) the master agent's dense
+    cache -- gathered from its pool slots on the owning rank -- goes
+    point-to-point to every other rank holding family members.  NVLink
+    receive roofline of the busiest rank."""
+    import torch
+    import torch.distributed as dist
+    from paper_2604_03143_b200 import dist as tdist
+    strong = spec.sessions > 1
+    if strong:
+        rank_of = {a: r for r in range(world) for a in rounds_shard(spec, r, world)}
+    else:                         # weak: each rank owns a full config's agents
+        rank_of = {a: r for r in range(world)
+                   for a in range(r * spec.num_agents, (r + 1) * spec.num_agents)}
+    fams = {}
+    for a, r in rank_of.items():
+        fams.setdefault(spec.session_of(a % spec.num_agents) if strong else 0, {})[a] = r
+    local = {a: m for a, m in zip(agents, maps)}
+    T = spec.tokens_per_agent
+    L, H, D = spec.num_layers, spec.num_heads, spec.head_dim
+    plan = []
+    for f, members in sorted(fams.items()):
+        master = min(members)               # elected: synthetic deviations rank by id
+        src, dsts = tdist.family_master_transfers(members, master)
+        if rank == src or rank in dsts:
+            plan.append((master, src, dsts))
+    recv = sum(spec.dense_bytes for _, src, _ in plan if src != rank)   # K+V per family
+    shape = (L, T, H, D)
+
+    def one_round():
+        outs = []
+        for master, src, dsts in plan:
+            if rank == src:
+                sl = local[master].device_slots(dev)
+                planes = (pool.k[:, sl], pool.v[:, sl])       # gather (K3-equivalent copy)
+                outs.append(tdist.exchange_family_master(planes, None, src, dsts, rank))
+            else:
+                like = (torch.empty(shape, dtype=pool.dtype, device=dev),) * 2
+                outs.append(tdist.exchange_family_master(None, like, src, dsts, rank))
+        return outs
+
+    one_round()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        one_round()
+    e1.record(stream)
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
+    busiest = int(max_over_ranks(float(recv)))
+    return {"families": len(fams), "families_touching_this_rank": len(plan),
+            "recv_bytes_max_rank": busiest, "ms": round(ms, 4),
+            "achieved": round(busiest / (ms * 1e-3) / 1e9, 1) if ms > 0 else None,
+            "peak": 900.0, "unit": "GB/s",
+            "frac": round(busiest / (ms * 1e-3) / 1e9 / 900.0, 4) if ms > 0 else None,
+            "backend": args.dist_backend,
+            "note": "master = the family's lowest agent id; its dense K/V (gathered from "
+                    "the pool) sent point-to-point to the ranks holding mirrors "
+                    "(dist.exchange_family_master)"}
+
+
+def rounds_shard(spec, rank, world):
+    from paper_2604_03143_b200 import rounds
+    return rounds.shard(spec.num_agents, rank, world)
 
 
 def selection_bench(tk, spec, pool, maps, dev, args, peak):

@@ -16,11 +16,17 @@ has two exchange steps:
 * ``elect_master`` -- an all-gather of every rank's (deviation, request id)
   pairs so all ranks elect the same family master,
   argmin over (score, id) exactly as collective.select_master
-  (collective.py:117-121).
+  (collective.py:117-121);
+* ``exchange_family_master`` / ``encode_family_sharded`` -- the family
+  master cache (SURVEY §8e collective 3): the elected master's dense K/V
+  planes go point-to-point from the rank holding them to every rank holding
+  another member of the family, and each rank encodes its own mirrors against
+  that one master (DiffStore.encode_family, diffstore.py:411-439: every
+  mirror of a family is a diff against the same elected master).
 """
 from __future__ import annotations
 
-from typing import Dict, Optional
+from typing import Callable, Dict, List, Optional, Sequence, Tuple
 
 import torch
 import torch.distributed as dist
@@ -162,3 +168,90 @@ def elect_master(local_scores: Dict[int, float], group=None,
     dist.all_gather(parts, buf, group=group)
     pairs = [(float(s), int(r)) for part in parts for s, r in part.tolist() if s != float("inf")]
     return min(pairs)[1]
+
+
+# ---------------------------------------------------------------------------
+# family master exchange (SURVEY §8e collective 3)
+
+
+def family_master_transfers(member_rank: Dict[int, int], master_id: int) -> Tuple[int, List[int]]:
+    """(source rank, destination ranks) of one family's master cache: the
+    rank holding the elected master sends it to every other rank holding at
+    least one mirror of the family."""
+    src = member_rank[master_id]
+    dsts = sorted({r for rid, r in member_rank.items() if rid != master_id and r != src})
+    return src, dsts
+
+
+def exchange_family_master(master_planes, like: Optional[Tuple[torch.Tensor, torch.Tensor]],
+                           src: int, dsts: Sequence[int], rank: int, group=None):
+    """Move the family master's dense (L, T, H, D) K and V planes from
+    ``src`` to ``dsts`` (NCCL send/recv between GPUs; gloo stages CUDA
+    tensors through host memory).  ``master_planes`` is (k, v) on ``src``;
+    destinations allocate the receive buffers shaped like ``like`` (one of
+    their local mirrors: a family's members share every dimension).  Returns
+    the (k, v) planes on ``src`` and every destination, None elsewhere.
+    Bytes received per destination: 2 * L*T*H*D * elt."""
+    if rank != src and rank not in dsts:
+        return None
+    staged = dist.get_backend(group) == "gloo"
+    ops, fix = [], []
+    if rank == src:
+        k, v = master_planes
+        k, v = k.contiguous(), v.contiguous()
+        send = (k.cpu(), v.cpu()) if staged and k.is_cuda else (k, v)
+        for d in dsts:
+            for t in send:
+                ops.append(dist.P2POp(dist.isend, t, d, group=group))
+        out = (k, v)
+    else:
+        ref_k, ref_v = like
+        k = torch.empty(ref_k.shape, dtype=ref_k.dtype, device=ref_k.device)
+        v = torch.empty(ref_v.shape, dtype=ref_v.dtype, device=ref_v.device)
+        for t in (k, v):
+            if staged and t.is_cuda:
+                buf = torch.empty(t.shape, dtype=t.dtype)
+                ops.append(dist.P2POp(dist.irecv, buf, src, group=group))
+                fix.append((buf, t))
+            else:
+                ops.append(dist.P2POp(dist.irecv, t, src, group=group))
+        out = (k, v)
+    if ops:
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+        for buf, t in fix:
+            t.copy_(buf)
+    return out
+
+
+def encode_family_sharded(local_kv: Dict[int, object], local_hints: Dict[int, object],
+                          local_scores: Dict[int, float], member_rank: Dict[int, int],
+                          encode: Callable, make_kv: Callable, group=None,
+                          device: Optional[torch.device] = None):
+    """One family spread over ranks, encoded as DiffStore.encode_family does
+    in one process (diffstore.py:411-439): elect the master over every rank's
+    deviation scores (collective.py:117-121), ship the master's dense cache
+    to the ranks holding mirrors, and encode this rank's mirrors (ascending
+    request id) against it.
+
+    ``local_kv``: rid -> LayeredKv of this rank's members; ``member_rank``:
+    rid -> rank for the whole family (known to every rank: the agent
+    sharding is deterministic); ``encode(master_kv, mirrors, hints)`` is the
+    batched encoder (``encode_batch`` on the GPU); ``make_kv(k, v,
+    positions)`` wraps received planes.  Returns (master_id, {rid: diff})
+    for this rank's mirrors."""
+    rank = dist.get_rank(group)
+    master_id = elect_master(local_scores, group=group, device=device)
+    src, dsts = family_master_transfers(member_rank, master_id)
+    mirrors = sorted(rid for rid in local_kv if rid != master_id)
+    if rank == src:
+        mkv = local_kv[master_id]
+        exchange_family_master((mkv.k, mkv.v), None, src, dsts, rank, group)
+    elif mirrors:
+        like = local_kv[mirrors[0]]
+        k, v = exchange_family_master(None, (like.k, like.v), src, dsts, rank, group)
+        mkv = make_kv(k, v, like.positions)
+    if not mirrors:
+        return master_id, {}
+    diffs = encode(mkv, [local_kv[r] for r in mirrors], [local_hints[r] for r in mirrors])
+    return master_id, dict(zip(mirrors, diffs))

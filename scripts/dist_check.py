@@ -9,6 +9,7 @@ Backend: nccl on multi-GPU boxes, gloo when ranks share one GPU.
 import os
 import sys
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -61,6 +62,7 @@ def main():
     assert master == want, (master, want)
     check_sessions(rank, world, dev)
     check_peer(rank, world, dev)
+    check_family(rank, world, dev)
     dist.barrier()
     if rank == 0:
         print(f"dist_check ok: world={world} backend={backend}")
@@ -161,6 +163,49 @@ def check_peer(rank, world, dev):
     want = sum(int(arena.seg_len[s]) for s in range(spec.num_segments) if owners[s] != rank)
     row = spec.num_heads * spec.head_dim * k.element_size()
     assert peer.peer_bytes(plan) == 2 * spec.num_layers * row * want
+    dist.barrier()
+
+
+def check_family(rank, world, dev):
+    """Family master exchange (SURVEY §8e collective 3): 7 bf16 members of
+    one family spread over the ranks; the elected master's dense cache goes
+    from its rank to the ranks holding mirrors, each rank encodes its mirrors
+    with encode_batch (K2), and the union equals a single-process encode of
+    the whole family bit for bit (indices and payload)."""
+    from paper_2604_03143_b200.dist import encode_family_sharded
+    L, T, H, D, bs, n = 3, 300, 4, 128, 32, 7
+    g = torch.Generator(device="cpu").manual_seed(5)
+    base_k = torch.randn((L, T, H, D), generator=g).to(torch.bfloat16)
+    base_v = torch.randn((L, T, H, D), generator=g).to(torch.bfloat16)
+    nb = -(-T // bs)
+    kvs, hints = {}, {}
+    for rid in range(n):
+        k, v = base_k.clone(), base_v.clone()
+        b = (3 * rid) % nb
+        k[:, b * bs:(b + 1) * bs] += 1.0
+        v[:, b * bs:(b + 1) * bs] -= 1.0
+        kvs[rid] = tk.LayeredKv(k.to(dev), v.to(dev), np.arange(T))
+        hints[rid] = np.arange(T)               # every block hinted
+    scores = {rid: float((rid * 5 + 3) % n) for rid in range(n)}
+    member_rank = {rid: (rid * world) // n for rid in range(n)}
+    mine = [rid for rid in range(n) if member_rank[rid] == rank]
+    blocks = tk.CacheBlockConfig(bs)
+    master_id, diffs = encode_family_sharded(
+        {r: kvs[r] for r in mine}, {r: hints[r] for r in mine}, {r: scores[r] for r in mine},
+        member_rank, lambda m, mirs, hs: tk.encode_batch(m, mirs, hs, blocks),
+        lambda k, v, pos: tk.LayeredKv(k, v, pos),
+        device=dev if dist.get_backend() == "nccl" else torch.device("cpu"))
+    assert master_id == min((s, r) for r, s in scores.items())[1]
+    mirrors = [r for r in range(n) if r != master_id]
+    whole = tk.encode_batch(kvs[master_id], [kvs[r] for r in mirrors], [hints[r] for r in mirrors],
+                            blocks)
+    want = dict(zip(mirrors, whole))
+    assert sorted(diffs) == [r for r in mine if r != master_id]
+    for rid, d in diffs.items():
+        w = want[rid]
+        assert [x.indices.tolist() for x in d.layers] == [x.indices.tolist() for x in w.layers]
+        for a, b in zip(d.layers, w.layers):
+            assert torch.equal(a.k_blocks, b.k_blocks) and torch.equal(a.v_blocks, b.v_blocks)
     dist.barrier()
 
 

@@ -515,8 +515,118 @@ def gen_recovery():
     return meta
 
 
+T3_CASES = {
+    # two groups (history lengths 12 / 9) and a singleton remainder (20)
+    "roomy": dict(history=(12, 12, 12, 9, 9, 9, 20), capacity=4096),
+    # the same rounds in a pool too small for the restore verification
+    "tight": dict(history=(12, 12, 12, 9, 9, 9, 20), capacity=470),
+}
+
+
+def gen_t3():
+    """The reference's own T3 rounds (trace._run_t3, trace.py:332-403, via
+    run_trace): the report rows -- ledger counters, compression lists,
+    fidelity, restores verified -- plus every input a replay through another
+    implementation of the hot path needs (the prepared requests of each group
+    and of the remainder, the seeded segment rows, the oracle caches).  The
+    prepared requests are captured by wrapping the reference's own calls;
+    nothing about the control flow is restated here."""
+    import roundkv.trace as trace
+    from roundkv.core import flatten_prompt
+    from roundkv.pic import PicConfig as _Pic
+    from roundkv.trace import SimulationSpec, run_trace
+    meta, arrays = {}, {}
+    for case, cfg in T3_CASES.items():
+        model = ModelConfig(num_layers=3, num_heads=2, head_dim=8, vocab_size=512,
+                            weight_seed=21)
+        wl = WorkloadSpec(num_agents=len(cfg["history"]), num_rounds=2,
+                          history_len=cfg["history"], shared_block_len=6, token_seed=31,
+                          permutation_seed=17)
+        spec = SimulationSpec(model=model, workload=wl, pic=_Pic(0.15, 1),
+                              blocks=CacheBlockConfig(8), pool_capacity_tokens=cfg["capacity"])
+        seen = {"seeds": [], "groups": [], "remainder": []}
+        real_seeds, real_cr, real_rp = trace._round_seeds, trace.collective_recover, \
+            trace.recover_prepared
+
+        def seeds_hook(spec_, weights_, rnd_):
+            out = real_seeds(spec_, weights_, rnd_)
+            seen["seeds"].append((rnd_.round_id, out))
+            return out
+
+        def cr_hook(weights_, group, pic_, ledger_=None):
+            res, plan = real_cr(weights_, group, pic_, ledger_)
+            seen["groups"].append((list(group.members), plan))
+            return res, plan
+
+        def rp_hook(weights_, prep, pic_, ledger_=None):
+            seen["remainder"].append(prep)
+            return real_rp(weights_, prep, pic_, ledger_)
+
+        trace._round_seeds, trace.collective_recover, trace.recover_prepared = \
+            seeds_hook, cr_hook, rp_hook
+        try:
+            report = run_trace(spec, paths=("T3",))
+        finally:
+            trace._round_seeds, trace.collective_recover, trace.recover_prepared = \
+                real_seeds, real_cr, real_rp
+        # seeded segment rows, keyed by the digest the hits resolve to
+        seed_key = {}
+        for rnd_id, seeds in seen["seeds"]:
+            for a, (seg, rows, _ctx) in enumerate(seeds):
+                key = f"{case}_seed_r{rnd_id}_a{a}"
+                seed_key[seg.digest] = key
+                arrays[key + "_k"], arrays[key + "_v"] = rows.k, rows.v
+                arrays[key + "_pos"] = rows.positions
+                arrays[key + "_tokens"] = np.asarray(seg.tokens, np.int64)
+
+        def prep_meta(prep, tag):
+            for name in ("tokens", "positions", "private_idx", "structural_idx",
+                         "label_entry", "label_offset"):
+                arrays[f"{tag}_{name}"] = np.asarray(getattr(prep, name))
+            return {"rid": int(prep.request_id), "tag": tag,
+                    "slots": None if prep.slot_map is None else prep.slot_map.slots.tolist(),
+                    "hits": [{"seed": seed_key[h.entry.digest], "target": h.target_idx.tolist()}
+                             for h in prep.hits]}
+
+        rounds_meta = []
+        gi = ri = 0
+        for row in report["rows"]:
+            rnd = generate_round(wl, model, row["round"])
+            weights = build_weights(model)
+            for a, p in enumerate(rnd.prompts):
+                o = full_prefill(weights, flatten_prompt(p, model.separator_token))
+                arrays[f"{case}_oracle_r{row['round']}_a{a}_k"] = o.k
+                arrays[f"{case}_oracle_r{row['round']}_a{a}_v"] = o.v
+            groups = []
+            for _ in range(row["num_groups"]):
+                members, plan = seen["groups"][gi]
+                groups.append({
+                    "members": [prep_meta(m, f"{case}_g{gi}_r{m.request_id}") for m in members],
+                    "master_id": int(plan.master_id),
+                    "hints": {str(k): v.tolist() for k, v in plan.mirror_diff_hints.items()}})
+                gi += 1
+            remainder = []
+            for _ in range(row["num_remainder"]):
+                prep = seen["remainder"][ri]
+                remainder.append(prep_meta(prep, f"{case}_rem{ri}_r{prep.request_id}"))
+                ri += 1
+            rounds_meta.append({
+                "round": row["round"],
+                "prompts": [[int(p.agent_id), len(flatten_prompt(p, model.separator_token))]
+                            for p in rnd.prompts],
+                "seeds": [f"{case}_seed_r{row['round']}_a{a}"
+                          for a in range(len(rnd.shared_outputs))],
+                "groups": groups, "remainder": remainder, "row": row})
+        meta[case] = {"model": [3, 2, 8, 512, 21], "block_size": 8,
+                      "capacity": cfg["capacity"], "restore_shift": spec.restore_shift,
+                      "fraction": 0.15, "check_layer": 1, "rounds": rounds_meta}
+    np.savez_compressed(os.path.join(HERE, "t3.npz"), **arrays)
+    return meta
+
+
 def main():
     golden = {
+        "t3": gen_t3(),
         "recovery": gen_recovery(),
         "toymodel": gen_toymodel(),
         "generator": "tests/golden/make_golden.py",
@@ -537,13 +647,16 @@ def main():
 
 
 if __name__ == "__main__":
-    if sys.argv[1:] == ["--known-only"]:      # refresh one section in place
+    if sys.argv[1:] in (["--known-only"], ["--t3-only"]):   # refresh one section in place
         path = os.path.join(HERE, "golden.json")
         with open(path) as f:
             golden = json.load(f)
-        golden["known"] = gen_known_answers()
+        if sys.argv[1] == "--known-only":
+            golden["known"] = gen_known_answers()
+        else:
+            golden["t3"] = gen_t3()
         with open(path, "w") as f:
             json.dump(golden, f, indent=1, sort_keys=True)
-        print("updated known answers in", path)
+        print("updated", sys.argv[1][2:], "in", path)
     else:
         main()

@@ -204,3 +204,100 @@ def test_peer_unit_sources_follow_segment_owners():
     assert src.tolist() == owners[seg_of].tolist()
     with pytest.raises(ValueError):
         unit_sources(np.array([int(seg_len.sum())]), seg_row0, seg_len, owners)
+
+
+class _Kv:
+    """A member cache as the exchange sees it: torch planes + positions."""
+
+    def __init__(self, k, v, positions):
+        self.k, self.v, self.positions = k, v, positions
+
+
+def _family_members(n, seed=11, L=2, T=75, H=2, D=8, bs=16):
+    """Master-like base cache; member i re-draws its own blocks (a family
+    whose members differ from each other in a few blocks each)."""
+    rng = np.random.default_rng(seed)
+    base_k = rng.standard_normal((L, T, H, D)).astype(np.float32)
+    base_v = rng.standard_normal((L, T, H, D)).astype(np.float32)
+    nb = -(-T // bs)
+    kvs, changed = {}, {}
+    for rid in range(n):
+        k, v = base_k.copy(), base_v.copy()
+        blocks = sorted(rng.choice(nb, 2, replace=False).tolist())
+        for b in blocks:
+            k[:, b * bs:(b + 1) * bs] = rng.standard_normal(k[:, b * bs:(b + 1) * bs].shape)
+            v[:, b * bs:(b + 1) * bs] = rng.standard_normal(v[:, b * bs:(b + 1) * bs].shape)
+        kvs[rid] = (k, v)
+        changed[rid] = blocks
+    scores = {rid: float(rng.integers(0, 5)) for rid in range(n)}   # ties -> lowest id
+    return kvs, changed, scores, bs
+
+
+def _hints_vs(master_blocks, own_blocks, T, bs):
+    blocks = sorted(set(master_blocks) | set(own_blocks))
+    return np.concatenate([np.arange(b * bs, min(T, b * bs + bs)) for b in blocks])
+
+
+def _family_worker(rank, world, port, n, member_rank, results):
+    from paper_2604_03143_b200.dist import encode_family_sharded
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        kvs, changed, scores, bs = _family_members(n)
+        T = kvs[0][0].shape[1]
+        master_id = ref.select_master(scores)       # hints need it: every member vs the master
+        mine = [rid for rid in range(n) if member_rank[rid] == rank]
+        local_kv = {rid: _Kv(torch.from_numpy(kvs[rid][0]), torch.from_numpy(kvs[rid][1]),
+                             np.arange(T)) for rid in mine}
+        local_hints = {rid: _hints_vs(changed[master_id], changed[rid], T, bs) for rid in mine}
+
+        def encode(m, mirrors, hints):
+            return [ref.encode_diff(m.k.numpy(), m.v.numpy(), x.k.numpy(), x.v.numpy(), h, bs)
+                    for x, h in zip(mirrors, hints)]
+
+        got_master, diffs = encode_family_sharded(
+            local_kv, local_hints, {rid: scores[rid] for rid in mine}, member_rank, encode,
+            lambda k, v, pos: _Kv(k, v, pos))
+        results[rank] = (got_master, {rid: [(d.indices.tolist(), d.k_blocks.tobytes(),
+                                             d.v_blocks.tobytes()) for d in layers]
+                                      for rid, layers in diffs.items()})
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,member_rank", [
+    (2, {0: 0, 1: 0, 2: 1, 3: 1, 4: 1}),           # contiguous shards
+    (3, {0: 2, 1: 0, 2: 1, 3: 2, 4: 0, 5: 1}),     # master off rank 0, scattered members
+])
+def test_family_master_exchange_equals_single_process_encode(world, member_rank):
+    """A family spread over ranks (SURVEY §8e collective 3): every rank
+    elects the same master, receives its dense cache from the rank holding
+    it, and encodes its own mirrors against it; the union of the per-rank
+    diffs equals a single-process encode_family (diffstore.py:411-439) bit
+    for bit."""
+    n = len(member_rank)
+    port = _free_port()
+    with mp.Manager() as manager:
+        results = manager.dict()
+        mp.spawn(_family_worker, args=(world, port, n, member_rank, results), nprocs=world,
+                 join=True)
+        results = dict(results)
+    kvs, changed, scores, bs = _family_members(n)
+    T = kvs[0][0].shape[1]
+    master_id = ref.select_master(scores)
+    assert {results[r][0] for r in range(world)} == {master_id}
+    union = {}
+    for r in range(world):
+        assert not set(union) & set(results[r][1])
+        union.update(results[r][1])
+    assert sorted(union) == [rid for rid in range(n) if rid != master_id]
+    mk, mv = kvs[master_id]
+    for rid, got in union.items():
+        want = ref.encode_diff(mk, mv, kvs[rid][0], kvs[rid][1],
+                               _hints_vs(changed[master_id], changed[rid], T, bs), bs)
+        assert got == [(d.indices.tolist(), d.k_blocks.tobytes(), d.v_blocks.tobytes())
+                       for d in want]
+    src = member_rank[master_id]
+    from paper_2604_03143_b200.dist import family_master_transfers
+    s, dsts = family_master_transfers(member_rank, master_id)
+    assert s == src and src not in dsts
