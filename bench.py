@@ -622,6 +622,9 @@ def run_tdkv(args):
         if args.codec_sweep:
             line["codec_sweep"] = codec_sweep(tk, spec, pool, maps, dev, args, peak)
 
+    if not args.no_codec and not args.profile and rank == 0:
+        line["host_planning"] = planning_bench()
+
     if not args.no_cpu and not args.profile and rank == 0 and world == 1:
         line["cpu_baseline"] = cpu_baseline(spec, args.cpu_seconds)
 
@@ -695,6 +698,72 @@ def family_exchange_bench(spec, pool, maps, agents, rank, world, dev, stream, ba
             "note": "master = the family's lowest agent id; its dense K/V (gathered from "
                     "the pool) sent point-to-point to the ranks holding mirrors "
                     "(dist.exchange_family_master)"}
+
+
+def planning_bench(spec_name: str = "c5", agents: int = 0):
+    """Host planning of one round from the reference's objects (SURVEY §8f
+    #4): the round's PromptLayouts (C5: 1000 agents, each a 512-token private
+    history + 16 shared 256-token outputs) -> native prepare_request of every
+    prompt (tdkv_prepare_batch: flatten, segment-index lookups, labels,
+    structural sets) -> the collector's job arrays -> the collector's unit
+    plan (plan_host_offsets).  Host wall clock, median of 5; the oracle's
+    pure-Python prepare_request restatement is timed on 40 prompts."""
+    from oracle import roundkv_port as ref
+    from paper_2604_03143_b200 import prepare as pp, rounds
+    from paper_2604_03143_b200.collector import pick_tile_rows, plan_host_offsets
+    spec = rounds.CONFIGS[spec_name]
+    if agents:
+        spec = spec.scaled(num_agents=agents)
+    n = spec.num_agents
+    sep = 151643                     # Qwen2.5's <|endoftext|>
+    layouts, index, eseg = rounds.round_layouts(spec, range(n), sep)
+    T = spec.tokens_per_agent
+    base = np.arange(n, dtype=np.int64) * T
+    seg_row0 = np.arange(spec.total_segments, dtype=np.int64) * spec.seg_len
+    seg_len = np.full(spec.total_segments, spec.seg_len, np.int64)
+    tile = pick_tile_rows(spec.row_bytes)
+
+    class _M:
+        separator_token = sep
+
+    def native():
+        t0 = time.perf_counter()
+        preps = pp.prepare_requests(layouts, _M, index)
+        t1 = time.perf_counter()
+        batch = pp.prepare_batch(layouts, sep, index)
+        segs, dst, delta = pp.plan_offsets_from_prepared(batch, eseg, base)
+        t2 = time.perf_counter()
+        plan_host_offsets(seg_row0, seg_len, segs, dst, delta, spec.num_layers, tile)
+        t3 = time.perf_counter()
+        return preps, (t1 - t0, t2 - t1, t3 - t2)
+
+    native()
+    runs = [native()[1] for _ in range(5)]
+    med = [statistics.median(r[i] for r in runs) for i in range(3)]
+    port_index = ref.SegmentIndexPort(1 << 62)
+    for e in index.entries():
+        port_index.insert(e)
+    k = min(40, n)
+    t0 = time.perf_counter()
+    for lay in layouts[:k]:
+        ref.prepare_request_port([(s.kind.value, s.tokens, s.digest) for s in lay.segments],
+                                 sep, port_index.lookup)
+    port_s = (time.perf_counter() - t0) / k
+    total = med[1] + med[2]
+    return {"workload": spec.name, "agents": n, "tokens_per_agent": T,
+            "prepare_requests_ms": round(med[0] * 1e3, 3),
+            "prepare_and_offsets_ms": round(med[1] * 1e3, 3),
+            "unit_plan_ms": round(med[2] * 1e3, 3),
+            "round_planning_ms": round(total * 1e3, 3),
+            "agents_per_s": round(n / total, 1),
+            "oracle_prepare_ms_per_agent": round(port_s * 1e3, 4),
+            "oracle_prepare_round_ms_extrapolated": round(port_s * n * 1e3, 1),
+            "note": "host wall clock, median of 5: prepare_requests = the drop-in "
+                    "PreparedRequest objects of every prompt (one tdkv_prepare_batch "
+                    "call); prepare_and_offsets = the native batch + the collector's job "
+                    "arrays (segment, slot-arena offset, delta) from the hits; unit_plan = "
+                    "plan_host_offsets; oracle = roundkv_port.prepare_request_port (the "
+                    "reference's algorithm in Python) on 40 prompts, 1 core"}
 
 
 def rounds_shard(spec, rank, world):

@@ -421,6 +421,44 @@ int32_t tdkv_segidx_evict(void* handle, int64_t budget_bytes, tdkv_pinned_fn pin
 /* Live entry ids, least recently used first. */
 int32_t tdkv_segidx_entries(void* handle, int64_t* out_ids, int64_t cap, int64_t* n_out);
 
+/* ------------------------------------------------------------------------
+ * Request preparation for a round (host; replaces pic.prepare_request,
+ * pic.py:110-163, with core.flatten_prompt core.py:130-140 and
+ * PromptLayout.segment_starts core.py:120-127).
+ *
+ * The round's prompts index a table of distinct segments: segment s has kind
+ * seg_kind[s] (TDKV_SEG_*), tokens seg_tokens[seg_tok_off[s] ..
+ * seg_tok_off[s+1]) and a 16-byte digest.  Prompt p is the segment ids
+ * prompt_seg[prompt_seg_off[p] .. prompt_seg_off[p+1]) (private history
+ * first, exactly once).  Every SHARED segment is looked up in the segment
+ * index, in prompt order then segment order, refreshing recency like
+ * SegmentIndex.lookup.  Outputs (caller-allocated; flat token count and the
+ * structural capacity follow from the inputs, see paper_2604_03143_b200/
+ * prepare.py): per prompt its flat tokens (one separator between
+ * consecutive segments), label_entry / label_offset (entry id and offset in
+ * the segment for hit positions, -1 elsewhere; entry id = nid_entry[native
+ * id]), its ascending structural positions (separators, misses, task
+ * segments), its private length, and one hit record (prompt segment index,
+ * entry id, target start, length) + native entry id per hit.
+ * threads <= 0 = all hardware threads (capped at 32).
+ * Errors: TDKV_EINVAL with the reference's message for a separator inside a
+ * segment, an empty segment, a negative token, a misplaced private segment.
+ * ---------------------------------------------------------------------- */
+#define TDKV_SEG_PRIVATE 0
+#define TDKV_SEG_SHARED 1
+#define TDKV_SEG_TASK 2
+
+int32_t tdkv_prepare_batch(void* segidx, int32_t n_prompts, const int32_t* prompt_seg_off,
+                           const int32_t* prompt_seg, int32_t n_segs, const int32_t* seg_kind,
+                           const int64_t* seg_tok_off, const int64_t* seg_tokens,
+                           const uint8_t* seg_digest16, int64_t separator,
+                           const int64_t* nid_entry, int64_t n_nid, int64_t* out_tok_off,
+                           int64_t* out_tokens, int64_t* out_label_entry,
+                           int64_t* out_label_offset, int64_t* out_struct_off,
+                           int64_t* out_structural, int64_t* out_private_len,
+                           int64_t* out_hits, int64_t* out_hit_off, int64_t* out_hit_nid,
+                           int32_t threads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -623,3 +623,59 @@ class SegmentIndexPort:
         self.total -= e.nbytes
         if self.on_evict is not None:
             self.on_evict(e)
+
+
+# ---------------------------------------------------------------------------
+# request preparation (pic.py:110-163, core.py:120-140)
+
+
+@dataclass
+class PreparedPort:
+    tokens: np.ndarray
+    private_idx: np.ndarray
+    structural_idx: np.ndarray
+    hits: list                   # [(entry, target_idx)]
+    label_entry: np.ndarray
+    label_offset: np.ndarray
+
+
+def prepare_request_port(segments, separator: int, lookup) -> PreparedPort:
+    """Restates prepare_request (pic.py:110-163) over a list of
+    (kind, tokens, digest) segments: flatten with one separator between
+    consecutive segments (core.py:130-140; a separator inside a segment is a
+    ValueError), the private history is the first segment's range, every
+    SHARED segment is looked up (``lookup(digest)`` -> entry or None, in
+    segment order), a hit labels its positions with (entry.entry_id, offset),
+    a miss or a task segment is structural, and so is the separator before
+    every segment after the first."""
+    for _, toks, _ in segments:
+        if separator in toks:
+            raise ValueError("separator id must not occur inside a segment")
+    flat = []
+    starts = []
+    for i, (_, toks, _) in enumerate(segments):
+        if i:
+            flat.append(int(separator))
+        starts.append(len(flat))
+        flat.extend(int(t) for t in toks)
+    total = len(flat)
+    label_entry = np.full(total, -1, np.int64)
+    label_offset = np.full(total, -1, np.int64)
+    private = np.empty(0, np.int64)
+    structural, hits = [], []
+    for (kind, toks, digest), start in zip(segments, starts):
+        idx = np.arange(start, start + len(toks), dtype=np.int64)
+        if kind == "private_history":
+            private = idx
+            continue
+        entry = lookup(digest) if kind == "shared_output" else None
+        if entry is None:
+            structural.extend(idx.tolist())
+            continue
+        hits.append((entry, idx))
+        label_entry[idx] = entry.entry_id
+        label_offset[idx] = np.arange(len(toks))
+    structural.extend(s - 1 for s in starts[1:])
+    return PreparedPort(np.asarray(flat, np.int64), private,
+                        np.asarray(sorted(structural), np.int64), hits, label_entry,
+                        label_offset)

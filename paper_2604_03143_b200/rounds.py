@@ -342,3 +342,51 @@ def toy_round(weights: ToyWeights, num_agents: int = 8, num_segments: int = 4,
                                   np.asarray([st - 1 for st in starts], np.int64), hits,
                                   label_entry, label_offset))
     return members
+
+
+class _SeedRows:
+    """The cached rows of a segment master as the index sees them (count
+    and source positions; the planes live in the round's master arena)."""
+
+    def __init__(self, positions: np.ndarray) -> None:
+        self.positions = positions
+
+    @property
+    def num_tokens(self) -> int:
+        return int(self.positions.size)
+
+
+class _SeedRef:
+    def __init__(self, kv) -> None:
+        self.kv = kv
+
+
+def round_layouts(spec: RoundSpec, agents, separator: int, seed: int = 7):
+    """The round as the reference's objects: one PromptLayout per agent
+    (private history, then the session's shared outputs in the agent's
+    order -- the layout ``segment_starts`` describes) and a SegmentIndex
+    holding every segment master at its source positions.  Returns
+    (layouts, index, {id(entry): global segment})."""
+    from .prepare import PromptLayout, Segment, SegmentKind
+    from .segment_index import SegmentCacheEntry, SegmentIndex
+    rng = np.random.default_rng(seed)
+    vocab = max(2, separator)
+    shared = [Segment(tuple(rng.integers(0, vocab, spec.seg_len).tolist()),
+                      SegmentKind.SHARED_OUTPUT) for _ in range(spec.total_segments)]
+    index = SegmentIndex(1 << 62)
+    src = source_offsets(spec)
+    entry_segment = {}
+    for g, seg in enumerate(shared):
+        pos = np.arange(src[g], src[g] + spec.seg_len, dtype=np.int64)
+        e = SegmentCacheEntry(seg.digest, pos, _SeedRef(_SeedRows(pos)), b"",
+                              2 * spec.num_layers * spec.seg_len * spec.row_bytes)
+        index.insert(e)
+        entry_segment[id(e)] = g
+    layouts = []
+    for a in agents:
+        hist = Segment(tuple(rng.integers(0, vocab, spec.hist_len).tolist()),
+                       SegmentKind.PRIVATE_HISTORY)
+        base = spec.session_of(a) * spec.num_segments
+        order = agent_order(a, spec.num_segments)
+        layouts.append(PromptLayout(a, (hist,) + tuple(shared[base + s] for s in order)))
+    return layouts, index, entry_segment

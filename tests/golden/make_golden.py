@@ -583,7 +583,18 @@ def gen_t3():
             for name in ("tokens", "positions", "private_idx", "structural_idx",
                          "label_entry", "label_offset"):
                 arrays[f"{tag}_{name}"] = np.asarray(getattr(prep, name))
-            return {"rid": int(prep.request_id), "tag": tag,
+            # the prompt layout itself (for the native prepare_request parity)
+            segs = prep.layout.segments
+            arrays[f"{tag}_layout_kinds"] = np.array([s.kind.value for s in segs])
+            arrays[f"{tag}_layout_lens"] = np.array([len(s) for s in segs], np.int64)
+            arrays[f"{tag}_layout_tokens"] = np.concatenate(
+                [np.asarray(s.tokens, np.int64) for s in segs])
+            ent_key = {}
+            for h in prep.hits:
+                ent_key[int(h.entry.entry_id)] = seed_key[h.entry.digest]
+            arrays[f"{tag}_label_seed"] = np.array(
+                [ent_key.get(int(e), "") for e in prep.label_entry])
+            return {"rid": int(prep.request_id), "tag": tag, "agent": int(prep.layout.agent_id),
                     "slots": None if prep.slot_map is None else prep.slot_map.slots.tolist(),
                     "hits": [{"seed": seed_key[h.entry.digest], "target": h.target_idx.tolist()}
                              for h in prep.hits]}
@@ -624,8 +635,76 @@ def gen_t3():
     return meta
 
 
+def _prepare_world():
+    """A segment index of named entries and prompts exercising every branch
+    of prepare_request (pic.py:110-163): hits, a miss, a task segment, a
+    digest with two entries (the most recent wins), a repeated segment, a
+    private-only prompt.  Shared by gen_prepare and the parity tests (which
+    rebuild the same world from the recorded names and tokens)."""
+    from roundkv.core import PromptLayout, Segment, SegmentKind
+    rng = np.random.default_rng(404)
+    toks = {n: tuple(int(t) for t in rng.integers(1, 500, ln))
+            for n, ln in (("A", 5), ("B", 3), ("C", 4), ("M", 6), ("T", 3), ("P0", 6),
+                          ("P1", 2), ("P2", 9))}
+    segs = {n: Segment(toks[n], SegmentKind.PRIVATE_HISTORY if n.startswith("P") else
+                       SegmentKind.ROUND_TASK if n == "T" else SegmentKind.SHARED_OUTPUT)
+            for n in toks}
+    # entries: name -> (segment, first source position); A2 re-caches A later
+    entries = [("A1", "A", 10), ("B", "B", 0), ("C", "C", 40), ("A2", "A", 3)]
+    prompts = [["P0", "A", "T", "M", "B"], ["P1", "B", "A", "C", "A"], ["P2"]]
+    return toks, segs, entries, prompts
+
+
+def gen_prepare():
+    """The reference's prepare_request on _prepare_world's prompts, plus the
+    index's recency order afterwards and the entries an over-budget insert
+    then evicts (lookups refresh recency in prompt/segment order)."""
+    from roundkv.core import PromptLayout
+    toks, segs, entries, prompts = _prepare_world()
+    model = ModelConfig(num_layers=1, num_heads=1, head_dim=2, vocab_size=512)
+    index = SegmentIndex(budget_bytes=10_000)
+    name_of = {}
+    for name, seg, src in entries:
+        n = len(toks[seg])
+        kv = LayeredKv(np.zeros((1, n, 1, 2), np.float32), np.zeros((1, n, 1, 2), np.float32),
+                       np.arange(src, src + n))
+        e = SegmentCacheEntry(segs[seg].digest, kv.positions, SimpleNamespace(kv=kv), b"ctx",
+                              1000)
+        index.insert(e)
+        name_of[e.entry_id] = name
+    out = {"prompts": prompts, "tokens": {n: list(t) for n, t in toks.items()},
+           "entries": [list(e) for e in entries], "separator": model.separator_token,
+           "requests": []}
+    for i, names in enumerate(prompts):
+        lay = PromptLayout(i, tuple(segs[n] for n in names))
+        prep = prepare_request(lay, model, index, request_id=i)
+        out["requests"].append({
+            "tokens": prep.tokens.tolist(), "private_idx": prep.private_idx.tolist(),
+            "structural_idx": prep.structural_idx.tolist(),
+            "label_entry": [name_of.get(int(e), None) for e in prep.label_entry],
+            "label_offset": prep.label_offset.tolist(),
+            "hits": [[name_of[h.entry.entry_id], h.target_idx.tolist(), h.delta.tolist()]
+                     for h in prep.hits]})
+    out["recency"] = [name_of[e.entry_id] for e in index.entries()]
+    evicted = []
+    index._on_evict = lambda e: evicted.append(name_of[e.entry_id])
+    n = len(toks["A"])
+    kv = LayeredKv(np.zeros((1, n, 1, 2), np.float32), np.zeros((1, n, 1, 2), np.float32),
+                   np.arange(n))
+    index.insert(SegmentCacheEntry(b"x" * 16, kv.positions, SimpleNamespace(kv=kv), b"ctx", 7000))
+    out["evicted_after_insert"] = evicted
+    # errors
+    bad = PromptLayout(9, (segs["P0"], segs["A"]))
+    try:
+        prepare_request(bad, ModelConfig(vocab_size=toks["A"][0] + 1), index)
+    except ValueError as e:
+        out["separator_error"] = str(e)
+    return out
+
+
 def main():
     golden = {
+        "prepare": gen_prepare(),
         "t3": gen_t3(),
         "recovery": gen_recovery(),
         "toymodel": gen_toymodel(),
@@ -647,12 +726,14 @@ def main():
 
 
 if __name__ == "__main__":
-    if sys.argv[1:] in (["--known-only"], ["--t3-only"]):   # refresh one section in place
+    if sys.argv[1:] in (["--known-only"], ["--t3-only"], ["--prepare-only"]):  # one section
         path = os.path.join(HERE, "golden.json")
         with open(path) as f:
             golden = json.load(f)
         if sys.argv[1] == "--known-only":
             golden["known"] = gen_known_answers()
+        elif sys.argv[1] == "--prepare-only":
+            golden["prepare"] = gen_prepare()
         else:
             golden["t3"] = gen_t3()
         with open(path, "w") as f:
