@@ -990,7 +990,10 @@ def codec_bench(tk, spec, pool, maps, dev, args, peak, frac=None, hint_all=False
     T = spec.tokens_per_agent
     nb = -(-T // bs)
     frac = args.mirror_frac if frac is None else frac
-    n_mirrors = max(1, min(len(maps) - 1, args.codec_mirrors))
+    # a family is one session (trace.py:365-386: one family per group): at
+    # C3 the master and the other 24 agents of its session
+    per_family = spec.agents_per_session if spec.sessions > 1 else len(maps)
+    n_mirrors = max(1, min(len(maps) - 1, per_family - 1, args.codec_mirrors))
     sl0 = maps[0].device_slots(dev)
     mk = pool.k[:, sl0].contiguous()
     mv = pool.v[:, sl0].contiguous()

@@ -96,7 +96,7 @@ assert DIFF_PAIR.itemsize == 32 and DIFF_OUT.itemsize == 40 and ROWS_JOB.itemsiz
 
 EXPORTS = (
     "tdkv_version", "tdkv_last_error", "tdkv_launch_count", "tdkv_rope_table",
-    "tdkv_collect", "tdkv_collect_sources", "tdkv_diff_compare", "tdkv_diff_compact", "tdkv_diff_encode", "tdkv_rows",
+    "tdkv_collect", "tdkv_collect_round", "tdkv_collect_sources", "tdkv_diff_compare", "tdkv_diff_compact", "tdkv_diff_encode", "tdkv_rows",
     "tdkv_keydiff", "tdkv_select_important", "tdkv_gemm", "tdkv_qkv_rope", "tdkv_attention",
     "tdkv_attention_many",
     "tdkv_fill_rows", "tdkv_alloc_create", "tdkv_alloc_destroy", "tdkv_alloc_free_count",
@@ -116,6 +116,8 @@ _SIGS = {
     "tdkv_rope_table": (_I32, [_P, _I64, _P, _I32, _I32, _P, _P]),
     "tdkv_collect": (_I32, [_P, _P, _I64, _P, _I32, _I32, _P, _P, _P, _I32, _P, _P, _I64,
                             _I32, _I32, _I32, _I32, _I32, _P]),
+    "tdkv_collect_round": (_I32, [_P, _I64, _P, _P, _P, _P, _I64, _P, _I32, _I32, _P, _P, _P,
+                                  _P, _I64, _I32, _I32, _I32, _I32, _I32, _P]),
     "tdkv_collect_sources": (_I32, [_P, _P, _I32, _P, _I64, _P, _I32, _I32, _P, _P, _P, _I32,
                                     _P, _P, _I64, _I32, _I32, _I32, _I32, _I32, _P]),
     "tdkv_diff_compare": (_I32, [_P, _I32, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32,
@@ -199,8 +201,19 @@ def raise_last(name: str, rc: int = -1) -> None:
 PINNED_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64)
 
 
+_graph_launches = [0]
+
+
+def note_launches(n: int) -> None:
+    """Count kernels launched by a CUDA graph replay (their launches bypass
+    the library's own counter)."""
+    _graph_launches[0] += int(n)
+
+
 def launch_count() -> int:
-    return int(load().tdkv_launch_count())
+    """tdkv kernels launched by this process: the library's counter plus the
+    kernels of replayed graphs."""
+    return int(load().tdkv_launch_count()) + _graph_launches[0]
 
 
 def version() -> int:

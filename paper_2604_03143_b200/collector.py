@@ -37,6 +37,9 @@ _TILE_SMEM = int(os.environ.get("TDKV_TILE_SMEM", 32 * 1024))
 _SMS = 148
 
 
+_AUTO_GRAPH = os.environ.get("TDKV_ROUND_GRAPHS", "1") != "0"
+
+
 def pick_tile_rows(row_bytes: int, budget: int = _TILE_SMEM) -> int:
     rows = max(1, budget // (4 * row_bytes))
     p = 1
@@ -406,11 +409,12 @@ class CollectPlan:
 
     def launch(self, arena: MasterArena, dst_k: torch.Tensor, dst_v: Optional[torch.Tensor],
                dst_layer_stride: int, grid_limit: int = 0) -> int:
-        """K0 + K1 over every layer; returns the kernels launched.  The
-        argument lists of both launches are built once per (arena,
-        destination, stream) and kept as ctypes values, so a replayed round
-        costs two foreign calls (small rounds are launch-bound: C1 moves
-        75 MB in ~20 us)."""
+        """K0 + K1 over every layer in one foreign call (tdkv_collect_round:
+        both kernels launched with programmatic dependent launch, so K1's
+        launch and first tile loads overlap K0); returns the kernels
+        launched.  The argument list is built once per (arena, destination,
+        stream) and kept as ctypes values (small rounds are launch-bound: C1
+        moves 75 MB in ~12 us of DRAM time)."""
         if self.num_jobs == 0:
             return 0
         stream = stream_handle(self.device)
@@ -423,36 +427,29 @@ class CollectPlan:
                 raise ValueError("arena, destination and plan dtypes differ")
             lib = _lib.load()
             C = ctypes
-            k0 = None
-            if self.rotate:
-                inv = _kernels.inv_freq_device(self.device, self.head_dim, self.rope_base)
-                k0 = (C.c_void_p(ptr(self.d_deltas)), C.c_int64(int(self.d_deltas.numel())),
-                      C.c_void_p(ptr(inv)), C.c_int32(self.head_dim // 2),
-                      C.c_int32(dtype_code(self.kv_dtype)), C.c_void_p(ptr(self.table)), stream)
+            n_tbl = int(self.d_deltas.numel()) if self.rotate else 0
+            inv = (_kernels.inv_freq_device(self.device, self.head_dim, self.rope_base)
+                   if self.rotate else None)
             with_v = dst_v is not None
-            k1 = (C.c_void_p(ptr(arena.k)), C.c_void_p(ptr(arena.v) if with_v else 0),
-                  C.c_int64(arena.layer_stride), C.c_void_p(ptr(self.d_units)),
-                  C.c_int32(int(self.units_host.size)), C.c_int32(self.tile_rows),
-                  C.c_void_p(ptr(self.d_jobs)), C.c_void_p(ptr(self.d_dst_rows)),
-                  C.c_void_p(ptr(self.table) if self.rotate else 0), C.c_int32(int(self.rotate)),
-                  C.c_void_p(ptr(dst_k)), C.c_void_p(ptr(dst_v) if with_v else 0),
-                  C.c_int64(int(dst_layer_stride)), C.c_int32(self.num_layers),
-                  C.c_int32(self.num_heads), C.c_int32(self.head_dim),
-                  C.c_int32(dtype_code(self.kv_dtype)), C.c_int32(int(grid_limit)), stream)
+            args = (C.c_void_p(ptr(self.d_deltas) if n_tbl else 0), C.c_int64(n_tbl),
+                    C.c_void_p(ptr(inv) if n_tbl else 0), C.c_void_p(ptr(self.table)),
+                    C.c_void_p(ptr(arena.k)), C.c_void_p(ptr(arena.v) if with_v else 0),
+                    C.c_int64(arena.layer_stride), C.c_void_p(ptr(self.d_units)),
+                    C.c_int32(int(self.units_host.size)), C.c_int32(self.tile_rows),
+                    C.c_void_p(ptr(self.d_jobs)), C.c_void_p(ptr(self.d_dst_rows)),
+                    C.c_void_p(ptr(dst_k)), C.c_void_p(ptr(dst_v) if with_v else 0),
+                    C.c_int64(int(dst_layer_stride)), C.c_int32(self.num_layers),
+                    C.c_int32(self.num_heads), C.c_int32(self.head_dim),
+                    C.c_int32(dtype_code(self.kv_dtype)), C.c_int32(int(grid_limit)), stream)
             if len(self._fast) >= 16:
                 self._fast.clear()
             # keep the tensors whose addresses are baked in alive with the entry
-            fast = self._fast[key] = (lib.tdkv_rope_table, k0, lib.tdkv_collect, k1,
-                                      (arena.k, arena.v, dst_k, dst_v))
-        f0, k0, f1, k1, _ = fast
-        n = 0
-        if k0 is not None:
-            if f0(*k0):
-                _lib.raise_last("tdkv_rope_table")
-            n += 1
-        if f1(*k1):
-            _lib.raise_last("tdkv_collect")
-        return n + 1
+            fast = self._fast[key] = (lib.tdkv_collect_round, args, 2 if n_tbl else 1,
+                                      (arena.k, arena.v, dst_k, dst_v, inv))
+        fn, args, kernels, _ = fast
+        if fn(*args):
+            _lib.raise_last("tdkv_collect_round")
+        return kernels
 
 
 class KVCollector:
@@ -469,6 +466,11 @@ class KVCollector:
         self.pool = pool
         self.rope_base = float(rope_base)
         self.tile_rows = tile_rows
+        # a plan collected twice in a row is captured as a CUDA graph and
+        # replayed from then on (TDKV_ROUND_GRAPHS=0 disables)
+        self.auto_graph = _AUTO_GRAPH
+        self._last = None            # (plan, grid_limit, stream) of the previous collect
+        self._graph = None           # (key, RoundGraph)
 
     def plan(self, jobs: Sequence[CollectJob]) -> CollectPlan:
         return CollectPlan(self.arena, jobs, self.rope_base, self.tile_rows, self.pool.device)
@@ -499,8 +501,24 @@ class KVCollector:
 
     def collect(self, plan: CollectPlan, ledger: Optional[CostLedger] = None,
                 grid_limit: int = 0) -> int:
-        n = plan.launch(self.arena, self.pool.k, self.pool.v, self.pool.layer_stride,
-                        grid_limit)
+        """Run the round (K0 + K1).  A plan collected again right after itself
+        (a replayed round) is captured once as a CUDA graph (RoundGraph) and
+        replayed: one graph launch per round instead of the launch path."""
+        stream = torch.cuda.current_stream(self.pool.device)
+        key = (id(plan), int(grid_limit), stream.cuda_stream)
+        g = self._graph
+        if g is not None and g[0] == key and g[1].plan is plan:
+            n = g[1].replay()
+        elif (self.auto_graph and plan.num_jobs and self._last is not None
+              and self._last[0] is plan and self._last[1:] == key[1:]
+              and not torch.cuda.is_current_stream_capturing()):
+            graph = RoundGraph(self, plan, grid_limit)   # runs the round once, then captures
+            self._graph = (key, graph)
+            n = graph.kernels
+        else:
+            n = plan.launch(self.arena, self.pool.k, self.pool.v, self.pool.layer_stride,
+                            grid_limit)
+        self._last = (plan,) + key[1:]
         if ledger is not None and plan.num_jobs:
             for layer in range(plan.num_layers):
                 ledger.record_rope_call(layer)
@@ -558,22 +576,29 @@ class RoundGraph:
     graph launch instead of the per-kernel launch path; for small rounds
     (C1: two kernels, 38 us) the launch overhead is a visible share."""
 
-    def __init__(self, collector: "KVCollector", plan: CollectPlan) -> None:
+    def __init__(self, collector: "KVCollector", plan: CollectPlan, grid_limit: int = 0) -> None:
         self.collector = collector
         self.plan = plan                 # keeps the descriptor buffers alive
         device = collector.pool.device
+        pool = collector.pool
+
+        def run():
+            return plan.launch(collector.arena, pool.k, pool.v, pool.layer_stride, grid_limit)
+
         side = torch.cuda.Stream(device)
         side.wait_stream(torch.cuda.current_stream(device))
         with torch.cuda.stream(side):    # first launches outside capture (attributes set)
-            collector.collect(plan)
+            run()
         torch.cuda.current_stream(device).wait_stream(side)
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
-            self.kernels = collector.collect(plan)
+            self.kernels = run()
 
     def replay(self) -> int:
-        """Run the captured round; returns the kernels it launches."""
+        """Run the captured round; returns the kernels it launches (they are
+        added to tdkv's launch counter)."""
         self.graph.replay()
+        _lib.note_launches(self.kernels)
         return self.kernels
 
 

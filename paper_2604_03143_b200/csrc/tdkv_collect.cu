@@ -21,6 +21,11 @@ __global__ void rope_table_kernel(const int64_t* __restrict__ deltas, int64_t n_
                                   const double* __restrict__ inv_freq, int half,
                                   Tbl* __restrict__ out) {
     const int64_t total = n_rows * half;
+    // under PDL (tdkv_collect_round): the previous round's K1 may still read
+    // the table -- wait for every predecessor, then let this round's K1 start
+    // launching (its master-tile prefetch overlaps this kernel)
+    griddep_wait();
+    griddep_launch_dependents();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t r = i / half;
@@ -176,6 +181,11 @@ __global__ void __launch_bounds__(256) collect_kernel(const CollectParams p) {
         }
     }
 
+    // PDL (tdkv_collect_round): everything above reads plan state and the
+    // master arena only; the cos/sin table comes from the K0 launched just
+    // before, and no pool row may be written before the predecessors finish
+    griddep_wait();
+
     for (int iter = 0; item < n_items; item += gridDim.x, ++iter) {
         const int b = iter & 1;
         uint8_t* buf = smem + (size_t)b * 2 * tile_bytes;
@@ -292,7 +302,7 @@ __global__ void __launch_bounds__(256) collect_kernel(const CollectParams p) {
 }
 
 template <typename T, int UB, bool BULK>
-static int32_t launch_collect(const CollectParams& p, int grid_limit, cudaStream_t s) {
+static int32_t launch_collect(const CollectParams& p, int grid_limit, cudaStream_t s, bool pdl) {
     auto kern = collect_kernel<T, UB, BULK>;
     const int threads = 256;
     const size_t smem = (size_t)4 * p.max_rows * p.row_elems * sizeof(T);
@@ -309,7 +319,8 @@ static int32_t launch_collect(const CollectParams& p, int grid_limit, cudaStream
     int grid = sm_count() * per_sm;
     if (grid_limit > 0 && grid > grid_limit) grid = grid_limit;
     if (grid > items) grid = items;
-    kern<<<grid, threads, smem, s>>>(p);
+    if (launch_maybe_pdl(kern, dim3(grid), dim3(threads), smem, s, pdl, p) != cudaSuccess)
+        return check_launch("tdkv_collect: launch");
     count_launch();
     return check_launch("tdkv_collect");
 }
@@ -318,9 +329,20 @@ static int32_t launch_collect(const CollectParams& p, int grid_limit, cudaStream
 
 using namespace tdkv;
 
+static int32_t rope_table_impl(const int64_t* d_deltas, int64_t n_rows, const double* d_inv_freq,
+                               int32_t half_dim, int32_t table_dtype, void* d_table, void* stream,
+                               bool pdl);
+
 extern "C" int32_t tdkv_rope_table(const int64_t* d_deltas, int64_t n_rows,
                                    const double* d_inv_freq, int32_t half_dim,
                                    int32_t table_dtype, void* d_table, void* stream) {
+    return rope_table_impl(d_deltas, n_rows, d_inv_freq, half_dim, table_dtype, d_table, stream,
+                           false);
+}
+
+static int32_t rope_table_impl(const int64_t* d_deltas, int64_t n_rows, const double* d_inv_freq,
+                               int32_t half_dim, int32_t table_dtype, void* d_table, void* stream,
+                               bool pdl) {
     if (n_rows < 0 || half_dim <= 0) return set_error(TDKV_EINVAL, "tdkv_rope_table: bad sizes");
     if (n_rows == 0) return TDKV_OK;
     if (!d_deltas || !d_inv_freq || !d_table)
@@ -329,15 +351,19 @@ extern "C" int32_t tdkv_rope_table(const int64_t* d_deltas, int64_t n_rows,
     const int64_t total = n_rows * half_dim;
     int grid = (int)((total + 255) / 256);
     if (grid > sm_count() * 8) grid = sm_count() * 8;
+    cudaError_t e;
     if (table_dtype == TDKV_F32) {
-        rope_table_kernel<double2><<<grid, 256, 0, s>>>(d_deltas, n_rows, d_inv_freq, half_dim,
-                                                        static_cast<double2*>(d_table));
+        e = launch_maybe_pdl(rope_table_kernel<double2>, dim3(grid), dim3(256), 0, s, pdl,
+                             d_deltas, n_rows, d_inv_freq, (int)half_dim,
+                             static_cast<double2*>(d_table));
     } else if (table_dtype == TDKV_BF16) {
-        rope_table_kernel<float2><<<grid, 256, 0, s>>>(d_deltas, n_rows, d_inv_freq, half_dim,
-                                                       static_cast<float2*>(d_table));
+        e = launch_maybe_pdl(rope_table_kernel<float2>, dim3(grid), dim3(256), 0, s, pdl,
+                             d_deltas, n_rows, d_inv_freq, (int)half_dim,
+                             static_cast<float2*>(d_table));
     } else {
         return set_error(TDKV_EUNSUPPORTED, "tdkv_rope_table: dtype %d", table_dtype);
     }
+    if (e != cudaSuccess) return check_launch("tdkv_rope_table: launch");
     count_launch();
     return check_launch("tdkv_rope_table");
 }
@@ -350,7 +376,7 @@ static int32_t collect_impl(const void* d_master_k, const void* d_master_v,
                             int32_t num_layers, int32_t num_heads, int32_t head_dim,
                             int32_t dtype, int32_t grid_limit, void* stream,
                             const uint8_t* d_unit_src, const void* const* h_src_k,
-                            const void* const* h_src_v, int32_t n_src) {
+                            const void* const* h_src_v, int32_t n_src, bool pdl = false) {
     if (n_units < 0 || num_layers <= 0 || num_heads <= 0 || head_dim <= 0 || (head_dim & 1))
         return set_error(TDKV_EINVAL, "tdkv_collect: bad geometry L=%d H=%d D=%d", num_layers,
                          num_heads, head_dim);
@@ -406,16 +432,16 @@ static int32_t collect_impl(const void* d_master_k, const void* d_master_v,
 
     if (dtype == TDKV_F32) {
         if (ub == 16)
-            return bulk ? launch_collect<float, 16, true>(p, grid_limit, s)
-                        : launch_collect<float, 16, false>(p, grid_limit, s);
-        return bulk ? launch_collect<float, 8, true>(p, grid_limit, s)
-                    : launch_collect<float, 8, false>(p, grid_limit, s);
+            return bulk ? launch_collect<float, 16, true>(p, grid_limit, s, pdl)
+                        : launch_collect<float, 16, false>(p, grid_limit, s, pdl);
+        return bulk ? launch_collect<float, 8, true>(p, grid_limit, s, pdl)
+                    : launch_collect<float, 8, false>(p, grid_limit, s, pdl);
     }
     if (ub == 16)
-        return bulk ? launch_collect<__nv_bfloat16, 16, true>(p, grid_limit, s)
-                    : launch_collect<__nv_bfloat16, 16, false>(p, grid_limit, s);
-    return bulk ? launch_collect<__nv_bfloat16, 4, true>(p, grid_limit, s)
-                : launch_collect<__nv_bfloat16, 4, false>(p, grid_limit, s);
+        return bulk ? launch_collect<__nv_bfloat16, 16, true>(p, grid_limit, s, pdl)
+                    : launch_collect<__nv_bfloat16, 16, false>(p, grid_limit, s, pdl);
+    return bulk ? launch_collect<__nv_bfloat16, 4, true>(p, grid_limit, s, pdl)
+                : launch_collect<__nv_bfloat16, 4, false>(p, grid_limit, s, pdl);
 }
 
 extern "C" int32_t tdkv_collect(const void* d_master_k, const void* d_master_v,
@@ -429,6 +455,37 @@ extern "C" int32_t tdkv_collect(const void* d_master_k, const void* d_master_v,
                         d_jobs, d_dst_rows, d_table, rotate, d_dst_k, d_dst_v, dst_layer_stride,
                         num_layers, num_heads, head_dim, dtype, grid_limit, stream, nullptr,
                         nullptr, nullptr, 0);
+}
+
+// One round in one call: K0 (this round's cos/sin rows) and K1, both
+// launched with programmatic dependent launch -- K0 waits for the previous
+// round (its table is being overwritten) and then releases K1, whose launch,
+// barrier setup and first master-tile TMA loads overlap K0; K1 waits for K0
+// only before it rotates or writes.  TDKV_PDL=0 launches them plainly.
+extern "C" int32_t tdkv_collect_round(const int64_t* d_deltas, int64_t n_table_rows,
+                                      const double* d_inv_freq, void* d_table,
+                                      const void* d_master_k, const void* d_master_v,
+                                      int64_t master_layer_stride,
+                                      const tdkv_collect_unit* d_units, int32_t n_units,
+                                      int32_t max_rows, const tdkv_collect_job* d_jobs,
+                                      const int64_t* d_dst_rows, void* d_dst_k, void* d_dst_v,
+                                      int64_t dst_layer_stride, int32_t num_layers,
+                                      int32_t num_heads, int32_t head_dim, int32_t dtype,
+                                      int32_t grid_limit, void* stream) {
+    static const bool pdl = [] {
+        const char* e = getenv("TDKV_PDL");
+        return !(e && e[0] == '0');
+    }();
+    const bool rotate = n_table_rows > 0;
+    if (rotate) {
+        const int32_t rc = rope_table_impl(d_deltas, n_table_rows, d_inv_freq, head_dim / 2, dtype,
+                                           d_table, stream, pdl);
+        if (rc) return rc;
+    }
+    return collect_impl(d_master_k, d_master_v, master_layer_stride, d_units, n_units, max_rows,
+                        d_jobs, d_dst_rows, rotate ? d_table : nullptr, rotate ? 1 : 0, d_dst_k,
+                        d_dst_v, dst_layer_stride, num_layers, num_heads, head_dim, dtype,
+                        grid_limit, stream, nullptr, nullptr, nullptr, 0, pdl && rotate);
 }
 
 extern "C" int32_t tdkv_collect_sources(const void* const* h_src_k, const void* const* h_src_v,
