@@ -593,6 +593,7 @@ class RoundGraph:
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
             self.kernels = run()
+        _lib.note_launches(-self.kernels)     # captured, not run: counted at each replay
 
     def replay(self) -> int:
         """Run the captured round; returns the kernels it launches (they are

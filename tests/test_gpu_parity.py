@@ -630,3 +630,49 @@ def test_round_graph_replay_equals_eager_collect():
         assert graph.replay() == 2
         torch.cuda.synchronize()
         assert torch.equal(pa.k, pb.k) and torch.equal(pa.v, pb.v), step
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_replayed_plan_auto_graph_and_pdl(dtype):
+    """KVCollector.collect of the same plan again is captured as a CUDA graph
+    (K0 + K1 of tdkv_collect_round, programmatic dependent launch) and
+    replayed; every replay reads the arena as it is then -- bit-identical to
+    plain per-round launches (auto_graph off) -- and the replays are counted
+    as tdkv launches."""
+    base = rounds.CONFIGS["c1"] if dtype == "f32" else rounds.CONFIGS["c2"]
+    spec = base.scaled(num_layers=3, num_agents=6, num_segments=4, hist_len=21)
+    mk, mv = rounds.master_planes_host(spec)
+    dt = spec.torch_dtype
+    arena = rounds.make_arena(spec, torch.from_numpy(mk).to(DEV).to(dt),
+                              torch.from_numpy(mv).to(DEV).to(dt))
+    T = spec.tokens_per_agent
+    runs = []
+    for auto in (True, False):
+        pool = tk.PagedPool(spec.num_agents * T, spec.num_layers, spec.num_heads, spec.head_dim,
+                            dtype=dt, device=DEV)
+        maps = [pool.allocate(T, a) for a in range(spec.num_agents)]
+        col = tk.KVCollector(arena, pool)
+        col.auto_graph = auto
+        plan = col.plan([j for a, m in enumerate(maps) for j in rounds.agent_jobs(spec, a, m.slots)])
+        runs.append((pool, col, plan, maps))
+    for step in range(5):
+        arena.k.mul_(-1) if step % 2 else arena.v.add_(1)     # new master contents every round
+        outs = []
+        for pool, col, plan, _ in runs:
+            before = tk.launch_count()
+            assert col.collect(plan) == 2
+            assert tk.launch_count() - before == 2
+            torch.cuda.synchronize()
+            outs.append((pool.k.clone(), pool.v.clone()))
+        assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1]), step
+    assert runs[0][1]._graph is not None and runs[1][1]._graph is None
+    # and the graph-replayed pool still equals the oracle (f32: 1e-5)
+    if dtype == "f32":
+        pool, col, plan, maps = runs[0]
+        gk = pool.k.cpu().numpy()
+        ak = arena.k.cpu().numpy()
+        for a, m in enumerate(maps):
+            for j in rounds.agent_jobs(spec, a, m.slots):
+                r0 = j.segment * spec.seg_len
+                want = ref.rope_apply(ak[1, r0:r0 + spec.seg_len], j.delta)
+                assert np.abs(gk[1, j.dst_rows] - want).max() <= F32_TOL
