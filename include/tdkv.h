@@ -331,7 +331,10 @@ int32_t tdkv_attention(const float* d_q, const float* d_k_fresh, const float* d_
  * total), each CTA serving one tile of one member with every staged
  * key/value tile.  rows_per_tile 8 (head_dim <= 128): two-pass softmax over a
  * stored score row; rows_per_tile 16 (head_dim <= 128): online softmax
- * (running max / sum, float64 accumulators rescaled per 32-token tile).
+ * (running max / sum, float64 accumulators rescaled per 32-token tile);
+ * rows_per_tile 64 (head_dim 8, 16, 32, 64 or 128): register-blocked, 256
+ * threads per CTA, 64-token key/value tiles double-buffered by 16-byte async
+ * copies, 4x4 score blocks, float32 P.V sums per tile folded into float64.
  * n_tiles == 0 runs one CTA per row. */
 typedef struct {
     const float* ctx_k;          /* (L, num_tokens, H*D) context planes */

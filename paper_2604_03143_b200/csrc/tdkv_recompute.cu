@@ -443,6 +443,243 @@ __global__ void __launch_bounds__(128)
     }
 }
 
+// Register-blocked attention (rows_per_tile 64): one CTA serves 64 fixed
+// rows of one member and one head with 256 threads, staging 64-token key and
+// value tiles (double-buffered 16-byte async copies, fresh rows overriding
+// cached ones).  Scores: thread (tq, tk) owns the 4 x 4 block of queries
+// 4tq.. and keys tk + 16j, each score the same sequential fmaf chain over d
+// as the other forms (then * scale); 8 FMAs per 16-byte shared load.  Online
+// softmax per query (running max across the 16 threads of its row, float32
+// exp as numpy).  P.V: thread owns 4 queries x D/16 output columns (D = 8:
+// 2 x 1), summing a key tile in float32 and folding each tile's partial into
+// float64 accumulators rescaled by the running-max correction -- float32
+// throughput, and an accumulation error of one 64-term float32 sum per tile
+// instead of one over the whole context.
+constexpr int kBlkQ = 64;          // queries per CTA
+constexpr int kBlkK = 64;          // keys per staged tile
+constexpr int kBlkThreads = 256;
+
+__host__ __device__ constexpr int blk_pitch(int D) { return D + 4; }
+
+template <int D>
+__host__ __device__ constexpr size_t blk_smem_floats() {
+    // q tile + 2 x (K tile + V tile) + P^T tile (+ per-query state)
+    return (size_t)kBlkQ * blk_pitch(D) + 4 * (size_t)kBlkK * blk_pitch(D) +
+           (size_t)kBlkK * (kBlkQ + 4) + 2 * kBlkQ;
+}
+
+// 16-byte async staging of head h of token rows [t0, t0 + n) (fresh row when
+// fresh_of[t] >= 0, else the context row) into s_tile (pitch floats per row)
+template <int D>
+__device__ __forceinline__ void blk_stage(float* s_tile, const float* fresh, const float* ctx,
+                                          const int32_t* fresh_of, int t0, int n, int h, int hid) {
+    constexpr int kChunks = D / 4;
+    for (int i = threadIdx.x; i < n * kChunks; i += kBlkThreads) {
+        const int t = i / kChunks, c = i - t * kChunks;
+        const int fr = __ldg(fresh_of + t0 + t);
+        const float* src = (fr >= 0 ? fresh + (size_t)fr * hid : ctx + (size_t)(t0 + t) * hid) +
+                           h * D + 4 * c;
+        const uint32_t dst = smem_u32(s_tile + t * blk_pitch(D) + 4 * c);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+    }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kBlkThreads)
+    attention_block_kernel(const float* __restrict__ q, const float* __restrict__ k_fresh,
+                           const float* __restrict__ v_fresh,
+                           const tdkv_attn_member* __restrict__ members, int n_members, int layer,
+                           int H, float scale, float* __restrict__ mix) {
+    constexpr int P = blk_pitch(D);
+    constexpr int PP = kBlkQ + 4;                           // P^T pitch
+    // P.V thread layout: QPT queries x DPT columns
+    constexpr int DG = D >= 16 ? 16 : D;                   // column groups
+    constexpr int DPT = D / DG;                            // columns per thread
+    constexpr int QG = kBlkThreads / DG;                   // query groups
+    constexpr int QPT = kBlkQ / QG;                        // queries per thread
+    extern __shared__ __align__(16) float s_dyn[];
+    float* s_q = s_dyn;                                    // [64][P]
+    float* s_kv = s_q + kBlkQ * P;                         // 2 buffers x (K [64][P], V [64][P])
+    float* s_pt = s_kv + 4 * kBlkK * P;                    // P^T [64 keys][PP]
+    float* s_corr = s_pt + kBlkK * PP;                     // [64]
+    float* s_lsum = s_corr + kBlkQ;                        // [64]
+    const int tid = threadIdx.x;
+    const int h = blockIdx.y;
+    int lo = 0, hi = n_members - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (members[mid].tile0 <= (int)blockIdx.x) lo = mid; else hi = mid - 1;
+    }
+    const tdkv_attn_member m = members[lo];
+    const int r0 = ((int)blockIdx.x - m.tile0) * kBlkQ;
+    const int nq = min(kBlkQ, m.n_rows - r0);
+    const int hid = H * D;
+    const size_t lofs = (size_t)layer * m.ctx_layer_stride;
+    const float* ctx_k = m.ctx_k + lofs;
+    const float* ctx_v = m.ctx_v + lofs;
+    const float* kf = k_fresh + (size_t)m.row0 * hid;
+    const float* vf = v_fresh + (size_t)m.row0 * hid;
+    const int tn = (int)m.fix_idx[r0 + nq - 1] + 1;        // keys any row of the tile sees
+    const int ntiles = (tn + kBlkK - 1) / kBlkK;
+
+    // stage q rows and the first key/value tile
+    for (int i = tid; i < kBlkQ * (D / 4); i += kBlkThreads) {
+        const int qi = i / (D / 4), c = i - qi * (D / 4);
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (qi < nq) v = *reinterpret_cast<const float4*>(q + (size_t)(m.row0 + r0 + qi) * hid + h * D + 4 * c);
+        *reinterpret_cast<float4*>(s_q + qi * P + 4 * c) = v;
+    }
+    blk_stage<D>(s_kv, kf, ctx_k, m.fresh_of, 0, min(kBlkK, tn), h, hid);
+    blk_stage<D>(s_kv + kBlkK * P, vf, ctx_v, m.fresh_of, 0, min(kBlkK, tn), h, hid);
+    cp_async_commit();
+
+    // score-phase ownership: queries 4tq + i, keys tk + 16j
+    const int tq = tid >> 4, tk = tid & 15;
+    int tnq[4];
+    float mrun[4];
+    double lrun[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int qi = 4 * tq + i;
+        tnq[i] = qi < nq ? (int)m.fix_idx[r0 + qi] + 1 : 0;
+        mrun[i] = -INFINITY;
+        lrun[i] = 0.0;
+    }
+    // P.V ownership: queries QPT*pq + i, columns DPT*pd + c
+    const int pq = tid / DG, pd = tid - (tid / DG) * DG;
+    double acc[QPT][DPT];
+#pragma unroll
+    for (int i = 0; i < QPT; ++i)
+#pragma unroll
+        for (int c = 0; c < DPT; ++c) acc[i][c] = 0.0;
+
+    for (int it = 0; it < ntiles; ++it) {
+        const int t0 = it * kBlkK;
+        const int n = min(kBlkK, tn - t0);
+        float* s_k = s_kv + (it & 1) * 2 * kBlkK * P;
+        float* s_v = s_k + kBlkK * P;
+        if (it + 1 < ntiles) {                              // prefetch the next tile
+            float* nk = s_kv + ((it + 1) & 1) * 2 * kBlkK * P;
+            const int t1 = t0 + kBlkK;
+            blk_stage<D>(nk, kf, ctx_k, m.fresh_of, t1, min(kBlkK, tn - t1), h, hid);
+            blk_stage<D>(nk + kBlkK * P, vf, ctx_v, m.fresh_of, t1, min(kBlkK, tn - t1), h, hid);
+            cp_async_commit();
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();                                    // tile it (and q) resident
+        // ---- scores: sequential fmaf chains over d
+        float a[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) a[i][j] = 0.f;
+#pragma unroll 2
+        for (int d = 0; d < D; d += 4) {
+            float4 qv[4], kv[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) qv[i] = *reinterpret_cast<const float4*>(s_q + (4 * tq + i) * P + d);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) kv[j] = *reinterpret_cast<const float4*>(s_k + (tk + 16 * j) * P + d);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    a[i][j] = fmaf(qv[i].x, kv[j].x, a[i][j]);
+                    a[i][j] = fmaf(qv[i].y, kv[j].y, a[i][j]);
+                    a[i][j] = fmaf(qv[i].z, kv[j].z, a[i][j]);
+                    a[i][j] = fmaf(qv[i].w, kv[j].w, a[i][j]);
+                }
+        }
+        // ---- online softmax (the 16 threads of a query row are one half-warp)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            float sc[4];
+            float tmax = -INFINITY;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int key = tk + 16 * j;
+                sc[j] = (key < n && t0 + key < tnq[i]) ? a[i][j] * scale : -INFINITY;
+                tmax = fmaxf(tmax, sc[j]);
+            }
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+            const float mnew = fmaxf(mrun[i], tmax);
+            const float corr = (mrun[i] == -INFINITY || mnew == -INFINITY) ? 1.f : expf(mrun[i] - mnew);
+            float ps = 0.f;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float p = sc[j] == -INFINITY ? 0.f : expf(sc[j] - mnew);
+                s_pt[(tk + 16 * j) * PP + 4 * tq + i] = p;
+                ps += p;
+            }
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
+            lrun[i] = lrun[i] * (double)corr + (double)ps;
+            mrun[i] = mnew;
+            if (tk == 0) s_corr[4 * tq + i] = corr;
+        }
+        __syncthreads();                                    // P^T and corrections ready
+        // ---- P.V: float32 sum over the tile's keys, folded into float64
+        float o[QPT][DPT];
+#pragma unroll
+        for (int i = 0; i < QPT; ++i)
+#pragma unroll
+            for (int c = 0; c < DPT; ++c) o[i][c] = 0.f;
+        for (int kk = 0; kk < n; ++kk) {
+            float pv[QPT], vv[DPT];
+#pragma unroll
+            for (int i = 0; i < QPT; ++i) pv[i] = s_pt[kk * PP + QPT * pq + i];
+#pragma unroll
+            for (int c = 0; c < DPT; ++c) vv[c] = s_v[kk * P + DPT * pd + c];
+#pragma unroll
+            for (int i = 0; i < QPT; ++i)
+#pragma unroll
+                for (int c = 0; c < DPT; ++c) o[i][c] = fmaf(pv[i], vv[c], o[i][c]);
+        }
+#pragma unroll
+        for (int i = 0; i < QPT; ++i) {
+            const double cr = (double)s_corr[QPT * pq + i];
+#pragma unroll
+            for (int c = 0; c < DPT; ++c) acc[i][c] = acc[i][c] * cr + (double)o[i][c];
+        }
+        __syncthreads();                                    // buffers reusable
+    }
+    if (tk == 0) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) s_lsum[4 * tq + i] = (float)lrun[i];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < QPT; ++i) {
+        const int qi = QPT * pq + i;
+        if (qi >= nq) continue;
+        const double l = (double)s_lsum[qi];
+#pragma unroll
+        for (int c = 0; c < DPT; ++c)
+            mix[(size_t)(m.row0 + r0 + qi) * hid + h * D + DPT * pd + c] = (float)(acc[i][c] / l);
+    }
+}
+
+template <int D>
+static int32_t launch_attention_block(const float* d_q, const float* d_k_fresh,
+                                      const float* d_v_fresh, const tdkv_attn_member* d_members,
+                                      int32_t n_members, int32_t layer, int32_t n_tiles,
+                                      int32_t num_heads, float scale, float* d_mix,
+                                      cudaStream_t s) {
+    auto kern = attention_block_kernel<D>;
+    const size_t smem = blk_smem_floats<D>() * sizeof(float);
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return check_launch("tdkv_attention_many: cudaFuncSetAttribute");
+    kern<<<dim3(n_tiles, num_heads), kBlkThreads, smem, s>>>(d_q, d_k_fresh, d_v_fresh, d_members,
+                                                             n_members, layer, num_heads, scale,
+                                                             d_mix);
+    count_launch();
+    return check_launch("tdkv_attention_many");
+}
+
 }  // namespace tdkv
 
 using namespace tdkv;
@@ -500,6 +737,19 @@ extern "C" int32_t tdkv_attention_many(const float* d_q, const float* d_k_fresh,
     if (n_members == 0 || total_rows == 0) return TDKV_OK;
     if (!d_q || !d_k_fresh || !d_v_fresh || !d_members || !d_mix)
         return set_error(TDKV_EINVAL, "tdkv_attention_many: null pointer");
+    if (n_tiles > 0 && rows_per_tile == kBlkQ) {
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        switch (head_dim) {
+            case 8: return launch_attention_block<8>(d_q, d_k_fresh, d_v_fresh, d_members, n_members, layer, n_tiles, num_heads, scale, d_mix, s);
+            case 16: return launch_attention_block<16>(d_q, d_k_fresh, d_v_fresh, d_members, n_members, layer, n_tiles, num_heads, scale, d_mix, s);
+            case 32: return launch_attention_block<32>(d_q, d_k_fresh, d_v_fresh, d_members, n_members, layer, n_tiles, num_heads, scale, d_mix, s);
+            case 64: return launch_attention_block<64>(d_q, d_k_fresh, d_v_fresh, d_members, n_members, layer, n_tiles, num_heads, scale, d_mix, s);
+            case 128: return launch_attention_block<128>(d_q, d_k_fresh, d_v_fresh, d_members, n_members, layer, n_tiles, num_heads, scale, d_mix, s);
+            default:
+                return set_error(TDKV_EINVAL, "tdkv_attention_many: 64-row tiles need head_dim "
+                                 "in {8, 16, 32, 64, 128}, got %d", head_dim);
+        }
+    }
     const size_t smem = ((size_t)max_tokens + (size_t)kAttnTile * attn_pitch(head_dim)) * sizeof(float);
     if (smem > 200 * 1024)
         return set_error(TDKV_EUNSUPPORTED, "tdkv_attention_many: %d tokens exceed shared memory",

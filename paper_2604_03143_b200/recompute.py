@@ -136,9 +136,17 @@ def selective_forward(weights, tokens, positions, fix_idx, ctx_k, ctx_v,
 _ATTN_ONLINE = os.environ.get("TDKV_ATTN_ONLINE", "1") != "0"
 
 
+# TDKV_ATTN_BLOCK=0 keeps the 16-row online kernel for head dims the
+# register-blocked 64-row kernel serves
+_ATTN_BLOCK = os.environ.get("TDKV_ATTN_BLOCK", "1") != "0"
+
+
 def _attn_rows_per_tile(head_dim: int) -> int:
-    """Fixed rows per CTA of the query-tiled attention: 16 with the online
-    softmax (head_dim <= 128; 11% faster on the recovery round), else 8."""
+    """Fixed rows per CTA of the query-tiled attention: 64 with the
+    register-blocked kernel (head_dim 8, 16, 32, 64 or 128), else 16 with the
+    online softmax (head_dim <= 128), else 8."""
+    if _ATTN_BLOCK and _ATTN_ONLINE and head_dim in (8, 16, 32, 64, 128):
+        return 64
     return 16 if _ATTN_ONLINE and head_dim <= 128 else 8
 
 
