@@ -403,8 +403,13 @@ def run_tdkv(args):
     for _ in range(args.warmup):
         round_step()
     barrier()
+    # per-step events bracket K1 when a step has more than the round's kernels
+    # (N>1: the exchange); at N=1 a step IS the round (K0 + K1, or K1 alone
+    # with the fused table) and the step time is K1's, without the per-step
+    # event records' host cost (visible at C1's ~20 us rounds)
+    per_step = world > 1
     k1_events = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                 for _ in range(args.steps)]
+                 for _ in range(args.steps)] if per_step else [None] * args.steps
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = tk.launch_count()
     sampler = ClockSampler(local)
@@ -418,7 +423,8 @@ def run_tdkv(args):
     launches = tk.launch_count() - launches0
     elapsed_ms = max_over_ranks(start.elapsed_time(stop))
     ms_step = elapsed_ms / args.steps
-    k1_ms = sum(a.elapsed_time(b) for a, b in k1_events) / args.steps
+    k1_ms = (sum(a.elapsed_time(b) for a, b in k1_events) / args.steps if per_step
+             else start.elapsed_time(stop) / args.steps)
     value = total_bytes / (ms_step * 1e-3) / 1e9
     agents_per_s = total_agents / (ms_step * 1e-3)
 

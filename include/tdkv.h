@@ -105,10 +105,11 @@ int32_t tdkv_collect(const void* d_master_k, const void* d_master_v,
 /* One round in one call (replaces the K0 + K1 pair of a collector round,
  * pic.py:208-235): tdkv_rope_table over d_deltas[n_table_rows] into d_table
  * (n_table_rows = 0: no rotation, K1 alone), then tdkv_collect with that
- * table.  Both kernels are launched with programmatic dependent launch: K1's
- * launch and first master-tile loads overlap K0, K0 waits for the previous
- * kernels in the stream before overwriting the table (TDKV_PDL=0: plain
- * launches).  Capturable into a CUDA graph. */
+ * table.  With TDKV_PDL=1 both kernels are launched with programmatic
+ * dependent launch (K1's launch and first master-tile loads overlap K0, K0
+ * waits for the previous kernels before overwriting the table); by default
+ * they are plain launches (measured faster at C2).  Capturable into a CUDA
+ * graph. */
 int32_t tdkv_collect_round(const int64_t* d_deltas, int64_t n_table_rows,
                            const double* d_inv_freq, void* d_table, const void* d_master_k,
                            const void* d_master_v, int64_t master_layer_stride,
@@ -116,7 +117,13 @@ int32_t tdkv_collect_round(const int64_t* d_deltas, int64_t n_table_rows,
                            const tdkv_collect_job* d_jobs, const int64_t* d_dst_rows,
                            void* d_dst_k, void* d_dst_v, int64_t dst_layer_stride,
                            int32_t num_layers, int32_t num_heads, int32_t head_dim,
-                           int32_t dtype, int32_t grid_limit, void* stream);
+                           int32_t dtype, int32_t grid_limit, int32_t flags, void* stream);
+/* flags of tdkv_collect_round: TDKV_ROUND_FUSE_TABLE computes each job
+ * group's cos/sin rows inside K1 (shared memory, the K0 arithmetic) instead
+ * of launching K0 -- one kernel per round, for launch-bound small rounds.
+ * Requires one table row per job (every job's delta constant: tbl_stride 0,
+ * tbl_row indexing d_deltas). */
+#define TDKV_ROUND_FUSE_TABLE 1
 /* d_master_v == d_dst_v == NULL makes a K-only collect (align_cached alone;
  * the reference copies V in _skeleton). */
 

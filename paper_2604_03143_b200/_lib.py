@@ -25,6 +25,7 @@ TDKV_BF16 = 1
 NO_VIOLATION = 0x7F7F7F7F
 ROWS_CONTIGUOUS = 1
 ROWS_JOB_MINOR = 2
+ROUND_FUSE_TABLE = 1
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -117,7 +118,7 @@ _SIGS = {
     "tdkv_collect": (_I32, [_P, _P, _I64, _P, _I32, _I32, _P, _P, _P, _I32, _P, _P, _I64,
                             _I32, _I32, _I32, _I32, _I32, _P]),
     "tdkv_collect_round": (_I32, [_P, _I64, _P, _P, _P, _P, _I64, _P, _I32, _I32, _P, _P, _P,
-                                  _P, _I64, _I32, _I32, _I32, _I32, _I32, _P]),
+                                  _P, _I64, _I32, _I32, _I32, _I32, _I32, _I32, _P]),
     "tdkv_collect_sources": (_I32, [_P, _P, _I32, _P, _I64, _P, _I32, _I32, _P, _P, _P, _I32,
                                     _P, _P, _I64, _I32, _I32, _I32, _I32, _I32, _P]),
     "tdkv_diff_compare": (_I32, [_P, _I32, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32,

@@ -38,6 +38,11 @@ _SMS = 148
 
 
 _AUTO_GRAPH = os.environ.get("TDKV_ROUND_GRAPHS", "1") != "0"
+# fused K0 (table rows computed inside K1): for rounds up to this many
+# algorithmic bytes (C1: 75 MB), where a second launch is a visible share;
+# larger rounds keep K0 (recomputing rows per work item would cost more)
+_FUSE_TABLE = os.environ.get("TDKV_FUSE_TABLE", "auto")
+_FUSE_TABLE_MAX_BYTES = 1 << 30
 
 
 def pick_tile_rows(row_bytes: int, budget: int = _TILE_SMEM) -> int:
@@ -328,6 +333,12 @@ class CollectPlan:
         self.d_dst_rows = h2d(host.dst_rows, self.device) if offsets is None else offsets[2]
         self.d_deltas = h2d(host.deltas, self.device)
         self._fast: dict = {}
+        # small rounds are launch-bound: compute the cos/sin rows inside K1
+        # (one kernel per round) when every job has one constant delta
+        self.fuse_table = bool(
+            self.rotate and host.jobs.size and (host.jobs["tbl_stride"] == 0).all()
+            and (_FUSE_TABLE == "1" or (_FUSE_TABLE != "0"
+                                        and self.algorithmic_bytes() <= _FUSE_TABLE_MAX_BYTES)))
         self.table = torch.empty((max(host.deltas.size, 1), self.head_dim // 2, 2),
                                  dtype=torch.float64 if self.kv_dtype == torch.float32
                                  else torch.float32, device=self.device)
@@ -440,11 +451,13 @@ class CollectPlan:
                     C.c_void_p(ptr(dst_k)), C.c_void_p(ptr(dst_v) if with_v else 0),
                     C.c_int64(int(dst_layer_stride)), C.c_int32(self.num_layers),
                     C.c_int32(self.num_heads), C.c_int32(self.head_dim),
-                    C.c_int32(dtype_code(self.kv_dtype)), C.c_int32(int(grid_limit)), stream)
+                    C.c_int32(dtype_code(self.kv_dtype)), C.c_int32(int(grid_limit)),
+                    C.c_int32(_lib.ROUND_FUSE_TABLE if self.fuse_table else 0), stream)
             if len(self._fast) >= 16:
                 self._fast.clear()
             # keep the tensors whose addresses are baked in alive with the entry
-            fast = self._fast[key] = (lib.tdkv_collect_round, args, 2 if n_tbl else 1,
+            fast = self._fast[key] = (lib.tdkv_collect_round, args,
+                                      2 if n_tbl and not self.fuse_table else 1,
                                       (arena.k, arena.v, dst_k, dst_v, inv))
         fn, args, kernels, _ = fast
         if fn(*args):

@@ -71,6 +71,13 @@ struct CollectParams {
     const uint8_t* unit_src;
     const void* src_k[kMaxSources];
     const void* src_v[kMaxSources];
+    // fused K0 (tdkv_collect_round with TDKV_ROUND_FUSE_TABLE): every job has
+    // one constant delta (tbl_stride 0); each job group's cos/sin rows are
+    // computed into shared memory from deltas[tbl_row] * inv_freq, the
+    // arithmetic of rope_table_kernel, instead of read from a K0 table
+    const int64_t* deltas;
+    const double* inv_freq;
+    int32_t fuse_table;
 };
 
 // Per-job destination metadata is staged in shared memory in groups of
@@ -167,6 +174,18 @@ __global__ void __launch_bounds__(256) collect_kernel(const CollectParams p) {
 #pragma unroll
         for (int q = 0; q < kPairs; ++q) cs[q] = __ldg(trow + q);
     };
+    // fused K0: the group's rows live in shared memory after the tiles
+    const bool fused = p.fuse_table != 0;
+    Tbl* s_cs = reinterpret_cast<Tbl*>(smem + (size_t)4 * tile_bytes);
+    auto load_cs_job = [&](Tbl* cs, int jj, const int4& m, int j0) {
+        if (fused) {
+            const Tbl* trow = s_cs + (size_t)jj * half + j0;
+#pragma unroll
+            for (int q = 0; q < kPairs; ++q) cs[q] = trow[q];
+        } else {
+            load_cs(cs, m.x, j0);
+        }
+    };
 
     int item = blockIdx.x;
     if constexpr (BULK) {
@@ -241,6 +260,22 @@ __global__ void __launch_bounds__(256) collect_kernel(const CollectParams p) {
             }
             __syncthreads();
             const int ng = min(gsz, u.job_end - u.job_begin - g * gsz);
+            if (fused && rotate) {
+                // this group's cos/sin rows (rope_table_kernel's arithmetic)
+                for (int idx = tid; idx < ng * half; idx += nthr) {
+                    const int jj = idx / half, j = idx - jj * half;
+                    const double theta =
+                        __dmul_rn((double)p.deltas[s_meta[mb][jj].x], p.inv_freq[j]);
+                    double sn, cn;
+                    sincos(theta, &sn, &cn);
+                    if constexpr (sizeof(Tbl) == 16) {
+                        s_cs[idx] = make_double2(cn, sn);
+                    } else {
+                        s_cs[idx] = make_float2((float)cn, (float)sn);
+                    }
+                }
+                __syncthreads();
+            }
             if constexpr (BULK) {
                 if (v_tma && tid < ng) {
                     const int64_t* dr = &s_drow[mb][tid * kMaxTileRows];
@@ -264,10 +299,10 @@ __global__ void __launch_bounds__(256) collect_kernel(const CollectParams p) {
                     const int j0 = ((c * kEpu) % p.head_dim) >> 1;
                     Tbl cs[kPairs], csn[kPairs];
                     int4 m = s_meta[mb][0];
-                    if (rotate && m.y == 0) load_cs(cs, m.x, j0);
+                    if (rotate && m.y == 0) load_cs_job(cs, 0, m, j0);
                     for (int jj = 0; jj < ng; ++jj) {
                         const int4 mn = jj + 1 < ng ? s_meta[mb][jj + 1] : m;
-                        if (rotate && jj + 1 < ng && mn.y == 0) load_cs(csn, mn.x, j0);
+                        if (rotate && jj + 1 < ng && mn.y == 0) load_cs_job(csn, jj + 1, mn, j0);
                         const int64_t* dr = &s_drow[mb][jj * kMaxTileRows];
                         for (int r = ty; r < u.nrows; r += rows_per_pass) {
                             const int64_t drow = dr[r];
@@ -305,7 +340,10 @@ template <typename T, int UB, bool BULK>
 static int32_t launch_collect(const CollectParams& p, int grid_limit, cudaStream_t s, bool pdl) {
     auto kern = collect_kernel<T, UB, BULK>;
     const int threads = 256;
-    const size_t smem = (size_t)4 * p.max_rows * p.row_elems * sizeof(T);
+    const size_t smem = (size_t)4 * p.max_rows * p.row_elems * sizeof(T) +
+                        (p.fuse_table ? (size_t)kJobGroup * (p.head_dim / 2) *
+                                            sizeof(typename Elt<T>::Table)
+                                      : 0);
     if (smem > 227 * 1024)
         return set_error(TDKV_EINVAL, "tdkv_collect: tile of %d rows needs %zu B of shared memory",
                          p.max_rows, smem);
@@ -376,14 +414,17 @@ static int32_t collect_impl(const void* d_master_k, const void* d_master_v,
                             int32_t num_layers, int32_t num_heads, int32_t head_dim,
                             int32_t dtype, int32_t grid_limit, void* stream,
                             const uint8_t* d_unit_src, const void* const* h_src_k,
-                            const void* const* h_src_v, int32_t n_src, bool pdl = false) {
+                            const void* const* h_src_v, int32_t n_src, bool pdl = false,
+                            const int64_t* d_deltas = nullptr,
+                            const double* d_inv_freq = nullptr) {
     if (n_units < 0 || num_layers <= 0 || num_heads <= 0 || head_dim <= 0 || (head_dim & 1))
         return set_error(TDKV_EINVAL, "tdkv_collect: bad geometry L=%d H=%d D=%d", num_layers,
                          num_heads, head_dim);
     if (n_units == 0) return TDKV_OK;
     if (max_rows <= 0 || max_rows > kMaxTileRows)
         return set_error(TDKV_EINVAL, "tdkv_collect: max_rows must be in [1, %d]", kMaxTileRows);
-    if (!d_master_k || !d_units || !d_jobs || !d_dst_rows || !d_dst_k || (rotate && !d_table) ||
+    if (!d_master_k || !d_units || !d_jobs || !d_dst_rows || !d_dst_k ||
+        (rotate && !d_table && !(d_deltas && d_inv_freq)) ||
         ((d_dst_v == nullptr) != (d_master_v == nullptr)))
         return set_error(TDKV_EINVAL, "tdkv_collect: null pointer");
     if (dtype != TDKV_F32 && dtype != TDKV_BF16)
@@ -407,6 +448,9 @@ static int32_t collect_impl(const void* d_master_k, const void* d_master_v,
     p.head_dim = head_dim;
     p.row_elems = num_heads * head_dim;
     p.unit_src = d_unit_src;
+    p.deltas = d_deltas;
+    p.inv_freq = d_inv_freq;
+    p.fuse_table = (rotate && d_deltas && d_inv_freq) ? 1 : 0;
     for (int i = 0; i < kMaxSources; ++i) {
         p.src_k[i] = i < n_src ? h_src_k[i] : nullptr;
         p.src_v[i] = i < n_src && h_src_v ? h_src_v[i] : nullptr;
@@ -461,7 +505,8 @@ extern "C" int32_t tdkv_collect(const void* d_master_k, const void* d_master_v,
 // launched with programmatic dependent launch -- K0 waits for the previous
 // round (its table is being overwritten) and then releases K1, whose launch,
 // barrier setup and first master-tile TMA loads overlap K0; K1 waits for K0
-// only before it rotates or writes.  TDKV_PDL=0 launches them plainly.
+// only before it rotates or writes.  Opt-in (TDKV_PDL=1): plain launches
+// measured faster at C2.
 extern "C" int32_t tdkv_collect_round(const int64_t* d_deltas, int64_t n_table_rows,
                                       const double* d_inv_freq, void* d_table,
                                       const void* d_master_k, const void* d_master_v,
@@ -471,21 +516,25 @@ extern "C" int32_t tdkv_collect_round(const int64_t* d_deltas, int64_t n_table_r
                                       const int64_t* d_dst_rows, void* d_dst_k, void* d_dst_v,
                                       int64_t dst_layer_stride, int32_t num_layers,
                                       int32_t num_heads, int32_t head_dim, int32_t dtype,
-                                      int32_t grid_limit, void* stream) {
+                                      int32_t grid_limit, int32_t flags, void* stream) {
+    // off by default: measured 4% slower at C2 on B200 (K1's early-launched
+    // CTAs idle at griddepcontrol.wait while holding their SM slots)
     static const bool pdl = [] {
         const char* e = getenv("TDKV_PDL");
-        return !(e && e[0] == '0');
+        return e && e[0] == '1';
     }();
     const bool rotate = n_table_rows > 0;
-    if (rotate) {
+    const bool fuse = rotate && (flags & TDKV_ROUND_FUSE_TABLE);
+    if (rotate && !fuse) {
         const int32_t rc = rope_table_impl(d_deltas, n_table_rows, d_inv_freq, head_dim / 2, dtype,
                                            d_table, stream, pdl);
         if (rc) return rc;
     }
     return collect_impl(d_master_k, d_master_v, master_layer_stride, d_units, n_units, max_rows,
-                        d_jobs, d_dst_rows, rotate ? d_table : nullptr, rotate ? 1 : 0, d_dst_k,
-                        d_dst_v, dst_layer_stride, num_layers, num_heads, head_dim, dtype,
-                        grid_limit, stream, nullptr, nullptr, nullptr, 0, pdl && rotate);
+                        d_jobs, d_dst_rows, rotate && !fuse ? d_table : nullptr, rotate ? 1 : 0,
+                        d_dst_k, d_dst_v, dst_layer_stride, num_layers, num_heads, head_dim, dtype,
+                        grid_limit, stream, nullptr, nullptr, nullptr, 0, pdl && rotate && !fuse,
+                        fuse ? d_deltas : nullptr, fuse ? d_inv_freq : nullptr);
 }
 
 extern "C" int32_t tdkv_collect_sources(const void* const* h_src_k, const void* const* h_src_v,
