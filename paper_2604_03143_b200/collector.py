@@ -35,6 +35,9 @@ from .ledger import CostLedger
 # smem budget per CTA for the double-buffered K+V master tile (3 CTAs / SM)
 _TILE_SMEM = int(os.environ.get("TDKV_TILE_SMEM", 32 * 1024))
 _SMS = 148
+# (layer, tile, job-chunk) work items a plan aims for (job chunks split until
+# the launch has this many items); TDKV_PLAN_ITEMS overrides for A/B runs
+_TARGET_ITEMS = int(os.environ.get("TDKV_PLAN_ITEMS", 4 * _SMS))
 
 
 _AUTO_GRAPH = os.environ.get("TDKV_ROUND_GRAPHS", "1") != "0"
@@ -139,7 +142,7 @@ class HostPlan:
 
 def plan_host(seg_row0: np.ndarray, seg_len: np.ndarray, segments: np.ndarray,
               dst_rows: np.ndarray, deltas: np.ndarray, num_layers: int, tile_rows: int,
-              target_items: int = 4 * _SMS * 3) -> HostPlan:
+              target_items: int = _TARGET_ITEMS) -> HostPlan:
     """Vectorized round planning.  ``segments`` (J,) names each job's
     segment; ``dst_rows``/``deltas`` are the jobs' per-token rows and deltas
     concatenated in job order (job j covers seg_len[segments[j]] tokens)."""
@@ -210,7 +213,7 @@ def _build_units(seg_row0, seg_len, seg_o: np.ndarray, num_layers: int, tile_row
 
 def plan_host_offsets(seg_row0: np.ndarray, seg_len: np.ndarray, segments: np.ndarray,
                       dst_off: np.ndarray, job_delta: np.ndarray, num_layers: int,
-                      tile_rows: int, target_items: int = 4 * _SMS * 3) -> HostPlan:
+                      tile_rows: int, target_items: int = _TARGET_ITEMS) -> HostPlan:
     """Planning when every job's destination rows are a contiguous run of a
     device-resident row table (e.g. the agents' slot maps, see SlotArena):
     job j's token i lands at rows[dst_off[j] + i] and rotates by the
