@@ -150,6 +150,41 @@ int32_t tdkv_collect_sources(const void* const* h_src_k, const void* const* h_sr
                              int32_t num_layers, int32_t num_heads, int32_t head_dim,
                              int32_t dtype, int32_t grid_limit, void* stream);
 
+/* Family restore: the fused decoder of a whole family as the collector
+ * round of its master.  Replaces fused_restore (restore.py:50-104) over every
+ * mirror of one or more families -- DiffStore.encode_family's output restored
+ * the way trace._verify_family_restores (trace.py:289-329) walks it -- with
+ * each master tile read from HBM once for all of its mirrors.  Source i
+ * (h_src_k/h_src_v[i], n_src <= 16) is one master cache (L, source_rows, H,
+ * D); the plan's arena rows are virtual: row i*source_rows + r is row r of
+ * source i (units and jobs' seg_row0 use them).  Job j (of n_jobs) is one
+ * mirror whose rows go to d_dst_rows (pool slots) rotated by its table row(s)
+ * exactly as tdkv_collect, except where its diff stores the (layer l, block
+ * b): d_overlay[j].map_k[l*nb + b] >= 0 names the payload block of
+ * d_overlay[j].pay_k holding those K rows (rows of block_size tokens: the
+ * encoder's slab), and likewise map_v / pay_v for V (a NULL map = no diff of
+ * that plane; the encoder's diffs share one map).  Payload-sourced planes are skipped by K1 and written by a second
+ * kernel in the same call (payload -> rotate -> pool): the overlay precedes
+ * rotation (restore.py:5-8).  max_rows must divide block_size (a tile never
+ * straddles a diff block); masters, payloads and the pool 16-byte aligned
+ * with 16-byte rows.  Stream-ordered and capturable. */
+typedef struct {
+    const void* pay_k;
+    const void* pay_v;
+    const int32_t* map_k;    /* (L * nb) payload block or -1 */
+    const int32_t* map_v;
+} tdkv_collect_overlay;
+
+int32_t tdkv_restore_family(const void* const* h_src_k, const void* const* h_src_v,
+                            int32_t n_src, int64_t source_rows,
+                            const tdkv_collect_unit* d_units, int32_t n_units, int32_t max_rows,
+                            const tdkv_collect_job* d_jobs, int32_t n_jobs,
+                            const int64_t* d_dst_rows, const tdkv_collect_overlay* d_overlay,
+                            int32_t nb, int32_t block_size,
+                            const void* d_table, int32_t rotate, void* d_dst_k, void* d_dst_v,
+                            int64_t dst_layer_stride, int32_t num_layers, int32_t num_heads,
+                            int32_t head_dim, int32_t dtype, int32_t grid_limit, void* stream);
+
 /* ------------------------------------------------------------------------
  * K2  block-diff encoder.  Replaces diffstore.encode_diff
  * (diffstore.py:119-182) for a batch of (master, mirror) pairs of identical

@@ -90,14 +90,17 @@ WIRE_SEG = np.dtype([("offset", "<u8"), ("nbytes", "<u8"), ("ptr", "<u8"), ("kin
 ATTN_MEMBER = np.dtype([("ctx_k", "<u8"), ("ctx_v", "<u8"), ("fresh_of", "<u8"),
                         ("fix_idx", "<u8"), ("ctx_layer_stride", "<i8"), ("row0", "<i4"),
                         ("n_rows", "<i4"), ("num_tokens", "<i4"), ("tile0", "<i4")])
+COLLECT_OVERLAY = np.dtype([("pay_k", "<u8"), ("pay_v", "<u8"), ("map_k", "<u8"),
+                            ("map_v", "<u8")])
 WIRE_RAW, WIRE_BF16_TO_F32, WIRE_F32_TO_BF16 = 0, 1, 2
 assert WIRE_SEG.itemsize == 32 and ATTN_MEMBER.itemsize == 56
 assert COLLECT_JOB.itemsize == 24 and COLLECT_UNIT.itemsize == 16
+assert COLLECT_OVERLAY.itemsize == 32
 assert DIFF_PAIR.itemsize == 32 and DIFF_OUT.itemsize == 40 and ROWS_JOB.itemsize == 112
 
 EXPORTS = (
     "tdkv_version", "tdkv_last_error", "tdkv_launch_count", "tdkv_rope_table",
-    "tdkv_collect", "tdkv_collect_round", "tdkv_collect_sources", "tdkv_diff_compare", "tdkv_diff_compact", "tdkv_diff_encode", "tdkv_rows",
+    "tdkv_collect", "tdkv_collect_round", "tdkv_collect_sources", "tdkv_restore_family", "tdkv_diff_compare", "tdkv_diff_compact", "tdkv_diff_encode", "tdkv_rows",
     "tdkv_keydiff", "tdkv_select_important", "tdkv_gemm", "tdkv_qkv_rope", "tdkv_attention",
     "tdkv_attention_many",
     "tdkv_fill_rows", "tdkv_alloc_create", "tdkv_alloc_destroy", "tdkv_alloc_free_count",
@@ -121,6 +124,9 @@ _SIGS = {
                                   _P, _I64, _I32, _I32, _I32, _I32, _I32, _I32, _P]),
     "tdkv_collect_sources": (_I32, [_P, _P, _I32, _P, _I64, _P, _I32, _I32, _P, _P, _P, _I32,
                                     _P, _P, _I64, _I32, _I32, _I32, _I32, _I32, _P]),
+    "tdkv_restore_family": (_I32, [_P, _P, _I32, _I64, _P, _I32, _I32, _P, _I32, _P, _P,
+                                   _I32, _I32, _P, _I32, _P, _P, _I64, _I32, _I32, _I32, _I32,
+                                   _I32, _P]),
     "tdkv_diff_compare": (_I32, [_P, _I32, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32,
                                  _I32, _P]),
     "tdkv_diff_compact": (_I32, [_P, _P, _I32, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32,

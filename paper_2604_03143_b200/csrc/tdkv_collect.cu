@@ -78,6 +78,16 @@ struct CollectParams {
     const int64_t* deltas;
     const double* inv_freq;
     int32_t fuse_table;
+    // family restore (tdkv_restore_family): source i holds the virtual arena
+    // rows [i*source_rows, (i+1)*source_rows) -- one master cache each -- and
+    // a job whose overlay names a payload block for the tile's (layer,
+    // block) takes the tile's K and V rows from that diff payload instead of
+    // the staged master rows (the overlay precedes rotation, restore.py:5-8)
+    int64_t source_rows;
+    const tdkv_collect_overlay* ovl;      // per job: payload slabs + block maps
+    int32_t nb;                           // diff blocks per layer
+    int32_t block_size;
+    int32_t n_jobs;
 };
 
 // Per-job destination metadata is staged in shared memory in groups of
@@ -94,8 +104,11 @@ __device__ __forceinline__ int job_group_size(int nj) {
 }
 constexpr int kMaxTileRows = 32;
 
-template <typename T, int UB, bool BULK>
-__global__ void __launch_bounds__(256) collect_kernel(const CollectParams p) {
+// OVL: the family-restore instantiation (diff overlay); the collector's
+// instantiations compile it out, keeping their register count (and so four
+// resident CTAs per SM)
+template <typename T, int UB, bool BULK, bool OVL>
+__global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) {
     using V = typename UnitBits<UB>::V;
     using Tbl = typename Elt<T>::Table;
     constexpr int kEpu = UB / (int)sizeof(T);      // elements per unit
@@ -105,6 +118,7 @@ __global__ void __launch_bounds__(256) collect_kernel(const CollectParams p) {
     __shared__ __align__(8) uint64_t bars[2];
     __shared__ __align__(16) int64_t s_drow[2][kJobGroup * kMaxTileRows];
     __shared__ int4 s_meta[2][kJobGroup];          // tbl_row, tbl_stride, i0
+    __shared__ int2 s_map[2][kJobGroup];           // OVL: the tile's K / V payload blocks
 
     const int tid = threadIdx.x;
     const int nthr = blockDim.x;
@@ -140,18 +154,24 @@ __global__ void __launch_bounds__(256) collect_kernel(const CollectParams p) {
         const int layer = item / p.n_units;
         const int ui = item - layer * p.n_units;
         u = p.units[ui];
-        const size_t off = (size_t)layer * p.mls + (size_t)u.row0 * p.row_elems;
+        int64_t row0 = u.row0;
         const void* bk = p.mk;
         const void* bv = p.mv;
         if (p.unit_src) {
             const int src = p.unit_src[ui];
             bk = p.src_k[src];
             bv = p.src_v[src];
+        } else if (OVL && p.source_rows > 0) {
+            const int src = (int)(row0 / p.source_rows);
+            row0 -= (int64_t)src * p.source_rows;
+            bk = p.src_k[src];
+            bv = p.src_v[src];
         }
+        const size_t off = (size_t)layer * p.mls + (size_t)row0 * p.row_elems;
         gk = static_cast<const T*>(bk) + off;
         gv = static_cast<const T*>(bv) + off;
     };
-    auto stage_meta = [&](const tdkv_collect_unit& u, int g, int mb) {
+    auto stage_meta = [&](const tdkv_collect_unit& u, int layer, int g, int mb) {
         const int gsz = job_group_size(u.job_end - u.job_begin);
         const int jbase = u.job_begin + g * gsz;
         const int ng = min(gsz, u.job_end - jbase);
@@ -165,7 +185,18 @@ __global__ void __launch_bounds__(256) collect_kernel(const CollectParams p) {
         }
         if (tid < ng) {
             const tdkv_collect_job jb = p.jobs[jbase + tid];
-            s_meta[mb][tid] = make_int4(jb.tbl_row, jb.tbl_stride, u.row0 - jb.seg_row0, 0);
+            const int i0 = u.row0 - jb.seg_row0;
+            s_meta[mb][tid] = make_int4(jb.tbl_row, jb.tbl_stride, i0, 0);
+            if constexpr (OVL) {
+                // the tile lies inside one diff block (block_size % max_rows
+                // == 0): fetch its K / V payload blocks with the rows
+                const tdkv_collect_overlay o = p.ovl[jbase + tid];
+                const size_t e = (size_t)layer * p.nb + i0 / p.block_size;
+                if (o.map_k) cp_async_4(&s_map[mb][tid].x, o.map_k + e);
+                else s_map[mb][tid].x = -1;
+                if (o.map_v) cp_async_4(&s_map[mb][tid].y, o.map_v + e);
+                else s_map[mb][tid].y = -1;
+            }
         }
         cp_async_commit();
     };
@@ -210,7 +241,7 @@ __global__ void __launch_bounds__(256) collect_kernel(const CollectParams p) {
         uint8_t* buf = smem + (size_t)b * 2 * tile_bytes;
         const int layer = item / p.n_units;
         const tdkv_collect_unit u = p.units[item - layer * p.n_units];
-        stage_meta(u, 0, 0);
+        stage_meta(u, layer, 0, 0);
 
         if constexpr (BULK) {
             const int next = item + gridDim.x;
@@ -253,7 +284,7 @@ __global__ void __launch_bounds__(256) collect_kernel(const CollectParams p) {
         for (int g = 0; g < ngroups; ++g) {
             const int mb = g & 1;
             if (g + 1 < ngroups) {
-                stage_meta(u, g + 1, mb ^ 1);
+                stage_meta(u, layer, g + 1, mb ^ 1);
                 cp_async_wait<1>();
             } else {
                 cp_async_wait<0>();
@@ -277,7 +308,11 @@ __global__ void __launch_bounds__(256) collect_kernel(const CollectParams p) {
                 __syncthreads();
             }
             if constexpr (BULK) {
-                if (v_tma && tid < ng) {
+                // a job whose tile comes from its diff payload moves V in
+                // the thread loop below
+                // (family restore: a job's payload-sourced planes are the
+                // overlay pass's)
+                if (v_tma && tid < ng && !(OVL && s_map[mb][tid].y >= 0)) {
                     const int64_t* dr = &s_drow[mb][tid * kMaxTileRows];
                     const int64_t r0 = dr[0];
                     bool contig = true;
@@ -304,7 +339,12 @@ __global__ void __launch_bounds__(256) collect_kernel(const CollectParams p) {
                         const int4 mn = jj + 1 < ng ? s_meta[mb][jj + 1] : m;
                         if (rotate && jj + 1 < ng && mn.y == 0) load_cs_job(csn, jj + 1, mn, j0);
                         const int64_t* dr = &s_drow[mb][jj * kMaxTileRows];
-                        for (int r = ty; r < u.nrows; r += rows_per_pass) {
+                        // overlay flags are uniform across the CTA: a plane
+                        // taken from the payload is the overlay pass's
+                        const bool ovk = OVL && s_map[mb][jj].x >= 0;
+                        const bool ovv = OVL && s_map[mb][jj].y >= 0;
+                        for (int r = ty; r < u.nrows && !(ovk && (ovv || v_tma || !has_v));
+                             r += rows_per_pass) {
                             const int64_t drow = dr[r];
                             V kv = sk[r * upr + c];
                             if (rotate) {
@@ -314,9 +354,10 @@ __global__ void __launch_bounds__(256) collect_kernel(const CollectParams p) {
                                 for (int q = 0; q < kPairs; ++q)
                                     rot_pair(e[2 * q], e[2 * q + 1], cs[q]);
                             }
-                            st_stream(reinterpret_cast<V*>(dk_l + (size_t)drow * p.row_elems) + c,
-                                      kv);
-                            if (has_v && !v_tma)
+                            if (!ovk)
+                                st_stream(reinterpret_cast<V*>(dk_l + (size_t)drow * p.row_elems) + c,
+                                          kv);
+                            if (has_v && !v_tma && !ovv)
                                 st_stream(reinterpret_cast<V*>(dv_l + (size_t)drow * p.row_elems) + c,
                                           sv[r * upr + c]);
                         }
@@ -336,9 +377,9 @@ __global__ void __launch_bounds__(256) collect_kernel(const CollectParams p) {
     }
 }
 
-template <typename T, int UB, bool BULK>
+template <typename T, int UB, bool BULK, bool OVL = false>
 static int32_t launch_collect(const CollectParams& p, int grid_limit, cudaStream_t s, bool pdl) {
-    auto kern = collect_kernel<T, UB, BULK>;
+    auto kern = collect_kernel<T, UB, BULK, OVL>;
     const int threads = 256;
     const size_t smem = (size_t)4 * p.max_rows * p.row_elems * sizeof(T) +
                         (p.fuse_table ? (size_t)kJobGroup * (p.head_dim / 2) *
@@ -361,6 +402,130 @@ static int32_t launch_collect(const CollectParams& p, int grid_limit, cudaStream
         return check_launch("tdkv_collect: launch");
     count_launch();
     return check_launch("tdkv_collect");
+}
+
+// Overlay pass of the family restore: the (job, layer, block)s whose rows
+// come from the job's diff payload (K1 skipped them), K rotated by the job's
+// table row(s), V copied, to the job's destination rows.  A CTA scans
+// kOvlChunk block-map entries, compacts the changed ones in shared memory and
+// moves them with all threads, four rows per thread loaded before any is
+// stored (chunks small enough that even a 24-mirror family spreads its
+// changed blocks over every SM).
+constexpr int kOvlChunk = 32;
+template <typename T>
+__global__ void __launch_bounds__(256) overlay_rows_kernel(const CollectParams p) {
+    using V = uint4;
+    using Tbl = typename Elt<T>::Table;
+    constexpr int kEpu = 16 / (int)sizeof(T);
+    constexpr int kPairs = kEpu / 2;
+    constexpr int kR = 4;
+    __shared__ int s_list[kOvlChunk];
+    __shared__ int s_n;
+    const int tid = threadIdx.x;
+    const int upr = p.row_elems * (int)sizeof(T) / 16;
+    const int tx_n = upr < 256 ? upr : 256;
+    const int rows_per_pass = 256 / tx_n;
+    const int tx = tid % tx_n, ty = tid / tx_n;
+    const Tbl* __restrict__ table = static_cast<const Tbl*>(p.table);
+    const int half = p.head_dim >> 1;
+    const long long n_entries = (long long)p.n_jobs * p.num_layers * p.nb;
+    const long long per_job = (long long)p.num_layers * p.nb;
+    // entry e = (job, layer, block), job-major
+    auto map_at = [&](long long e) {
+        const int job = (int)(e / per_job);
+        const long long lb = e - job * per_job;
+        const tdkv_collect_overlay o = p.ovl[job];
+        return make_int2(o.map_k ? __ldg(o.map_k + lb) : -1, o.map_v ? __ldg(o.map_v + lb) : -1);
+    };
+    for (long long e0 = (long long)blockIdx.x * kOvlChunk; e0 < n_entries;
+         e0 += (long long)gridDim.x * kOvlChunk) {
+        if (tid == 0) s_n = 0;
+        __syncthreads();
+        const long long e = e0 + tid;
+        if (tid < kOvlChunk && e < n_entries) {
+            const int2 m = map_at(e);
+            if (m.x >= 0 || m.y >= 0) s_list[atomicAdd(&s_n, 1)] = tid;
+        }
+        __syncthreads();
+        const int n = s_n;
+        for (int i = 0; i < n; ++i) {
+            const long long ei = e0 + s_list[i];
+            const int2 m = map_at(ei);
+            const int b = (int)(ei % p.nb);
+            const long long jl = ei / p.nb;
+            const int layer = (int)(jl % p.num_layers);
+            const int job = (int)(jl / p.num_layers);
+            const tdkv_collect_job jb = p.jobs[job];
+            const tdkv_collect_overlay o = p.ovl[job];
+            const int i0 = b * p.block_size;
+            const int nrows = (int)min((int64_t)p.block_size, p.source_rows - i0);
+            const V* pk = m.x >= 0 ? reinterpret_cast<const V*>(static_cast<const T*>(o.pay_k) +
+                                                                (size_t)m.x * p.block_size * p.row_elems)
+                                   : nullptr;
+            const V* pv = m.y >= 0 ? reinterpret_cast<const V*>(static_cast<const T*>(o.pay_v) +
+                                                                (size_t)m.y * p.block_size * p.row_elems)
+                                   : nullptr;
+            T* dk_l = static_cast<T*>(p.dk) + (size_t)layer * p.dls;
+            T* dv_l = p.dv ? static_cast<T*>(p.dv) + (size_t)layer * p.dls : nullptr;
+            const int64_t* drows = p.dst_rows + jb.dst_off + i0;
+            if (ty < rows_per_pass) {
+                for (int c = tx; c < upr; c += tx_n) {
+                    const int j0 = ((c * kEpu) % p.head_dim) >> 1;
+                    for (int r0 = ty; r0 < nrows; r0 += kR * rows_per_pass) {
+                        V kx[kR], vx[kR];
+                        int64_t drow[kR];
+#pragma unroll
+                        for (int q = 0; q < kR; ++q) {
+                            const int r = r0 + q * rows_per_pass;
+                            if (r < nrows) {
+                                drow[q] = __ldg(drows + r);
+                                if (pk) kx[q] = ld_stream(pk + (size_t)r * upr + c);
+                                if (pv) vx[q] = ld_stream(pv + (size_t)r * upr + c);
+                            }
+                        }
+#pragma unroll
+                        for (int q = 0; q < kR; ++q) {
+                            const int r = r0 + q * rows_per_pass;
+                            if (r >= nrows) continue;
+                            if (pk) {
+                                if (p.rotate) {
+                                    const Tbl* trow = table + (size_t)(jb.tbl_row +
+                                                                       (i0 + r) * jb.tbl_stride) *
+                                                                  half + j0;
+                                    T* x = reinterpret_cast<T*>(&kx[q]);
+#pragma unroll
+                                    for (int w = 0; w < kPairs; ++w)
+                                        rot_pair(x[2 * w], x[2 * w + 1], __ldg(trow + w));
+                                }
+                                st_stream(reinterpret_cast<V*>(dk_l + (size_t)drow[q] * p.row_elems) + c,
+                                          kx[q]);
+                            }
+                            if (pv && dv_l)
+                                st_stream(reinterpret_cast<V*>(dv_l + (size_t)drow[q] * p.row_elems) + c,
+                                          vx[q]);
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();                           // s_list / s_n reused
+    }
+}
+
+template <typename T>
+static int32_t launch_overlay_pass(const CollectParams& p, cudaStream_t s) {
+    auto kern = overlay_rows_kernel<T>;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
+    if (per_sm < 1) per_sm = 1;
+    const long long chunks = ((long long)p.n_jobs * p.num_layers * p.nb + kOvlChunk - 1) /
+                             kOvlChunk;
+    long long grid = (long long)sm_count() * per_sm;
+    if (grid > chunks) grid = chunks;
+    if (grid < 1) return TDKV_OK;
+    kern<<<(unsigned)grid, 256, 0, s>>>(p);
+    count_launch();
+    return check_launch("tdkv_restore_family: overlay pass");
 }
 
 }  // namespace tdkv
@@ -416,7 +581,9 @@ static int32_t collect_impl(const void* d_master_k, const void* d_master_v,
                             const uint8_t* d_unit_src, const void* const* h_src_k,
                             const void* const* h_src_v, int32_t n_src, bool pdl = false,
                             const int64_t* d_deltas = nullptr,
-                            const double* d_inv_freq = nullptr) {
+                            const double* d_inv_freq = nullptr, int64_t source_rows = 0,
+                            const tdkv_collect_overlay* d_overlay = nullptr,
+                            int32_t block_size = 0, int32_t nb = 0, int32_t n_jobs = 0) {
     if (n_units < 0 || num_layers <= 0 || num_heads <= 0 || head_dim <= 0 || (head_dim & 1))
         return set_error(TDKV_EINVAL, "tdkv_collect: bad geometry L=%d H=%d D=%d", num_layers,
                          num_heads, head_dim);
@@ -451,6 +618,11 @@ static int32_t collect_impl(const void* d_master_k, const void* d_master_v,
     p.deltas = d_deltas;
     p.inv_freq = d_inv_freq;
     p.fuse_table = (rotate && d_deltas && d_inv_freq) ? 1 : 0;
+    p.source_rows = source_rows;
+    p.ovl = d_overlay;
+    p.block_size = block_size;
+    p.nb = nb;
+    p.n_jobs = n_jobs;
     for (int i = 0; i < kMaxSources; ++i) {
         p.src_k[i] = i < n_src ? h_src_k[i] : nullptr;
         p.src_v[i] = i < n_src && h_src_v ? h_src_v[i] : nullptr;
@@ -474,6 +646,18 @@ static int32_t collect_impl(const void* d_master_k, const void* d_master_v,
         return set_error(TDKV_EINVAL, "tdkv_collect: master planes must be 4-byte aligned");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
 
+    if (d_overlay) {
+        // the family restore needs the TMA-staged, 16-byte form
+        if (!(bulk && ub == 16))
+            return set_error(TDKV_EINVAL, "tdkv_restore_family: masters, payloads and the pool "
+                             "must be 16-byte aligned with 16-byte rows");
+        const int32_t rc = dtype == TDKV_F32
+                               ? launch_collect<float, 16, true, true>(p, grid_limit, s, pdl)
+                               : launch_collect<__nv_bfloat16, 16, true, true>(p, grid_limit, s, pdl);
+        if (rc) return rc;
+        return dtype == TDKV_F32 ? launch_overlay_pass<float>(p, s)
+                                 : launch_overlay_pass<__nv_bfloat16>(p, s);
+    }
     if (dtype == TDKV_F32) {
         if (ub == 16)
             return bulk ? launch_collect<float, 16, true>(p, grid_limit, s, pdl)
@@ -567,4 +751,47 @@ extern "C" int32_t tdkv_collect_sources(const void* const* h_src_k, const void* 
                         d_dst_rows, d_table, rotate, d_dst_k, d_dst_v, dst_layer_stride,
                         num_layers, num_heads, head_dim, dtype, grid_limit, stream, d_unit_src,
                         h_src_k, h_src_v, n_src);
+}
+
+// Family restore: K1 writing every master-sourced (mirror, tile) + the
+// overlay pass writing the payload-sourced blocks (see tdkv.h).
+extern "C" int32_t tdkv_restore_family(const void* const* h_src_k, const void* const* h_src_v,
+                                       int32_t n_src, int64_t source_rows,
+                                       const tdkv_collect_unit* d_units, int32_t n_units,
+                                       int32_t max_rows, const tdkv_collect_job* d_jobs,
+                                       int32_t n_jobs, const int64_t* d_dst_rows,
+                                       const tdkv_collect_overlay* d_overlay, int32_t nb,
+                                       int32_t block_size,
+                                       const void* d_table, int32_t rotate, void* d_dst_k,
+                                       void* d_dst_v, int64_t dst_layer_stride,
+                                       int32_t num_layers, int32_t num_heads, int32_t head_dim,
+                                       int32_t dtype, int32_t grid_limit, void* stream) {
+    if (n_src <= 0 || n_src > kMaxSources || !h_src_k || source_rows <= 0)
+        return set_error(TDKV_EINVAL, "tdkv_restore_family: %d masters (1..%d) of %lld rows",
+                         n_src, kMaxSources, (long long)source_rows);
+    if (n_jobs < 0) return set_error(TDKV_EINVAL, "tdkv_restore_family: %d jobs", n_jobs);
+    if (n_jobs == 0 || n_units == 0) return TDKV_OK;
+    if (!d_overlay) return set_error(TDKV_EINVAL, "tdkv_restore_family: null overlay array");
+    if (block_size <= 0 || max_rows <= 0 || block_size % max_rows != 0)
+        return set_error(TDKV_EINVAL, "tdkv_restore_family: tiles of %d rows must divide the "
+                         "diff block size %d", max_rows, block_size);
+    if (nb != (int32_t)((source_rows + block_size - 1) / block_size))
+        return set_error(TDKV_EINVAL, "tdkv_restore_family: %d blocks per layer for %lld rows "
+                         "of block size %d", nb, (long long)source_rows, block_size);
+    if ((h_src_v == nullptr) != (d_dst_v == nullptr))
+        return set_error(TDKV_EINVAL, "tdkv_restore_family: null pointer");
+    for (int i = 0; i < n_src; ++i) {
+        if (!h_src_k[i] || (h_src_v && !h_src_v[i]))
+            return set_error(TDKV_EINVAL, "tdkv_restore_family: master %d is null", i);
+        if (!aligned(h_src_k[i], 16) || (h_src_v && !aligned(h_src_v[i], 16)))
+            return set_error(TDKV_EINVAL, "tdkv_restore_family: master %d not 16-byte aligned",
+                             i);
+    }
+    const void* const* src_v = h_src_v;
+    const int64_t mls = source_rows * (int64_t)num_heads * head_dim;   // each master's layer stride
+    return collect_impl(h_src_k[0], src_v ? src_v[0] : nullptr, mls, d_units,
+                        n_units, max_rows, d_jobs, d_dst_rows, d_table, rotate, d_dst_k, d_dst_v,
+                        dst_layer_stride, num_layers, num_heads, head_dim, dtype, grid_limit,
+                        stream, nullptr, h_src_k, src_v, n_src, false, nullptr, nullptr,
+                        source_rows, d_overlay, block_size, nb, n_jobs);
 }

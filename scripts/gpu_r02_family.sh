@@ -1,13 +1,11 @@
-# r02: GPU suite + family-order A/B for K2/K3 + DRAM bytes per launch (one GPU)
+# family restore (K1 + diff overlay): tests, codec numbers at C2/C3, C1 K1 ncu capture
 OUT=gpurun_out
 mkdir -p $OUT
-timeout 1500 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1; echo pytest=$?
-tail -5 $OUT/pytest_gpu.log
-for mode in family legacy; do
-  if [ $mode = legacy ]; then export TDKV_ENCODE_ORDER=pair TDKV_RESTORE_ORDER=job; fi
-  timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu --no-e2e > $OUT/bench_c2_$mode.json 2> $OUT/bench_c2_$mode.err; echo bench_$mode=$?
-  timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum \
-    --clock-control none -k regex:"diff_encode|rows_tma" -c 6 --csv --log-file $OUT/ncu_codec_$mode.csv \
-    python bench.py --steps 1 --warmup 1 --no-cpu --no-e2e > $OUT/ncu_codec_$mode.log 2>&1; echo ncu_$mode=$?
+timeout 900 python -m pytest tests/test_gpu_family_restore.py tests/test_gpu_bf16_codec.py tests/test_gpu_wire.py -x -q > $OUT/pytest_family.log 2>&1; echo pytest=$?
+tail -15 $OUT/pytest_family.log
+for c in c3 c2; do
+  for v in 1 0; do TDKV_RESTORE_FAMILY=$v timeout 600 python bench.py --config $c --no-cpu --no-e2e > $OUT/fam_${c}_$v.json 2> $OUT/fam_${c}_$v.err; echo "$c fam=$v"=$?; done
 done
-unset TDKV_ENCODE_ORDER TDKV_RESTORE_ORDER
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:collect_kernel -s 20 -c 1 -o $OUT/k1_c1 python bench.py --config c1 --steps 5 --warmup 3 --no-cpu --no-codec --no-e2e > $OUT/ncu_c1.log 2>&1; echo ncu_c1=$?
+for v in 1 0; do TDKV_RESTORE_FAMILY=$v timeout 300 python scripts/restore_ab.py > $OUT/restore_ab_$v.txt 2>&1; echo rab$v=$?; cat $OUT/restore_ab_$v.txt; done
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:collect_kernel -s 3 -c 1 -o $OUT/k1fam_c2 python scripts/restore_ab.py > $OUT/ncu_fam.log 2>&1; echo ncu_fam=$?

@@ -1,4 +1,5 @@
-"""A/B timing of the fused restore (K0 + K3) at the C2 codec-bench shape:
+"""A/B timing of the fused family restore at the C2 codec-bench shape
+(TDKV_RESTORE_FAMILY=1: K0 + K1 with the diff overlay; 0: K0 + K3):
 run once per library build (TDKV_LIBRARY=...), prints median GB/s of 15
 samples of 6 back-to-back 49-mirror family restores (diagnostic)."""
 import os
@@ -10,7 +11,9 @@ import torch
 sys.path.insert(0, ".")
 import paper_2604_03143_b200 as tk  # noqa: E402
 
-L, T, H, D, bs, P = 28, 4624, 4, 128, 32, 49
+# RESTORE_SHAPE=c3: the C3 codec family (one session: 24 mirrors of 717 tokens, L=48, H=8)
+L, T, H, D, bs, P = ((48, 717, 8, 128, 32, 24) if os.environ.get("RESTORE_SHAPE") == "c3"
+                     else (28, 4624, 4, 128, 32, 49))
 dev = torch.device("cuda:0")
 g = torch.Generator(device=dev).manual_seed(0)
 mk = torch.randn(L, T, H, D, generator=g, device=dev).bfloat16()
@@ -46,6 +49,19 @@ for _ in range(5):       # 6 back-to-back restores per sample: host prep overlap
     b.record()
     torch.cuda.synchronize()
     res.append(a.elapsed_time(b) * 1e-3 / 6)
+import time  # noqa: E402
+host = []
+for _ in range(7):       # host-side cost of one call (the GPU idle before it)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    tk.fused_restore_many(handles, spans, pool, maps, 10000.0)
+    host.append(time.perf_counter() - t0)
+torch.cuda.synchronize()
+print("host ms per call (submission, median of 7)", round(np.median(host) * 1e3, 4))
 dense = 2 * L * T * H * D * 2
+payload = sum(2 * sum(ld.indices.size for ld in d.layers) * bs * H * D * 2 for d in diffs)
+fam_bytes = dense + payload + P * dense
+print("family model GB/s median", round(fam_bytes / np.median(res) / 1e9, 1),
+      "ms", round(np.median(res) * 1e3, 4))
 print(os.environ.get("TDKV_LIBRARY", "in-tree"), "fused restore GB/s median",
       round(P * 2 * dense / np.median(res) / 1e9, 1), "best", round(P * 2 * dense / min(res) / 1e9, 1))

@@ -42,7 +42,8 @@ def test_descriptor_layouts_match_header():
                        ("tdkv_collect_unit", _lib.COLLECT_UNIT),
                        ("tdkv_diff_pair", _lib.DIFF_PAIR), ("tdkv_diff_out", _lib.DIFF_OUT),
                        ("tdkv_wire_seg", _lib.WIRE_SEG),
-                       ("tdkv_rows_job", _lib.ROWS_JOB)]:
+                       ("tdkv_rows_job", _lib.ROWS_JOB),
+                       ("tdkv_collect_overlay", _lib.COLLECT_OVERLAY)]:
         body = re.search(r"typedef struct \{([^{}]*)\}\s*" + struct + ";", text).group(1)
         # field count and total size (pointers / int64 = 8 B, int32 = 4 B)
         sizes = []
