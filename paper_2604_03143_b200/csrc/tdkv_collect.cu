@@ -99,15 +99,20 @@ constexpr int kJobGroup = 16;                      // capacity; groups are balan
 // jobs per group for a unit of nj jobs: the fewest groups of <= kJobGroup,
 // evenly filled (50 jobs -> 4 x 13, not 3 x 16 + 2)
 __device__ __forceinline__ int job_group_size(int nj) {
+    if (nj <= kJobGroup) return nj > 0 ? nj : 1;  // one group: no division
     const int groups = (nj + kJobGroup - 1) / kJobGroup;
-    return groups > 0 ? (nj + groups - 1) / groups : 1;
+    return (nj + groups - 1) / groups;
 }
 constexpr int kMaxTileRows = 32;
 
 // OVL: the family-restore instantiation (diff overlay); the collector's
 // instantiations compile it out, keeping their register count (and so four
-// resident CTAs per SM)
-template <typename T, int UB, bool BULK, bool OVL>
+// resident CTAs per SM).  FUSE: the fused-K0 instantiation for 16-byte units
+// (small rounds, where the instruction count per stored unit -- not HBM --
+// bounds the kernel): every job has one constant delta, its cos/sin row sits
+// in shared memory, and the scatter loop is the rotation, one 32-bit-indexed
+// address and the store.
+template <typename T, int UB, bool BULK, bool OVL, bool FUSE = false>
 __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) {
     using V = typename UnitBits<UB>::V;
     using Tbl = typename Elt<T>::Table;
@@ -130,6 +135,11 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
     const int tx = tid % tx_n;
     const int ty = tid / tx_n;
     const int n_items = p.n_units * p.num_layers;
+    // pair index of this thread's first unit (the usual single c = tx)
+    const int j0_tx = ((tx * kEpu) % p.head_dim) >> 1;
+    // log2(head_dim / 2) when a power of two (the fused table's index split)
+    const int half_shift = ((p.head_dim >> 1) & ((p.head_dim >> 1) - 1)) == 0
+                               ? __ffs(p.head_dim >> 1) - 1 : -1;
     const Tbl* __restrict__ table = static_cast<const Tbl*>(p.table);
     const int half = p.head_dim >> 1;
     const bool has_v = p.dv != nullptr;            // K-only collect (align_cached)
@@ -150,9 +160,7 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
 
     // item -> (layer, unit); units vary fastest so consecutive CTAs stream
     // neighbouring tiles of one layer plane
-    auto stage_src = [&](int item, const T*& gk, const T*& gv, tdkv_collect_unit& u) {
-        const int layer = item / p.n_units;
-        const int ui = item - layer * p.n_units;
+    auto stage_src = [&](int layer, int ui, const T*& gk, const T*& gv, tdkv_collect_unit& u) {
         u = p.units[ui];
         int64_t row0 = u.row0;
         const void* bk = p.mk;
@@ -175,13 +183,14 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
         const int gsz = job_group_size(u.job_end - u.job_begin);
         const int jbase = u.job_begin + g * gsz;
         const int ng = min(gsz, u.job_end - jbase);
-        const int cnt = ng * u.nrows;
-        for (int idx = tid; idx < cnt; idx += nthr) {
-            const int jj = idx / u.nrows;
-            const int r = idx - jj * u.nrows;
-            const tdkv_collect_job* jp = p.jobs + jbase + jj;
-            const int64_t off = jp->dst_off + (u.row0 - jp->seg_row0) + r;
-            cp_async_8(&s_drow[mb][jj * kMaxTileRows + r], p.dst_rows + off);
+        // one warp per job, one lane per tile row (kMaxTileRows == 32)
+        const int lane = tid & 31;
+        if (lane < u.nrows) {
+            for (int jj = tid >> 5; jj < ng; jj += nthr >> 5) {
+                const tdkv_collect_job* jp = p.jobs + jbase + jj;
+                const int64_t off = jp->dst_off + (u.row0 - jp->seg_row0) + lane;
+                cp_async_8(&s_drow[mb][jj * kMaxTileRows + lane], p.dst_rows + off);
+            }
         }
         if (tid < ng) {
             const tdkv_collect_job jb = p.jobs[jbase + tid];
@@ -219,11 +228,16 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
     };
 
     int item = blockIdx.x;
+    // item -> (layer, unit) tracked incrementally (items advance by gridDim.x)
+    int layer = item / p.n_units;
+    int ui = item - layer * p.n_units;
+    const int step_l = (int)gridDim.x / p.n_units;
+    const int step_u = (int)gridDim.x - step_l * p.n_units;
     if constexpr (BULK) {
         if (tid == 0 && item < n_items) {
             const T *gk, *gv;
             tdkv_collect_unit u;
-            stage_src(item, gk, gv, u);
+            stage_src(layer, ui, gk, gv, u);
             const uint32_t bytes = (uint32_t)u.nrows * row_bytes;
             mbar_arrive_expect_tx(&bars[0], (has_v ? 2 : 1) * bytes);
             bulk_g2s(smem, gk, bytes, &bars[0]);
@@ -239,9 +253,15 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
     for (int iter = 0; item < n_items; item += gridDim.x, ++iter) {
         const int b = iter & 1;
         uint8_t* buf = smem + (size_t)b * 2 * tile_bytes;
-        const int layer = item / p.n_units;
-        const tdkv_collect_unit u = p.units[item - layer * p.n_units];
+        const tdkv_collect_unit u = p.units[ui];
         stage_meta(u, layer, 0, 0);
+        const int cur_layer = layer, cur_ui = ui;
+        ui += step_u;
+        layer += step_l;
+        if (ui >= p.n_units) {
+            ui -= p.n_units;
+            ++layer;
+        }
 
         if constexpr (BULK) {
             const int next = item + gridDim.x;
@@ -251,7 +271,7 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
                 fence_proxy_async_smem();
                 const T *gk, *gv;
                 tdkv_collect_unit un;
-                stage_src(next, gk, gv, un);
+                stage_src(layer, ui, gk, gv, un);
                 const uint32_t bytes = (uint32_t)un.nrows * row_bytes;
                 uint8_t* nb = smem + (size_t)(b ^ 1) * 2 * tile_bytes;
                 mbar_arrive_expect_tx(&bars[b ^ 1], (has_v ? 2 : 1) * bytes);
@@ -262,7 +282,7 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
         } else {
             const T *gk, *gv;
             tdkv_collect_unit un;
-            stage_src(item, gk, gv, un);
+            stage_src(cur_layer, cur_ui, gk, gv, un);
             const int words = u.nrows * row_bytes / 4;
             const uint32_t* sk32 = reinterpret_cast<const uint32_t*>(gk);
             const uint32_t* sv32 = reinterpret_cast<const uint32_t*>(gv);
@@ -276,25 +296,27 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
 
         const V* sk = reinterpret_cast<const V*>(buf);
         const V* sv = reinterpret_cast<const V*>(buf + tile_bytes);
-        T* dk_l = static_cast<T*>(p.dk) + (size_t)layer * p.dls;
-        T* dv_l = static_cast<T*>(p.dv) + (size_t)layer * p.dls;
-        const int gsz = job_group_size(u.job_end - u.job_begin);
-        const int ngroups = (u.job_end - u.job_begin + gsz - 1) / gsz;
+        T* dk_l = static_cast<T*>(p.dk) + (size_t)cur_layer * p.dls;
+        T* dv_l = static_cast<T*>(p.dv) + (size_t)cur_layer * p.dls;
+        const int nj = u.job_end - u.job_begin;
+        const int gsz = job_group_size(nj);
+        const int ngroups = nj <= kJobGroup ? 1 : (nj + gsz - 1) / gsz;
 
         for (int g = 0; g < ngroups; ++g) {
             const int mb = g & 1;
             if (g + 1 < ngroups) {
-                stage_meta(u, layer, g + 1, mb ^ 1);
+                stage_meta(u, cur_layer, g + 1, mb ^ 1);
                 cp_async_wait<1>();
             } else {
                 cp_async_wait<0>();
             }
             __syncthreads();
             const int ng = min(gsz, u.job_end - u.job_begin - g * gsz);
-            if (fused && rotate) {
+            if (FUSE || (fused && rotate)) {
                 // this group's cos/sin rows (rope_table_kernel's arithmetic)
                 for (int idx = tid; idx < ng * half; idx += nthr) {
-                    const int jj = idx / half, j = idx - jj * half;
+                    const int jj = half_shift >= 0 ? idx >> half_shift : idx / half;
+                    const int j = idx - jj * half;
                     const double theta =
                         __dmul_rn((double)p.deltas[s_meta[mb][jj].x], p.inv_freq[j]);
                     double sn, cn;
@@ -329,9 +351,38 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
                     bulk_commit();
                 }
             }
-            if (ty < rows_per_pass) {
+            if constexpr (FUSE) {
+              if (ty < rows_per_pass) {
+                // constant delta per job, cos/sin rows in shared memory
+                const uint32_t upr32 = (uint32_t)upr;
                 for (int c = tx; c < upr; c += tx_n) {
-                    const int j0 = ((c * kEpu) % p.head_dim) >> 1;
+                    const int j0 = c == tx ? j0_tx : ((c * kEpu) % p.head_dim) >> 1;
+                    V* __restrict__ dkc = reinterpret_cast<V*>(dk_l) + c;
+                    V* __restrict__ dvc = reinterpret_cast<V*>(dv_l) + c;
+                    const V* skc = sk + c;
+                    const V* svc = sv + c;
+                    for (int jj = 0; jj < ng; ++jj) {
+                        Tbl cs[kPairs];
+                        const Tbl* trow = s_cs + jj * half + j0;
+#pragma unroll
+                        for (int q = 0; q < kPairs; ++q) cs[q] = trow[q];
+                        const int64_t* dr = &s_drow[mb][jj * kMaxTileRows];
+#pragma unroll 2
+                        for (int r = ty; r < u.nrows; r += rows_per_pass) {
+                            const size_t o = (size_t)(uint32_t)dr[r] * upr32;
+                            V kv = skc[r * upr];
+                            T* e = reinterpret_cast<T*>(&kv);
+#pragma unroll
+                            for (int q = 0; q < kPairs; ++q) rot_pair(e[2 * q], e[2 * q + 1], cs[q]);
+                            st_stream(dkc + o, kv);
+                            if (has_v && !v_tma) st_stream(dvc + o, svc[r * upr]);
+                        }
+                    }
+                }
+              }
+            } else if (ty < rows_per_pass) {
+                for (int c = tx; c < upr; c += tx_n) {
+                    const int j0 = c == tx ? j0_tx : ((c * kEpu) % p.head_dim) >> 1;
                     Tbl cs[kPairs], csn[kPairs];
                     int4 m = s_meta[mb][0];
                     if (rotate && m.y == 0) load_cs_job(cs, 0, m, j0);
@@ -345,7 +396,7 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
                         const bool ovv = OVL && s_map[mb][jj].y >= 0;
                         for (int r = ty; r < u.nrows && !(ovk && (ovv || v_tma || !has_v));
                              r += rows_per_pass) {
-                            const int64_t drow = dr[r];
+                            const size_t drow = (size_t)(uint32_t)dr[r];
                             V kv = sk[r * upr + c];
                             if (rotate) {
                                 if (m.y != 0) load_cs(cs, m.x + (m.z + r) * m.y, j0);
@@ -380,6 +431,9 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
 template <typename T, int UB, bool BULK, bool OVL = false>
 static int32_t launch_collect(const CollectParams& p, int grid_limit, cudaStream_t s, bool pdl) {
     auto kern = collect_kernel<T, UB, BULK, OVL>;
+    if constexpr (UB == 16 && BULK && !OVL) {
+        if (p.fuse_table) kern = collect_kernel<T, UB, BULK, OVL, true>;
+    }
     const int threads = 256;
     const size_t smem = (size_t)4 * p.max_rows * p.row_elems * sizeof(T) +
                         (p.fuse_table ? (size_t)kJobGroup * (p.head_dim / 2) *
@@ -596,6 +650,9 @@ static int32_t collect_impl(const void* d_master_k, const void* d_master_v,
         return set_error(TDKV_EINVAL, "tdkv_collect: null pointer");
     if (dtype != TDKV_F32 && dtype != TDKV_BF16)
         return set_error(TDKV_EUNSUPPORTED, "tdkv_collect: dtype %d", dtype);
+    // destination rows are indexed in 32 bits inside K1
+    if (dst_layer_stride / ((int64_t)num_heads * head_dim) > (int64_t)UINT32_MAX)
+        return set_error(TDKV_EINVAL, "tdkv_collect: destination planes of more than 2^32 rows");
 
     CollectParams p;
     p.mk = d_master_k;
