@@ -1,5 +1,4 @@
 # per-kernel device time of GPU collective_recover on configs[0] (run under gpurun)
-python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --print-units base --log-file gpurun_out/rec_launches.csv python scripts/recovery_profile.py > /dev/null 2>&1
 python - <<'PY'
 import csv, collections, re
