@@ -88,6 +88,7 @@ struct CollectParams {
     int32_t nb;                           // diff blocks per layer
     int32_t block_size;
     int32_t n_jobs;
+    int32_t ovl_inline;                   // OVL: K1's CTAs run the overlay pass after their items
 };
 
 // Per-job destination metadata is staged in shared memory in groups of
@@ -104,6 +105,120 @@ __device__ __forceinline__ int job_group_size(int nj) {
     return (nj + groups - 1) / groups;
 }
 constexpr int kMaxTileRows = 32;
+
+// Overlay pass of the family restore: the (job, layer, block)s whose rows
+// come from the job's diff payload (K1 skipped them), K rotated by the job's
+// table row(s), V copied, to the job's destination rows.  A CTA scans
+// kOvlChunk block-map entries, compacts the changed ones in shared memory and
+// moves them with all threads, kR rows per thread loaded before any is
+// stored (chunks small enough that even a 24-mirror family spreads its
+// changed blocks over every SM).  Run by K1's CTAs once their items are done
+// (CollectParams::ovl_inline: the overlay fills K1's tail, one launch), or
+// as its own kernel.
+constexpr int kOvlChunk = 32;
+template <typename T, int kR>
+__device__ __forceinline__ void overlay_rows(const CollectParams& p, long long chunk0,
+                                             long long chunk_step) {
+    using V = uint4;
+    using Tbl = typename Elt<T>::Table;
+    constexpr int kEpu = 16 / (int)sizeof(T);
+    constexpr int kPairs = kEpu / 2;
+    __shared__ int s_list[kOvlChunk];
+    __shared__ int s_n;
+    const int tid = threadIdx.x;
+    const int upr = p.row_elems * (int)sizeof(T) / 16;
+    const int tx_n = upr < 256 ? upr : 256;
+    const int rows_per_pass = 256 / tx_n;
+    const int tx = tid % tx_n, ty = tid / tx_n;
+    const Tbl* __restrict__ table = static_cast<const Tbl*>(p.table);
+    const int half = p.head_dim >> 1;
+    const long long n_entries = (long long)p.n_jobs * p.num_layers * p.nb;
+    const long long per_job = (long long)p.num_layers * p.nb;
+    // entry e = (job, layer, block), job-major
+    auto map_at = [&](long long e) {
+        const int job = (int)(e / per_job);
+        const long long lb = e - job * per_job;
+        const tdkv_collect_overlay o = p.ovl[job];
+        return make_int2(o.map_k ? __ldg(o.map_k + lb) : -1, o.map_v ? __ldg(o.map_v + lb) : -1);
+    };
+    for (long long e0 = chunk0 * kOvlChunk; e0 < n_entries; e0 += chunk_step * kOvlChunk) {
+        if (tid == 0) s_n = 0;
+        __syncthreads();
+        const long long e = e0 + tid;
+        if (tid < kOvlChunk && e < n_entries) {
+            const int2 m = map_at(e);
+            if (m.x >= 0 || m.y >= 0) s_list[atomicAdd(&s_n, 1)] = tid;
+        }
+        __syncthreads();
+        const int n = s_n;
+        for (int i = 0; i < n; ++i) {
+            const long long ei = e0 + s_list[i];
+            const int2 m = map_at(ei);
+            const int b = (int)(ei % p.nb);
+            const long long jl = ei / p.nb;
+            const int layer = (int)(jl % p.num_layers);
+            const int job = (int)(jl / p.num_layers);
+            const tdkv_collect_job jb = p.jobs[job];
+            const tdkv_collect_overlay o = p.ovl[job];
+            const int i0 = b * p.block_size;
+            const int nrows = (int)min((int64_t)p.block_size, p.source_rows - i0);
+            const V* pk = m.x >= 0 ? reinterpret_cast<const V*>(static_cast<const T*>(o.pay_k) +
+                                                                (size_t)m.x * p.block_size * p.row_elems)
+                                   : nullptr;
+            const V* pv = m.y >= 0 ? reinterpret_cast<const V*>(static_cast<const T*>(o.pay_v) +
+                                                                (size_t)m.y * p.block_size * p.row_elems)
+                                   : nullptr;
+            T* dk_l = static_cast<T*>(p.dk) + (size_t)layer * p.dls;
+            T* dv_l = p.dv ? static_cast<T*>(p.dv) + (size_t)layer * p.dls : nullptr;
+            const int64_t* drows = p.dst_rows + jb.dst_off + i0;
+            if (ty < rows_per_pass) {
+                for (int c = tx; c < upr; c += tx_n) {
+                    const int j0 = ((c * kEpu) % p.head_dim) >> 1;
+                    for (int r0 = ty; r0 < nrows; r0 += kR * rows_per_pass) {
+                        V kx[kR], vx[kR];
+                        int64_t drow[kR];
+#pragma unroll
+                        for (int q = 0; q < kR; ++q) {
+                            const int r = r0 + q * rows_per_pass;
+                            if (r < nrows) {
+                                drow[q] = __ldg(drows + r);
+                                if (pk) kx[q] = ld_stream(pk + (size_t)r * upr + c);
+                                if (pv) vx[q] = ld_stream(pv + (size_t)r * upr + c);
+                            }
+                        }
+#pragma unroll
+                        for (int q = 0; q < kR; ++q) {
+                            const int r = r0 + q * rows_per_pass;
+                            if (r >= nrows) continue;
+                            if (pk) {
+                                if (p.rotate) {
+                                    const Tbl* trow = table + (size_t)(jb.tbl_row +
+                                                                       (i0 + r) * jb.tbl_stride) *
+                                                                  half + j0;
+                                    T* x = reinterpret_cast<T*>(&kx[q]);
+#pragma unroll
+                                    for (int w = 0; w < kPairs; ++w)
+                                        rot_pair(x[2 * w], x[2 * w + 1], __ldg(trow + w));
+                                }
+                                st_stream(reinterpret_cast<V*>(dk_l + (size_t)drow[q] * p.row_elems) + c,
+                                          kx[q]);
+                            }
+                            if (pv && dv_l)
+                                st_stream(reinterpret_cast<V*>(dv_l + (size_t)drow[q] * p.row_elems) + c,
+                                          vx[q]);
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();                           // s_list / s_n reused
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) overlay_rows_kernel(const CollectParams p) {
+    overlay_rows<T, 4>(p, blockIdx.x, gridDim.x);
+}
 
 // OVL: the family-restore instantiation (diff overlay); the collector's
 // instantiations compile it out, keeping their register count (and so four
@@ -423,6 +538,11 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
             __syncthreads();
         }
     }
+    if constexpr (OVL) {
+        // payload-sourced (mirror, layer, block)s: disjoint from every row
+        // this kernel's items wrote, so no ordering against them is needed
+        if (p.ovl_inline) overlay_rows<T, 2>(p, blockIdx.x, gridDim.x);
+    }
     if constexpr (BULK) {
         if (v_tma && tid < kJobGroup) bulk_wait<0>();
     }
@@ -456,114 +576,6 @@ static int32_t launch_collect(const CollectParams& p, int grid_limit, cudaStream
         return check_launch("tdkv_collect: launch");
     count_launch();
     return check_launch("tdkv_collect");
-}
-
-// Overlay pass of the family restore: the (job, layer, block)s whose rows
-// come from the job's diff payload (K1 skipped them), K rotated by the job's
-// table row(s), V copied, to the job's destination rows.  A CTA scans
-// kOvlChunk block-map entries, compacts the changed ones in shared memory and
-// moves them with all threads, four rows per thread loaded before any is
-// stored (chunks small enough that even a 24-mirror family spreads its
-// changed blocks over every SM).
-constexpr int kOvlChunk = 32;
-template <typename T>
-__global__ void __launch_bounds__(256) overlay_rows_kernel(const CollectParams p) {
-    using V = uint4;
-    using Tbl = typename Elt<T>::Table;
-    constexpr int kEpu = 16 / (int)sizeof(T);
-    constexpr int kPairs = kEpu / 2;
-    constexpr int kR = 4;
-    __shared__ int s_list[kOvlChunk];
-    __shared__ int s_n;
-    const int tid = threadIdx.x;
-    const int upr = p.row_elems * (int)sizeof(T) / 16;
-    const int tx_n = upr < 256 ? upr : 256;
-    const int rows_per_pass = 256 / tx_n;
-    const int tx = tid % tx_n, ty = tid / tx_n;
-    const Tbl* __restrict__ table = static_cast<const Tbl*>(p.table);
-    const int half = p.head_dim >> 1;
-    const long long n_entries = (long long)p.n_jobs * p.num_layers * p.nb;
-    const long long per_job = (long long)p.num_layers * p.nb;
-    // entry e = (job, layer, block), job-major
-    auto map_at = [&](long long e) {
-        const int job = (int)(e / per_job);
-        const long long lb = e - job * per_job;
-        const tdkv_collect_overlay o = p.ovl[job];
-        return make_int2(o.map_k ? __ldg(o.map_k + lb) : -1, o.map_v ? __ldg(o.map_v + lb) : -1);
-    };
-    for (long long e0 = (long long)blockIdx.x * kOvlChunk; e0 < n_entries;
-         e0 += (long long)gridDim.x * kOvlChunk) {
-        if (tid == 0) s_n = 0;
-        __syncthreads();
-        const long long e = e0 + tid;
-        if (tid < kOvlChunk && e < n_entries) {
-            const int2 m = map_at(e);
-            if (m.x >= 0 || m.y >= 0) s_list[atomicAdd(&s_n, 1)] = tid;
-        }
-        __syncthreads();
-        const int n = s_n;
-        for (int i = 0; i < n; ++i) {
-            const long long ei = e0 + s_list[i];
-            const int2 m = map_at(ei);
-            const int b = (int)(ei % p.nb);
-            const long long jl = ei / p.nb;
-            const int layer = (int)(jl % p.num_layers);
-            const int job = (int)(jl / p.num_layers);
-            const tdkv_collect_job jb = p.jobs[job];
-            const tdkv_collect_overlay o = p.ovl[job];
-            const int i0 = b * p.block_size;
-            const int nrows = (int)min((int64_t)p.block_size, p.source_rows - i0);
-            const V* pk = m.x >= 0 ? reinterpret_cast<const V*>(static_cast<const T*>(o.pay_k) +
-                                                                (size_t)m.x * p.block_size * p.row_elems)
-                                   : nullptr;
-            const V* pv = m.y >= 0 ? reinterpret_cast<const V*>(static_cast<const T*>(o.pay_v) +
-                                                                (size_t)m.y * p.block_size * p.row_elems)
-                                   : nullptr;
-            T* dk_l = static_cast<T*>(p.dk) + (size_t)layer * p.dls;
-            T* dv_l = p.dv ? static_cast<T*>(p.dv) + (size_t)layer * p.dls : nullptr;
-            const int64_t* drows = p.dst_rows + jb.dst_off + i0;
-            if (ty < rows_per_pass) {
-                for (int c = tx; c < upr; c += tx_n) {
-                    const int j0 = ((c * kEpu) % p.head_dim) >> 1;
-                    for (int r0 = ty; r0 < nrows; r0 += kR * rows_per_pass) {
-                        V kx[kR], vx[kR];
-                        int64_t drow[kR];
-#pragma unroll
-                        for (int q = 0; q < kR; ++q) {
-                            const int r = r0 + q * rows_per_pass;
-                            if (r < nrows) {
-                                drow[q] = __ldg(drows + r);
-                                if (pk) kx[q] = ld_stream(pk + (size_t)r * upr + c);
-                                if (pv) vx[q] = ld_stream(pv + (size_t)r * upr + c);
-                            }
-                        }
-#pragma unroll
-                        for (int q = 0; q < kR; ++q) {
-                            const int r = r0 + q * rows_per_pass;
-                            if (r >= nrows) continue;
-                            if (pk) {
-                                if (p.rotate) {
-                                    const Tbl* trow = table + (size_t)(jb.tbl_row +
-                                                                       (i0 + r) * jb.tbl_stride) *
-                                                                  half + j0;
-                                    T* x = reinterpret_cast<T*>(&kx[q]);
-#pragma unroll
-                                    for (int w = 0; w < kPairs; ++w)
-                                        rot_pair(x[2 * w], x[2 * w + 1], __ldg(trow + w));
-                                }
-                                st_stream(reinterpret_cast<V*>(dk_l + (size_t)drow[q] * p.row_elems) + c,
-                                          kx[q]);
-                            }
-                            if (pv && dv_l)
-                                st_stream(reinterpret_cast<V*>(dv_l + (size_t)drow[q] * p.row_elems) + c,
-                                          vx[q]);
-                        }
-                    }
-                }
-            }
-        }
-        __syncthreads();                           // s_list / s_n reused
-    }
 }
 
 template <typename T>
@@ -655,6 +667,7 @@ static int32_t collect_impl(const void* d_master_k, const void* d_master_v,
         return set_error(TDKV_EINVAL, "tdkv_collect: destination planes of more than 2^32 rows");
 
     CollectParams p;
+    p.ovl_inline = 0;
     p.mk = d_master_k;
     p.mv = d_master_v;
     p.mls = master_layer_stride;
@@ -708,10 +721,15 @@ static int32_t collect_impl(const void* d_master_k, const void* d_master_v,
         if (!(bulk && ub == 16))
             return set_error(TDKV_EINVAL, "tdkv_restore_family: masters, payloads and the pool "
                              "must be 16-byte aligned with 16-byte rows");
+        static const bool separate = [] {
+            const char* e = getenv("TDKV_OVERLAY_SEPARATE");
+            return e && e[0] == '1';
+        }();
+        p.ovl_inline = separate ? 0 : 1;
         const int32_t rc = dtype == TDKV_F32
                                ? launch_collect<float, 16, true, true>(p, grid_limit, s, pdl)
                                : launch_collect<__nv_bfloat16, 16, true, true>(p, grid_limit, s, pdl);
-        if (rc) return rc;
+        if (rc || !separate) return rc;
         return dtype == TDKV_F32 ? launch_overlay_pass<float>(p, s)
                                  : launch_overlay_pass<__nv_bfloat16>(p, s);
     }
