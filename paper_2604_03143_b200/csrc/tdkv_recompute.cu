@@ -8,6 +8,7 @@
 //                  context, fresh rows overriding cached ones
 //   tdkv_gemm      h += mix @ Wm                       (tensor cores)
 #include "tdkv_common.cuh"
+#include "tdkv_umma.cuh"
 
 namespace tdkv {
 
@@ -680,6 +681,313 @@ static int32_t launch_attention_block(const float* d_q, const float* d_k_fresh,
     return check_launch("tdkv_attention_many");
 }
 
+
+// Tensor-core attention (rows_per_tile 128, head_dim 32 or 64): one CTA of
+// 256 threads serves 128 fixed rows of one member and one head.  Query row r
+// is TMEM lane r; warps w and w + 4 share that lane quadrant and split each
+// row's columns (keys of S, head dims of O) in halves.  Per 64-key tile:
+//   S = Q K^T    tcgen05.mma kind::tf32 as 3xTF32 (Q_hi K_hi + Q_hi K_lo +
+//                Q_lo K_hi: ~22 mantissa bits, float32 accumulation in TMEM)
+//   softmax      each thread's half score row from TMEM (tcgen05.ld), masked
+//                causally by sequence index, the row max exchanged with the
+//                partner thread, float32 exp as numpy; P written to shared
+//                memory split into tf32 hi / lo
+//   O = P V      3xTF32 again into a second TMEM accumulator (V staged
+//                transposed: the B operand is K-major over keys)
+//   acc          float32 per-row accumulators rescaled by the max correction
+// Operands sit in the canonical no-swizzle K-major core-matrix layout (8 rows
+// x 16 bytes per core matrix); key and value rows come from the fresh rows
+// when fresh_of[t] >= 0, else from the context planes.
+constexpr int kTcQ = 128;          // queries per CTA (TMEM lanes)
+constexpr int kTcK = 64;           // keys per tile
+constexpr int kTcThreads = 256;
+
+template <int D>
+struct TcAttnSmem {
+    static constexpr int kQ = kTcQ * D * 4;        // one tf32 plane of Q
+    static constexpr int kK = kTcK * D * 4;        // K tile
+    static constexpr int kV = D * kTcK * 4;        // V^T tile
+    static constexpr int kP = kTcQ * kTcK * 4;     // P tile
+    static constexpr int kBytes = 2 * (kQ + kK + kV + kP);
+};
+
+__device__ __forceinline__ void split_store16(uint8_t* hi, uint8_t* lo, uint32_t off, float4 v) {
+    uint4 h, l;
+    h.x = tf32_rna(v.x); l.x = tf32_rna(v.x - __uint_as_float(h.x));
+    h.y = tf32_rna(v.y); l.y = tf32_rna(v.y - __uint_as_float(h.y));
+    h.z = tf32_rna(v.z); l.z = tf32_rna(v.z - __uint_as_float(h.z));
+    h.w = tf32_rna(v.w); l.w = tf32_rna(v.w - __uint_as_float(h.w));
+    *reinterpret_cast<uint4*>(hi + off) = h;
+    *reinterpret_cast<uint4*>(lo + off) = l;
+}
+
+template <int N>
+__device__ __forceinline__ void tmem_row(uint32_t addr, float (&x)[N]) {
+    static_assert(N % 8 == 0, "8-column loads");
+#pragma unroll
+    for (int c0 = 0; c0 < N; c0 += 8) {
+        uint32_t r[8];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+              "=r"(r[6]), "=r"(r[7])
+            : "r"(addr + c0));
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[c0 + j] = __uint_as_float(r[j]);
+    }
+    tmem_ld_wait();
+}
+
+template <int D>
+__global__ void __launch_bounds__(kTcThreads, 1)
+    attention_tc_kernel(const float* __restrict__ q, const float* __restrict__ k_fresh,
+                        const float* __restrict__ v_fresh,
+                        const tdkv_attn_member* __restrict__ members, int n_members, int layer,
+                        int H, float scale, float* __restrict__ mix) {
+    using SM = TcAttnSmem<D>;
+    constexpr int kCq = D / 4;                     // 16-byte chunks per Q / K row
+    constexpr int kCp = kTcK / 4;                  // chunks per P / V^T row
+    constexpr int kSh = kTcK / 2;                  // S columns per thread
+    constexpr int kOh = D / 2;                     // O columns per thread
+    constexpr uint32_t kTmemCols = kTcK + D <= 128 ? 128 : 256;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* q_hi = smem;
+    uint8_t* q_lo = q_hi + SM::kQ;
+    uint8_t* k_hi = q_lo + SM::kQ;
+    uint8_t* k_lo = k_hi + SM::kK;
+    uint8_t* v_hi = k_lo + SM::kK;
+    uint8_t* v_lo = v_hi + SM::kV;
+    uint8_t* p_hi = v_lo + SM::kV;
+    uint8_t* p_lo = p_hi + SM::kP;
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ uint32_t s_tmem;
+    __shared__ float s_x[2][kTcQ];                 // partner exchange (row max, row sum)
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int row = tid & (kTcQ - 1);              // query row = TMEM lane
+    const int hf = tid >> 7;                       // which half of the columns
+    const int h = blockIdx.y;
+    int lo = 0, hi = n_members - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (members[mid].tile0 <= (int)blockIdx.x) lo = mid; else hi = mid - 1;
+    }
+    const tdkv_attn_member m = members[lo];
+    const int r0 = ((int)blockIdx.x - m.tile0) * kTcQ;
+    const int nq = min(kTcQ, m.n_rows - r0);
+    const int hid = H * D;
+    const size_t lofs = (size_t)layer * m.ctx_layer_stride;
+    const float* ctx_k = m.ctx_k + lofs;
+    const float* ctx_v = m.ctx_v + lofs;
+    const float* kf = k_fresh + (size_t)m.row0 * hid;
+    const float* vf = v_fresh + (size_t)m.row0 * hid;
+    const int tn = (int)m.fix_idx[r0 + nq - 1] + 1;        // keys any row of the tile sees
+    const int ntiles = (tn + kTcK - 1) / kTcK;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(&s_tmem)),
+                     "n"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+    }
+    // the query rows, split into tf32 hi / lo (each thread half a row)
+    const bool valid = row < nq;
+    const int tnq = valid ? (int)m.fix_idx[r0 + row] + 1 : 0;
+    {
+        const float* qrow = q + (size_t)(m.row0 + r0 + row) * hid + h * D;
+#pragma unroll
+        for (int c = hf * (kCq / 2); c < (hf + 1) * (kCq / 2); ++c) {
+            const float4 v = valid ? *reinterpret_cast<const float4*>(qrow + 4 * c)
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+            split_store16(q_hi, q_lo, core_off(row, c, kCq), v);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = s_tmem;
+    const uint32_t lane = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t t_s = tmem + lane + hf * kSh;             // S: columns [0, kTcK)
+    const uint32_t t_o = tmem + lane + kTcK + hf * kOh;      // O: columns [kTcK, kTcK + D)
+    const uint32_t idesc_s = umma_idesc(2, kTcQ, kTcK);
+    const uint32_t idesc_o = umma_idesc(2, kTcQ, D);
+
+    float acc[kOh];
+#pragma unroll
+    for (int d = 0; d < kOh; ++d) acc[d] = 0.f;
+    float mrun = -INFINITY;
+    float lrun = 0.f;                               // this half's share of the row sum
+    uint32_t phase = 0;
+
+    // K / V rows of a tile: eight consecutive threads take eight keys of one
+    // 16-byte column; tile it + 1 is loaded into registers while tile it is
+    // multiplied and softmaxed, then split and stored
+    constexpr int kPer = kTcK * kCq / kTcThreads;          // chunks per thread
+    float4 kreg[kPer], vreg[kPer];
+    auto load_tile = [&](int it) {
+        const int t0 = it * kTcK;
+        const int n = min(kTcK, tn - t0);
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+            const int idx = tid + i * kTcThreads;
+            const int key = (idx & 7) + ((idx / (8 * kCq)) << 3);
+            const int c = (idx >> 3) % kCq;
+            kreg[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            vreg[i] = kreg[i];
+            if (key < n) {
+                const int t = t0 + key;
+                const int fr = __ldg(m.fresh_of + t);
+                const size_t off = (size_t)h * D + 4 * c;
+                kreg[i] = *reinterpret_cast<const float4*>(
+                    (fr >= 0 ? kf + (size_t)fr * hid : ctx_k + (size_t)t * hid) + off);
+                vreg[i] = *reinterpret_cast<const float4*>(
+                    (fr >= 0 ? vf + (size_t)fr * hid : ctx_v + (size_t)t * hid) + off);
+            }
+        }
+    };
+    load_tile(0);
+
+    for (int it = 0; it < ntiles; ++it) {
+        const int t0 = it * kTcK;
+        const int n = min(kTcK, tn - t0);
+        // ---- store K (rows = keys) and V^T (rows = head dims), tf32 hi / lo
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+            const int idx = tid + i * kTcThreads;
+            const int key = (idx & 7) + ((idx / (8 * kCq)) << 3);
+            const int c = (idx >> 3) % kCq;
+            split_store16(k_hi, k_lo, core_off(key, c, kCq), kreg[i]);
+            const float vx[4] = {vreg[i].x, vreg[i].y, vreg[i].z, vreg[i].w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t o = core_off(4 * c + j, key >> 2, kCp) + (key & 3) * 4;
+                const uint32_t hb = tf32_rna(vx[j]);
+                *reinterpret_cast<uint32_t*>(v_hi + o) = hb;
+                *reinterpret_cast<uint32_t*>(v_lo + o) = tf32_rna(vx[j] - __uint_as_float(hb));
+            }
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        if (tid == 0) {
+            tc_fence_after();
+#pragma unroll
+            for (int s = 0; s < D / 8; ++s) {
+                const uint32_t koff = s * 256;
+                const uint64_t dqh = umma_desc(smem_u32(q_hi) + koff, 128, kCq * 128);
+                const uint64_t dql = umma_desc(smem_u32(q_lo) + koff, 128, kCq * 128);
+                const uint64_t dkh = umma_desc(smem_u32(k_hi) + koff, 128, kCq * 128);
+                const uint64_t dkl = umma_desc(smem_u32(k_lo) + koff, 128, kCq * 128);
+                umma<true>(tmem, dqh, dkh, idesc_s, s > 0 ? 1u : 0u);
+                umma<true>(tmem, dqh, dkl, idesc_s, 1u);
+                umma<true>(tmem, dql, dkh, idesc_s, 1u);
+            }
+            umma_commit(&bar);
+        }
+        if (it + 1 < ntiles) load_tile(it + 1);     // in flight over the softmax
+        mbar_wait(&bar, phase);
+        phase ^= 1;
+        tc_fence_after();
+        // ---- this half of the score row -> P (online softmax)
+        float x[kSh];
+        tmem_row<kSh>(t_s, x);
+        float tmax = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < kSh; ++j) {
+            const int key = hf * kSh + j;
+            x[j] = (key < n && t0 + key < tnq) ? x[j] * scale : -INFINITY;
+            tmax = fmaxf(tmax, x[j]);
+        }
+        s_x[hf][row] = tmax;
+        __syncthreads();
+        const float mnew = fmaxf(mrun, fmaxf(tmax, s_x[hf ^ 1][row]));
+        const float corr = (mrun == -INFINITY || mnew == -INFINITY) ? 1.f : expf(mrun - mnew);
+        float psum = 0.f;
+#pragma unroll
+        for (int j = 0; j < kSh; ++j) {
+            x[j] = x[j] == -INFINITY ? 0.f : expf(x[j] - mnew);
+            psum += x[j];
+        }
+        lrun = lrun * corr + psum;
+        mrun = mnew;
+#pragma unroll
+        for (int c = 0; c < kCp / 2; ++c)
+            split_store16(p_hi, p_lo, core_off(row, hf * (kCp / 2) + c, kCp),
+                          make_float4(x[4 * c], x[4 * c + 1], x[4 * c + 2], x[4 * c + 3]));
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        if (tid == 0) {
+            tc_fence_after();
+#pragma unroll
+            for (int s = 0; s < kTcK / 8; ++s) {
+                const uint32_t koff = s * 256;
+                const uint64_t dph = umma_desc(smem_u32(p_hi) + koff, 128, kCp * 128);
+                const uint64_t dpl = umma_desc(smem_u32(p_lo) + koff, 128, kCp * 128);
+                const uint64_t dvh = umma_desc(smem_u32(v_hi) + koff, 128, kCp * 128);
+                const uint64_t dvl = umma_desc(smem_u32(v_lo) + koff, 128, kCp * 128);
+                umma<true>(tmem + kTcK, dph, dvh, idesc_o, s > 0 ? 1u : 0u);
+                umma<true>(tmem + kTcK, dph, dvl, idesc_o, 1u);
+                umma<true>(tmem + kTcK, dpl, dvh, idesc_o, 1u);
+            }
+            umma_commit(&bar);
+        }
+        mbar_wait(&bar, phase);
+        phase ^= 1;
+        tc_fence_after();
+        {
+            float o[kOh];
+            tmem_row<kOh>(t_o, o);
+#pragma unroll
+            for (int d = 0; d < kOh; ++d) acc[d] = fmaf(acc[d], corr, o[d]);
+        }
+        // K / V / P shared memory and both accumulators are reused next tile
+        tc_fence_before();
+        __syncthreads();
+        tc_fence_after();
+    }
+    s_x[hf][row] = lrun;
+    __syncthreads();
+    if (valid) {
+        const float l = s_x[0][row] + s_x[1][row];
+        float* out = mix + (size_t)(m.row0 + r0 + row) * hid + h * D + hf * kOh;
+#pragma unroll
+        for (int c = 0; c < kOh / 4; ++c)
+            *reinterpret_cast<float4*>(out + 4 * c) =
+                make_float4(acc[4 * c] / l, acc[4 * c + 1] / l, acc[4 * c + 2] / l,
+                            acc[4 * c + 3] / l);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "n"(kTmemCols)
+                     : "memory");
+    }
+}
+
+template <int D>
+static int32_t launch_attention_tc(const float* d_q, const float* d_k_fresh,
+                                   const float* d_v_fresh, const tdkv_attn_member* d_members,
+                                   int32_t n_members, int32_t layer, int32_t n_tiles,
+                                   int32_t num_heads, float scale, float* d_mix, cudaStream_t s) {
+    auto kern = attention_tc_kernel<D>;
+    const size_t smem = TcAttnSmem<D>::kBytes;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return check_launch("tdkv_attention_many: cudaFuncSetAttribute");
+    kern<<<dim3(n_tiles, num_heads), kTcThreads, smem, s>>>(d_q, d_k_fresh, d_v_fresh, d_members,
+                                                     n_members, layer, num_heads, scale, d_mix);
+    count_launch();
+    return check_launch("tdkv_attention_many");
+}
+
 }  // namespace tdkv
 
 using namespace tdkv;
@@ -737,6 +1045,16 @@ extern "C" int32_t tdkv_attention_many(const float* d_q, const float* d_k_fresh,
     if (n_members == 0 || total_rows == 0) return TDKV_OK;
     if (!d_q || !d_k_fresh || !d_v_fresh || !d_members || !d_mix)
         return set_error(TDKV_EINVAL, "tdkv_attention_many: null pointer");
+    if (n_tiles > 0 && rows_per_tile == kTcQ) {
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        switch (head_dim) {
+            case 32: return launch_attention_tc<32>(d_q, d_k_fresh, d_v_fresh, d_members, n_members, layer, n_tiles, num_heads, scale, d_mix, s);
+            case 64: return launch_attention_tc<64>(d_q, d_k_fresh, d_v_fresh, d_members, n_members, layer, n_tiles, num_heads, scale, d_mix, s);
+            default:
+                return set_error(TDKV_EINVAL, "tdkv_attention_many: 128-row tensor-core tiles "
+                                 "need head_dim 32 or 64, got %d", head_dim);
+        }
+    }
     if (n_tiles > 0 && rows_per_tile == kBlkQ) {
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         switch (head_dim) {

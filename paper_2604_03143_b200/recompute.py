@@ -141,10 +141,18 @@ _ATTN_ONLINE = os.environ.get("TDKV_ATTN_ONLINE", "1") != "0"
 _ATTN_BLOCK = os.environ.get("TDKV_ATTN_BLOCK", "1") != "0"
 
 
+# TDKV_ATTN_TC=0 keeps the CUDA-core kernels for head dims the tensor-core
+# attention serves
+_ATTN_TC = os.environ.get("TDKV_ATTN_TC", "1") != "0"
+
+
 def _attn_rows_per_tile(head_dim: int) -> int:
-    """Fixed rows per CTA of the query-tiled attention: 64 with the
-    register-blocked kernel (head_dim 8, 16, 32, 64 or 128), else 16 with the
-    online softmax (head_dim <= 128), else 8."""
+    """Fixed rows per CTA of the query-tiled attention: 128 with the
+    tensor-core kernel (head_dim 32 or 64: tcgen05 3xTF32 for Q K^T and P V),
+    64 with the register-blocked kernel (head_dim 8, 16, 32, 64 or 128), else
+    16 with the online softmax (head_dim <= 128), else 8."""
+    if _ATTN_TC and _ATTN_ONLINE and head_dim in (32, 64):
+        return 128
     if _ATTN_BLOCK and _ATTN_ONLINE and head_dim in (8, 16, 32, 64, 128):
         return 64
     return 16 if _ATTN_ONLINE and head_dim <= 128 else 8
