@@ -211,10 +211,16 @@ def fused_restore_many(mirrors: Sequence[MirrorHandle], spans: Sequence[Position
         return 2
     recs, deltas, tbl_row = [], [], 0
     max_t, L, H, D = 0, pool.num_layers, pool.num_heads, pool.head_dim
+    # host masters are uploaded once per master and the device planes kept
+    # alive until the launch: the descriptors hold raw addresses, and a plane
+    # freed inside this loop would be reused by the next master's upload
+    planes = {}
     for mirror, span, smap in zip(mirrors, spans, slot_maps):
         kv = mirror.master.kv
         T = kv.num_tokens
-        mk, mv = _master_planes(mirror, pool)
+        if id(kv) not in planes:
+            planes[id(kv)] = (kv, _master_planes(mirror, pool))
+        mk, mv = planes[id(kv)][1]
         dd = mirror.diff.device_form(pool.device, pool.dtype)
         rows, stride, rotate = _delta_rows(span.delta)
         recs.append(_kernels.rows_job(mk, mv, T * H * D, pool.k, pool.v, pool.layer_stride, T,

@@ -218,3 +218,38 @@ def test_family_restore_ledger_and_marks_match_k3(monkeypatch):
     assert got[0][0] == got[1][0]
     for (ka, va), (kb, vb) in zip(got[0][1], got[1][1]):
         assert np.array_equal(ka, kb) and np.array_equal(va, vb)
+
+
+def test_k3_batch_of_host_masters_keeps_every_master(monkeypatch):
+    """The per-mirror K3 form over mirrors of several HOST masters (fewer
+    than _FAMILY_MIN mirrors per master): each master is uploaded once and
+    stays alive until the launch -- descriptors hold raw addresses, so a
+    master's device copy freed and reused by the next master's upload before
+    the kernel ran would restore the wrong master (families interleaved
+    A, B, A, C, B, ... to make every alias visible)."""
+    monkeypatch.setattr(rs, "_FAMILY_K1", False)
+    L, T, H, D, bs = 2, 96, 4, 128, 16
+    rng = np.random.default_rng(11)
+    fams = []
+    for f in range(3):
+        mk, mv, mirrors, hints = _family_host(rng, L, T, H, D, 2, bs)
+        pos = np.arange(T, dtype=np.int64)
+        entry = tk.MasterEntry(f, tk.LayeredKv(mk, mv, pos), pin_count=2)
+        for (k, v), h in zip(mirrors, hints):
+            d = tk.encode_diff(entry.kv, tk.LayeredKv(k, v, pos), h, tk.CacheBlockConfig(bs))
+            fams.append((entry, d, k, v))
+    order = [0, 2, 4, 1, 3, 5]              # families 0, 1, 2, 0, 1, 2
+    handles = [tk.MirrorHandle(fams[i][0].family_id, 10 + i, fams[i][0], fams[i][1])
+               for i in order]
+    pool = _pool_f32(8 * T, L, H, D)
+    maps = [pool.allocate(T, i) for i in range(len(order))]
+    spans = [tk.PositionSpan.shifted(np.arange(T, dtype=np.int64), 5 + j)
+             for j in range(len(order))]
+    tk.fused_restore_many(handles, spans, pool, maps, 10000.0)
+    torch.cuda.synchronize()
+    for j, i in enumerate(order):
+        _, _, k, v = fams[i]
+        gk, gv = _read(pool, maps[j])
+        assert np.array_equal(gv, v), f"mirror {j}: V"
+        want = np.stack([ref.rope_apply(k[layer], np.full(T, 5 + j)) for layer in range(L)])
+        assert np.array_equal(gk, want), f"mirror {j}: K"
