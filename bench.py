@@ -370,10 +370,35 @@ def run_tdkv(args):
 
     stream = torch.cuda.current_stream(dev)
 
+    # a round whose working set (masters read + pool rows written) would stay
+    # resident in the 126 MB L2 across steps (C1) rotates over R independent
+    # copies of the round (own arena, pool and plan; R x working set > 2 x
+    # L2): every step's inputs were evicted by the R - 1 rounds before it,
+    # and steps run back to back like a serving loop
+    l2_size = int(getattr(torch.cuda.get_device_properties(dev), "L2_cache_size", 0) or 0)
+    l2_size = l2_size or 126 * 2**20
+    working_set = spec.master_bytes + step_bytes
+    rotation = [(collector, plans)]
+    if working_set < 2 * l2_size and world == 1 and peer is None:
+        for _ in range(-(-2 * l2_size // working_set)):
+            arena_r = rounds.make_arena(spec, arena.k.clone(), arena.v.clone())
+            pool_r = tk.PagedPool(sb * T, L, H, D, dtype=dt, device=dev, debug=False)
+            maps_r = [pool_r.allocate(T, a) for a in batches[0]]
+            col_r = tk.KVCollector(arena_r, pool_r)
+            rotation.append((col_r, [col_r.plan([j for a, m in zip(b, maps_r)
+                                                 for j in rounds.agent_jobs(spec, a, m.slots)])
+                                     for b in batches]))
+    rot_i = [0]
+
     def round_step(events=None):
         if events is not None:
             events[0].record(stream)
-        if peer is not None:
+        if len(rotation) > 1:
+            col_r, plans_r = rotation[rot_i[0] % len(rotation)]
+            rot_i[0] += 1
+            for p in plans_r:
+                col_r.collect(p)
+        elif peer is not None:
             # device-side round barriers around the peer-read collect
             peer.ready()
             for p in plans:
@@ -410,28 +435,14 @@ def run_tdkv(args):
     total_agents = int(reduce_over_ranks(float(n_local), dist.ReduceOp.SUM if world > 1 else None))
 
     # -- device-timed rounds ------------------------------------------------
-    # a round whose working set (masters read + pool rows written) would stay
-    # resident in the 126 MB L2 across steps (C1) is timed cold: a buffer of
-    # twice the L2 size is written between timed rounds, outside the events
-    l2_size = int(getattr(torch.cuda.get_device_properties(dev), "L2_cache_size", 0) or 0)
-    l2_size = l2_size or 126 * 2**20
-    working_set = spec.master_bytes + step_bytes
-    flush_buf = (torch.empty(2 * l2_size, dtype=torch.uint8, device=dev)
-                 if working_set < 2 * l2_size else None)
-
-    def flush_l2():
-        if flush_buf is not None:
-            flush_buf.fill_(1)
-
-    for _ in range(args.warmup):
-        flush_l2()
+    for _ in range(args.warmup * len(rotation)):
         round_step()
     barrier()
     # per-step events bracket K1 when a step has more than the round's kernels
-    # (N>1: the exchange) or when L2 is flushed between rounds; otherwise at
-    # N=1 a step IS the round (K0 + K1, or K1 alone with the fused table) and
-    # the step time is K1's, without the per-step event records' host cost
-    per_step = world > 1 or flush_buf is not None
+    # (N>1: the exchange); otherwise at N=1 a step IS the round (K0 + K1, or
+    # K1 alone with the fused table) and the step time is K1's, without the
+    # per-step event records' host cost
+    per_step = world > 1
     k1_events = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                  for _ in range(args.steps)] if per_step else [None] * args.steps
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -441,21 +452,38 @@ def run_tdkv(args):
         barrier()
         start.record(stream)
         for i in range(args.steps):
-            flush_l2()
             round_step(k1_events[i])
         stop.record(stream)
         barrier()
     launches = tk.launch_count() - launches0
-    if flush_buf is not None:
-        # the rounds alone: the flushes between them are not part of a step
-        elapsed_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in k1_events))
-    else:
-        elapsed_ms = max_over_ranks(start.elapsed_time(stop))
+    elapsed_ms = max_over_ranks(start.elapsed_time(stop))
     ms_step = elapsed_ms / args.steps
     k1_ms = (sum(a.elapsed_time(b) for a, b in k1_events) / args.steps if per_step
              else start.elapsed_time(stop) / args.steps)
     value = total_bytes / (ms_step * 1e-3) / 1e9
     agents_per_s = total_agents / (ms_step * 1e-3)
+
+    # the same round timed cold and alone (rotating rounds only): a 2 x L2
+    # buffer written before each round, CUDA events around the round
+    cold = None
+    if len(rotation) > 1:
+        flush_buf = torch.empty(2 * l2_size, dtype=torch.uint8, device=dev)
+        cev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        for i in range(args.steps + args.warmup):
+            flush_buf.fill_(1)
+            if i >= args.warmup:
+                cev[i - args.warmup][0].record(stream)
+            round_step()
+            if i >= args.warmup:
+                cev[i - args.warmup][1].record(stream)
+        torch.cuda.synchronize(dev)
+        c_ms = sum(a.elapsed_time(b) for a, b in cev) / args.steps
+        del flush_buf
+        cold = {"ms_per_round": round(c_ms, 5),
+                "value": round(step_bytes / (c_ms * 1e-3) / 1e9, 1), "unit": "GB/s",
+                "note": "each round alone after a 2 x L2 buffer write (dirty L2, idle GPU, "
+                        "launch ramp and tail inside the events)"}
 
     # the exchange alone (N>1): NVLink receive roofline of the busiest rank
     exchange = None
@@ -519,9 +547,11 @@ def run_tdkv(args):
                    "tokens_per_agent": T, "parallelism": f"agent-shard x{world}",
                    "exchange": (None if world == 1 else
                                 "p2p" if peer is not None else "nccl"),
-                   "l2": (f"L2 flushed between timed rounds ({2 * l2_size / 2**20:.0f} MiB "
-                          "buffer written outside the per-round events; working set "
-                          f"{working_set / 2**20:.0f} MiB < 2 x L2)" if flush_buf is not None
+                   "l2": (f"inputs larger than L2: steps rotate over {len(rotation)} "
+                          "independent copies of the round (arena, pool, plan), "
+                          f"{len(rotation) * working_set / 2**20:.0f} MiB in all vs "
+                          f"{l2_size / 2**20:.0f} MiB of L2, so no step's data is "
+                          "L2-resident when it starts" if len(rotation) > 1
                           else "inputs larger than L2 (master arena "
                           f"{spec.master_bytes / 2**20:.0f} MiB read, "
                           f"{step_bytes / 1e9:.1f} GB moved per GPU per step)")},
@@ -536,6 +566,9 @@ def run_tdkv(args):
         "gpu_launches": launches,
         "clocks": sampler.summary(),
     }
+    if cold is not None:
+        cold["frac"] = round(cold["value"] / peak, 4)
+        line["cold_round"] = cold
     if exchange is not None:
         line["exchange"] = exchange
     if line_family is not None:
@@ -543,33 +576,24 @@ def run_tdkv(args):
 
     # -- the same rounds replayed from a captured CUDA graph (N=1) -----------
     if world == 1 and len(plans) == 1 and not args.profile:
-        graph = collector.capture(plan)
+        graphs = [col_r.capture(plans_r[0]) for col_r, plans_r in rotation]
         for _ in range(args.warmup):
-            graph.replay()
+            for g in graphs:
+                g.replay()
         torch.cuda.synchronize(dev)
-        if flush_buf is not None:
-            gev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                   for _ in range(args.steps)]
-            for a, b in gev:
-                flush_l2()
-                a.record(stream)
-                graph.replay()
-                b.record(stream)
-            torch.cuda.synchronize(dev)
-            g_ms = sum(a.elapsed_time(b) for a, b in gev) / args.steps
-        else:
-            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            g0.record(stream)
-            for _ in range(args.steps):
-                graph.replay()
-            g1.record(stream)
-            torch.cuda.synchronize(dev)
-            g_ms = g0.elapsed_time(g1) / args.steps
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for i in range(args.steps):
+            graphs[i % len(graphs)].replay()
+        g1.record(stream)
+        torch.cuda.synchronize(dev)
+        g_ms = g0.elapsed_time(g1) / args.steps
+        graph = graphs[0]
         line["graph"] = {"value": round(step_bytes / (g_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
                          "ms_per_step": round(g_ms, 4), "kernels_per_replay": graph.kernels,
                          "note": "KVCollector.capture(plan): the round (K0 + K1) as one CUDA "
                                  "graph, replayed; not counted in gpu_launches"}
-        del graph
+        del graph, graphs
 
     # -- e2e: public API with host buffers ---------------------------------
     if len(batches) > 1 and not args.no_e2e:
