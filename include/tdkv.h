@@ -376,7 +376,11 @@ int32_t tdkv_attention(const float* d_q, const float* d_k_fresh, const float* d_
  * (running max / sum, float64 accumulators rescaled per 32-token tile);
  * rows_per_tile 64 (head_dim 8, 16, 32, 64 or 128): register-blocked, 256
  * threads per CTA, 64-token key/value tiles double-buffered by 16-byte async
- * copies, 4x4 score blocks, float32 P.V sums per tile folded into float64.
+ * copies, 4x4 score blocks, float32 P.V sums per tile folded into float64;
+ * rows_per_tile 128 (head_dim 32 or 64): tensor cores, 256 threads per CTA,
+ * the tile's rows in TMEM lanes, S = Q K^T and O = P V per 64-key tile as
+ * tcgen05.mma kind::tf32 in 3xTF32 (hi/lo split operands), online softmax in
+ * float32 with the running max shared by the two threads of a row.
  * n_tiles == 0 runs one CTA per row. */
 typedef struct {
     const float* ctx_k;          /* (L, num_tokens, H*D) context planes */
