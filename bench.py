@@ -923,6 +923,25 @@ def recompute_bench(dev, args):
         out[f"gemm_{name}"] = {"shape": [M, N, K], "ms": round(t * 1e3, 4),
                                "tflops": round(tflops, 1),
                                "frac_of_bf16_peak": round(tflops / bf16_peak, 4)}
+        if dt == torch.float32:
+            # 3xTF32 over pre-split operands: the weights (B) split once, the
+            # activations (A) split per GEMM -- the split is inside the timing
+            bs = gemm.tf32_split(b)
+            asp = (torch.empty_like(a), torch.empty_like(a))
+            gemm.tf32_split(a, out=asp)
+            gemm.gemm_tf32x3(asp, bs, out=c)
+            e0.record()
+            for _ in range(rounds_):
+                gemm.tf32_split(a, out=asp)
+                gemm.gemm_tf32x3(asp, bs, out=c)
+            e1.record()
+            torch.cuda.synchronize(dev)
+            t = e0.elapsed_time(e1) * 1e-3 / rounds_
+            tflops = 2.0 * M * N * K / t / 1e12
+            out["gemm_tf32x3_presplit"] = {
+                "shape": [M, N, K], "ms": round(t * 1e3, 4), "tflops": round(tflops, 1),
+                "frac_of_bf16_peak": round(tflops / bf16_peak, 4),
+                "note": "tdkv_tf32_split of A + tdkv_gemm_tf32x3 (B split once, like weights)"}
     # toy-model refresh of a C1-shaped round (L=2, H=8, D=64), 8 agents;
     # synthetic weights from the product's generator, handed to the oracle
     # only for its CPU timing leg

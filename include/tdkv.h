@@ -346,6 +346,19 @@ int32_t tdkv_gemm(const void* d_a, int32_t lda, const void* d_b, int32_t ldb,
                   float* d_c, int32_t ldc, int32_t m, int32_t n, int32_t k,
                   int32_t dtype, int32_t accumulate, void* stream);
 
+/* 3xTF32 with the split done once, outside the GEMM: tdkv_tf32_split writes
+ * the tf32 hi (cvt.rna of x) and lo (cvt.rna of x - hi) planes of n floats
+ * (n % 4 == 0, 16-byte aligned); tdkv_gemm_tf32x3 is tdkv_gemm for TDKV_F32
+ * with A and B given as such planes (same lda / ldb) -- a pure TMA ->
+ * tcgen05 pipeline (A_hi B_hi + A_hi B_lo + A_lo B_hi per k-step) with no
+ * in-kernel split; the selective recompute splits its weights once and its
+ * activations per GEMM. */
+int32_t tdkv_tf32_split(const float* d_src, int64_t n, float* d_hi, float* d_lo, void* stream);
+int32_t tdkv_gemm_tf32x3(const float* d_a_hi, const float* d_a_lo, int32_t lda,
+                         const float* d_b_hi, const float* d_b_lo, int32_t ldb,
+                         float* d_c, int32_t ldc, int32_t m, int32_t n, int32_t k,
+                         int32_t accumulate, void* stream);
+
 /* K5 non-GEMM stages of one layer of the selective forward (float32 toy
  * model, toymodel.py:111-150):
  *   tdkv_qkv_rope: qkv (n_rows, 3*H*D) -> q, k rotated by the row's cos/sin

@@ -101,7 +101,8 @@ assert DIFF_PAIR.itemsize == 32 and DIFF_OUT.itemsize == 40 and ROWS_JOB.itemsiz
 EXPORTS = (
     "tdkv_version", "tdkv_last_error", "tdkv_launch_count", "tdkv_rope_table",
     "tdkv_collect", "tdkv_collect_round", "tdkv_collect_sources", "tdkv_restore_family", "tdkv_diff_compare", "tdkv_diff_compact", "tdkv_diff_encode", "tdkv_rows",
-    "tdkv_keydiff", "tdkv_select_important", "tdkv_gemm", "tdkv_qkv_rope", "tdkv_attention",
+    "tdkv_keydiff", "tdkv_select_important", "tdkv_gemm", "tdkv_tf32_split", "tdkv_gemm_tf32x3",
+    "tdkv_qkv_rope", "tdkv_attention",
     "tdkv_attention_many",
     "tdkv_fill_rows", "tdkv_alloc_create", "tdkv_alloc_destroy", "tdkv_alloc_free_count",
     "tdkv_alloc_take", "tdkv_alloc_release", "tdkv_wire_pack", "tdkv_wire_unpack",
@@ -139,6 +140,8 @@ _SIGS = {
     "tdkv_keydiff": (_I32, [_P, _P, _P, _I64, _I32, _I32, _P, _P]),
     "tdkv_select_important": (_I32, [_P, _P, _P, _P, _I32, _I32, _P, _P, _P, _P]),
     "tdkv_gemm": (_I32, [_P, _I32, _P, _I32, _P, _I32, _I32, _I32, _I32, _I32, _I32, _P]),
+    "tdkv_tf32_split": (_I32, [_P, _I64, _P, _P, _P]),
+    "tdkv_gemm_tf32x3": (_I32, [_P, _P, _I32, _P, _P, _I32, _P, _I32, _I32, _I32, _I32, _I32, _P]),
     "tdkv_qkv_rope": (_I32, [_P, _P, _I32, _I32, _I32, _P, _P, _P, _P]),
     "tdkv_alloc_create": (_P, [_I64, _I32]),
     "tdkv_alloc_destroy": (None, [_P]),

@@ -121,13 +121,20 @@ class PositionSpan:
             raise ValueError("span positions must be strictly increasing")
         object.__setattr__(self, "old_positions", old)
         object.__setattr__(self, "new_positions", new)
+        object.__setattr__(self, "_delta", None)
 
     def __len__(self) -> int:
         return int(self.old_positions.size)
 
     @property
     def delta(self) -> np.ndarray:
-        return self.new_positions - self.old_positions
+        """new - old (computed once: a span is immutable; read-only view)."""
+        d = self._delta
+        if d is None:
+            d = self.new_positions - self.old_positions
+            d.flags.writeable = False
+            object.__setattr__(self, "_delta", d)
+        return d
 
     @classmethod
     def identity(cls, positions: Iterable[int]) -> "PositionSpan":

@@ -241,12 +241,19 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* m
 }
 
 
-template <typename T, int BN, int kStages>
+// PRE (float32 only): the operands arrive already split into tf32 hi / lo
+// planes in global memory (tdkv_tf32_split; weights split once), so the TMA
+// producer loads four tiles per stage and no warp splits in shared memory --
+// the 3xTF32 GEMM becomes a pure TMA -> tcgen05 pipeline.
+template <typename T, int BN, int kStages, bool PRE = false>
 __global__ void __launch_bounds__(192, 1)
     gemm_tma_kernel(const __grid_constant__ CUtensorMap map_a,
-                    const __grid_constant__ CUtensorMap map_b, float* __restrict__ C, int ldc,
+                    const __grid_constant__ CUtensorMap map_b,
+                    const __grid_constant__ CUtensorMap map_al,
+                    const __grid_constant__ CUtensorMap map_bl, float* __restrict__ C, int ldc,
                     int M, int N, int K, int accumulate_c) {
     constexpr bool kTF32 = sizeof(T) == 4;
+    static_assert(!PRE || kTF32, "pre-split operands are float32 (3xTF32)");
     constexpr int kBK = 128 / (int)sizeof(T);              // one 128-byte atom of K
     constexpr int kABytes = kGemmBM * 128;
     constexpr int kBBytes = BN * 128;
@@ -298,9 +305,13 @@ __global__ void __launch_bounds__(192, 1)
             for (int kb = 0; kb < nk; ++kb) {
                 const int st = kb % kStages;
                 if (kb >= kStages) mbar_wait(&empty[st], (uint32_t)((kb / kStages - 1) & 1));
-                mbar_arrive_expect_tx(&full[st], kABytes + kBBytes);
+                mbar_arrive_expect_tx(&full[st], (PRE ? 2 : 1) * (kABytes + kBBytes));
                 tma_load_2d(a_hi(st), &map_a, &full[st], kb * kBK, m0);
                 tma_load_2d(b_hi(st), &map_b, &full[st], kb * kBK, n0);
+                if constexpr (PRE) {
+                    tma_load_2d(a_lo(st), &map_al, &full[st], kb * kBK, m0);
+                    tma_load_2d(b_lo(st), &map_bl, &full[st], kb * kBK, n0);
+                }
             }
         }
     } else if (warp == 1) {
@@ -308,7 +319,7 @@ __global__ void __launch_bounds__(192, 1)
             const uint32_t idesc = umma_idesc(kTF32 ? 2 : 1, kGemmBM, BN);
             for (int kb = 0; kb < nk; ++kb) {
                 const int st = kb % kStages;
-                mbar_wait(kTF32 ? &split[st] : &full[st], (uint32_t)((kb / kStages) & 1));
+                mbar_wait((kTF32 && !PRE) ? &split[st] : &full[st], (uint32_t)((kb / kStages) & 1));
                 tc_fence_after();
 #pragma unroll
                 for (int s = 0; s < 4; ++s) {                // 4 x 32 bytes of K per atom
@@ -328,7 +339,7 @@ __global__ void __launch_bounds__(192, 1)
         }
     } else {
         const int et = tid - 64;                             // 0..127
-        if constexpr (kTF32) {                               // ---- 3xTF32 split
+        if constexpr (kTF32 && !PRE) {                       // ---- 3xTF32 split
             for (int kb = 0; kb < nk; ++kb) {
                 const int st = kb % kStages;
                 mbar_wait(&full[st], (uint32_t)((kb / kStages) & 1));
@@ -769,21 +780,26 @@ static bool make_map(CUtensorMap* map, const void* base, int dtype, int rows, in
     return r == CUDA_SUCCESS;
 }
 
-template <typename T, int BN, int kStages>
+template <typename T, int BN, int kStages, bool PRE = false>
 static int32_t launch_gemm_tma(const void* A, int lda, const void* B, int ldb, float* C, int ldc,
                                int M, int N, int K, int accumulate, int dtype, cudaStream_t s,
-                               bool* ok) {
-    CUtensorMap ma, mb;
+                               bool* ok, const void* A_lo = nullptr, const void* B_lo = nullptr) {
+    CUtensorMap ma, mb, mal, mbl;
     *ok = make_map(&ma, A, dtype, M, K, lda, kGemmBM) && make_map(&mb, B, dtype, N, K, ldb, BN);
+    if (PRE)
+        *ok = *ok && make_map(&mal, A_lo, dtype, M, K, lda, kGemmBM) &&
+              make_map(&mbl, B_lo, dtype, N, K, ldb, BN);
+    else
+        mal = ma, mbl = mb;
     if (!*ok) return TDKV_OK;
-    auto kern = gemm_tma_kernel<T, BN, kStages>;
+    auto kern = gemm_tma_kernel<T, BN, kStages, PRE>;
     constexpr int kPlanes = sizeof(T) == 4 ? 2 : 1;
     const size_t smem = (size_t)kStages * kPlanes * (kGemmBM + BN) * 128 + 1024;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
         return check_launch("tdkv_gemm: cudaFuncSetAttribute");
     dim3 grid((M + kGemmBM - 1) / kGemmBM, (N + BN - 1) / BN);
-    kern<<<grid, 192, smem, s>>>(ma, mb, C, ldc, M, N, K, accumulate);
+    kern<<<grid, 192, smem, s>>>(ma, mb, mal, mbl, C, ldc, M, N, K, accumulate);
     return TDKV_OK;
 }
 
@@ -897,4 +913,66 @@ extern "C" int32_t tdkv_gemm(const void* d_a, int32_t lda, const void* d_b, int3
     if (rc) return rc;
     count_launch();
     return check_launch("tdkv_gemm");
+}
+
+// ---------------------------------------------------------------------------
+// 3xTF32 with pre-split operands
+
+__global__ void tf32_split_kernel(const float4* __restrict__ src, long long n4,
+                                  uint4* __restrict__ hi, uint4* __restrict__ lo) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+         i += (long long)gridDim.x * blockDim.x) {
+        const float4 v = src[i];
+        uint4 h, l;
+        h.x = tf32_rna(v.x); l.x = tf32_rna(v.x - __uint_as_float(h.x));
+        h.y = tf32_rna(v.y); l.y = tf32_rna(v.y - __uint_as_float(h.y));
+        h.z = tf32_rna(v.z); l.z = tf32_rna(v.z - __uint_as_float(h.z));
+        h.w = tf32_rna(v.w); l.w = tf32_rna(v.w - __uint_as_float(h.w));
+        hi[i] = h;
+        lo[i] = l;
+    }
+}
+
+extern "C" int32_t tdkv_tf32_split(const float* d_src, int64_t n, float* d_hi, float* d_lo,
+                                   void* stream) {
+    if (n < 0) return set_error(TDKV_EINVAL, "tdkv_tf32_split: negative size");
+    if (n == 0) return TDKV_OK;
+    if (!d_src || !d_hi || !d_lo) return set_error(TDKV_EINVAL, "tdkv_tf32_split: null pointer");
+    if (n % 4 || !aligned(d_src, 16) || !aligned(d_hi, 16) || !aligned(d_lo, 16))
+        return set_error(TDKV_EINVAL, "tdkv_tf32_split: 16-byte aligned multiples of 4 floats");
+    const long long n4 = n / 4;
+    long long grid = (n4 + 255) / 256;
+    if (grid > sm_count() * 8) grid = sm_count() * 8;
+    tf32_split_kernel<<<(unsigned)grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        reinterpret_cast<const float4*>(d_src), n4, reinterpret_cast<uint4*>(d_hi),
+        reinterpret_cast<uint4*>(d_lo));
+    count_launch();
+    return check_launch("tdkv_tf32_split");
+}
+
+extern "C" int32_t tdkv_gemm_tf32x3(const float* d_a_hi, const float* d_a_lo, int32_t lda,
+                                    const float* d_b_hi, const float* d_b_lo, int32_t ldb,
+                                    float* d_c, int32_t ldc, int32_t m, int32_t n, int32_t k,
+                                    int32_t accumulate, void* stream) {
+    if (m < 0 || n < 0 || k < 0) return set_error(TDKV_EINVAL, "tdkv_gemm_tf32x3: negative size");
+    if (m == 0 || n == 0) return TDKV_OK;
+    if (k == 0) return set_error(TDKV_EINVAL, "tdkv_gemm_tf32x3: K must be positive");
+    if (!d_a_hi || !d_a_lo || !d_b_hi || !d_b_lo || !d_c)
+        return set_error(TDKV_EINVAL, "tdkv_gemm_tf32x3: null pointer");
+    if (!aligned(d_a_hi, 16) || !aligned(d_a_lo, 16) || !aligned(d_b_hi, 16) ||
+        !aligned(d_b_lo, 16) || (lda * 4) % 16 || (ldb * 4) % 16)
+        return set_error(TDKV_EINVAL, "tdkv_gemm_tf32x3: A/B rows must be 16-byte aligned");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    bool tma = false;
+    const int32_t rc =
+        n <= 64 ? launch_gemm_tma<float, 64, 4, true>(d_a_hi, lda, d_b_hi, ldb, d_c, ldc, m, n, k,
+                                                      accumulate, TDKV_F32, s, &tma, d_a_lo,
+                                                      d_b_lo)
+                : launch_gemm_tma<float, 128, 3, true>(d_a_hi, lda, d_b_hi, ldb, d_c, ldc, m, n,
+                                                       k, accumulate, TDKV_F32, s, &tma, d_a_lo,
+                                                       d_b_lo);
+    if (rc) return rc;
+    if (!tma) return set_error(TDKV_EUNSUPPORTED, "tdkv_gemm_tf32x3: tensor maps unavailable");
+    count_launch();
+    return check_launch("tdkv_gemm_tf32x3");
 }

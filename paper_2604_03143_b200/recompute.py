@@ -31,7 +31,7 @@ import torch
 from . import _kernels, _lib
 from ._device import default_device, h2d, is_host, ptr, stream_handle, to_device, to_host
 from .core import LayeredKv, ModelConfig, union_sorted
-from .gemm import gemm_tn
+from .gemm import gemm_tf32x3, gemm_tn, tf32_split
 from .ledger import CostLedger
 
 
@@ -92,6 +92,12 @@ class ToyModel:
                                 wv.transpose(0, 2, 1)], axis=1)
         self.wqkv_t = to_device(np.ascontiguousarray(qkv_t), device)
         self.wm_t = to_device(np.ascontiguousarray(wm.transpose(0, 2, 1)), device)
+        # the weights' tf32 hi / lo planes, split once (3xTF32 GEMMs over
+        # pre-split operands); TDKV_GEMM_PRESPLIT=0 splits inside every GEMM
+        self.presplit = _PRESPLIT
+        if self.presplit:
+            self.wqkv_t_split = tf32_split(self.wqkv_t)
+            self.wm_t_split = tf32_split(self.wm_t)
 
     @classmethod
     def of(cls, weights, device: Optional[torch.device] = None) -> "ToyModel":
@@ -131,6 +137,8 @@ def selective_forward(weights, tokens, positions, fix_idx, ctx_k, ctx_v,
         return to_host(out_k), to_host(out_v)
     return out_k, out_v
 
+
+_PRESPLIT = os.environ.get("TDKV_GEMM_PRESPLIT", "1") != "0"
 
 # TDKV_ATTN_ONLINE=0 keeps the two-pass (stored score row) attention everywhere
 _ATTN_ONLINE = os.environ.get("TDKV_ATTN_ONLINE", "1") != "0"
@@ -243,8 +251,18 @@ def forward_many(m: ToyModel, items, layers: int, k_only_last: bool = False):
     d_members = mem_base
     scale = float(np.float32(1.0 / np.sqrt(D)))
     stream = stream_handle(dev)
+    if m.presplit:
+        a_split = (torch.empty((R, hid), dtype=torch.float32, device=dev),
+                   torch.empty((R, hid), dtype=torch.float32, device=dev))
     for layer in range(layers):
-        if k_only_last and layer == layers - 1:
+        if m.presplit:
+            tf32_split(h, out=a_split)
+            wh, wl = m.wqkv_t_split[0][layer], m.wqkv_t_split[1][layer]
+            if k_only_last and layer == layers - 1:
+                gemm_tf32x3(a_split, (wh[hid:2 * hid], wl[hid:2 * hid]), out=qkv[:, hid:2 * hid])
+            else:
+                gemm_tf32x3(a_split, (wh, wl), out=qkv)
+        elif k_only_last and layer == layers - 1:
             # K columns only; Q and V of this layer are never read
             gemm_tn(h, m.wqkv_t[layer][hid:2 * hid], out=qkv[:, hid:2 * hid])
         else:
@@ -256,7 +274,12 @@ def forward_many(m: ToyModel, items, layers: int, k_only_last: bool = False):
         _lib.call("tdkv_attention_many", ptr(q), ptr(out_k[layer]), ptr(out_v[layer]),
                   d_members, n_live, layer, R, n_tiles, rows_per_tile, max(Ts), H, D,
                   scale, ptr(mix), stream)
-        gemm_tn(mix, m.wm_t[layer], out=h, accumulate=True)
+        if m.presplit:
+            tf32_split(mix, out=a_split)
+            gemm_tf32x3(a_split, (m.wm_t_split[0][layer], m.wm_t_split[1][layer]), out=h,
+                        accumulate=True)
+        else:
+            gemm_tn(mix, m.wm_t[layer], out=h, accumulate=True)
     return out_k, out_v, row0
 
 

@@ -27,8 +27,13 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--round", default="r01")
     r = ap.parse_args().round
-    for src, dst in (("bench.log", "c2"), ("bench_c1.log", "c1"), ("bench_c3.log", "c3"),
-                     ("bench_c4.log", "c4"), ("bench_c5.log", "c5"), ("bench_ref.log", "ref")):
+    # r01: the default bench line was C2; from r02 the default is C3
+    default = "c2" if r == "r01" else "c3"
+    for src, dst in (("bench.log", default), ("bench_c1.log", "c1"), ("bench_c2.log", "c2"),
+                     ("bench_c3.log", "c3"), ("bench_c4.log", "c4"), ("bench_c5.log", "c5"),
+                     ("bench_ref.log", "ref")):
+        if not os.path.exists(os.path.join(OUT, src)):
+            continue
         d = last_json(os.path.join(OUT, src))
         with open(os.path.join(PROF, f"{r}_bench_{dst}.json"), "w") as f:
             json.dump(d, f, indent=1)
@@ -48,13 +53,14 @@ def main():
             with open(path) as f:
                 keep = [l.rstrip() for l in f if "passed" in l or "failed" in l or "SUMMARY" in l]
             lines += [f"## {tool}"] + keep[-2:]
-    with open(os.path.join(PROF, f"{r}_sanitizers.txt"), "w") as f:
-        f.write("\n".join(lines) + "\n")
+    if not os.path.exists(os.path.join(PROF, f"{r}_sanitizers.txt")):
+        with open(os.path.join(PROF, f"{r}_sanitizers.txt"), "w") as f:
+            f.write("\n".join(lines) + "\n")
     for script in ("ncu_summary.py", "ncu_export.py"):
         subprocess.run([sys.executable, os.path.join(ROOT, "scripts", script), "--round", r],
                        check=True, stdout=subprocess.DEVNULL)
-    d = json.load(open(os.path.join(PROF, f"{r}_bench_c2.json")))
-    print("c2", d["value"], d["roofline"]["frac"], d["e2e"]["value"], d["codec"]["encode_gbs"],
+    d = json.load(open(os.path.join(PROF, f"{r}_bench_{default}.json")))
+    print(default, d["value"], d["roofline"]["frac"], d["e2e"]["value"], d["codec"]["encode_gbs"],
           d["codec"]["decode_gbs"], d["selection"]["device_ms"], d["recovery"]["speedup"])
 
 

@@ -105,7 +105,10 @@ def main():
     for rep in sorted(glob.glob(os.path.join(args.dir, "*.ncu-rep"))):
         for rec in parse_rep(rep):
             rec["round"] = args.round
-            summary[short(rec["kernel"])] = rec
+            # one entry per (kernel, capture): the same kernel is captured on
+            # several workloads (e.g. K1 at C1 / C2 / C3 and as the family restore)
+            name = os.path.splitext(os.path.basename(rep))[0]
+            summary[f"{short(rec['kernel'])}@{name}"] = rec
     with open(summary_path, "w") as f:
         json.dump(summary, f, indent=1, sort_keys=True)
     launches = os.path.join(args.dir, "launches.csv")

@@ -21,6 +21,26 @@ def test_gemm_tf32x3_matches_float64(M, N, K):
     assert err <= 2e-6 * max(1.0, scale) * max(1.0, (K / 64) ** 0.5), (err, scale)
 
 
+@pytest.mark.parametrize("M,N,K", [(1, 8, 8), (128, 64, 32), (130, 100, 72), (300, 512, 512),
+                                   (17, 1536, 512), (2048, 4608, 512)])
+def test_gemm_presplit_equals_in_kernel_split(M, N, K):
+    """tdkv_gemm_tf32x3 over tdkv_tf32_split planes performs the same
+    tf32 splits and the same MMA sequence as the in-kernel split of
+    tdkv_gemm: bit-identical results, plain and accumulating (the toy
+    model's residual update h += mix @ Wm)."""
+    g = torch.Generator(device=DEV).manual_seed(M + 7 * N + 13 * K)
+    a = torch.randn(M, K, generator=g, device=DEV)
+    b = torch.randn(N, K, generator=g, device=DEV) * 0.1
+    c0 = torch.randn(M, N, generator=g, device=DEV)
+    hi, lo = gemm.tf32_split(a)
+    assert torch.equal(hi + lo, hi + lo) and (hi.view(torch.int32) & 0x1FFF).eq(0).all()
+    for acc in (False, True):
+        want, got = c0.clone(), c0.clone()
+        gemm.gemm_tn(a, b, out=want, accumulate=acc)
+        gemm.gemm_tf32x3((hi, lo), gemm.tf32_split(b), out=got, accumulate=acc)
+        assert torch.equal(got, want), (acc, (got - want).abs().max().item())
+
+
 def test_gemm_accumulate_residual():
     g = torch.Generator(device=DEV).manual_seed(7)
     a = torch.randn(200, 64, generator=g, device=DEV)
