@@ -175,9 +175,9 @@ def load(path: Optional[str] = None) -> ctypes.CDLL:
     """Load libtdkv.so (once; ``TDKV_LIBRARY`` overrides the in-tree path for
     A/B builds).  Raises TdkvUnavailable when it is missing."""
     global _lib
-    path = path or os.environ.get("TDKV_LIBRARY") or LIB_PATH
-    if _lib is not None:
+    if _lib is not None:                 # every launch passes here: no env lookup
         return _lib
+    path = path or os.environ.get("TDKV_LIBRARY") or LIB_PATH
     with _lock:
         if _lib is not None:
             return _lib

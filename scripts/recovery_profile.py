@@ -31,4 +31,4 @@ for _ in range(5):
     pic.collective_recover(w, group, _Pic, CostLedger(2))
 torch.cuda.synchronize()
 pr.disable()
-pstats.Stats(pr).sort_stats("tottime").print_stats(25)
+pstats.Stats(pr).sort_stats("cumulative").print_stats(45)
