@@ -394,6 +394,9 @@ int32_t tdkv_attention(const float* d_q, const float* d_k_fresh, const float* d_
  * the tile's rows in TMEM lanes, S = Q K^T and O = P V per 64-key tile as
  * tcgen05.mma kind::tf32 in 3xTF32 (hi/lo split operands), online softmax in
  * float32 with the running max shared by the two threads of a row.
+ * The 64- and 128-row tiles move 16-byte vectors: every row plane (q, fresh
+ * K/V, mix and each member's context planes) 16-byte aligned, H*D % 4 == 0
+ * (TDKV_EINVAL otherwise, for the planes passed here).
  * n_tiles == 0 runs one CTA per row. */
 typedef struct {
     const float* ctx_k;          /* (L, num_tokens, H*D) context planes */

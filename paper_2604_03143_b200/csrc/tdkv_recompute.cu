@@ -1045,6 +1045,12 @@ extern "C" int32_t tdkv_attention_many(const float* d_q, const float* d_k_fresh,
     if (n_members == 0 || total_rows == 0) return TDKV_OK;
     if (!d_q || !d_k_fresh || !d_v_fresh || !d_members || !d_mix)
         return set_error(TDKV_EINVAL, "tdkv_attention_many: null pointer");
+    if (n_tiles > 0 && (rows_per_tile == kTcQ || rows_per_tile == kBlkQ) &&
+        (!aligned(d_q, 16) || !aligned(d_k_fresh, 16) || !aligned(d_v_fresh, 16) ||
+         !aligned(d_mix, 16) || (num_heads * head_dim) % 4))
+        return set_error(TDKV_EINVAL, "tdkv_attention_many: %d-row tiles read and write "
+                         "16-byte vectors: row planes must be 16-byte aligned with H*D %% 4 == 0",
+                         rows_per_tile);
     if (n_tiles > 0 && rows_per_tile == kTcQ) {
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         switch (head_dim) {
