@@ -679,3 +679,46 @@ def test_replayed_plan_auto_graph_and_fused_table(dtype):
                 r0 = j.segment * spec.seg_len
                 want = ref.rope_apply(ak[1, r0:r0 + spec.seg_len], j.delta)
                 assert np.abs(gk[1, j.dst_rows] - want).max() <= F32_TOL
+
+
+@pytest.mark.parametrize("dtype,heads,head_dim,agents", [
+    ("bf16", 4, 128, 40),      # 40 jobs per tile: three job groups in the fused instantiation
+    ("f32", 8, 64, 21),        # C1 rows, two groups
+    ("f32", 1, 6, 9),          # 24-byte rows: 8-byte units, the generic kernel's fused path
+    ("bf16", 3, 10, 17),       # 60-byte rows: 4-byte units, no TMA staging
+])
+def test_fused_table_equals_k0_table(dtype, heads, head_dim, agents):
+    """A round collected with the cos/sin rows computed inside K1 (fused K0)
+    equals the same round with K0's table, bit for bit, whatever the unit
+    width, the job-group count per tile and the staging path; and matches the
+    oracle (f32 within 1e-5)."""
+    base = rounds.CONFIGS["c1"] if dtype == "f32" else rounds.CONFIGS["c2"]
+    spec = base.scaled(num_layers=2, num_heads=heads, head_dim=head_dim, num_agents=agents,
+                       num_segments=3, seg_len=40, hist_len=13)
+    mk, mv = rounds.master_planes_host(spec)
+    dt = spec.torch_dtype
+    arena = rounds.make_arena(spec, torch.from_numpy(mk).to(DEV).to(dt),
+                              torch.from_numpy(mv).to(DEV).to(dt))
+    T = spec.tokens_per_agent
+    outs = []
+    for fused in (True, False):
+        pool = tk.PagedPool(agents * T + 40, spec.num_layers, heads, head_dim, dtype=dt,
+                            device=DEV)
+        maps = [pool.allocate(T, a) for a in range(agents)]
+        col = tk.KVCollector(arena, pool)
+        col.auto_graph = False
+        plan = col.plan([j for a, m in enumerate(maps) for j in rounds.agent_jobs(spec, a, m.slots)])
+        plan.fuse_table = fused
+        col.collect(plan)
+        torch.cuda.synchronize()
+        outs.append((pool.k.float().cpu().numpy(), pool.v.float().cpu().numpy(), maps))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    if dtype == "f32":
+        gk, gv, maps = outs[0]
+        for a, m in enumerate(maps):
+            for j in rounds.agent_jobs(spec, a, m.slots):
+                r0 = j.segment * spec.seg_len
+                for layer in range(spec.num_layers):
+                    want = ref.rope_apply(mk[layer, r0:r0 + spec.seg_len], j.delta)
+                    assert np.abs(gk[layer, j.dst_rows] - want).max() <= F32_TOL
+                    assert np.array_equal(gv[layer, j.dst_rows], mv[layer, r0:r0 + spec.seg_len])
