@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--codec-sweep", action="store_true",
                     help="encode/decode sweep over changed-block fractions (C4)")
     ap.add_argument("--profile", action="store_true", help="few launches, no extras (for ncu)")
+    ap.add_argument("--rope-style", default="interleaved", choices=["interleaved", "neox"],
+                    help="rotary pairing of the collector (the reference's interleaved pairs, "
+                         "or rotate-half)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
                     help="N>1 master exchange: NCCL broadcast / send-recv into each rank's "
@@ -328,7 +331,7 @@ def run_tdkv(args):
     pool = tk.PagedPool(sb * T, L, H, D, dtype=dt, device=dev, debug=False)
     maps = [pool.allocate(T, a) for a in batches[0]]
 
-    collector = tk.KVCollector(arena, pool)
+    collector = tk.KVCollector(arena, pool, rope_style=args.rope_style)
     plans = [collector.plan([j for a, m in zip(b, maps) for j in rounds.agent_jobs(spec, a, m.slots)])
              for b in batches]
     plan = plans[0]
@@ -384,7 +387,7 @@ def run_tdkv(args):
             arena_r = rounds.make_arena(spec, arena.k.clone(), arena.v.clone())
             pool_r = tk.PagedPool(sb * T, L, H, D, dtype=dt, device=dev, debug=False)
             maps_r = [pool_r.allocate(T, a) for a in batches[0]]
-            col_r = tk.KVCollector(arena_r, pool_r)
+            col_r = tk.KVCollector(arena_r, pool_r, rope_style=args.rope_style)
             rotation.append((col_r, [col_r.plan([j for a, m in zip(b, maps_r)
                                                  for j in rounds.agent_jobs(spec, a, m.slots)])
                                      for b in batches]))
@@ -545,6 +548,7 @@ def run_tdkv(args):
                    "sub_batches_per_gpu": len(batches), "shared_blocks": spec.num_segments,
                    "block_len": spec.seg_len, "layers": L, "kv_heads": H, "head_dim": D,
                    "tokens_per_agent": T, "parallelism": f"agent-shard x{world}",
+                   "rope_pairs": args.rope_style,
                    "exchange": (None if world == 1 else
                                 "p2p" if peer is not None else "nccl"),
                    "l2": (f"inputs larger than L2: steps rotate over {len(rotation)} "

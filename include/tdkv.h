@@ -124,6 +124,13 @@ int32_t tdkv_collect_round(const int64_t* d_deltas, int64_t n_table_rows,
  * Requires one table row per job (every job's delta constant: tbl_stride 0,
  * tbl_row indexing d_deltas). */
 #define TDKV_ROUND_FUSE_TABLE 1
+/* TDKV_ROUND_NEOX rotates rotate-half pairs (element j of a head with element
+ * j + D/2, angle index j; GPT-NeoX / Llama layout) instead of the reference's
+ * interleaved pairs (toymodel.py:78-82): a thread owns a 16-byte unit of a
+ * head's lower half and the unit D/2 elements on, so both members of every
+ * pair are in its registers.  Requires 16-byte-aligned planes and half heads
+ * of whole 16-byte units. */
+#define TDKV_ROUND_NEOX 2
 /* d_master_v == d_dst_v == NULL makes a K-only collect (align_cached alone;
  * the reference copies V in _skeleton). */
 

@@ -33,7 +33,7 @@ from typing import List, Optional, Sequence, Tuple
 import numpy as np
 
 __all__ = [
-    "inv_freq", "rope_apply", "rope_recover", "block_count", "block_range",
+    "inv_freq", "rope_apply", "rope_apply_neox", "rope_recover", "block_count", "block_range",
     "valid_len", "allocate_slots", "CollectJob", "collect_into_contexts",
     "collect_into_pool", "DiffLayer", "HintViolation", "encode_diff",
     "decode_dense", "wire_size", "serialize", "deserialize", "WireError",
@@ -72,6 +72,28 @@ def rope_apply(k: np.ndarray, positions: np.ndarray, base: float = 10000.0) -> n
     even, odd = pairs[..., 0], pairs[..., 1]
     out = np.stack((even * c - odd * s, even * s + odd * c), axis=-1)
     return out.reshape(k.shape).astype(np.float32)
+
+
+def rope_apply_neox(k: np.ndarray, positions: np.ndarray, base: float = 10000.0) -> np.ndarray:
+    """The rotate-half (GPT-NeoX / Llama) pairing of the same rotation: element
+    j pairs with j + D/2 of its head, angle index j (an extension beyond the
+    reference, which pairs interleaved elements, toymodel.py:78-82); the
+    arithmetic is rope_apply's -- float64 angles and rotation, one cast to
+    float32."""
+    if k.ndim != 3:
+        raise ValueError("expected (tokens, heads, head_dim)")
+    t, _, d = k.shape
+    if d % 2:
+        raise ValueError("head_dim must be even")
+    pos = np.asarray(positions, dtype=np.float64)
+    if pos.shape != (t,):
+        raise ValueError("one position per token required")
+    theta = pos.reshape(t, 1) * inv_freq(d, base).reshape(1, d // 2)
+    c = np.cos(theta).reshape(t, 1, d // 2)
+    s = np.sin(theta).reshape(t, 1, d // 2)
+    x = k.astype(np.float64)
+    lo, hi = x[..., :d // 2], x[..., d // 2:]
+    return np.concatenate((lo * c - hi * s, lo * s + hi * c), axis=-1).astype(np.float32)
 
 
 def rope_recover(old_positions: np.ndarray, new_positions: np.ndarray,

@@ -26,6 +26,7 @@ NO_VIOLATION = 0x7F7F7F7F
 ROWS_CONTIGUOUS = 1
 ROWS_JOB_MINOR = 2
 ROUND_FUSE_TABLE = 1
+ROUND_NEOX = 2
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

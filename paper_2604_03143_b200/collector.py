@@ -342,6 +342,9 @@ class CollectPlan:
             self.rotate and host.jobs.size and (host.jobs["tbl_stride"] == 0).all()
             and (_FUSE_TABLE == "1" or (_FUSE_TABLE != "0"
                                         and self.algorithmic_bytes() <= _FUSE_TABLE_MAX_BYTES)))
+        # rotate-half pairs (KVCollector(rope_style="neox")); the reference's
+        # interleaved pairs otherwise
+        self.neox = False
         self.table = torch.empty((max(host.deltas.size, 1), self.head_dim // 2, 2),
                                  dtype=torch.float64 if self.kv_dtype == torch.float32
                                  else torch.float32, device=self.device)
@@ -370,6 +373,10 @@ class CollectPlan:
                        dst_v: Optional[torch.Tensor], dst_layer_stride: int,
                        layers: Optional[tuple] = None, grid_limit: int = 0) -> int:
         """K1 over all layers or the layer range ``layers = (l0, l1)``."""
+        if self.neox:
+            raise ValueError("rotate-half (neox) plans run through KVCollector.collect "
+                             "(tdkv_collect_round); the chunked and multi-source launches "
+                             "rotate interleaved pairs only")
         if arena.k.dtype != self.kv_dtype or dst_k.dtype != self.kv_dtype:
             raise ValueError("arena, destination and plan dtypes differ")
         if self.num_jobs == 0:
@@ -401,6 +408,10 @@ class CollectPlan:
         """K1 over every layer, unit u's tile read from ``sources[unit_src[u]]``
         (arenas of identical layout: the local one or peer GPUs' arenas
         mapped over NVLink); ``d_unit_src`` from ``unit_sources``."""
+        if self.neox:
+            raise ValueError("rotate-half (neox) plans run through KVCollector.collect "
+                             "(tdkv_collect_round); the chunked and multi-source launches "
+                             "rotate interleaved pairs only")
         if not sources or any(a.k.shape != sources[0].k.shape or a.k.dtype != self.kv_dtype
                               for a in sources):
             raise ValueError("sources must be arenas of one layout and the plan's dtype")
@@ -455,7 +466,8 @@ class CollectPlan:
                     C.c_int64(int(dst_layer_stride)), C.c_int32(self.num_layers),
                     C.c_int32(self.num_heads), C.c_int32(self.head_dim),
                     C.c_int32(dtype_code(self.kv_dtype)), C.c_int32(int(grid_limit)),
-                    C.c_int32(_lib.ROUND_FUSE_TABLE if self.fuse_table else 0), stream)
+                    C.c_int32((_lib.ROUND_FUSE_TABLE if self.fuse_table else 0)
+                              | (_lib.ROUND_NEOX if self.neox else 0)), stream)
             if len(self._fast) >= 16:
                 self._fast.clear()
             # keep the tensors whose addresses are baked in alive with the entry
@@ -472,7 +484,13 @@ class KVCollector:
     """Arena + pool binding: plan rounds and collect them into the pool."""
 
     def __init__(self, arena: MasterArena, pool, rope_base: float = 10000.0,
-                 tile_rows: Optional[int] = None) -> None:
+                 tile_rows: Optional[int] = None, rope_style: str = "interleaved") -> None:
+        """``rope_style``: "interleaved" -- the reference's pairs (2j, 2j+1),
+        toymodel.py:78-82 -- or "neox" (j, j + D/2; GPT-NeoX / Llama), an
+        extension for models laid out that way (same angles, same arithmetic)."""
+        if rope_style not in ("interleaved", "neox"):
+            raise ValueError(f"rope_style must be 'interleaved' or 'neox', got {rope_style!r}")
+        self.rope_style = rope_style
         if (arena.num_layers, arena.k.shape[2], arena.k.shape[3]) != (
                 pool.num_layers, pool.num_heads, pool.head_dim):
             raise ValueError("arena and pool geometry differ")
@@ -488,8 +506,13 @@ class KVCollector:
         self._last = None            # (plan, grid_limit, stream) of the previous collect
         self._graph = None           # (key, RoundGraph)
 
+    def _styled(self, plan: CollectPlan) -> CollectPlan:
+        plan.neox = self.rope_style == "neox"
+        return plan
+
     def plan(self, jobs: Sequence[CollectJob]) -> CollectPlan:
-        return CollectPlan(self.arena, jobs, self.rope_base, self.tile_rows, self.pool.device)
+        return self._styled(CollectPlan(self.arena, jobs, self.rope_base, self.tile_rows,
+                                        self.pool.device))
 
     def capture(self, plan: CollectPlan) -> "RoundGraph":
         """The round as a replayable CUDA graph (see RoundGraph)."""
@@ -508,12 +531,14 @@ class KVCollector:
         return self.plan(jobs)
 
     def plan_offsets(self, segments, dst_off, job_delta, slot_arena: "SlotArena") -> CollectPlan:
-        return CollectPlan.from_offsets(self.arena, segments, dst_off, job_delta,
-                                        slot_arena.rows, self.rope_base, self.tile_rows)
+        return self._styled(CollectPlan.from_offsets(self.arena, segments, dst_off, job_delta,
+                                                     slot_arena.rows, self.rope_base,
+                                                     self.tile_rows))
 
     def plan_arrays(self, segments, dst_rows, deltas) -> CollectPlan:
-        return CollectPlan.from_arrays(self.arena, segments, dst_rows, deltas, self.rope_base,
-                                       self.tile_rows, self.pool.device)
+        return self._styled(CollectPlan.from_arrays(self.arena, segments, dst_rows, deltas,
+                                                    self.rope_base, self.tile_rows,
+                                                    self.pool.device))
 
     def collect(self, plan: CollectPlan, ledger: Optional[CostLedger] = None,
                 grid_limit: int = 0) -> int:

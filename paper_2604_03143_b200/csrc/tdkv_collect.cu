@@ -89,6 +89,7 @@ struct CollectParams {
     int32_t block_size;
     int32_t n_jobs;
     int32_t ovl_inline;                   // OVL: K1's CTAs run the overlay pass after their items
+    int32_t neox;                         // rotate-half pairs (collect_kernel<..., NEOX>)
 };
 
 // Per-job destination metadata is staged in shared memory in groups of
@@ -227,12 +228,20 @@ __global__ void __launch_bounds__(256) overlay_rows_kernel(const CollectParams p
 // bounds the kernel): every job has one constant delta, its cos/sin row sits
 // in shared memory, and the scatter loop is the rotation, one 32-bit-indexed
 // address and the store.
-template <typename T, int UB, bool BULK, bool OVL, bool FUSE = false>
+//
+// NEOX: the rotate-half pairing (element j of a head with element j + D/2,
+// angle index j) instead of the reference's interleaved pairs.  A thread owns
+// a unit of the head's lower half AND the unit D/2 elements on, so every pair
+// is in its registers (no shuffle between the two halves' lanes: that form
+// measured 0.58 of peak at C2/C3 -- twice the cos/sin loads and shuffles per
+// stored unit, and spills).
+template <typename T, int UB, bool BULK, bool OVL, bool FUSE = false, bool NEOX = false>
 __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) {
     using V = typename UnitBits<UB>::V;
     using Tbl = typename Elt<T>::Table;
     constexpr int kEpu = UB / (int)sizeof(T);      // elements per unit
     constexpr int kPairs = kEpu / 2;
+    constexpr int kCs = kPairs;                   // cos/sin entries per interleaved unit
 
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ __align__(8) uint64_t bars[2];
@@ -251,7 +260,16 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
     const int ty = tid / tx_n;
     const int n_items = p.n_units * p.num_layers;
     // pair index of this thread's first unit (the usual single c = tx)
-    const int j0_tx = ((tx * kEpu) % p.head_dim) >> 1;
+    auto angle0 = [&](int c) { return ((c * kEpu) % p.head_dim) >> 1; };
+    const int j0_tx = angle0(tx);
+    // NEOX: slots = (head, unit of the lower half); slot s owns units c_lo and
+    // c_lo + hh of its row (hh = units per half head)
+    const int hh = (p.head_dim >> 1) / kEpu;
+    const int n_slots = upr >> 1;
+    const int sx_n = n_slots < nthr ? n_slots : nthr;
+    const int slot_rows = sx_n > 0 ? nthr / sx_n : 0;
+    const int sx = sx_n > 0 ? tid % sx_n : 0;
+    const int sy = sx_n > 0 ? tid / sx_n : 0;
     // log2(head_dim / 2) when a power of two (the fused table's index split)
     const int half_shift = ((p.head_dim >> 1) & ((p.head_dim >> 1) - 1)) == 0
                                ? __ffs(p.head_dim >> 1) - 1 : -1;
@@ -327,7 +345,13 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
     auto load_cs = [&](Tbl* cs, int tbl_row, int j0) {
         const Tbl* trow = table + (size_t)tbl_row * half + j0;
 #pragma unroll
-        for (int q = 0; q < kPairs; ++q) cs[q] = __ldg(trow + q);
+        for (int q = 0; q < kCs; ++q) cs[q] = __ldg(trow + q);
+    };
+    // rotate one unit's interleaved pairs in place
+    auto rotate_unit_k = [&](V& kv, const Tbl* cs, bool) {
+        T* e = reinterpret_cast<T*>(&kv);
+#pragma unroll
+        for (int q = 0; q < kPairs; ++q) rot_pair(e[2 * q], e[2 * q + 1], cs[q]);
     };
     // fused K0: the group's rows live in shared memory after the tiles
     const bool fused = p.fuse_table != 0;
@@ -336,7 +360,7 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
         if (fused) {
             const Tbl* trow = s_cs + (size_t)jj * half + j0;
 #pragma unroll
-            for (int q = 0; q < kPairs; ++q) cs[q] = trow[q];
+            for (int q = 0; q < kCs; ++q) cs[q] = trow[q];
         } else {
             load_cs(cs, m.x, j0);
         }
@@ -466,29 +490,69 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
                     bulk_commit();
                 }
             }
-            if constexpr (FUSE) {
+            if constexpr (NEOX) {
+              if (sy < slot_rows) {
+                const uint32_t upr32 = (uint32_t)upr;
+                for (int sl = sx; sl < n_slots; sl += sx_n) {
+                    const int c_lo = (sl / hh) * (2 * hh) + sl % hh;
+                    const int c_hi = c_lo + hh;
+                    const int j0 = (sl % hh) * kEpu;       // angle of the slot's first element
+                    for (int jj = 0; jj < ng; ++jj) {
+                        const int4 mj = s_meta[mb][jj];
+                        Tbl cs[kEpu];
+                        if (mj.y == 0) {
+                            const Tbl* trow = FUSE ? s_cs + jj * half + j0
+                                                   : table + (size_t)mj.x * half + j0;
+#pragma unroll
+                            for (int q = 0; q < kEpu; ++q) cs[q] = trow[q];
+                        }
+                        const int64_t* dr = &s_drow[mb][jj * kMaxTileRows];
+                        for (int r = sy; r < u.nrows; r += slot_rows) {
+                            if (!FUSE && mj.y != 0) {
+                                const Tbl* trow = table + (size_t)(mj.x + (mj.z + r) * mj.y) * half + j0;
+#pragma unroll
+                                for (int q = 0; q < kEpu; ++q) cs[q] = __ldg(trow + q);
+                            }
+                            const size_t o = (size_t)(uint32_t)dr[r] * upr32;
+                            V lo = sk[r * upr + c_lo], hi = sk[r * upr + c_hi];
+                            if (rotate) {
+                                T* a = reinterpret_cast<T*>(&lo);
+                                T* b = reinterpret_cast<T*>(&hi);
+#pragma unroll
+                                for (int q = 0; q < kEpu; ++q) rot_pair(a[q], b[q], cs[q]);
+                            }
+                            st_stream(reinterpret_cast<V*>(dk_l) + o + c_lo, lo);
+                            st_stream(reinterpret_cast<V*>(dk_l) + o + c_hi, hi);
+                            if (has_v && !v_tma) {
+                                st_stream(reinterpret_cast<V*>(dv_l) + o + c_lo, sv[r * upr + c_lo]);
+                                st_stream(reinterpret_cast<V*>(dv_l) + o + c_hi, sv[r * upr + c_hi]);
+                            }
+                        }
+                    }
+                }
+              }
+            } else if constexpr (FUSE) {
               if (ty < rows_per_pass) {
                 // constant delta per job, cos/sin rows in shared memory
                 const uint32_t upr32 = (uint32_t)upr;
                 for (int c = tx; c < upr; c += tx_n) {
-                    const int j0 = c == tx ? j0_tx : ((c * kEpu) % p.head_dim) >> 1;
+                    const int j0 = c == tx ? j0_tx : angle0(c);
+                    const bool fh = true;
                     V* __restrict__ dkc = reinterpret_cast<V*>(dk_l) + c;
                     V* __restrict__ dvc = reinterpret_cast<V*>(dv_l) + c;
                     const V* skc = sk + c;
                     const V* svc = sv + c;
                     for (int jj = 0; jj < ng; ++jj) {
-                        Tbl cs[kPairs];
+                        Tbl cs[kCs];
                         const Tbl* trow = s_cs + jj * half + j0;
 #pragma unroll
-                        for (int q = 0; q < kPairs; ++q) cs[q] = trow[q];
+                        for (int q = 0; q < kCs; ++q) cs[q] = trow[q];
                         const int64_t* dr = &s_drow[mb][jj * kMaxTileRows];
 #pragma unroll 2
                         for (int r = ty; r < u.nrows; r += rows_per_pass) {
                             const size_t o = (size_t)(uint32_t)dr[r] * upr32;
                             V kv = skc[r * upr];
-                            T* e = reinterpret_cast<T*>(&kv);
-#pragma unroll
-                            for (int q = 0; q < kPairs; ++q) rot_pair(e[2 * q], e[2 * q + 1], cs[q]);
+                            rotate_unit_k(kv, cs, fh);
                             st_stream(dkc + o, kv);
                             if (has_v && !v_tma) st_stream(dvc + o, svc[r * upr]);
                         }
@@ -497,8 +561,9 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
               }
             } else if (ty < rows_per_pass) {
                 for (int c = tx; c < upr; c += tx_n) {
-                    const int j0 = c == tx ? j0_tx : ((c * kEpu) % p.head_dim) >> 1;
-                    Tbl cs[kPairs], csn[kPairs];
+                    const int j0 = c == tx ? j0_tx : angle0(c);
+                    const bool fh = true;
+                    Tbl cs[kCs], csn[kCs];
                     int4 m = s_meta[mb][0];
                     if (rotate && m.y == 0) load_cs_job(cs, 0, m, j0);
                     for (int jj = 0; jj < ng; ++jj) {
@@ -515,10 +580,7 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
                             V kv = sk[r * upr + c];
                             if (rotate) {
                                 if (m.y != 0) load_cs(cs, m.x + (m.z + r) * m.y, j0);
-                                T* e = reinterpret_cast<T*>(&kv);
-#pragma unroll
-                                for (int q = 0; q < kPairs; ++q)
-                                    rot_pair(e[2 * q], e[2 * q + 1], cs[q]);
+                                rotate_unit_k(kv, cs, fh);
                             }
                             if (!ovk)
                                 st_stream(reinterpret_cast<V*>(dk_l + (size_t)drow * p.row_elems) + c,
@@ -529,7 +591,7 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
                         }
                         m = mn;
 #pragma unroll
-                        for (int q = 0; q < kPairs; ++q) cs[q] = csn[q];
+                        for (int q = 0; q < kCs; ++q) cs[q] = csn[q];
                     }
                 }
             }
@@ -552,7 +614,13 @@ template <typename T, int UB, bool BULK, bool OVL = false>
 static int32_t launch_collect(const CollectParams& p, int grid_limit, cudaStream_t s, bool pdl) {
     auto kern = collect_kernel<T, UB, BULK, OVL>;
     if constexpr (UB == 16 && BULK && !OVL) {
-        if (p.fuse_table) kern = collect_kernel<T, UB, BULK, OVL, true>;
+        if (p.neox)
+            kern = p.fuse_table ? collect_kernel<T, UB, BULK, OVL, true, true>
+                                : collect_kernel<T, UB, BULK, OVL, false, true>;
+        else if (p.fuse_table)
+            kern = collect_kernel<T, UB, BULK, OVL, true>;
+    } else {
+        if (p.neox) return set_error(TDKV_EINVAL, "tdkv_collect: NeoX pairs need 16-byte units");
     }
     const int threads = 256;
     const size_t smem = (size_t)4 * p.max_rows * p.row_elems * sizeof(T) +
@@ -649,7 +717,8 @@ static int32_t collect_impl(const void* d_master_k, const void* d_master_v,
                             const int64_t* d_deltas = nullptr,
                             const double* d_inv_freq = nullptr, int64_t source_rows = 0,
                             const tdkv_collect_overlay* d_overlay = nullptr,
-                            int32_t block_size = 0, int32_t nb = 0, int32_t n_jobs = 0) {
+                            int32_t block_size = 0, int32_t nb = 0, int32_t n_jobs = 0,
+                            bool neox = false) {
     if (n_units < 0 || num_layers <= 0 || num_heads <= 0 || head_dim <= 0 || (head_dim & 1))
         return set_error(TDKV_EINVAL, "tdkv_collect: bad geometry L=%d H=%d D=%d", num_layers,
                          num_heads, head_dim);
@@ -668,6 +737,7 @@ static int32_t collect_impl(const void* d_master_k, const void* d_master_v,
 
     CollectParams p;
     p.ovl_inline = 0;
+    p.neox = neox ? 1 : 0;
     p.mk = d_master_k;
     p.mv = d_master_v;
     p.mls = master_layer_stride;
@@ -715,6 +785,14 @@ static int32_t collect_impl(const void* d_master_k, const void* d_master_v,
     if (!aligned(d_master_k, 4) || !aligned(d_master_v, 4))
         return set_error(TDKV_EINVAL, "tdkv_collect: master planes must be 4-byte aligned");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (neox) {
+        // partner units by warp shuffle: whole warps per row, both halves of a
+        // head within one warp
+        const int epu = (int)(16 / esz);
+        if (!(bulk && ub == 16) || (head_dim / 2) % epu || d_overlay)
+            return set_error(TDKV_EINVAL, "tdkv_collect: NeoX pairs need 16-byte-aligned planes "
+                             "and half heads of whole 16-byte units");
+    }
 
     if (d_overlay) {
         // the family restore needs the TMA-staged, 16-byte form
@@ -784,6 +862,7 @@ extern "C" int32_t tdkv_collect_round(const int64_t* d_deltas, int64_t n_table_r
     }();
     const bool rotate = n_table_rows > 0;
     const bool fuse = rotate && (flags & TDKV_ROUND_FUSE_TABLE);
+    const bool neox = rotate && (flags & TDKV_ROUND_NEOX);
     if (rotate && !fuse) {
         const int32_t rc = rope_table_impl(d_deltas, n_table_rows, d_inv_freq, head_dim / 2, dtype,
                                            d_table, stream, pdl);
@@ -793,7 +872,8 @@ extern "C" int32_t tdkv_collect_round(const int64_t* d_deltas, int64_t n_table_r
                         d_jobs, d_dst_rows, rotate && !fuse ? d_table : nullptr, rotate ? 1 : 0,
                         d_dst_k, d_dst_v, dst_layer_stride, num_layers, num_heads, head_dim, dtype,
                         grid_limit, stream, nullptr, nullptr, nullptr, 0, pdl && rotate && !fuse,
-                        fuse ? d_deltas : nullptr, fuse ? d_inv_freq : nullptr);
+                        fuse ? d_deltas : nullptr, fuse ? d_inv_freq : nullptr, 0, nullptr, 0, 0,
+                        0, neox);
 }
 
 extern "C" int32_t tdkv_collect_sources(const void* const* h_src_k, const void* const* h_src_v,

@@ -722,3 +722,76 @@ def test_fused_table_equals_k0_table(dtype, heads, head_dim, agents):
                     want = ref.rope_apply(mk[layer, r0:r0 + spec.seg_len], j.delta)
                     assert np.abs(gk[layer, j.dst_rows] - want).max() <= F32_TOL
                     assert np.array_equal(gv[layer, j.dst_rows], mv[layer, r0:r0 + spec.seg_len])
+
+
+@pytest.mark.parametrize("dtype,heads,head_dim,fused", [
+    ("f32", 8, 64, True), ("f32", 8, 64, False),      # C1 rows: 2 KiB, 16 units per head
+    ("bf16", 4, 128, True), ("bf16", 4, 128, False),  # C2 rows: 1 KiB
+    ("bf16", 8, 128, False),                          # C3 rows: 2 KiB
+    ("bf16", 16, 32, True),                           # 4 units per head
+    ("f32", 2, 256, False),                           # 64 units per head
+])
+def test_collector_neox_pairs_match_oracle(dtype, heads, head_dim, fused):
+    """KVCollector(rope_style="neox") rotates element j of a head with
+    element j + D/2 (one thread owns both units of a pair) -- an extension
+    beyond the reference's interleaved pairs -- and equals
+    oracle.rope_apply_neox: f32 bit for bit, bf16 within the bf16
+    tolerance; V is copied."""
+    base = rounds.CONFIGS["c1"] if dtype == "f32" else rounds.CONFIGS["c2"]
+    spec = base.scaled(num_layers=2, num_heads=heads, head_dim=head_dim, num_agents=19,
+                       num_segments=3, seg_len=40, hist_len=13)
+    mk, mv = rounds.master_planes_host(spec)
+    dt = spec.torch_dtype
+    arena = rounds.make_arena(spec, torch.from_numpy(mk).to(DEV).to(dt),
+                              torch.from_numpy(mv).to(DEV).to(dt))
+    if dtype == "bf16":           # the oracle sees the bf16 values the kernel reads
+        mk = arena.k.float().cpu().numpy()
+        mv = arena.v.float().cpu().numpy()
+    T = spec.tokens_per_agent
+    pool = tk.PagedPool(19 * T + 40, 2, heads, head_dim, dtype=dt, device=DEV)
+    maps = [pool.allocate(T, a) for a in range(19)]
+    col = tk.KVCollector(arena, pool, rope_style="neox")
+    col.auto_graph = False
+    plan = col.plan([j for a, m in enumerate(maps) for j in rounds.agent_jobs(spec, a, m.slots)])
+    plan.fuse_table = fused
+    col.collect(plan)
+    torch.cuda.synchronize()
+    gk, gv = pool.k.float().cpu().numpy(), pool.v.float().cpu().numpy()
+    for a, m in enumerate(maps):
+        for j in rounds.agent_jobs(spec, a, m.slots):
+            r0 = j.segment * spec.seg_len
+            for layer in range(2):
+                want = ref.rope_apply_neox(mk[layer, r0:r0 + spec.seg_len], j.delta)
+                got = gk[layer, j.dst_rows]
+                if dtype == "f32":
+                    assert np.array_equal(got, want)
+                else:
+                    assert np.abs(got - want).max() <= 1e-2 * max(1.0, np.abs(want).max())
+                assert np.array_equal(gv[layer, j.dst_rows], mv[layer, r0:r0 + spec.seg_len])
+    # the interleaved form differs (the pairing is not a no-op)
+    col2 = tk.KVCollector(arena, pool)
+    col2.collect(col2.plan([j for a, m in enumerate(maps)
+                            for j in rounds.agent_jobs(spec, a, m.slots)]))
+    torch.cuda.synchronize()
+    assert not np.array_equal(pool.k.float().cpu().numpy(), gk)
+
+
+def test_collector_neox_rejects_unsupported_layouts():
+    """Half a head must be whole 16-byte units (f32 head_dim 4: 8 bytes); the
+    chunked launch paths refuse rotate-half plans rather than rotate them
+    interleaved."""
+    spec = rounds.CONFIGS["c1"].scaled(num_layers=1, num_heads=2, head_dim=4, num_agents=2,
+                                       num_segments=1, seg_len=8, hist_len=3)
+    mk, mv = rounds.master_planes_host(spec)
+    arena = rounds.make_arena(spec, torch.from_numpy(mk).to(DEV), torch.from_numpy(mv).to(DEV))
+    T = spec.tokens_per_agent
+    pool = tk.PagedPool(2 * T, 1, 2, 4, device=DEV)
+    maps = [pool.allocate(T, a) for a in range(2)]
+    col = tk.KVCollector(arena, pool, rope_style="neox")
+    plan = col.plan([j for a, m in enumerate(maps) for j in rounds.agent_jobs(spec, a, m.slots)])
+    with pytest.raises(tk.TdkvError, match="NeoX"):
+        col.collect(plan)
+    with pytest.raises(ValueError, match="neox"):
+        plan.launch_collect(arena, pool.k, pool.v, pool.layer_stride)
+    with pytest.raises(ValueError, match="rope_style"):
+        tk.KVCollector(arena, pool, rope_style="gptj")

@@ -333,3 +333,22 @@ def test_product_value_types_match_the_reference():
         tk.ReuseGroup(0, [_M(1)])
     with pytest.raises(ValueError):
         tk.ReuseGroup(0, [_M(1), _M(1)])
+
+
+def test_oracle_neox_rotation_is_rotate_half():
+    """oracle.rope_apply_neox (the collector's rope_style="neox" checker)
+    equals the usual rotate-half formula q*cos + rotate_half(q)*sin with the
+    reference's angles, and reduces to rope_apply on a head whose halves are
+    the interleaved pairs."""
+    rng = np.random.default_rng(0)
+    k = rng.standard_normal((5, 3, 16)).astype(np.float32)
+    pos = np.array([0, 3, 17, -4, 900])
+    th = pos[:, None] * ref.inv_freq(16)[None, :]
+    cos = np.concatenate([np.cos(th)] * 2, axis=-1)[:, None, :]
+    sin = np.concatenate([np.sin(th)] * 2, axis=-1)[:, None, :]
+    x = k.astype(np.float64)
+    rot_half = np.concatenate([-x[..., 8:], x[..., :8]], axis=-1)
+    assert np.array_equal(ref.rope_apply_neox(k, pos), (x * cos + rot_half * sin).astype(np.float32))
+    # a permutation maps one pairing onto the other
+    perm = np.stack([np.arange(8), np.arange(8, 16)], axis=-1).reshape(-1)   # (j, j + 8) -> (2j, 2j+1)
+    assert np.array_equal(ref.rope_apply_neox(k, pos)[..., perm], ref.rope_apply(k[..., perm], pos))
