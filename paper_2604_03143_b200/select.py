@@ -17,6 +17,7 @@ Host helpers keep the reference's exact integer semantics:
 from __future__ import annotations
 
 import math
+import threading
 from typing import Dict, List, Optional, Sequence, Tuple
 
 import numpy as np
@@ -81,8 +82,8 @@ _PLANS: Dict[tuple, _SelectPlan] = {}
 def _plan(counts: Sequence[int], device, budgets: Optional[Sequence[int]] = None,
           fraction: Optional[float] = None) -> _SelectPlan:
     """The resident plan of a round shape: budgets given, or ceil(r * n)."""
-    counts = tuple(int(c) for c in counts)
-    key = (device.index, counts, tuple(int(b) for b in budgets) if budgets is not None
+    counts = counts if type(counts) is tuple else tuple(map(int, counts))
+    key = (device.index, counts, tuple(map(int, budgets)) if budgets is not None
            else ("r", float(fraction)))
     p = _PLANS.get(key)
     if p is None:
@@ -95,22 +96,24 @@ def _plan(counts: Sequence[int], device, budgets: Optional[Sequence[int]] = None
 
 
 def _launch_select(mags: torch.Tensor, p: _SelectPlan):
-    dev = mags.device
+    """K4's selection launch into ONE int32 buffer [counts | deviation bits |
+    packed indices] (a single D2H); returns (result offsets, buffer)."""
     m = p.m
-    # one int32 buffer [counts | deviation bits | packed indices] -> a single D2H
-    buf = torch.empty(2 * m + max(p.packed, 1), dtype=torch.int32, device=dev)
-    out_cnt = buf[:m]
-    dev_sum = buf[m:2 * m].view(torch.float32)
-    out_idx = buf[2 * m:]
+    buf = torch.empty(2 * m + max(p.packed, 1), dtype=torch.int32, device=mags.device)
     if m:
-        _lib.call("tdkv_select_important", ptr(mags), ptr(p.d_off), ptr(p.d_budget),
-                  ptr(p.d_out_off), m, p.max_count, ptr(out_idx), ptr(out_cnt), ptr(dev_sum),
-                  stream_handle(dev))
-    return p.out_off, out_idx, out_cnt, dev_sum, buf
+        b = buf.data_ptr()
+        _lib.call("tdkv_select_important", mags.data_ptr(), p.d_off.data_ptr(),
+                  p.d_budget.data_ptr(), p.d_out_off.data_ptr(), m, p.max_count,
+                  b + 8 * m, b, b + 4 * m, stream_handle(mags.device))
+    return p.out_off, buf
 
 
 def _select_device(mags: torch.Tensor, counts: Sequence[int], budgets: Sequence[int]):
-    return _launch_select(mags, _plan(counts, mags.device, budgets=budgets))
+    """(result offsets, indices, counts, deviations) views of the result buffer."""
+    p = _plan(counts, mags.device, budgets=budgets)
+    off, buf = _launch_select(mags, p)
+    m = p.m
+    return off, buf[2 * m:], buf[:m], buf[m:2 * m].view(torch.float32)
 
 
 def select_important(magnitudes, budget: int) -> np.ndarray:
@@ -121,7 +124,7 @@ def select_important(magnitudes, budget: int) -> np.ndarray:
         return np.empty(0, dtype=np.int64)
     dev = magnitudes.device if isinstance(magnitudes, torch.Tensor) else default_device()
     mags = to_device(magnitudes, dev, torch.float32)
-    _, idx, cnt, _, _ = _select_device(mags, [n], [budget])
+    _, idx, cnt, _ = _select_device(mags, [n], [budget])
     k = int(cnt[0].item())
     return idx[:k].cpu().numpy().astype(np.int64)
 
@@ -134,8 +137,7 @@ def selection_kernels(fresh: torch.Tensor, cached: torch.Tensor,
     indices]); member m's indices start at result offset m (the prefix of
     the budgets)."""
     mags = _mags_device(fresh, cached, cached_rows)
-    off, _, _, _, buf = _launch_select(mags, _plan(counts, fresh.device, fraction=fraction))
-    return off, buf
+    return _launch_select(mags, _plan(counts, fresh.device, fraction=fraction))
 
 
 def batched_selection(fresh, cached, counts: Sequence[int], fraction: float,
@@ -158,7 +160,7 @@ def batched_selection(fresh, cached, counts: Sequence[int], fraction: float,
                                                      else cached_rows, dev)
     if rows is None and tuple(c.shape) != tuple(f.shape):
         raise ValueError("key tensors must have identical shapes")
-    counts = [int(x) for x in counts]
+    counts = tuple(map(int, counts))
     if sum(counts) != int(f.shape[0]):
         raise ValueError("member counts must cover every fresh row")
     off, buf = selection_kernels(f, c, rows, counts, fraction)
@@ -166,22 +168,31 @@ def batched_selection(fresh, cached, counts: Sequence[int], fraction: float,
         ledger.record_selection_pass()
     m = len(counts)
     # results through pinned memory (a pageable D2H runs several times slower)
-    staged = torch.empty(buf.shape, dtype=buf.dtype, pin_memory=True)
-    staged.copy_(buf, non_blocking=True)
+    staged = _staging(buf.numel())
+    staged[:buf.numel()].copy_(buf, non_blocking=True)
     torch.cuda.current_stream(buf.device).synchronize()
-    host = staged.numpy()
+    host = staged.numpy()[:buf.numel()]
     cnt_h = host[:m].tolist()
     sums = host[m:2 * m].view(np.float32).tolist()
-    idx_h = host[2 * m:].astype(np.int64)        # one widening for every member
+    idx_h = host[2 * m:].astype(np.int64)        # one widening (and copy) for every member
     starts = off.tolist()
-    out = []
-    for i, n in enumerate(counts):
-        if n == 0:
-            out.append((np.empty(0, dtype=np.int64), 0.0))
-            continue
-        a = starts[i]
-        out.append((idx_h[a:a + cnt_h[i]], sums[i]))
-    return out
+    empty = np.empty(0, dtype=np.int64)
+    return [(idx_h[a:a + k], d) if n else (empty.copy(), 0.0)
+            for n, a, k, d in zip(counts, starts, cnt_h, sums)]
+
+
+_STAGE = threading.local()
+
+
+def _staging(n: int) -> torch.Tensor:
+    """A reused pinned int32 staging buffer of at least ``n`` elements, one
+    per host thread (the caller synchronizes before reading it, so one buffer
+    serves every call of that thread; concurrent groups on other threads
+    have their own)."""
+    buf = getattr(_STAGE, "buf", None)
+    if buf is None or buf.numel() < n:
+        buf = _STAGE.buf = torch.empty(max(n, 1 << 16), dtype=torch.int32, pin_memory=True)
+    return buf
 
 
 def select_master(deviation_scores: Dict[int, float]) -> int:
