@@ -90,6 +90,9 @@ struct CollectParams {
     int32_t n_jobs;
     int32_t ovl_inline;                   // OVL: K1's CTAs run the overlay pass after their items
     int32_t neox;                         // rotate-half pairs (collect_kernel<..., NEOX>)
+    int32_t cs_tiles;                     // tile planes before the cos/sin rows (4, or 2 when
+                                          // every CTA takes one item: no prefetch buffer)
+    int32_t drow_off;                     // byte offset of the destination-row buffers
 };
 
 // Per-job destination metadata is staged in shared memory in groups of
@@ -245,7 +248,11 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
 
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ __align__(8) uint64_t bars[2];
-    __shared__ __align__(16) int64_t s_drow[2][kJobGroup * kMaxTileRows];
+    // per job group: the destination row of every (job, tile row), stride
+    // max_rows, two group buffers -- dynamic, after the tiles and the cos/sin rows
+    const int drow_stride = p.max_rows;
+    int64_t* s_drow0 = reinterpret_cast<int64_t*>(smem + p.drow_off);
+    auto s_drow_b = [&](int mb) { return s_drow0 + (size_t)mb * kJobGroup * drow_stride; };
     __shared__ int4 s_meta[2][kJobGroup];          // tbl_row, tbl_stride, i0
     __shared__ int2 s_map[2][kJobGroup];           // OVL: the tile's K / V payload blocks
 
@@ -322,7 +329,7 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
             for (int jj = tid >> 5; jj < ng; jj += nthr >> 5) {
                 const tdkv_collect_job* jp = p.jobs + jbase + jj;
                 const int64_t off = jp->dst_off + (u.row0 - jp->seg_row0) + lane;
-                cp_async_8(&s_drow[mb][jj * kMaxTileRows + lane], p.dst_rows + off);
+                cp_async_8(s_drow_b(mb) + jj * drow_stride + lane, p.dst_rows + off);
             }
         }
         if (tid < ng) {
@@ -355,7 +362,7 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
     };
     // fused K0: the group's rows live in shared memory after the tiles
     const bool fused = p.fuse_table != 0;
-    Tbl* s_cs = reinterpret_cast<Tbl*>(smem + (size_t)4 * tile_bytes);
+    Tbl* s_cs = reinterpret_cast<Tbl*>(smem + (size_t)p.cs_tiles * tile_bytes);
     auto load_cs_job = [&](Tbl* cs, int jj, const int4& m, int j0) {
         if (fused) {
             const Tbl* trow = s_cs + (size_t)jj * half + j0;
@@ -474,7 +481,7 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
                 // (family restore: a job's payload-sourced planes are the
                 // overlay pass's)
                 if (v_tma && tid < ng && !(OVL && s_map[mb][tid].y >= 0)) {
-                    const int64_t* dr = &s_drow[mb][tid * kMaxTileRows];
+                    const int64_t* dr = s_drow_b(mb) + tid * drow_stride;
                     const int64_t r0 = dr[0];
                     bool contig = true;
                     for (int r = 1; r < u.nrows; ++r) contig &= dr[r] == r0 + r;
@@ -506,7 +513,7 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
 #pragma unroll
                             for (int q = 0; q < kEpu; ++q) cs[q] = trow[q];
                         }
-                        const int64_t* dr = &s_drow[mb][jj * kMaxTileRows];
+                        const int64_t* dr = s_drow_b(mb) + jj * drow_stride;
                         for (int r = sy; r < u.nrows; r += slot_rows) {
                             if (!FUSE && mj.y != 0) {
                                 const Tbl* trow = table + (size_t)(mj.x + (mj.z + r) * mj.y) * half + j0;
@@ -547,7 +554,7 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
                         const Tbl* trow = s_cs + jj * half + j0;
 #pragma unroll
                         for (int q = 0; q < kCs; ++q) cs[q] = trow[q];
-                        const int64_t* dr = &s_drow[mb][jj * kMaxTileRows];
+                        const int64_t* dr = s_drow_b(mb) + jj * drow_stride;
 #pragma unroll 2
                         for (int r = ty; r < u.nrows; r += rows_per_pass) {
                             const size_t o = (size_t)(uint32_t)dr[r] * upr32;
@@ -569,7 +576,7 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
                     for (int jj = 0; jj < ng; ++jj) {
                         const int4 mn = jj + 1 < ng ? s_meta[mb][jj + 1] : m;
                         if (rotate && jj + 1 < ng && mn.y == 0) load_cs_job(csn, jj + 1, mn, j0);
-                        const int64_t* dr = &s_drow[mb][jj * kMaxTileRows];
+                        const int64_t* dr = s_drow_b(mb) + jj * drow_stride;
                         // overlay flags are uniform across the CTA: a plane
                         // taken from the payload is the overlay pass's
                         const bool ovk = OVL && s_map[mb][jj].x >= 0;
@@ -622,11 +629,25 @@ static int32_t launch_collect(const CollectParams& p, int grid_limit, cudaStream
     } else {
         if (p.neox) return set_error(TDKV_EINVAL, "tdkv_collect: NeoX pairs need 16-byte units");
     }
-    const int threads = 256;
-    const size_t smem = (size_t)4 * p.max_rows * p.row_elems * sizeof(T) +
-                        (p.fuse_table ? (size_t)kJobGroup * (p.head_dim / 2) *
-                                            sizeof(typename Elt<T>::Table)
-                                      : 0);
+    // small rounds (the fused-table form): one item per CTA of 128 threads,
+    // every item resident at once -- no item waits behind another's chain of
+    // dependent loads (TDKV_K1_SINGLE=0 keeps the persistent form)
+    static const bool single_env = [] {
+        const char* e = getenv("TDKV_K1_SINGLE");
+        return !(e && e[0] == '0');
+    }();
+    CollectParams pp = p;
+    const int items = p.n_units * p.num_layers;
+    const bool single = UB == 16 && BULK && !OVL && p.fuse_table && single_env &&
+                        grid_limit <= 0;
+    pp.cs_tiles = single ? 2 : 4;
+    const int threads = single ? 128 : 256;
+    const size_t cs_bytes = p.fuse_table ? (size_t)kJobGroup * (p.head_dim / 2) *
+                                               sizeof(typename Elt<T>::Table)
+                                         : 0;
+    pp.drow_off = (int32_t)(((size_t)pp.cs_tiles * p.max_rows * p.row_elems * sizeof(T) +
+                             cs_bytes + 15) / 16 * 16);
+    const size_t smem = (size_t)pp.drow_off + (size_t)2 * kJobGroup * p.max_rows * 8;
     if (smem > 227 * 1024)
         return set_error(TDKV_EINVAL, "tdkv_collect: tile of %d rows needs %zu B of shared memory",
                          p.max_rows, smem);
@@ -636,11 +657,10 @@ static int32_t launch_collect(const CollectParams& p, int grid_limit, cudaStream
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
     if (per_sm < 1) per_sm = 1;
-    const int items = p.n_units * p.num_layers;
-    int grid = sm_count() * per_sm;
+    int grid = single ? items : sm_count() * per_sm;
     if (grid_limit > 0 && grid > grid_limit) grid = grid_limit;
     if (grid > items) grid = items;
-    if (launch_maybe_pdl(kern, dim3(grid), dim3(threads), smem, s, pdl, p) != cudaSuccess)
+    if (launch_maybe_pdl(kern, dim3(grid), dim3(threads), smem, s, pdl, pp) != cudaSuccess)
         return check_launch("tdkv_collect: launch");
     count_launch();
     return check_launch("tdkv_collect");

@@ -18,4 +18,4 @@ for _ in range(10):
     ab.tk.fused_restore_many(ab.handles, ab.spans, ab.pool, ab.maps, 10000.0)
 pr.disable()
 torch.cuda.synchronize()
-pstats.Stats(pr).sort_stats("tottime").print_stats(22)
+pstats.Stats(pr).sort_stats("cumulative").print_stats(30)
