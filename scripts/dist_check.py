@@ -56,6 +56,15 @@ def main():
     rc.collect(rc.plan(jobs))
     torch.cuda.synchronize(dev)
     assert torch.equal(pool.k, ref_pool.k) and torch.equal(pool.v, ref_pool.v), "collect"
+    dump = os.environ.get("TDKV_DIST_DUMP")
+    if dump:
+        # this rank's pool rows of every job, for the test to check against
+        # the CPU oracle (tests/test_gpu_dist.py)
+        rows = np.concatenate([np.asarray(j.dst_rows, np.int64) for j in jobs])
+        sel = torch.from_numpy(rows).to(dev)
+        np.savez(os.path.join(dump, f"rank{rank}.npz"), agents=np.asarray(list(agents)),
+                 slots=np.stack([m.slots for m in maps]),
+                 k=pool.k[:, sel].float().cpu().numpy(), v=pool.v[:, sel].float().cpu().numpy())
     scores = {a: float((a * 7919) % 13) / 4.0 for a in agents}
     master = elect_master(scores, device=dev if backend == "nccl" else torch.device("cpu"))
     want = min(((float((a * 7919) % 13) / 4.0, a) for a in range(spec.num_agents)))[1]
