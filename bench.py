@@ -674,7 +674,24 @@ def run_tdkv(args):
         plan_round()
         torch.cuda.synchronize(dev)
         plan_ms = (time.perf_counter() - tp) * 1e3
+        # the PCIe ceiling of this box: one pinned 512 MiB host -> HBM copy
+        probe_h = torch.empty(1 << 29, dtype=torch.uint8).pin_memory()
+        probe_d = torch.empty(1 << 29, dtype=torch.uint8, device=dev)
+        ceil_ms = []
+        for _ in range(3):
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0.record(stream)
+            probe_d.copy_(probe_h, non_blocking=True)
+            c1.record(stream)
+            torch.cuda.synchronize(dev)
+            ceil_ms.append(c0.elapsed_time(c1))
+        del probe_h, probe_d
+        h2d_ceiling = (1 << 29) / (min(ceil_ms) * 1e-3) / 1e9
+        master_bytes_step = 2 * host_k.numel() * host_k.element_size()
         line["e2e"] = {"value": round(e2e_gbs, 2), "unit": "GB/s",
+                       "h2d_gbs": round(master_bytes_step / wall / 1e9, 2),
+                       "h2d_ceiling_gbs": round(h2d_ceiling, 2),
+                       "h2d_frac": round(master_bytes_step / wall / 1e9 / h2d_ceiling, 4),
                        "h2d_bytes_per_step": int(2 * host_k.numel() * host_k.element_size()
                                                  + p.h2d_bytes),
                        "d2h_bytes_per_step": int(status.numel() * status.element_size()),
