@@ -232,15 +232,20 @@ __device__ __noinline__ void record_violation(const V* mk, const V* mv, const V*
     }
 }
 
+// 128-thread CTAs, 8 per SM, three rounds of 4 loads in flight per thread:
+// as many bytes in flight per SM as 4 CTAs of 256, but twice the CTAs, so one
+// CTA's barrier / look-back / copy phase overlaps the others' streaming
+// (C2 family encode 0.87 -> 0.99 of the copy peak; 64-thread CTAs and 4
+// rounds per thread measured lower)
 template <typename T, int UB>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(128, 8)
     diff_encode_kernel(const tdkv_diff_pair* __restrict__ pairs,
                        const tdkv_diff_out* __restrict__ outs, const uint8_t* __restrict__ hinted,
                        int32_t* flags, int32_t* ticket, int32_t* __restrict__ counts,
                        int32_t* __restrict__ violation, float* __restrict__ viol_maxabs,
                        const CodecGeom g) {
     using V = typename UnitBits<UB>::V;
-    constexpr int kUnroll = 2;
+    constexpr int kUnroll = 3;
     __shared__ int s_tile, s_before;
     if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
     __syncthreads();
@@ -499,20 +504,20 @@ extern "C" int32_t tdkv_diff_encode(const tdkv_diff_pair* d_pairs, const tdkv_di
     const dim3 grid((unsigned)items);
     if (dtype == TDKV_F32) {
         if (ub == 16)
-            diff_encode_kernel<float, 16><<<grid, 256, 0, s>>>(d_pairs, d_outs, d_hinted, d_flags,
+            diff_encode_kernel<float, 16><<<grid, 128, 0, s>>>(d_pairs, d_outs, d_hinted, d_flags,
                                                                d_ticket, d_counts, d_violation,
                                                                d_viol_maxabs, g);
         else
-            diff_encode_kernel<float, 4><<<grid, 256, 0, s>>>(d_pairs, d_outs, d_hinted, d_flags,
+            diff_encode_kernel<float, 4><<<grid, 128, 0, s>>>(d_pairs, d_outs, d_hinted, d_flags,
                                                               d_ticket, d_counts, d_violation,
                                                               d_viol_maxabs, g);
     } else {
         if (ub == 16)
-            diff_encode_kernel<__nv_bfloat16, 16><<<grid, 256, 0, s>>>(
+            diff_encode_kernel<__nv_bfloat16, 16><<<grid, 128, 0, s>>>(
                 d_pairs, d_outs, d_hinted, d_flags, d_ticket, d_counts, d_violation, d_viol_maxabs,
                 g);
         else
-            diff_encode_kernel<__nv_bfloat16, 4><<<grid, 256, 0, s>>>(
+            diff_encode_kernel<__nv_bfloat16, 4><<<grid, 128, 0, s>>>(
                 d_pairs, d_outs, d_hinted, d_flags, d_ticket, d_counts, d_violation, d_viol_maxabs,
                 g);
     }
