@@ -131,6 +131,10 @@ int32_t tdkv_collect_round(const int64_t* d_deltas, int64_t n_table_rows,
  * pair are in its registers.  Requires 16-byte-aligned planes and half heads
  * of whole 16-byte units. */
 #define TDKV_ROUND_NEOX 2
+/* TDKV_ROUND_ONE_ITEM (with TDKV_ROUND_FUSE_TABLE): one work item per CTA of
+ * 128 threads, no persistent prefetch -- for rounds whose items carry few
+ * jobs (the planner sets it for <= 8 jobs per tile). */
+#define TDKV_ROUND_ONE_ITEM 4
 /* d_master_v == d_dst_v == NULL makes a K-only collect (align_cached alone;
  * the reference copies V in _skeleton). */
 

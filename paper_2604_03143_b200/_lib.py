@@ -27,6 +27,7 @@ ROWS_CONTIGUOUS = 1
 ROWS_JOB_MINOR = 2
 ROUND_FUSE_TABLE = 1
 ROUND_NEOX = 2
+ROUND_ONE_ITEM = 4
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

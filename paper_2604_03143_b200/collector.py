@@ -46,6 +46,7 @@ _AUTO_GRAPH = os.environ.get("TDKV_ROUND_GRAPHS", "1") != "0"
 # larger rounds keep K0 (recomputing rows per work item would cost more)
 _FUSE_TABLE = os.environ.get("TDKV_FUSE_TABLE", "auto")
 _FUSE_TABLE_MAX_BYTES = 1 << 30
+_ONE_ITEM_MAX_JOBS = int(os.environ.get("TDKV_ONE_ITEM_MAX_JOBS", 8))
 
 
 def pick_tile_rows(row_bytes: int, budget: int = _TILE_SMEM) -> int:
@@ -345,6 +346,10 @@ class CollectPlan:
         # rotate-half pairs (KVCollector(rope_style="neox")); the reference's
         # interleaved pairs otherwise
         self.neox = False
+        # fused small rounds whose tiles carry few jobs run one item per CTA
+        # (measured ahead of the persistent form up to ~8 jobs per tile)
+        self.one_item = bool(host.units.size) and int(
+            (host.units["job_end"] - host.units["job_begin"]).max()) <= _ONE_ITEM_MAX_JOBS
         self.table = torch.empty((max(host.deltas.size, 1), self.head_dim // 2, 2),
                                  dtype=torch.float64 if self.kv_dtype == torch.float32
                                  else torch.float32, device=self.device)
@@ -467,7 +472,9 @@ class CollectPlan:
                     C.c_int32(self.num_heads), C.c_int32(self.head_dim),
                     C.c_int32(dtype_code(self.kv_dtype)), C.c_int32(int(grid_limit)),
                     C.c_int32((_lib.ROUND_FUSE_TABLE if self.fuse_table else 0)
-                              | (_lib.ROUND_NEOX if self.neox else 0)), stream)
+                              | (_lib.ROUND_NEOX if self.neox else 0)
+                              | (_lib.ROUND_ONE_ITEM if self.fuse_table and self.one_item
+                                 else 0)), stream)
             if len(self._fast) >= 16:
                 self._fast.clear()
             # keep the tensors whose addresses are baked in alive with the entry

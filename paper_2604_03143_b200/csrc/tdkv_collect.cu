@@ -93,6 +93,7 @@ struct CollectParams {
     int32_t cs_tiles;                     // tile planes before the cos/sin rows (4, or 2 when
                                           // every CTA takes one item: no prefetch buffer)
     int32_t drow_off;                     // byte offset of the destination-row buffers
+    int32_t one_item;                     // fused rounds: one item per 128-thread CTA
 };
 
 // Per-job destination metadata is staged in shared memory in groups of
@@ -629,25 +630,31 @@ static int32_t launch_collect(const CollectParams& p, int grid_limit, cudaStream
     } else {
         if (p.neox) return set_error(TDKV_EINVAL, "tdkv_collect: NeoX pairs need 16-byte units");
     }
-    // small rounds (the fused-table form): one item per CTA of 128 threads,
-    // every item resident at once -- no item waits behind another's chain of
-    // dependent loads (TDKV_K1_SINGLE=0 keeps the persistent form)
+    // small rounds (the fused-table form) whose items carry few jobs: one
+    // item per CTA of 128 threads with no prefetch buffer, so no item waits
+    // behind another's chain of dependent loads (the planner's
+    // TDKV_ROUND_ONE_ITEM flag).  Measured: C1 (4 jobs per item) 0.64 -> 0.68
+    // of peak, C2 with 3 agents 0.84 -> 0.96; items of 16-32 jobs (C1 with
+    // 32-64 agents) stay faster persistent.  TDKV_K1_SINGLE=0 disables.
     static const bool single_env = [] {
         const char* e = getenv("TDKV_K1_SINGLE");
         return !(e && e[0] == '0');
     }();
     CollectParams pp = p;
     const int items = p.n_units * p.num_layers;
-    const bool single = UB == 16 && BULK && !OVL && p.fuse_table && single_env &&
-                        grid_limit <= 0;
-    pp.cs_tiles = single ? 2 : 4;
-    const int threads = single ? 128 : 256;
     const size_t cs_bytes = p.fuse_table ? (size_t)kJobGroup * (p.head_dim / 2) *
                                                sizeof(typename Elt<T>::Table)
                                          : 0;
-    pp.drow_off = (int32_t)(((size_t)pp.cs_tiles * p.max_rows * p.row_elems * sizeof(T) +
-                             cs_bytes + 15) / 16 * 16);
-    const size_t smem = (size_t)pp.drow_off + (size_t)2 * kJobGroup * p.max_rows * 8;
+    auto smem_for = [&](int cs_tiles, int32_t& drow_off) {
+        drow_off = (int32_t)(((size_t)cs_tiles * p.max_rows * p.row_elems * sizeof(T) +
+                              cs_bytes + 15) / 16 * 16);
+        return (size_t)drow_off + (size_t)2 * kJobGroup * p.max_rows * 8;
+    };
+    const bool single = UB == 16 && BULK && !OVL && p.fuse_table && p.one_item && single_env &&
+                        grid_limit <= 0;
+    pp.cs_tiles = single ? 2 : 4;
+    const int threads = single ? 128 : 256;
+    const size_t smem = smem_for(pp.cs_tiles, pp.drow_off);
     if (smem > 227 * 1024)
         return set_error(TDKV_EINVAL, "tdkv_collect: tile of %d rows needs %zu B of shared memory",
                          p.max_rows, smem);
@@ -738,7 +745,7 @@ static int32_t collect_impl(const void* d_master_k, const void* d_master_v,
                             const double* d_inv_freq = nullptr, int64_t source_rows = 0,
                             const tdkv_collect_overlay* d_overlay = nullptr,
                             int32_t block_size = 0, int32_t nb = 0, int32_t n_jobs = 0,
-                            bool neox = false) {
+                            bool neox = false, bool one_item = false) {
     if (n_units < 0 || num_layers <= 0 || num_heads <= 0 || head_dim <= 0 || (head_dim & 1))
         return set_error(TDKV_EINVAL, "tdkv_collect: bad geometry L=%d H=%d D=%d", num_layers,
                          num_heads, head_dim);
@@ -757,7 +764,10 @@ static int32_t collect_impl(const void* d_master_k, const void* d_master_v,
 
     CollectParams p;
     p.ovl_inline = 0;
+    p.cs_tiles = 4;
+    p.drow_off = 0;
     p.neox = neox ? 1 : 0;
+    p.one_item = one_item ? 1 : 0;
     p.mk = d_master_k;
     p.mv = d_master_v;
     p.mls = master_layer_stride;
@@ -883,6 +893,7 @@ extern "C" int32_t tdkv_collect_round(const int64_t* d_deltas, int64_t n_table_r
     const bool rotate = n_table_rows > 0;
     const bool fuse = rotate && (flags & TDKV_ROUND_FUSE_TABLE);
     const bool neox = rotate && (flags & TDKV_ROUND_NEOX);
+    const bool one_item = fuse && (flags & TDKV_ROUND_ONE_ITEM);
     if (rotate && !fuse) {
         const int32_t rc = rope_table_impl(d_deltas, n_table_rows, d_inv_freq, head_dim / 2, dtype,
                                            d_table, stream, pdl);
@@ -893,7 +904,7 @@ extern "C" int32_t tdkv_collect_round(const int64_t* d_deltas, int64_t n_table_r
                         d_dst_k, d_dst_v, dst_layer_stride, num_layers, num_heads, head_dim, dtype,
                         grid_limit, stream, nullptr, nullptr, nullptr, 0, pdl && rotate && !fuse,
                         fuse ? d_deltas : nullptr, fuse ? d_inv_freq : nullptr, 0, nullptr, 0, 0,
-                        0, neox);
+                        0, neox, one_item);
 }
 
 extern "C" int32_t tdkv_collect_sources(const void* const* h_src_k, const void* const* h_src_v,
