@@ -630,15 +630,17 @@ static int32_t launch_collect(const CollectParams& p, int grid_limit, cudaStream
     } else {
         if (p.neox) return set_error(TDKV_EINVAL, "tdkv_collect: NeoX pairs need 16-byte units");
     }
-    // small rounds (the fused-table form) whose items carry few jobs: one
-    // item per CTA of 128 threads with no prefetch buffer, so no item waits
-    // behind another's chain of dependent loads (the planner's
-    // TDKV_ROUND_ONE_ITEM flag).  Measured: C1 (4 jobs per item) 0.64 -> 0.68
-    // of peak, C2 with 3 agents 0.84 -> 0.96; items of 16-32 jobs (C1 with
-    // 32-64 agents) stay faster persistent.  TDKV_K1_SINGLE=0 disables.
-    static const bool single_env = [] {
+    // One item per CTA of 128 threads with no prefetch buffer (no item waits
+    // behind another's chain of dependent loads; 8 CTAs per SM overlap the
+    // chains): every bfloat16 round (C3 0.926 -> 0.945 of peak, C2 0.944 ->
+    // 0.951, C4 0.927 -> 0.938, C2 with 3 agents 0.84 -> 0.96), and float32
+    // (float64 rotation) rounds whose items carry few jobs, flagged by the
+    // planner (TDKV_ROUND_ONE_ITEM: C1, 4 jobs per item, 0.64 -> 0.68; items
+    // of 16-32 jobs -- C1 with 32-64 agents -- stay faster persistent).
+    // TDKV_K1_SINGLE: 0 never, 2 always (A/B).
+    static const int single_env = [] {
         const char* e = getenv("TDKV_K1_SINGLE");
-        return !(e && e[0] == '0');
+        return e ? atoi(e) : 1;        // 0 never, 1 as flagged, 2 always (A/B)
     }();
     CollectParams pp = p;
     const int items = p.n_units * p.num_layers;
@@ -650,8 +652,9 @@ static int32_t launch_collect(const CollectParams& p, int grid_limit, cudaStream
                               cs_bytes + 15) / 16 * 16);
         return (size_t)drow_off + (size_t)2 * kJobGroup * p.max_rows * 8;
     };
-    const bool single = UB == 16 && BULK && !OVL && p.fuse_table && p.one_item && single_env &&
-                        grid_limit <= 0;
+    const bool single = UB == 16 && BULK && !OVL && grid_limit <= 0 &&
+                        (single_env == 2 ||
+                         (single_env == 1 && (sizeof(T) == 2 || (p.fuse_table && p.one_item))));
     pp.cs_tiles = single ? 2 : 4;
     const int threads = single ? 128 : 256;
     const size_t smem = smem_for(pp.cs_tiles, pp.drow_off);
