@@ -132,8 +132,9 @@ __device__ __forceinline__ void overlay_rows(const CollectParams& p, long long c
     __shared__ int s_n;
     const int tid = threadIdx.x;
     const int upr = p.row_elems * (int)sizeof(T) / 16;
-    const int tx_n = upr < 256 ? upr : 256;
-    const int rows_per_pass = 256 / tx_n;
+    const int nthr = (int)blockDim.x;             // 256, or 128 inside a one-item K1
+    const int tx_n = upr < nthr ? upr : nthr;
+    const int rows_per_pass = nthr / tx_n;
     const int tx = tid % tx_n, ty = tid / tx_n;
     const Tbl* __restrict__ table = static_cast<const Tbl*>(p.table);
     const int half = p.head_dim >> 1;
@@ -636,7 +637,8 @@ static int32_t launch_collect(const CollectParams& p, int grid_limit, cudaStream
     // 0.951, C4 0.927 -> 0.938, C2 with 3 agents 0.84 -> 0.96), and float32
     // (float64 rotation) rounds whose items carry few jobs, flagged by the
     // planner (TDKV_ROUND_ONE_ITEM: C1, 4 jobs per item, 0.64 -> 0.68; items
-    // of 16-32 jobs -- C1 with 32-64 agents -- stay faster persistent).
+    // of 16-32 jobs -- C1 with 32-64 agents -- stay faster persistent); and
+    // the family restore (OVL: C2 2.62 -> 2.31 ms, C3 0.74 -> 0.66 ms).
     // TDKV_K1_SINGLE: 0 never, 2 always (A/B).
     static const int single_env = [] {
         const char* e = getenv("TDKV_K1_SINGLE");
@@ -652,9 +654,10 @@ static int32_t launch_collect(const CollectParams& p, int grid_limit, cudaStream
                               cs_bytes + 15) / 16 * 16);
         return (size_t)drow_off + (size_t)2 * kJobGroup * p.max_rows * 8;
     };
-    const bool single = UB == 16 && BULK && !OVL && grid_limit <= 0 &&
+    const bool single = UB == 16 && BULK && grid_limit <= 0 &&
                         (single_env == 2 ||
-                         (single_env == 1 && (sizeof(T) == 2 || (p.fuse_table && p.one_item))));
+                         (single_env == 1 &&
+                          (sizeof(T) == 2 || OVL || (p.fuse_table && p.one_item))));
     pp.cs_tiles = single ? 2 : 4;
     const int threads = single ? 128 : 256;
     const size_t smem = smem_for(pp.cs_tiles, pp.drow_off);
