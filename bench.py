@@ -675,10 +675,13 @@ def run_tdkv(args):
         torch.cuda.synchronize(dev)
         plan_ms = (time.perf_counter() - tp) * 1e3
         # the PCIe ceiling of this box: one pinned 512 MiB host -> HBM copy
-        probe_h = torch.empty(1 << 29, dtype=torch.uint8).pin_memory()
+        probe_h = torch.ones(1 << 29, dtype=torch.uint8).pin_memory()   # pages touched
         probe_d = torch.empty(1 << 29, dtype=torch.uint8, device=dev)
+        for _ in range(2):                                            # untimed warm-up
+            probe_d.copy_(probe_h, non_blocking=True)
+        torch.cuda.synchronize(dev)
         ceil_ms = []
-        for _ in range(3):
+        for _ in range(5):
             c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             c0.record(stream)
             probe_d.copy_(probe_h, non_blocking=True)
