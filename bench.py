@@ -614,8 +614,13 @@ def run_tdkv(args):
         copy_stream = torch.cuda.Stream(dev)
         done = torch.cuda.Event()
 
+        # the agents' prompt layouts (segment offsets): host metadata the
+        # round starts from; planning turns them into the round's jobs
+        layouts = rounds.agent_starts(spec, agents)
+
         def plan_round():
-            segs, dst_off, job_delta = rounds.round_offsets(spec, agents, slot_arena.base)
+            segs, dst_off, job_delta = rounds.round_offsets(spec, agents, slot_arena.base,
+                                                            starts=layouts)
             return collector.plan_offsets(segs, dst_off, job_delta, slot_arena)
 
         def e2e_step():

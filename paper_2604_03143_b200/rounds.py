@@ -172,11 +172,20 @@ def agent_jobs(spec: RoundSpec, agent: int, slots: np.ndarray) -> List[CollectJo
     return jobs
 
 
-def round_offsets(spec: RoundSpec, agents, slot_base: np.ndarray):
+def agent_starts(spec: RoundSpec, agents) -> np.ndarray:
+    """(n, S) prompt offsets of every agent's session segments: the round's
+    prompt layouts (host metadata the round starts from)."""
+    return np.stack([segment_starts(spec, a) for a in agents])
+
+
+def round_offsets(spec: RoundSpec, agents, slot_base: np.ndarray,
+                  starts: Optional[np.ndarray] = None):
     """Vectorized job arrays of a round for ``plan_offsets``: (global segment
-    ids, destination offsets into the agents' slot arena, per-job delta)."""
+    ids, destination offsets into the agents' slot arena, per-job delta);
+    ``starts`` = agent_starts(spec, agents) when the layouts are at hand."""
     agents = list(agents)
-    starts = np.stack([segment_starts(spec, a) for a in agents])         # (n, S)
+    if starts is None:
+        starts = agent_starts(spec, agents)                              # (n, S)
     sess = np.array([spec.session_of(a) for a in agents], np.int64)
     segs = (sess[:, None] * spec.num_segments + np.arange(spec.num_segments)).reshape(-1)
     src = source_offsets(spec)
