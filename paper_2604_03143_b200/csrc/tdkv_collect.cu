@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
         for (int q = 0; q < kCs; ++q) cs[q] = __ldg(trow + q);
     };
     // rotate one unit's interleaved pairs in place
-    auto rotate_unit_k = [&](V& kv, const Tbl* cs, bool) {
+    auto rotate_unit_k = [&](V& kv, const Tbl* cs) {
         T* e = reinterpret_cast<T*>(&kv);
 #pragma unroll
         for (int q = 0; q < kPairs; ++q) rot_pair(e[2 * q], e[2 * q + 1], cs[q]);
@@ -546,7 +546,6 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
                 const uint32_t upr32 = (uint32_t)upr;
                 for (int c = tx; c < upr; c += tx_n) {
                     const int j0 = c == tx ? j0_tx : angle0(c);
-                    const bool fh = true;
                     V* __restrict__ dkc = reinterpret_cast<V*>(dk_l) + c;
                     V* __restrict__ dvc = reinterpret_cast<V*>(dv_l) + c;
                     const V* skc = sk + c;
@@ -561,7 +560,7 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
                         for (int r = ty; r < u.nrows; r += rows_per_pass) {
                             const size_t o = (size_t)(uint32_t)dr[r] * upr32;
                             V kv = skc[r * upr];
-                            rotate_unit_k(kv, cs, fh);
+                            rotate_unit_k(kv, cs);
                             st_stream(dkc + o, kv);
                             if (has_v && !v_tma) st_stream(dvc + o, svc[r * upr]);
                         }
@@ -571,7 +570,6 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
             } else if (ty < rows_per_pass) {
                 for (int c = tx; c < upr; c += tx_n) {
                     const int j0 = c == tx ? j0_tx : angle0(c);
-                    const bool fh = true;
                     Tbl cs[kCs], csn[kCs];
                     int4 m = s_meta[mb][0];
                     if (rotate && m.y == 0) load_cs_job(cs, 0, m, j0);
@@ -589,7 +587,7 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
                             V kv = sk[r * upr + c];
                             if (rotate) {
                                 if (m.y != 0) load_cs(cs, m.x + (m.z + r) * m.y, j0);
-                                rotate_unit_k(kv, cs, fh);
+                                rotate_unit_k(kv, cs);
                             }
                             if (!ovk)
                                 st_stream(reinterpret_cast<V*>(dk_l + (size_t)drow * p.row_elems) + c,
