@@ -719,6 +719,8 @@ def run_tdkv(args):
     if not args.no_codec and not args.profile:
         line["codec"] = codec_bench(tk, spec, pool, maps, dev, args, peak)
         line["selection"] = selection_bench(tk, spec, pool, maps, dev, args, peak)
+        if world == 1:
+            line["dropin"] = dropin_bench(tk, args)
         line["recompute"] = recompute_bench(dev, args)
         line["recovery"] = recovery_bench(dev, args)
         if args.codec_sweep:
@@ -871,6 +873,79 @@ def planning_bench(spec_name: str = "c5", agents: int = 0):
 def rounds_shard(spec, rank, world):
     from paper_2604_03143_b200 import rounds
     return rounds.shard(spec.num_agents, rank, world)
+
+
+def dropin_bench(tk, args):
+    """The reference contract end to end: ``skeleton_values`` +
+    ``align_cached`` (pic.py:203-204, 208-235) on HOST numpy contexts -- the
+    drop-in call a reference caller makes -- on BASELINE configs[0] (8 agents
+    x 4 shared 256-token blocks, L=2, H=8, D=64, float32): masters and
+    contexts go host -> HBM, K1 runs, the rows come back over PCIe into the
+    numpy contexts.  Timed beside the oracle's collector on the same inputs
+    (numpy, one host core)."""
+    import torch
+    from paper_2604_03143_b200 import rounds
+    from oracle import roundkv_port as ref   # CPU timing leg only
+    spec = rounds.CONFIGS["c1"]
+    mk, mv = rounds.master_planes_host(spec)
+    src = rounds.source_offsets(spec)
+    L, H, D, n = spec.num_layers, spec.num_heads, spec.head_dim, spec.seg_len
+    masters = [tk.LayeredKv(np.ascontiguousarray(mk[:, g * n:(g + 1) * n]),
+                            np.ascontiguousarray(mv[:, g * n:(g + 1) * n]),
+                            np.arange(src[g], src[g] + n)) for g in range(spec.total_segments)]
+
+    class _Hit:
+        def __init__(self, kv, target, delta):
+            self.kv, self.target_idx, self.delta = kv, target, delta
+
+    class _Member:
+        def __init__(self, hits):
+            self.hits = hits
+
+    T = spec.tokens_per_agent
+    members, jobs = [], []
+    for a in range(spec.num_agents):
+        starts = rounds.segment_starts(spec, a)
+        hits = []
+        for sgm in range(spec.num_segments):
+            tgt = np.arange(starts[sgm], starts[sgm] + n, dtype=np.int64)
+            delta = tgt - masters[sgm].positions
+            hits.append(_Hit(masters[sgm], tgt, delta))
+            jobs.append(ref.CollectJob(a, masters[sgm].k, masters[sgm].v, tgt, delta))
+        members.append(_Member(hits))
+
+    def fresh():
+        return [(np.zeros((L, T, H, D), np.float32), np.zeros((L, T, H, D), np.float32))
+                for _ in range(spec.num_agents)]
+
+    def ours(ctx):
+        tk.skeleton_values(members, ctx)
+        tk.align_cached(members, ctx, 10000.0)
+
+    for _ in range(3):
+        ours(fresh())
+    times = []
+    for _ in range(max(5, min(args.steps, 20))):
+        ctx = fresh()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ours(ctx)
+        times.append(time.perf_counter() - t0)
+    t_ours = float(np.median(times))
+    ctx_ref = fresh()
+    t0 = time.perf_counter()
+    ref.collect_into_contexts(jobs, ctx_ref, 10000.0)
+    t_ref = time.perf_counter() - t0
+    same_v = all(np.array_equal(a[1], b[1]) for a, b in zip(ctx, ctx_ref))
+    err_k = max(float(np.abs(a[0] - b[0]).max()) for a, b in zip(ctx, ctx_ref))
+    moved = spec.collector_bytes()
+    return {"path": "skeleton_values + align_cached on host numpy contexts (the reference "
+                    "contract): masters and rows over PCIe both ways",
+            "config": spec.name, "ms_per_round": round(t_ours * 1e3, 3),
+            "gbs": round(moved / t_ours / 1e9, 2),
+            "cpu_oracle_ms_1core": round(t_ref * 1e3, 2),
+            "speedup_vs_cpu": round(t_ref / t_ours, 1),
+            "v_bit_exact": bool(same_v), "k_max_abs_err": err_k}
 
 
 def selection_bench(tk, spec, pool, maps, dev, args, peak):

@@ -809,10 +809,20 @@ def _scatter_back(jobs, offs, staged: torch.Tensor, contexts, plane: int,
                   staged_v: Optional[torch.Tensor] = None) -> None:
     first = contexts[jobs[0][0]][plane]
     if is_host(first):
-        host = to_host(staged)
+        # one D2H through pinned memory (a pageable read runs several times
+        # slower), then each hit's rows into its context: a slice copy when
+        # the target rows are one contiguous run (prompt segments are)
+        pinned = torch.empty(staged.shape, dtype=staged.dtype, pin_memory=True)
+        pinned.copy_(staged)
+        host = pinned.float().numpy() if staged.dtype == torch.bfloat16 else pinned.numpy()
         for (i, hit), off in zip(jobs, offs):
-            n = len(hit.target_idx)
-            contexts[i][plane][:, np.asarray(hit.target_idx)] = host[:, off:off + n]
+            tgt = np.asarray(hit.target_idx)
+            n = tgt.size
+            if n and int(tgt[-1]) - int(tgt[0]) == n - 1 and (n == 1 or (np.diff(tgt) == 1).all()):
+                t0 = int(tgt[0])
+                contexts[i][plane][:, t0:t0 + n] = host[:, off:off + n]
+            else:
+                contexts[i][plane][:, tgt] = host[:, off:off + n]
         return
     L, R, H, D = staged.shape
     hd = H * D
