@@ -805,24 +805,85 @@ def collect_into_contexts(members, contexts, rope_base: float,
     _scatter_back(jobs, offs, staged_k, contexts, plane=0, staged_v=staged_v)
 
 
+# host threads for the numpy side of the host-context read-back (numpy's
+# copies release the GIL); TDKV_HOST_THREADS=1 keeps it on the caller thread
+_HOST_THREADS = int(os.environ.get("TDKV_HOST_THREADS", min(8, os.cpu_count() or 1)))
+_host_pool = None
+# read-backs below this many bytes stay one chunk on the caller thread
+_HOST_CHUNK_MIN = 4 << 20
+
+
+def _host_executor():
+    global _host_pool
+    if _host_pool is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _host_pool = ThreadPoolExecutor(_HOST_THREADS, thread_name_prefix="tdkv-host")
+    return _host_pool
+
+
+def _put_rows(ctx_plane, tgt, rows) -> None:
+    """``ctx_plane[:, tgt] = rows`` -- a slice copy when the targets are one
+    contiguous run (prompt segments are)."""
+    n = tgt.size
+    if n and int(tgt[-1]) - int(tgt[0]) == n - 1 and (n == 1 or (np.diff(tgt) == 1).all()):
+        t0 = int(tgt[0])
+        ctx_plane[:, t0:t0 + n] = rows
+    else:
+        ctx_plane[:, tgt] = rows
+
+
+def _scatter_back_host(jobs, offs, staged: torch.Tensor, contexts, plane: int) -> None:
+    """Staged rows (device) -> host numpy contexts.  The D2H goes through
+    pinned memory (a pageable read runs several times slower) in chunks of
+    whole hits, each chunk's rows handed to a host thread as soon as its copy
+    event fires, so PCIe and the host-side writes into the contexts overlap."""
+    L, R = staged.shape[0], staged.shape[1]
+    pinned = torch.empty(staged.shape, dtype=staged.dtype, pin_memory=True)
+    nbytes = staged.numel() * staged.element_size()
+    # chunks end at member boundaries (a member's hits stay on one thread, in
+    # order, so overlapping targets keep the serial last-write-wins result);
+    # one chunk when the read-back is small or two members share a context
+    planes = [id(contexts[i][plane]) for i in {i for i, _ in jobs}]
+    bounds = [0]
+    if nbytes >= _HOST_CHUNK_MIN and _HOST_THREADS > 1 and len(set(planes)) == len(planes):
+        want = R / min(2 * _HOST_THREADS, len(planes))
+        for k in range(1, len(jobs)):
+            if jobs[k][0] != jobs[k - 1][0] and offs[k] >= want * len(bounds):
+                bounds.append(k)
+    bounds.append(len(jobs))
+    row_of = list(offs) + [R]
+    stream = torch.cuda.current_stream(staged.device)
+    events = []
+    for c in range(len(bounds) - 1):
+        r0, r1 = row_of[bounds[c]], row_of[bounds[c + 1]]
+        for layer in range(L):
+            pinned[layer, r0:r1].copy_(staged[layer, r0:r1], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        events.append(ev)
+
+    def work(c):
+        events[c].synchronize()
+        r0, r1 = row_of[bounds[c]], row_of[bounds[c + 1]]
+        part = pinned[:, r0:r1]
+        host = part.float().numpy() if staged.dtype == torch.bfloat16 else part.numpy()
+        for k in range(bounds[c], bounds[c + 1]):
+            i, hit = jobs[k]
+            tgt = np.asarray(hit.target_idx)
+            o = offs[k] - r0
+            _put_rows(contexts[i][plane], tgt, host[:, o:o + tgt.size])
+
+    if len(events) == 1:
+        work(0)
+    else:
+        list(_host_executor().map(work, range(len(events))))
+
+
 def _scatter_back(jobs, offs, staged: torch.Tensor, contexts, plane: int,
                   staged_v: Optional[torch.Tensor] = None) -> None:
     first = contexts[jobs[0][0]][plane]
     if is_host(first):
-        # one D2H through pinned memory (a pageable read runs several times
-        # slower), then each hit's rows into its context: a slice copy when
-        # the target rows are one contiguous run (prompt segments are)
-        pinned = torch.empty(staged.shape, dtype=staged.dtype, pin_memory=True)
-        pinned.copy_(staged)
-        host = pinned.float().numpy() if staged.dtype == torch.bfloat16 else pinned.numpy()
-        for (i, hit), off in zip(jobs, offs):
-            tgt = np.asarray(hit.target_idx)
-            n = tgt.size
-            if n and int(tgt[-1]) - int(tgt[0]) == n - 1 and (n == 1 or (np.diff(tgt) == 1).all()):
-                t0 = int(tgt[0])
-                contexts[i][plane][:, t0:t0 + n] = host[:, off:off + n]
-            else:
-                contexts[i][plane][:, tgt] = host[:, off:off + n]
+        _scatter_back_host(jobs, offs, staged, contexts, plane)
         return
     L, R, H, D = staged.shape
     hd = H * D

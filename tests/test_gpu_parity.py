@@ -145,6 +145,56 @@ def test_align_cached_device_contexts():
         assert np.array_equal(ctx[a][1].cpu().numpy()[:, shared], z[f"agent{a}_v_shared"])
 
 
+def test_align_cached_host_contexts_chunked_readback():
+    """configs[0]-sized host contexts take the chunked, threaded read-back
+    (one chunk per member run): equal to the oracle collector (V bit for bit,
+    K bit for bit in float32); a member whose hits overlap keeps the serial
+    last-write-wins result; two members sharing one context fall back to one
+    chunk and still match a serial scatter."""
+    spec = rounds.CONFIGS["c1"]
+    mk, mv = rounds.master_planes_host(spec)
+    src = rounds.source_offsets(spec)
+    L, H, D, n = spec.num_layers, spec.num_heads, spec.head_dim, spec.seg_len
+    masters = [tk.LayeredKv(np.ascontiguousarray(mk[:, g * n:(g + 1) * n]),
+                            np.ascontiguousarray(mv[:, g * n:(g + 1) * n]),
+                            np.arange(src[g], src[g] + n)) for g in range(spec.total_segments)]
+    T = spec.tokens_per_agent
+    members, jobs = [], []
+    for a in range(spec.num_agents):
+        starts = rounds.segment_starts(spec, a)
+        hits = []
+        for sgm in range(spec.num_segments):
+            tgt = np.arange(starts[sgm], starts[sgm] + n, dtype=np.int64)
+            hits.append(_Hit(masters[sgm], tgt, tgt - masters[sgm].positions))
+        if a == 3:      # a late hit overwriting part of an earlier one
+            part = tk.LayeredKv(np.ascontiguousarray(masters[1].k[:, :n // 2]),
+                                np.ascontiguousarray(masters[1].v[:, :n // 2]),
+                                masters[1].positions[:n // 2])
+            tgt = np.arange(starts[0] + 5, starts[0] + 5 + n // 2, dtype=np.int64)
+            hits.append(_Hit(part, tgt, tgt - part.positions))
+        for h in hits:
+            jobs.append(ref.CollectJob(a, h.kv.k, h.kv.v, h.target_idx, h.delta))
+        members.append(_Member(hits))
+    ctx = [(np.zeros((L, T, H, D), np.float32), np.zeros((L, T, H, D), np.float32))
+           for _ in range(spec.num_agents)]
+    want = [(np.zeros((L, T, H, D), np.float32), np.zeros((L, T, H, D), np.float32))
+            for _ in range(spec.num_agents)]
+    tk.skeleton_values(members, ctx)
+    tk.align_cached(members, ctx, 10000.0)
+    ref.collect_into_contexts(jobs, want, 10000.0)
+    for a in range(spec.num_agents):
+        assert np.array_equal(ctx[a][1], want[a][1])
+        assert np.array_equal(ctx[a][0], want[a][0])
+    # members 0 and 1 share one context pair: serial order, member 1 last
+    shared = (np.zeros((L, T, H, D), np.float32), np.zeros((L, T, H, D), np.float32))
+    ctx2 = [shared, shared] + ctx[2:]
+    tk.align_cached(members, ctx2, 10000.0)
+    want2 = (np.zeros((L, T, H, D), np.float32), np.zeros((L, T, H, D), np.float32))
+    ref.collect_into_contexts([j for j in jobs if j.agent in (0, 1)],
+                              [want2, want2], 10000.0)
+    assert np.array_equal(shared[0], want2[0])
+
+
 def _collect_case(spec: rounds.RoundSpec, tile_rows=None, seed=0):
     """Run the pool-form collector on a synthetic round and the oracle on the
     same (f32-upcast) inputs; return (pool_k, pool_v, want_k, want_v, slots)."""
