@@ -1314,7 +1314,19 @@ def codec_bench(tk, spec, pool, maps, dev, args, peak, frac=None, hint_all=False
     torch.cuda.synchronize(dev)
     unpack_s = time.perf_counter() - t0
     unpack_bytes = sum(len(w) for w in images[:8])
+    # the same images as Python bytes objects (pageable: what a reader of
+    # files / sockets holds) -- staged through the pinned ring
+    owned = [bytes(w) for w in images[:8]]
     del images
+    for w in owned[:2]:               # both pinned ring buffers allocated
+        tk.deserialize_to_device(w, dev, pool.k.dtype)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for w in owned:
+        tk.deserialize_to_device(w, dev, pool.k.dtype)
+    torch.cuda.synchronize(dev)
+    unpack_bytes_s = time.perf_counter() - t0
+    del owned
     return {
         "mirrors": n_mirrors, "changed_block_fraction": round(changed / (n_mirrors * spec.num_layers * nb), 4),
         "encode_gbs": round(enc_bytes / enc_s / 1e9, 1),
@@ -1344,10 +1356,14 @@ def codec_bench(tk, spec, pool, maps, dev, args, peak, frac=None, hint_all=False
         "payload_ratio_mean": round(float(np.mean([dense / max(1, b) for b in pay_bytes])), 3),
         "wire_pack_gbs": round(wire_total / pack_s / 1e9, 2),
         "wire_unpack_gbs": round(unpack_bytes / unpack_s / 1e9, 2),
+        "wire_unpack_pageable_gbs": round(unpack_bytes / unpack_bytes_s / 1e9, 2),
         "wire_note": "serialize_many of the family (GPU pack, one D2H into pinned memory, "
                      "images as memoryviews) and "
                      "deserialize_to_device of 8 images (host parse, one H2D each, GPU "
-                     "unpack); wall clock after one untimed call, float32 wire bytes",
+                     "unpack): wire_unpack_gbs from those pinned views (H2D straight from "
+                     "them), wire_unpack_pageable_gbs from bytes copies of them (host threads "
+                     "stage each into a pinned ring buffer); wall clock after one untimed "
+                     "call, float32 wire bytes",
         "bytes": "encode: 2*dense + payload + 4*changed per mirror (host read included); "
                  "fused decode: 2*dense per mirror (K0+K3 device time)",
     }

@@ -49,6 +49,14 @@ int32_t tdkv_version(void);
 const char* tdkv_last_error(void);
 /* Number of kernels this library has launched in the process so far. */
 int64_t tdkv_launch_count(void);
+/* 1 when p lies in page-locked host memory (cudaHostAlloc / cudaHostRegister),
+ * else 0.  Lets a caller holding a wire image in pinned memory skip the
+ * staging copy of deserialize_to_device (diffstore.py:242-306 parses from a
+ * bytes object; the GPU form moves the image over PCIe). */
+int32_t tdkv_host_is_pinned(const void* p);
+/* Asynchronous host -> device copy of nbytes on `stream` (full PCIe rate
+ * only from page-locked memory). */
+int32_t tdkv_copy_h2d(void* d_dst, const void* h_src, int64_t nbytes, void* stream);
 
 /* ------------------------------------------------------------------------
  * K0  rotary table.  Replaces the angle/cos/sin part of rope_apply

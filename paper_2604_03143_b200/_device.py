@@ -6,6 +6,7 @@ byte of KV arithmetic runs in libtdkv.so.
 from __future__ import annotations
 
 import ctypes
+import os
 from typing import Optional, Union
 
 import numpy as np
@@ -101,3 +102,95 @@ def to_host(t: torch.Tensor) -> np.ndarray:
     if t.dtype == torch.bfloat16:
         t = t.float()
     return t.detach().cpu().numpy()
+
+
+# host threads for the host side of PCIe transfers (numpy's large copies
+# release the GIL); TDKV_HOST_THREADS=1 keeps that work on the caller thread
+HOST_THREADS = int(os.environ.get("TDKV_HOST_THREADS", min(8, os.cpu_count() or 1)))
+_host_pool = None
+
+
+def host_executor():
+    global _host_pool
+    if _host_pool is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _host_pool = ThreadPoolExecutor(HOST_THREADS, thread_name_prefix="tdkv-host")
+    return _host_pool
+
+
+# host bytes go to the device through a ring of two pinned staging buffers
+# per device (grown to the largest image seen): the host threads fill one
+# buffer in chunks of _STAGE_CHUNK while the previous image's H2D drains from
+# the other.  Measured on the B200 box for a 51 MB image: a fresh pinned
+# block per call 3.2 ms, H2D chunk by chunk during the fill 2.5 ms, a reused
+# buffer filled by 8 threads + one H2D ~1.8 ms (scripts/stage_probe.py).
+_STAGE_CHUNK = 2 << 20
+_stage_rings: dict = {}
+_stage_lock = None
+_pinned_inflight: list = []       # (event, source buffer) of direct H2Ds
+
+
+class _Staging:
+    __slots__ = ("buf", "event")
+
+    def __init__(self):
+        self.buf = None
+        self.event = None
+
+
+def bytes_to_device(buf, device: torch.device, pad: int = 0):
+    """Host bytes (any buffer) -> a device uint8 tensor of len(buf) + pad
+    bytes through pinned staging (one H2D on the current stream; large
+    images are copied into the staging buffer by the host threads).
+    Returns the device tensor; the trailing ``pad`` bytes are unspecified."""
+    global _stage_lock
+    import threading
+    if _stage_lock is None:
+        _stage_lock = threading.Lock()
+    src = np.frombuffer(buf, np.uint8)
+    n = src.size
+    out = torch.empty(n + pad, dtype=torch.uint8, device=device)
+    lib = _lib.load()
+    addr = src.ctypes.data if n else 0
+    if n and lib.tdkv_host_is_pinned(addr) and lib.tdkv_host_is_pinned(addr + n - 1):
+        # already page-locked (e.g. serialize_many(copy=False) views): one
+        # H2D straight from the caller's buffer, kept alive until it drains
+        _lib.call("tdkv_copy_h2d", ptr(out), addr, n, stream_handle(device))
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(device))
+        with _stage_lock:
+            _pinned_inflight[:] = [(e, b) for e, b in _pinned_inflight if not e.query()]
+            _pinned_inflight.append((ev, buf))
+        return out
+    with _stage_lock:
+        ring = _stage_rings.setdefault(device, [[_Staging(), _Staging()], 0])
+        st = ring[0][ring[1]]
+        ring[1] ^= 1
+        if st.event is not None:
+            st.event.synchronize()          # its previous H2D has drained
+        if st.buf is None or st.buf.numel() < n + pad:
+            st.buf = torch.empty(max(n + pad, 1 << 20), dtype=torch.uint8, pin_memory=True)
+        sv = st.buf.numpy()
+        if n < 2 * _STAGE_CHUNK or HOST_THREADS <= 1:
+            sv[:n] = src
+        else:
+            bounds = list(range(0, n, _STAGE_CHUNK)) + [n]
+
+            def fill(c):
+                a, b = bounds[c], bounds[c + 1]
+                sv[a:b] = src[a:b]
+
+            list(host_executor().map(fill, range(len(bounds) - 1)))
+        out.copy_(st.buf[:n + pad], non_blocking=True)
+        st.event = torch.cuda.Event()
+        st.event.record(torch.cuda.current_stream(device))
+    return out
+
+
+def release_inflight() -> None:
+    """Drop the references bytes_to_device keeps to pinned source buffers
+    whose H2D has drained (so their pinned blocks can be reused)."""
+    if _stage_lock is None:
+        return
+    with _stage_lock:
+        _pinned_inflight[:] = [(e, b) for e, b in _pinned_inflight if not e.query()]

@@ -101,7 +101,8 @@ assert COLLECT_OVERLAY.itemsize == 32
 assert DIFF_PAIR.itemsize == 32 and DIFF_OUT.itemsize == 40 and ROWS_JOB.itemsize == 112
 
 EXPORTS = (
-    "tdkv_version", "tdkv_last_error", "tdkv_launch_count", "tdkv_rope_table",
+    "tdkv_version", "tdkv_last_error", "tdkv_launch_count", "tdkv_host_is_pinned",
+    "tdkv_copy_h2d", "tdkv_rope_table",
     "tdkv_collect", "tdkv_collect_round", "tdkv_collect_sources", "tdkv_restore_family", "tdkv_diff_compare", "tdkv_diff_compact", "tdkv_diff_encode", "tdkv_rows",
     "tdkv_keydiff", "tdkv_select_important", "tdkv_gemm", "tdkv_tf32_split", "tdkv_gemm_tf32x3",
     "tdkv_qkv_rope", "tdkv_attention",
@@ -120,6 +121,8 @@ _SIGS = {
     "tdkv_version": (_I32, []),
     "tdkv_last_error": (ctypes.c_char_p, []),
     "tdkv_launch_count": (_I64, []),
+    "tdkv_host_is_pinned": (_I32, [_P]),
+    "tdkv_copy_h2d": (_I32, [_P, _P, _I64, _P]),
     "tdkv_rope_table": (_I32, [_P, _I64, _P, _I32, _I32, _P, _P]),
     "tdkv_collect": (_I32, [_P, _P, _I64, _P, _I32, _I32, _P, _P, _P, _I32, _P, _P, _I64,
                             _I32, _I32, _I32, _I32, _I32, _P]),

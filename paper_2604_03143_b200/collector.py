@@ -27,8 +27,8 @@ import numpy as np
 import torch
 
 from . import _kernels, _lib
-from ._device import (default_device, dtype_code, h2d, is_host, ptr, stream_handle, to_device,
-                      to_host, upload)
+from ._device import (HOST_THREADS, default_device, dtype_code, h2d, host_executor, is_host, ptr,
+                      stream_handle, to_device, to_host, upload)
 from .core import LayeredKv
 from .ledger import CostLedger
 
@@ -805,20 +805,8 @@ def collect_into_contexts(members, contexts, rope_base: float,
     _scatter_back(jobs, offs, staged_k, contexts, plane=0, staged_v=staged_v)
 
 
-# host threads for the numpy side of the host-context read-back (numpy's
-# copies release the GIL); TDKV_HOST_THREADS=1 keeps it on the caller thread
-_HOST_THREADS = int(os.environ.get("TDKV_HOST_THREADS", min(8, os.cpu_count() or 1)))
-_host_pool = None
 # read-backs below this many bytes stay one chunk on the caller thread
 _HOST_CHUNK_MIN = 4 << 20
-
-
-def _host_executor():
-    global _host_pool
-    if _host_pool is None:
-        from concurrent.futures import ThreadPoolExecutor
-        _host_pool = ThreadPoolExecutor(_HOST_THREADS, thread_name_prefix="tdkv-host")
-    return _host_pool
 
 
 def _put_rows(ctx_plane, tgt, rows) -> None:
@@ -845,8 +833,8 @@ def _scatter_back_host(jobs, offs, staged: torch.Tensor, contexts, plane: int) -
     # one chunk when the read-back is small or two members share a context
     planes = [id(contexts[i][plane]) for i in {i for i, _ in jobs}]
     bounds = [0]
-    if nbytes >= _HOST_CHUNK_MIN and _HOST_THREADS > 1 and len(set(planes)) == len(planes):
-        want = R / min(2 * _HOST_THREADS, len(planes))
+    if nbytes >= _HOST_CHUNK_MIN and HOST_THREADS > 1 and len(set(planes)) == len(planes):
+        want = R / min(2 * HOST_THREADS, len(planes))
         for k in range(1, len(jobs)):
             if jobs[k][0] != jobs[k - 1][0] and offs[k] >= want * len(bounds):
                 bounds.append(k)
@@ -876,7 +864,7 @@ def _scatter_back_host(jobs, offs, staged: torch.Tensor, contexts, plane: int) -
     if len(events) == 1:
         work(0)
     else:
-        list(_host_executor().map(work, range(len(events))))
+        list(host_executor().map(work, range(len(events))))
 
 
 def _scatter_back(jobs, offs, staged: torch.Tensor, contexts, plane: int,

@@ -52,4 +52,25 @@ const char* tdkv_last_error(void) { return tdkv::g_err; }
 
 int64_t tdkv_launch_count(void) { return tdkv::g_launches.load(std::memory_order_relaxed); }
 
+int32_t tdkv_host_is_pinned(const void* p) {
+    if (p == nullptr) return 0;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();  // a pageable pointer is not an error to keep
+        return 0;
+    }
+    return a.type == cudaMemoryTypeHost ? 1 : 0;
+}
+
+int32_t tdkv_copy_h2d(void* d_dst, const void* h_src, int64_t nbytes, void* stream) {
+    if (nbytes < 0) return tdkv::set_error(TDKV_EINVAL, "tdkv_copy_h2d: negative size");
+    if (nbytes == 0) return TDKV_OK;
+    if (d_dst == nullptr || h_src == nullptr)
+        return tdkv::set_error(TDKV_EINVAL, "tdkv_copy_h2d: null pointer");
+    cudaError_t e = cudaMemcpyAsync(d_dst, h_src, (size_t)nbytes, cudaMemcpyHostToDevice,
+                                    (cudaStream_t)stream);
+    if (e != cudaSuccess) return tdkv::set_error(TDKV_ECUDA, "tdkv_copy_h2d: %s", cudaGetErrorString(e));
+    return TDKV_OK;
+}
+
 }  // extern "C"

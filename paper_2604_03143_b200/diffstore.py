@@ -28,8 +28,8 @@ import numpy as np
 import torch
 
 from . import _kernels, _lib
-from ._device import (default_device, dtype_code, h2d, ptr, stream_handle, to_device,
-                      to_host, upload)
+from ._device import (bytes_to_device, default_device, release_inflight, dtype_code, h2d, ptr, stream_handle,
+                      to_device, to_host, upload)
 from .core import CacheBlockConfig, LayeredKv, kv_dense_nbytes
 
 MAGIC = b"TDDF"
@@ -578,6 +578,7 @@ def serialize_many(diffs: Sequence[BlockSparseDiff], copy: bool = True) -> list:
     if not gpu:
         return out
     device = diffs[gpu[0]]._slab.pay_k.device
+    release_inflight()      # earlier direct H2Ds from pinned images that have drained
     lit = bytearray()
     segs: list = []
     spans = []
@@ -738,9 +739,7 @@ def deserialize_to_device(buf: bytes, device: Optional[torch.device] = None,
             segs.append((wl.v_off, vc[layer] * blk * 4, ptr(pay_v) + v_rows[layer] * blk * esz,
                          kind, 0))
     # the image (+ 4 bytes of padding for the funnel-shift reads) in one copy
-    staged = torch.empty(len(buf) + 8, dtype=torch.uint8, pin_memory=True)
-    staged.numpy()[:len(buf)] = np.frombuffer(buf, np.uint8)
-    image = staged.to(device, non_blocking=True)
+    image = bytes_to_device(buf, device, pad=8)
     table = np.array(segs, dtype=_lib.WIRE_SEG) if segs else np.zeros(0, _lib.WIRE_SEG)
     d_maps = torch.from_numpy(maps.reshape(2, -1)).to(device, non_blocking=True)
     if segs:
@@ -754,7 +753,7 @@ def deserialize_to_device(buf: bytes, device: Optional[torch.device] = None,
                                 v_indices=wl.v_indices))
     diff = BlockSparseDiff(num_layers, bs, heads, dim, total, layers)
     diff._dev = _DeviceDiff(pay_k, pay_v, d_maps[0], d_maps[1])
-    diff._keepalive = (image, staged)             # until the unpack has run
+    diff._keepalive = image                       # until the unpack has run
     return diff
 
 

@@ -126,3 +126,47 @@ def test_serialize_many_views_equal_bytes():
     assert [bytes(v) for v in views] == owned
     back = tk.deserialize_to_device(views[1], DEV)
     assert all(np.array_equal(a.indices, b.indices) for a, b in zip(diffs[1].layers, back.layers))
+
+
+def test_unpack_large_image_through_chunked_staging():
+    """An image several staging chunks long (and not a chunk multiple) goes
+    host -> pinned -> device in pieces filled by the host threads; the
+    unpacked slabs equal the host parser's blocks bit for bit."""
+    from paper_2604_03143_b200 import _device
+    rng = np.random.default_rng(11)
+    t, layers, heads, dim, bs = 4000, 4, 8, 128, 32      # ~ 3 chunks of f32 wire
+    _, _, diffs = _family(rng, torch.float32, t, layers, heads, dim, bs, 1, 0.3)
+    wire = tk.serialize_diff(diffs[0])
+    assert len(wire) > 2 * _device._STAGE_CHUNK and len(wire) % _device._STAGE_CHUNK
+    host = tk.deserialize_diff(wire)
+    for src in (wire, memoryview(bytearray(wire))):
+        dev = tk.deserialize_to_device(src, DEV, torch.float32)
+        for lh, ld in zip(host.layers, dev.layers):
+            assert np.array_equal(lh.indices, ld.indices)
+            assert np.array_equal(lh.k_blocks, ld.k_blocks.cpu().numpy())
+            assert np.array_equal(lh.v_blocks, ld.v_blocks.cpu().numpy())
+
+
+def test_pinned_views_take_the_direct_h2d_and_match_bytes():
+    """serialize_many(copy=False) views live in page-locked memory
+    (tdkv_host_is_pinned), so deserialize_to_device copies straight from
+    them; the unpacked slabs equal the ones from bytes copies."""
+    from paper_2604_03143_b200 import _lib
+    lib = _lib.load()
+    pinned = torch.empty(4096, dtype=torch.uint8, pin_memory=True)
+    assert lib.tdkv_host_is_pinned(pinned.data_ptr()) == 1
+    assert lib.tdkv_host_is_pinned(pinned.data_ptr() + 4095) == 1
+    assert lib.tdkv_host_is_pinned(np.zeros(4096, np.uint8).ctypes.data) == 0
+    rng = np.random.default_rng(4)
+    _, _, diffs = _family(rng, torch.bfloat16, 900, 3, 4, 64, 32, 3, 0.4)
+    views = tk.serialize_many(diffs, copy=False)
+    addr = np.frombuffer(views[2], np.uint8).ctypes.data
+    assert lib.tdkv_host_is_pinned(addr) == 1
+    for v in views:
+        a = tk.deserialize_to_device(v, DEV)
+        b = tk.deserialize_to_device(bytes(v), DEV)
+        for la, lb in zip(a.layers, b.layers):
+            assert np.array_equal(la.indices, lb.indices)
+            assert torch.equal(la.k_blocks, lb.k_blocks) and torch.equal(la.v_blocks, lb.v_blocks)
+    del views                      # the in-flight list keeps the source alive
+    torch.cuda.synchronize()
