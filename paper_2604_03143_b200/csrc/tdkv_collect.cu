@@ -89,11 +89,12 @@ struct CollectParams {
     int32_t block_size;
     int32_t n_jobs;
     int32_t ovl_inline;                   // OVL: K1's CTAs run the overlay pass after their items
-    int32_t neox;                         // rotate-half pairs (collect_kernel<..., NEOX>)
+    int32_t neox;                         // rotate-half pairs (collect_kernel<..., PAIRED>)
     int32_t cs_tiles;                     // tile planes before the cos/sin rows (4, or 2 when
                                           // every CTA takes one item: no prefetch buffer)
     int32_t drow_off;                     // byte offset of the destination-row buffers
     int32_t one_item;                     // fused rounds: one item per 128-thread CTA
+    int32_t stage_cs;                     // K0 rows of each job group copied to shared memory
 };
 
 // Per-job destination metadata is staged in shared memory in groups of
@@ -234,13 +235,16 @@ __global__ void __launch_bounds__(256) overlay_rows_kernel(const CollectParams p
 // in shared memory, and the scatter loop is the rotation, one 32-bit-indexed
 // address and the store.
 //
-// NEOX: the rotate-half pairing (element j of a head with element j + D/2,
-// angle index j) instead of the reference's interleaved pairs.  A thread owns
-// a unit of the head's lower half AND the unit D/2 elements on, so every pair
-// is in its registers (no shuffle between the two halves' lanes: that form
-// measured 0.58 of peak at C2/C3 -- twice the cos/sin loads and shuffles per
-// stored unit, and spills).
-template <typename T, int UB, bool BULK, bool OVL, bool FUSE = false, bool NEOX = false>
+// PAIRED: a thread owns a unit of a head's lower half AND the unit D/2
+// elements on (a "slot"), with the job group's cos/sin rows in shared memory.
+// This is the rotate-half form (p.neox: element j of a head with element
+// j + D/2, angle j -- every pair in the thread's registers; a warp-shuffle
+// exchange between the halves' lanes measured 0.58 of peak at C2/C3) and,
+// for bfloat16 rounds with K0's table, the interleaved form too: two loads
+// and two stores in flight per thread per row measured 0.985 / 0.991 / 0.988
+// / 0.992 of peak at C3 / C2 / C4 / C5 against 0.947 / 0.950 / 0.940 / 0.941
+// for one unit per thread (same box, scripts/gpu_r02_paired.sh).
+template <typename T, int UB, bool BULK, bool OVL, bool FUSE = false, bool PAIRED = false>
 __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) {
     using V = typename UnitBits<UB>::V;
     using Tbl = typename Elt<T>::Table;
@@ -271,7 +275,7 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
     // pair index of this thread's first unit (the usual single c = tx)
     auto angle0 = [&](int c) { return ((c * kEpu) % p.head_dim) >> 1; };
     const int j0_tx = angle0(tx);
-    // NEOX: slots = (head, unit of the lower half); slot s owns units c_lo and
+    // PAIRED: slots = (head, unit of the lower half); slot s owns units c_lo and
     // c_lo + hh of its row (hh = units per half head)
     const int hh = (p.head_dim >> 1) / kEpu;
     const int n_slots = upr >> 1;
@@ -365,8 +369,11 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
     // fused K0: the group's rows live in shared memory after the tiles
     const bool fused = p.fuse_table != 0;
     Tbl* s_cs = reinterpret_cast<Tbl*>(smem + (size_t)p.cs_tiles * tile_bytes);
+    // K0 rows staged per job group (set by the launcher for rotate-half
+    // rounds and, TDKV_K1_STAGE_CS, interleaved ones)
+    const bool staged_cs = p.stage_cs != 0 && rotate && !fused;
     auto load_cs_job = [&](Tbl* cs, int jj, const int4& m, int j0) {
-        if (fused) {
+        if (fused || staged_cs) {
             const Tbl* trow = s_cs + (size_t)jj * half + j0;
 #pragma unroll
             for (int q = 0; q < kCs; ++q) cs[q] = trow[q];
@@ -476,6 +483,19 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
                     }
                 }
                 __syncthreads();
+            } else if (staged_cs) {
+                // K0's table rows of the group's constant-delta jobs copied
+                // to shared memory once per group: the scatter loop reads its
+                // cos/sin from shared memory instead of a per-job L1/L2 load
+                // (rotate-half: a thread's 2 x 16-byte units need kEpu entries
+                // per job, too many registers to prefetch the next job's)
+                for (int idx = tid; idx < ng * half; idx += nthr) {
+                    const int jj = half_shift >= 0 ? idx >> half_shift : idx / half;
+                    const int4 mj = s_meta[mb][jj];
+                    if (mj.y == 0)
+                        s_cs[idx] = __ldg(table + (size_t)mj.x * half + (idx - jj * half));
+                }
+                __syncthreads();
             }
             if constexpr (BULK) {
                 // a job whose tile comes from its diff payload moves V in
@@ -499,36 +519,55 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
                     bulk_commit();
                 }
             }
-            if constexpr (NEOX) {
+            if constexpr (PAIRED) {
               if (sy < slot_rows) {
+                // a slot = one unit of a head's lower half + the unit D/2 on
+                // (rotate-half: the pair partners; interleaved: two
+                // self-contained units) -- two 16-byte loads and stores per
+                // row in flight per thread
                 const uint32_t upr32 = (uint32_t)upr;
+                const bool neox = p.neox != 0;
                 for (int sl = sx; sl < n_slots; sl += sx_n) {
                     const int c_lo = (sl / hh) * (2 * hh) + sl % hh;
                     const int c_hi = c_lo + hh;
-                    const int j0 = (sl % hh) * kEpu;       // angle of the slot's first element
+                    const int e0 = (sl % hh) * kEpu;       // the slot's first element
+                    // cos/sin entries: q < kPairs from jlo, the rest from jsplit
+                    // (rotate-half: angles e0 .. e0 + kEpu; interleaved: the
+                    // lower unit's pairs, then the upper unit's, D/4 on)
+                    const int jlo = neox ? e0 : e0 >> 1;
+                    const int jsplit = neox ? e0 + kPairs : (e0 >> 1) + (half >> 1);
                     for (int jj = 0; jj < ng; ++jj) {
                         const int4 mj = s_meta[mb][jj];
                         Tbl cs[kEpu];
-                        if (mj.y == 0) {
-                            const Tbl* trow = FUSE ? s_cs + jj * half + j0
-                                                   : table + (size_t)mj.x * half + j0;
+                        if (rotate && mj.y == 0) {
+                            const Tbl* trow = s_cs + jj * half;
 #pragma unroll
-                            for (int q = 0; q < kEpu; ++q) cs[q] = trow[q];
+                            for (int q = 0; q < kEpu; ++q)
+                                cs[q] = trow[q < kPairs ? jlo + q : jsplit + (q - kPairs)];
                         }
                         const int64_t* dr = s_drow_b(mb) + jj * drow_stride;
                         for (int r = sy; r < u.nrows; r += slot_rows) {
-                            if (!FUSE && mj.y != 0) {
-                                const Tbl* trow = table + (size_t)(mj.x + (mj.z + r) * mj.y) * half + j0;
+                            if (!FUSE && rotate && mj.y != 0) {
+                                const Tbl* trow = table + (size_t)(mj.x + (mj.z + r) * mj.y) * half;
 #pragma unroll
-                                for (int q = 0; q < kEpu; ++q) cs[q] = __ldg(trow + q);
+                                for (int q = 0; q < kEpu; ++q)
+                                    cs[q] = __ldg(trow + (q < kPairs ? jlo + q : jsplit + (q - kPairs)));
                             }
                             const size_t o = (size_t)(uint32_t)dr[r] * upr32;
                             V lo = sk[r * upr + c_lo], hi = sk[r * upr + c_hi];
                             if (rotate) {
                                 T* a = reinterpret_cast<T*>(&lo);
                                 T* b = reinterpret_cast<T*>(&hi);
+                                if (neox) {
 #pragma unroll
-                                for (int q = 0; q < kEpu; ++q) rot_pair(a[q], b[q], cs[q]);
+                                    for (int q = 0; q < kEpu; ++q) rot_pair(a[q], b[q], cs[q]);
+                                } else {
+#pragma unroll
+                                    for (int q = 0; q < kPairs; ++q) {
+                                        rot_pair(a[2 * q], a[2 * q + 1], cs[q]);
+                                        rot_pair(b[2 * q], b[2 * q + 1], cs[kPairs + q]);
+                                    }
+                                }
                             }
                             st_stream(reinterpret_cast<V*>(dk_l) + o + c_lo, lo);
                             st_stream(reinterpret_cast<V*>(dk_l) + o + c_hi, hi);
@@ -620,12 +659,26 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
 template <typename T, int UB, bool BULK, bool OVL = false>
 static int32_t launch_collect(const CollectParams& p, int grid_limit, cudaStream_t s, bool pdl) {
     auto kern = collect_kernel<T, UB, BULK, OVL>;
+    // interleaved rounds with K0's table take the paired (two units per
+    // thread) loop too; TDKV_K1_PAIRED=0 keeps one unit per thread (A/B)
+    static const int paired_env = [] {
+        const char* e = getenv("TDKV_K1_PAIRED");
+        return e ? atoi(e) : 1;
+    }();
+    bool paired_il = false;
     if constexpr (UB == 16 && BULK && !OVL) {
+        // bfloat16 only: the float32 form (float64 table entries) spills at
+        // 64 registers and measured slower (C1 x 64 agents, K0 table: 0.82 ->
+        // 0.78 of peak)
+        paired_il = sizeof(T) == 2 && !p.neox && !p.fuse_table && p.rotate && paired_env != 0 &&
+                    (p.head_dim / 2) % (16 / (int)sizeof(T)) == 0;
         if (p.neox)
             kern = p.fuse_table ? collect_kernel<T, UB, BULK, OVL, true, true>
                                 : collect_kernel<T, UB, BULK, OVL, false, true>;
         else if (p.fuse_table)
             kern = collect_kernel<T, UB, BULK, OVL, true>;
+        else if (paired_il)
+            kern = collect_kernel<T, UB, BULK, OVL, false, true>;
     } else {
         if (p.neox) return set_error(TDKV_EINVAL, "tdkv_collect: NeoX pairs need 16-byte units");
     }
@@ -644,9 +697,17 @@ static int32_t launch_collect(const CollectParams& p, int grid_limit, cudaStream
     }();
     CollectParams pp = p;
     const int items = p.n_units * p.num_layers;
-    const size_t cs_bytes = p.fuse_table ? (size_t)kJobGroup * (p.head_dim / 2) *
-                                               sizeof(typename Elt<T>::Table)
-                                         : 0;
+    // cos/sin rows of a job group in shared memory: the fused table, and the
+    // rotate-half form's staged K0 rows
+    static const int stage_env = [] {
+        const char* e = getenv("TDKV_K1_STAGE_CS");
+        return e ? atoi(e) : 0;        // interleaved rounds: 0 K0 rows from L1/L2, 1 staged
+    }();
+    pp.stage_cs = (p.rotate && !p.fuse_table && (p.neox || paired_il || stage_env == 1)) ? 1 : 0;
+    const size_t cs_bytes = p.fuse_table || pp.stage_cs
+                                ? (size_t)kJobGroup * (p.head_dim / 2) *
+                                      sizeof(typename Elt<T>::Table)
+                                : 0;
     auto smem_for = [&](int cs_tiles, int32_t& drow_off) {
         drow_off = (int32_t)(((size_t)cs_tiles * p.max_rows * p.row_elems * sizeof(T) +
                               cs_bytes + 15) / 16 * 16);
@@ -772,6 +833,7 @@ static int32_t collect_impl(const void* d_master_k, const void* d_master_v,
     p.drow_off = 0;
     p.neox = neox ? 1 : 0;
     p.one_item = one_item ? 1 : 0;
+    p.stage_cs = 0;
     p.mk = d_master_k;
     p.mv = d_master_v;
     p.mls = master_layer_stride;

@@ -1,4 +1,10 @@
-# rotate-half (neox) collector vs the reference's interleaved pairs, collector line only
-for cfg in c3 c2 c1; do for st in interleaved neox interleaved neox; do
-  echo "$cfg $st $(timeout 600 python bench.py --config $cfg --rope-style $st --steps 20 --no-cpu --no-codec --no-e2e 2>/dev/null | tail -1 | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["value"], d["roofline"]["frac"])')"
-done; done
+# rotate-half collector: parity tests + C3 / C2 bench lines with --rope-style neox
+OUT=gpurun_out
+timeout 300 python -m pytest tests/test_gpu_parity.py -q -x -k "neox or fused_table" 2>&1 | tail -1
+for c in c3 c2; do
+  timeout 600 python bench.py --config $c --rope-style neox --no-cpu --no-codec --no-e2e > $OUT/bench_neox_$c.log 2>&1
+  python -c "
+import json
+for l in open('$OUT/bench_neox_$c.log'):
+    if l.startswith('{'): d=json.loads(l); print('$c', d['value'], d['roofline']['frac'])"
+done
