@@ -538,6 +538,11 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
                     const int jsplit = neox ? e0 + kPairs : (e0 >> 1) + (half >> 1);
                     for (int jj = 0; jj < ng; ++jj) {
                         const int4 mj = s_meta[mb][jj];
+                        // family restore: a plane taken from the job's diff
+                        // payload is the overlay pass's (flags uniform per CTA)
+                        const bool ovk = OVL && s_map[mb][jj].x >= 0;
+                        const bool ovv = OVL && s_map[mb][jj].y >= 0;
+                        if (ovk && (ovv || v_tma || !has_v)) continue;
                         Tbl cs[kEpu];
                         if (rotate && mj.y == 0) {
                             const Tbl* trow = s_cs + jj * half;
@@ -569,9 +574,11 @@ __global__ void __launch_bounds__(256, 4) collect_kernel(const CollectParams p) 
                                     }
                                 }
                             }
-                            st_stream(reinterpret_cast<V*>(dk_l) + o + c_lo, lo);
-                            st_stream(reinterpret_cast<V*>(dk_l) + o + c_hi, hi);
-                            if (has_v && !v_tma) {
+                            if (!ovk) {
+                                st_stream(reinterpret_cast<V*>(dk_l) + o + c_lo, lo);
+                                st_stream(reinterpret_cast<V*>(dk_l) + o + c_hi, hi);
+                            }
+                            if (has_v && !v_tma && !ovv) {
                                 st_stream(reinterpret_cast<V*>(dv_l) + o + c_lo, sv[r * upr + c_lo]);
                                 st_stream(reinterpret_cast<V*>(dv_l) + o + c_hi, sv[r * upr + c_hi]);
                             }
@@ -679,6 +686,11 @@ static int32_t launch_collect(const CollectParams& p, int grid_limit, cudaStream
             kern = collect_kernel<T, UB, BULK, OVL, true>;
         else if (paired_il)
             kern = collect_kernel<T, UB, BULK, OVL, false, true>;
+    } else if constexpr (UB == 16 && BULK && OVL && sizeof(T) == 2) {
+        // the family restore's collector round (interleaved, K0 table)
+        paired_il = sizeof(T) == 2 && !p.neox && p.rotate && paired_env != 0 &&
+                    (p.head_dim / 2) % (16 / (int)sizeof(T)) == 0;
+        if (paired_il) kern = collect_kernel<T, UB, BULK, OVL, false, true>;
     } else {
         if (p.neox) return set_error(TDKV_EINVAL, "tdkv_collect: NeoX pairs need 16-byte units");
     }
