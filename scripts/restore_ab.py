@@ -14,6 +14,7 @@ import paper_2604_03143_b200 as tk  # noqa: E402
 # RESTORE_SHAPE=c3: the C3 codec family (one session: 24 mirrors of 717 tokens, L=48, H=8)
 L, T, H, D, bs, P = ((48, 717, 8, 128, 32, 24) if os.environ.get("RESTORE_SHAPE") == "c3"
                      else (28, 4624, 4, 128, 32, 49))
+P = int(os.environ.get("RESTORE_MIRRORS", P))      # family size override (threshold sweeps)
 dev = torch.device("cuda:0")
 g = torch.Generator(device=dev).manual_seed(0)
 mk = torch.randn(L, T, H, D, generator=g, device=dev).bfloat16()
