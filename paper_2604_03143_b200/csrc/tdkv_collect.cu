@@ -677,9 +677,12 @@ static int32_t launch_collect(const CollectParams& p, int grid_limit, cudaStream
         // bfloat16 only: the float32 form (float64 table entries) spills at
         // 64 registers and measured slower (C1 x 64 agents, K0 table: 0.82 ->
         // 0.78 of peak)
-        paired_il = sizeof(T) == 2 && !p.neox && !p.fuse_table && p.rotate && paired_env != 0 &&
-                    (p.head_dim / 2) % (16 / (int)sizeof(T)) == 0;
-        if (p.neox)
+        // (TDKV_K1_PAIRED=2: every 16-byte interleaved form, the fused table
+        // and float32 included -- A/B only)
+        const bool halves = (p.head_dim / 2) % (16 / (int)sizeof(T)) == 0;
+        paired_il = !p.neox && p.rotate && halves &&
+                    ((paired_env == 1 && sizeof(T) == 2 && !p.fuse_table) || paired_env == 2);
+        if (p.neox || (paired_il && p.fuse_table))
             kern = p.fuse_table ? collect_kernel<T, UB, BULK, OVL, true, true>
                                 : collect_kernel<T, UB, BULK, OVL, false, true>;
         else if (p.fuse_table)

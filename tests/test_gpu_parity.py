@@ -845,3 +845,52 @@ def test_collector_neox_rejects_unsupported_layouts():
         plan.launch_collect(arena, pool.k, pool.v, pool.layer_stride)
     with pytest.raises(ValueError, match="rope_style"):
         tk.KVCollector(arena, pool, rope_style="gptj")
+
+
+@pytest.mark.parametrize("heads,dim", [(1, 64), (3, 64), (8, 128), (2, 256), (5, 32)])
+@pytest.mark.parametrize("style", ["interleaved", "neox"])
+@pytest.mark.parametrize("fuse", ["0", "1"])
+def test_paired_loop_geometries_bf16_against_oracle(heads, dim, style, fuse, monkeypatch):
+    """bfloat16 rounds run K1's paired loop (two 16-byte units per thread,
+    K0 rows staged per job group): odd head counts, head_dim 32-256, a job
+    whose delta varies per row (per-row table rows, not staged), jobs of
+    several segments and more jobs per tile than one group holds -- every
+    rotated key within 1e-2 of the oracle on the bf16-rounded masters, V
+    bit for bit."""
+    from paper_2604_03143_b200 import collector as col_mod
+    # "0": K0's table (the paired loop with staged rows); "1": the fused table
+    monkeypatch.setattr(col_mod, "_FUSE_TABLE", fuse)
+    rng = np.random.default_rng(heads * 1000 + dim)
+    L, n_seg, seg = 2, 3, 37
+    mk = rng.standard_normal((L, n_seg * seg, heads, dim)).astype(np.float32)
+    mv = rng.standard_normal((L, n_seg * seg, heads, dim)).astype(np.float32)
+    mk_b = torch.from_numpy(mk).to(DEV).bfloat16()
+    mv_b = torch.from_numpy(mv).to(DEV).bfloat16()
+    pos = [np.arange(s * 50, s * 50 + seg) for s in range(n_seg)]
+    arena = tk.MasterArena(mk_b, mv_b, np.arange(n_seg) * seg, np.full(n_seg, seg), pos)
+    jobs = []
+    for j in range(40):                          # > 16 jobs per master tile
+        s = j % n_seg
+        if j == 7 and fuse == "0":               # per-row deltas (table rows not staged)
+            delta = rng.integers(-300, 300, seg)
+        else:
+            delta = np.full(seg, int(rng.integers(-500, 2000)))
+        jobs.append(tk.CollectJob(s, np.arange(j * seg, (j + 1) * seg), delta))
+    rows = 40 * seg
+    pool = tk.PagedPool(rows + 8, L, heads, dim, dtype=torch.bfloat16, device=DEV)
+    col = tk.KVCollector(arena, pool, 10000.0, rope_style=style)
+    plan = col.plan(jobs)
+    assert plan.fuse_table == (fuse == "1")
+    col.collect(plan)
+    got_k = pool.k.float().cpu().numpy()
+    got_v = pool.v.float().cpu().numpy()
+    mk32 = mk_b.float().cpu().numpy()
+    mv32 = mv_b.float().cpu().numpy()
+    rope = ref.rope_apply if style == "interleaved" else ref.rope_apply_neox
+    for j, job in enumerate(jobs):
+        r0 = job.segment * seg
+        dst = job.dst_rows
+        for layer in range(L):
+            want = rope(mk32[layer, r0:r0 + seg], job.delta)
+            assert np.abs(got_k[layer, dst] - want).max() <= 1e-2 * max(1.0, np.abs(want).max())
+            assert np.array_equal(got_v[layer, dst], mv32[layer, r0:r0 + seg])
