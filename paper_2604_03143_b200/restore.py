@@ -209,7 +209,7 @@ def fused_restore_many(mirrors: Sequence[MirrorHandle], spans: Sequence[Position
             if ledger is not None:
                 _fused_ledger(mirror, ledger)
         return 2
-    recs, deltas, tbl_row = [], [], 0
+    recs, deltas, tbl_row, const_row = [], [], 0, {}
     max_t, L, H, D = 0, pool.num_layers, pool.num_heads, pool.head_dim
     # host masters are uploaded once per master and the device planes kept
     # alive until the launch: the descriptors hold raw addresses, and a plane
@@ -223,12 +223,22 @@ def fused_restore_many(mirrors: Sequence[MirrorHandle], spans: Sequence[Position
         mk, mv = planes[id(kv)][1]
         dd = mirror.diff.device_form(pool.device, pool.dtype)
         rows, stride, rotate = _delta_rows(span.delta)
+        if stride == 0:
+            # constant shifts share one table row per distinct delta (a family
+            # restored to one offset needs a one-row table: cached, no K0 launch)
+            row = const_row.get(int(rows[0]))
+            if row is None:
+                row = const_row[int(rows[0])] = tbl_row
+                deltas.append(rows)
+                tbl_row += 1
+        else:
+            row = tbl_row
+            deltas.append(rows)
+            tbl_row += rows.size
         recs.append(_kernels.rows_job(mk, mv, T * H * D, pool.k, pool.v, pool.layer_stride, T,
                                       dst_rows=smap.device_slots(pool.device), pay_k=dd.pay_k,
                                       pay_v=dd.pay_v, map_k=dd.map_k, map_v=dd.map_v,
-                                      tbl_row=tbl_row, tbl_stride=stride, rotate=rotate))
-        deltas.append(rows)
-        tbl_row += rows.size
+                                      tbl_row=row, tbl_stride=stride, rotate=rotate))
         max_t = max(max_t, T)
     table = _kernels.rope_table(np.concatenate(deltas), D, rope_base, pool.dtype, pool.device)
     # jobs of one family share the master planes: order the work so each
