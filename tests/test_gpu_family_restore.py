@@ -253,3 +253,35 @@ def test_k3_batch_of_host_masters_keeps_every_master(monkeypatch):
         assert np.array_equal(gv, v), f"mirror {j}: V"
         want = np.stack([ref.rope_apply(k[layer], np.full(T, 5 + j)) for layer in range(L)])
         assert np.array_equal(gk, want), f"mirror {j}: K"
+
+
+def test_k3_batch_shared_shift_rows_match_oracle(monkeypatch):
+    """The K3 form gives mirrors restored by the same constant shift one
+    shared cos/sin row (a repeated shift -> the cached one-row table): a batch
+    mixing repeated shifts, a zero shift, a negative shift and a per-token
+    shift restores every mirror bit-exactly as the oracle (float32)."""
+    monkeypatch.setattr(rs, "_FAMILY_K1", False)
+    L, T, H, D, bs = 2, 80, 2, 64, 16
+    rng = np.random.default_rng(29)
+    mk, mv, mirrors, hints = _family_host(rng, L, T, H, D, 7, bs)
+    pos = np.arange(T, dtype=np.int64)
+    entry = tk.MasterEntry(0, tk.LayeredKv(mk, mv, pos), pin_count=7)
+    diffs = [tk.encode_diff(entry.kv, tk.LayeredKv(k, v, pos), h, tk.CacheBlockConfig(bs))
+             for (k, v), h in zip(mirrors, hints)]
+    handles = [tk.MirrorHandle(0, 1 + i, entry, d) for i, d in enumerate(diffs)]
+    per_token = np.cumsum(rng.integers(1, 5, T)).astype(np.int64) + 3
+    spans = [tk.PositionSpan.shifted(pos, 16), tk.PositionSpan.shifted(pos, 16),
+             tk.PositionSpan.shifted(pos, 0), tk.PositionSpan(pos, per_token),
+             tk.PositionSpan.shifted(pos, -9), tk.PositionSpan.shifted(pos, 16),
+             tk.PositionSpan.shifted(pos, -9)]
+    pool = _pool_f32(8 * T + 512, L, H, D)
+    maps = [pool.allocate(T, 100 + i) for i in range(len(handles))]
+    tk.fused_restore_many(handles, spans, pool, maps, 10000.0)
+    torch.cuda.synchronize()
+    for j, (span, smap) in enumerate(zip(spans, maps)):
+        k, v = mirrors[j]
+        layers = ref.encode_diff(mk, mv, k, v, hints[j], bs)
+        wk, wv = _oracle_pool(mk, mv, layers, bs, span, smap.slots, pool.capacity)
+        gk, gv = _read(pool, smap)
+        assert np.array_equal(gv, wv), f"mirror {j}: V"
+        assert np.array_equal(gk, wk), f"mirror {j}: K"
