@@ -559,6 +559,23 @@ int32_t tdkv_prepare_batch(void* segidx, int32_t n_prompts, const int32_t* promp
                            int64_t* out_hits, int64_t* out_hit_off, int64_t* out_hit_nid,
                            int32_t threads);
 
+/* ---- Round planning (host only) -------------------------------------------
+ * The collector plan of a round whose job j writes rows[dst_off[j] + i] of a
+ * device-resident row table and rotates by job_delta[j]: jobs sorted by
+ * segment (stable), (tile, job-chunk) units over the segments read, enough
+ * (layer, unit) items for target_items.  Replaces the numpy planning of
+ * KVCollector.plan_offsets (the batched form of align_cached's per-agent walk
+ * over its hits, pic.py:208-235).  out_jobs / out_deltas: n_jobs entries;
+ * out_units: unit_cap entries; out_info = [n_units, rotate, rows_written,
+ * master_rows].  TDKV_EINVAL (out_info[0] = units needed) when unit_cap is
+ * too small. */
+int32_t tdkv_plan_offsets(int32_t n_seg, const int64_t* seg_row0, const int64_t* seg_len,
+                          int32_t n_jobs, const int64_t* segments, const int64_t* dst_off,
+                          const int64_t* job_delta, int32_t num_layers, int32_t tile_rows,
+                          int64_t target_items, tdkv_collect_job* out_jobs, int64_t* out_deltas,
+                          tdkv_collect_unit* out_units, int64_t unit_cap, int64_t* out_info);
+
+
 #ifdef __cplusplus
 }
 #endif

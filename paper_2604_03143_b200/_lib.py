@@ -111,7 +111,7 @@ EXPORTS = (
     "tdkv_alloc_take", "tdkv_alloc_release", "tdkv_wire_pack", "tdkv_wire_unpack",
     "tdkv_segidx_create", "tdkv_segidx_destroy", "tdkv_segidx_count", "tdkv_segidx_total",
     "tdkv_segidx_insert", "tdkv_segidx_lookup", "tdkv_segidx_remove", "tdkv_segidx_evict",
-    "tdkv_segidx_entries", "tdkv_prepare_batch",
+    "tdkv_segidx_entries", "tdkv_prepare_batch", "tdkv_plan_offsets",
 )
 
 _P = ctypes.c_void_p
@@ -164,6 +164,8 @@ _SIGS = {
     "tdkv_segidx_evict": (_I32, [_P, _I64, _P, _P, _P, _I32, _P]),
     "tdkv_segidx_entries": (_I32, [_P, _P, _I64, _P]),
     "tdkv_wire_unpack": (_I32, [_P, _I32, _I64, _P, _P]),
+    "tdkv_plan_offsets": (_I32, [_I32, _P, _P, _I32, _P, _P, _P, _I32, _I32, _I64, _P, _P, _P,
+                                 _I64, _P]),
     "tdkv_prepare_batch": (_I32, [_P, _I32, _P, _P, _I32, _P, _P, _P, _P, _I64, _P, _I64, _P,
                                   _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32]),
     "tdkv_attention_many": (_I32, [_P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _I32,

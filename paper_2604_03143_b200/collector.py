@@ -218,23 +218,35 @@ def plan_host_offsets(seg_row0: np.ndarray, seg_len: np.ndarray, segments: np.nd
     """Planning when every job's destination rows are a contiguous run of a
     device-resident row table (e.g. the agents' slot maps, see SlotArena):
     job j's token i lands at rows[dst_off[j] + i] and rotates by the
-    constant ``job_delta[j]``.  Nothing per-token is built or uploaded."""
-    segments = np.asarray(segments, np.int64)
+    constant ``job_delta[j]``.  Nothing per-token is built or uploaded.
+
+    Runs in C++ (``tdkv_plan_offsets``): jobs stably sorted by segment, the
+    (tile, job-chunk) units of ``_build_units``; tests/test_plan.py checks it
+    against the numpy restatement record for record."""
+    seg_row0 = np.ascontiguousarray(seg_row0, np.int64)
+    seg_len = np.ascontiguousarray(seg_len, np.int64)
+    segments = np.ascontiguousarray(segments, np.int64)
     J = segments.size
-    if J == 0:
-        return HostPlan(np.zeros(0, _lib.COLLECT_UNIT), np.zeros(0, _lib.COLLECT_JOB),
-                        np.zeros(0, np.int64), np.zeros(0, np.int64), False, 0, 0)
-    order = np.argsort(segments, kind="stable")
-    seg_o = segments[order]
-    job_delta = np.asarray(job_delta, np.int64)[order]
+    dst_off = np.ascontiguousarray(dst_off, np.int64)
+    job_delta = np.ascontiguousarray(job_delta, np.int64)
+    if dst_off.size != J or job_delta.size != J or seg_row0.size != seg_len.size:
+        raise ValueError("plan_host_offsets: one dst_off and one delta per job, "
+                         "one row0 per segment length")
     jobs = np.zeros(J, dtype=_lib.COLLECT_JOB)
-    jobs["dst_off"] = np.asarray(dst_off, np.int64)[order]
-    jobs["seg_row0"] = np.asarray(seg_row0, np.int64)[seg_o]
-    jobs["tbl_row"] = np.arange(J)
-    units, master_rows = _build_units(seg_row0, seg_len, seg_o, num_layers, tile_rows,
-                                      target_items)
-    total = int(np.asarray(seg_len, np.int64)[segments].sum())
-    return HostPlan(units, jobs, None, job_delta, bool(job_delta.any()), total, master_rows)
+    deltas = np.zeros(J, np.int64)
+    info = np.zeros(4, np.int64)
+    # units <= tiles + target_items / L (see tdkv_plan.cu's chunking rule)
+    cap = int(((seg_len + tile_rows - 1) // tile_rows).sum()) + target_items // max(1, num_layers) + 1
+    units = np.zeros(cap, dtype=_lib.COLLECT_UNIT)
+    try:
+        _lib.call("tdkv_plan_offsets", int(seg_len.size), seg_row0.ctypes.data,
+                  seg_len.ctypes.data, J, segments.ctypes.data, dst_off.ctypes.data,
+                  job_delta.ctypes.data, int(num_layers), int(tile_rows), int(target_items),
+                  jobs.ctypes.data, deltas.ctypes.data, units.ctypes.data, cap, info.ctypes.data)
+    except _lib.TdkvError as e:
+        raise ValueError(str(e)) from None
+    return HostPlan(units[:int(info[0])], jobs, None, deltas, bool(info[1]), int(info[2]),
+                    int(info[3]))
 
 
 def unit_sources(unit_row0: np.ndarray, seg_row0: np.ndarray, seg_len: np.ndarray,
