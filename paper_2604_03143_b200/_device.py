@@ -81,6 +81,21 @@ def upload(arr: np.ndarray, device: Optional[torch.device] = None) -> torch.Tens
     return h2d(np.ascontiguousarray(arr).view(np.uint8).reshape(-1), device)
 
 
+def upload_many(arrays, device: Optional[torch.device] = None):
+    """Several host arrays in ONE pinned upload (16-byte aligned); returns the
+    device byte buffer and one uint8 view of it per array (views share the
+    buffer's lifetime)."""
+    offs, total = [], 0
+    for a in arrays:
+        offs.append(total)
+        total += (a.nbytes + 15) // 16 * 16
+    buf = np.zeros(max(total, 16), np.uint8)
+    for a, o in zip(arrays, offs):
+        buf[o:o + a.nbytes] = np.ascontiguousarray(a).view(np.uint8).reshape(-1)
+    d = h2d(buf, device)
+    return d, [d[o:o + a.nbytes] for a, o in zip(arrays, offs)]
+
+
 def h2d(arr: np.ndarray, device: Optional[torch.device] = None) -> torch.Tensor:
     """Host array -> device tensor through pinned staging, asynchronous on the
     current stream (the caching host allocator keeps the staging buffer alive

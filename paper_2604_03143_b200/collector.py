@@ -28,7 +28,7 @@ import torch
 
 from . import _kernels, _lib
 from ._device import (HOST_THREADS, default_device, dtype_code, h2d, host_executor, is_host, ptr,
-                      stream_handle, to_device, to_host, upload)
+                      stream_handle, to_device, to_host, upload, upload_many)
 from .core import LayeredKv
 from .ledger import CostLedger
 
@@ -344,10 +344,14 @@ class CollectPlan:
         self.rows_written = host.rows_written
         self.units_host = host.units
         # device residency
-        self.d_units = upload(host.units, self.device)
-        self.d_jobs = upload(host.jobs, self.device)
-        self.d_dst_rows = h2d(host.dst_rows, self.device) if offsets is None else offsets[2]
-        self.d_deltas = h2d(host.deltas, self.device)
+        # device residency: units, jobs, deltas (+ rows) in one pinned upload
+        arrays = [host.units, host.jobs, host.deltas]
+        if offsets is None:
+            arrays.append(np.ascontiguousarray(host.dst_rows, np.int64))
+        self._d_buf, views = upload_many(arrays, self.device)
+        self.d_units, self.d_jobs = views[0], views[1]
+        self.d_deltas = views[2].view(torch.int64)
+        self.d_dst_rows = views[3].view(torch.int64) if offsets is None else offsets[2]
         self._fast: dict = {}
         # small rounds are launch-bound: compute the cos/sin rows inside K1
         # (one kernel per round) when every job has one constant delta

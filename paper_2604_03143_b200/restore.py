@@ -150,6 +150,12 @@ def _family_restore(mirrors, spans, pool: PagedPool, slot_maps, rope_base: float
             host = plan_host_offsets(seg_row0, seg_len, segs,
                                      np.arange(len(members), dtype=np.int64) * T, job_delta,
                                      L, tile)
+            if host.rotate:
+                # one cos/sin row per distinct shift (a family restored to one
+                # offset: the cached one-row table, no K0 launch)
+                uniq, inv = np.unique(host.deltas, return_inverse=True)
+                host.jobs["tbl_row"] = inv
+                const_table = _kernels.rope_table(uniq, D, rope_base, pool.dtype, dev)
         else:
             host = plan_host(seg_row0, seg_len, segs,
                              np.concatenate([np.asarray(slot_maps[i].slots, np.int64)
@@ -168,7 +174,10 @@ def _family_restore(mirrors, spans, pool: PagedPool, slot_maps, rope_base: float
         keep.append(buf)
         d_rows = addrs[4] if not const else ptr(rows_dev)
         table = None
-        if host.rotate:
+        if host.rotate and const:
+            table = const_table
+            keep.append(table)
+        elif host.rotate:
             n_tbl = int(host.deltas.size)
             table = torch.empty((n_tbl, D // 2, 2), dtype=table_dtype(pool.dtype), device=dev)
             _lib.call("tdkv_rope_table", addrs[3], n_tbl,
